@@ -1,0 +1,163 @@
+"""Pin the numpy oracle against golden vectors produced by the real reference
+(oracle/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from golden_util import golden
+
+TOL = {"f64": 1e-9, "f32": 2e-5}
+
+
+def close(got, want, tol):
+    err = O.compare(got, want)
+    assert err <= tol, f"max rel err {err:.3e} > {tol:.1e}"
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_bdrln(dt):
+    g = golden(f"bdrln_{dt}")
+    eps = float(g["eps"])
+    r = O.bdrln_fwd(g["h"], g["b"], g["m"], g["r"], g["g"], g["be"], eps)
+    close(r["y"], g["y"], TOL[dt])
+    bw = O.bdrln_bwd(g["dy"], r["s"], g["g"], g["m"], eps)
+    close(bw["dh"], g["dh"], TOL[dt])
+    close(bw["ds"], g["dr"], TOL[dt])
+    close(bw["dbias"], g["db"], TOL[dt])
+    close(bw["dgamma"], g["dg"], TOL[dt])
+    close(bw["dbeta"], g["dbe"], TOL[dt])
+    # mask values are keep/(1-p)
+    np.testing.assert_allclose(O.mask_values(g["keep"], float(g["p"]), g["m"].dtype), g["m"])
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_scaled_masked_softmax(dt):
+    g = golden(f"softmax_{dt}")
+    p, pd = O.scaled_masked_softmax_fwd(g["sc"], float(g["divisor"]), g["am"], g["dm"])
+    close(p, g["p_out"], TOL[dt])
+    close(pd, g["pd"], TOL[dt])
+    dsc = O.scaled_masked_softmax_bwd(g["dy"], p, g["dm"], float(g["divisor"]))
+    close(dsc, g["dsc"], TOL[dt])
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_bias_gelu(dt):
+    g = golden(f"bias_gelu_{dt}")
+    pre, y = O.bias_gelu_fwd(g["f"], g["b"])
+    close(y, g["y"], TOL[dt])
+    dpre, db = O.bias_gelu_bwd(g["dy"], pre)
+    close(dpre, g["df"], TOL[dt])
+    close(db, g["db"], TOL[dt])
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_bert_layer(dt):
+    g = golden(f"bert_layer_{dt}")
+    B, S, NH = int(g["B"]), int(g["S"]), int(g["NH"])
+    prm = {k: g[k] for k in O.BERT_WEIGHTS}
+    out, cache = O.bert_layer_fwd(prm, g["x"], g["am"], g["dm"], g["m1"], g["m2"], B, S, NH,
+                                  float(g["eps"]))
+    close(out, g["out"], TOL[dt])
+    grads = O.bert_layer_bwd(prm, cache, g["dy"])
+    for k in ("x",) + O.BERT_WEIGHTS:
+        close(grads[k], g["d_" + k], TOL[dt] * 10)
+
+
+@pytest.mark.parametrize("name", ["mbconv_s1_f64", "mbconv_s1_f32", "mbconv_s2_f64"])
+def test_mbconv(name):
+    g = golden(name)
+    tol = TOL[name[-3:]] * 10
+    prm = {k: g[k] for k in O.MBCONV_WEIGHTS}
+    y, nrm, nrv, cache = O.mbconv_fwd(prm, g["x"], int(g["stride"]), float(g["eps"]),
+                                      float(g["momentum"]))
+    close(y, g["y"], tol)
+    close(nrm, g["new_rm"], tol)
+    close(nrv, g["new_rv"], tol)
+    grads = O.mbconv_bwd(prm, cache, g["dy"])
+    for k in ("x", "wdw", "g", "b", "wr", "br", "we", "be"):
+        close(grads[k], g["d_" + k], tol)
+
+
+@pytest.mark.parametrize("tag", ["4d", "5d"])
+def test_norm_sweep(tag):
+    g = golden("norm_sweep_f64")
+    p = lambda k: g[f"ln{tag}_{k}"]  # noqa: E731
+    y, _ = O.ln_swish_fwd(p("x"), p("g"), p("b"))
+    close(y, p("y"), 1e-9)
+    dx, dg, db = O.ln_swish_bwd(p("dy"), p("x"), p("g"), p("b"))
+    close(dx, p("dx"), 1e-9)
+    close(dg, p("dg"), 1e-9)
+    close(db, p("db"), 1e-9)
+    q = lambda k: g[f"bn{tag}_{k}"]  # noqa: E731
+    y, nrm, nrv = O.bn_swish_fwd(q("x"), q("g"), q("b"), q("rm"), q("rv"))
+    close(y, q("y"), 1e-9)
+    close(nrm, q("new_rm"), 1e-9)
+    close(nrv, q("new_rv"), 1e-9)
+    dx, dg, db = O.bn_swish_bwd(q("dy"), q("x"), q("g"), q("b"))
+    close(dx, q("dx"), 1e-9)
+    close(dg, q("dg"), 1e-9)
+    close(db, q("db"), 1e-9)
+
+
+def test_known_answers():
+    g = golden("known_answers")
+    for i in range(3):
+        pads = tuple(int(v) for v in g[f"dw{i}_pads"])
+        y = O.dwconv(g[f"dw{i}_x"], g[f"dw{i}_w"], int(g[f"dw{i}_stride"]), pads)
+        close(y, g[f"dw{i}_y"], 1e-12)
+    y, nm, nv, _, _ = O.batchnorm_train(g["bn_x"], g["bn_scale"], g["bn_bias"], g["bn_rm"],
+                                        g["bn_rv"], 1e-5, 0.8)
+    close(y, g["bn_y"], 1e-12)
+    close(nm, g["bn_new_rm"], 1e-12)
+    close(nv, g["bn_new_rv"], 1e-12)
+    close(O.layernorm(g["ln_x"], g["ln_g"], g["ln_b"], 1e-3), g["ln_y"], 1e-12)
+    close(O.softmax(g["sm_x"]), g["sm_y"], 1e-12)
+    close(O.gemm(g["gemm_a"], g["gemm_b"], g["gemm_c"], 0.5, 2.0, trans_a=True), g["gemm_y"], 1e-12)
+    close(g["gap_x"].mean(axis=(2, 3), keepdims=True), g["gap_y"], 1e-12)
+
+
+def test_reference_closed_forms():
+    """Closed-form known answers from the reference's own tests
+    (test_frontend.py:187-217, 260-276)."""
+    np.testing.assert_allclose(O.softmax(np.array([0.0, 0.0])), [0.5, 0.5])
+    rng = np.random.default_rng(11)
+    gamma, beta = rng.standard_normal(6), rng.standard_normal(6)
+    y = O.layernorm(np.full((3, 6), 2.5), gamma, beta)
+    np.testing.assert_allclose(y, np.broadcast_to(beta, (3, 6)), atol=1e-12)
+
+
+def test_bf16_rounding():
+    x = np.array([1.0, 1.00390625, 1.005859375, -3.1415926, 65504.0, 1e-30], dtype=np.float32)
+    r = O.round_bf16(x)
+    # exactly representable values are unchanged; others land on the bf16 grid
+    assert r[0] == 1.0 and r[1] == 1.0  # 1 + 2^-8 ties to even -> 1.0
+    assert r[2] == np.float32(1.0078125)
+    assert (r.view(np.uint32) & 0xFFFF == 0).all()
+
+
+def test_finite_difference_bert_small():
+    """Backward pinned by central differences as well (the reference ships no
+    AD tests)."""
+    g = golden("bert_layer_f64")
+    B, S, NH = int(g["B"]), int(g["S"]), int(g["NH"])
+    prm = {k: g[k].copy() for k in O.BERT_WEIGHTS}
+    args = (g["am"], g["dm"], g["m1"], g["m2"], B, S, NH, float(g["eps"]))
+    out, cache = O.bert_layer_fwd(prm, g["x"], *args)
+    dy = g["dy"]
+    grads = O.bert_layer_bwd(prm, cache, dy)
+    rng = np.random.default_rng(3)
+    for name in ("x", "wq", "w1", "g1", "b2"):
+        base = g[name] if name == "x" else prm[name]
+        for idx in rng.integers(0, base.size, size=3):
+            h = 1e-6
+            def loss(delta):
+                p2 = dict(prm)
+                x2 = g["x"].copy()
+                arr = (x2 if name == "x" else p2[name].copy())
+                arr.flat[idx] += delta
+                if name != "x":
+                    p2[name] = arr
+                return float((O.bert_layer_fwd(p2, x2, *args)[0] * dy).sum())
+            fd = (loss(h) - loss(-h)) / (2 * h)
+            assert abs(fd - grads[name].flat[idx]) <= 1e-5 * max(1.0, abs(fd))
