@@ -1,0 +1,364 @@
+"""Benchmark of the fused training hot path (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A *step* is one training step of a BERT-base encoder layer (H=768, 12 heads,
+FFN 3072, post-LN, tanh-GELU, dropout p=0.1 with explicit keep masks) in bf16
+at batch 8 x seq 512 per GPU: forward + backward + SGD update (+ gradient
+allreduce over NCCL when N > 1, weak scaling).  Synthetic inputs and
+random-init weights (seeded), resident in HBM for ``value``; ``e2e`` repeats
+the measurement through the host-buffer API (pinned H2D of the step's inputs,
+D2H of dx inside the timed region).
+
+Timing: W warm-up steps, then K steps each bracketed by CUDA events on the
+launching stream, with a 256 MiB L2 flush between steps (outside the events);
+barrier + synchronize on both sides; max over ranks.  Every library call is
+also bracketed by events to attribute time per kernel; the dominant one is
+reported against MEASURED_PEAKS.json as ``roofline``.
+
+``--impl reference`` times the reference's CPU path (the numpy oracle port in
+oracle/, float64 like dfir) on this host, bounded to one sequence per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B, S, H, NH, FF = 8, 512, 768, 12, 3072
+P_DROP = 0.1
+METRIC = "BERT-base encoder layer fwd+bwd+SGD training throughput (bf16, B=8 x S=512 per GPU)"
+UNIT = "samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# CPU reference path (oracle port, float64 numpy — the reference computes in f64)
+
+
+def cpu_reference_sample(seconds: float, seq=S):
+    """Run fwd+bwd of ONE sequence (B=1, S=512) through the oracle until
+    ``seconds`` have elapsed (at least once).  Returns (samples/s, reps)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(0)
+    T = seq
+    prm = {}
+    for nm, shp in [("wq", (H, H)), ("wk", (H, H)), ("wv", (H, H)), ("wo", (H, H)),
+                    ("w1", (FF, H)), ("w2", (H, FF))]:
+        prm[nm] = 0.02 * rng.standard_normal(shp)
+    for nm, n in [("bq", H), ("bk", H), ("bv", H), ("bo", H), ("b1", FF), ("b2", H)]:
+        prm[nm] = 0.1 * rng.standard_normal(n)
+    for i in "12":
+        prm["g" + i] = 1 + 0.1 * rng.standard_normal(H)
+        prm["be" + i] = 0.1 * rng.standard_normal(H)
+    x = rng.standard_normal((T, H))
+    am = np.zeros((1, 1, 1, seq))
+    dm = O.mask_values(rng.random((1, NH, seq, seq)) >= P_DROP, P_DROP, np.float64)
+    m1 = O.mask_values(rng.random((T, H)) >= P_DROP, P_DROP, np.float64)
+    m2 = O.mask_values(rng.random((T, H)) >= P_DROP, P_DROP, np.float64)
+    dout = rng.standard_normal((T, H))
+    reps = 0
+    t0 = time.perf_counter()
+    while True:
+        out, cache = O.bert_layer_fwd(prm, x, am, dm, m1, m2, 1, seq, NH, 1e-12)
+        O.bert_layer_bwd(prm, cache, dout)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return reps / el, reps, el
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    warm = max(0, min(args.warmup, 1))
+    for _ in range(warm):
+        cpu_reference_sample(0.0)
+    per_step = []
+    for _ in range(args.steps):
+        v, reps, el = cpu_reference_sample(0.0)
+        per_step.append(el)
+        if sum(per_step) > 150:
+            break
+    k = len(per_step)
+    ms = 1e3 * statistics.mean(per_step)
+    value = 1e3 / ms  # one sequence per step
+    sample = (f"1 sequence (B=1, S={S}) fwd+bwd per step, float64 numpy oracle "
+              f"(oracle/oracle.py), {k} steps")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": world, "steps": k, "warmup": warm, "ms_per_step": round(ms, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy)",
+        "config": {"workload": "bert_base_encoder_layer_train_step", "global_batch": 1, "seq_len": S,
+                   "hidden": H, "heads": NH, "ffn": FF, "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.count(",") >= 7]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" == r[4 + i].strip()})
+        pw = [float(r[3]) for r in rows if r[3].strip() not in ("[N/A]", "")]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------
+# our path
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return {"hbm_gbs": d["hbm_gbs"], "tflops": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "tflops_burst": d["bf16_tflops"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "tflops": 1590.0, "tflops_burst": 1590.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2110_10802_b200 import kernels as K
+    from paper_2110_10802_b200.bert import BertEncoderLayer, BertLayerConfig
+
+    cfg = BertLayerConfig(hidden=H, heads=NH, ffn=FF, p_drop=P_DROP, dtype=torch.bfloat16)
+    layer = BertEncoderLayer(cfg, device=f"cuda:{local}", seed=1234)
+    T = B * S
+    gen = torch.Generator(device="cpu").manual_seed(100 + rank)
+    x = torch.randn(T, H, generator=gen).bfloat16()
+    dout = torch.randn(T, H, generator=gen).bfloat16()
+    am = torch.where(torch.rand(B, S, generator=gen) < 0.1, -10000.0, 0.0).float()
+    keep_attn = (torch.rand(B, NH, S, S, generator=gen) >= P_DROP).to(torch.uint8)
+    keep1 = (torch.rand(T, H, generator=gen) >= P_DROP).to(torch.uint8)
+    keep2 = (torch.rand(T, H, generator=gen) >= P_DROP).to(torch.uint8)
+    host = {k: v.pin_memory() for k, v in dict(x=x, dout=dout, add_mask=am, keep_attn=keep_attn,
+                                                 keep1=keep1, keep2=keep2).items()}
+    dev = layer.device_inputs(B, S)
+    for k, v in host.items():
+        dev[k].copy_(v)
+    dx_host = torch.empty(T, H, dtype=torch.bfloat16).pin_memory()
+    lr = 1e-4
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    # The step is captured once into a CUDA graph (host launch path off the
+    # critical path); an instrumented twin with event-record nodes around
+    # every library call attributes time per kernel in a second pass.
+    K.reset_launch_count()
+    timer = K.KernelTimer()
+    if world > 1:
+        g_step, g_inst = layer.capture_step(B, S, None, timer)
+    else:
+        g_step, g_inst = layer.capture_step(B, S, lr, timer)
+    K.reset_launch_count()  # count one eager step's launches (the graph replays the same set)
+    layer.forward(dev["x"], dev["add_mask"], dev["keep_attn"], dev["keep1"], dev["keep2"])
+    layer.backward(dev["dout"])
+    if world == 1:
+        layer.sgd_step(lr)
+    launches_per_step = K.launch_count()
+
+    def step(g=g_step):
+        g.replay()
+        if world > 1:
+            dist.all_reduce(layer.grad.flat)  # NCCL sum; averaging folded into the lr
+            layer.sgd_step(lr / world)
+
+    def timed(fn, k, per_step=None):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(k):
+            flush.zero_()
+            evs[i][0].record()
+            fn()
+            evs[i][1].record()
+            if per_step is not None:
+                per_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    sampler = ClockSampler(local)
+    with sampler:
+        for _ in range(max(3, args.warmup)):
+            step()
+        torch.cuda.synchronize()
+        total_ms = timed(step, args.steps)
+        launches = launches_per_step * args.steps
+        # attribution pass: same step with event-record nodes, collected per replay
+        timer.totals = {}
+        inst_ms = timed(lambda: step(g_inst), args.steps, per_step=timer.collect)
+    clocks = sampler.summary()
+    ms_step = total_ms / args.steps
+    value = world * B * 1e3 / ms_step
+
+    # e2e through the host-buffer API (pinned H2D of inputs, graph replay, D2H of dx)
+    def host_step():
+        layer.train_step_host(host, lr=None if world > 1 else lr, dx_host=dx_host)
+        if world > 1:
+            dist.all_reduce(layer.grad.flat)
+            layer.sgd_step(lr / world)
+
+    for _ in range(3):
+        host_step()
+    ke = max(5, args.steps // 2)
+    e2e_ms = timed(host_step, ke) / ke
+    h2d, d2h = layer.host_inputs_bytes(B, S)
+
+    # per-kernel roofline
+    pk = peaks()
+    rows = []
+    for r in timer.summary():
+        per_call_ms = r["ms"] / r["calls"]
+        work = r["work"] / r["calls"]
+        if r["kind"] == "hbm":
+            ach, peak, unit = work / (per_call_ms * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
+        else:
+            ach, peak, unit = work / (per_call_ms * 1e-3) / 1e12, pk["tflops"], "TFLOP/s"
+        rows.append({"kernel": r["label"], "bound": "hbm" if r["kind"] == "hbm" else "tensor",
+                     "calls_per_step": r["calls"] / args.steps, "us_per_call": round(per_call_ms * 1e3, 2),
+                     "share": 0.0, "achieved": round(ach, 1), "unit": unit, "frac": round(ach / peak, 3),
+                     "work_per_call": work})
+    tot = sum(r["us_per_call"] * r["calls_per_step"] for r in rows)
+    for r in rows:
+        r["share"] = round(r["us_per_call"] * r["calls_per_step"] / tot, 3)
+    dom = max(rows, key=lambda r: r["us_per_call"] * r["calls_per_step"])
+    roofline = {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"],
+                "peak": pk["hbm_gbs"] if dom["bound"] == "hbm" else pk["tflops"], "unit": dom["unit"],
+                "frac": dom["frac"], "traffic": None, "peak_source": pk["source"]}
+    gemm_us = sum(r["us_per_call"] * r["calls_per_step"] for r in rows if r["bound"] == "tensor")
+    from oracle.oracle import bert_layer_flops  # algorithmic flop count only
+
+    flops = bert_layer_flops(B, S, H, NH, FF)
+    gemm_tflops = flops / (gemm_us * 1e-6) / 1e12
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, reps, el = cpu_reference_sample(args.cpu_seconds)
+        cpu = {"value": round(v, 4), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{reps} x one sequence (B=1, S={S}) fwd+bwd, float64 numpy oracle, {el:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded torch.randn inputs, random-init weights, explicit dropout keep masks)",
+            "config": {"workload": "bert_base_encoder_layer_train_step (BASELINE.json configs[1])",
+                       "global_batch": B * world, "seq_len": S, "hidden": H, "heads": NH, "ffn": FF,
+                       "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) between timed steps",
+                       "step": "fwd + bwd + SGD" + (" + NCCL grad allreduce" if world > 1 else "")},
+            "e2e": {"value": round(world * B * 1e3 / e2e_ms, 2), "unit": UNIT, "ms_per_step": round(e2e_ms, 4),
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "instrumented_ms_per_step": round(inst_ms / args.steps, 4),
+            "roofline": roofline,
+            "gemm_tflops": round(gemm_tflops, 1),
+            "kernels": rows,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/*
+ * dfx.h — C ABI of the B200 (sm_100a) fused training hot path.
+ *
+ * This is the drop-in boundary that replaces the CPU execution of the fused
+ * memory-bound subgraphs of a training step in the reference `dfir` package
+ * (arXiv 2110.10802 re-specification, /root/reference/pkg/src/dfir).  The
+ * reference executes these subgraphs through
+ *
+ *     interp.execute(g, inputs, bindings, library_eval)      interp.py:1301-1317
+ *       -> _Execution.run_library -> library_eval(op, attrs, inputs)
+ *                                                             interp.py:337-368
+ *       -> frontend.reference_apply(op, attrs, inputs)        frontend.py:146-150
+ *
+ * and through the manual VJPs of autodiff.py (1363-1617).  The Python host
+ * layer (paper_2110_10802_b200/library_eval.py) binds every entry point below
+ * with ctypes and exposes the same `library_eval(op, attrs, inputs)` seam;
+ * INTEGRATION.md shows the binding.  Each function cites the reference
+ * operator(s) whose semantics it implements.
+ *
+ * Conventions
+ *  - Plain pointers to DEVICE memory, element counts and element strides; no
+ *    framework types.  `stream` is a cudaStream_t passed as void*.
+ *  - Calls are asynchronous and stream-ordered; no host synchronisation, no
+ *    allocation.  Callers own every buffer (interp.py:206-212 ownership rule).
+ *  - Reductions are fixed-order (no float atomics): results are bitwise
+ *    reproducible run to run (the reference's determinism, autodiff.py:19-25).
+ *  - Return value: DFX_OK (0) or a DFX_ERR_* code; dfx_last_error() returns a
+ *    thread-local message (mirrors ShapeError / ExecError text).
+ *  - dtype codes extend the DTNS codes (dtns.py:30-45): 0=f32 1=f64 2=i64
+ *    3=bool, plus 4=bf16 and 5=u8.  Activation tensors are f32 or bf16;
+ *    parameter vectors (bias, gamma, beta) and statistics are always f32.
+ *  - Dropout masks are u8 keep flags (0/1) plus keep_scale = 1/(1-p): the
+ *    reference's explicit float mask tensor equals keep * keep_scale
+ *    (no Dropout op exists in the reference).
+ */
+#ifndef DFX_H_
+#define DFX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum dfx_dtype { DFX_F32 = 0, DFX_F64 = 1, DFX_I64 = 2, DFX_BOOL = 3, DFX_BF16 = 4, DFX_U8 = 5 };
+
+enum dfx_status {
+  DFX_OK = 0,
+  DFX_ERR_SHAPE = 1,       /* frontend.ShapeError analogue */
+  DFX_ERR_DTYPE = 2,
+  DFX_ERR_ALIGN = 3,       /* pointer/stride alignment the kernel needs */
+  DFX_ERR_CUDA = 4,        /* launch or runtime failure */
+  DFX_ERR_UNSUPPORTED = 5, /* frontend.UnsupportedOp analogue */
+  DFX_ERR_WORKSPACE = 6
+};
+
+/* ---- library ------------------------------------------------------------ */
+const char* dfx_last_error(void);
+int dfx_version(void);
+/* DFX_OK iff the current device is an sm_100 part the cubins were built for. */
+int dfx_device_check(void);
+/* Number of kernel launches issued by this thread since the last reset. */
+int64_t dfx_launch_count(void);
+void dfx_reset_launch_count(void);
+
+/* ---- a1/a2: bias + dropout + residual + LayerNorm (forward) --------------
+ * s = (h + bias) * keep * keep_scale + residual ; y = LN(s) over the last axis
+ * Replaces Add (frontend.py:291) + Mul (293) + Add + LayerNormalization
+ * (frontend.py:519-529; biased variance).  keep may be NULL (no dropout),
+ * bias may be NULL, residual may be NULL.  s_stash, mean, rstd may be NULL;
+ * the backward needs s_stash (or recomputes nothing else). */
+int dfx_bdrln_fwd(int dtype, int64_t rows, int64_t cols, const void* h, const float* bias,
+                  const uint8_t* keep, float keep_scale, const void* residual,
+                  const float* gamma, const float* beta, float eps, void* y, void* s_stash,
+                  float* mean, float* rstd, void* stream);
+
+/* ---- a3: backward of the above -------------------------------------------
+ * LN VJP (autodiff.py:1490-1545): ds = rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat))
+ * dh = ds * keep * keep_scale ; dgamma = sum_rows dy*xhat ; dbeta = sum_rows dy ;
+ * dbias = sum_rows dh.  ds is also the gradient of `residual`.  Any of dh,
+ * dgamma, dbeta, dbias may be NULL.  Workspace: dfx_bdrln_bwd_workspace(). */
+size_t dfx_bdrln_bwd_workspace(int64_t rows, int64_t cols);
+int dfx_bdrln_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const void* s_stash,
+                  const float* gamma, const uint8_t* keep, float keep_scale, float eps,
+                  void* ds, void* dh, float* dgamma, float* dbeta, float* dbias, void* workspace,
+                  size_t ws_bytes, void* stream);
+
+/* ---- a4/a5: scaled + masked softmax + dropout (forward) -------------------
+ * rows are [batch, heads, q] (row-major), cols = k.
+ * p  = softmax(scores * inv_divisor + add_mask[b, :])     (Div frontend.py:294,
+ *      Add 175-188, Softmax 493-501)
+ * pd = p * keep * keep_scale                               (Mul 293)
+ * add_mask is f32 [batch, cols] or NULL; keep/pd may be NULL. */
+int dfx_softmax_fwd(int dtype, int64_t batch, int64_t heads, int64_t q, int64_t cols,
+                    const void* scores, float inv_divisor, const float* add_mask,
+                    const uint8_t* keep, float keep_scale, void* p, void* pd, void* stream);
+
+/* ---- a6: backward (autodiff.py:1465-1484, stashes the forward output p) ----
+ * g = dpd * keep * keep_scale ; dscores = (g - sum(g*p)) * p * inv_divisor */
+int dfx_softmax_bwd(int dtype, int64_t rows, int64_t cols, const void* dpd, const void* p,
+                    const uint8_t* keep, float keep_scale, float inv_divisor, void* dscores,
+                    void* stream);
+
+/* ---- a7: bias + tanh-GELU -------------------------------------------------
+ * pre = f + bias ; y = 0.5*pre*(1+tanh(0.7978845608*(pre+0.044715*pre^3)))
+ * (Pow/Mul/Add/Tanh chain, frontend.py:223-295).  pre may be NULL. */
+int dfx_bias_gelu_fwd(int dtype, int64_t rows, int64_t cols, const void* f, const float* bias,
+                      void* pre, void* y, void* stream);
+/* dpre = dy * gelu'(pre) (symexpr.py:672-738 derivative); dbias = colsum(dpre)
+ * (NULL to skip).  Workspace: dfx_colsum_workspace(rows, cols). */
+int dfx_bias_gelu_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const void* pre,
+                      void* dpre, float* dbias, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- column sums (bias gradients; Gemm VJP of C, autodiff.py:1452-1458) ---- */
+size_t dfx_colsum_workspace(int64_t rows, int64_t cols);
+int dfx_colsum(int dtype, int64_t rows, int64_t cols, const void* x, int64_t ld, float* out,
+               int accumulate, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- a8: contractions -------------------------------------------------------
+ * D[b1,b2][m,n] = epilogue( alpha * sum_k A[b1,b2](m,k) * B[b1,b2](n,k) )
+ * Gemm (frontend.py:369-405) / MatMul (335-366) / Einsum (408-481) with their
+ * VJPs (autodiff.py:1363-1459).  A and B are each either K-contiguous
+ * (stride_k == 1) or M/N-contiguous (stride_m/stride_n == 1); D is
+ * N-contiguous.  bf16 inputs run on tcgen05 tensor cores (TMA-fed, TMEM
+ * accumulator) when the shape tiles (m%128, n%16, k%64, 16B-aligned strides);
+ * everything else (and f32) runs on the CUDA-core FP32 path so f32 results
+ * meet the 1e-4 parity bar. */
+enum dfx_epilogue {
+  DFX_EPI_NONE = 0,      /* D = alpha*acc                                     */
+  DFX_EPI_BIAS = 1,      /* D = alpha*acc + bias[n]                           */
+  DFX_EPI_BIAS_GELU = 2, /* pre = alpha*acc + bias[n]; aux_out = pre; D = gelu(pre) */
+  DFX_EPI_GELU_BWD = 3,  /* D = alpha*acc * gelu'(aux)                        */
+  DFX_EPI_ADD = 4        /* D = alpha*acc + beta*aux                          */
+};
+
+typedef struct dfx_gemm_args {
+  int32_t in_dtype;   /* DFX_F32 or DFX_BF16 (A and B)                */
+  int32_t out_dtype;  /* DFX_F32 or DFX_BF16 (D, aux, aux_out)         */
+  int32_t epilogue;   /* enum dfx_epilogue                             */
+  int32_t force_simt; /* 1: skip the tensor-core path (testing)        */
+  int64_t m, n, k;
+  int64_t batch1, batch2; /* >= 1 */
+  const void* a;
+  int64_t a_stride_m, a_stride_k, a_stride_b1, a_stride_b2;
+  const void* b;
+  int64_t b_stride_n, b_stride_k, b_stride_b1, b_stride_b2;
+  void* d;
+  int64_t d_stride_m, d_stride_b1, d_stride_b2;
+  float alpha, beta;
+  const float* bias; /* [n] */
+  const void* aux;
+  int64_t aux_stride_m, aux_stride_b1, aux_stride_b2;
+  void* aux_out;
+  int64_t aux_out_stride_m, aux_out_stride_b1, aux_out_stride_b2;
+} dfx_gemm_args;
+
+int dfx_gemm(const dfx_gemm_args* args, void* stream);
+/* 1 if the call would take the tcgen05 path. */
+int dfx_gemm_uses_tensor_cores(const dfx_gemm_args* args);
+
+/* ---- optimizer (the user-written SGD step of the training loop) --
+ * master -= lr * grad (f32); if weights_bf16 != NULL also refresh the bf16 copy. */
+int dfx_sgd_update(int64_t n, float* master, const float* grad, float lr, void* weights_bf16,
+                   void* stream);
+/* y = x * scale (f32, in place allowed) — gradient averaging after allreduce. */
+int dfx_scale_f32(int64_t n, float* x, float scale, void* stream);
+/* bf16 <-> f32 casts of flat buffers. */
+int dfx_cast(int64_t n, int src_dtype, const void* src, int dst_dtype, void* dst, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* DFX_H_ */

@@ -222,11 +222,21 @@ BERT_WEIGHTS = ("wq", "wk", "wv", "wo", "w1", "w2", "bq", "bk", "bv", "bo", "b1"
                 "g1", "be1", "g2", "be2")
 
 
-def bert_layer_fwd(prm, x, am, dm, m1, m2, B, S, NH, eps=1e-12):
+def _ident(a):
+    return a
+
+
+def bert_layer_fwd(prm, x, am, dm, m1, m2, B, S, NH, eps=1e-12, rnd=None):
     """Forward of one post-LN encoder layer with explicit dropout masks.
 
     prm: dict of weights (Linear layout [out, in]); x [T,H]; am [B,1,1,S]
-    additive mask; dm [B,NH,S,S], m1/m2 [T,H] dropout mask values."""
+    additive mask; dm [B,NH,S,S], m1/m2 [T,H] dropout mask values.
+
+    ``rnd`` (default: identity) is the storage model: it is applied to every
+    intermediate the B200 path materialises in HBM, at the point it is
+    stored (``round_bf16`` emulates the bf16 pipeline; the arithmetic itself
+    stays float64).  With the identity this is exactly the reference chain."""
+    R = rnd or _ident
     x = _a(x)
     T, H = x.shape
     dh = H // NH
@@ -235,56 +245,61 @@ def bert_layer_fwd(prm, x, am, dm, m1, m2, B, S, NH, eps=1e-12):
     def heads(t):
         return t.reshape(B, S, NH, dh)
 
-    q = heads(gemm(x, P["wq"], P["bq"], trans_b=True))
-    k = heads(gemm(x, P["wk"], P["bk"], trans_b=True))
-    v = heads(gemm(x, P["wv"], P["bv"], trans_b=True))
-    sc = np.einsum("bsnd,btnd->bnst", q, k)
-    p, pd = scaled_masked_softmax_fwd(sc, float(np.sqrt(dh)), am, dm)
-    ctx = np.einsum("bnst,btnd->bsnd", pd, v).reshape(T, H)
-    a1 = gemm(ctx, P["wo"], trans_b=True)
+    q = heads(R(gemm(x, P["wq"], P["bq"], trans_b=True)))
+    k = heads(R(gemm(x, P["wk"], P["bk"], trans_b=True)))
+    v = heads(R(gemm(x, P["wv"], P["bv"], trans_b=True)))
+    sc = R(np.einsum("bsnd,btnd->bnst", q, k))
+    p_exact, pd = scaled_masked_softmax_fwd(sc, float(np.sqrt(dh)), am, dm)
+    p, pd = R(p_exact), R(pd)
+    ctx = R(np.einsum("bnst,btnd->bsnd", pd, v).reshape(T, H))
+    a1 = R(gemm(ctx, P["wo"], trans_b=True))
     r1 = bdrln_fwd(a1, P["bo"], m1, x, P["g1"], P["be1"], eps)
-    ln1 = r1["y"]
-    pre, g = bias_gelu_fwd(gemm(ln1, P["w1"], trans_b=True), P["b1"])
-    a2 = gemm(g, P["w2"], trans_b=True)
+    ln1 = R(r1["y"])
+    pre_exact, g = bias_gelu_fwd(gemm(ln1, P["w1"], trans_b=True), P["b1"])
+    pre, g = R(pre_exact), R(g)
+    a2 = R(gemm(g, P["w2"], trans_b=True))
     r2 = bdrln_fwd(a2, P["b2"], m2, ln1, P["g2"], P["be2"], eps)
-    cache = dict(x=x, q=q, k=k, v=v, p=p, pd=pd, ctx=ctx, s1=r1["s"], ln1=ln1, pre=pre, g=g,
-                 s2=r2["s"], dm=_a(dm), m1=_a(m1), m2=_a(m2), B=B, S=S, NH=NH, eps=eps)
-    return r2["y"], cache
+    cache = dict(x=x, q=q, k=k, v=v, p=p, pd=pd, ctx=ctx, s1=R(r1["s"]), ln1=ln1, pre=pre, g=g,
+                 s2=R(r2["s"]), dm=_a(dm), m1=_a(m1), m2=_a(m2), B=B, S=S, NH=NH, eps=eps, rnd=R)
+    return R(r2["y"]), cache
 
 
 def bert_layer_bwd(prm, cache, dout):
-    """Reverse pass of bert_layer_fwd; returns grads keyed like prm plus 'x'."""
+    """Reverse pass of bert_layer_fwd; returns grads keyed like prm plus 'x'.
+    Stored gradient activations go through the same storage model."""
     P = {k: _a(v) for k, v in prm.items()}
     c = cache
+    R = c.get("rnd") or _ident
     B, S, NH, eps = c["B"], c["S"], c["NH"], c["eps"]
     T, H = c["x"].shape
     dh = H // NH
     gr = {}
     r2 = bdrln_bwd(dout, c["s2"], P["g2"], c["m2"], eps)
     gr["g2"], gr["be2"], gr["b2"] = r2["dgamma"], r2["dbeta"], r2["dbias"]
-    da2 = r2["dh"]
+    ds2, da2 = R(r2["ds"]), R(r2["dh"])
     gr["w2"] = da2.T @ c["g"]
-    dg = da2 @ P["w2"]
-    dpre, gr["b1"] = bias_gelu_bwd(dg, c["pre"])
+    dpre, _ = bias_gelu_bwd(da2 @ P["w2"], c["pre"])
+    dpre = R(dpre)
+    gr["b1"] = dpre.sum(0)
     gr["w1"] = dpre.T @ c["ln1"]
-    dln1 = dpre @ P["w1"] + r2["ds"]
+    dln1 = R(dpre @ P["w1"] + ds2)
     r1 = bdrln_bwd(dln1, c["s1"], P["g1"], c["m1"], eps)
     gr["g1"], gr["be1"], gr["bo"] = r1["dgamma"], r1["dbeta"], r1["dbias"]
-    da1 = r1["dh"]
+    ds1, da1 = R(r1["ds"]), R(r1["dh"])
     gr["wo"] = da1.T @ c["ctx"]
-    dctx = (da1 @ P["wo"]).reshape(B, S, NH, dh)
-    dpd = np.einsum("bsnd,btnd->bnst", dctx, c["v"])
-    dv = np.einsum("bnst,bsnd->btnd", c["pd"], dctx)
-    dsc = scaled_masked_softmax_bwd(dpd, c["p"], c["dm"], float(np.sqrt(dh)))
-    dq = np.einsum("bnst,btnd->bsnd", dsc, c["k"])
-    dk = np.einsum("bnst,bsnd->btnd", dsc, c["q"])
-    dx = r1["ds"].copy()
+    dctx = R(da1 @ P["wo"]).reshape(B, S, NH, dh)
+    dpd = R(np.einsum("bsnd,btnd->bnst", dctx, c["v"]))
+    dv = R(np.einsum("bnst,bsnd->btnd", c["pd"], dctx))
+    dsc = R(scaled_masked_softmax_bwd(dpd, c["p"], c["dm"], float(np.sqrt(dh))))
+    dq = R(np.einsum("bnst,btnd->bsnd", dsc, c["k"]))
+    dk = R(np.einsum("bnst,bsnd->btnd", dsc, c["q"]))
+    dx = ds1.copy()
     for t, d in (("q", dq), ("k", dk), ("v", dv)):
         d2 = d.reshape(T, H)
         gr["w" + t] = d2.T @ c["x"]
         gr["b" + t] = d2.sum(0)
         dx += d2 @ P["w" + t]
-    gr["x"] = dx
+    gr["x"] = R(dx)
     return gr
 
 

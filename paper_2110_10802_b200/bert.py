@@ -1,0 +1,369 @@
+"""BERT encoder layer training step on the B200 hot path.
+
+The layer is the one the reference expresses with registry operators
+(golden graph in oracle/make_golden.py):
+
+    QKV   = x @ Wqkvᵀ + bqkv                           Gemm (frontend.py:369-405)
+    S     = Q Kᵀ (per batch, head)                     Einsum bsnd,btnd->bnst (408-481)
+    P, Pd = softmax(S / sqrt(dh) + mask), P * drop     Div/Add/Softmax/Mul (294, 175-188, 493-501)
+    ctx   = Pd V                                       Einsum bnst,btnd->bsnd
+    ln1   = LN((ctx Woᵀ + bo) * drop1 + x)             Gemm/Add/Mul/Add/LayerNormalization (519-529)
+    g     = gelu_tanh(ln1 W1ᵀ + b1)                    Gemm + Pow/Mul/Add/Tanh chain (223-295)
+    out   = LN((g W2ᵀ + b2) * drop2 + ln1)
+
+and its reverse pass follows the manual VJPs of autodiff.py (Gemm/Einsum
+1363-1459, Softmax 1465-1484, LayerNormalization 1490-1545) and the symexpr
+derivative of the GELU chain.  Every operation is one call into the sm_100a
+library: 9 launches forward (5 tcgen05 GEMMs carrying bias / bias+GELU
+epilogues, the fused softmax, two fused bias+dropout+residual+LN kernels) and
+the mirrored backward.  Weights live in one flat f32 master arena (plus a bf16
+copy of it for the tensor cores) and gradients in one flat f32 arena, so the
+data-parallel allreduce and the SGD step each touch a single buffer.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from . import kernels as K
+from ._lib import EPI_ADD, EPI_BIAS, EPI_BIAS_GELU, EPI_GELU_BWD
+from .errors import ShapeError
+
+
+@dataclass(frozen=True)
+class BertLayerConfig:
+    hidden: int = 768
+    heads: int = 12
+    ffn: int = 3072
+    eps: float = 1e-12
+    p_drop: float = 0.1
+    dtype: torch.dtype = torch.bfloat16
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+
+def _param_specs(c: BertLayerConfig):
+    H, F = c.hidden, c.ffn
+    return [("wqkv", (3 * H, H)), ("wo", (H, H)), ("w1", (F, H)), ("w2", (H, F)),
+            ("bqkv", (3 * H,)), ("bo", (H,)), ("g1", (H,)), ("be1", (H,)), ("b1", (F,)),
+            ("b2", (H,)), ("g2", (H,)), ("be2", (H,))]
+
+
+MATRICES = ("wqkv", "wo", "w1", "w2")
+
+
+class FlatArena:
+    """Named views into one contiguous buffer (parameters or gradients)."""
+
+    def __init__(self, specs, dtype, device):
+        self.offsets = {}
+        off = 0
+        for name, shape in specs:
+            n = 1
+            for d in shape:
+                n *= d
+            # keep every view 16-byte aligned for 128-bit / TMA access
+            self.offsets[name] = (off, shape)
+            off += (n + 7) // 8 * 8
+        self.flat = torch.zeros(off, dtype=dtype, device=device)
+        self.views = {name: self.flat[o:o + _numel(s)].view(s) for name, (o, s) in self.offsets.items()}
+
+    def __getitem__(self, name):
+        return self.views[name]
+
+
+def _numel(shape):
+    n = 1
+    for d in shape:
+        n *= d
+    return n
+
+
+class BertEncoderLayer:
+    def __init__(self, cfg: BertLayerConfig = BertLayerConfig(), device="cuda", seed: int = 0):
+        if cfg.dtype not in (torch.float32, torch.bfloat16):
+            raise ShapeError("BertEncoderLayer: dtype must be float32 or bfloat16")
+        if cfg.hidden % cfg.heads:
+            raise ShapeError("hidden must be divisible by heads")
+        _lib.load(check_device=True)
+        self.cfg = cfg
+        self.device = torch.device(device)
+        specs = _param_specs(cfg)
+        self.master = FlatArena(specs, torch.float32, self.device)
+        self.grad = FlatArena(specs, torch.float32, self.device)
+        self.wlow = FlatArena(specs, torch.bfloat16, self.device) if cfg.dtype == torch.bfloat16 else None
+        self._bufs = {}
+        self._init_params(seed)
+
+    # ------------------------------------------------------------ parameters
+    def _init_params(self, seed):
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        H = self.cfg.hidden
+        vals = {}
+        for name, shape in _param_specs(self.cfg):
+            if name.startswith("w"):
+                vals[name] = 0.02 * torch.randn(shape, generator=g)
+            elif name.startswith("g"):
+                vals[name] = 1.0 + 0.1 * torch.randn(shape, generator=g)
+            else:
+                vals[name] = 0.1 * torch.randn(shape, generator=g)
+        del H
+        self.load_params(vals)
+
+    def load_params(self, vals: dict):
+        """Load weights given either fused ``wqkv``/``bqkv`` or the separate
+        ``wq, wk, wv`` / ``bq, bk, bv`` of the reference graph."""
+        v = {k: torch.as_tensor(x, dtype=torch.float32) for k, x in vals.items()}
+        if "wq" in v:
+            v["wqkv"] = torch.cat([v.pop("wq"), v.pop("wk"), v.pop("wv")], 0)
+            v["bqkv"] = torch.cat([v.pop("bq"), v.pop("bk"), v.pop("bv")], 0)
+        for name, _ in _param_specs(self.cfg):
+            self.master[name].copy_(v[name].to(self.device))
+        self.refresh_low_precision()
+
+    def refresh_low_precision(self):
+        if self.wlow is not None:
+            K.cast(self.master.flat, self.wlow.flat)
+
+    def weight(self, name):
+        """Matrix operand as consumed by the GEMMs (bf16 copy or f32 master)."""
+        return self.wlow[name] if self.wlow is not None else self.master[name]
+
+    def params_numpy(self, split_qkv=True):
+        out = {k: v.detach().cpu().numpy().astype("float64") for k, v in self.master.views.items()}
+        if self.wlow is not None:  # the GEMMs see bf16-rounded matrices
+            for k in MATRICES:
+                out[k] = self.wlow[k].float().cpu().numpy().astype("float64")
+        if split_qkv:
+            H = self.cfg.hidden
+            w, b = out.pop("wqkv"), out.pop("bqkv")
+            for i, t in enumerate("qkv"):
+                out["w" + t] = w[i * H:(i + 1) * H]
+                out["b" + t] = b[i * H:(i + 1) * H]
+        return out
+
+    def grads_numpy(self, split_qkv=True):
+        out = {k: v.detach().cpu().numpy().astype("float64") for k, v in self.grad.views.items()}
+        if split_qkv:
+            H = self.cfg.hidden
+            w, b = out.pop("wqkv"), out.pop("bqkv")
+            for i, t in enumerate("qkv"):
+                out["w" + t] = w[i * H:(i + 1) * H]
+                out["b" + t] = b[i * H:(i + 1) * H]
+        return out
+
+    @property
+    def num_params(self) -> int:
+        return sum(_numel(s) for _, s in _param_specs(self.cfg))
+
+    # ------------------------------------------------------------ activations
+    def buffers(self, B: int, S: int):
+        key = (B, S)
+        if key not in self._bufs:
+            c = self.cfg
+            T, H, F, NH = B * S, c.hidden, c.ffn, c.heads
+            dt, dev = c.dtype, self.device
+            e = lambda *s: torch.empty(s, dtype=dt, device=dev)  # noqa: E731
+            self._bufs[key] = dict(
+                qkv=e(T, 3 * H), scores=e(B, NH, S, S), p=e(B, NH, S, S), pd=e(B, NH, S, S),
+                ctx=e(T, H), a1=e(T, H), s1=e(T, H), ln1=e(T, H), pre=e(T, F), g=e(T, F),
+                a2=e(T, H), s2=e(T, H), out=e(T, H),
+                ds2=e(T, H), da2=e(T, H), dpre=e(T, F), dln1=e(T, H), ds1=e(T, H), da1=e(T, H),
+                dctx=e(T, H), dpd=e(B, NH, S, S), dsc=e(B, NH, S, S), dqkv=e(T, 3 * H), dx=e(T, H),
+            )
+        return self._bufs[key]
+
+    def _heads(self, t, B, S, which):
+        """[B, NH, S, dh] view of the Q/K/V (which=0/1/2) block of a [T, 3H] tensor."""
+        c = self.cfg
+        H, NH, dh = c.hidden, c.heads, c.head_dim
+        return t.as_strided((B, NH, S, dh), (S * 3 * H, dh, 3 * H, 1), t.storage_offset() + which * H)
+
+    def _ctx_heads(self, t, B, S):
+        c = self.cfg
+        return t.as_strided((B, c.heads, S, c.head_dim), (S * c.hidden, c.head_dim, c.hidden, 1),
+                            t.storage_offset())
+
+    # ------------------------------------------------------------ forward
+    def forward(self, x, add_mask, keep_attn, keep1, keep2):
+        """x [T, H] (T = B*S); add_mask f32 [B, S]; keep_* u8 dropout keep flags
+        ([B, NH, S, S], [T, H], [T, H]).  Returns the layer output [T, H]."""
+        c = self.cfg
+        B, S = add_mask.shape
+        T = B * S
+        if x.shape != (T, c.hidden) or x.dtype != c.dtype:
+            raise ShapeError(f"x must be [{T}, {c.hidden}] {c.dtype}")
+        ks = 1.0 / (1.0 - c.p_drop)
+        b = self.buffers(B, S)
+        P = self.master
+        self._saved = (x, add_mask, keep_attn, keep1, keep2, B, S)
+        L = K.label
+        with L("fwd.qkv_gemm+bias"):
+            K.gemm(x, self.weight("wqkv"), b["qkv"], EPI_BIAS, bias=P["bqkv"])
+        q, k, v = (self._heads(b["qkv"], B, S, i) for i in range(3))
+        with L("fwd.scores_gemm"):
+            K.gemm(q, k, b["scores"])
+        with L("fwd.softmax"):
+            K.softmax_fwd(b["scores"], 1.0 / (c.head_dim ** 0.5), add_mask, keep_attn, ks, b["p"], b["pd"])
+        with L("fwd.ctx_gemm"):
+            K.gemm(b["pd"], v.transpose(-1, -2), self._ctx_heads(b["ctx"], B, S))
+        with L("fwd.out_gemm"):
+            K.gemm(b["ctx"], self.weight("wo"), b["a1"])
+        with L("fwd.bdrln1"):
+            K.bdrln_fwd(b["a1"], P["bo"], keep1, ks, x, P["g1"], P["be1"], c.eps, y=b["ln1"], s=b["s1"])
+        with L("fwd.ffn1_gemm+bias+gelu"):
+            K.gemm(b["ln1"], self.weight("w1"), b["g"], EPI_BIAS_GELU, bias=P["b1"], aux_out=b["pre"])
+        with L("fwd.ffn2_gemm"):
+            K.gemm(b["g"], self.weight("w2"), b["a2"])
+        with L("fwd.bdrln2"):
+            K.bdrln_fwd(b["a2"], P["b2"], keep2, ks, b["ln1"], P["g2"], P["be2"], c.eps, y=b["out"], s=b["s2"])
+        return b["out"]
+
+    # ------------------------------------------------------------ backward
+    def backward(self, dout):
+        """Gradients of <dout, out> w.r.t. x (returned) and every parameter
+        (written into ``self.grad``)."""
+        c = self.cfg
+        x, add_mask, keep_attn, keep1, keep2, B, S = self._saved
+        ks = 1.0 / (1.0 - c.p_drop)
+        b = self.buffers(B, S)
+        P, G = self.master, self.grad
+        L = K.label
+        with L("bwd.bdrln2"):
+            K.bdrln_bwd(dout, b["s2"], P["g2"], keep2, ks, c.eps, ds=b["ds2"], dh=b["da2"],
+                        dgamma=G["g2"], dbeta=G["be2"], dbias=G["b2"])
+        # FFN2: dgrad with the GELU-backward epilogue, wgrad straight into f32 grads
+        with L("bwd.ffn2_dgrad+gelu_bwd"):
+            K.gemm(b["da2"], self.weight("w2").t(), b["dpre"], EPI_GELU_BWD, aux=b["pre"])
+        with L("bwd.ffn2_wgrad"):
+            K.gemm(b["da2"].t(), b["g"].t(), G["w2"])
+        with L("bwd.ffn1_bias_grad"):
+            K.colsum(b["dpre"], G["b1"])
+        # FFN1: dgrad + residual gradient from LN2
+        with L("bwd.ffn1_dgrad+residual"):
+            K.gemm(b["dpre"], self.weight("w1").t(), b["dln1"], EPI_ADD, aux=b["ds2"])
+        with L("bwd.ffn1_wgrad"):
+            K.gemm(b["dpre"].t(), b["ln1"].t(), G["w1"])
+        with L("bwd.bdrln1"):
+            K.bdrln_bwd(b["dln1"], b["s1"], P["g1"], keep1, ks, c.eps, ds=b["ds1"], dh=b["da1"],
+                        dgamma=G["g1"], dbeta=G["be1"], dbias=G["bo"])
+        with L("bwd.out_dgrad"):
+            K.gemm(b["da1"], self.weight("wo").t(), b["dctx"])
+        with L("bwd.out_wgrad"):
+            K.gemm(b["da1"].t(), b["ctx"].t(), G["wo"])
+        # attention
+        q, k, v = (self._heads(b["qkv"], B, S, i) for i in range(3))
+        dq, dk, dv = (self._heads(b["dqkv"], B, S, i) for i in range(3))
+        dctx = self._ctx_heads(b["dctx"], B, S)
+        with L("bwd.dprobs_gemm"):
+            K.gemm(dctx, v, b["dpd"])
+        with L("bwd.dv_gemm"):
+            K.gemm(b["pd"].transpose(-1, -2), dctx.transpose(-1, -2), dv)
+        with L("bwd.softmax"):
+            K.softmax_bwd(b["dpd"], b["p"], keep_attn, ks, 1.0 / (c.head_dim ** 0.5), out=b["dsc"])
+        with L("bwd.dq_gemm"):
+            K.gemm(b["dsc"], k.transpose(-1, -2), dq)
+        with L("bwd.dk_gemm"):
+            K.gemm(b["dsc"].transpose(-1, -2), q.transpose(-1, -2), dk)
+        with L("bwd.qkv_bias_grad"):
+            K.colsum(b["dqkv"], G["bqkv"])
+        with L("bwd.qkv_dgrad+residual"):
+            K.gemm(b["dqkv"], self.weight("wqkv").t(), b["dx"], EPI_ADD, aux=b["ds1"])
+        with L("bwd.qkv_wgrad"):
+            K.gemm(b["dqkv"].t(), x.t(), G["wqkv"])
+        return b["dx"]
+
+    def sgd_step(self, lr: float):
+        with K.label("sgd_update"):
+            K.sgd_update(self.master.flat, self.grad.flat, lr,
+                         None if self.wlow is None else self.wlow.flat)
+
+    def train_step(self, x, add_mask, keep_attn, keep1, keep2, dout, lr=None):
+        out = self.forward(x, add_mask, keep_attn, keep1, keep2)
+        dx = self.backward(dout)
+        if lr is not None:
+            self.sgd_step(lr)
+        return out, dx
+
+    # ------------------------------------------------------------ host-buffer API
+    def host_inputs_bytes(self, B: int, S: int) -> tuple[int, int]:
+        """(H2D, D2H) bytes per train_step_host call."""
+        c = self.cfg
+        T, H = B * S, c.hidden
+        esz = torch.tensor([], dtype=c.dtype).element_size()
+        h2d = 2 * T * H * esz + B * S * 4 + B * c.heads * S * S + 2 * T * H
+        return h2d, T * H * esz
+
+    def train_step_host(self, host: dict, lr=None, dx_host=None, graph=True):
+        """One training step from HOST buffers: copies x, dout, the additive
+        mask and the dropout keep masks to the device (pinned memory,
+        stream-ordered), runs forward + backward (+ SGD when ``lr`` is given)
+        as one CUDA-graph replay and copies dx back into ``dx_host``.  This
+        is the call the e2e benchmark times: the reference's
+        ``interp.execute`` likewise takes host arrays (interp.py:1301-1317)."""
+        B, S = host["add_mask"].shape
+        dev = self._dev_inputs(B, S)
+        for k in ("x", "add_mask", "keep_attn", "keep1", "keep2", "dout"):
+            dev[k].copy_(host[k], non_blocking=True)
+        if graph:
+            key = ("graph", B, S, lr)
+            if key not in self._bufs:
+                self._bufs[key] = self.capture_step(B, S, lr)
+            self._bufs[key].replay()
+            dx = self.buffers(B, S)["dx"]
+        else:
+            self.forward(dev["x"], dev["add_mask"], dev["keep_attn"], dev["keep1"], dev["keep2"])
+            dx = self.backward(dev["dout"])
+            if lr is not None:
+                self.sgd_step(lr)
+        if dx_host is not None:
+            dx_host.copy_(dx, non_blocking=True)
+        return dx_host
+
+    def _dev_inputs(self, B, S):
+        key = ("in", B, S)
+        if key not in self._bufs:
+            c = self.cfg
+            T, H, NH, dev = B * S, c.hidden, c.heads, self.device
+            u8 = torch.uint8
+            self._bufs[key] = dict(
+                x=torch.empty(T, H, dtype=c.dtype, device=dev),
+                dout=torch.empty(T, H, dtype=c.dtype, device=dev),
+                add_mask=torch.empty(B, S, dtype=torch.float32, device=dev),
+                keep_attn=torch.empty(B, NH, S, S, dtype=u8, device=dev),
+                keep1=torch.empty(T, H, dtype=u8, device=dev),
+                keep2=torch.empty(T, H, dtype=u8, device=dev))
+        return self._bufs[key]
+
+    # ------------------------------------------------------------ CUDA graphs
+    def capture_step(self, B: int, S: int, lr=None, timer=None):
+        """Capture forward + backward (+ SGD) on the static device input
+        buffers (``device_inputs``) into a CUDA graph; returns a
+        ``CapturedStep`` whose ``replay()`` runs one training step."""
+        from .graphs import CapturedStep
+
+        dev = self._dev_inputs(B, S)
+
+        def fn():
+            self.forward(dev["x"], dev["add_mask"], dev["keep_attn"], dev["keep1"], dev["keep2"])
+            self.backward(dev["dout"])
+            if lr is not None:
+                self.sgd_step(lr)
+
+        if timer is None:
+            return CapturedStep(fn)
+        cs = CapturedStep(fn)  # warm-up/capture without events, then an instrumented twin
+        timer.reset_records()
+        with timer:
+            inst = CapturedStep(fn, warmup=0)
+        return cs, inst
+
+    def device_inputs(self, B: int, S: int) -> dict:
+        """Static device buffers a captured step reads (fill before replay)."""
+        return self._dev_inputs(B, S)
+

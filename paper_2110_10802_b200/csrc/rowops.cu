@@ -1,0 +1,788 @@
+// rowops.cu — HBM-bound row kernels of the BERT encoder hot path (sm_100a).
+//
+//  * bias + dropout + residual + LayerNorm, forward and backward
+//      reference: Add/Mul/Add (frontend.py:291-293) + LayerNormalization
+//      (frontend.py:519-529), VJP autodiff.py:1490-1545.
+//  * scaled + masked softmax + dropout, forward and backward
+//      reference: Div (frontend.py:294) + Add (175-188) + Softmax (493-501) +
+//      Mul (293), VJP autodiff.py:1465-1484.
+//  * bias + tanh-GELU forward/backward (frontend.py:223-295 chain).
+//  * deterministic column sums (bias gradients, autodiff.py:1452-1458).
+//
+// Layout: one warp per row, every lane owns NCH chunks of V contiguous
+// elements (128-bit accesses: V=8 for bf16, V=4 for f32), so the row lives in
+// registers between the reduction and the write-back: each tensor is read once
+// and written once.  Row statistics use warp shuffles only.  Column
+// reductions keep per-lane partials for the lane's fixed columns across a
+// grid-stride loop over rows, reduce the 8 warps of a block in fixed order
+// through shared memory and finish with a fixed-order pass over blocks — no
+// float atomics, so results are bitwise reproducible.
+#include "common.cuh"
+
+namespace dfx {
+namespace {
+
+constexpr int kWarps = 8;            // rows per 256-thread block
+constexpr int kMaxColBlocks = 296;   // 2 x 148 SMs: partial-sum slots
+
+template <typename T> struct VecWidth { static constexpr int value = 8; };
+template <> struct VecWidth<float> { static constexpr int value = 4; };
+
+// ---------------------------------------------------------------------------
+// bias + dropout + residual + LayerNorm
+
+template <typename T, int V, int NCH>
+__global__ void __launch_bounds__(256) bdrln_fwd_kernel(
+    int64_t rows, int cols, const T* __restrict__ h, const float* __restrict__ bias,
+    const uint8_t* __restrict__ keep, float ks, const T* __restrict__ res,
+    const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+    T* __restrict__ y, T* __restrict__ s_out, float* __restrict__ mean_out,
+    float* __restrict__ rstd_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kWarps + warp;
+  if (row >= rows) return;
+  const int nvec = cols / V;
+  const size_t base = (size_t)row * cols;
+  float x[NCH][V];
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      const int col = vi * V;
+      Vec<T, V> hv;
+      hv.load(h + base + col);
+      float b[V], m[V], r[V];
+      if (bias) { Vec<float, V> bv; bv.load(bias + col);
+#pragma unroll
+        for (int i = 0; i < V; ++i) b[i] = bv.v[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) b[i] = 0.f;
+      }
+      if (keep) load_keep<V>(keep + base + col, ks, m);
+      else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) m[i] = 1.f;
+      }
+      if (res) { Vec<T, V> rv; rv.load(res + base + col);
+#pragma unroll
+        for (int i = 0; i < V; ++i) r[i] = rv.v[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) r[i] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        x[c][i] = (hv.v[i] + b[i]) * m[i] + r[i];
+        sum += x[c][i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[c][i] = 0.f;
+    }
+  }
+  const float inv_n = 1.f / (float)cols;
+  const float mu = warp_sum(sum) * inv_n;
+  float sq = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (lane + c * 32 < nvec) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) { const float d = x[c][i] - mu; sq += d * d; }
+    }
+  }
+  const float var = warp_sum(sq) * inv_n;
+  const float rstd = rsqrtf(var + eps);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      const int col = vi * V;
+      Vec<float, V> g, bt;
+      g.load(gamma + col);
+      bt.load(beta + col);
+      if (s_out) {
+        Vec<T, V> sv;
+#pragma unroll
+        for (int i = 0; i < V; ++i) sv.v[i] = x[c][i];
+        sv.store(s_out + base + col);
+      }
+      Vec<T, V> yv;
+#pragma unroll
+      for (int i = 0; i < V; ++i) yv.v[i] = (x[c][i] - mu) * rstd * g.v[i] + bt.v[i];
+      yv.store(y + base + col);
+    }
+  }
+  if (lane == 0) {
+    if (mean_out) mean_out[row] = mu;
+    if (rstd_out) rstd_out[row] = rstd;
+  }
+}
+
+// Fixed-order reduction of per-lane column partials of the 8 warps of a block
+// into part[blockIdx.x * cols + col].  acc is [NCH][V] per lane.
+template <int V, int NCH>
+__device__ __forceinline__ void block_colsum_store(float (&acc)[NCH][V], int cols, float* red,
+                                                   float* __restrict__ part) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nvec = cols / V;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) red[warp * cols + vi * V + i] = acc[c][i];
+    }
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += red[w * cols + col];
+    part[(size_t)blockIdx.x * cols + col] = s;
+  }
+  __syncthreads();
+}
+
+template <typename T, int V, int NCH>
+__global__ void __launch_bounds__(256) bdrln_bwd_kernel(
+    int64_t rows, int cols, const T* __restrict__ dy, const T* __restrict__ s,
+    const float* __restrict__ gamma, const uint8_t* __restrict__ keep, float ks, float eps,
+    T* __restrict__ ds_out, T* __restrict__ dh_out, float* __restrict__ part_g,
+    float* __restrict__ part_b, float* __restrict__ part_h) {
+  extern __shared__ float red[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nvec = cols / V;
+  const float inv_n = 1.f / (float)cols;
+  float acc_g[NCH][V], acc_b[NCH][V], acc_h[NCH][V];
+  float gam[NCH][V];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+#pragma unroll
+    for (int i = 0; i < V; ++i) { acc_g[c][i] = 0.f; acc_b[c][i] = 0.f; acc_h[c][i] = 0.f; gam[c][i] = 0.f; }
+    if (vi < nvec) {
+      Vec<float, V> g; g.load(gamma + vi * V);
+#pragma unroll
+      for (int i = 0; i < V; ++i) gam[c][i] = g.v[i];
+    }
+  }
+  for (int64_t row = (int64_t)blockIdx.x * kWarps + warp; row < rows;
+       row += (int64_t)gridDim.x * kWarps) {
+    const size_t base = (size_t)row * cols;
+    float x[NCH][V], g[NCH][V];
+    float sum = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int vi = lane + c * 32;
+      if (vi < nvec) {
+        Vec<T, V> sv, dv;
+        sv.load(s + base + vi * V);
+        dv.load(dy + base + vi * V);
+#pragma unroll
+        for (int i = 0; i < V; ++i) { x[c][i] = sv.v[i]; g[c][i] = dv.v[i]; sum += sv.v[i]; }
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) { x[c][i] = 0.f; g[c][i] = 0.f; }
+      }
+    }
+    const float mu = warp_sum(sum) * inv_n;
+    float sq = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+      if (lane + c * 32 < nvec) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) { const float d = x[c][i] - mu; sq += d * d; }
+      }
+    const float rstd = rsqrtf(warp_sum(sq) * inv_n + eps);
+    float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        x[c][i] = (x[c][i] - mu) * rstd;  // xhat (0 on padding lanes: gamma=0, dy=0)
+        const float dyg = g[c][i] * gam[c][i];
+        m1 += dyg;
+        m2 += dyg * x[c][i];
+      }
+    m1 = warp_sum(m1) * inv_n;
+    m2 = warp_sum(m2) * inv_n;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int vi = lane + c * 32;
+      if (vi < nvec) {
+        const int col = vi * V;
+        float m[V];
+        if (keep) load_keep<V>(keep + base + col, ks, m);
+        else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) m[i] = 1.f;
+        }
+        Vec<T, V> dsv, dhv;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const float dsi = rstd * (g[c][i] * gam[c][i] - m1 - x[c][i] * m2);
+          dsv.v[i] = dsi;
+          dhv.v[i] = dsi * m[i];
+          acc_g[c][i] += g[c][i] * x[c][i];
+          acc_b[c][i] += g[c][i];
+          acc_h[c][i] += dsi * m[i];
+        }
+        if (ds_out) dsv.store(ds_out + base + col);
+        if (dh_out) dhv.store(dh_out + base + col);
+      }
+    }
+  }
+  block_colsum_store<V, NCH>(acc_g, cols, red, part_g);
+  block_colsum_store<V, NCH>(acc_b, cols, red, part_b);
+  block_colsum_store<V, NCH>(acc_h, cols, red, part_h);
+}
+
+// out_q[col] (+)= sum_b part[q][b][col] for q = blockIdx.y.  Warp w sums
+// partial rows b = w, w+8, ... for 32 consecutive columns (coalesced), then
+// the 8 warp sums are added in fixed order: deterministic.
+__global__ void __launch_bounds__(256) finalize_colsum_kernel(int nparts, int cols,
+                                                              const float* __restrict__ part,
+                                                              float* out0, float* out1, float* out2,
+                                                              int accumulate) {
+  __shared__ float red[kWarps][33];
+  const int q = blockIdx.y;
+  float* out = q == 0 ? out0 : (q == 1 ? out1 : out2);
+  if (out == nullptr) return;
+  const float* pq = part + (size_t)q * nparts * cols;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (col < cols) {
+#pragma unroll 4
+    for (int b = warp; b < nparts; b += kWarps) s += pq[(size_t)b * cols + col];
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && col < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) t += red[w][lane];
+    out[col] = accumulate ? out[col] + t : t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// scaled + masked softmax + dropout
+
+template <typename T, int V, int NCH>
+__global__ void __launch_bounds__(256) softmax_fwd_kernel(
+    int64_t rows, int cols, int64_t rows_per_batch, const T* __restrict__ x, float inv_div,
+    const float* __restrict__ am, const uint8_t* __restrict__ keep, float ks,
+    T* __restrict__ p_out, T* __restrict__ pd_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kWarps + warp;
+  if (row >= rows) return;
+  const int nvec = cols / V;
+  const size_t base = (size_t)row * cols;
+  const float* amr = am ? am + (size_t)(row / rows_per_batch) * cols : nullptr;
+  constexpr float kLog2e = 1.4426950408889634f;
+  float z[NCH][V];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      Vec<T, V> xv;
+      xv.load(x + base + vi * V);
+      float a[V];
+      if (amr) { Vec<float, V> av; av.load(amr + vi * V);
+#pragma unroll
+        for (int i = 0; i < V; ++i) a[i] = av.v[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) a[i] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        z[c][i] = (xv.v[i] * inv_div + a[i]) * kLog2e;
+        mx = fmaxf(mx, z[c][i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) z[c][i] = -INFINITY;
+    }
+  }
+  mx = warp_max(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      z[c][i] = exp2f(z[c][i] - mx);
+      sum += z[c][i];
+    }
+  const float inv = 1.f / warp_sum(sum);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      const int col = vi * V;
+      Vec<T, V> pv;
+#pragma unroll
+      for (int i = 0; i < V; ++i) pv.v[i] = z[c][i] * inv;
+      if (p_out) pv.store(p_out + base + col);
+      if (pd_out) {
+        float m[V];
+        if (keep) load_keep<V>(keep + base + col, ks, m);
+        else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) m[i] = 1.f;
+        }
+        Vec<T, V> dv;
+#pragma unroll
+        for (int i = 0; i < V; ++i) dv.v[i] = pv.v[i] * m[i];
+        dv.store(pd_out + base + col);
+      }
+    }
+  }
+}
+
+template <typename T, int V, int NCH>
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(
+    int64_t rows, int cols, const T* __restrict__ dpd, const T* __restrict__ p,
+    const uint8_t* __restrict__ keep, float ks, float inv_div, T* __restrict__ dx) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kWarps + warp;
+  if (row >= rows) return;
+  const int nvec = cols / V;
+  const size_t base = (size_t)row * cols;
+  float gv[NCH][V], pv[NCH][V];
+  float dot = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      const int col = vi * V;
+      Vec<T, V> a, b;
+      a.load(dpd + base + col);
+      b.load(p + base + col);
+      float m[V];
+      if (keep) load_keep<V>(keep + base + col, ks, m);
+      else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) m[i] = 1.f;
+      }
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        gv[c][i] = a.v[i] * m[i];
+        pv[c][i] = b.v[i];
+        dot += gv[c][i] * pv[c][i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) { gv[c][i] = 0.f; pv[c][i] = 0.f; }
+    }
+  }
+  dot = warp_sum(dot);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      Vec<T, V> o;
+#pragma unroll
+      for (int i = 0; i < V; ++i) o.v[i] = (gv[c][i] - dot) * pv[c][i] * inv_div;
+      o.store(dx + base + vi * V);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bias + GELU (elementwise; one V-vector per thread, grid-stride)
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256) bias_gelu_fwd_kernel(int64_t nvec, int cols,
+                                                            const T* __restrict__ f,
+                                                            const float* __restrict__ bias,
+                                                            T* __restrict__ pre, T* __restrict__ y) {
+  for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec;
+       vi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = vi * V;
+    const int col = (int)(e % cols);
+    Vec<T, V> fv;
+    fv.load(f + e);
+    Vec<T, V> pv, yv;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float x = fv.v[i] + (bias ? bias[col + i] : 0.f);
+      pv.v[i] = x;
+      yv.v[i] = gelu_f(x);
+    }
+    if (pre) pv.store(pre + e);
+    yv.store(y + e);
+  }
+}
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256) gelu_bwd_kernel(int64_t nvec, const T* __restrict__ dy,
+                                                       const T* __restrict__ pre,
+                                                       T* __restrict__ dpre) {
+  for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec;
+       vi += (int64_t)gridDim.x * blockDim.x) {
+    Vec<T, V> a, b, o;
+    a.load(dy + vi * V);
+    b.load(pre + vi * V);
+#pragma unroll
+    for (int i = 0; i < V; ++i) o.v[i] = a.v[i] * gelu_grad_f(b.v[i]);
+    o.store(dpre + vi * V);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// column sums: grid (col strips of 32*V, row groups); part[y][cols]
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256) colsum_kernel(int64_t rows, int cols, int64_t ld,
+                                                     const T* __restrict__ x,
+                                                     float* __restrict__ part) {
+  __shared__ float red[kWarps][32 * V];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col0 = blockIdx.x * 32 * V + lane * V;
+  float acc[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) acc[i] = 0.f;
+  if (col0 < cols) {
+    for (int64_t r = (int64_t)blockIdx.y * kWarps + warp; r < rows; r += (int64_t)gridDim.y * kWarps) {
+      Vec<T, V> v;
+      v.load(x + r * ld + col0);
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] += v.v[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < V; ++i) red[warp][lane * V + i] = acc[i];
+  __syncthreads();
+  for (int j = threadIdx.x; j < 32 * V; j += blockDim.x) {
+    const int col = blockIdx.x * 32 * V + j;
+    if (col < cols) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += red[w][j];
+      part[(size_t)blockIdx.y * cols + col] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// optimizer / casts
+
+__global__ void sgd_kernel(int64_t n, float* __restrict__ w, const float* __restrict__ g, float lr,
+                           __nv_bfloat16* __restrict__ wb) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = w[i] - lr * g[i];
+    w[i] = v;
+    if (wb) wb[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void scale_kernel(int64_t n, float* __restrict__ x, float s) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] *= s;
+}
+
+template <typename S, typename D>
+__global__ void cast_kernel(int64_t n, const S* __restrict__ s, D* __restrict__ d) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = from_f<D>(to_f<S>(s[i]));
+}
+
+// ---------------------------------------------------------------------------
+// host dispatch helpers
+
+inline int grid_for(int64_t n, int per_block, int cap) {
+  int64_t g = (n + per_block - 1) / per_block;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// Row kernels are instantiated for NCH in this list (chunks of 32*V columns).
+#define DFX_NCH_LIST(X) X(1) X(2) X(3) X(4) X(6) X(8) X(12) X(16)
+
+inline int pick_nch(int nvec) {
+  const int need = (nvec + 31) / 32;
+  static const int opts[] = {1, 2, 3, 4, 6, 8, 12, 16};
+  for (int o : opts)
+    if (o >= need) return o;
+  return -1;
+}
+
+template <typename T> int check_row_shape(int64_t cols, const char* op) {
+  constexpr int V = VecWidth<T>::value;
+  if (cols <= 0 || cols % V != 0)
+    return fail(DFX_ERR_SHAPE, std::string(op) + ": cols must be a positive multiple of " + std::to_string(V));
+  if (pick_nch((int)(cols / V)) < 0)
+    return fail(DFX_ERR_SHAPE, std::string(op) + ": cols too large (max " + std::to_string(16 * 32 * V) + ")");
+  return DFX_OK;
+}
+
+size_t colsum_ws_bytes(int64_t rows, int64_t cols) {
+  (void)rows;
+  return (size_t)kMaxColBlocks * (size_t)cols * sizeof(float);
+}
+
+template <typename T>
+int bdrln_fwd_t(int64_t rows, int64_t cols, const void* h, const float* bias, const uint8_t* keep,
+                float ks, const void* res, const float* gamma, const float* beta, float eps, void* y,
+                void* s_out, float* mean, float* rstd, cudaStream_t st) {
+  constexpr int V = VecWidth<T>::value;
+  if (int rc = check_row_shape<T>(cols, "dfx_bdrln_fwd")) return rc;
+  const int nch = pick_nch((int)(cols / V));
+  const int grid = (int)((rows + kWarps - 1) / kWarps);
+  if (rows == 0) return DFX_OK;
+#define L(N)                                                                                  \
+  if (nch == N)                                                                               \
+    bdrln_fwd_kernel<T, V, N><<<grid, 256, 0, st>>>(rows, (int)cols, (const T*)h, bias, keep, ks, \
+                                                    (const T*)res, gamma, beta, eps, (T*)y,   \
+                                                    (T*)s_out, mean, rstd);
+  DFX_NCH_LIST(L)
+#undef L
+  DFX_LAUNCH_CHECK("dfx_bdrln_fwd");
+  return DFX_OK;
+}
+
+template <typename T>
+int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const float* gamma,
+                const uint8_t* keep, float ks, float eps, void* ds, void* dh, float* dgamma,
+                float* dbeta, float* dbias, void* ws, size_t ws_bytes, cudaStream_t st) {
+  constexpr int V = VecWidth<T>::value;
+  if (int rc = check_row_shape<T>(cols, "dfx_bdrln_bwd")) return rc;
+  if (rows == 0) return DFX_OK;
+  const int nch = pick_nch((int)(cols / V));
+  const int grid = grid_for(rows, kWarps, kMaxColBlocks);
+  const size_t need = 3 * (size_t)grid * cols * sizeof(float);
+  DFX_REQUIRE(ws_bytes >= need, DFX_ERR_WORKSPACE, "dfx_bdrln_bwd: workspace too small");
+  float* pg = (float*)ws;
+  float* pb = pg + (size_t)grid * cols;
+  float* ph = pb + (size_t)grid * cols;
+  const size_t smem = (size_t)kWarps * cols * sizeof(float);
+#define L(N)                                                                                       \
+  if (nch == N) {                                                                                  \
+    auto kfn = bdrln_bwd_kernel<T, V, N>;                                                          \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    kfn<<<grid, 256, smem, st>>>(rows, (int)cols, (const T*)dy, (const T*)s, gamma, keep, ks, eps, \
+                                 (T*)ds, (T*)dh, pg, pb, ph);                                      \
+  }
+  DFX_NCH_LIST(L)
+#undef L
+  DFX_LAUNCH_CHECK("dfx_bdrln_bwd");
+  if (dgamma || dbeta || dbias) {
+    finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 3), 256, 0, st>>>(grid, (int)cols, pg, dgamma,
+                                                                               dbeta, dbias, 0);
+    DFX_LAUNCH_CHECK("dfx_bdrln_bwd finalize");
+  }
+  return DFX_OK;
+}
+
+template <typename T>
+int softmax_fwd_t(int64_t batch, int64_t heads, int64_t q, int64_t cols, const void* x, float inv_div,
+                  const float* am, const uint8_t* keep, float ks, void* p, void* pd, cudaStream_t st) {
+  constexpr int V = VecWidth<T>::value;
+  if (int rc = check_row_shape<T>(cols, "dfx_softmax_fwd")) return rc;
+  const int64_t rows = batch * heads * q;
+  if (rows == 0) return DFX_OK;
+  const int nch = pick_nch((int)(cols / V));
+  const int64_t grid = (rows + kWarps - 1) / kWarps;
+#define L(N)                                                                                    \
+  if (nch == N)                                                                                 \
+    softmax_fwd_kernel<T, V, N><<<(unsigned)grid, 256, 0, st>>>(rows, (int)cols, heads * q,     \
+                                                                (const T*)x, inv_div, am, keep, \
+                                                                ks, (T*)p, (T*)pd);
+  DFX_NCH_LIST(L)
+#undef L
+  DFX_LAUNCH_CHECK("dfx_softmax_fwd");
+  return DFX_OK;
+}
+
+template <typename T>
+int softmax_bwd_t(int64_t rows, int64_t cols, const void* dpd, const void* p, const uint8_t* keep,
+                  float ks, float inv_div, void* dx, cudaStream_t st) {
+  constexpr int V = VecWidth<T>::value;
+  if (int rc = check_row_shape<T>(cols, "dfx_softmax_bwd")) return rc;
+  if (rows == 0) return DFX_OK;
+  const int nch = pick_nch((int)(cols / V));
+  const int64_t grid = (rows + kWarps - 1) / kWarps;
+#define L(N)                                                                                     \
+  if (nch == N)                                                                                  \
+    softmax_bwd_kernel<T, V, N><<<(unsigned)grid, 256, 0, st>>>(rows, (int)cols, (const T*)dpd,  \
+                                                                (const T*)p, keep, ks, inv_div,  \
+                                                                (T*)dx);
+  DFX_NCH_LIST(L)
+#undef L
+  DFX_LAUNCH_CHECK("dfx_softmax_bwd");
+  return DFX_OK;
+}
+
+template <typename T>
+int colsum_t(int64_t rows, int64_t cols, const void* x, int64_t ld, float* out, int accumulate,
+             void* ws, size_t ws_bytes, cudaStream_t st) {
+  constexpr int V = VecWidth<T>::value;
+  DFX_REQUIRE(cols > 0 && cols % V == 0 && ld % V == 0, DFX_ERR_SHAPE,
+              "dfx_colsum: cols and ld must be multiples of the vector width");
+  DFX_REQUIRE(aligned16(x), DFX_ERR_ALIGN, "dfx_colsum: x must be 16-byte aligned");
+  const int gx = (int)((cols + 32 * V - 1) / (32 * V));
+  int gy = (int)std::max<int64_t>(1, std::min<int64_t>((rows + kWarps - 1) / kWarps, kMaxColBlocks / gx));
+  DFX_REQUIRE(ws_bytes >= (size_t)gy * cols * sizeof(float), DFX_ERR_WORKSPACE,
+              "dfx_colsum: workspace too small");
+  colsum_kernel<T, V><<<dim3(gx, gy), 256, 0, st>>>(rows, (int)cols, ld, (const T*)x, (float*)ws);
+  DFX_LAUNCH_CHECK("dfx_colsum");
+  finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 1), 256, 0, st>>>(gy, (int)cols, (const float*)ws, out,
+                                                                              nullptr, nullptr, accumulate);
+  DFX_LAUNCH_CHECK("dfx_colsum finalize");
+  return DFX_OK;
+}
+
+}  // namespace
+}  // namespace dfx
+
+using namespace dfx;
+
+extern "C" {
+
+int dfx_bdrln_fwd(int dtype, int64_t rows, int64_t cols, const void* h, const float* bias,
+                  const uint8_t* keep, float keep_scale, const void* residual, const float* gamma,
+                  const float* beta, float eps, void* y, void* s_stash, float* mean, float* rstd,
+                  void* stream) {
+  DFX_REQUIRE(h && gamma && beta && y, DFX_ERR_SHAPE, "dfx_bdrln_fwd: null required pointer");
+  if (dtype == DFX_BF16)
+    return bdrln_fwd_t<__nv_bfloat16>(rows, cols, h, bias, keep, keep_scale, residual, gamma, beta,
+                                      eps, y, s_stash, mean, rstd, as_stream(stream));
+  if (dtype == DFX_F32)
+    return bdrln_fwd_t<float>(rows, cols, h, bias, keep, keep_scale, residual, gamma, beta, eps, y,
+                              s_stash, mean, rstd, as_stream(stream));
+  return fail(DFX_ERR_DTYPE, "dfx_bdrln_fwd: dtype must be f32 or bf16");
+}
+
+size_t dfx_bdrln_bwd_workspace(int64_t rows, int64_t cols) {
+  return 3 * colsum_ws_bytes(rows, cols);
+}
+
+int dfx_bdrln_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const void* s_stash,
+                  const float* gamma, const uint8_t* keep, float keep_scale, float eps, void* ds,
+                  void* dh, float* dgamma, float* dbeta, float* dbias, void* workspace,
+                  size_t ws_bytes, void* stream) {
+  DFX_REQUIRE(dy && s_stash && gamma, DFX_ERR_SHAPE, "dfx_bdrln_bwd: null required pointer");
+  if (dtype == DFX_BF16)
+    return bdrln_bwd_t<__nv_bfloat16>(rows, cols, dy, s_stash, gamma, keep, keep_scale, eps, ds, dh,
+                                      dgamma, dbeta, dbias, workspace, ws_bytes, as_stream(stream));
+  if (dtype == DFX_F32)
+    return bdrln_bwd_t<float>(rows, cols, dy, s_stash, gamma, keep, keep_scale, eps, ds, dh, dgamma,
+                              dbeta, dbias, workspace, ws_bytes, as_stream(stream));
+  return fail(DFX_ERR_DTYPE, "dfx_bdrln_bwd: dtype must be f32 or bf16");
+}
+
+int dfx_softmax_fwd(int dtype, int64_t batch, int64_t heads, int64_t q, int64_t cols,
+                    const void* scores, float inv_divisor, const float* add_mask,
+                    const uint8_t* keep, float keep_scale, void* p, void* pd, void* stream) {
+  DFX_REQUIRE(scores && (p || pd), DFX_ERR_SHAPE, "dfx_softmax_fwd: null required pointer");
+  if (dtype == DFX_BF16)
+    return softmax_fwd_t<__nv_bfloat16>(batch, heads, q, cols, scores, inv_divisor, add_mask, keep,
+                                        keep_scale, p, pd, as_stream(stream));
+  if (dtype == DFX_F32)
+    return softmax_fwd_t<float>(batch, heads, q, cols, scores, inv_divisor, add_mask, keep,
+                                keep_scale, p, pd, as_stream(stream));
+  return fail(DFX_ERR_DTYPE, "dfx_softmax_fwd: dtype must be f32 or bf16");
+}
+
+int dfx_softmax_bwd(int dtype, int64_t rows, int64_t cols, const void* dpd, const void* p,
+                    const uint8_t* keep, float keep_scale, float inv_divisor, void* dscores,
+                    void* stream) {
+  DFX_REQUIRE(dpd && p && dscores, DFX_ERR_SHAPE, "dfx_softmax_bwd: null required pointer");
+  if (dtype == DFX_BF16)
+    return softmax_bwd_t<__nv_bfloat16>(rows, cols, dpd, p, keep, keep_scale, inv_divisor, dscores,
+                                        as_stream(stream));
+  if (dtype == DFX_F32)
+    return softmax_bwd_t<float>(rows, cols, dpd, p, keep, keep_scale, inv_divisor, dscores,
+                                as_stream(stream));
+  return fail(DFX_ERR_DTYPE, "dfx_softmax_bwd: dtype must be f32 or bf16");
+}
+
+int dfx_bias_gelu_fwd(int dtype, int64_t rows, int64_t cols, const void* f, const float* bias,
+                      void* pre, void* y, void* stream) {
+  DFX_REQUIRE(f && y, DFX_ERR_SHAPE, "dfx_bias_gelu_fwd: null required pointer");
+  const int V = dtype == DFX_BF16 ? 8 : 4;
+  DFX_REQUIRE(cols > 0 && cols % V == 0, DFX_ERR_SHAPE, "dfx_bias_gelu_fwd: cols must be a multiple of the vector width");
+  const int64_t nvec = rows * cols / V;
+  if (nvec == 0) return DFX_OK;
+  const int grid = grid_for(nvec, 256, 148 * 16);
+  cudaStream_t st = as_stream(stream);
+  if (dtype == DFX_BF16)
+    bias_gelu_fwd_kernel<__nv_bfloat16, 8><<<grid, 256, 0, st>>>(nvec, (int)cols, (const __nv_bfloat16*)f, bias, (__nv_bfloat16*)pre, (__nv_bfloat16*)y);
+  else if (dtype == DFX_F32)
+    bias_gelu_fwd_kernel<float, 4><<<grid, 256, 0, st>>>(nvec, (int)cols, (const float*)f, bias, (float*)pre, (float*)y);
+  else
+    return fail(DFX_ERR_DTYPE, "dfx_bias_gelu_fwd: dtype must be f32 or bf16");
+  DFX_LAUNCH_CHECK("dfx_bias_gelu_fwd");
+  return DFX_OK;
+}
+
+int dfx_bias_gelu_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const void* pre,
+                      void* dpre, float* dbias, void* workspace, size_t ws_bytes, void* stream) {
+  DFX_REQUIRE(dy && pre && dpre, DFX_ERR_SHAPE, "dfx_bias_gelu_bwd: null required pointer");
+  const int V = dtype == DFX_BF16 ? 8 : 4;
+  DFX_REQUIRE(cols > 0 && cols % V == 0, DFX_ERR_SHAPE, "dfx_bias_gelu_bwd: cols must be a multiple of the vector width");
+  const int64_t nvec = rows * cols / V;
+  if (nvec == 0) return DFX_OK;
+  const int grid = grid_for(nvec, 256, 148 * 16);
+  cudaStream_t st = as_stream(stream);
+  if (dtype == DFX_BF16)
+    gelu_bwd_kernel<__nv_bfloat16, 8><<<grid, 256, 0, st>>>(nvec, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)pre, (__nv_bfloat16*)dpre);
+  else if (dtype == DFX_F32)
+    gelu_bwd_kernel<float, 4><<<grid, 256, 0, st>>>(nvec, (const float*)dy, (const float*)pre, (float*)dpre);
+  else
+    return fail(DFX_ERR_DTYPE, "dfx_bias_gelu_bwd: dtype must be f32 or bf16");
+  DFX_LAUNCH_CHECK("dfx_bias_gelu_bwd");
+  if (dbias) return dfx_colsum(dtype, rows, cols, dpre, cols, dbias, 0, workspace, ws_bytes, stream);
+  return DFX_OK;
+}
+
+size_t dfx_colsum_workspace(int64_t rows, int64_t cols) { return colsum_ws_bytes(rows, cols); }
+
+int dfx_colsum(int dtype, int64_t rows, int64_t cols, const void* x, int64_t ld, float* out,
+               int accumulate, void* workspace, size_t ws_bytes, void* stream) {
+  DFX_REQUIRE(x && out, DFX_ERR_SHAPE, "dfx_colsum: null pointer");
+  if (dtype == DFX_BF16)
+    return colsum_t<__nv_bfloat16>(rows, cols, x, ld, out, accumulate, workspace, ws_bytes, as_stream(stream));
+  if (dtype == DFX_F32)
+    return colsum_t<float>(rows, cols, x, ld, out, accumulate, workspace, ws_bytes, as_stream(stream));
+  return fail(DFX_ERR_DTYPE, "dfx_colsum: dtype must be f32 or bf16");
+}
+
+int dfx_sgd_update(int64_t n, float* master, const float* grad, float lr, void* weights_bf16,
+                   void* stream) {
+  DFX_REQUIRE(master && grad, DFX_ERR_SHAPE, "dfx_sgd_update: null pointer");
+  if (n == 0) return DFX_OK;
+  sgd_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, as_stream(stream)>>>(n, master, grad, lr, (__nv_bfloat16*)weights_bf16);
+  DFX_LAUNCH_CHECK("dfx_sgd_update");
+  return DFX_OK;
+}
+
+int dfx_scale_f32(int64_t n, float* x, float scale, void* stream) {
+  if (n == 0) return DFX_OK;
+  scale_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, as_stream(stream)>>>(n, x, scale);
+  DFX_LAUNCH_CHECK("dfx_scale_f32");
+  return DFX_OK;
+}
+
+int dfx_cast(int64_t n, int sd, const void* src, int dd, void* dst, void* stream) {
+  if (n == 0) return DFX_OK;
+  cudaStream_t st = as_stream(stream);
+  const int g = grid_for(n, 256, 148 * 8);
+  if (sd == DFX_F32 && dd == DFX_BF16) cast_kernel<float, __nv_bfloat16><<<g, 256, 0, st>>>(n, (const float*)src, (__nv_bfloat16*)dst);
+  else if (sd == DFX_BF16 && dd == DFX_F32) cast_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>(n, (const __nv_bfloat16*)src, (float*)dst);
+  else if (sd == DFX_F32 && dd == DFX_F32) cast_kernel<float, float><<<g, 256, 0, st>>>(n, (const float*)src, (float*)dst);
+  else return fail(DFX_ERR_DTYPE, "dfx_cast: unsupported dtype pair");
+  DFX_LAUNCH_CHECK("dfx_cast");
+  return DFX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,399 @@
+"""Typed wrappers over the C ABI for tensors already resident on the GPU.
+
+PyTorch is used only as the device-memory / stream plumbing: every function
+here hands raw pointers, extents and ``torch.cuda.current_stream()`` to the
+sm_100a library through ``_lib`` (ctypes) and launches nothing itself.
+Shapes and dtypes are validated on the host before launch (dfx.h error
+contract); violations raise ``ShapeError`` like the reference's
+``frontend.infer_shapes`` (frontend.py:132-143).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import GemmArgs
+from .errors import ShapeError
+
+_DT = {torch.float32: _lib.DFX_F32, torch.bfloat16: _lib.DFX_BF16}
+
+
+def dfx_dtype(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise ShapeError(f"dtype {t.dtype} is not supported on the B200 path (f32, bf16)") from None
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _contig(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ShapeError(f"{name}: tensor must be on the GPU")
+    if not t.is_contiguous():
+        raise ShapeError(f"{name}: tensor must be contiguous")
+    return t
+
+
+def _vec(t, n, name):
+    if t is None:
+        return None
+    if t.dtype != torch.float32 or t.numel() != n:
+        raise ShapeError(f"{name}: expected f32 vector of {n} elements")
+    return _contig(t, name)
+
+
+def _u8(t, numel, name):
+    if t is None:
+        return None
+    if t.dtype not in (torch.uint8, torch.bool) or t.numel() != numel:
+        raise ShapeError(f"{name}: expected a u8 keep mask with {numel} elements")
+    return _contig(t, name)
+
+
+class _Workspace:
+    """Grow-only scratch buffer per (device, stream); stream-ordered reuse."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
+        buf = self.bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
+            self.bufs[key] = buf
+        return buf
+
+
+WORKSPACE = _Workspace()
+
+
+# ---------------------------------------------------------------------------
+# optional per-call CUDA-event timing (bench.py roofline accounting)
+
+
+class KernelTimer:
+    """Records a CUDA event pair around every library call made while active,
+    on the stream the call launches on, together with the call's algorithmic
+    work: ``("hbm", bytes)`` for row kernels or ``("tensor"|"simt", flops)``
+    for contractions.
+
+    Works eagerly and under CUDA-graph capture (events are created with
+    ``external=True`` so they become event-record nodes of the graph): call
+    ``collect()`` after each synchronized replay to accumulate durations."""
+
+    def __init__(self):
+        self.records = []
+        self.totals = {}
+
+    def __enter__(self):
+        global _TIMER
+        _TIMER = self
+        return self
+
+    def __exit__(self, *exc):
+        global _TIMER
+        _TIMER = None
+
+    def collect(self):
+        torch.cuda.synchronize()
+        for label, kind, work, e0, e1 in self.records:
+            a = self.totals.setdefault(label, {"label": label, "kind": kind, "calls": 0, "ms": 0.0,
+                                               "work": 0.0})
+            a["calls"] += 1
+            a["ms"] += e0.elapsed_time(e1)
+            a["work"] += work
+
+    def reset_records(self):
+        self.records = []
+
+    def summary(self):
+        if not self.totals:
+            self.collect()
+        return sorted(self.totals.values(), key=lambda r: -r["ms"])
+
+
+_TIMER = None
+
+
+class _Span:
+    __slots__ = ("label", "kind", "work", "e0")
+
+    def __init__(self, label, kind, work):
+        self.label, self.kind, self.work = label, kind, work
+
+    def __enter__(self):
+        self.e0 = torch.cuda.Event(enable_timing=True, external=True)
+        self.e0.record()
+
+    def __exit__(self, *exc):
+        e1 = torch.cuda.Event(enable_timing=True, external=True)
+        e1.record()
+        if _TIMER is not None:
+            _TIMER.records.append((self.label, self.kind, self.work, self.e0, e1))
+
+
+class _Null:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NULL = _Null()
+_LABEL = [None]
+
+
+def _span(default_label, kind, work_fn):
+    if _TIMER is None:
+        return _NULL
+    return _Span(_LABEL[0] or default_label, kind, work_fn())
+
+
+class label:
+    """Context manager naming the calls made inside it (per-call-site rows)."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        self.prev = _LABEL[0]
+        _LABEL[0] = self.name
+
+    def __exit__(self, *exc):
+        _LABEL[0] = self.prev
+
+
+# ---------------------------------------------------------------------------
+# bias + dropout + residual + LayerNorm
+
+
+def bdrln_fwd(h, bias, keep, keep_scale, residual, gamma, beta, eps, y=None, s=None, mean=None,
+              rstd=None):
+    _contig(h, "h")
+    cols = h.shape[-1]
+    rows = h.numel() // cols
+    y = torch.empty_like(h) if y is None else y
+    if residual is not None and (residual.shape != h.shape or residual.dtype != h.dtype):
+        raise ShapeError("bdrln: residual must match h")
+    esz = h.element_size()
+    work = lambda: rows * cols * (esz * (2 + (residual is not None) + (s is not None))  # noqa: E731
+                                  + (keep is not None)) + rows * 8 * (mean is not None) + 3 * cols * 4
+    with _span("bdrln_fwd", "hbm", work):
+        _lib.call("dfx_bdrln_fwd", dfx_dtype(h), rows, cols, h.data_ptr(), _ptr(_vec(bias, cols, "bias")),
+                  _ptr(_u8(keep, h.numel(), "keep")), float(keep_scale),
+                  _ptr(None if residual is None else _contig(residual, "residual")),
+                  _ptr(_vec(gamma, cols, "gamma")), _ptr(_vec(beta, cols, "beta")), float(eps),
+                  _contig(y, "y").data_ptr(), _ptr(s), _ptr(mean), _ptr(rstd), _stream())
+    return y
+
+
+def bdrln_bwd(dy, s, gamma, keep, keep_scale, eps, ds=None, dh=None, dgamma=None, dbeta=None,
+              dbias=None):
+    _contig(dy, "dy")
+    cols = dy.shape[-1]
+    rows = dy.numel() // cols
+    if s.shape != dy.shape or s.dtype != dy.dtype:
+        raise ShapeError("bdrln_bwd: stash must match dy")
+    ws_n = _lib.load().dfx_bdrln_bwd_workspace(rows, cols)
+    ws = WORKSPACE.get(ws_n)
+    esz = dy.element_size()
+    work = lambda: rows * cols * (esz * (2 + (ds is not None) + (dh is not None))  # noqa: E731
+                                  + (keep is not None)) + 4 * cols * 4
+    with _span("bdrln_bwd", "hbm", work):
+        _lib.call("dfx_bdrln_bwd", dfx_dtype(dy), rows, cols, dy.data_ptr(), _contig(s, "s").data_ptr(),
+                  _vec(gamma, cols, "gamma").data_ptr(), _ptr(_u8(keep, dy.numel(), "keep")),
+                  float(keep_scale), float(eps), _ptr(ds), _ptr(dh), _ptr(dgamma), _ptr(dbeta),
+                  _ptr(dbias), ws.data_ptr(), ws.numel(), _stream())
+
+
+# ---------------------------------------------------------------------------
+# scaled + masked softmax + dropout
+
+
+def softmax_fwd(scores, inv_divisor, add_mask, keep, keep_scale, p=None, pd=None):
+    """scores [B, NH, Q, K]; add_mask f32 [B, K] (or None)."""
+    _contig(scores, "scores")
+    if scores.dim() != 4:
+        raise ShapeError("softmax_fwd: scores must be [B, NH, Q, K]")
+    B, NH, Q, K = scores.shape
+    if add_mask is not None:
+        if add_mask.dtype != torch.float32 or add_mask.numel() != B * K:
+            raise ShapeError("softmax_fwd: add_mask must be f32 with B*K elements")
+        _contig(add_mask, "add_mask")
+    n, esz = scores.numel(), scores.element_size()
+    work = lambda: n * (esz * (1 + (p is not None) + (pd is not None)) + (keep is not None)) + B * K * 4  # noqa: E731
+    with _span("softmax_fwd", "hbm", work):
+        _lib.call("dfx_softmax_fwd", dfx_dtype(scores), B, NH, Q, K, scores.data_ptr(), float(inv_divisor),
+                  _ptr(add_mask), _ptr(_u8(keep, scores.numel(), "keep")), float(keep_scale), _ptr(p),
+                  _ptr(pd), _stream())
+    return p, pd
+
+
+def softmax_bwd(dpd, p, keep, keep_scale, inv_divisor, out=None):
+    _contig(dpd, "dpd")
+    _contig(p, "p")
+    K = dpd.shape[-1]
+    out = torch.empty_like(dpd) if out is None else out
+    work = lambda: dpd.numel() * (3 * dpd.element_size() + (keep is not None))  # noqa: E731
+    with _span("softmax_bwd", "hbm", work):
+        _lib.call("dfx_softmax_bwd", dfx_dtype(dpd), dpd.numel() // K, K, dpd.data_ptr(), p.data_ptr(),
+                  _ptr(_u8(keep, dpd.numel(), "keep")), float(keep_scale), float(inv_divisor),
+                  out.data_ptr(), _stream())
+    return out
+
+
+# ---------------------------------------------------------------------------
+# bias + GELU, column sums
+
+
+def bias_gelu_fwd(f, bias, pre=None, y=None):
+    _contig(f, "f")
+    cols = f.shape[-1]
+    y = torch.empty_like(f) if y is None else y
+    work = lambda: f.numel() * f.element_size() * (2 + (pre is not None))  # noqa: E731
+    with _span("bias_gelu_fwd", "hbm", work):
+        _lib.call("dfx_bias_gelu_fwd", dfx_dtype(f), f.numel() // cols, cols, f.data_ptr(),
+                  _ptr(_vec(bias, cols, "bias")), _ptr(pre), y.data_ptr(), _stream())
+    return y
+
+
+def bias_gelu_bwd(dy, pre, dpre=None, dbias=None):
+    _contig(dy, "dy")
+    cols = dy.shape[-1]
+    rows = dy.numel() // cols
+    dpre = torch.empty_like(dy) if dpre is None else dpre
+    ws = WORKSPACE.get(_lib.load().dfx_colsum_workspace(rows, cols))
+    work = lambda: dy.numel() * dy.element_size() * (3 + (dbias is not None))  # noqa: E731
+    with _span("bias_gelu_bwd", "hbm", work):
+        _lib.call("dfx_bias_gelu_bwd", dfx_dtype(dy), rows, cols, dy.data_ptr(), _contig(pre, "pre").data_ptr(),
+                  dpre.data_ptr(), _ptr(dbias), ws.data_ptr(), ws.numel(), _stream())
+    return dpre
+
+
+def colsum(x2d, out, accumulate=False):
+    """out[c] (+)= sum_r x2d[r, c]; x2d may have a row stride."""
+    if x2d.dim() != 2 or x2d.stride(1) != 1:
+        raise ShapeError("colsum: x must be a 2-D row-major view")
+    rows, cols = x2d.shape
+    ws = WORKSPACE.get(_lib.load().dfx_colsum_workspace(rows, cols))
+    with _span("colsum", "hbm", lambda: rows * cols * x2d.element_size() + cols * 4):
+        _lib.call("dfx_colsum", dfx_dtype(x2d), rows, cols, x2d.data_ptr(), x2d.stride(0), out.data_ptr(),
+                  int(accumulate), ws.data_ptr(), ws.numel(), _stream())
+    return out
+
+
+# ---------------------------------------------------------------------------
+# contractions
+
+
+def _bstr(t, nb):
+    """(count1, stride1, count2, stride2) of up to two leading batch dims."""
+    lead = t.shape[:-2]
+    if len(lead) > 2:
+        raise ShapeError("gemm: at most two batch dimensions")
+    shp = list(lead) + [1] * (2 - len(lead))
+    st = list(t.stride()[:-2]) + [0] * (2 - len(lead))
+    return shp[0], st[0], shp[1], st[1]
+
+
+def gemm_args(a, b, d, epilogue=_lib.EPI_NONE, alpha=1.0, beta=1.0, bias=None, aux=None,
+              aux_out=None, force_simt=False) -> GemmArgs:
+    """D[..., m, n] = epi(alpha * A[..., m, k] @ B[..., n, k]^T) on tensor VIEWS.
+
+    Any view works as long as each of A and B has a unit stride along one of
+    its two trailing dims (transposed operands need no copy)."""
+    if a.dim() != b.dim() or a.dim() != d.dim() or a.dim() < 2:
+        raise ShapeError("gemm: A, B, D must have the same rank >= 2")
+    m, k = a.shape[-2:]
+    n, k2 = b.shape[-2:]
+    if k != k2 or tuple(d.shape[-2:]) != (m, n):
+        raise ShapeError(f"gemm: shapes {tuple(a.shape)} x {tuple(b.shape)} -> {tuple(d.shape)}")
+    if a.shape[:-2] != b.shape[:-2] or a.shape[:-2] != d.shape[:-2]:
+        raise ShapeError("gemm: batch dims differ")
+    if d.stride(-1) != 1:
+        raise ShapeError("gemm: D must be contiguous along n")
+    if a.dtype != b.dtype:
+        raise ShapeError("gemm: A and B dtypes differ")
+    g = GemmArgs()
+    g.in_dtype, g.out_dtype, g.epilogue, g.force_simt = dfx_dtype(a), dfx_dtype(d), int(epilogue), int(force_simt)
+    g.m, g.n, g.k = m, n, k
+    b1, sa1, b2, sa2 = _bstr(a, 0)
+    _, sb1, _, sb2 = _bstr(b, 0)
+    _, sd1, _, sd2 = _bstr(d, 0)
+    g.batch1, g.batch2 = b1, b2
+    g.a, g.a_stride_m, g.a_stride_k, g.a_stride_b1, g.a_stride_b2 = a.data_ptr(), a.stride(-2), a.stride(-1), sa1, sa2
+    g.b, g.b_stride_n, g.b_stride_k, g.b_stride_b1, g.b_stride_b2 = b.data_ptr(), b.stride(-2), b.stride(-1), sb1, sb2
+    g.d, g.d_stride_m, g.d_stride_b1, g.d_stride_b2 = d.data_ptr(), d.stride(-2), sd1, sd2
+    g.alpha, g.beta = float(alpha), float(beta)
+    if bias is not None:
+        g.bias = _vec(bias, n, "bias").data_ptr()
+    for name, t in (("aux", aux), ("aux_out", aux_out)):
+        if t is None:
+            continue
+        if tuple(t.shape) != tuple(d.shape) or t.dtype != d.dtype or t.stride(-1) != 1:
+            raise ShapeError(f"gemm: {name} must match D")
+        _, s1, _, s2 = _bstr(t, 0)
+        setattr(g, name, t.data_ptr())
+        setattr(g, name + "_stride_m", t.stride(-2))
+        setattr(g, name + "_stride_b1", s1)
+        setattr(g, name + "_stride_b2", s2)
+    return g
+
+
+def gemm(a, b, d, epilogue=_lib.EPI_NONE, alpha=1.0, beta=1.0, bias=None, aux=None, aux_out=None,
+         force_simt=False):
+    g = gemm_args(a, b, d, epilogue, alpha, beta, bias, aux, aux_out, force_simt)
+    lib = _lib.load()
+    if _TIMER is None:
+        _lib.check(lib.dfx_gemm(g, _stream()), "dfx_gemm")
+        return d
+    kind = "tensor" if lib.dfx_gemm_uses_tensor_cores(g) else "simt"
+    with _span("gemm", kind, lambda: 2.0 * g.m * g.n * g.k * g.batch1 * g.batch2):
+        _lib.check(lib.dfx_gemm(g, _stream()), "dfx_gemm")
+    return d
+
+
+def gemm_uses_tensor_cores(a, b, d, **kw) -> bool:
+    return bool(_lib.load().dfx_gemm_uses_tensor_cores(gemm_args(a, b, d, **kw)))
+
+
+# ---------------------------------------------------------------------------
+# optimizer
+
+
+def sgd_update(master, grad, lr, bf16_copy=None):
+    if master.dtype != torch.float32 or grad.dtype != torch.float32 or master.numel() != grad.numel():
+        raise ShapeError("sgd_update: master and grad must be f32 of equal size")
+    work = lambda: master.numel() * (12 + (2 if bf16_copy is not None else 0))  # noqa: E731
+    with _span("sgd_update", "hbm", work):
+        _lib.call("dfx_sgd_update", master.numel(), master.data_ptr(), grad.data_ptr(), float(lr),
+                  _ptr(bf16_copy), _stream())
+
+
+def scale_(x, s):
+    _lib.call("dfx_scale_f32", x.numel(), x.data_ptr(), float(s), _stream())
+
+
+def cast(src, dst):
+    if src.numel() != dst.numel():
+        raise ShapeError("cast: size mismatch")
+    _lib.call("dfx_cast", src.numel(), dfx_dtype(src), src.data_ptr(), dfx_dtype(dst), dst.data_ptr(), _stream())
+    return dst
+
+
+def launch_count() -> int:
+    return int(_lib.load().dfx_launch_count())
+
+
+def reset_launch_count() -> None:
+    _lib.load().dfx_reset_launch_count()
