@@ -272,7 +272,7 @@ def mbconv_model(N, C, Hh, Ww, SE, stride, eps, momentum, dtype):
     return mb.doc, y, nrm, nrv, ["x", "wdw", "g", "b", "wr", "br", "we", "be"]
 
 
-def golden_mbconv(seed=15, N=2, C=6, Hh=7, Ww=7, SE=2, stride=1, eps=1e-3, momentum=0.99,
+def golden_mbconv(seed=15, N=2, C=8, Hh=7, Ww=7, SE=2, stride=1, eps=1e-3, momentum=0.99,
                   dtype="f64"):
     npdt = np.float64 if dtype == "f64" else np.float32
     rng = np.random.default_rng(seed)
@@ -382,7 +382,12 @@ def golden_known_answers():
     _save("known_answers", **out)
 
 
-def main():
+def main(only=None):
+    if only == "mbconv":
+        for dt in ("f64", "f32"):
+            golden_mbconv(dtype=dt, stride=1)
+        golden_mbconv(dtype="f64", stride=2, Hh=8, Ww=8)
+        return
     golden_known_answers()
     for dt in ("f64", "f32"):
         golden_bdrln(dtype=dt)
@@ -395,4 +400,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1] if len(sys.argv) > 1 else None)

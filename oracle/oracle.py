@@ -86,6 +86,22 @@ def compare(got, want) -> float:
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0)))
 
 
+def compare_scaled(got, want) -> float:
+    """max|a-b| / max(max|b|, 1): the compare metric normalised by the
+    tensor's scale instead of per element.  Used for bf16 *reduction* outputs
+    (parameter gradients = sums over T rows), whose near-zero elements are
+    dominated by bf16 rounding-boundary flips: perturbing the oracle's own
+    bf16 storage model by 1e-6 relative moves them by several percent
+    element-wise but by <1e-2 on this metric (tests/test_oracle_golden.py::
+    test_bf16_flip_sensitivity)."""
+    a, b = _a(got), _a(want)
+    if a.shape != b.shape:
+        raise ValueError(f"shape mismatch {a.shape} vs {b.shape}")
+    if a.size == 0:
+        return 0.0
+    return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1.0))
+
+
 # ---------------------------------------------------------------------------
 # a1-a3: bias + dropout + residual + LayerNorm
 
@@ -402,27 +418,37 @@ def swish_grad(x):
 MBCONV_WEIGHTS = ("wdw", "g", "b", "rm", "rv", "wr", "br", "we", "be")
 
 
-def mbconv_fwd(prm, x, stride=1, eps=1e-3, momentum=0.99):
-    """dw3x3 + BN(train) + swish + squeeze-excite (SURVEY.md:512-514)."""
+def mbconv_fwd(prm, x, stride=1, eps=1e-3, momentum=0.99, rnd=None, pads=(1, 1, 1, 1)):
+    """dw3x3 + BN(train) + swish + squeeze-excite (SURVEY.md:512-514).
+
+    ``rnd`` is the storage model (see bert_layer_fwd): applied to z, the only
+    full-size intermediate the B200 path stores; BN statistics come from the
+    unrounded z, as on the GPU."""
+    R = rnd or _ident
     P = {k: _a(v) for k, v in prm.items()}
     x = _a(x)
     n, c = x.shape[:2]
-    z = dwconv(x, P["wdw"], stride, (1, 1, 1, 1))
-    u, new_rm, new_rv, mu, var = batchnorm_train(z, P["g"], P["b"], P["rm"], P["rv"], eps, momentum)
+    z_exact = dwconv(x, P["wdw"], stride, pads)
+    _, new_rm, new_rv, mu, var = batchnorm_train(z_exact, P["g"], P["b"], P["rm"], P["rv"], eps, momentum)
+    z = R(z_exact)
+    shp = (1, -1, 1, 1)
+    u = (z - mu.reshape(shp)) / np.sqrt(var.reshape(shp) + eps) * P["g"].reshape(shp) + P["b"].reshape(shp)
     a = swish(u)
     pooled = a.mean(axis=(2, 3))
     r = gemm(pooled, P["wr"], P["br"], trans_b=True)
     r2 = swish(r)
     e = gemm(r2, P["we"], P["be"], trans_b=True)
     s = sigmoid(e)
-    y = a * s.reshape(n, c, 1, 1)
-    cache = dict(x=x, z=z, u=u, a=a, pooled=pooled, r=r, r2=r2, e=e, s=s, stride=stride, eps=eps)
+    y = R(a * s.reshape(n, c, 1, 1))
+    cache = dict(x=x, z=z, u=u, a=a, pooled=pooled, r=r, r2=r2, e=e, s=s, stride=stride, eps=eps,
+                 mu=mu, var=var, rnd=R, pads=pads)
     return y, new_rm, new_rv, cache
 
 
 def mbconv_bwd(prm, cache, dy):
     P = {k: _a(v) for k, v in prm.items()}
     c = cache
+    R = c.get("rnd") or _ident
     dy = _a(dy)
     n, ch, oh, ow = dy.shape
     gr = {}
@@ -438,8 +464,17 @@ def mbconv_bwd(prm, cache, dy):
     dpooled = dr @ P["wr"]
     da = dy * s4 + dpooled.reshape(n, ch, 1, 1) / (oh * ow)
     du = da * swish_grad(c["u"])
-    dz, gr["g"], gr["b"] = batchnorm_train_bwd(du, c["z"], P["g"], c["eps"])
-    gr["x"], gr["wdw"] = dwconv_bwd(dz, c["x"], P["wdw"], c["stride"], (1, 1, 1, 1))
+    # BN VJP (autodiff.py:1557-1617) with the forward batch statistics
+    shp = (1, -1, 1, 1)
+    rstd = 1.0 / np.sqrt(c["var"] + c["eps"])
+    xhat = (c["z"] - c["mu"].reshape(shp)) * rstd.reshape(shp)
+    m1 = du.mean(axis=(0, 2, 3), keepdims=True)
+    m2 = (du * xhat).mean(axis=(0, 2, 3), keepdims=True)
+    dz = P["g"].reshape(shp) * rstd.reshape(shp) * (du - m1 - xhat * m2)
+    gr["g"] = (du * xhat).sum(axis=(0, 2, 3))
+    gr["b"] = du.sum(axis=(0, 2, 3))
+    dx, gr["wdw"] = dwconv_bwd(dz, c["x"], P["wdw"], c["stride"], c.get("pads", (1, 1, 1, 1)))
+    gr["x"] = R(dx)
     return gr
 
 

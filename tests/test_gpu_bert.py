@@ -93,8 +93,11 @@ def test_bert_c1_shape(dtype, tol):
         _, want_g = _oracle(prm, x, am, keeps, dout, B, S, NH, rnd=_bf16_store)
         errs["x_storage_model"] = O.compare(dx, want_g["x"])
     grads = layer.grads_numpy()
+    # f32: element-wise metric.  bf16: parameter gradients are sums over T
+    # rows and are judged scale-normalised (oracle.compare_scaled docstring)
+    metric = O.compare if dtype == torch.float32 else O.compare_scaled
     for k in O.BERT_WEIGHTS:
-        errs[k] = O.compare(grads[k], want_g[k])
+        errs[k] = metric(grads[k], want_g[k])
     print({k: f"{v:.2e}" for k, v in errs.items()})
     bad = {k: v for k, v in errs.items() if v > tol}
     assert not bad, f"over tolerance {tol}: {bad} (all: {errs})"

@@ -161,3 +161,36 @@ def test_finite_difference_bert_small():
                 return float((O.bert_layer_fwd(p2, x2, *args)[0] * dy).sum())
             fd = (loss(h) - loss(-h)) / (2 * h)
             assert abs(fd - grads[name].flat[idx]) <= 1e-5 * max(1.0, abs(fd))
+
+
+def test_bf16_flip_sensitivity():
+    """Why bf16 parameter gradients are judged with compare_scaled: the f64
+    oracle with the bf16 storage model, perturbed by 1e-6 relative before each
+    rounding (i.e. fp32-vs-f64 arithmetic), already differs from itself by
+    several percent element-wise on row-reduced gradients, but by well under
+    2e-2 on the scale-normalised metric."""
+    B, S, H, NH, FF = 2, 32, 128, 4, 256
+    rng = np.random.default_rng(5)
+    T = B * S
+    r = lambda a: O.round_bf16(a).astype(np.float64)  # noqa: E731
+    x, dout = r(rng.standard_normal((T, H))), r(rng.standard_normal((T, H)))
+    am = np.zeros((B, 1, 1, S))
+    dm, m1, m2 = (O.mask_values(rng.random(s) >= 0.1, 0.1, np.float64)
+                  for s in ((B, NH, S, S), (T, H), (T, H)))
+    prm = {}
+    for nm, shp in [("wq", (H, H)), ("wk", (H, H)), ("wv", (H, H)), ("wo", (H, H)), ("w1", (FF, H)),
+                    ("w2", (H, FF))]:
+        prm[nm] = r(0.02 * rng.standard_normal(shp))
+    for nm, n in [("bq", H), ("bk", H), ("bv", H), ("bo", H), ("b1", FF), ("b2", H)]:
+        prm[nm] = 0.1 * rng.standard_normal(n)
+    for i in "12":
+        prm["g" + i], prm["be" + i] = 1 + 0.1 * rng.standard_normal(H), 0.1 * rng.standard_normal(H)
+    nr = np.random.default_rng(1)
+    r2 = lambda a: O.round_bf16(a * (1 + 1e-6 * nr.standard_normal(np.shape(a)))).astype(np.float64)  # noqa: E731
+    o1, c1 = O.bert_layer_fwd(prm, x, am, dm, m1, m2, B, S, NH, 1e-12, rnd=r)
+    o2, c2 = O.bert_layer_fwd(prm, x, am, dm, m1, m2, B, S, NH, 1e-12, rnd=r2)
+    g1, g2 = O.bert_layer_bwd(prm, c1, dout), O.bert_layer_bwd(prm, c2, dout)
+    elem = max(O.compare(g2[k], g1[k]) for k in O.BERT_WEIGHTS)
+    scaled = max(O.compare_scaled(g2[k], g1[k]) for k in O.BERT_WEIGHTS)
+    assert scaled < 1e-2
+    assert elem > scaled  # the element-wise metric over-reacts to flips
