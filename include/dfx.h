@@ -213,6 +213,39 @@ int dfx_mbconv_bwd_dx(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
                       double count, void* dx, float* dw_dw, void* workspace, size_t ws_bytes,
                       void* stream);
 
+/* ---- C4: normalisation sweep (LayerNorm vs BatchNorm fused with an activation)
+ * act: 0 = none, 1 = swish (Mul(u, Sigmoid(u)), frontend.py:229, 293).
+ * LayerNorm over the last axis (frontend.py:519-529; VJP autodiff.py:1490-1545):
+ * rows x cols, y = act(LN(x)); the backward recomputes the statistics from x.
+ * Workspace: dfx_bdrln_bwd_workspace(rows, cols). */
+int dfx_layernorm_act_fwd(int dtype, int64_t rows, int64_t cols, const void* x, const float* gamma,
+                          const float* beta, float eps, int act, void* y, void* stream);
+int dfx_layernorm_act_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const void* x,
+                          const float* gamma, const float* beta, float eps, int act, void* dx,
+                          float* dgamma, float* dbeta, void* workspace, size_t ws_bytes,
+                          void* stream);
+/* BatchNorm over the channel axis, channels-last [rows, C] (rows = N x spatial),
+ * training mode (frontend.py:544-591; VJP autodiff.py:1557-1617).
+ *   stats: local[3][C] = (count, mean, M2) — finalize with dfx_bn_finalize
+ *          (nsets = #ranks for SyncBN)
+ *   apply: y = act((x - mean) * rstd * gamma + beta)
+ *   bwd_reduce: bnsum[2][C] = (sum du, sum du*xhat) = (dbeta, dgamma)
+ *   bwd_dx: dx = gamma*rstd*(du - bnsum[0]/count - xhat*bnsum[1]/count) */
+size_t dfx_batchnorm_workspace(int64_t rows, int64_t C);
+int dfx_batchnorm_stats(int dtype, int64_t rows, int64_t C, const void* x, float* local,
+                        void* workspace, size_t ws_bytes, void* stream);
+int dfx_batchnorm_act_apply(int dtype, int64_t rows, int64_t C, const void* x, const float* mean,
+                            const float* rstd, const float* gamma, const float* beta, int act,
+                            void* y, void* stream);
+int dfx_batchnorm_act_bwd_reduce(int dtype, int64_t rows, int64_t C, const void* dy, const void* x,
+                                 const float* mean, const float* rstd, const float* gamma,
+                                 const float* beta, int act, float* bnsum, void* workspace,
+                                 size_t ws_bytes, void* stream);
+int dfx_batchnorm_act_bwd_dx(int dtype, int64_t rows, int64_t C, const void* dy, const void* x,
+                             const float* mean, const float* rstd, const float* gamma,
+                             const float* beta, int act, const float* bnsum, double count, void* dx,
+                             void* stream);
+
 /* ---- optimizer (the user-written SGD step of the training loop) --
  * master -= lr * grad (f32); if weights_bf16 != NULL also refresh the bf16 copy. */
 int dfx_sgd_update(int64_t n, float* master, const float* grad, float lr, void* weights_bf16,

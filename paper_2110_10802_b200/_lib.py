@@ -89,6 +89,22 @@ _SIGS = [
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, ctypes.c_double,
                                   c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("dfx_layernorm_act_fwd", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_float,
+                                      c_int, c_void_p, c_void_p]),
+    ("dfx_layernorm_act_bwd", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_float, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                                      c_void_p]),
+    ("dfx_batchnorm_workspace", c_size_t, [c_int64, c_int64]),
+    ("dfx_batchnorm_stats", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_size_t,
+                                    c_void_p]),
+    ("dfx_batchnorm_act_apply", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_int, c_void_p, c_void_p]),
+    ("dfx_batchnorm_act_bwd_reduce", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                             c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+                                             c_size_t, c_void_p]),
+    ("dfx_batchnorm_act_bwd_dx", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_int, c_void_p, ctypes.c_double, c_void_p,
+                                         c_void_p]),
     ("dfx_sgd_update", c_int, [c_int64, c_void_p, c_void_p, c_float, c_void_p, c_void_p]),
     ("dfx_scale_f32", c_int, [c_int64, c_void_p, c_float, c_void_p]),
     ("dfx_cast", c_int, [c_int64, c_int, c_void_p, c_int, c_void_p, c_void_p]),

@@ -149,6 +149,8 @@ __device__ __forceinline__ void load_keep(const uint8_t* p, float scale, float (
   }
 }
 
+__device__ __forceinline__ float sigmoid_f(float u) { return 1.f / (1.f + __expf(-u)); }
+
 __device__ __forceinline__ float gelu_f(float x) {
   const float c0 = 0.044715f, c1 = 0.7978845608028654f;
   float u = c1 * (x + c0 * x * x * x);

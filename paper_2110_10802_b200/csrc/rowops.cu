@@ -31,7 +31,7 @@ template <> struct VecWidth<float> { static constexpr int value = 4; };
 // ---------------------------------------------------------------------------
 // bias + dropout + residual + LayerNorm
 
-template <typename T, int V, int NCH>
+template <typename T, int V, int NCH, int ACT = 0>
 __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
     int64_t rows, int cols, const T* __restrict__ h, const float* __restrict__ bias,
     const uint8_t* __restrict__ keep, float ks, const T* __restrict__ res,
@@ -110,7 +110,10 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
       }
       Vec<T, V> yv;
 #pragma unroll
-      for (int i = 0; i < V; ++i) yv.v[i] = (x[c][i] - mu) * rstd * g.v[i] + bt.v[i];
+      for (int i = 0; i < V; ++i) {
+        const float u = (x[c][i] - mu) * rstd * g.v[i] + bt.v[i];
+        yv.v[i] = ACT ? u * sigmoid_f(u) : u;
+      }
       yv.store(y + base + col);
     }
   }
@@ -145,10 +148,11 @@ __device__ __forceinline__ void block_colsum_store(float (&acc)[NCH][V], int col
   __syncthreads();
 }
 
-template <typename T, int V, int NCH>
+template <typename T, int V, int NCH, int ACT = 0>
 __global__ void __launch_bounds__(256) bdrln_bwd_kernel(
     int64_t rows, int cols, const T* __restrict__ dy, const T* __restrict__ s,
-    const float* __restrict__ gamma, const uint8_t* __restrict__ keep, float ks, float eps,
+    const float* __restrict__ gamma, const float* __restrict__ beta,
+    const uint8_t* __restrict__ keep, float ks, float eps,
     T* __restrict__ ds_out, T* __restrict__ dh_out, float* __restrict__ part_g,
     float* __restrict__ part_b, float* __restrict__ part_h) {
   extern __shared__ float red[];
@@ -156,16 +160,21 @@ __global__ void __launch_bounds__(256) bdrln_bwd_kernel(
   const int nvec = cols / V;
   const float inv_n = 1.f / (float)cols;
   float acc_g[NCH][V], acc_b[NCH][V], acc_h[NCH][V];
-  float gam[NCH][V];
+  float gam[NCH][V], bet[NCH][V];
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int vi = lane + c * 32;
 #pragma unroll
-    for (int i = 0; i < V; ++i) { acc_g[c][i] = 0.f; acc_b[c][i] = 0.f; acc_h[c][i] = 0.f; gam[c][i] = 0.f; }
+    for (int i = 0; i < V; ++i) { acc_g[c][i] = 0.f; acc_b[c][i] = 0.f; acc_h[c][i] = 0.f; gam[c][i] = 0.f; bet[c][i] = 0.f; }
     if (vi < nvec) {
       Vec<float, V> g; g.load(gamma + vi * V);
 #pragma unroll
       for (int i = 0; i < V; ++i) gam[c][i] = g.v[i];
+      if (ACT) {
+        Vec<float, V> b; b.load(beta + vi * V);
+#pragma unroll
+        for (int i = 0; i < V; ++i) bet[c][i] = b.v[i];
+      }
     }
   }
   for (int64_t row = (int64_t)blockIdx.x * kWarps + warp; row < rows;
@@ -202,6 +211,11 @@ __global__ void __launch_bounds__(256) bdrln_bwd_kernel(
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         x[c][i] = (x[c][i] - mu) * rstd;  // xhat (0 on padding lanes: gamma=0, dy=0)
+        if (ACT) {  // dy w.r.t. the LN output through swish
+          const float u = x[c][i] * gam[c][i] + bet[c][i];
+          const float sg = sigmoid_f(u);
+          g[c][i] *= sg + u * sg * (1.f - sg);
+        }
         const float dyg = g[c][i] * gam[c][i];
         m1 += dyg;
         m2 += dyg * x[c][i];
@@ -516,8 +530,7 @@ inline int pick_nch(int nvec) {
   return -1;
 }
 
-template <typename T> int check_row_shape(int64_t cols, const char* op) {
-  constexpr int V = VecWidth<T>::value;
+template <typename T, int V> int check_row_shape(int64_t cols, const char* op) {
   if (cols <= 0 || cols % V != 0)
     return fail(DFX_ERR_SHAPE, std::string(op) + ": cols must be a positive multiple of " + std::to_string(V));
   if (pick_nch((int)(cols / V)) < 0)
@@ -530,32 +543,54 @@ size_t colsum_ws_bytes(int64_t rows, int64_t cols) {
   return (size_t)kMaxColBlocks * (size_t)cols * sizeof(float);
 }
 
-template <typename T>
+template <typename T, int V>
 int bdrln_fwd_t(int64_t rows, int64_t cols, const void* h, const float* bias, const uint8_t* keep,
                 float ks, const void* res, const float* gamma, const float* beta, float eps, void* y,
-                void* s_out, float* mean, float* rstd, cudaStream_t st) {
-  constexpr int V = VecWidth<T>::value;
-  if (int rc = check_row_shape<T>(cols, "dfx_bdrln_fwd")) return rc;
+                void* s_out, float* mean, float* rstd, cudaStream_t st, int act = 0) {
+  if (int rc = check_row_shape<T, V>(cols, "dfx_bdrln_fwd")) return rc;
   const int nch = pick_nch((int)(cols / V));
   const int grid = (int)((rows + kWarps - 1) / kWarps);
   if (rows == 0) return DFX_OK;
-#define L(N)                                                                                  \
-  if (nch == N)                                                                               \
-    bdrln_fwd_kernel<T, V, N><<<grid, 256, 0, st>>>(rows, (int)cols, (const T*)h, bias, keep, ks, \
-                                                    (const T*)res, gamma, beta, eps, (T*)y,   \
-                                                    (T*)s_out, mean, rstd);
+#define L(N)                                                                                        \
+  if (nch == N) {                                                                                   \
+    if (act)                                                                                        \
+      bdrln_fwd_kernel<T, V, N, 1><<<grid, 256, 0, st>>>(rows, (int)cols, (const T*)h, bias, keep, ks, \
+                                                         (const T*)res, gamma, beta, eps, (T*)y,    \
+                                                         (T*)s_out, mean, rstd);                   \
+    else                                                                                            \
+      bdrln_fwd_kernel<T, V, N, 0><<<grid, 256, 0, st>>>(rows, (int)cols, (const T*)h, bias, keep, ks, \
+                                                         (const T*)res, gamma, beta, eps, (T*)y,    \
+                                                         (T*)s_out, mean, rstd);                   \
+  }
   DFX_NCH_LIST(L)
 #undef L
   DFX_LAUNCH_CHECK("dfx_bdrln_fwd");
   return DFX_OK;
 }
 
-template <typename T>
+template <typename T, int V, int ACT>
+int bdrln_bwd_launch(int nch, int grid, size_t smem, int64_t rows, int64_t cols, const void* dy, const void* s,
+                     const float* gamma, const float* beta, const uint8_t* keep, float ks, float eps, void* ds,
+                     void* dh, float* pg, float* pb, float* ph, cudaStream_t st) {
+#define L(N)                                                                                       \
+  if (nch == N) {                                                                                  \
+    auto kfn = bdrln_bwd_kernel<T, V, N, ACT>;                                                     \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    kfn<<<grid, 256, smem, st>>>(rows, (int)cols, (const T*)dy, (const T*)s, gamma, beta, keep, ks, eps, \
+                                 (T*)ds, (T*)dh, pg, pb, ph);                                      \
+  }
+  DFX_NCH_LIST(L)
+#undef L
+  DFX_LAUNCH_CHECK("dfx_bdrln_bwd");
+  return DFX_OK;
+}
+
+template <typename T, int V>
 int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const float* gamma,
                 const uint8_t* keep, float ks, float eps, void* ds, void* dh, float* dgamma,
-                float* dbeta, float* dbias, void* ws, size_t ws_bytes, cudaStream_t st) {
-  constexpr int V = VecWidth<T>::value;
-  if (int rc = check_row_shape<T>(cols, "dfx_bdrln_bwd")) return rc;
+                float* dbeta, float* dbias, void* ws, size_t ws_bytes, cudaStream_t st, int act = 0,
+                const float* beta = nullptr) {
+  if (int rc = check_row_shape<T, V>(cols, "dfx_bdrln_bwd")) return rc;
   if (rows == 0) return DFX_OK;
   const int nch = pick_nch((int)(cols / V));
   const int grid = grid_for(rows, kWarps, kMaxColBlocks);
@@ -565,16 +600,11 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
   float* pb = pg + (size_t)grid * cols;
   float* ph = pb + (size_t)grid * cols;
   const size_t smem = (size_t)kWarps * cols * sizeof(float);
-#define L(N)                                                                                       \
-  if (nch == N) {                                                                                  \
-    auto kfn = bdrln_bwd_kernel<T, V, N>;                                                          \
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    kfn<<<grid, 256, smem, st>>>(rows, (int)cols, (const T*)dy, (const T*)s, gamma, keep, ks, eps, \
-                                 (T*)ds, (T*)dh, pg, pb, ph);                                      \
-  }
-  DFX_NCH_LIST(L)
-#undef L
-  DFX_LAUNCH_CHECK("dfx_bdrln_bwd");
+  int rc = act ? bdrln_bwd_launch<T, V, 1>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, ks, eps, ds, dh,
+                                        pg, pb, ph, st)
+               : bdrln_bwd_launch<T, V, 0>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, ks, eps, ds, dh,
+                                        pg, pb, ph, st);
+  if (rc) return rc;
   if (dgamma || dbeta || dbias) {
     finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 3), 256, 0, st>>>(grid, (int)cols, pg, dgamma,
                                                                                dbeta, dbias, 0);
@@ -583,11 +613,10 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
   return DFX_OK;
 }
 
-template <typename T>
+template <typename T, int V>
 int softmax_fwd_t(int64_t batch, int64_t heads, int64_t q, int64_t cols, const void* x, float inv_div,
                   const float* am, const uint8_t* keep, float ks, void* p, void* pd, cudaStream_t st) {
-  constexpr int V = VecWidth<T>::value;
-  if (int rc = check_row_shape<T>(cols, "dfx_softmax_fwd")) return rc;
+  if (int rc = check_row_shape<T, V>(cols, "dfx_softmax_fwd")) return rc;
   const int64_t rows = batch * heads * q;
   if (rows == 0) return DFX_OK;
   const int nch = pick_nch((int)(cols / V));
@@ -603,11 +632,10 @@ int softmax_fwd_t(int64_t batch, int64_t heads, int64_t q, int64_t cols, const v
   return DFX_OK;
 }
 
-template <typename T>
+template <typename T, int V>
 int softmax_bwd_t(int64_t rows, int64_t cols, const void* dpd, const void* p, const uint8_t* keep,
                   float ks, float inv_div, void* dx, cudaStream_t st) {
-  constexpr int V = VecWidth<T>::value;
-  if (int rc = check_row_shape<T>(cols, "dfx_softmax_bwd")) return rc;
+  if (int rc = check_row_shape<T, V>(cols, "dfx_softmax_bwd")) return rc;
   if (rows == 0) return DFX_OK;
   const int nch = pick_nch((int)(cols / V));
   const int64_t grid = (rows + kWarps - 1) / kWarps;
@@ -621,6 +649,18 @@ int softmax_bwd_t(int64_t rows, int64_t cols, const void* dpd, const void* p, co
   DFX_LAUNCH_CHECK("dfx_softmax_bwd");
   return DFX_OK;
 }
+
+// Width dispatch: 128-bit vectors when cols is a multiple of the vector width,
+// scalar lanes otherwise (the reference accepts any extent).
+#define DFX_VDISPATCH(FN)                                                              \
+  template <typename T, typename... A> int FN##_any(int64_t cols, A... a) {             \
+    if (cols % VecWidth<T>::value == 0) return FN<T, VecWidth<T>::value>(a...);        \
+    return FN<T, 1>(a...);                                                              \
+  }
+DFX_VDISPATCH(bdrln_fwd_t)
+DFX_VDISPATCH(bdrln_bwd_t)
+DFX_VDISPATCH(softmax_fwd_t)
+DFX_VDISPATCH(softmax_bwd_t)
 
 template <typename T>
 int colsum_t(int64_t rows, int64_t cols, const void* x, int64_t ld, float* out, int accumulate,
@@ -654,10 +694,10 @@ int dfx_bdrln_fwd(int dtype, int64_t rows, int64_t cols, const void* h, const fl
                   void* stream) {
   DFX_REQUIRE(h && gamma && beta && y, DFX_ERR_SHAPE, "dfx_bdrln_fwd: null required pointer");
   if (dtype == DFX_BF16)
-    return bdrln_fwd_t<__nv_bfloat16>(rows, cols, h, bias, keep, keep_scale, residual, gamma, beta,
+    return bdrln_fwd_t_any<__nv_bfloat16>(cols, rows, cols, h, bias, keep, keep_scale, residual, gamma, beta,
                                       eps, y, s_stash, mean, rstd, as_stream(stream));
   if (dtype == DFX_F32)
-    return bdrln_fwd_t<float>(rows, cols, h, bias, keep, keep_scale, residual, gamma, beta, eps, y,
+    return bdrln_fwd_t_any<float>(cols, rows, cols, h, bias, keep, keep_scale, residual, gamma, beta, eps, y,
                               s_stash, mean, rstd, as_stream(stream));
   return fail(DFX_ERR_DTYPE, "dfx_bdrln_fwd: dtype must be f32 or bf16");
 }
@@ -672,10 +712,10 @@ int dfx_bdrln_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const v
                   size_t ws_bytes, void* stream) {
   DFX_REQUIRE(dy && s_stash && gamma, DFX_ERR_SHAPE, "dfx_bdrln_bwd: null required pointer");
   if (dtype == DFX_BF16)
-    return bdrln_bwd_t<__nv_bfloat16>(rows, cols, dy, s_stash, gamma, keep, keep_scale, eps, ds, dh,
+    return bdrln_bwd_t_any<__nv_bfloat16>(cols, rows, cols, dy, s_stash, gamma, keep, keep_scale, eps, ds, dh,
                                       dgamma, dbeta, dbias, workspace, ws_bytes, as_stream(stream));
   if (dtype == DFX_F32)
-    return bdrln_bwd_t<float>(rows, cols, dy, s_stash, gamma, keep, keep_scale, eps, ds, dh, dgamma,
+    return bdrln_bwd_t_any<float>(cols, rows, cols, dy, s_stash, gamma, keep, keep_scale, eps, ds, dh, dgamma,
                               dbeta, dbias, workspace, ws_bytes, as_stream(stream));
   return fail(DFX_ERR_DTYPE, "dfx_bdrln_bwd: dtype must be f32 or bf16");
 }
@@ -685,10 +725,10 @@ int dfx_softmax_fwd(int dtype, int64_t batch, int64_t heads, int64_t q, int64_t 
                     const uint8_t* keep, float keep_scale, void* p, void* pd, void* stream) {
   DFX_REQUIRE(scores && (p || pd), DFX_ERR_SHAPE, "dfx_softmax_fwd: null required pointer");
   if (dtype == DFX_BF16)
-    return softmax_fwd_t<__nv_bfloat16>(batch, heads, q, cols, scores, inv_divisor, add_mask, keep,
+    return softmax_fwd_t_any<__nv_bfloat16>(cols, batch, heads, q, cols, scores, inv_divisor, add_mask, keep,
                                         keep_scale, p, pd, as_stream(stream));
   if (dtype == DFX_F32)
-    return softmax_fwd_t<float>(batch, heads, q, cols, scores, inv_divisor, add_mask, keep,
+    return softmax_fwd_t_any<float>(cols, batch, heads, q, cols, scores, inv_divisor, add_mask, keep,
                                 keep_scale, p, pd, as_stream(stream));
   return fail(DFX_ERR_DTYPE, "dfx_softmax_fwd: dtype must be f32 or bf16");
 }
@@ -698,10 +738,10 @@ int dfx_softmax_bwd(int dtype, int64_t rows, int64_t cols, const void* dpd, cons
                     void* stream) {
   DFX_REQUIRE(dpd && p && dscores, DFX_ERR_SHAPE, "dfx_softmax_bwd: null required pointer");
   if (dtype == DFX_BF16)
-    return softmax_bwd_t<__nv_bfloat16>(rows, cols, dpd, p, keep, keep_scale, inv_divisor, dscores,
+    return softmax_bwd_t_any<__nv_bfloat16>(cols, rows, cols, dpd, p, keep, keep_scale, inv_divisor, dscores,
                                         as_stream(stream));
   if (dtype == DFX_F32)
-    return softmax_bwd_t<float>(rows, cols, dpd, p, keep, keep_scale, inv_divisor, dscores,
+    return softmax_bwd_t_any<float>(cols, rows, cols, dpd, p, keep, keep_scale, inv_divisor, dscores,
                                 as_stream(stream));
   return fail(DFX_ERR_DTYPE, "dfx_softmax_bwd: dtype must be f32 or bf16");
 }
@@ -755,6 +795,33 @@ int dfx_colsum(int dtype, int64_t rows, int64_t cols, const void* x, int64_t ld,
   if (dtype == DFX_F32)
     return colsum_t<float>(rows, cols, x, ld, out, accumulate, workspace, ws_bytes, as_stream(stream));
   return fail(DFX_ERR_DTYPE, "dfx_colsum: dtype must be f32 or bf16");
+}
+
+int dfx_layernorm_act_fwd(int dtype, int64_t rows, int64_t cols, const void* x, const float* gamma,
+                          const float* beta, float eps, int act, void* y, void* stream) {
+  DFX_REQUIRE(x && gamma && beta && y, DFX_ERR_SHAPE, "dfx_layernorm_act_fwd: null pointer");
+  DFX_REQUIRE(act == 0 || act == 1, DFX_ERR_UNSUPPORTED, "dfx_layernorm_act_fwd: act must be 0 (none) or 1 (swish)");
+  if (dtype == DFX_BF16)
+    return bdrln_fwd_t_any<__nv_bfloat16>(cols, rows, cols, x, nullptr, nullptr, 1.f, nullptr, gamma, beta, eps, y, nullptr,
+                                      nullptr, nullptr, as_stream(stream), act);
+  if (dtype == DFX_F32)
+    return bdrln_fwd_t_any<float>(cols, rows, cols, x, nullptr, nullptr, 1.f, nullptr, gamma, beta, eps, y, nullptr, nullptr,
+                              nullptr, as_stream(stream), act);
+  return fail(DFX_ERR_DTYPE, "dfx_layernorm_act_fwd: dtype must be f32 or bf16");
+}
+
+int dfx_layernorm_act_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const void* x,
+                          const float* gamma, const float* beta, float eps, int act, void* dx, float* dgamma,
+                          float* dbeta, void* workspace, size_t ws_bytes, void* stream) {
+  DFX_REQUIRE(dy && x && gamma && beta && dx, DFX_ERR_SHAPE, "dfx_layernorm_act_bwd: null pointer");
+  DFX_REQUIRE(act == 0 || act == 1, DFX_ERR_UNSUPPORTED, "dfx_layernorm_act_bwd: act must be 0 (none) or 1 (swish)");
+  if (dtype == DFX_BF16)
+    return bdrln_bwd_t_any<__nv_bfloat16>(cols, rows, cols, dy, x, gamma, nullptr, 1.f, eps, dx, nullptr, dgamma, dbeta, nullptr,
+                                      workspace, ws_bytes, as_stream(stream), act, beta);
+  if (dtype == DFX_F32)
+    return bdrln_bwd_t_any<float>(cols, rows, cols, dy, x, gamma, nullptr, 1.f, eps, dx, nullptr, dgamma, dbeta, nullptr,
+                              workspace, ws_bytes, as_stream(stream), act, beta);
+  return fail(DFX_ERR_DTYPE, "dfx_layernorm_act_bwd: dtype must be f32 or bf16");
 }
 
 int dfx_sgd_update(int64_t n, float* master, const float* grad, float lr, void* weights_bf16,

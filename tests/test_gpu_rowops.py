@@ -191,10 +191,30 @@ def test_colsum_strided():
 
 
 def test_errors_raise():
+    """Host-side validation mirrors the reference's ShapeError behaviour."""
     from paper_2110_10802_b200.errors import ShapeError
 
     k = K()
-    x = torch.zeros(4, 7, device="cuda")  # 7 not a multiple of the f32 vector width
-    g = torch.ones(7, device="cuda")
+    x = torch.zeros(4, 1001, device="cuda")  # odd width beyond the scalar-lane limit
+    g = torch.ones(1001, device="cuda")
     with pytest.raises(ShapeError):
         k.bdrln_fwd(x, None, None, 1.0, None, g, g, 1e-5)
+    with pytest.raises(ShapeError):  # f64 is not a B200 activation dtype
+        k.bdrln_fwd(x.double(), None, None, 1.0, None, g, g, 1e-5)
+    a = torch.zeros(64, 32, device="cuda")
+    with pytest.raises(ShapeError):  # contracted dims differ
+        k.gemm(a, torch.zeros(16, 48, device="cuda"), torch.zeros(64, 16, device="cuda"))
+
+
+def test_odd_widths_scalar_lanes():
+    """Widths that are not a multiple of the vector width take scalar lanes
+    (the reference accepts any extent)."""
+    k = K()
+    rng = np.random.default_rng(1)
+    for cols in (5, 7, 33, 500):
+        x = rng.standard_normal((9, cols))
+        g, b = 1 + 0.1 * rng.standard_normal(cols), 0.1 * rng.standard_normal(cols)
+        y = k.bdrln_fwd(dev(x, torch.float32), None, None, 1.0, None, dev(g, torch.float32),
+                        dev(b, torch.float32), 1e-5)
+        torch.cuda.synchronize()
+        assert_close(host(y), O.layernorm(x, g, b, 1e-5), 1e-4, f"cols={cols}")
