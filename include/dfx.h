@@ -126,7 +126,7 @@ int dfx_colsum(int dtype, int64_t rows, int64_t cols, const void* x, int64_t ld,
  * VJPs (autodiff.py:1363-1459).  A and B are each either K-contiguous
  * (stride_k == 1) or M/N-contiguous (stride_m/stride_n == 1); D is
  * N-contiguous.  bf16 inputs run on tcgen05 tensor cores (TMA-fed, TMEM
- * accumulator) when the shape tiles (m%128, n%16, k%64, 16B-aligned strides);
+ * accumulator) when the shape tiles (m%128, k%64, 16B-aligned rows/strides);
  * everything else (and f32) runs on the CUDA-core FP32 path so f32 results
  * meet the 1e-4 parity bar. */
 enum dfx_epilogue {
@@ -156,9 +156,13 @@ typedef struct dfx_gemm_args {
   int64_t aux_stride_m, aux_stride_b1, aux_stride_b2;
   void* aux_out;
   int64_t aux_out_stride_m, aux_out_stride_b1, aux_out_stride_b2;
+  void* workspace; /* split-K partials (tensor-core path); see dfx_gemm_workspace */
+  size_t workspace_bytes;
 } dfx_gemm_args;
 
 int dfx_gemm(const dfx_gemm_args* args, void* stream);
+/* Workspace bytes dfx_gemm needs for these args (0 when none). */
+size_t dfx_gemm_workspace(const dfx_gemm_args* args);
 /* 1 if the call would take the tcgen05 path. */
 int dfx_gemm_uses_tensor_cores(const dfx_gemm_args* args);
 

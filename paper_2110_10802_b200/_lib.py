@@ -40,6 +40,7 @@ class GemmArgs(ctypes.Structure):
         ("aux_stride_b2", c_int64),
         ("aux_out", c_void_p), ("aux_out_stride_m", c_int64), ("aux_out_stride_b1", c_int64),
         ("aux_out_stride_b2", c_int64),
+        ("workspace", c_void_p), ("workspace_bytes", c_size_t),
     ]
 
 
@@ -70,6 +71,7 @@ _SIGS = [
                            c_size_t, c_void_p]),
     ("dfx_gemm", c_int, [POINTER(GemmArgs), c_void_p]),
     ("dfx_gemm_uses_tensor_cores", c_int, [POINTER(GemmArgs)]),
+    ("dfx_gemm_workspace", c_size_t, [POINTER(GemmArgs)]),
     ("dfx_mbconv_workspace", c_size_t, [c_int64, c_int64, c_int64, c_int64, c_int, c_void_p, c_int]),
     ("dfx_mbconv_fwd_stats", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_void_p,
                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,

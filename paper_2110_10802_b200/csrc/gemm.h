@@ -10,4 +10,6 @@ int gemm_simt(const dfx_gemm_args& p, cudaStream_t st);
 // when the shape/layout does not tile for tcgen05.
 bool gemm_tc_supported(const dfx_gemm_args& p);
 int gemm_tc(const dfx_gemm_args& p, cudaStream_t st);
+size_t gemm_tc_workspace(const dfx_gemm_args& p);
+void gemm_tc_set_trace(void* buf);
 }  // namespace dfx

@@ -7,21 +7,28 @@
 // its epilogue (bias, bias+GELU with pre-activation stash, GELU-backward,
 // residual add).
 //
-// Design (persistent, warp-specialised, one CTA per SM):
+// Design (persistent, warp-specialised, one CTA per SM, 10 warps):
 //   warp 0 (1 thread)  TMA producer: A and B tiles -> 128B-swizzled smem ring
 //                      (STAGES deep), completion via mbarrier tx-count.
 //   warp 1 (1 thread)  MMA issuer: tcgen05.mma.cta_group::1.kind::f16,
 //                      128 x BN x 16 per instruction, fp32 accumulator in TMEM;
 //                      tcgen05.commit frees smem stages / publishes accumulators.
-//   warps 2-5          epilogue: tcgen05.ld (32 lanes x 32 columns) -> fused
-//                      epilogue math in registers -> 16-byte global stores.
+//   warps 2-9          epilogue, two warps per TMEM lane quadrant (each owns
+//                      half of the tile's columns): tcgen05.ld (32 lanes x 32
+//                      columns) -> fused epilogue math in registers -> staged
+//                      in shared memory -> TMA bulk-tensor store (full 32x32
+//                      boxes, out-of-range rows/cols clipped by the TMA unit).
 //   TMEM holds two BN-column accumulators, so the epilogue of tile i overlaps
 //   the MMAs of tile i+1.
 // Operands may be K-major or MN-major (the UMMA descriptor's major bit), so
 // dgrad and wgrad GEMMs read activations and weights in place without
-// transposes.
+// transposes.  GEMMs with too few output tiles to fill the 148 SMs (the
+// 768-wide weight gradients) split K; fp32 partial tiles go to a workspace and
+// a fixed-order reduction writes the result (deterministic, no atomics).
 #include <cuda.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -32,32 +39,50 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle atom row
-constexpr int kThreads = 192;
-
-template <int BN> struct TcCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+constexpr int kEpiWarps = 16;
+constexpr int kThreads = (2 + kEpiWarps) * 32;
+template <int BN, int CG = 1> struct TcCfg {
+  // epilogue staging (TMA store source) per epilogue warp, and the smem ring
+  // depth: both sized so the CTA uses <= 227 KB
+  static constexpr int EPI_WARP_BYTES = 4096;  // output unit + aux unit, 32 rows x 64 B each
+  static constexpr int STAGES = CG == 2 ? (BN == 256 ? 5 : 6) : (BN == 256 ? 3 : (BN == 128 ? 5 : 6));
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = BN / CG * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_BYTES = kEpiWarps * EPI_WARP_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct TcParams {
   int64_t m, n, k;
   int64_t batch2;
   int32_t m_tiles, n_tiles, k_blocks, num_tiles;
-  int32_t a_mn, b_mn;  // operand is MN-major
+  int32_t splits, kb_per_split;  // split-K (splits > 1 -> fp32 partials to the workspace map)
+  int32_t a_mn, b_mn;            // operand is MN-major
   int32_t epilogue;
+  int32_t has_aux_out;
   float alpha, beta;
   const float* bias;
-  void* d;
-  int64_t d_stride_m, d_stride_b1, d_stride_b2;
   const void* aux;
   int64_t aux_stride_m, aux_stride_b1, aux_stride_b2;
+  void* d;
+  int64_t d_stride_m, d_stride_b1, d_stride_b2;
   void* aux_out;
   int64_t aux_out_stride_m, aux_out_stride_b1, aux_out_stride_b2;
+  float* part;  // split-K partials [split][z][m][n]
+  unsigned long long* trace;  // debug timeline (tools/gemm_trace.py), normally null
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot)                                                                       \
+  do {                                                                                    \
+    if (p.trace) p.trace[(size_t)blockIdx.x * 32 + (slot)] = gtime();                    \
+  } while (0)
 
 // ----------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -67,8 +92,7 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -85,52 +109,84 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
-                                            int c1, int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
+template <int CG>
+__device__ __forceinline__ void tma_load_4d_cg(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1,
+                                               int c2, int c3) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+  }
 }
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accum) {
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
   asm volatile(
       "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      ".reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(cta)
       : "memory");
 }
-// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+template <int CG>
+__device__ __forceinline__ void tc_commit_cg(uint64_t* bar) {
+  if constexpr (CG == 2) {
+    // arrive on the barrier at the same offset in both CTAs of the pair
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  } else {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tc_mma_cg(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accum) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+  }
+}
+// 32 lanes x 16 consecutive fp32 columns -> 16 registers per thread.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
-        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
-        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), sm100 version 1.
@@ -139,225 +195,432 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
 
-// Instruction descriptor: bf16 x bf16 -> f32, M=128, N=BN, majors.
-__host__ __device__ constexpr uint32_t make_idesc(int n, int a_mn, int b_mn) {
+// Instruction descriptor: bf16 x bf16 -> f32, M (128 or 256), N, majors.
+__host__ __device__ constexpr uint32_t make_idesc(int n, int m, int a_mn, int b_mn) {
   return (1u << 4)                      // c_format = F32
          | (1u << 7)                    // a_format = BF16
          | (1u << 10)                   // b_format = BF16
          | ((uint32_t)a_mn << 15)       // a major
          | ((uint32_t)b_mn << 16)       // b major
          | ((uint32_t)(n >> 3) << 17)   // N >> 3
-         | ((uint32_t)(BM >> 4) << 24); // M >> 4
+         | ((uint32_t)(m >> 4) << 24);  // M >> 4
 }
 
-template <typename TO> __device__ __forceinline__ void store32(TO* dst, const float (&v)[32]);
-template <> __device__ __forceinline__ void store32<float>(float* dst, const float (&v)[32]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-template <> __device__ __forceinline__ void store32<__nv_bfloat16>(__nv_bfloat16* dst, const float (&v)[32]) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    uint4 t;
-    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&t);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[8 * i + 2 * j], v[8 * i + 2 * j + 1]);
-    reinterpret_cast<uint4*>(dst)[i] = t;
+// bf16-output epilogues use the hardware tanh (error far below bf16 rounding)
+template <typename TO> __device__ __forceinline__ float gelu_epi(float x) {
+  if constexpr (sizeof(TO) == 2) {
+    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+    return 0.5f * x * (1.f + tanh_fast(u));
+  } else {
+    return gelu_f(x);
   }
 }
-template <typename TO> __device__ __forceinline__ void load32(const TO* src, float (&v)[32]);
-template <> __device__ __forceinline__ void load32<float>(const float* src, float (&v)[32]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    float4 t = reinterpret_cast<const float4*>(src)[i];
-    v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
-  }
-}
-template <> __device__ __forceinline__ void load32<__nv_bfloat16>(const __nv_bfloat16* src, float (&v)[32]) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    uint4 t = reinterpret_cast<const uint4*>(src)[i];
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&t);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float2 f = __bfloat1622float2(h[j]);
-      v[8 * i + 2 * j] = f.x; v[8 * i + 2 * j + 1] = f.y;
-    }
+template <typename TO> __device__ __forceinline__ float gelu_grad_epi(float x) {
+  if constexpr (sizeof(TO) == 2) {
+    const float c0 = 0.044715f, c1 = 0.7978845608028654f;
+    const float t = tanh_fast(c1 * (x + c0 * x * x * x));
+    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c1 * (1.f + 3.f * c0 * x * x);
+  } else {
+    return gelu_grad_f(x);
   }
 }
 
-template <int BN, typename TO>
+// ---- epilogue staging: a warp owns 32 rows; a staging unit is 32 rows x
+// UB bytes (UB = 128, or 64 for the narrowest tiles) of one output tensor.
+// Thread t writes row t; 16-byte chunk j of row r lives at chunk j ^ (r % L)
+// (L = UB / 16 chunks per row) so both the row-wise writes and the
+// column-coalesced read-back hit distinct banks.
+
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
+template <typename TO> __device__ __forceinline__ uint4 pack4(const float* v);  // 16 bytes of TO
+template <> __device__ __forceinline__ uint4 pack4<float>(const float* v) {
+  return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
+}
+template <> __device__ __forceinline__ uint4 pack4<__nv_bfloat16>(const float* v) {
+  uint4 t;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&t);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+  return t;
+}
+template <typename TO> __device__ __forceinline__ void unpack4(uint4 t, float* v);
+template <> __device__ __forceinline__ void unpack4<float>(uint4 t, float* v) {
+  v[0] = __uint_as_float(t.x); v[1] = __uint_as_float(t.y); v[2] = __uint_as_float(t.z); v[3] = __uint_as_float(t.w);
+}
+template <> __device__ __forceinline__ void unpack4<__nv_bfloat16>(uint4 t, float* v) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float2 f = __bfloat1622float2(h[e]);
+    v[2 * e] = f.x; v[2 * e + 1] = f.y;
+  }
+}
+
+// Stage this thread's 16 fp32 values (row `lane`, element offset `e0` within
+// the unit) as TO / read them back.
+template <typename TO, int L>
+__device__ __forceinline__ void stage16(uint32_t base, int lane, int e0, const float (&v)[16]) {
+  constexpr int EPC = 16 / (int)sizeof(TO);
+#pragma unroll
+  for (int j = 0; j < 16 / EPC; ++j) {
+    const int chunk = e0 / EPC + j;
+    sts128(base + lane * (L * 16) + ((chunk ^ (lane % L)) * 16), pack4<TO>(&v[j * EPC]));
+  }
+}
+template <typename TO, int L>
+__device__ __forceinline__ void unstage16(uint32_t base, int lane, int e0, float (&v)[16]) {
+  constexpr int EPC = 16 / (int)sizeof(TO);
+#pragma unroll
+  for (int j = 0; j < 16 / EPC; ++j) {
+    const int chunk = e0 / EPC + j;
+    unpack4<TO>(lds128(base + lane * (L * 16) + ((chunk ^ (lane % L)) * 16)), &v[j * EPC]);
+  }
+}
+template <typename TO, int L>
+__device__ __forceinline__ void store_unit(uint32_t base, int lane, TO* g, int64_t ld, int64_t m0, int64_t m,
+                                           int64_t n0, int64_t n) {
+  constexpr int EPC = 16 / (int)sizeof(TO);
+  constexpr int RPI = 32 / L;  // rows per instruction
+  const int c = lane % L;
+#pragma unroll
+  for (int it = 0; it < L; ++it) {
+    const int r = it * RPI + lane / L;
+    const uint4 v = lds128(base + r * (L * 16) + ((c ^ (r % L)) * 16));
+    const int64_t gm = m0 + r, gn = n0 + c * EPC;
+    if (gm < m && gn < n) *reinterpret_cast<uint4*>(g + gm * ld + gn) = v;
+  }
+}
+// Coalesced copy global rows -> staged unit (zeros out of range).
+template <typename TO, int L>
+__device__ __forceinline__ void load_unit(uint32_t base, int lane, const TO* g, int64_t ld, int64_t m0, int64_t m,
+                                          int64_t n0, int64_t n) {
+  constexpr int EPC = 16 / (int)sizeof(TO);
+  constexpr int RPI = 32 / L;
+  const int c = lane % L;
+#pragma unroll
+  for (int it = 0; it < L; ++it) {
+    const int r = it * RPI + lane / L;
+    const int64_t gm = m0 + r, gn = n0 + c * EPC;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (gm < m && gn < n) v = __ldg(reinterpret_cast<const uint4*>(g + gm * ld + gn));
+    sts128(base + r * (L * 16) + ((c ^ (r % L)) * 16), v);
+  }
+}
+
+// Decompose a linear tile index: n fastest, then m, then batch, then split.
+struct TileIdx {
+  int nb, mb, b1, b2, z, split;
+};
+__device__ __forceinline__ TileIdx tile_of(int t, const TcParams& p) {
+  TileIdx r;
+  r.nb = t % p.n_tiles;
+  int rest = t / p.n_tiles;
+  r.mb = rest % p.m_tiles;
+  rest /= p.m_tiles;
+  const int nz = p.num_tiles / (p.m_tiles * p.n_tiles * p.splits);
+  r.z = rest % nz;
+  r.split = rest / nz;
+  r.b1 = (int)(r.z / p.batch2);
+  r.b2 = (int)(r.z % p.batch2);
+  return r;
+}
+
+// CG = 1: one CTA per 128 x BN tile.  CG = 2: a CTA pair (cluster of 2) per
+// 256 x BN tile: each CTA loads its 128 rows of A and BN/2 columns of B, the
+// leader issues tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' shared
+// memory, and each CTA's TMEM receives its 128 accumulator rows.  Halving B
+// traffic per SM raises the flop-per-L2-byte ratio from 85 to 128.
+template <int BN, typename TO, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const TcParams p) {
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int BN_LOAD = BN / CG;  // B columns each CTA loads
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* epi_smem = smem + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + Cfg::EPI_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;   // [2]
-  uint64_t* tempty = tfull + 2;       // [2]
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TRACE(0);
+  uint32_t rank = 0;
+  if constexpr (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const bool leader = rank == 0;
+  const int cluster_id = CG == 2 ? blockIdx.x / 2 : blockIdx.x;
+  const int num_clusters = CG == 2 ? gridDim.x / 2 : gridDim.x;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * kEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "n"(Cfg::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(Cfg::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(Cfg::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  const int tiles_mn = p.m_tiles * p.n_tiles;
+  if (threadIdx.x == 0) TRACE(1);
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ producer
+      // (CG = 2: both CTAs load their halves; transaction bytes land on the
+      //  leader's full barrier, addressed by clearing the peer bit)
+      const uint32_t full_addr_mask = CG == 2 ? 0xFEFFFFFFu : 0xFFFFFFFFu;
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const int nb = t % p.n_tiles;
-        const int mb = (t / p.n_tiles) % p.m_tiles;
-        const int z = t / tiles_mn;
-        const int b1 = (int)(z / p.batch2), b2 = (int)(z % p.batch2);
-        const int m0 = mb * BM, n0 = nb * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+        const TileIdx ti = tile_of(t, p);
+        const int m0 = ti.mb * BM * CG + (int)rank * BM;
+        const int n0 = ti.nb * BN + (int)rank * BN_LOAD;
+        const int kb0 = ti.split * p.kb_per_split;
+        const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
-          mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+          if (leader) mbar_expect_tx(&full[s], CG * Cfg::STAGE_BYTES);
+          const uint32_t bar = smem_u32(&full[s]) & full_addr_mask;
           const int k0 = kb * BK;
           if (p.a_mn) {
-            tma_load_4d(&map_a, &full[s], sa, m0, k0, b2, b1);
-            tma_load_4d(&map_a, &full[s], sa + 8192, m0 + 64, k0, b2, b1);
+            tma_load_4d_cg<CG>(&map_a, bar, sa, m0, k0, ti.b2, ti.b1);
+            tma_load_4d_cg<CG>(&map_a, bar, sa + 8192, m0 + 64, k0, ti.b2, ti.b1);
           } else {
-            tma_load_4d(&map_a, &full[s], sa, k0, m0, b2, b1);
+            tma_load_4d_cg<CG>(&map_a, bar, sa, k0, m0, ti.b2, ti.b1);
           }
           if (p.b_mn) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_4d(&map_b, &full[s], sb + j * 8192, n0 + 64 * j, k0, b2, b1);
+            for (int j = 0; j < BN_LOAD / 64; ++j)
+              tma_load_4d_cg<CG>(&map_b, bar, sb + j * 8192, n0 + 64 * j, k0, ti.b2, ti.b1);
           } else {
-            tma_load_4d(&map_b, &full[s], sb, k0, n0, b2, b1);
+            tma_load_4d_cg<CG>(&map_b, bar, sb, k0, n0, ti.b2, ti.b1);
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       // ------------------------------------------------------------ MMA issuer
-      const uint32_t idesc = make_idesc(BN, p.a_mn, p.b_mn);
+      const uint32_t idesc = make_idesc(BN, BM * CG, p.a_mn, p.b_mn);
       // per-UMMA_K (16 elements) descriptor advance, in 16-byte units
       const uint32_t a_step = p.a_mn ? (2048 >> 4) : (32 >> 4);
       const uint32_t b_step = p.b_mn ? (2048 >> 4) : (32 >> 4);
       const uint32_t a_lbo = p.a_mn ? 8192 : 16, b_lbo = p.b_mn ? 8192 : 16;
       uint32_t it = 0, lt = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++lt) {
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++lt) {
+        const TileIdx ti = tile_of(t, p);
+        const int kb0 = ti.split * p.kb_per_split;
+        const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
         const int acc = lt & 1;
         const uint32_t aph = (lt >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          if (it == 0) TRACE(2);
           const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
           const uint32_t sb = sa + Cfg::A_BYTES;
           const uint64_t adesc = make_sdesc(sa, a_lbo, 1024);
           const uint64_t bdesc = make_sdesc(sb, b_lbo, 1024);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
-            tc_mma(tmem_d, adesc + (uint64_t)(kk * a_step), bdesc + (uint64_t)(kk * b_step), idesc,
-                   (kb | kk) != 0);
-          tc_commit(&empty[s]);
+            tc_mma_cg<CG>(tmem_d, adesc + (uint64_t)(kk * a_step), bdesc + (uint64_t)(kk * b_step), idesc,
+                          (kb != kb0 || kk != 0) ? 1u : 0u);
+          tc_commit_cg<CG>(&empty[s]);
         }
-        tc_commit(&tfull[acc]);
+        tc_commit_cg<CG>(&tfull[acc]);
+        if (lt < 8) TRACE(3 + lt);
       }
     }
   } else {
     // -------------------------------------------------------------- epilogue
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    // Four warps per TMEM lane quadrant (32 rows), each owning a quarter of
+    // the tile's columns.  Per staging unit (32 rows x 64 bytes):
+    // tcgen05.ld -> fused epilogue in registers -> swizzled smem -> coalesced
+    // 16-byte global stores (and the mirror path for the aux operand).
+    const int ew = warp - 2;          // 0..15
+    const int q = warp & 3;           // TMEM lane quadrant this warp may access
+    const int part = ew >> 2;         // which quarter of the tile's columns
+    constexpr int WCOLS = BN / 4;     // columns per warp
+    constexpr int ESZ = (int)sizeof(TO);
+    constexpr int UB = WCOLS * ESZ >= 64 ? 64 : WCOLS * ESZ;  // bytes per row per unit
+    constexpr int L = UB / 16;
+    constexpr int UCOLS = UB / ESZ;   // columns per unit (bf16 32, f32 16)
+    static_assert(WCOLS % UCOLS == 0, "warp columns must hold whole units");
+    constexpr int UNITS = WCOLS / UCOLS;
+    const bool split_out = p.splits > 1;
+    const uint32_t st_out = smem_u32(epi_smem + ew * Cfg::EPI_WARP_BYTES);
+    const uint32_t st_aux = st_out + 32 * UB;
+    const bool unit_alpha = p.alpha == 1.f;
     uint32_t lt = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++lt) {
-      const int nb = t % p.n_tiles;
-      const int mb = (t / p.n_tiles) % p.m_tiles;
-      const int z = t / tiles_mn;
-      const int64_t b1 = z / p.batch2, b2 = z % p.batch2;
+    for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++lt) {
+      const TileIdx ti = tile_of(t, p);
       const int acc = lt & 1;
       const uint32_t aph = (lt >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int64_t gm = (int64_t)mb * BM + q * 32 + lane;
-      TO* drow = (TO*)p.d + b1 * p.d_stride_b1 + b2 * p.d_stride_b2 + gm * p.d_stride_m;
-      const TO* xrow = p.aux ? (const TO*)p.aux + b1 * p.aux_stride_b1 + b2 * p.aux_stride_b2 + gm * p.aux_stride_m : nullptr;
-      TO* orow = p.aux_out ? (TO*)p.aux_out + b1 * p.aux_out_stride_b1 + b2 * p.aux_out_stride_b2 + gm * p.aux_out_stride_m : nullptr;
+      if (ew == 0 && lane == 0 && lt < 8) TRACE(11 + lt);
+      const int64_t m0 = (int64_t)ti.mb * BM * CG + (int)rank * BM + q * 32;
+      TO* dbase;
+      int64_t dld;
+      if (split_out) {
+        const int64_t nz = p.num_tiles / (p.m_tiles * p.n_tiles * p.splits);
+        dbase = reinterpret_cast<TO*>(p.part + ((int64_t)ti.split * nz + ti.z) * p.m * p.n);
+        dld = p.n;
+      } else {
+        dbase = (TO*)p.d + ti.b1 * p.d_stride_b1 + ti.b2 * p.d_stride_b2;
+        dld = p.d_stride_m;
+      }
+      const TO* xbase = p.aux ? (const TO*)p.aux + ti.b1 * p.aux_stride_b1 + ti.b2 * p.aux_stride_b2 : nullptr;
+      TO* obase = p.aux_out ? (TO*)p.aux_out + ti.b1 * p.aux_out_stride_b1 + ti.b2 * p.aux_out_stride_b2 : nullptr;
+      const bool use_aux = !split_out && (p.epilogue == DFX_EPI_GELU_BWD || p.epilogue == DFX_EPI_ADD);
+      const bool gelu = !split_out && p.epilogue == DFX_EPI_BIAS_GELU;
+      const bool biased = !split_out && (p.epilogue == DFX_EPI_BIAS || gelu) && p.bias != nullptr;
+      const bool store_pre = gelu && p.has_aux_out;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        const int64_t gn = (int64_t)nb * BN + c * 32;
-        if (gn >= p.n) break;  // n % 32 == 0 is required on this path
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
-        if (p.epilogue == DFX_EPI_BIAS || p.epilogue == DFX_EPI_BIAS_GELU) {
-          if (p.bias) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += __ldg(p.bias + gn + i);
-          }
-          if (p.epilogue == DFX_EPI_BIAS_GELU) {
-            if (orow) store32<TO>(orow + gn, v);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
-          }
-        } else if (p.epilogue == DFX_EPI_GELU_BWD) {
-          float a[32];
-          load32<TO>(xrow + gn, a);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(a[i]);
-        } else if (p.epilogue == DFX_EPI_ADD) {
-          float a[32];
-          load32<TO>(xrow + gn, a);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += p.beta * a[i];
+      for (int u = 0; u < UNITS; ++u) {
+        const int64_t n0 = (int64_t)ti.nb * BN + part * WCOLS + u * UCOLS;
+        if (n0 >= p.n) break;
+        if (use_aux) {
+          load_unit<TO, L>(st_aux, lane, xbase, p.aux_stride_m, m0, p.m, n0, p.n);
+          __syncwarp();
         }
-        store32<TO>(drow + gn, v);
+#pragma unroll
+        for (int hc = 0; hc < UCOLS / 16; ++hc) {
+          const int col = part * WCOLS + u * UCOLS + hc * 16;  // column within the tile
+          float v[16];
+          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
+          if (!unit_alpha) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] *= p.alpha;
+          }
+          if (biased) {
+            const int64_t gn = (int64_t)ti.nb * BN + col;
+            if (gn + 16 <= p.n && (reinterpret_cast<uintptr_t>(p.bias + gn) & 15) == 0) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + gn) + i);
+                v[4 * i] += b4.x; v[4 * i + 1] += b4.y; v[4 * i + 2] += b4.z; v[4 * i + 3] += b4.w;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] += (gn + i < p.n) ? __ldg(p.bias + gn + i) : 0.f;
+            }
+          }
+          if (use_aux) {
+            float a[16];
+            unstage16<TO, L>(st_aux, lane, hc * 16, a);
+            if (p.epilogue == DFX_EPI_GELU_BWD) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] *= gelu_grad_epi<TO>(a[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] += p.beta * a[i];
+            }
+          }
+          if (gelu) {
+            if (store_pre) stage16<TO, L>(st_aux, lane, hc * 16, v);  // the aux slot is free in this mode
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = gelu_epi<TO>(v[i]);
+          }
+          stage16<TO, L>(st_out, lane, hc * 16, v);
+        }
+        __syncwarp();
+        if (store_pre) store_unit<TO, L>(st_aux, lane, obase, p.aux_out_stride_m, m0, p.m, n0, p.n);
+        store_unit<TO, L>(st_out, lane, dbase, dld, m0, p.m, n0, p.n);
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (ew == 0 && lane == 0 && lt < 8) TRACE(19 + lt);
+      if (lane == 0) {
+        if (CG == 2 && !leader)
+          mbar_arrive_remote(&tempty[acc], 0);  // the leader's MMA waits for both CTAs
+        else
+          mbar_arrive(&tempty[acc]);
+      }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) TRACE(27);
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "n"(Cfg::TMEM_COLS)
-                 : "memory");
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::TMEM_COLS)
+                   : "memory");
+  }
+}
+
+// Fixed-order split-K reduction: D = sum_s part[s] (f32 workspace).
+template <typename TO>
+__global__ void splitk_reduce_kernel(int splits, int64_t Z, int64_t m, int64_t n, const float* __restrict__ part,
+                                     TO* __restrict__ d, int64_t d_stride_m, int64_t d_stride_b1,
+                                     int64_t d_stride_b2, int64_t batch2) {
+  const int64_t total = Z * m * n;
+  const int64_t per_split = total;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) acc += part[s * per_split + i];
+    const int64_t col = i % n, row = (i / n) % m, z = i / (n * m);
+    d[(z / batch2) * d_stride_b1 + (z % batch2) * d_stride_b2 + row * d_stride_m + col] = from_f<TO>(acc);
   }
 }
 
 // ----------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
-                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
-                                  CUtensorMapFloatOOBfill);
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
@@ -372,55 +635,140 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 4-D bf16 tensor map: dims (inner..outer) = {d0, d1, batch2, batch1}.
-int make_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, int64_t s1, int64_t nb2,
-             int64_t sb2, int64_t nb1, int64_t sb1, uint32_t box0, uint32_t box1) {
+// 4-D tensor map: dims (inner..outer) = {d0, d1, nb2, nb1}; strides in elements.
+int make_map(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t d1, int64_t s1, int64_t nb2,
+             int64_t sb2, int64_t nb1, int64_t sb1, uint32_t box0, uint32_t box1, bool swizzle128) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(DFX_ERR_CUDA, "dfx_gemm: cuTensorMapEncodeTiled unavailable");
-  const uint64_t esz = 2;
   cuuint64_t dims[4] = {d0, d1, (cuuint64_t)nb2, (cuuint64_t)nb1};
   // unused batch levels get a harmless 16B-multiple stride
   const uint64_t span = ((d1 * (uint64_t)s1 * esz) + 15) & ~uint64_t(15);
   cuuint64_t strides[3] = {(cuuint64_t)(s1 * esz), nb2 > 1 ? (cuuint64_t)(sb2 * esz) : span,
-                           nb1 > 1 ? (cuuint64_t)(sb1 * esz) : span};
+                           nb1 > 1 ? (cuuint64_t)(sb1 * esz) : span * (uint64_t)std::max<int64_t>(nb2, 1)};
   cuuint32_t box[4] = {box0, box1, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = fn(map, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(DFX_ERR_CUDA, "dfx_gemm: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  if (r != CUDA_SUCCESS)
+    return fail(DFX_ERR_CUDA, "dfx_gemm: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return DFX_OK;
 }
 
-int pick_bn(int64_t n) {
-  if (n <= 64) return 64;
-  if (n <= 128) return 128;
-  // minimise padded columns; ties prefer the wider tile
-  const int64_t w256 = ((n + 255) / 256) * 256 - n, w128 = ((n + 127) / 128) * 128 - n;
-  return w256 <= w128 ? 256 : 128;
+struct Plan {
+  int bn, cg, splits, kb_per_split;
+  int64_t tiles;  // work units (tiles x splits)
+};
+
+// Pick the tile shape by a wave-quantised cost model: time ~ waves x
+// (per-SM tile work / relative per-SM throughput).  The 2-CTA 256 x 256 tile
+// moves 2/3 of the L2 bytes per flop of a 1-CTA 128 x 256 tile (the GEMMs are
+// L2-bandwidth-bound on B200), hence its higher relative throughput.
+unsigned long long* g_trace = nullptr;
+
+Plan plan(const dfx_gemm_args& p) {
+  const int sms = num_sms();
+  static const char* force = getenv("DFX_GEMM_FORCE");  // "cg,bn" (tuning only)
+  if (force) {
+    int fcg = 1, fbn = 256;
+    if (sscanf(force, "%d,%d", &fcg, &fbn) == 2 && (fcg == 1 || fcg == 2) && (fbn == 64 || fbn == 128 || fbn == 256) &&
+        !(fcg == 2 && (fbn == 64 || p.m < 256))) {
+      const int64_t z = p.batch1 * p.batch2;
+      const int64_t kb = p.k / BK;
+      const int64_t units = z * ((p.m + BM * fcg - 1) / (BM * fcg)) * ((p.n + fbn - 1) / fbn);
+      return Plan{fbn, fcg, 1, (int)kb, units};
+    }
+  }
+  const int64_t z = p.batch1 * p.batch2;
+  const int64_t kb = p.k / BK;
+  struct Cand { int bn, cg; double thr; };
+  const Cand cands[] = {{256, 2, 1.5}, {128, 2, 1.0}, {256, 1, 1.0}, {128, 1, 0.8}, {64, 1, 0.6}};
+  Plan best{64, 1, 1, (int)kb, 0};
+  double best_cost = 1e30;
+  for (const Cand& c : cands) {
+    if (c.cg == 2 && (p.m < 256 || sms < 2)) continue;
+    const int64_t units = z * ((p.m + BM * c.cg - 1) / (BM * c.cg)) * ((p.n + c.bn - 1) / c.bn);
+    const int64_t slots = sms / c.cg;
+    const double waves = (double)((units + slots - 1) / slots);
+    // padded columns cost as much as real ones
+    const double cost = waves * (double)c.bn / c.thr;
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = Plan{c.bn, c.cg, 1, (int)kb, units};
+    }
+  }
+  // split K when a 1-CTA plan leaves most SMs idle (the 768-wide wgrads)
+  if (best.cg == 1 && p.epilogue == DFX_EPI_NONE && best.tiles * 2 <= sms && kb >= 8) {
+    if (best.bn == 256) {
+      best.bn = 128;
+      best.tiles = z * (p.m / BM) * ((p.n + 127) / 128);
+    }
+    int64_t s = std::min<int64_t>(sms / std::max<int64_t>(best.tiles, 1), kb / 4);
+    s = std::min<int64_t>(s, 8);
+    if (s >= 2) best.splits = (int)s;
+  }
+  best.kb_per_split = (int)((kb + best.splits - 1) / best.splits);
+  best.splits = (int)((kb + best.kb_per_split - 1) / best.kb_per_split);
+  best.tiles *= best.splits;
+  return best;
 }
 
-template <int BN, typename TO>
+template <int BN, typename TO, int CG>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& tp, cudaStream_t st) {
-  auto kfn = tc_gemm_kernel<BN, TO>;
+  auto kfn = tc_gemm_kernel<BN, TO, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::SMEM);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN, CG>::SMEM);
     attr_set = true;
   }
-  const int grid = std::min(tp.num_tiles, num_sms());
-  kfn<<<grid, kThreads, TcCfg<BN>::SMEM, st>>>(ma, mb, tp);
+  const int clusters = std::min(tp.num_tiles, num_sms() / CG);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * CG);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = TcCfg<BN, CG>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, tp);
+  if (e != cudaSuccess) return fail(DFX_ERR_CUDA, std::string("dfx_gemm (tcgen05) launch: ") + cudaGetErrorString(e));
   DFX_LAUNCH_CHECK("dfx_gemm (tcgen05)");
   return DFX_OK;
 }
 
+template <typename TO>
+int launch_tc_any(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& tp,
+                  cudaStream_t st) {
+  if (cg == 2) {
+    if (bn == 256) return launch_tc<256, TO, 2>(ma, mb, tp, st);
+    return launch_tc<128, TO, 2>(ma, mb, tp, st);
+  }
+  if (bn == 256) return launch_tc<256, TO, 1>(ma, mb, tp, st);
+  if (bn == 128) return launch_tc<128, TO, 1>(ma, mb, tp, st);
+  return launch_tc<64, TO, 1>(ma, mb, tp, st);
+}
+
 }  // namespace
+
+void gemm_tc_set_trace(void* buf) { g_trace = reinterpret_cast<unsigned long long*>(buf); }
+
+size_t gemm_tc_workspace(const dfx_gemm_args& p) {
+  if (!gemm_tc_supported(p)) return 0;
+  const Plan pl = plan(p);
+  if (pl.splits <= 1) return 0;
+  return (size_t)pl.splits * p.batch1 * p.batch2 * p.m * p.n * sizeof(float) + 256;
+}
 
 bool gemm_tc_supported(const dfx_gemm_args& p) {
   if (p.force_simt || p.in_dtype != DFX_BF16) return false;
   if (p.out_dtype != DFX_BF16 && p.out_dtype != DFX_F32) return false;
   if (p.m <= 0 || p.n <= 0 || p.k <= 0) return false;
-  if (p.m % BM || p.k % BK || p.n % 32) return false;
+  if (p.m % BM || p.k % BK) return false;
   const bool a_k = p.a_stride_k == 1, a_m = p.a_stride_m == 1;
   const bool b_k = p.b_stride_k == 1, b_n = p.b_stride_n == 1;
   if (!(a_k || a_m) || !(b_k || b_n)) return false;
@@ -432,44 +780,72 @@ bool gemm_tc_supported(const dfx_gemm_args& p) {
     return false;
   if (!aligned16(p.a) || !aligned16(p.b) || !aligned16(p.d)) return false;
   const int osz = p.out_dtype == DFX_BF16 ? 2 : 4;
-  if ((p.d_stride_m * osz) % 16) return false;
+  const int ovec = 16 / osz;
+  if (p.n % ovec || p.d_stride_m % ovec) return false;  // TMA store: 16-byte row strides
+  if ((p.batch2 > 1 && p.d_stride_b2 % ovec) || (p.batch1 > 1 && p.d_stride_b1 % ovec)) return false;
   if (p.aux && ((p.aux_stride_m * osz) % 16 || !aligned16(p.aux))) return false;
-  if (p.aux_out && ((p.aux_out_stride_m * osz) % 16 || !aligned16(p.aux_out))) return false;
-  if (p.batch1 * p.batch2 * (p.m / BM) * ((p.n + 63) / 64) > (1ll << 31)) return false;
+  if (p.aux_out && (p.aux_out_stride_m % ovec || !aligned16(p.aux_out) ||
+                    (p.batch2 > 1 && p.aux_out_stride_b2 % ovec) || (p.batch1 > 1 && p.aux_out_stride_b1 % ovec)))
+    return false;
+  if (p.batch1 * p.batch2 * (p.m / BM) * ((p.n + 63) / 64) * 8 > (1ll << 31)) return false;
   return true;
 }
 
 int gemm_tc(const dfx_gemm_args& p, cudaStream_t st) {
-  const int bn = pick_bn(p.n);
+  const Plan pl = plan(p);
+  const int bn = pl.bn;
   const bool a_mn = p.a_stride_k != 1, b_mn = p.b_stride_k != 1;
   CUtensorMap ma, mb;
   int rc;
   if (a_mn)
-    rc = make_map(&ma, p.a, p.m, p.k, p.a_stride_k, p.batch2, p.a_stride_b2, p.batch1, p.a_stride_b1, 64, 64);
+    rc = make_map(&ma, p.a, 2, p.m, p.k, p.a_stride_k, p.batch2, p.a_stride_b2, p.batch1, p.a_stride_b1, 64, 64, true);
   else
-    rc = make_map(&ma, p.a, p.k, p.m, p.a_stride_m, p.batch2, p.a_stride_b2, p.batch1, p.a_stride_b1, 64, BM);
+    rc = make_map(&ma, p.a, 2, p.k, p.m, p.a_stride_m, p.batch2, p.a_stride_b2, p.batch1, p.a_stride_b1, 64, BM, true);
   if (rc) return rc;
   if (b_mn)
-    rc = make_map(&mb, p.b, p.n, p.k, p.b_stride_k, p.batch2, p.b_stride_b2, p.batch1, p.b_stride_b1, 64, 64);
+    rc = make_map(&mb, p.b, 2, p.n, p.k, p.b_stride_k, p.batch2, p.b_stride_b2, p.batch1, p.b_stride_b1, 64, 64, true);
   else
-    rc = make_map(&mb, p.b, p.k, p.n, p.b_stride_n, p.batch2, p.b_stride_b2, p.batch1, p.b_stride_b1, 64, bn);
+    rc = make_map(&mb, p.b, 2, p.k, p.n, p.b_stride_n, p.batch2, p.b_stride_b2, p.batch1, p.b_stride_b1, 64,
+                  bn / pl.cg, true);
   if (rc) return rc;
+  const int64_t Z = p.batch1 * p.batch2;
+  float* part = nullptr;
+  if (pl.splits > 1) {
+    const size_t need = (size_t)pl.splits * Z * p.m * p.n * sizeof(float);
+    DFX_REQUIRE(p.workspace && p.workspace_bytes >= need && aligned16(p.workspace), DFX_ERR_WORKSPACE,
+                "dfx_gemm: split-K needs dfx_gemm_workspace() bytes of workspace");
+    part = (float*)p.workspace;  // partials [split][z][m][n] f32
+  }
   TcParams tp;
   tp.m = p.m; tp.n = p.n; tp.k = p.k; tp.batch2 = p.batch2;
-  tp.m_tiles = (int)(p.m / BM);
+  tp.m_tiles = (int)((p.m + BM * pl.cg - 1) / (BM * pl.cg));
   tp.n_tiles = (int)((p.n + bn - 1) / bn);
   tp.k_blocks = (int)(p.k / BK);
-  tp.num_tiles = (int)(p.batch1 * p.batch2 * tp.m_tiles * tp.n_tiles);
+  tp.splits = pl.splits;
+  tp.kb_per_split = pl.kb_per_split;
+  tp.num_tiles = (int)pl.tiles;
   tp.a_mn = a_mn; tp.b_mn = b_mn;
-  tp.epilogue = p.epilogue; tp.alpha = p.alpha; tp.beta = p.beta; tp.bias = p.bias;
-  tp.d = p.d; tp.d_stride_m = p.d_stride_m; tp.d_stride_b1 = p.d_stride_b1; tp.d_stride_b2 = p.d_stride_b2;
+  tp.epilogue = p.epilogue; tp.has_aux_out = p.aux_out != nullptr;
+  tp.alpha = p.alpha; tp.beta = p.beta; tp.bias = p.bias;
   tp.aux = p.aux; tp.aux_stride_m = p.aux_stride_m; tp.aux_stride_b1 = p.aux_stride_b1; tp.aux_stride_b2 = p.aux_stride_b2;
+  tp.d = p.d; tp.d_stride_m = p.d_stride_m; tp.d_stride_b1 = p.d_stride_b1; tp.d_stride_b2 = p.d_stride_b2;
   tp.aux_out = p.aux_out; tp.aux_out_stride_m = p.aux_out_stride_m; tp.aux_out_stride_b1 = p.aux_out_stride_b1;
   tp.aux_out_stride_b2 = p.aux_out_stride_b2;
-  const bool f32 = p.out_dtype == DFX_F32;
-  if (bn == 256) return f32 ? launch_tc<256, float>(ma, mb, tp, st) : launch_tc<256, __nv_bfloat16>(ma, mb, tp, st);
-  if (bn == 128) return f32 ? launch_tc<128, float>(ma, mb, tp, st) : launch_tc<128, __nv_bfloat16>(ma, mb, tp, st);
-  return f32 ? launch_tc<64, float>(ma, mb, tp, st) : launch_tc<64, __nv_bfloat16>(ma, mb, tp, st);
+  tp.part = part;
+  tp.trace = g_trace;
+  const bool f32 = pl.splits > 1 || p.out_dtype == DFX_F32;
+  rc = f32 ? launch_tc_any<float>(bn, pl.cg, ma, mb, tp, st) : launch_tc_any<__nv_bfloat16>(bn, pl.cg, ma, mb, tp, st);
+  if (rc || pl.splits <= 1) return rc;
+  const int64_t total = Z * p.m * p.n;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+  if (p.out_dtype == DFX_F32)
+    splitk_reduce_kernel<float><<<grid, 256, 0, st>>>(pl.splits, Z, p.m, p.n, part, (float*)p.d, p.d_stride_m,
+                                                      p.d_stride_b1, p.d_stride_b2, p.batch2);
+  else
+    splitk_reduce_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(pl.splits, Z, p.m, p.n, part, (__nv_bfloat16*)p.d,
+                                                              p.d_stride_m, p.d_stride_b1, p.d_stride_b2, p.batch2);
+  DFX_LAUNCH_CHECK("dfx_gemm split-K reduce");
+  return DFX_OK;
 }
 
 }  // namespace dfx

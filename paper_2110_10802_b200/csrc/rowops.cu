@@ -39,87 +39,97 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
     T* __restrict__ y, T* __restrict__ s_out, float* __restrict__ mean_out,
     float* __restrict__ rstd_out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * kWarps + warp;
-  if (row >= rows) return;
   const int nvec = cols / V;
-  const size_t base = (size_t)row * cols;
-  float x[NCH][V];
-  float sum = 0.f;
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    const int vi = lane + c * 32;
-    if (vi < nvec) {
-      const int col = vi * V;
-      Vec<T, V> hv;
-      hv.load(h + base + col);
-      float b[V], m[V], r[V];
-      if (bias) { Vec<float, V> bv; bv.load(bias + col);
-#pragma unroll
-        for (int i = 0; i < V; ++i) b[i] = bv.v[i];
-      } else {
-#pragma unroll
-        for (int i = 0; i < V; ++i) b[i] = 0.f;
-      }
-      if (keep) load_keep<V>(keep + base + col, ks, m);
-      else {
-#pragma unroll
-        for (int i = 0; i < V; ++i) m[i] = 1.f;
-      }
-      if (res) { Vec<T, V> rv; rv.load(res + base + col);
-#pragma unroll
-        for (int i = 0; i < V; ++i) r[i] = rv.v[i];
-      } else {
-#pragma unroll
-        for (int i = 0; i < V; ++i) r[i] = 0.f;
-      }
-#pragma unroll
-      for (int i = 0; i < V; ++i) {
-        x[c][i] = (hv.v[i] + b[i]) * m[i] + r[i];
-        sum += x[c][i];
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < V; ++i) x[c][i] = 0.f;
-    }
-  }
   const float inv_n = 1.f / (float)cols;
-  const float mu = warp_sum(sum) * inv_n;
-  float sq = 0.f;
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    if (lane + c * 32 < nvec) {
-#pragma unroll
-      for (int i = 0; i < V; ++i) { const float d = x[c][i] - mu; sq += d * d; }
-    }
-  }
-  const float var = warp_sum(sq) * inv_n;
-  const float rstd = rsqrtf(var + eps);
+  // the lane's parameter columns stay in registers across all its rows
+  float pb[NCH][V], pg[NCH][V], pbt[NCH][V];
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int vi = lane + c * 32;
+#pragma unroll
+    for (int i = 0; i < V; ++i) { pb[c][i] = 0.f; pg[c][i] = 0.f; pbt[c][i] = 0.f; }
     if (vi < nvec) {
-      const int col = vi * V;
       Vec<float, V> g, bt;
-      g.load(gamma + col);
-      bt.load(beta + col);
-      if (s_out) {
-        Vec<T, V> sv;
+      g.load(gamma + vi * V);
+      bt.load(beta + vi * V);
 #pragma unroll
-        for (int i = 0; i < V; ++i) sv.v[i] = x[c][i];
-        sv.store(s_out + base + col);
-      }
-      Vec<T, V> yv;
+      for (int i = 0; i < V; ++i) { pg[c][i] = g.v[i]; pbt[c][i] = bt.v[i]; }
+      if (bias) {
+        Vec<float, V> bv;
+        bv.load(bias + vi * V);
 #pragma unroll
-      for (int i = 0; i < V; ++i) {
-        const float u = (x[c][i] - mu) * rstd * g.v[i] + bt.v[i];
-        yv.v[i] = ACT ? u * sigmoid_f(u) : u;
+        for (int i = 0; i < V; ++i) pb[c][i] = bv.v[i];
       }
-      yv.store(y + base + col);
     }
   }
-  if (lane == 0) {
-    if (mean_out) mean_out[row] = mu;
-    if (rstd_out) rstd_out[row] = rstd;
+  for (int64_t row = (int64_t)blockIdx.x * kWarps + warp; row < rows; row += (int64_t)gridDim.x * kWarps) {
+    const size_t base = (size_t)row * cols;
+    float x[NCH][V];
+    float sum = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int vi = lane + c * 32;
+      if (vi < nvec) {
+        const int col = vi * V;
+        Vec<T, V> hv;
+        hv.load(h + base + col);
+        float m[V], r[V];
+        if (keep) load_keep<V>(keep + base + col, ks, m);
+        else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) m[i] = 1.f;
+        }
+        if (res) { Vec<T, V> rv; rv.load(res + base + col);
+#pragma unroll
+          for (int i = 0; i < V; ++i) r[i] = rv.v[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) r[i] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          x[c][i] = (hv.v[i] + pb[c][i]) * m[i] + r[i];
+          sum += x[c][i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) x[c][i] = 0.f;
+      }
+    }
+    const float mu = warp_sum(sum) * inv_n;
+    float sq = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      if (lane + c * 32 < nvec) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) { const float d = x[c][i] - mu; sq += d * d; }
+      }
+    }
+    const float rstd = rsqrtf(warp_sum(sq) * inv_n + eps);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int vi = lane + c * 32;
+      if (vi < nvec) {
+        const int col = vi * V;
+        if (s_out) {
+          Vec<T, V> sv;
+#pragma unroll
+          for (int i = 0; i < V; ++i) sv.v[i] = x[c][i];
+          sv.store(s_out + base + col);
+        }
+        Vec<T, V> yv;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const float u = (x[c][i] - mu) * rstd * pg[c][i] + pbt[c][i];
+          yv.v[i] = ACT ? u * sigmoid_f(u) : u;
+        }
+        yv.store(y + base + col);
+      }
+    }
+    if (lane == 0) {
+      if (mean_out) mean_out[row] = mu;
+      if (rstd_out) rstd_out[row] = rstd;
+    }
   }
 }
 
@@ -149,7 +159,7 @@ __device__ __forceinline__ void block_colsum_store(float (&acc)[NCH][V], int col
 }
 
 template <typename T, int V, int NCH, int ACT = 0>
-__global__ void __launch_bounds__(256) bdrln_bwd_kernel(
+__global__ void __launch_bounds__(256, 2) bdrln_bwd_kernel(
     int64_t rows, int cols, const T* __restrict__ dy, const T* __restrict__ s,
     const float* __restrict__ gamma, const float* __restrict__ beta,
     const uint8_t* __restrict__ keep, float ks, float eps,
@@ -160,23 +170,10 @@ __global__ void __launch_bounds__(256) bdrln_bwd_kernel(
   const int nvec = cols / V;
   const float inv_n = 1.f / (float)cols;
   float acc_g[NCH][V], acc_b[NCH][V], acc_h[NCH][V];
-  float gam[NCH][V], bet[NCH][V];
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    const int vi = lane + c * 32;
+  for (int c = 0; c < NCH; ++c)
 #pragma unroll
-    for (int i = 0; i < V; ++i) { acc_g[c][i] = 0.f; acc_b[c][i] = 0.f; acc_h[c][i] = 0.f; gam[c][i] = 0.f; bet[c][i] = 0.f; }
-    if (vi < nvec) {
-      Vec<float, V> g; g.load(gamma + vi * V);
-#pragma unroll
-      for (int i = 0; i < V; ++i) gam[c][i] = g.v[i];
-      if (ACT) {
-        Vec<float, V> b; b.load(beta + vi * V);
-#pragma unroll
-        for (int i = 0; i < V; ++i) bet[c][i] = b.v[i];
-      }
-    }
-  }
+    for (int i = 0; i < V; ++i) { acc_g[c][i] = 0.f; acc_b[c][i] = 0.f; acc_h[c][i] = 0.f; }
   for (int64_t row = (int64_t)blockIdx.x * kWarps + warp; row < rows;
        row += (int64_t)gridDim.x * kWarps) {
     const size_t base = (size_t)row * cols;
@@ -205,17 +202,37 @@ __global__ void __launch_bounds__(256) bdrln_bwd_kernel(
         for (int i = 0; i < V; ++i) { const float d = x[c][i] - mu; sq += d * d; }
       }
     const float rstd = rsqrtf(warp_sum(sq) * inv_n + eps);
+    // gamma (and beta) are re-read per row from L1: keeping them in
+    // registers would cost 2 blocks/SM of occupancy
+    float gam[NCH][V];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int vi = lane + c * 32;
+#pragma unroll
+      for (int i = 0; i < V; ++i) gam[c][i] = 0.f;
+      if (vi < nvec) {
+        Vec<float, V> gv;
+        gv.load(gamma + vi * V);
+#pragma unroll
+        for (int i = 0; i < V; ++i) gam[c][i] = gv.v[i];
+        if constexpr (ACT) {
+          Vec<float, V> bv;
+          bv.load(beta + vi * V);
+#pragma unroll
+          for (int i = 0; i < V; ++i) {  // dy w.r.t. the LN output through swish
+            const float u = (x[c][i] - mu) * rstd * gam[c][i] + bv.v[i];
+            const float sg = sigmoid_f(u);
+            g[c][i] *= sg + u * sg * (1.f - sg);
+          }
+        }
+      }
+    }
     float m1 = 0.f, m2 = 0.f;
 #pragma unroll
     for (int c = 0; c < NCH; ++c)
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         x[c][i] = (x[c][i] - mu) * rstd;  // xhat (0 on padding lanes: gamma=0, dy=0)
-        if (ACT) {  // dy w.r.t. the LN output through swish
-          const float u = x[c][i] * gam[c][i] + bet[c][i];
-          const float sg = sigmoid_f(u);
-          g[c][i] *= sg + u * sg * (1.f - sg);
-        }
         const float dyg = g[c][i] * gam[c][i];
         m1 += dyg;
         m2 += dyg * x[c][i];
@@ -549,7 +566,7 @@ int bdrln_fwd_t(int64_t rows, int64_t cols, const void* h, const float* bias, co
                 void* s_out, float* mean, float* rstd, cudaStream_t st, int act = 0) {
   if (int rc = check_row_shape<T, V>(cols, "dfx_bdrln_fwd")) return rc;
   const int nch = pick_nch((int)(cols / V));
-  const int grid = (int)((rows + kWarps - 1) / kWarps);
+  const int grid = grid_for(rows, kWarps, 4 * num_sms());
   if (rows == 0) return DFX_OK;
 #define L(N)                                                                                        \
   if (nch == N) {                                                                                   \

@@ -354,6 +354,10 @@ def gemm(a, b, d, epilogue=_lib.EPI_NONE, alpha=1.0, beta=1.0, bias=None, aux=No
          force_simt=False):
     g = gemm_args(a, b, d, epilogue, alpha, beta, bias, aux, aux_out, force_simt)
     lib = _lib.load()
+    need = lib.dfx_gemm_workspace(g)
+    if need:
+        ws = WORKSPACE.get(need)
+        g.workspace, g.workspace_bytes = ws.data_ptr(), ws.numel()
     if _TIMER is None:
         _lib.check(lib.dfx_gemm(g, _stream()), "dfx_gemm")
         return d

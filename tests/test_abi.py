@@ -28,7 +28,7 @@ def test_binding_covers_header():
 
 def test_gemm_args_layout_matches_header():
     # 4 int32 + 5 int64 + (ptr + 4 int64) * 2 + ptr + 3 int64 + 2 float + ptr + (ptr + 3 int64) * 2
-    assert ctypes.sizeof(_lib.GemmArgs) == 4 * 4 + 5 * 8 + 2 * 40 + 32 + 8 + 8 + 2 * 32
+    assert ctypes.sizeof(_lib.GemmArgs) == 4 * 4 + 5 * 8 + 2 * 40 + 32 + 8 + 8 + 2 * 32 + 16
 
 
 def test_cpu_only_calls_do_not_need_gpu():

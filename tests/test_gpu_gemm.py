@@ -138,3 +138,40 @@ def test_tc_large_wgrad_fp32_out():
     torch.cuda.synchronize()
     want = (dpre.float().t() @ ln1.float()).double().cpu().numpy()
     _check(dw, want, 1e-3)
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_tc_split_k(out_dtype):
+    """Few-tile GEMMs (the 768x768 out-proj weight gradient) split K into f32
+    partials reduced in fixed order."""
+    kk = K()
+    T, H = 4096, 768
+    a = _rand((T, H), torch.bfloat16, 31)
+    b = _rand((T, H), torch.bfloat16, 32)
+    d = torch.empty(H, H, dtype=out_dtype, device="cuda")
+    from paper_2110_10802_b200 import _lib
+
+    g = kk.gemm_args(a.t(), b.t(), d)
+    assert _lib.load().dfx_gemm_workspace(g) > 0  # the split-K plan is taken
+    kk.gemm(a.t(), b.t(), d)
+    d2 = torch.empty_like(d)
+    kk.gemm(a.t(), b.t(), d2)
+    torch.cuda.synchronize()
+    assert torch.equal(d, d2)  # deterministic
+    want = (a.float().t() @ b.float()).double().cpu().numpy()
+    _check(d, want, 1e-2 if out_dtype == torch.bfloat16 else 1e-3)
+
+
+@pytest.mark.parametrize("n", [8, 40, 200])
+def test_tc_ragged_n(n):
+    """N not a multiple of the tile: TMA loads zero-fill, TMA stores clip."""
+    kk = K()
+    a, b = _operands(256, n, 128, "k", "k", torch.bfloat16, n)
+    bias = _rand((n,), torch.float32, 5, 0.1)
+    d = torch.full((256, n), 7.0, dtype=torch.bfloat16, device="cuda")
+    from paper_2110_10802_b200 import _lib
+
+    assert kk.gemm_uses_tensor_cores(a, b, d)
+    kk.gemm(a, b, d, _lib.EPI_BIAS, bias=bias)
+    torch.cuda.synchronize()
+    _check(d, _ref(a, b) + bias.double().cpu().numpy(), 1e-2)
