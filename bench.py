@@ -26,9 +26,7 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -43,8 +41,8 @@ UNIT = "samples/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -136,46 +134,59 @@ def run_reference(args):
 
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock / power / throttle-reason samples taken DURING the timed
+    region by a background thread polling NVML every 5 ms (nvidia-smi's
+    100 ms loop sees at most a sample or two of a sub-second timed region)."""
 
-    def __init__(self, index):
-        self.index = index
-        self.proc = None
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+
+    def __init__(self, index, period_s=0.005):
+        self.index, self.period = index, period_s
+        self.rows, self.thread, self.nv = [], None, None
 
     def __enter__(self):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
-                stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 — no NVML: report "unsampled"
+            self.nv = None
+            return self
+        self.stop = threading.Event()
+        self.thread = threading.Thread(target=self._loop, daemon=True)
+        self.thread.start()
         return self
 
-    def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
+    def _loop(self):
+        nv, h = self.nv, self.h
+        while not self.stop.is_set():
             try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+                self.rows.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                  nv.nvmlDeviceGetPowerUsage(h) / 1e3,
+                                  nv.nvmlDeviceGetCurrentClocksEventReasons(h),
+                                  nv.nvmlDeviceGetUtilizationRates(h).gpu))
+            except Exception:  # noqa: BLE001
+                pass
+            self.stop.wait(self.period)
+
+    def __exit__(self, *exc):
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join()
 
     def summary(self):
-        self.f.flush()
-        self.f.seek(0)
-        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.count(",") >= 7]
-        os.unlink(self.f.name)
-        if not rows:
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in rows]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" == r[4 + i].strip()})
-        pw = [float(r[3]) for r in rows if r[3].strip() not in ("[N/A]", "")]
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(pw) if pw else None}
+        busy = [r for r in self.rows if r[3] > 0] or self.rows
+        reasons = sorted({n for r in busy for n, bit in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in busy), "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "samples": len(self.rows), "samples_under_load": len(busy),
+                "power_w_max": round(max(r[1] for r in self.rows), 1), "source": "NVML, 5 ms poll"}
 
 
 # ---------------------------------------------------------------------------
