@@ -105,6 +105,34 @@ int dfx_softmax_bwd(int dtype, int64_t rows, int64_t cols, const void* dpd, cons
                     const uint8_t* keep, float keep_scale, float inv_divisor, void* dscores,
                     void* stream);
 
+/* ---- a4-a6 + a8 fused: scaled-masked-softmax attention (bf16, tcgen05) -----
+ * The QKᵀ Einsum (frontend.py:408-481), Div by `divisor` (294), additive mask
+ * (175-188), Softmax (493-501), dropout Mul (293) and the PV Einsum of one
+ * encoder layer in one kernel, the [B,NH,S,S] scores never leaving the SM
+ * (the reference recipe's per-query-row attention map).
+ * qkv: bf16 [B*S, ld_qkv] holding Q | K | V column blocks of NH*64 columns
+ * (head h = columns h*64..h*64+63 of each block); head_dim must be 64,
+ * seq a multiple of 128 and <= 512.
+ *   ctx[b*S+s, h*64+d] = sum_t Pd[b,h,s,t] V[b*S+t, h*64+d]   (bf16)
+ *   lse[b,h,s]          = log2 sum_t exp2(log2e*(S/divisor + mask))  (f32)
+ *   keep_bits_row[b,h,s,t/32] bit t%32 = keep[b,h,s,t]; keep_bits_col[b,h,t,s/32]
+ *   bit s%32 = keep[b,h,s,t] — the packed dropout masks the backward reads
+ *   (each [B,NH,S,S/32] u32; pass both or neither; keep may be NULL = no dropout). */
+int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t head_dim, const void* qkv,
+                 int64_t ld_qkv, const float* add_mask, const uint8_t* keep, float keep_scale,
+                 float inv_divisor, void* ctx, int64_t ld_ctx, float* lse, uint32_t* keep_bits_row,
+                 uint32_t* keep_bits_col, void* stream);
+/* Backward of the above (Einsum VJPs autodiff.py:1363-1415, Softmax VJP
+ * 1465-1484, dropout Mul VJP): writes dQ | dK | dV into dqkv [B*S, ld_dqkv]
+ * (bf16, same column layout as qkv).  ctx is the forward output, dctx its
+ * gradient (both [B*S, ld_ctx] bf16).  Workspace: dfx_attn_bwd_workspace(). */
+size_t dfx_attn_bwd_workspace(int64_t batch, int64_t heads, int64_t seq);
+int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t head_dim, const void* qkv,
+                 int64_t ld_qkv, const void* ctx, const void* dctx, int64_t ld_ctx,
+                 const float* add_mask, const float* lse, const uint32_t* keep_bits_row,
+                 const uint32_t* keep_bits_col, float keep_scale, float inv_divisor, void* dqkv,
+                 int64_t ld_dqkv, void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- a7: bias + tanh-GELU -------------------------------------------------
  * pre = f + bias ; y = 0.5*pre*(1+tanh(0.7978845608*(pre+0.044715*pre^3)))
  * (Pow/Mul/Add/Tanh chain, frontend.py:223-295).  pre may be NULL. */

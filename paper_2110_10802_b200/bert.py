@@ -41,6 +41,9 @@ class BertLayerConfig:
     eps: float = 1e-12
     p_drop: float = 0.1
     dtype: torch.dtype = torch.bfloat16
+    # bf16: QKᵀ -> softmax -> dropout -> PV as one tcgen05 kernel per direction
+    # (csrc/attn.cu); False keeps the unfused GEMM + softmax-kernel chain
+    fused_attention: bool = True
 
     @property
     def head_dim(self) -> int:
@@ -176,7 +179,19 @@ class BertEncoderLayer:
                 ds2=e(T, H), da2=e(T, H), dpre=e(T, F), dln1=e(T, H), ds1=e(T, H), da1=e(T, H),
                 dctx=e(T, H), dpd=e(B, NH, S, S), dsc=e(B, NH, S, S), dqkv=e(T, 3 * H), dx=e(T, H),
             )
+            if self._fused(S):
+                for nm in ("scores", "p", "pd", "dpd", "dsc"):
+                    del self._bufs[key][nm]
+                i32 = dict(dtype=torch.int32, device=dev)
+                self._bufs[key].update(lse=torch.empty(B, NH, S, dtype=torch.float32, device=dev),
+                                       kbits_row=torch.empty(B, NH, S, S // 32, **i32),
+                                       kbits_col=torch.empty(B, NH, S, S // 32, **i32))
         return self._bufs[key]
+
+    def _fused(self, S) -> bool:
+        c = self.cfg
+        return (c.fused_attention and c.dtype == torch.bfloat16 and c.head_dim == 64
+                and S % 128 == 0 and S <= 512)
 
     def _heads(self, t, B, S, which):
         """[B, NH, S, dh] view of the Q/K/V (which=0/1/2) block of a [T, 3H] tensor."""
@@ -205,13 +220,18 @@ class BertEncoderLayer:
         L = K.label
         with L("fwd.qkv_gemm+bias"):
             K.gemm(x, self.weight("wqkv"), b["qkv"], EPI_BIAS, bias=P["bqkv"])
-        q, k, v = (self._heads(b["qkv"], B, S, i) for i in range(3))
-        with L("fwd.scores_gemm"):
-            K.gemm(q, k, b["scores"])
-        with L("fwd.softmax"):
-            K.softmax_fwd(b["scores"], 1.0 / (c.head_dim ** 0.5), add_mask, keep_attn, ks, b["p"], b["pd"])
-        with L("fwd.ctx_gemm"):
-            K.gemm(b["pd"], v.transpose(-1, -2), self._ctx_heads(b["ctx"], B, S))
+        if self._fused(S):
+            with L("fwd.attention"):
+                K.attn_fwd(b["qkv"], B, S, c.heads, add_mask, keep_attn, ks, 1.0 / (c.head_dim ** 0.5), b["ctx"],
+                           b["lse"], b["kbits_row"], b["kbits_col"])
+        else:
+            q, k, v = (self._heads(b["qkv"], B, S, i) for i in range(3))
+            with L("fwd.scores_gemm"):
+                K.gemm(q, k, b["scores"])
+            with L("fwd.softmax"):
+                K.softmax_fwd(b["scores"], 1.0 / (c.head_dim ** 0.5), add_mask, keep_attn, ks, b["p"], b["pd"])
+            with L("fwd.ctx_gemm"):
+                K.gemm(b["pd"], v.transpose(-1, -2), self._ctx_heads(b["ctx"], B, S))
         with L("fwd.out_gemm"):
             K.gemm(b["ctx"], self.weight("wo"), b["a1"])
         with L("fwd.bdrln1"):
@@ -257,6 +277,22 @@ class BertEncoderLayer:
         with L("bwd.out_wgrad"):
             K.gemm(b["da1"].t(), b["ctx"].t(), G["wo"])
         # attention
+        if self._fused(S):
+            with L("bwd.attention"):
+                K.attn_bwd(b["qkv"], b["ctx"], b["dctx"], B, S, c.heads, add_mask, b["lse"], b["kbits_row"],
+                           b["kbits_col"], ks, 1.0 / (c.head_dim ** 0.5), b["dqkv"])
+        else:
+            self._attn_bwd_unfused(b, B, S, keep_attn, ks)
+        with L("bwd.qkv_bias_grad"):
+            K.colsum(b["dqkv"], G["bqkv"])
+        with L("bwd.qkv_dgrad+residual"):
+            K.gemm(b["dqkv"], self.weight("wqkv").t(), b["dx"], EPI_ADD, aux=b["ds1"])
+        with L("bwd.qkv_wgrad"):
+            K.gemm(b["dqkv"].t(), x.t(), G["wqkv"])
+        return b["dx"]
+
+    def _attn_bwd_unfused(self, b, B, S, keep_attn, ks):
+        c, L = self.cfg, K.label
         q, k, v = (self._heads(b["qkv"], B, S, i) for i in range(3))
         dq, dk, dv = (self._heads(b["dqkv"], B, S, i) for i in range(3))
         dctx = self._ctx_heads(b["dctx"], B, S)
@@ -270,13 +306,6 @@ class BertEncoderLayer:
             K.gemm(b["dsc"], k.transpose(-1, -2), dq)
         with L("bwd.dk_gemm"):
             K.gemm(b["dsc"].transpose(-1, -2), q.transpose(-1, -2), dk)
-        with L("bwd.qkv_bias_grad"):
-            K.colsum(b["dqkv"], G["bqkv"])
-        with L("bwd.qkv_dgrad+residual"):
-            K.gemm(b["dqkv"], self.weight("wqkv").t(), b["dx"], EPI_ADD, aux=b["ds1"])
-        with L("bwd.qkv_wgrad"):
-            K.gemm(b["dqkv"].t(), x.t(), G["wqkv"])
-        return b["dx"]
 
     def sgd_step(self, lr: float):
         with K.label("sgd_update"):

@@ -1,0 +1,837 @@
+// attn.cu — fused scaled-masked-softmax attention on the 5th-gen tensor cores.
+//
+// Replaces, for one BERT encoder layer, the chain the reference evaluates as
+// separate registry operators:
+//     S  = Einsum bsnd,btnd->bnst (Q, K)            frontend.py:408-481
+//     P  = Softmax(Div(S, divisor) + mask)          frontend.py:294, 175-188, 493-501
+//     Pd = Mul(P, dropout mask)                     frontend.py:293
+//     O  = Einsum bnst,btnd->bsnd (Pd, V)
+// and its reverse pass (Einsum VJPs autodiff.py:1363-1415, Softmax VJP
+// 1465-1484).  The reference recipe itself fuses exactly this into one
+// per-query-row map (SURVEY.md §3D kernel 4, §8f.1); here the [B,NH,S,S]
+// score / probability tensors never touch HBM.
+//
+// One CTA owns a 128-row strip (128 TMEM lanes) against all S <= 512 keys:
+// the whole fp32 score strip fits the 512 TMEM columns, so the softmax is
+// exact (two passes over TMEM: row max, then exp/sum) instead of online.
+// Warp roles (576 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
+// single-thread tcgen05.mma issuer, warps 2..17 = 16 softmax warps (four per
+// TMEM lane quadrant, each owning S/4 columns).
+//
+//   fwd    S = Q·Kᵀ (TMEM) -> P̃d = exp2(S·c·log2e + mask·log2e - max)·keep·ks
+//          written as bf16 into 128B-swizzled smem (UMMA K-major A operand)
+//          -> O = P̃d·V (TMEM, reusing S's columns) -> ctx = O / rowsum.
+//          Also writes lse (log2 domain) and the dropout keep flags packed to
+//          bits twice: row-major (for dQ) and transposed (for dK/dV, built
+//          with warp ballots) — 2 x 3.1 MB instead of re-reading 25 MB of u8
+//          keep flags in each backward kernel.
+//   bwd_dq   per 128-query strip, 128-key chunks: S and dPd = dO·Vᵀ in TMEM,
+//            dS = P∘(dPd∘M - D)·c in smem, dQ += dS·K.   D = rowsum(dO∘O).
+//   bwd_dkdv per 128-key strip, 128-query chunks: Sᵀ = K·Qᵀ, dPdᵀ = V·dOᵀ,
+//            dV += Pdᵀ·dO, dK += dSᵀ·Q.
+// No cross-CTA reductions: every output element is produced by one CTA in a
+// fixed order (bitwise reproducible, no atomics).
+#include <cuda.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace dfx {
+namespace {
+
+constexpr int DH = 64;   // head dim = one 128-byte swizzle row of bf16
+constexpr int QT = 128;  // rows per strip (TMEM lanes)
+constexpr int kSoftWarps = 16;
+constexpr int kAttnThreads = (2 + kSoftWarps) * 32;
+constexpr int kMaxSeq = 512;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int KB = 1024;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// keep flags: 4 bytes (each 0 or 1) -> 4 bits (byte k -> bit k), no carries
+__device__ __forceinline__ uint32_t keep_nibble(uint32_t w) { return (w * 0x01020408u) >> 24; }
+
+// 32x32 bit-matrix transpose across a warp: lane i holds row word r_i on
+// entry; on exit lane j holds the column word whose bit i is bit j of r_i.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const int j = 16 >> t;
+    const uint32_t m = masks[t];
+    const uint32_t o = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((o >> j) & m)) : ((x & m) | ((o & m) << j));
+  }
+  return x;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Store 8 consecutive bf16 (16 bytes) of row `r`, 16-byte chunk `ch` (0..7)
+// of a [rows x 64] K-major SWIZZLE_128B tile at `tile`.
+__device__ __forceinline__ void st_sw128(uint32_t tile, int r, int ch, uint4 v) {
+  sts128(tile + r * 128 + ((ch ^ (r & 7)) << 4), v);
+}
+
+struct AttnFwdParams {
+  int B, NH, S, H;
+  int64_t ld_ctx;
+  const float* add_mask;  // [B, S] or null
+  const uint8_t* keep;    // [B, NH, S, S] u8 or null
+  float ks;               // keep scale 1/(1-p) (1 when keep is null)
+  float sc2;              // inv_divisor * log2(e)
+  __nv_bfloat16* ctx;
+  float* lse;             // [B, NH, S], log2 domain
+  uint32_t* kb_row;       // [B, NH, S, S/32] or null
+  uint32_t* kb_col;       // [B, NH, S(key), S/32] or null
+};
+
+// shared-memory plan of the forward kernel (bytes from a 1024-aligned base)
+struct FwdSmem {
+  static constexpr int Q = 0;
+  static constexpr int K = Q + QT * 128;            // S keys x 128 B
+  static constexpr int V = K + kMaxSeq * 128;
+  static constexpr int P2 = V + kMaxSeq * 128;      // P chunks 4..7 (0..3 reuse K)
+  static constexpr int MASK = P2 + 4 * QT * 128;    // S floats
+  static constexpr int RED = MASK + kMaxSeq * 4;    // [2][4][128] floats
+  static constexpr int BAR = RED + 2 * 4 * QT * 4;  // mbarriers
+  static constexpr int TOTAL = BAR + 128 + KB;      // + alignment slack
+};
+static_assert(FwdSmem::TOTAL <= 227 * 1024, "attention forward exceeds shared memory");
+
+__device__ __forceinline__ uint32_t p_chunk(uint32_t base, int c) {
+  return c < 4 ? base + FwdSmem::K + c * (QT * 128) : base + FwdSmem::P2 + (c - 4) * (QT * 128);
+}
+
+__global__ void __launch_bounds__(kAttnThreads, 1)
+attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FwdSmem::BAR);
+  uint64_t *bar_qk = bar, *bar_v = bar + 1, *bar_s = bar + 2, *bar_p = bar + 3, *bar_o = bar + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
+  float* mask2 = reinterpret_cast<float*>(smem + FwdSmem::MASK);
+  float* red_max = reinterpret_cast<float*>(smem + FwdSmem::RED);
+  float* red_sum = red_max + 4 * QT;
+
+  const int S = p.S;
+  const int qblocks = S / QT;
+  const int qb = blockIdx.x % qblocks;
+  const int bh = blockIdx.x / qblocks;
+  const int b = bh / p.NH, h = bh % p.NH;
+  const int q0 = qb * QT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_qk, 1);
+    mbar_init(bar_v, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_p, kSoftWarps);
+    mbar_init(bar_o, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- producer
+      const int row0 = b * S;
+      mbar_expect_tx(bar_qk, (QT + S) * 128);
+      const uint32_t bqk = smem_u32(bar_qk), bv = smem_u32(bar_v);
+      tma_load_4d_cg<1>(&map_qkv, bqk, smem + FwdSmem::Q, h * DH, row0 + q0, 0, 0);
+      tma_load_4d_cg<1>(&map_qkv, bqk, smem + FwdSmem::Q + 8 * KB, h * DH, row0 + q0 + 64, 0, 0);
+      for (int j = 0; j < S / 64; ++j)
+        tma_load_4d_cg<1>(&map_qkv, bqk, smem + FwdSmem::K + j * 8 * KB, p.H + h * DH, row0 + 64 * j, 0, 0);
+      mbar_expect_tx(bar_v, S * 128);
+      for (int j = 0; j < S / 64; ++j)
+        tma_load_4d_cg<1>(&map_qkv, bv, smem + FwdSmem::V + j * 8 * KB, 2 * p.H + h * DH, row0 + 64 * j, 0, 0);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- MMA issuer
+      mbar_wait(bar_qk, 0);
+      tc_fence_after();
+      const uint32_t idesc_s = make_idesc(128, QT, 0, 0);
+      const uint64_t qdesc = make_sdesc(sbase + FwdSmem::Q, 16, 1024);
+      for (int nb = 0; nb < S / 128; ++nb) {
+        const uint64_t kdesc = make_sdesc(sbase + FwdSmem::K + nb * 16 * KB, 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          tc_mma_cg<1>(tmem + nb * 128, qdesc + 2 * kk, kdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
+      }
+      tc_commit_cg<1>(bar_s);
+      mbar_wait(bar_p, 0);
+      mbar_wait(bar_v, 0);
+      tc_fence_after();
+      const uint32_t idesc_o = make_idesc(DH, QT, 0, 1);
+      const uint64_t vdesc = make_sdesc(sbase + FwdSmem::V, 8 * KB, 1024);
+      for (int kc = 0; kc < S / 16; ++kc) {
+        const uint64_t pdesc = make_sdesc(p_chunk(sbase, kc >> 2), 16, 1024);
+        tc_mma_cg<1>(tmem, pdesc + 2 * (kc & 3), vdesc + (uint64_t)(kc * (2048 >> 4)), idesc_o, kc > 0 ? 1u : 0u);
+      }
+      tc_commit_cg<1>(bar_o);
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps
+    const int sw = warp - 2;
+    const int q = warp & 3;          // TMEM lane quadrant
+    const int part = sw >> 2;        // column quarter
+    const int cpp = S / 4;           // columns per part (<= 128)
+    const int c0 = part * cpp;
+    const int rl = q * 32 + lane;    // row within the strip
+    const int grow = q0 + rl;        // query index
+    const int st = threadIdx.x - 64; // 0..511
+    for (int i = st; i < S; i += kSoftWarps * 32)
+      mask2[i] = p.add_mask ? p.add_mask[(size_t)b * S + i] * kLog2e : 0.f;
+    // dropout keep flags of this thread's row segment, 32 bytes per chunk
+    const size_t rowoff = ((size_t)bh * S + grow) * S;
+    const uint4* kp = reinterpret_cast<const uint4*>(p.keep + rowoff + c0);
+    const uint4 ones = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    uint4 kv0 = p.keep ? __ldg(kp) : ones, kv1 = p.keep ? __ldg(kp + 1) : ones;
+    named_bar(1, kSoftWarps * 32);
+    const float4* mask4 = reinterpret_cast<const float4*>(mask2);
+    mbar_wait(bar_s, 0);
+    tc_fence_after();
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    // pass 1: row max of t = S*c*log2e + mask*log2e (TMEM load of chunk j+1
+    // in flight while chunk j is reduced)
+    float mx = -INFINITY;
+    const int nj = cpp / 32;
+    {
+      float v[2][32];
+      tmem_ld32(trow + c0, v[0]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= nj) break;
+        if (j + 1 < nj) tmem_ld32_nowait(trow + c0 + (j + 1) * 32, v[(j + 1) & 1]);
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 m = mask4[(c0 + j * 32 + i) >> 2];
+          const float* w = v[j & 1];
+          mx = fmax3(mx, fmaf(w[i], p.sc2, m.x), fmaf(w[i + 1], p.sc2, m.y));
+          mx = fmax3(mx, fmaf(w[i + 2], p.sc2, m.z), fmaf(w[i + 3], p.sc2, m.w));
+        }
+        tmem_wait_ld();
+      }
+    }
+    red_max[part * QT + rl] = mx;
+    named_bar(1, kSoftWarps * 32);
+    mx = fmaxf(fmaxf(red_max[rl], red_max[QT + rl]), fmaxf(red_max[2 * QT + rl], red_max[3 * QT + rl]));
+    // pass 2: e = exp2(t - max); rowsum; P̃d = e * keep (the 1/(1-p) scale is
+    // applied to O) -> bf16 swizzled smem; keep flags -> packed bits
+    float sum = 0.f;
+    const int words = S / 32;
+#pragma unroll 1
+    for (int j = 0; j < nj; ++j) {
+      float w[32];
+      tmem_ld32_nowait(trow + c0 + j * 32, w);
+      const uint32_t kw[8] = {kv0.x, kv0.y, kv0.z, kv0.w, kv1.x, kv1.y, kv1.z, kv1.w};
+      if (j + 1 < nj && p.keep) {  // next chunk's keep flags
+        kv0 = __ldg(kp + 2 * (j + 1));
+        kv1 = __ldg(kp + 2 * (j + 1) + 1);
+      }
+      tmem_wait_ld();
+      uint32_t pk[16];
+      uint32_t bits = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {  // 4 columns per keep word
+        const float4 m = mask4[(c0 + j * 32 + 4 * u) >> 2];
+        const float e0 = ex2(fmaf(w[4 * u], p.sc2, m.x) - mx);
+        const float e1 = ex2(fmaf(w[4 * u + 1], p.sc2, m.y) - mx);
+        const float e2 = ex2(fmaf(w[4 * u + 2], p.sc2, m.z) - mx);
+        const float e3 = ex2(fmaf(w[4 * u + 3], p.sc2, m.w) - mx);
+        sum += (e0 + e1) + (e2 + e3);
+        const uint32_t ff = kw[u] * 0xFFu;  // bytes 0x00 / 0xFF
+        pk[2 * u] = pack_bf16x2(e0, e1) & __byte_perm(ff, 0, 0x1100);
+        pk[2 * u + 1] = pack_bf16x2(e2, e3) & __byte_perm(ff, 0, 0x3322);
+        bits |= keep_nibble(kw[u]) << (4 * u);
+      }
+      const int col = c0 + j * 32;
+      const uint32_t tile = p_chunk(sbase, col >> 6);
+      const int ch0 = (col & 63) >> 3;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        st_sw128(tile, rl, ch0 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+      if (p.kb_row) {
+        p.kb_row[((size_t)bh * S + grow) * words + (col >> 5)] = bits;
+        // transposed: bit i of word [key][q/32] = keep of query (32-row group base + i)
+        const uint32_t colword = warp_transpose32(bits, lane);
+        p.kb_col[((size_t)bh * S + col + lane) * words + (grow >> 5)] = colword;
+      }
+    }
+    // P̃d complete in smem -> the MMA warp may issue O = P̃d·V (and reuse TMEM)
+    fence_async_smem();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_p);
+    red_sum[part * QT + rl] = sum;
+    named_bar(1, kSoftWarps * 32);
+    const float tot = red_sum[rl] + red_sum[QT + rl] + red_sum[2 * QT + rl] + red_sum[3 * QT + rl];
+    const float inv = p.ks / tot;
+    if (part == 0) p.lse[(size_t)bh * S + grow] = mx + __log2f(tot);
+    mbar_wait(bar_o, 0);
+    tc_fence_after();
+    float o[16];
+    tmem_ld16(trow + part * 16, o);
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = pack_bf16x2(o[2 * i] * inv, o[2 * i + 1] * inv);
+    uint4* dst = reinterpret_cast<uint4*>(p.ctx + ((size_t)b * S + grow) * p.ld_ctx + h * DH + part * 16);
+    dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// --------------------------------------------------------------------- backward
+struct AttnBwdParams {
+  int B, NH, S, H;
+  int64_t ld_ctx, ld_dqkv;
+  const __nv_bfloat16* ctx;   // O   [T, ld_ctx]
+  const __nv_bfloat16* dctx;  // dO  [T, ld_ctx]
+  const float* add_mask;      // [B, S] or null
+  const float* lse;           // [B, NH, S] log2 domain
+  float* delta;               // [B, NH, S]  D = rowsum(dO∘O) (written by dq, read by dkdv)
+  const uint32_t* kb_row;     // or null (no dropout)
+  const uint32_t* kb_col;
+  float ks, sc2, scale;       // keep scale, inv_divisor*log2e, inv_divisor
+  __nv_bfloat16* dqkv;        // [T, ld_dqkv]: dQ | dK | dV column blocks
+};
+
+constexpr int CH = 128;  // keys (dq) / queries (dkdv) per chunk
+
+struct DqSmem {
+  static constexpr int Q = 0;
+  static constexpr int DO = Q + QT * 128;
+  static constexpr int K = DO + QT * 128;
+  static constexpr int V = K + kMaxSeq * 128;
+  static constexpr int DS = V + kMaxSeq * 128;      // [128 x 128] bf16 as 2 x [128 x 64]
+  static constexpr int MASK = DS + QT * CH * 2;
+  static constexpr int RED = MASK + kMaxSeq * 4;
+  static constexpr int BAR = RED + 4 * QT * 4;
+  static constexpr int TOTAL = BAR + 256 + KB;
+};
+static_assert(DqSmem::TOTAL <= 227 * 1024, "attention dq exceeds shared memory");
+
+struct DkvSmem {
+  static constexpr int K = 0;
+  static constexpr int V = K + QT * 128;
+  static constexpr int RING = V + QT * 128;          // 2 stages x (Q_j, dO_j)
+  static constexpr int STAGE = 2 * CH * 128;
+  static constexpr int PD = RING + 2 * STAGE;
+  static constexpr int DS = PD + QT * CH * 2;
+  static constexpr int LSE = DS + QT * CH * 2;
+  static constexpr int DEL = LSE + kMaxSeq * 4;
+  static constexpr int BAR = DEL + kMaxSeq * 4;
+  static constexpr int TOTAL = BAR + 256 + KB;
+};
+static_assert(DkvSmem::TOTAL <= 227 * 1024, "attention dkdv exceeds shared memory");
+
+// Write 32 consecutive columns (col0 % 32 == 0, within a 128-column chunk) of
+// row r of a [128 x 128] bf16 operand stored as two [128 x 64] SW128 tiles.
+__device__ __forceinline__ void st_row32(uint32_t buf, int r, int col0, const uint32_t (&pk)[16]) {
+  const uint32_t tile = buf + (col0 >> 6) * (QT * 128);
+  const int ch0 = (col0 & 63) >> 3;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) st_sw128(tile, r, ch0 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+}
+
+__device__ __forceinline__ void store_bf16x16(__nv_bfloat16* g, const float (&o)[16]) {
+  uint32_t w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = pack_bf16x2(o[2 * i], o[2 * i + 1]);
+  uint4* dst = reinterpret_cast<uint4*>(g);
+  dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+__device__ __forceinline__ float dot16_bf16(const __nv_bfloat16* a, const __nv_bfloat16* b) {
+  float s = 0.f;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(a) + u), y = __ldg(reinterpret_cast<const uint4*>(b) + u);
+    const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&x);
+    const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 fx = __bfloat1622float2(hx[i]), fy = __bfloat1622float2(hy[i]);
+      s = fmaf(fx.x, fy.x, s);
+      s = fmaf(fx.y, fy.y, s);
+    }
+  }
+  return s;
+}
+
+// dQ strip: CTA = (b, h, 128-query block); loops over 128-key chunks.
+__global__ void __launch_bounds__(kAttnThreads, 1)
+attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
+                   const AttnBwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + DqSmem::BAR);
+  uint64_t *bar_q = bar, *bar_s = bar + 1, *bar_tfree = bar + 2, *bar_ds = bar + 3, *bar_dsfree = bar + 4;
+  uint64_t* bar_kv = bar + 8;  // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  float* mask2 = reinterpret_cast<float*>(smem + DqSmem::MASK);
+  float* red = reinterpret_cast<float*>(smem + DqSmem::RED);
+
+  const int S = p.S, nch = S / CH;
+  const int qb = blockIdx.x % (S / QT);
+  const int bh = blockIdx.x / (S / QT);
+  const int b = bh / p.NH, h = bh % p.NH;
+  const int q0 = qb * QT, row0 = b * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_q, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_tfree, kSoftWarps);
+    mbar_init(bar_ds, kSoftWarps);
+    mbar_init(bar_dsfree, 1);
+    for (int j = 0; j < 4; ++j) mbar_init(&bar_kv[j], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t T_S = 0, T_DP = 128, T_DQ = 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(bar_q, 2 * QT * 128);
+      const uint32_t bq = smem_u32(bar_q);
+      for (int u = 0; u < 2; ++u) {
+        tma_load_4d_cg<1>(&map_qkv, bq, smem + DqSmem::Q + u * 8 * KB, h * DH, row0 + q0 + 64 * u, 0, 0);
+        tma_load_4d_cg<1>(&map_do, bq, smem + DqSmem::DO + u * 8 * KB, h * DH, row0 + q0 + 64 * u, 0, 0);
+      }
+      for (int j = 0; j < nch; ++j) {
+        mbar_expect_tx(&bar_kv[j], 2 * CH * 128);
+        const uint32_t bk = smem_u32(&bar_kv[j]);
+        for (int u = 0; u < 2; ++u) {
+          const int r = row0 + j * CH + 64 * u;
+          tma_load_4d_cg<1>(&map_qkv, bk, smem + DqSmem::K + (j * 2 + u) * 8 * KB, p.H + h * DH, r, 0, 0);
+          tma_load_4d_cg<1>(&map_qkv, bk, smem + DqSmem::V + (j * 2 + u) * 8 * KB, 2 * p.H + h * DH, r, 0, 0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc_s = make_idesc(CH, QT, 0, 0);
+      const uint32_t idesc_q = make_idesc(DH, QT, 0, 1);
+      const uint64_t qdesc = make_sdesc(sbase + DqSmem::Q, 16, 1024);
+      const uint64_t dodesc = make_sdesc(sbase + DqSmem::DO, 16, 1024);
+      mbar_wait(bar_q, 0);
+      tc_fence_after();
+      auto issue_dq = [&](int j) {  // dQ += dS_j · K_j   (K_j read MN-major)
+        mbar_wait(bar_ds, j & 1);
+        tc_fence_after();
+        const uint64_t kdesc = make_sdesc(sbase + DqSmem::K + j * 16 * KB, 8 * KB, 1024);
+#pragma unroll
+        for (int kc = 0; kc < CH / 16; ++kc) {
+          const uint64_t adesc = make_sdesc(sbase + DqSmem::DS + (kc >> 2) * 16 * KB, 16, 1024);
+          tc_mma_cg<1>(tmem + T_DQ, adesc + 2 * (kc & 3), kdesc + (uint64_t)(kc * (2048 >> 4)), idesc_q,
+                       (j > 0 || kc > 0) ? 1u : 0u);
+        }
+        tc_commit_cg<1>(bar_dsfree);
+      };
+      for (int j = 0; j < nch; ++j) {
+        mbar_wait(&bar_kv[j], 0);
+        if (j > 0) mbar_wait(bar_tfree, (j - 1) & 1);
+        tc_fence_after();
+        const uint64_t kdesc = make_sdesc(sbase + DqSmem::K + j * 16 * KB, 16, 1024);
+        const uint64_t vdesc = make_sdesc(sbase + DqSmem::V + j * 16 * KB, 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          tc_mma_cg<1>(tmem + T_S, qdesc + 2 * kk, kdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
+          tc_mma_cg<1>(tmem + T_DP, dodesc + 2 * kk, vdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        tc_commit_cg<1>(bar_s);
+        if (j > 0) issue_dq(j - 1);
+      }
+      issue_dq(nch - 1);
+    }
+  } else {
+    const int sw = warp - 2, q = warp & 3, part = sw >> 2;
+    const int rl = q * 32 + lane, grow = q0 + rl;
+    const int st = threadIdx.x - 64;
+    const size_t rowi = (size_t)bh * S + grow;
+    for (int i = st; i < S; i += kSoftWarps * 32)
+      mask2[i] = p.add_mask ? p.add_mask[(size_t)b * S + i] * kLog2e : 0.f;
+    // D = rowsum(dO ∘ O): each of the 4 warps of a quadrant sums 16 of the 64
+    const size_t goff = (size_t)(row0 + grow) * p.ld_ctx + h * DH + part * 16;
+    red[part * QT + rl] = dot16_bf16(p.dctx + goff, p.ctx + goff);
+    const float lse_c = p.lse[rowi] - __log2f(p.scale);  // folds the 1/divisor into P
+    named_bar(1, kSoftWarps * 32);
+    const float D = red[rl] + red[QT + rl] + red[2 * QT + rl] + red[3 * QT + rl];
+    if (part == 0) p.delta[rowi] = D;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const int words = S / 32;
+    for (int j = 0; j < nch; ++j) {
+      mbar_wait(bar_s, j & 1);
+      tc_fence_after();
+      float s[32], dp[32];
+      tmem_ld32(trow + T_S + part * 32, s);
+      tmem_ld32(trow + T_DP + part * 32, dp);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_tfree);
+      const int key0 = j * CH + part * 32;
+      const uint32_t bits = p.kb_row ? p.kb_row[rowi * words + (key0 >> 5)] : 0xFFFFFFFFu;
+      const float4* m4 = reinterpret_cast<const float4*>(mask2 + key0);
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 m = m4[i >> 2];
+        const float mm[4] = {m.x, m.y, m.z, m.w};
+        float d[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          // P' = scale * P ; dS = P' * (dPd * keep * ks - D)
+          const float P = ex2(fmaf(s[i + e], p.sc2, mm[e]) - lse_c);
+          d[e] = P * (((bits >> (i + e)) & 1u) ? fmaf(dp[i + e], p.ks, -D) : -D);
+        }
+        pk[i >> 1] = pack_bf16x2(d[0], d[1]);
+        pk[(i >> 1) + 1] = pack_bf16x2(d[2], d[3]);
+      }
+      if (j > 0) mbar_wait(bar_dsfree, (j - 1) & 1);
+      st_row32(sbase + DqSmem::DS, rl, part * 32, pk);
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_ds);
+    }
+    mbar_wait(bar_dsfree, (nch - 1) & 1);
+    tc_fence_after();
+    float o[16];
+    tmem_ld16(trow + T_DQ + part * 16, o);
+    store_bf16x16(p.dqkv + (size_t)(row0 + grow) * p.ld_dqkv + h * DH + part * 16, o);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// dK / dV strip: CTA = (b, h, 128-key block); loops over 128-query chunks.
+__global__ void __launch_bounds__(kAttnThreads, 1)
+attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
+                     const AttnBwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + DkvSmem::BAR);
+  uint64_t *bar_a = bar, *bar_s = bar + 1, *bar_tfree = bar + 2, *bar_pds = bar + 3, *bar_pdsfree = bar + 4;
+  uint64_t* full = bar + 8;    // [2]
+  uint64_t* empty = bar + 10;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  float* lse_s = reinterpret_cast<float*>(smem + DkvSmem::LSE);
+  float* del_s = reinterpret_cast<float*>(smem + DkvSmem::DEL);
+
+  const int S = p.S, nch = S / CH;
+  const int kb = blockIdx.x % (S / QT);
+  const int bh = blockIdx.x / (S / QT);
+  const int b = bh / p.NH, h = bh % p.NH;
+  const int k0 = kb * QT, row0 = b * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_a, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_tfree, kSoftWarps);
+    mbar_init(bar_pds, kSoftWarps);
+    mbar_init(bar_pdsfree, 1);
+    for (int s = 0; s < 2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t T_S = 0, T_DP = 128, T_DK = 256, T_DV = 320;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(bar_a, 2 * QT * 128);
+      const uint32_t ba = smem_u32(bar_a);
+      for (int u = 0; u < 2; ++u) {
+        tma_load_4d_cg<1>(&map_qkv, ba, smem + DkvSmem::K + u * 8 * KB, p.H + h * DH, row0 + k0 + 64 * u, 0, 0);
+        tma_load_4d_cg<1>(&map_qkv, ba, smem + DkvSmem::V + u * 8 * KB, 2 * p.H + h * DH, row0 + k0 + 64 * u, 0, 0);
+      }
+      for (int j = 0; j < nch; ++j) {
+        const int s = j & 1;
+        mbar_wait(&empty[s], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&full[s], DkvSmem::STAGE);
+        const uint32_t bf = smem_u32(&full[s]);
+        uint8_t* stq = smem + DkvSmem::RING + s * DkvSmem::STAGE;
+        for (int u = 0; u < 2; ++u) {
+          tma_load_4d_cg<1>(&map_qkv, bf, stq + u * 8 * KB, h * DH, row0 + j * CH + 64 * u, 0, 0);
+          tma_load_4d_cg<1>(&map_do, bf, stq + CH * 128 + u * 8 * KB, h * DH, row0 + j * CH + 64 * u, 0, 0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc_s = make_idesc(CH, QT, 0, 0);
+      const uint32_t idesc_g = make_idesc(DH, QT, 0, 1);
+      const uint64_t kdesc = make_sdesc(sbase + DkvSmem::K, 16, 1024);
+      const uint64_t vdesc = make_sdesc(sbase + DkvSmem::V, 16, 1024);
+      mbar_wait(bar_a, 0);
+      auto issue_grads = [&](int j) {  // dV += Pdᵀ·dO_j ; dK += dSᵀ·Q_j   (B operands MN-major)
+        mbar_wait(bar_pds, j & 1);
+        tc_fence_after();
+        const uint32_t stq = sbase + DkvSmem::RING + (j & 1) * DkvSmem::STAGE;
+        const uint64_t qmn = make_sdesc(stq, 8 * KB, 1024);
+        const uint64_t domn = make_sdesc(stq + CH * 128, 8 * KB, 1024);
+#pragma unroll
+        for (int kc = 0; kc < CH / 16; ++kc) {
+          const uint64_t pd = make_sdesc(sbase + DkvSmem::PD + (kc >> 2) * 16 * KB, 16, 1024);
+          const uint64_t ds = make_sdesc(sbase + DkvSmem::DS + (kc >> 2) * 16 * KB, 16, 1024);
+          const uint32_t acc = (j > 0 || kc > 0) ? 1u : 0u;
+          tc_mma_cg<1>(tmem + T_DV, pd + 2 * (kc & 3), domn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
+          tc_mma_cg<1>(tmem + T_DK, ds + 2 * (kc & 3), qmn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
+        }
+        tc_commit_cg<1>(&empty[j & 1]);
+        tc_commit_cg<1>(bar_pdsfree);
+      };
+      for (int j = 0; j < nch; ++j) {
+        mbar_wait(&full[j & 1], (j >> 1) & 1);
+        if (j > 0) mbar_wait(bar_tfree, (j - 1) & 1);
+        tc_fence_after();
+        const uint32_t stq = sbase + DkvSmem::RING + (j & 1) * DkvSmem::STAGE;
+        const uint64_t qdesc = make_sdesc(stq, 16, 1024);
+        const uint64_t dodesc = make_sdesc(stq + CH * 128, 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          tc_mma_cg<1>(tmem + T_S, kdesc + 2 * kk, qdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
+          tc_mma_cg<1>(tmem + T_DP, vdesc + 2 * kk, dodesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        tc_commit_cg<1>(bar_s);
+        if (j > 0) issue_grads(j - 1);
+      }
+      issue_grads(nch - 1);
+    }
+  } else {
+    const int sw = warp - 2, q = warp & 3, part = sw >> 2;
+    const int rl = q * 32 + lane, key = k0 + rl;
+    const int st = threadIdx.x - 64;
+    const float lsc = __log2f(p.scale);
+    for (int i = st; i < S; i += kSoftWarps * 32) {
+      lse_s[i] = p.lse[(size_t)bh * S + i] - lsc;  // P' = P / divisor
+      del_s[i] = p.delta[(size_t)bh * S + i];
+    }
+    const float mrow = p.add_mask ? p.add_mask[(size_t)b * S + key] * kLog2e : 0.f;
+    named_bar(1, kSoftWarps * 32);
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const int words = S / 32;
+    const size_t keyi = (size_t)bh * S + key;
+    for (int j = 0; j < nch; ++j) {
+      mbar_wait(bar_s, j & 1);
+      tc_fence_after();
+      float s[32], dp[32];
+      tmem_ld32(trow + T_S + part * 32, s);
+      tmem_ld32(trow + T_DP + part * 32, dp);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_tfree);
+      const int qc0 = j * CH + part * 32;
+      const uint32_t bits = p.kb_col ? p.kb_col[keyi * words + (qc0 >> 5)] : 0xFFFFFFFFu;
+      const float4* l4 = reinterpret_cast<const float4*>(lse_s + qc0);
+      const float4* d4 = reinterpret_cast<const float4*>(del_s + qc0);
+      uint32_t pkp[16], pks[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 l = l4[i >> 2], dd = d4[i >> 2];
+        const float ll[4] = {l.x, l.y, l.z, l.w}, DD[4] = {dd.x, dd.y, dd.z, dd.w};
+        float pd[4], ds[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          // P' = P / divisor; Pd' = P' * keep (dV is rescaled by ks * divisor);
+          // dS = P' * (dPd * keep * ks - D)
+          const float P = ex2(fmaf(s[i + e], p.sc2, mrow) - ll[e]);
+          const bool kept = (bits >> (i + e)) & 1u;
+          pd[e] = kept ? P : 0.f;
+          ds[e] = P * (kept ? fmaf(dp[i + e], p.ks, -DD[e]) : -DD[e]);
+        }
+        pkp[i >> 1] = pack_bf16x2(pd[0], pd[1]);
+        pkp[(i >> 1) + 1] = pack_bf16x2(pd[2], pd[3]);
+        pks[i >> 1] = pack_bf16x2(ds[0], ds[1]);
+        pks[(i >> 1) + 1] = pack_bf16x2(ds[2], ds[3]);
+      }
+      if (j > 0) mbar_wait(bar_pdsfree, (j - 1) & 1);
+      st_row32(sbase + DkvSmem::PD, rl, part * 32, pkp);
+      st_row32(sbase + DkvSmem::DS, rl, part * 32, pks);
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_pds);
+    }
+    mbar_wait(bar_pdsfree, (nch - 1) & 1);
+    tc_fence_after();
+    float o[16];
+    __nv_bfloat16* grow_ptr = p.dqkv + (size_t)(row0 + key) * p.ld_dqkv + h * DH + part * 16;
+    tmem_ld16(trow + T_DK + part * 16, o);
+    store_bf16x16(grow_ptr + p.H, o);
+    tmem_ld16(trow + T_DV + part * 16, o);
+    const float dvs = p.ks / p.scale;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i] *= dvs;
+    store_bf16x16(grow_ptr + 2 * p.H, o);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+int check_common(int64_t B, int64_t NH, int64_t S, int64_t dh, const void* qkv, int64_t ld_qkv) {
+  DFX_REQUIRE(B >= 1 && NH >= 1, DFX_ERR_SHAPE, "dfx_attn: batch and heads must be >= 1");
+  DFX_REQUIRE(dh == DH, DFX_ERR_UNSUPPORTED, "dfx_attn: head_dim must be 64");
+  DFX_REQUIRE(S >= 128 && S <= kMaxSeq && S % 128 == 0, DFX_ERR_UNSUPPORTED,
+              "dfx_attn: seq must be a multiple of 128 in [128, 512]");
+  DFX_REQUIRE(ld_qkv >= 3 * NH * DH && ld_qkv % 8 == 0, DFX_ERR_SHAPE, "dfx_attn: ld_qkv must be >= 3*H, %8");
+  DFX_REQUIRE(aligned16(qkv), DFX_ERR_ALIGN, "dfx_attn: qkv must be 16-byte aligned");
+  return DFX_OK;
+}
+
+}  // namespace
+}  // namespace dfx
+
+using namespace dfx;
+
+extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t head_dim, const void* qkv,
+                            int64_t ld_qkv, const float* add_mask, const uint8_t* keep, float keep_scale,
+                            float inv_divisor, void* ctx, int64_t ld_ctx, float* lse, uint32_t* keep_bits_row,
+                            uint32_t* keep_bits_col, void* stream) {
+  int rc = check_common(batch, heads, seq, head_dim, qkv, ld_qkv);
+  if (rc) return rc;
+  DFX_REQUIRE(ctx && lse, DFX_ERR_SHAPE, "dfx_attn_fwd: ctx and lse are required");
+  DFX_REQUIRE(ld_ctx >= heads * DH && ld_ctx % 8 == 0 && aligned16(ctx), DFX_ERR_ALIGN,
+              "dfx_attn_fwd: ctx rows must be 16-byte aligned, ld >= H");
+  DFX_REQUIRE(!keep || aligned16(keep), DFX_ERR_ALIGN, "dfx_attn_fwd: keep must be 16-byte aligned");
+  DFX_REQUIRE((keep_bits_row == nullptr) == (keep_bits_col == nullptr), DFX_ERR_SHAPE,
+              "dfx_attn_fwd: pass both packed keep-bit outputs or neither");
+  DFX_REQUIRE(!keep_bits_row || keep, DFX_ERR_SHAPE, "dfx_attn_fwd: keep bits need keep flags");
+  CUtensorMap map;
+  const int64_t T = batch * seq;
+  rc = make_map(&map, qkv, 2, (uint64_t)ld_qkv, (uint64_t)T, ld_qkv, 1, 0, 1, 0, 64, 64, true);
+  if (rc) return rc;
+  AttnFwdParams p;
+  p.B = (int)batch; p.NH = (int)heads; p.S = (int)seq; p.H = (int)(heads * DH);
+  p.ld_ctx = ld_ctx;
+  p.add_mask = add_mask;
+  p.keep = keep;
+  p.ks = keep ? keep_scale : 1.f;
+  p.sc2 = inv_divisor * kLog2e;
+  p.ctx = reinterpret_cast<__nv_bfloat16*>(ctx);
+  p.lse = lse;
+  p.kb_row = keep_bits_row;
+  p.kb_col = keep_bits_col;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem::TOTAL);
+    attr = true;
+  }
+  const int grid = (int)(batch * heads * (seq / QT));
+  attn_fwd_kernel<<<grid, kAttnThreads, FwdSmem::TOTAL, as_stream(stream)>>>(map, p);
+  DFX_LAUNCH_CHECK("dfx_attn_fwd");
+  return DFX_OK;
+}
+
+extern "C" size_t dfx_attn_bwd_workspace(int64_t batch, int64_t heads, int64_t seq) {
+  return (size_t)(batch * heads * seq) * sizeof(float) + 256;
+}
+
+extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t head_dim, const void* qkv,
+                            int64_t ld_qkv, const void* ctx, const void* dctx, int64_t ld_ctx, const float* add_mask,
+                            const float* lse, const uint32_t* keep_bits_row, const uint32_t* keep_bits_col,
+                            float keep_scale, float inv_divisor, void* dqkv, int64_t ld_dqkv, void* workspace,
+                            size_t ws_bytes, void* stream) {
+  int rc = check_common(batch, heads, seq, head_dim, qkv, ld_qkv);
+  if (rc) return rc;
+  DFX_REQUIRE(ctx && dctx && lse && dqkv, DFX_ERR_SHAPE, "dfx_attn_bwd: ctx, dctx, lse, dqkv are required");
+  DFX_REQUIRE(ld_ctx >= heads * DH && ld_ctx % 8 == 0 && aligned16(ctx) && aligned16(dctx), DFX_ERR_ALIGN,
+              "dfx_attn_bwd: ctx/dctx rows must be 16-byte aligned, ld >= H");
+  DFX_REQUIRE(ld_dqkv >= 3 * heads * DH && ld_dqkv % 8 == 0 && aligned16(dqkv), DFX_ERR_ALIGN,
+              "dfx_attn_bwd: dqkv rows must be 16-byte aligned, ld >= 3H");
+  DFX_REQUIRE((keep_bits_row == nullptr) == (keep_bits_col == nullptr), DFX_ERR_SHAPE,
+              "dfx_attn_bwd: pass both packed keep-bit tensors or neither");
+  DFX_REQUIRE(workspace && ws_bytes >= dfx_attn_bwd_workspace(batch, heads, seq) && aligned16(workspace),
+              DFX_ERR_WORKSPACE, "dfx_attn_bwd: needs dfx_attn_bwd_workspace() bytes of workspace");
+  const int64_t T = batch * seq;
+  CUtensorMap mqkv, mdo;
+  rc = make_map(&mqkv, qkv, 2, (uint64_t)ld_qkv, (uint64_t)T, ld_qkv, 1, 0, 1, 0, 64, 64, true);
+  if (rc) return rc;
+  rc = make_map(&mdo, dctx, 2, (uint64_t)ld_ctx, (uint64_t)T, ld_ctx, 1, 0, 1, 0, 64, 64, true);
+  if (rc) return rc;
+  AttnBwdParams p;
+  p.B = (int)batch; p.NH = (int)heads; p.S = (int)seq; p.H = (int)(heads * DH);
+  p.ld_ctx = ld_ctx; p.ld_dqkv = ld_dqkv;
+  p.ctx = reinterpret_cast<const __nv_bfloat16*>(ctx);
+  p.dctx = reinterpret_cast<const __nv_bfloat16*>(dctx);
+  p.add_mask = add_mask; p.lse = lse;
+  p.delta = reinterpret_cast<float*>(workspace);
+  p.kb_row = keep_bits_row; p.kb_col = keep_bits_col;
+  p.ks = keep_bits_row ? keep_scale : 1.f;
+  p.sc2 = inv_divisor * kLog2e;
+  p.scale = inv_divisor;
+  p.dqkv = reinterpret_cast<__nv_bfloat16*>(dqkv);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem::TOTAL);
+    cudaFuncSetAttribute(attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvSmem::TOTAL);
+    attr = true;
+  }
+  const int grid = (int)(batch * heads * (seq / QT));
+  attn_bwd_dq_kernel<<<grid, kAttnThreads, DqSmem::TOTAL, as_stream(stream)>>>(mqkv, mdo, p);
+  DFX_LAUNCH_CHECK("dfx_attn_bwd (dq)");
+  attn_bwd_dkdv_kernel<<<grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream)>>>(mqkv, mdo, p);
+  DFX_LAUNCH_CHECK("dfx_attn_bwd (dk, dv)");
+  return DFX_OK;
+}

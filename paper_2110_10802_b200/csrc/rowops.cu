@@ -32,7 +32,7 @@ template <> struct VecWidth<float> { static constexpr int value = 4; };
 // bias + dropout + residual + LayerNorm
 
 template <typename T, int V, int NCH, int ACT = 0>
-__global__ void __launch_bounds__(256) bdrln_fwd_kernel(
+__global__ void __launch_bounds__(256, 4) bdrln_fwd_kernel(
     int64_t rows, int cols, const T* __restrict__ h, const float* __restrict__ bias,
     const uint8_t* __restrict__ keep, float ks, const T* __restrict__ res,
     const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
@@ -41,27 +41,8 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvec = cols / V;
   const float inv_n = 1.f / (float)cols;
-  // the lane's parameter columns stay in registers across all its rows
-  float pb[NCH][V], pg[NCH][V], pbt[NCH][V];
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    const int vi = lane + c * 32;
-#pragma unroll
-    for (int i = 0; i < V; ++i) { pb[c][i] = 0.f; pg[c][i] = 0.f; pbt[c][i] = 0.f; }
-    if (vi < nvec) {
-      Vec<float, V> g, bt;
-      g.load(gamma + vi * V);
-      bt.load(beta + vi * V);
-#pragma unroll
-      for (int i = 0; i < V; ++i) { pg[c][i] = g.v[i]; pbt[c][i] = bt.v[i]; }
-      if (bias) {
-        Vec<float, V> bv;
-        bv.load(bias + vi * V);
-#pragma unroll
-        for (int i = 0; i < V; ++i) pb[c][i] = bv.v[i];
-      }
-    }
-  }
+  // gamma/beta/bias are re-read per row (L1-resident): holding them in
+  // registers would cap occupancy below one wave of row-warps
   for (int64_t row = (int64_t)blockIdx.x * kWarps + warp; row < rows; row += (int64_t)gridDim.x * kWarps) {
     const size_t base = (size_t)row * cols;
     float x[NCH][V];
@@ -73,6 +54,16 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
         const int col = vi * V;
         Vec<T, V> hv;
         hv.load(h + base + col);
+        float pb[V];
+        if (bias) {
+          Vec<float, V> bv;
+          bv.load(bias + col);
+#pragma unroll
+          for (int i = 0; i < V; ++i) pb[i] = bv.v[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) pb[i] = 0.f;
+        }
         float m[V], r[V];
         if (keep) load_keep<V>(keep + base + col, ks, m);
         else {
@@ -88,7 +79,7 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
         }
 #pragma unroll
         for (int i = 0; i < V; ++i) {
-          x[c][i] = (hv.v[i] + pb[c][i]) * m[i] + r[i];
+          x[c][i] = (hv.v[i] + pb[i]) * m[i] + r[i];
           sum += x[c][i];
         }
       } else {
@@ -117,10 +108,13 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
           for (int i = 0; i < V; ++i) sv.v[i] = x[c][i];
           sv.store(s_out + base + col);
         }
+        Vec<float, V> gv, btv;
+        gv.load(gamma + col);
+        btv.load(beta + col);
         Vec<T, V> yv;
 #pragma unroll
         for (int i = 0; i < V; ++i) {
-          const float u = (x[c][i] - mu) * rstd * pg[c][i] + pbt[c][i];
+          const float u = (x[c][i] - mu) * rstd * gv.v[i] + btv.v[i];
           yv.v[i] = ACT ? u * sigmoid_f(u) : u;
         }
         yv.store(y + base + col);
@@ -270,14 +264,159 @@ __global__ void __launch_bounds__(256, 2) bdrln_bwd_kernel(
   block_colsum_store<V, NCH>(acc_h, cols, red, part_h);
 }
 
+
+// One-wave variant (bf16, rows <= 16 * kMaxColBlocks — the BERT C2 shape):
+// every warp owns exactly ONE row, so all rows are in flight at once (the
+// grid-stride kernel above is latency-bound there), and nothing is carried
+// across rows.  The row stays in registers as raw bf16 (24 registers for s
+// and dy at 768 columns) and is unpacked on each use, which keeps the kernel
+// at 64 registers = 2 CTAs x 16 warps per SM without spills.  The CTA's 16
+// rows are reduced per column in a fixed order through shared memory, one
+// quantity at a time (dbias, dgamma, dbeta partials).
+__device__ __forceinline__ void bf8(const uint4& r, float (&f)[8]) {
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
+    int64_t rows, int cols, const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ s,
+    const float* __restrict__ gamma, const uint8_t* __restrict__ keep, float ks, float eps,
+    __nv_bfloat16* __restrict__ ds_out, __nv_bfloat16* __restrict__ dh_out, float* __restrict__ part /*[3][grid][cols]*/) {
+  constexpr int V = 8;
+  extern __shared__ float red[];  // [16][cols]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nvec = cols / V;
+  const float inv_n = 1.f / (float)cols;
+  const int64_t row = (int64_t)blockIdx.x * 16 + warp;
+  const bool valid = row < rows;
+  const size_t base = (size_t)(valid ? row : 0) * cols;
+  uint4 sr[NCH], dr[NCH];
+  uint2 kr[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    const bool on = valid && vi < nvec;
+    sr[c] = on ? *reinterpret_cast<const uint4*>(s + base + vi * V) : make_uint4(0, 0, 0, 0);
+    dr[c] = on ? *reinterpret_cast<const uint4*>(dy + base + vi * V) : make_uint4(0, 0, 0, 0);
+    kr[c] = (on && keep) ? *reinterpret_cast<const uint2*>(keep + base + vi * V) : make_uint2(0x01010101u, 0x01010101u);
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    float x[8];
+    bf8(sr[c], x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sum += x[i];
+  }
+  const float mu = warp_sum(sum) * inv_n;
+  float sq = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (lane + c * 32 < nvec) {
+      float x[8];
+      bf8(sr[c], x);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { const float d = x[i] - mu; sq += d * d; }
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(sq) * inv_n + eps);
+  float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      Vec<float, V> gv;
+      gv.load(gamma + vi * V);
+      float x[8], g[8];
+      bf8(sr[c], x);
+      bf8(dr[c], g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float dyg = g[i] * gv.v[i];
+        m1 += dyg;
+        m2 += dyg * (x[i] - mu) * rstd;
+      }
+    }
+  }
+  m1 = warp_sum(m1) * inv_n;
+  m2 = warp_sum(m2) * inv_n;
+  const int64_t nparts = gridDim.x;
+  // ds, dh -> HBM; dh (the dbias contribution) also -> the reduction buffer
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      const int col = vi * V;
+      Vec<float, V> dhv;
+      Vec<float, V> gv;
+      gv.load(gamma + col);
+      float x[8], g[8];
+      bf8(sr[c], x);
+      bf8(dr[c], g);
+      const uint32_t kw[2] = {kr[c].x, kr[c].y};
+      Vec<__nv_bfloat16, V> dsv, dhs;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float dsi = rstd * (g[i] * gv.v[i] - m1 - (x[i] - mu) * rstd * m2);
+        dsv.v[i] = dsi;
+        dhv.v[i] = ((kw[i >> 2] >> (8 * (i & 3))) & 0xFFu) ? dsi * ks : 0.f;
+        dhs.v[i] = dhv.v[i];
+      }
+      if (valid) {
+        if (ds_out) dsv.store(ds_out + base + col);
+        if (dh_out) dhs.store(dh_out + base + col);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dhv.v[i] = 0.f;
+      }
+      dhv.store(red + warp * cols + col);
+    }
+  }
+  // column partials of the CTA's 16 rows in fixed order: dbias (staged
+  // above), then dgamma (dy * xhat), then dbeta (dy)
+#pragma unroll 1
+  for (int step = 0; step < 3; ++step) {
+    const int q = step == 0 ? 2 : step - 1;
+    if (step > 0) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const int vi = lane + c * 32;
+        if (vi < nvec) {
+          float x[8], g[8];
+          bf8(sr[c], x);
+          bf8(dr[c], g);
+          Vec<float, V> v;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v.v[i] = q == 0 ? g[i] * (x[i] - mu) * rstd : g[i];
+          v.store(red + warp * cols + vi * V);
+        }
+      }
+    }
+    __syncthreads();
+    for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 16; ++w) t += red[w * cols + col];
+      part[((size_t)q * nparts + blockIdx.x) * cols + col] = t;
+    }
+    __syncthreads();
+  }
+}
+
 // out_q[col] (+)= sum_b part[q][b][col] for q = blockIdx.y.  Warp w sums
 // partial rows b = w, w+8, ... for 32 consecutive columns (coalesced), then
 // the 8 warp sums are added in fixed order: deterministic.
-__global__ void __launch_bounds__(256) finalize_colsum_kernel(int nparts, int cols,
+constexpr int kFinWarps = 16;
+__global__ void __launch_bounds__(kFinWarps * 32) finalize_colsum_kernel(int nparts, int cols,
                                                               const float* __restrict__ part,
                                                               float* out0, float* out1, float* out2,
                                                               int accumulate) {
-  __shared__ float red[kWarps][33];
+  __shared__ float red[kFinWarps][33];
   const int q = blockIdx.y;
   float* out = q == 0 ? out0 : (q == 1 ? out1 : out2);
   if (out == nullptr) return;
@@ -286,15 +425,15 @@ __global__ void __launch_bounds__(256) finalize_colsum_kernel(int nparts, int co
   const int col = blockIdx.x * 32 + lane;
   float s = 0.f;
   if (col < cols) {
-#pragma unroll 4
-    for (int b = warp; b < nparts; b += kWarps) s += pq[(size_t)b * cols + col];
+#pragma unroll 8
+    for (int b = warp; b < nparts; b += kFinWarps) s += pq[(size_t)b * cols + col];
   }
   red[warp][lane] = s;
   __syncthreads();
   if (warp == 0 && col < cols) {
     float t = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) t += red[w][lane];
+    for (int w = 0; w < kFinWarps; ++w) t += red[w][lane];
     out[col] = accumulate ? out[col] + t : t;
   }
 }
@@ -610,20 +749,41 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
   if (int rc = check_row_shape<T, V>(cols, "dfx_bdrln_bwd")) return rc;
   if (rows == 0) return DFX_OK;
   const int nch = pick_nch((int)(cols / V));
-  const int grid = grid_for(rows, kWarps, kMaxColBlocks);
+  const bool wave = sizeof(T) == 2 && act == 0 && rows <= 16 * (int64_t)kMaxColBlocks && nch <= 3;
+  const int grid = wave ? (int)((rows + 15) / 16) : grid_for(rows, kWarps, kMaxColBlocks);
   const size_t need = 3 * (size_t)grid * cols * sizeof(float);
   DFX_REQUIRE(ws_bytes >= need, DFX_ERR_WORKSPACE, "dfx_bdrln_bwd: workspace too small");
   float* pg = (float*)ws;
   float* pb = pg + (size_t)grid * cols;
   float* ph = pb + (size_t)grid * cols;
+  int rc;
+  if (wave) {
+    const size_t wsm = (size_t)16 * cols * sizeof(float);
+#define LW(N)                                                                                      \
+  if (nch == N) {                                                                                  \
+    auto kfn = bdrln_bwd_wave_kernel<N>;                                                           \
+    if (wsm > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm); \
+    kfn<<<grid, 512, wsm, st>>>(rows, (int)cols, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)s, gamma, keep, \
+                                ks, eps, (__nv_bfloat16*)ds, (__nv_bfloat16*)dh, pg);              \
+  }
+    LW(1) LW(2) LW(3)
+#undef LW
+    DFX_LAUNCH_CHECK("dfx_bdrln_bwd");
+    if (dgamma || dbeta || dbias) {
+      finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 3), kFinWarps * 32, 0, st>>>(grid, (int)cols, pg,
+                                                                                      dgamma, dbeta, dbias, 0);
+      DFX_LAUNCH_CHECK("dfx_bdrln_bwd finalize");
+    }
+    return DFX_OK;
+  }
   const size_t smem = (size_t)kWarps * cols * sizeof(float);
-  int rc = act ? bdrln_bwd_launch<T, V, 1>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, ks, eps, ds, dh,
+  rc = act ? bdrln_bwd_launch<T, V, 1>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, ks, eps, ds, dh,
                                         pg, pb, ph, st)
                : bdrln_bwd_launch<T, V, 0>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, ks, eps, ds, dh,
                                         pg, pb, ph, st);
   if (rc) return rc;
   if (dgamma || dbeta || dbias) {
-    finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 3), 256, 0, st>>>(grid, (int)cols, pg, dgamma,
+    finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 3), kFinWarps * 32, 0, st>>>(grid, (int)cols, pg, dgamma,
                                                                                dbeta, dbias, 0);
     DFX_LAUNCH_CHECK("dfx_bdrln_bwd finalize");
   }
@@ -692,7 +852,7 @@ int colsum_t(int64_t rows, int64_t cols, const void* x, int64_t ld, float* out, 
               "dfx_colsum: workspace too small");
   colsum_kernel<T, V><<<dim3(gx, gy), 256, 0, st>>>(rows, (int)cols, ld, (const T*)x, (float*)ws);
   DFX_LAUNCH_CHECK("dfx_colsum");
-  finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 1), 256, 0, st>>>(gy, (int)cols, (const float*)ws, out,
+  finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 1), kFinWarps * 32, 0, st>>>(gy, (int)cols, (const float*)ws, out,
                                                                               nullptr, nullptr, accumulate);
   DFX_LAUNCH_CHECK("dfx_colsum finalize");
   return DFX_OK;

@@ -253,6 +253,46 @@ def softmax_bwd(dpd, p, keep, keep_scale, inv_divisor, out=None):
 
 
 # ---------------------------------------------------------------------------
+# fused attention (QKᵀ -> scale + mask -> softmax -> dropout -> PV)
+
+
+def attn_fwd(qkv, B, S, heads, add_mask, keep, keep_scale, inv_divisor, ctx, lse, kbits_row=None,
+             kbits_col=None):
+    """qkv bf16 [B*S, >=3H] (Q|K|V blocks); ctx bf16 [B*S, >=H]; lse f32 [B, NH, S];
+    keep u8 [B, NH, S, S] or None; kbits_* int32 [B, NH, S, S/32] (packed keep flags)."""
+    if qkv.dtype != torch.bfloat16 or ctx.dtype != torch.bfloat16:
+        raise ShapeError("attn_fwd: qkv and ctx must be bfloat16")
+    if qkv.stride(1) != 1 or ctx.stride(1) != 1:
+        raise ShapeError("attn_fwd: qkv/ctx rows must be contiguous")
+    if add_mask is not None and (add_mask.dtype != torch.float32 or add_mask.numel() != B * S):
+        raise ShapeError("attn_fwd: add_mask must be f32 with B*S elements")
+    flops = 4.0 * B * heads * S * S * 64
+    with _span("attn_fwd", "tensor", lambda: flops):
+        _lib.call("dfx_attn_fwd", B, heads, S, 64, qkv.data_ptr(), qkv.stride(0), _ptr(add_mask),
+                  _ptr(None if keep is None else _u8(keep, B * heads * S * S, "keep")), float(keep_scale),
+                  float(inv_divisor), ctx.data_ptr(), ctx.stride(0), lse.data_ptr(), _ptr(kbits_row),
+                  _ptr(kbits_col), _stream())
+    return ctx
+
+
+def attn_bwd(qkv, ctx, dctx, B, S, heads, add_mask, lse, kbits_row, kbits_col, keep_scale, inv_divisor, dqkv):
+    """Writes dQ | dK | dV into dqkv (bf16 [B*S, >=3H])."""
+    for t, nm in ((qkv, "qkv"), (ctx, "ctx"), (dctx, "dctx"), (dqkv, "dqkv")):
+        if t.dtype != torch.bfloat16 or t.stride(1) != 1:
+            raise ShapeError(f"attn_bwd: {nm} must be bfloat16 with contiguous rows")
+    if ctx.stride(0) != dctx.stride(0):
+        raise ShapeError("attn_bwd: ctx and dctx must share a row stride")
+    ws = WORKSPACE.get(_lib.load().dfx_attn_bwd_workspace(B, heads, S))
+    flops = 8.0 * B * heads * S * S * 64  # algorithmic: dPd, dV, dQ, dK (the S recomputes are extra)
+    with _span("attn_bwd", "tensor", lambda: flops):
+        _lib.call("dfx_attn_bwd", B, heads, S, 64, qkv.data_ptr(), qkv.stride(0), ctx.data_ptr(), dctx.data_ptr(),
+                  ctx.stride(0), _ptr(add_mask), lse.data_ptr(), _ptr(kbits_row), _ptr(kbits_col),
+                  float(keep_scale), float(inv_divisor), dqkv.data_ptr(), dqkv.stride(0), ws.data_ptr(),
+                  ws.numel(), _stream())
+    return dqkv
+
+
+# ---------------------------------------------------------------------------
 # bias + GELU, column sums
 
 

@@ -1,0 +1,153 @@
+"""GPU parity of the fused attention kernels (csrc/attn.cu) against the oracle.
+
+Forward: ctx = (softmax(QKᵀ/divisor + mask) ∘ dropout) V, the chain of
+reference operators Einsum / Div / Add / Softmax / Mul / Einsum
+(frontend.py:294, 175-188, 408-501); backward: their VJPs
+(autodiff.py:1363-1415, 1465-1484).  The oracle runs in float64 on the same
+bf16-rounded Q/K/V and the same explicit keep masks; tolerance 2e-2 (bf16) with
+the interp.compare_outputs metric."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P_DROP = 0.1
+
+
+def K():
+    from paper_2110_10802_b200 import kernels
+
+    return kernels
+
+
+def _case(B, NH, S, seed, dropout=True, masked=True):
+    rng = np.random.default_rng(seed)
+    H = NH * 64
+    qkv = O.round_bf16(rng.standard_normal((B * S, 3 * H))).astype(np.float64)
+    am = np.where(rng.random((B, S)) < 0.1, -10000.0, 0.0) if masked else np.zeros((B, S))
+    keep = rng.random((B, NH, S, S)) >= P_DROP if dropout else np.ones((B, NH, S, S), bool)
+    dctx = O.round_bf16(rng.standard_normal((B * S, H))).astype(np.float64)
+    return qkv, am, keep, dctx
+
+
+def _heads(x, B, S, NH, which):
+    H = NH * 64
+    return x[:, which * H:(which + 1) * H].reshape(B, S, NH, 64)
+
+
+def _oracle(qkv, am, keep, dctx, B, S, NH, p_drop=P_DROP):
+    q, k, v = (_heads(qkv, B, S, NH, i) for i in range(3))
+    scores = np.einsum("bsnd,btnd->bnst", q, k)
+    dm = O.mask_values(keep, p_drop, np.float64)
+    p, pd = O.scaled_masked_softmax_fwd(scores, 8.0, am.reshape(B, 1, 1, S), dm)
+    ctx = np.einsum("bnst,btnd->bsnd", pd, v).reshape(B * S, NH * 64)
+    do = dctx.reshape(B, S, NH, 64)
+    dpd = np.einsum("bsnd,btnd->bnst", do, v)
+    dv = np.einsum("bnst,bsnd->btnd", pd, do)
+    ds = O.scaled_masked_softmax_bwd(dpd, p, dm, 8.0)
+    dq = np.einsum("bnst,btnd->bsnd", ds, k)
+    dk = np.einsum("bnst,bsnd->btnd", ds, q)
+    lse2 = np.log2(np.exp(scores / 8.0 + am.reshape(B, 1, 1, S)).sum(-1))
+    dqkv = np.concatenate([t.reshape(B * S, NH * 64) for t in (dq, dk, dv)], 1)
+    return ctx, lse2, dqkv
+
+
+def _run(qkv, am, keep, dctx, B, S, NH, dropout=True):
+    k = K()
+    H = NH * 64
+    t_qkv = torch.as_tensor(qkv, dtype=torch.float32).bfloat16().cuda()
+    t_am = torch.as_tensor(am, dtype=torch.float32).cuda()
+    t_keep = torch.as_tensor(keep.astype(np.uint8)).cuda() if dropout else None
+    ctx = torch.empty(B * S, H, dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty(B, NH, S, dtype=torch.float32, device="cuda")
+    kr = torch.empty(B, NH, S, S // 32, dtype=torch.int32, device="cuda") if dropout else None
+    kc = torch.empty_like(kr) if dropout else None
+    ks = 1.0 / (1.0 - P_DROP) if dropout else 1.0
+    k.attn_fwd(t_qkv, B, S, NH, t_am, t_keep, ks, 0.125, ctx, lse, kr, kc)
+    t_do = torch.as_tensor(dctx, dtype=torch.float32).bfloat16().cuda()
+    dqkv = torch.zeros(B * S, 3 * H, dtype=torch.bfloat16, device="cuda")
+    k.attn_bwd(t_qkv, ctx, t_do, B, S, NH, t_am, lse, kr, kc, ks, 0.125, dqkv)
+    torch.cuda.synchronize()
+    f = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
+    return f(ctx), f(lse), f(dqkv), kr, kc
+
+
+@pytest.mark.parametrize("B,NH,S", [(2, 2, 128), (1, 3, 256), (2, 2, 384), (2, 12, 512)])
+def test_attention_vs_oracle(B, NH, S):
+    qkv, am, keep, dctx = _case(B, NH, S, seed=S + NH)
+    ctx, lse, dqkv, _, _ = _run(qkv, am, keep, dctx, B, S, NH)
+    w_ctx, w_lse, w_dqkv = _oracle(qkv, am, keep, dctx, B, S, NH)
+    assert O.compare(ctx, w_ctx) <= 2e-2, O.compare(ctx, w_ctx)
+    assert np.abs(lse - w_lse).max() <= 1e-2 * max(1.0, np.abs(w_lse).max()), np.abs(lse - w_lse).max()
+    H = NH * 64
+    for i, nm in enumerate("qkv"):
+        got, want = dqkv[:, i * H:(i + 1) * H], w_dqkv[:, i * H:(i + 1) * H]
+        err = O.compare_scaled(got, want)
+        assert err <= 2e-2, f"d{nm}: {err:.3e}"
+
+
+def test_attention_no_dropout_no_mask():
+    B, NH, S = 1, 2, 256
+    qkv, am, keep, dctx = _case(B, NH, S, seed=7, dropout=False, masked=False)
+    ctx, _, dqkv, _, _ = _run(qkv, am, keep, dctx, B, S, NH, dropout=False)
+    w_ctx, _, w_dqkv = _oracle(qkv, am, keep, dctx, B, S, NH, p_drop=0.0)
+    assert O.compare(ctx, w_ctx) <= 2e-2
+    assert O.compare_scaled(dqkv, w_dqkv) <= 2e-2
+
+
+def test_packed_keep_bits():
+    B, NH, S = 1, 2, 256
+    qkv, am, keep, dctx = _case(B, NH, S, seed=11)
+    _, _, _, kr, kc = _run(qkv, am, keep, dctx, B, S, NH)
+    w = (1 << np.arange(32, dtype=np.uint64))
+    rowbits = (keep.reshape(B, NH, S, S // 32, 32).astype(np.uint64) * w).sum(-1)
+    colbits = (np.swapaxes(keep, 2, 3).reshape(B, NH, S, S // 32, 32).astype(np.uint64) * w).sum(-1)
+    assert np.array_equal(kr.cpu().numpy().view(np.uint32).astype(np.uint64), rowbits)
+    assert np.array_equal(kc.cpu().numpy().view(np.uint32).astype(np.uint64), colbits)
+
+
+def test_attention_deterministic():
+    B, NH, S = 2, 4, 512
+    qkv, am, keep, dctx = _case(B, NH, S, seed=3)
+    a = _run(qkv, am, keep, dctx, B, S, NH)
+    b = _run(qkv, am, keep, dctx, B, S, NH)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2])
+
+
+def test_attention_rejects_bad_shapes():
+    from paper_2110_10802_b200.errors import UnsupportedOp
+
+    k = K()
+    qkv = torch.zeros(2 * 100, 3 * 128, dtype=torch.bfloat16, device="cuda")
+    ctx = torch.zeros(200, 128, dtype=torch.bfloat16, device="cuda")
+    lse = torch.zeros(2, 2, 100, device="cuda")
+    with pytest.raises(UnsupportedOp):
+        k.attn_fwd(qkv, 2, 100, 2, None, None, 1.0, 0.125, ctx, lse)
+
+
+def test_layer_fused_matches_unfused():
+    """The fused and the unfused attention paths of the encoder layer agree."""
+    from paper_2110_10802_b200.bert import BertEncoderLayer, BertLayerConfig
+
+    B, S, NH, H = 2, 256, 12, 768
+    rng = np.random.default_rng(5)
+    x = torch.as_tensor(rng.standard_normal((B * S, H)), dtype=torch.float32).bfloat16().cuda()
+    dout = torch.as_tensor(rng.standard_normal((B * S, H)), dtype=torch.float32).bfloat16().cuda()
+    am = torch.as_tensor(np.where(rng.random((B, S)) < 0.1, -10000.0, 0.0), dtype=torch.float32).cuda()
+    keeps = [torch.as_tensor((rng.random(s) >= 0.1).astype(np.uint8)).cuda()
+             for s in ((B, NH, S, S), (B * S, H), (B * S, H))]
+    outs = []
+    for fused in (True, False):
+        layer = BertEncoderLayer(BertLayerConfig(fused_attention=fused), seed=3)
+        out = layer.forward(x, am, *keeps).float().cpu().numpy()
+        dx = layer.backward(dout).float().cpu().numpy()
+        outs.append((out, dx, layer.grads_numpy()))
+    (o1, d1, g1), (o2, d2, g2) = outs
+    assert O.compare(o1, o2) <= 2e-2
+    assert O.compare_scaled(d1, d2) <= 2e-2
+    for name in ("wq", "wk", "wv", "bq", "wo", "w1"):
+        assert O.compare_scaled(g1[name], g2[name]) <= 2e-2, name
