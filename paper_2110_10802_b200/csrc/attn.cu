@@ -89,7 +89,20 @@ __device__ __forceinline__ void st_sw128(uint32_t tile, int r, int ch, uint4 v) 
   sts128(tile + r * 128 + ((ch ^ (r & 7)) << 4), v);
 }
 
+unsigned long long* g_attn_trace = nullptr;  // debug timeline (tools/attn_trace.py), normally null
+
+__device__ __forceinline__ unsigned long long gtime_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define ATRACE(slot)                                                                   \
+  do {                                                                                 \
+    if (p.trace) p.trace[(size_t)blockIdx.x * 16 + (slot)] = gtime_ns();              \
+  } while (0)
+
 struct AttnFwdParams {
+  unsigned long long* trace;
   int B, NH, S, H;
   int64_t ld_ctx;
   const float* add_mask;  // [B, S] or null
@@ -121,6 +134,7 @@ __device__ __forceinline__ uint32_t p_chunk(uint32_t base, int c) {
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
 attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams p) {
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -157,6 +171,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // setup above overlapped the previous kernel's tail
+  if (threadIdx.x == 0) ATRACE(0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -177,6 +193,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
       // ---------------------------------------------------------- MMA issuer
       mbar_wait(bar_qk, 0);
       tc_fence_after();
+      ATRACE(1);
       const uint32_t idesc_s = make_idesc(128, QT, 0, 0);
       const uint64_t qdesc = make_sdesc(sbase + FwdSmem::Q, 16, 1024);
       for (int nb = 0; nb < S / 128; ++nb) {
@@ -187,6 +204,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
       }
       tc_commit_cg<1>(bar_s);
       mbar_wait(bar_p, 0);
+      ATRACE(5);
       mbar_wait(bar_v, 0);
       tc_fence_after();
       const uint32_t idesc_o = make_idesc(DH, QT, 0, 1);
@@ -216,8 +234,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
     uint4 kv0 = p.keep ? __ldg(kp) : ones, kv1 = p.keep ? __ldg(kp + 1) : ones;
     named_bar(1, kSoftWarps * 32);
     const float4* mask4 = reinterpret_cast<const float4*>(mask2);
+    if (sw == 0 && lane == 0) ATRACE(2);
     mbar_wait(bar_s, 0);
     tc_fence_after();
+    if (sw == 0 && lane == 0) ATRACE(3);
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     // pass 1: row max of t = S*c*log2e + mask*log2e (TMEM load of chunk j+1
     // in flight while chunk j is reduced)
@@ -241,6 +261,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
       }
     }
     red_max[part * QT + rl] = mx;
+    if (sw == 0 && lane == 0) ATRACE(4);
     named_bar(1, kSoftWarps * 32);
     mx = fmaxf(fmaxf(red_max[rl], red_max[QT + rl]), fmaxf(red_max[2 * QT + rl], red_max[3 * QT + rl]));
     // pass 2: e = exp2(t - max); rowsum; P̃d = e * keep (the 1/(1-p) scale is
@@ -295,8 +316,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
     const float tot = red_sum[rl] + red_sum[QT + rl] + red_sum[2 * QT + rl] + red_sum[3 * QT + rl];
     const float inv = p.ks / tot;
     if (part == 0) p.lse[(size_t)bh * S + grow] = mx + __log2f(tot);
+    if (sw == 0 && lane == 0) ATRACE(6);
     mbar_wait(bar_o, 0);
     tc_fence_after();
+    if (sw == 0 && lane == 0) ATRACE(7);
     float o[16];
     tmem_ld16(trow + part * 16, o);
     uint32_t w[8];
@@ -308,6 +331,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ATRACE(8);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
@@ -316,6 +340,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
 
 // --------------------------------------------------------------------- backward
 struct AttnBwdParams {
+  unsigned long long* trace;
   int B, NH, S, H;
   int64_t ld_ctx, ld_dqkv;
   const __nv_bfloat16* ctx;   // O   [T, ld_ctx]
@@ -397,6 +422,7 @@ __device__ __forceinline__ float dot16_bf16(const __nv_bfloat16* a, const __nv_b
 __global__ void __launch_bounds__(kAttnThreads, 1)
 attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
                    const AttnBwdParams p) {
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -432,6 +458,7 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // setup above overlapped the previous kernel's tail
   constexpr uint32_t T_S = 0, T_DP = 128, T_DQ = 256;
 
   if (warp == 0) {
@@ -556,6 +583,7 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
 __global__ void __launch_bounds__(kAttnThreads, 1)
 attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
                      const AttnBwdParams p) {
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -592,6 +620,7 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // setup above overlapped the previous kernel's tail
   constexpr uint32_t T_S = 0, T_DP = 128, T_DK = 256, T_DV = 320;
 
   if (warp == 0) {
@@ -763,6 +792,7 @@ extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   rc = make_map(&map, qkv, 2, (uint64_t)ld_qkv, (uint64_t)T, ld_qkv, 1, 0, 1, 0, 64, 64, true);
   if (rc) return rc;
   AttnFwdParams p;
+  p.trace = g_attn_trace;
   p.B = (int)batch; p.NH = (int)heads; p.S = (int)seq; p.H = (int)(heads * DH);
   p.ld_ctx = ld_ctx;
   p.add_mask = add_mask;
@@ -779,7 +809,7 @@ extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
     attr = true;
   }
   const int grid = (int)(batch * heads * (seq / QT));
-  attn_fwd_kernel<<<grid, kAttnThreads, FwdSmem::TOTAL, as_stream(stream)>>>(map, p);
+  launch_k(attn_fwd_kernel, grid, kAttnThreads, FwdSmem::TOTAL, as_stream(stream), map, p);
   DFX_LAUNCH_CHECK("dfx_attn_fwd");
   return DFX_OK;
 }
@@ -811,6 +841,7 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   rc = make_map(&mdo, dctx, 2, (uint64_t)ld_ctx, (uint64_t)T, ld_ctx, 1, 0, 1, 0, 64, 64, true);
   if (rc) return rc;
   AttnBwdParams p;
+  p.trace = nullptr;
   p.B = (int)batch; p.NH = (int)heads; p.S = (int)seq; p.H = (int)(heads * DH);
   p.ld_ctx = ld_ctx; p.ld_dqkv = ld_dqkv;
   p.ctx = reinterpret_cast<const __nv_bfloat16*>(ctx);
@@ -829,9 +860,13 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
     attr = true;
   }
   const int grid = (int)(batch * heads * (seq / QT));
-  attn_bwd_dq_kernel<<<grid, kAttnThreads, DqSmem::TOTAL, as_stream(stream)>>>(mqkv, mdo, p);
+  launch_k(attn_bwd_dq_kernel, grid, kAttnThreads, DqSmem::TOTAL, as_stream(stream), mqkv, mdo, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dq)");
-  attn_bwd_dkdv_kernel<<<grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream)>>>(mqkv, mdo, p);
+  launch_k(attn_bwd_dkdv_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dk, dv)");
   return DFX_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) void dfx_debug_attn_trace(void* buf) {
+  dfx::g_attn_trace = reinterpret_cast<unsigned long long*>(buf);
 }

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "dfx.h"
 
@@ -34,6 +35,33 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 inline bool aligned_n(const void* p, int n) { return (reinterpret_cast<uintptr_t>(p) % n) == 0; }
+
+// ------------------------------------------------- programmatic dependent launch
+// Every kernel is launched with programmatic stream serialization: it
+// signals `launch_dependents` as soon as it starts (safe — the dependent grid
+// is only scheduled once EVERY CTA of this grid has started, so it can never
+// starve this grid of SMs) and executes `wait` before its first read of data
+// produced by the previous kernel.  Kernel N+1's launch latency and prologue
+// (barrier init, TMEM allocation, descriptor prefetch) then overlap kernel N's
+// tail, inside CUDA graphs too.  Both are no-ops without a programmatic edge.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- device
 __device__ __forceinline__ float warp_sum(float v) {

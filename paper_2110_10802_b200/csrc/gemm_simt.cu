@@ -15,6 +15,8 @@ constexpr int BM = 64, BN = 64, BK = 16;
 
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(256) simt_gemm_kernel(dfx_gemm_args p) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int tid = threadIdx.x;
@@ -88,13 +90,13 @@ int gemm_simt(const dfx_gemm_args& p, cudaStream_t st) {
   dim3 grid((unsigned)((p.n + BN - 1) / BN), (unsigned)((p.m + BM - 1) / BM), (unsigned)nb);
   DFX_REQUIRE(grid.y <= 65535, DFX_ERR_SHAPE, "dfx_gemm: m too large for the SIMT path");
   if (p.in_dtype == DFX_F32 && p.out_dtype == DFX_F32)
-    simt_gemm_kernel<float, float><<<grid, 256, 0, st>>>(p);
+    launch_k(simt_gemm_kernel<float, float>, grid, 256, 0, st, p);
   else if (p.in_dtype == DFX_BF16 && p.out_dtype == DFX_BF16)
-    simt_gemm_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, st>>>(p);
+    launch_k(simt_gemm_kernel<__nv_bfloat16, __nv_bfloat16>, grid, 256, 0, st, p);
   else if (p.in_dtype == DFX_BF16 && p.out_dtype == DFX_F32)
-    simt_gemm_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>(p);
+    launch_k(simt_gemm_kernel<__nv_bfloat16, float>, grid, 256, 0, st, p);
   else if (p.in_dtype == DFX_F32 && p.out_dtype == DFX_BF16)
-    simt_gemm_kernel<float, __nv_bfloat16><<<grid, 256, 0, st>>>(p);
+    launch_k(simt_gemm_kernel<float, __nv_bfloat16>, grid, 256, 0, st, p);
   else
     return fail(DFX_ERR_DTYPE, "dfx_gemm: in/out dtype must be f32 or bf16");
   DFX_LAUNCH_CHECK("dfx_gemm (simt)");

@@ -193,6 +193,7 @@ template <int BN, typename TO, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const TcParams p) {
+  pdl_trigger();
   using Cfg = TcCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int BN_LOAD = BN / CG;  // B columns each CTA loads
@@ -241,6 +242,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // setup above overlapped the previous kernel's tail
   if (threadIdx.x == 0) TRACE(1);
 
   if (warp == 0) {
@@ -451,6 +453,8 @@ template <typename TO>
 __global__ void splitk_reduce_kernel(int splits, int64_t Z, int64_t m, int64_t n, const float* __restrict__ part,
                                      TO* __restrict__ d, int64_t d_stride_m, int64_t d_stride_b1,
                                      int64_t d_stride_b2, int64_t batch2) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = Z * m * n;
   const int64_t per_split = total;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -576,13 +580,15 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& tp, 
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = TcCfg<BN, CG>::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see common.cuh
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, tp);
   if (e != cudaSuccess) return fail(DFX_ERR_CUDA, std::string("dfx_gemm (tcgen05) launch: ") + cudaGetErrorString(e));
   DFX_LAUNCH_CHECK("dfx_gemm (tcgen05)");
@@ -687,10 +693,10 @@ int gemm_tc(const dfx_gemm_args& p, cudaStream_t st) {
   const int64_t total = Z * p.m * p.n;
   const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
   if (p.out_dtype == DFX_F32)
-    splitk_reduce_kernel<float><<<grid, 256, 0, st>>>(pl.splits, Z, p.m, p.n, part, (float*)p.d, p.d_stride_m,
+    launch_k(splitk_reduce_kernel<float>, grid, 256, 0, st, pl.splits, Z, p.m, p.n, part, (float*)p.d, p.d_stride_m,
                                                       p.d_stride_b1, p.d_stride_b2, p.batch2);
   else
-    splitk_reduce_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(pl.splits, Z, p.m, p.n, part, (__nv_bfloat16*)p.d,
+    launch_k(splitk_reduce_kernel<__nv_bfloat16>, grid, 256, 0, st, pl.splits, Z, p.m, p.n, part, (__nv_bfloat16*)p.d,
                                                               p.d_stride_m, p.d_stride_b1, p.d_stride_b2, p.batch2);
   DFX_LAUNCH_CHECK("dfx_gemm split-K reduce");
   return DFX_OK;

@@ -40,6 +40,8 @@ template <> struct NV<float> { static constexpr int value = 4; };
 template <typename T, int V>
 __global__ void __launch_bounds__(kThreads) bn_stats_kernel(int64_t rows, int C, int64_t rpb, const T* __restrict__ x,
                                                            float* __restrict__ part /*[blocks][3][C]*/) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sm[];
   const int CV = C / V, PY = blockDim.x / CV;
   const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
@@ -82,6 +84,8 @@ __global__ void __launch_bounds__(kThreads) bn_stats_kernel(int64_t rows, int C,
 // one block per channel: merge block partials in a fixed tree order
 __global__ void __launch_bounds__(kThreads) bn_merge_kernel(int nparts, int C, const float* __restrict__ part,
                                                            float* __restrict__ out /*[3][C]*/) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sn[kThreads], smn[kThreads], sm2[kThreads];
   const int c = blockIdx.x;
   Wf acc = {0.f, 0.f, 0.f};
@@ -106,6 +110,8 @@ __global__ void __launch_bounds__(kThreads) bn_apply_kernel(int64_t nvec, int C,
                                                            const float* __restrict__ mean, const float* __restrict__ rstd,
                                                            const float* __restrict__ gamma, const float* __restrict__ beta,
                                                            T* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   const int CV = C / V;
   for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec; vi += (int64_t)gridDim.x * blockDim.x) {
     const int c0 = (int)(vi % CV) * V;
@@ -129,6 +135,8 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(int64_t rows, i
                                                                  const float* __restrict__ gamma,
                                                                  const float* __restrict__ beta,
                                                                  float* __restrict__ part /*[blocks][2][C]*/) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sm[];
   const int CV = C / V, PY = blockDim.x / CV;
   const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
@@ -171,6 +179,8 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(int64_t rows, i
 }
 
 __global__ void bn_sum_parts_kernel(int nparts, int C, const float* __restrict__ part, float* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= 2 * C) return;
   float acc = 0.f;
@@ -186,6 +196,8 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(int64_t nvec, int C
                                                             const float* __restrict__ beta,
                                                             const float* __restrict__ sums, float inv_count,
                                                             T* __restrict__ dx) {
+  pdl_trigger();
+  pdl_wait();
   const int CV = C / V;
   for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec; vi += (int64_t)gridDim.x * blockDim.x) {
     const int c0 = (int)(vi % CV) * V;
@@ -269,12 +281,12 @@ int dfx_batchnorm_stats(int dtype, int64_t rows, int64_t C, const void* x, float
   {                                                                                                       \
     auto k = bn_stats_kernel<TT, VV>;                                                                     \
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);   \
-    k<<<nb, CV * PY, sm, st>>>(rows, (int)C, rpb, (const TT*)x, (float*)workspace);                       \
+    launch_k(k, nb, CV * PY, sm, st, rows, (int)C, rpb, (const TT*)x, (float*)workspace);                       \
   }
   BN_DISPATCH(S, 0);
 #undef S
   DFX_LAUNCH_CHECK("dfx_batchnorm_stats");
-  bn_merge_kernel<<<(unsigned)C, kThreads, 0, st>>>(nb, (int)C, (const float*)workspace, local);
+  launch_k(bn_merge_kernel, (unsigned)C, kThreads, 0, st, nb, (int)C, (const float*)workspace, local);
   DFX_LAUNCH_CHECK("dfx_batchnorm_stats merge");
   return DFX_OK;
 }
@@ -288,7 +300,7 @@ int dfx_batchnorm_act_apply(int dtype, int64_t rows, int64_t C, const void* x, c
   const int V = vec_width(dtype, C);
   const int64_t nvec = rows * C / V;
   const int grid = (int)std::min<int64_t>((nvec + 255) / 256, (int64_t)num_sms() * 16);
-#define A(TT, VV, ACT) { bn_apply_kernel<TT, VV, ACT><<<grid, 256, 0, st>>>(nvec, (int)C, (const TT*)x, mean, rstd, gamma, beta, (TT*)y); }
+#define A(TT, VV, ACT) { launch_k(bn_apply_kernel<TT, VV, ACT>, grid, 256, 0, st, nvec, (int)C, (const TT*)x, mean, rstd, gamma, beta, (TT*)y); }
   BN_DISPATCH(A, act);
 #undef A
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_apply");
@@ -314,13 +326,13 @@ int dfx_batchnorm_act_bwd_reduce(int dtype, int64_t rows, int64_t C, const void*
   {                                                                                                         \
     auto k = bn_bwd_reduce_kernel<TT, VV, ACT>;                                                             \
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
-    k<<<nb, CV * PY, sm, st>>>(rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta,     \
+    launch_k(k, nb, CV * PY, sm, st, rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta,     \
                                (float*)workspace);                                                          \
   }
   BN_DISPATCH(R, act);
 #undef R
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_reduce");
-  bn_sum_parts_kernel<<<(unsigned)((2 * C + 255) / 256), 256, 0, st>>>(nb, (int)C, (const float*)workspace, bnsum);
+  launch_k(bn_sum_parts_kernel, (unsigned)((2 * C + 255) / 256), 256, 0, st, nb, (int)C, (const float*)workspace, bnsum);
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_reduce sum");
   return DFX_OK;
 }
@@ -338,7 +350,7 @@ int dfx_batchnorm_act_bwd_dx(int dtype, int64_t rows, int64_t C, const void* dy,
   const int grid = (int)std::min<int64_t>((nvec + 255) / 256, (int64_t)num_sms() * 16);
   const float ic = (float)(1.0 / count);
 #define D(TT, VV, ACT) \
-  { bn_bwd_dx_kernel<TT, VV, ACT><<<grid, 256, 0, st>>>(nvec, (int)C, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, bnsum, ic, (TT*)dx); }
+  { launch_k(bn_bwd_dx_kernel<TT, VV, ACT>, grid, 256, 0, st, nvec, (int)C, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, bnsum, ic, (TT*)dx); }
   BN_DISPATCH(D, act);
 #undef D
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_dx");

@@ -38,6 +38,8 @@ __global__ void __launch_bounds__(256, 4) bdrln_fwd_kernel(
     const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
     T* __restrict__ y, T* __restrict__ s_out, float* __restrict__ mean_out,
     float* __restrict__ rstd_out) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvec = cols / V;
   const float inv_n = 1.f / (float)cols;
@@ -159,6 +161,8 @@ __global__ void __launch_bounds__(256, 2) bdrln_bwd_kernel(
     const uint8_t* __restrict__ keep, float ks, float eps,
     T* __restrict__ ds_out, T* __restrict__ dh_out, float* __restrict__ part_g,
     float* __restrict__ part_b, float* __restrict__ part_h) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float red[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvec = cols / V;
@@ -287,6 +291,8 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     int64_t rows, int cols, const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ s,
     const float* __restrict__ gamma, const uint8_t* __restrict__ keep, float ks, float eps,
     __nv_bfloat16* __restrict__ ds_out, __nv_bfloat16* __restrict__ dh_out, float* __restrict__ part /*[3][grid][cols]*/) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int V = 8;
   extern __shared__ float red[];  // [16][cols]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -416,6 +422,8 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_colsum_kernel(int npa
                                                               const float* __restrict__ part,
                                                               float* out0, float* out1, float* out2,
                                                               int accumulate) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[kFinWarps][33];
   const int q = blockIdx.y;
   float* out = q == 0 ? out0 : (q == 1 ? out1 : out2);
@@ -446,6 +454,8 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(
     int64_t rows, int cols, int64_t rows_per_batch, const T* __restrict__ x, float inv_div,
     const float* __restrict__ am, const uint8_t* __restrict__ keep, float ks,
     T* __restrict__ p_out, T* __restrict__ pd_out) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kWarps + warp;
   if (row >= rows) return;
@@ -518,6 +528,8 @@ template <typename T, int V, int NCH>
 __global__ void __launch_bounds__(256) softmax_bwd_kernel(
     int64_t rows, int cols, const T* __restrict__ dpd, const T* __restrict__ p,
     const uint8_t* __restrict__ keep, float ks, float inv_div, T* __restrict__ dx) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kWarps + warp;
   if (row >= rows) return;
@@ -571,6 +583,8 @@ __global__ void __launch_bounds__(256) bias_gelu_fwd_kernel(int64_t nvec, int co
                                                             const T* __restrict__ f,
                                                             const float* __restrict__ bias,
                                                             T* __restrict__ pre, T* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec;
        vi += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = vi * V;
@@ -593,6 +607,8 @@ template <typename T, int V>
 __global__ void __launch_bounds__(256) gelu_bwd_kernel(int64_t nvec, const T* __restrict__ dy,
                                                        const T* __restrict__ pre,
                                                        T* __restrict__ dpre) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec;
        vi += (int64_t)gridDim.x * blockDim.x) {
     Vec<T, V> a, b, o;
@@ -611,6 +627,8 @@ template <typename T, int V>
 __global__ void __launch_bounds__(256) colsum_kernel(int64_t rows, int cols, int64_t ld,
                                                      const T* __restrict__ x,
                                                      float* __restrict__ part) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[kWarps][32 * V];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col0 = blockIdx.x * 32 * V + lane * V;
@@ -644,6 +662,8 @@ __global__ void __launch_bounds__(256) colsum_kernel(int64_t rows, int cols, int
 
 __global__ void sgd_kernel(int64_t n, float* __restrict__ w, const float* __restrict__ g, float lr,
                            __nv_bfloat16* __restrict__ wb) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float v = w[i] - lr * g[i];
@@ -653,6 +673,8 @@ __global__ void sgd_kernel(int64_t n, float* __restrict__ w, const float* __rest
 }
 
 __global__ void scale_kernel(int64_t n, float* __restrict__ x, float s) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     x[i] *= s;
@@ -660,6 +682,8 @@ __global__ void scale_kernel(int64_t n, float* __restrict__ x, float s) {
 
 template <typename S, typename D>
 __global__ void cast_kernel(int64_t n, const S* __restrict__ s, D* __restrict__ d) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     d[i] = from_f<D>(to_f<S>(s[i]));
@@ -710,11 +734,11 @@ int bdrln_fwd_t(int64_t rows, int64_t cols, const void* h, const float* bias, co
 #define L(N)                                                                                        \
   if (nch == N) {                                                                                   \
     if (act)                                                                                        \
-      bdrln_fwd_kernel<T, V, N, 1><<<grid, 256, 0, st>>>(rows, (int)cols, (const T*)h, bias, keep, ks, \
+      launch_k(bdrln_fwd_kernel<T, V, N, 1>, grid, 256, 0, st, rows, (int)cols, (const T*)h, bias, keep, ks, \
                                                          (const T*)res, gamma, beta, eps, (T*)y,    \
                                                          (T*)s_out, mean, rstd);                   \
     else                                                                                            \
-      bdrln_fwd_kernel<T, V, N, 0><<<grid, 256, 0, st>>>(rows, (int)cols, (const T*)h, bias, keep, ks, \
+      launch_k(bdrln_fwd_kernel<T, V, N, 0>, grid, 256, 0, st, rows, (int)cols, (const T*)h, bias, keep, ks, \
                                                          (const T*)res, gamma, beta, eps, (T*)y,    \
                                                          (T*)s_out, mean, rstd);                   \
   }
@@ -732,7 +756,7 @@ int bdrln_bwd_launch(int nch, int grid, size_t smem, int64_t rows, int64_t cols,
   if (nch == N) {                                                                                  \
     auto kfn = bdrln_bwd_kernel<T, V, N, ACT>;                                                     \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    kfn<<<grid, 256, smem, st>>>(rows, (int)cols, (const T*)dy, (const T*)s, gamma, beta, keep, ks, eps, \
+    launch_k(kfn, grid, 256, smem, st, rows, (int)cols, (const T*)dy, (const T*)s, gamma, beta, keep, ks, eps, \
                                  (T*)ds, (T*)dh, pg, pb, ph);                                      \
   }
   DFX_NCH_LIST(L)
@@ -763,14 +787,14 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
   if (nch == N) {                                                                                  \
     auto kfn = bdrln_bwd_wave_kernel<N>;                                                           \
     if (wsm > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm); \
-    kfn<<<grid, 512, wsm, st>>>(rows, (int)cols, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)s, gamma, keep, \
+    launch_k(kfn, grid, 512, wsm, st, rows, (int)cols, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)s, gamma, keep, \
                                 ks, eps, (__nv_bfloat16*)ds, (__nv_bfloat16*)dh, pg);              \
   }
     LW(1) LW(2) LW(3)
 #undef LW
     DFX_LAUNCH_CHECK("dfx_bdrln_bwd");
     if (dgamma || dbeta || dbias) {
-      finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 3), kFinWarps * 32, 0, st>>>(grid, (int)cols, pg,
+      launch_k(finalize_colsum_kernel, dim3((unsigned)((cols + 31) / 32), 3), kFinWarps * 32, 0, st, grid, (int)cols, pg,
                                                                                       dgamma, dbeta, dbias, 0);
       DFX_LAUNCH_CHECK("dfx_bdrln_bwd finalize");
     }
@@ -783,7 +807,7 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
                                         pg, pb, ph, st);
   if (rc) return rc;
   if (dgamma || dbeta || dbias) {
-    finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 3), kFinWarps * 32, 0, st>>>(grid, (int)cols, pg, dgamma,
+    launch_k(finalize_colsum_kernel, dim3((unsigned)((cols + 31) / 32), 3), kFinWarps * 32, 0, st, grid, (int)cols, pg, dgamma,
                                                                                dbeta, dbias, 0);
     DFX_LAUNCH_CHECK("dfx_bdrln_bwd finalize");
   }
@@ -800,7 +824,7 @@ int softmax_fwd_t(int64_t batch, int64_t heads, int64_t q, int64_t cols, const v
   const int64_t grid = (rows + kWarps - 1) / kWarps;
 #define L(N)                                                                                    \
   if (nch == N)                                                                                 \
-    softmax_fwd_kernel<T, V, N><<<(unsigned)grid, 256, 0, st>>>(rows, (int)cols, heads * q,     \
+    launch_k(softmax_fwd_kernel<T, V, N>, (unsigned)grid, 256, 0, st, rows, (int)cols, heads * q,     \
                                                                 (const T*)x, inv_div, am, keep, \
                                                                 ks, (T*)p, (T*)pd);
   DFX_NCH_LIST(L)
@@ -818,7 +842,7 @@ int softmax_bwd_t(int64_t rows, int64_t cols, const void* dpd, const void* p, co
   const int64_t grid = (rows + kWarps - 1) / kWarps;
 #define L(N)                                                                                     \
   if (nch == N)                                                                                  \
-    softmax_bwd_kernel<T, V, N><<<(unsigned)grid, 256, 0, st>>>(rows, (int)cols, (const T*)dpd,  \
+    launch_k(softmax_bwd_kernel<T, V, N>, (unsigned)grid, 256, 0, st, rows, (int)cols, (const T*)dpd,  \
                                                                 (const T*)p, keep, ks, inv_div,  \
                                                                 (T*)dx);
   DFX_NCH_LIST(L)
@@ -850,9 +874,9 @@ int colsum_t(int64_t rows, int64_t cols, const void* x, int64_t ld, float* out, 
   int gy = (int)std::max<int64_t>(1, std::min<int64_t>((rows + kWarps - 1) / kWarps, kMaxColBlocks / gx));
   DFX_REQUIRE(ws_bytes >= (size_t)gy * cols * sizeof(float), DFX_ERR_WORKSPACE,
               "dfx_colsum: workspace too small");
-  colsum_kernel<T, V><<<dim3(gx, gy), 256, 0, st>>>(rows, (int)cols, ld, (const T*)x, (float*)ws);
+  launch_k(colsum_kernel<T, V>, dim3(gx, gy), 256, 0, st, rows, (int)cols, ld, (const T*)x, (float*)ws);
   DFX_LAUNCH_CHECK("dfx_colsum");
-  finalize_colsum_kernel<<<dim3((unsigned)((cols + 31) / 32), 1), kFinWarps * 32, 0, st>>>(gy, (int)cols, (const float*)ws, out,
+  launch_k(finalize_colsum_kernel, dim3((unsigned)((cols + 31) / 32), 1), kFinWarps * 32, 0, st, gy, (int)cols, (const float*)ws, out,
                                                                               nullptr, nullptr, accumulate);
   DFX_LAUNCH_CHECK("dfx_colsum finalize");
   return DFX_OK;
@@ -933,9 +957,9 @@ int dfx_bias_gelu_fwd(int dtype, int64_t rows, int64_t cols, const void* f, cons
   const int grid = grid_for(nvec, 256, 148 * 16);
   cudaStream_t st = as_stream(stream);
   if (dtype == DFX_BF16)
-    bias_gelu_fwd_kernel<__nv_bfloat16, 8><<<grid, 256, 0, st>>>(nvec, (int)cols, (const __nv_bfloat16*)f, bias, (__nv_bfloat16*)pre, (__nv_bfloat16*)y);
+    launch_k(bias_gelu_fwd_kernel<__nv_bfloat16, 8>, grid, 256, 0, st, nvec, (int)cols, (const __nv_bfloat16*)f, bias, (__nv_bfloat16*)pre, (__nv_bfloat16*)y);
   else if (dtype == DFX_F32)
-    bias_gelu_fwd_kernel<float, 4><<<grid, 256, 0, st>>>(nvec, (int)cols, (const float*)f, bias, (float*)pre, (float*)y);
+    launch_k(bias_gelu_fwd_kernel<float, 4>, grid, 256, 0, st, nvec, (int)cols, (const float*)f, bias, (float*)pre, (float*)y);
   else
     return fail(DFX_ERR_DTYPE, "dfx_bias_gelu_fwd: dtype must be f32 or bf16");
   DFX_LAUNCH_CHECK("dfx_bias_gelu_fwd");
@@ -952,9 +976,9 @@ int dfx_bias_gelu_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, con
   const int grid = grid_for(nvec, 256, 148 * 16);
   cudaStream_t st = as_stream(stream);
   if (dtype == DFX_BF16)
-    gelu_bwd_kernel<__nv_bfloat16, 8><<<grid, 256, 0, st>>>(nvec, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)pre, (__nv_bfloat16*)dpre);
+    launch_k(gelu_bwd_kernel<__nv_bfloat16, 8>, grid, 256, 0, st, nvec, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)pre, (__nv_bfloat16*)dpre);
   else if (dtype == DFX_F32)
-    gelu_bwd_kernel<float, 4><<<grid, 256, 0, st>>>(nvec, (const float*)dy, (const float*)pre, (float*)dpre);
+    launch_k(gelu_bwd_kernel<float, 4>, grid, 256, 0, st, nvec, (const float*)dy, (const float*)pre, (float*)dpre);
   else
     return fail(DFX_ERR_DTYPE, "dfx_bias_gelu_bwd: dtype must be f32 or bf16");
   DFX_LAUNCH_CHECK("dfx_bias_gelu_bwd");
@@ -1005,14 +1029,14 @@ int dfx_sgd_update(int64_t n, float* master, const float* grad, float lr, void* 
                    void* stream) {
   DFX_REQUIRE(master && grad, DFX_ERR_SHAPE, "dfx_sgd_update: null pointer");
   if (n == 0) return DFX_OK;
-  sgd_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, as_stream(stream)>>>(n, master, grad, lr, (__nv_bfloat16*)weights_bf16);
+  launch_k(sgd_kernel, grid_for(n, 256, 148 * 8), 256, 0, as_stream(stream), n, master, grad, lr, (__nv_bfloat16*)weights_bf16);
   DFX_LAUNCH_CHECK("dfx_sgd_update");
   return DFX_OK;
 }
 
 int dfx_scale_f32(int64_t n, float* x, float scale, void* stream) {
   if (n == 0) return DFX_OK;
-  scale_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, as_stream(stream)>>>(n, x, scale);
+  launch_k(scale_kernel, grid_for(n, 256, 148 * 8), 256, 0, as_stream(stream), n, x, scale);
   DFX_LAUNCH_CHECK("dfx_scale_f32");
   return DFX_OK;
 }
@@ -1021,9 +1045,9 @@ int dfx_cast(int64_t n, int sd, const void* src, int dd, void* dst, void* stream
   if (n == 0) return DFX_OK;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(n, 256, 148 * 8);
-  if (sd == DFX_F32 && dd == DFX_BF16) cast_kernel<float, __nv_bfloat16><<<g, 256, 0, st>>>(n, (const float*)src, (__nv_bfloat16*)dst);
-  else if (sd == DFX_BF16 && dd == DFX_F32) cast_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>(n, (const __nv_bfloat16*)src, (float*)dst);
-  else if (sd == DFX_F32 && dd == DFX_F32) cast_kernel<float, float><<<g, 256, 0, st>>>(n, (const float*)src, (float*)dst);
+  if (sd == DFX_F32 && dd == DFX_BF16) launch_k(cast_kernel<float, __nv_bfloat16>, g, 256, 0, st, n, (const float*)src, (__nv_bfloat16*)dst);
+  else if (sd == DFX_BF16 && dd == DFX_F32) launch_k(cast_kernel<__nv_bfloat16, float>, g, 256, 0, st, n, (const __nv_bfloat16*)src, (float*)dst);
+  else if (sd == DFX_F32 && dd == DFX_F32) launch_k(cast_kernel<float, float>, g, 256, 0, st, n, (const float*)src, (float*)dst);
   else return fail(DFX_ERR_DTYPE, "dfx_cast: unsupported dtype pair");
   DFX_LAUNCH_CHECK("dfx_cast");
   return DFX_OK;

@@ -1,0 +1,45 @@
+"""Per-CTA timeline of the fused attention forward (debug hook
+dfx_debug_attn_trace): 0 start (after setup), 1 Q/K landed, 2 softmax ready,
+3 S in TMEM, 4 pass-1 done (warp 2), 5 P complete (MMA side), 6 pass-2 done,
+7 O in TMEM, 8 exit — µs from the earliest start."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2110_10802_b200 import _lib  # noqa: E402
+from paper_2110_10802_b200 import kernels as K  # noqa: E402
+
+B, S, NH = 8, 512, 12
+H = NH * 64
+lib = _lib.load()
+fn = lib.dfx_debug_attn_trace
+fn.argtypes = [ctypes.c_void_p]
+qkv = torch.randn(B * S, 3 * H, device="cuda").bfloat16()
+am = torch.zeros(B, S, device="cuda")
+keep = (torch.rand(B, NH, S, S, device="cuda") > 0.1).to(torch.uint8)
+ctx = torch.empty(B * S, H, device="cuda", dtype=torch.bfloat16)
+lse = torch.empty(B, NH, S, device="cuda")
+kr = torch.empty(B, NH, S, S // 32, device="cuda", dtype=torch.int32)
+kc = torch.empty_like(kr)
+run = lambda: K.attn_fwd(qkv, B, S, NH, am, keep, 1 / 0.9, 0.125, ctx, lse, kr, kc)  # noqa: E731
+for _ in range(3):
+    run()
+ncta = B * NH * S // 128
+tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
+fn(tr.data_ptr())
+run()
+torch.cuda.synchronize()
+fn(None)
+t = tr.view(ncta, 16).cpu().double()
+t0 = t[:, 0].min()
+rel = (t - t0) / 1e3
+print("cta   start   qk   sready  S_in   pass1   P_done  pass2   O_in   exit")
+for c in list(range(0, ncta, 37)) + [ncta - 1]:
+    print(f"{c:4d} " + " ".join(f"{rel[c, i].item():6.2f}" for i in range(9)))
+d = rel[:, 1:9] - rel[:, 0:8]
+names = ["setup->qk", "qk->sready", "sready->S", "S->pass1", "pass1->P", "P->pass2", "pass2->O", "O->exit"]
+print("mean phase durations (us):", {n: round(d[:, i].mean().item(), 2) for i, n in enumerate(names)})
+print("per-CTA total mean", (rel[:, 8] - rel[:, 0]).mean().item(), "kernel span", rel[:, 8].max().item())

@@ -6,10 +6,17 @@ import sys
 
 def main(path, top=40):
     rows = list(csv.reader(open(path)))
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+    for a, b in zip(starts, starts[1:]):
+        print("=====", rows[a][1][:100])
+        section(rows[a:b], top)
+
+
+def section(rows, top):
     hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
     hdr = rows[hdr_i]
     ix = {h: i for i, h in enumerate(hdr)}
-    data = [r for r in rows[hdr_i + 1:] if len(r) == len(hdr)]
+    data = [r for r in rows[hdr_i + 1:] if len(r) == len(hdr) and r[0] != "Address"]
     tot = sum(int(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in data)
     print(f"{len(data)} instructions, {tot} stall samples")
     data.sort(key=lambda r: -int(r[ix["Warp Stall Sampling (All Samples)"]] or 0))
