@@ -1,0 +1,646 @@
+// dwconv.cu — depthwise KSxKS convolution (stride 1/2), NHWC, sm_100a:
+// TMA row ring + register sliding window.
+//
+// The reference evaluates Conv(group=C) as a 9-tap loop nest with clamped
+// reads and ge() padding masks (lowering.py:930-1004; reference semantics
+// frontend.py:645-666) and differentiates it through the lowered nest
+// (autodiff.py:1623-1629, 1701-1745).  Here one CTA owns (image n, a band of
+// R output rows, a tile of Wt output columns, a chunk of Cb channels):
+//
+//   * a single producer thread streams the band's input rows, each a
+//     [Wb = (Wt-1)*s + KS columns][Cb channels] box, into a K-slot shared
+//     memory ring with cp.async.bulk.tensor (TMA) + mbarrier tx-counts.  TMA
+//     zero-fills everything outside the tensor, so the conv padding costs no
+//     predicates and no extra bytes; K = KS + 2s slots keep two output rows of
+//     loads in flight per CTA (two CTAs per SM);
+//   * threads = (V-channel vector, column segment): each walks its segment of
+//     output columns left to right holding a KS x KS window of input vectors in
+//     registers, so an output costs KS*s new shared-memory vectors, not KS^2;
+//   * outputs go straight from registers to HBM (V-channel vectors, every
+//     warp store covers whole pixels).
+//
+// Three modes share the loop:
+//   CONV_STATS (forward): z = conv(x, w), plus the per-CTA BatchNorm partial
+//       Welford sets of the unrounded z (frontend.py:558-591), merged in a
+//       fixed order (no atomics: bitwise reproducible);
+//   DZW (backward): dz = dBN(dswish(dy*s + dpool)) from (dy, z) rows streamed
+//       by TMA next to the x ring (the BN VJP autodiff.py:1557-1617 in closed
+//       form), dz stored for the dx pass, and dw[t] += window(x)[t] * dz with
+//       the UNROUNDED f32 dz — a bf16-rounded dz would break the BN-VJP
+//       orthogonality (sum dz = sum dz*z = 0) that dw cancels against;
+//   CONV (backward, stride 1): dx = conv(dz, flipped w) with the transposed
+//       padding (KS-1-pt, KS-1-pl).  Stride 2 uses a direct gather kernel.
+#include <algorithm>
+
+#include "common.cuh"
+#include "dwconv.h"
+#include "gemm.h"
+#include "tc_ptx.cuh"
+
+namespace dfx {
+namespace {
+
+enum { MODE_CONV = 0, MODE_STATS = 1, MODE_DZW = 2 };
+constexpr int kMaxThreads = 256;
+constexpr size_t kSmemBudget = 110 * 1024;  // two CTAs per SM
+
+template <int KS> struct VecOf { static constexpr int value = KS == 3 ? 4 : 2; };
+
+// V channels of T, raw in registers (bf16 unpacked on use)
+template <typename T, int V> struct RV;
+template <> struct RV<__nv_bfloat16, 4> {
+  uint2 r;
+  __device__ __forceinline__ void ld(const __nv_bfloat16* p) { r = *reinterpret_cast<const uint2*>(p); }
+  __device__ __forceinline__ void ldg(const __nv_bfloat16* p) { r = __ldg(reinterpret_cast<const uint2*>(p)); }
+  __device__ __forceinline__ float get(int i) const {
+    const uint32_t w = i < 2 ? r.x : r.y;
+    return __uint_as_float((i & 1) ? (w & 0xFFFF0000u) : (w << 16));
+  }
+};
+template <> struct RV<__nv_bfloat16, 2> {
+  uint32_t r;
+  __device__ __forceinline__ void ld(const __nv_bfloat16* p) { r = *reinterpret_cast<const uint32_t*>(p); }
+  __device__ __forceinline__ void ldg(const __nv_bfloat16* p) { r = __ldg(reinterpret_cast<const unsigned int*>(p)); }
+  __device__ __forceinline__ float get(int i) const { return __uint_as_float(i ? (r & 0xFFFF0000u) : (r << 16)); }
+};
+template <> struct RV<float, 4> {
+  float4 r;
+  __device__ __forceinline__ void ld(const float* p) { r = *reinterpret_cast<const float4*>(p); }
+  __device__ __forceinline__ void ldg(const float* p) { r = __ldg(reinterpret_cast<const float4*>(p)); }
+  __device__ __forceinline__ float get(int i) const { return i == 0 ? r.x : (i == 1 ? r.y : (i == 2 ? r.z : r.w)); }
+};
+template <> struct RV<float, 2> {
+  float2 r;
+  __device__ __forceinline__ void ld(const float* p) { r = *reinterpret_cast<const float2*>(p); }
+  __device__ __forceinline__ void ldg(const float* p) { r = __ldg(reinterpret_cast<const float2*>(p)); }
+  __device__ __forceinline__ float get(int i) const { return i ? r.y : r.x; }
+};
+
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+template <int V> __device__ __forceinline__ void stv(__nv_bfloat16* p, const float (&v)[V]) {
+  if constexpr (V == 4)
+    *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf2(v[0], v[1]), pack_bf2(v[2], v[3]));
+  else
+    *reinterpret_cast<uint32_t*>(p) = pack_bf2(v[0], v[1]);
+}
+template <int V> __device__ __forceinline__ void stv(float* p, const float (&v)[V]) {
+  if constexpr (V == 4)
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  else
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+}
+
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// bf16 path: one MUFU op (rel. error ~2^-11, below bf16 rounding); f32 keeps
+// the exact form for the 1e-4 parity bar
+template <typename T> __device__ __forceinline__ float sigm(float u) {
+  if constexpr (sizeof(T) == 2) return fmaf(0.5f, tanh_approx(0.5f * u), 0.5f);
+  else return 1.f / (1.f + __expf(-u));
+}
+
+struct Welford {
+  float n, mean, m2;
+};
+__device__ __forceinline__ Welford wmerge(Welford a, Welford b) {
+  const float n = a.n + b.n;
+  if (n == 0.f) return a;
+  const float d = b.mean - a.mean;
+  const float f = b.n / n;
+  return {n, a.mean + d * f, a.m2 + b.m2 + d * d * a.n * f};
+}
+
+struct RingP {
+  int Ho, Wo, C, pt, pl;
+  int Cb, Wt, Wb, R;
+  int ncb, nwt, nbands;
+  int nseg, L;
+  uint32_t in_slot, io_slot;  // bytes per ring slot (128-B multiples)
+  int flip;                   // CONV: w[KS*KS-1-t] (transposed conv)
+};
+
+template <typename T, int KS, int S, int MODE>
+__global__ void __launch_bounds__(kMaxThreads, 2)
+    dw_ring_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap dy_map,
+                   const __grid_constant__ CUtensorMap z_map, const RingP p, const float* __restrict__ w,
+                   T* __restrict__ out, float* __restrict__ part, const DzConsts dk) {
+  constexpr int V = VecOf<KS>::value;
+  constexpr int K = KS + 2 * S;
+  constexpr int T2 = KS * KS;
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+  T* ring = reinterpret_cast<T*>(sm);
+  T* dyr = reinterpret_cast<T*>(sm + K * p.in_slot);
+  T* zr = reinterpret_cast<T*>(sm + K * p.in_slot + 2 * p.io_slot);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + K * p.in_slot + (MODE == MODE_DZW ? 4 * p.io_slot : 0));
+
+  const int tid = threadIdx.x;
+  int b = blockIdx.x;
+  const int cb = b % p.ncb;
+  b /= p.ncb;
+  const int wt = b % p.nwt;
+  b /= p.nwt;
+  const int band = b % p.nbands;
+  const int n = b / p.nbands;
+  const int oy0 = band * p.R, nrows = min(p.R, p.Ho - oy0);
+  const int ox0 = wt * p.Wt, ncols = min(p.Wt, p.Wo - ox0);
+  const int NR = (nrows - 1) * S + KS;
+  const int iy0 = oy0 * S - p.pt, ix0 = ox0 * S - p.pl, c0 = cb * p.Cb;
+  const uint32_t in_el = p.in_slot / sizeof(T), io_el = p.io_slot / sizeof(T);
+  const uint32_t in_bytes = (uint32_t)(p.Wb * p.Cb * sizeof(T)), io_bytes = (uint32_t)(p.Wt * p.Cb * sizeof(T));
+
+  if (tid == 0) {
+    for (int i = 0; i < K + 2; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();  // every input below is produced by the previous kernel
+  pdl_trigger();
+  auto issue_in = [&](int j) {
+    uint64_t* bar = &bars[j % K];
+    mbar_expect_tx(bar, in_bytes);
+    tma_load_4d_cg<1>(&in_map, smem_u32(bar), ring + (j % K) * in_el, c0, ix0, iy0 + j, n);
+  };
+  auto issue_io = [&](int r) {
+    uint64_t* bar = &bars[K + (r & 1)];
+    mbar_expect_tx(bar, 2 * io_bytes);
+    tma_load_4d_cg<1>(&dy_map, smem_u32(bar), dyr + (r & 1) * io_el, c0, ox0, oy0 + r, n);
+    tma_load_4d_cg<1>(&z_map, smem_u32(bar), zr + (r & 1) * io_el, c0, ox0, oy0 + r, n);
+  };
+  if (tid == 0) {
+    for (int j = 0; j < min(K, NR); ++j) issue_in(j);
+    if (MODE == MODE_DZW)
+      for (int r = 0; r < min(2, nrows); ++r) issue_io(r);
+  }
+
+  const int CVn = p.Cb / V;
+  const int cv = tid % CVn, sg = tid / CVn;
+  const int xs = sg * p.L, xe = min(xs + p.L, ncols);
+  const bool act = xs < xe;
+  const int cc = c0 + cv * V;
+
+  float wr[MODE == MODE_DZW ? 1 : T2][V];
+  if constexpr (MODE != MODE_DZW) {
+#pragma unroll
+    for (int t = 0; t < T2; ++t)
+#pragma unroll
+      for (int i = 0; i < V; ++i) wr[t][i] = __ldg(w + (size_t)(p.flip ? T2 - 1 - t : t) * p.C + cc + i);
+  }
+  // DZW: dz = P*du + Cz*z + Bc, du = (dy*sv + dp) * swish'(z*P + Q)
+  float kP[V], kQ[V], kCz[V], kB[V], kS[V], kD[V];
+  if constexpr (MODE == MODE_DZW) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c = cc + i;
+      const float rs = dk.rstd[c], mu = dk.mean[c];
+      kP[i] = dk.gamma[c] * rs;
+      kQ[i] = dk.beta[c] - mu * kP[i];
+      const float mdu = dk.bnsum[c] * dk.inv_count, mdux = dk.bnsum[p.C + c] * dk.inv_count;
+      kCz[i] = -kP[i] * rs * mdux;
+      kB[i] = -kP[i] * mdu - kCz[i] * mu;
+      kS[i] = dk.s[(size_t)n * p.C + c];
+      kD[i] = dk.dpool[(size_t)n * p.C + c];
+    }
+  }
+  float st0[V], st1[V], shf[V];
+  float dwa[MODE == MODE_DZW ? T2 : 1][V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    st0[i] = 0.f;
+    st1[i] = 0.f;
+    shf[i] = 0.f;
+  }
+#pragma unroll
+  for (int t = 0; t < (MODE == MODE_DZW ? T2 : 1); ++t)
+#pragma unroll
+    for (int i = 0; i < V; ++i) dwa[t][i] = 0.f;
+  int cnt = 0;
+
+  for (int r = 0; r < nrows; ++r) {
+#pragma unroll
+    for (int ky = 0; ky < KS; ++ky) {
+      const int j = r * S + ky;
+      mbar_wait(&bars[j % K], (j / K) & 1);
+    }
+    if (MODE == MODE_DZW) mbar_wait(&bars[K + (r & 1)], (r >> 1) & 1);
+    if (act) {
+      const T* rows[KS];
+#pragma unroll
+      for (int ky = 0; ky < KS; ++ky) rows[ky] = ring + ((r * S + ky) % K) * in_el + cv * V;
+      RV<T, V> win[KS][KS];
+#pragma unroll
+      for (int ky = 0; ky < KS; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < KS; ++kx) win[ky][kx].ld(rows[ky] + (xs * S + kx) * p.Cb);
+      T* orow = out + (((size_t)n * p.Ho + oy0 + r) * p.Wo + ox0) * p.C + cc;
+      const T* dyrow = dyr + (r & 1) * io_el + cv * V;
+      const T* zrow = zr + (r & 1) * io_el + cv * V;
+      for (int x = xs; x < xe; ++x) {
+        if (x > xs) {
+#pragma unroll
+          for (int ky = 0; ky < KS; ++ky) {
+#pragma unroll
+            for (int kx = 0; kx < KS - S; ++kx) win[ky][kx] = win[ky][kx + S];
+#pragma unroll
+            for (int kx = KS - S; kx < KS; ++kx) win[ky][kx].ld(rows[ky] + (x * S + kx) * p.Cb);
+          }
+        }
+        if constexpr (MODE != MODE_DZW) {
+          float acc[V];
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] = 0.f;
+#pragma unroll
+          for (int ky = 0; ky < KS; ++ky)
+#pragma unroll
+            for (int kx = 0; kx < KS; ++kx)
+#pragma unroll
+              for (int i = 0; i < V; ++i) acc[i] = fmaf(win[ky][kx].get(i), wr[ky * KS + kx][i], acc[i]);
+          stv<V>(orow + (size_t)x * p.C, acc);
+          if constexpr (MODE == MODE_STATS) {
+            // shifted sums of the unrounded conv output
+            if (cnt == 0) {
+#pragma unroll
+              for (int i = 0; i < V; ++i) shf[i] = acc[i];
+            }
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+              const float d = acc[i] - shf[i];
+              st0[i] += d;
+              st1[i] = fmaf(d, d, st1[i]);
+            }
+            ++cnt;
+          }
+        } else {
+          RV<T, V> dv, zv;
+          dv.ld(dyrow + x * p.Cb);
+          zv.ld(zrow + x * p.Cb);
+          float dz[V];
+#pragma unroll
+          for (int i = 0; i < V; ++i) {
+            const float zz = zv.get(i);
+            const float u = fmaf(zz, kP[i], kQ[i]);
+            const float sgm = sigm<T>(u);
+            const float swp = sgm * fmaf(u, 1.f - sgm, 1.f);
+            const float du = fmaf(dv.get(i), kS[i], kD[i]) * swp;
+            dz[i] = fmaf(kP[i], du, fmaf(kCz[i], zz, kB[i]));
+          }
+          stv<V>(orow + (size_t)x * p.C, dz);
+#pragma unroll
+          for (int ky = 0; ky < KS; ++ky)
+#pragma unroll
+            for (int kx = 0; kx < KS; ++kx)
+#pragma unroll
+              for (int i = 0; i < V; ++i) dwa[ky * KS + kx][i] = fmaf(win[ky][kx].get(i), dz[i], dwa[ky * KS + kx][i]);
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with the rows that leave the window
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const int jn = r * S + q + K;
+        if (jn < NR) issue_in(jn);
+      }
+      if (MODE == MODE_DZW && r + 2 < nrows) issue_io(r + 2);
+    }
+  }
+
+  // ------------------------------------------------------------ CTA partials
+  // every issued load has been consumed: the ring is free scratch now
+  float* red = reinterpret_cast<float*>(sm);
+  const size_t tile = ((size_t)n * p.nbands + band) * p.nwt + wt;
+  if constexpr (MODE == MODE_STATS) {
+    float* s_n = red;
+    float* s_mean = red + p.nseg;
+    float* s_m2 = s_mean + p.nseg * p.Cb;
+    if (cv == 0) s_n[sg] = (float)cnt;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float m = cnt ? st0[i] / (float)cnt : 0.f;
+      s_mean[sg * p.Cb + cv * V + i] = shf[i] + m;
+      s_m2[sg * p.Cb + cv * V + i] = cnt ? fmaxf(st1[i] - st0[i] * m, 0.f) : 0.f;
+    }
+    __syncthreads();
+    for (int c = tid; c < p.Cb; c += blockDim.x) {
+      Welford acc = {0.f, 0.f, 0.f};
+      for (int j = 0; j < p.nseg; ++j) acc = wmerge(acc, Welford{s_n[j], s_mean[j * p.Cb + c], s_m2[j * p.Cb + c]});
+      part[(tile * 3 + 0) * p.C + c0 + c] = acc.n;
+      part[(tile * 3 + 1) * p.C + c0 + c] = acc.mean;
+      part[(tile * 3 + 2) * p.C + c0 + c] = acc.m2;
+    }
+  } else if constexpr (MODE == MODE_DZW) {
+#pragma unroll
+    for (int t = 0; t < T2; ++t) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) red[sg * p.Cb + cv * V + i] = dwa[t][i];
+      __syncthreads();
+      for (int c = tid; c < p.Cb; c += blockDim.x) {
+        float acc = 0.f;
+        for (int j = 0; j < p.nseg; ++j) acc += red[j * p.Cb + c];
+        part[(tile * T2 + t) * p.C + c0 + c] = acc;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// (n, mean, M2) partials [tiles][3][C] -> out [3][C], fixed merge order
+__global__ void __launch_bounds__(256) stats_merge_kernel(int ntiles, int C, const float* __restrict__ part,
+                                                          float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float sn[256], smn[256], sm2[256];
+  const int c = blockIdx.x;
+  Welford acc = {0.f, 0.f, 0.f};
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x)
+    acc = wmerge(acc, Welford{part[((size_t)t * 3) * C + c], part[((size_t)t * 3 + 1) * C + c],
+                              part[((size_t)t * 3 + 2) * C + c]});
+  sn[threadIdx.x] = acc.n;
+  smn[threadIdx.x] = acc.mean;
+  sm2[threadIdx.x] = acc.m2;
+  __syncthreads();
+  for (int sd = blockDim.x / 2; sd > 0; sd >>= 1) {
+    if (threadIdx.x < sd) {
+      const Welford m = wmerge(Welford{sn[threadIdx.x], smn[threadIdx.x], sm2[threadIdx.x]},
+                               Welford{sn[threadIdx.x + sd], smn[threadIdx.x + sd], sm2[threadIdx.x + sd]});
+      sn[threadIdx.x] = m.n;
+      smn[threadIdx.x] = m.mean;
+      sm2[threadIdx.x] = m.m2;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[c] = sn[0];
+    out[C + c] = smn[0];
+    out[2 * C + c] = sm2[0];
+  }
+}
+
+// dw[t][c] = sum_b part[b][t][c]: block = 32 channels x 8 part lanes, fixed order
+__global__ void __launch_bounds__(256) taps_sum_kernel(int nparts, int taps, int C, const float* __restrict__ part,
+                                                       float* __restrict__ dw) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, pl = threadIdx.x >> 5;
+  const int t = blockIdx.y, c = blockIdx.x * 32 + lane;
+  float acc = 0.f;
+  if (c < C) {
+#pragma unroll 4
+    for (int b = pl; b < nparts; b += 8) acc += part[((size_t)b * taps + t) * C + c];
+  }
+  red[pl][lane] = acc;
+  __syncthreads();
+  if (pl == 0 && c < C) {
+    float s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s2 += red[j][lane];
+    dw[t * C + c] = s2;
+  }
+}
+
+// dx for stride 2 (a gather: each input pixel receives the taps whose
+// output position has the right parity), V channels per thread
+template <typename T, int KS>
+__global__ void __launch_bounds__(256) dw_dx_s2_kernel(const DwShape g, const T* __restrict__ dz,
+                                                       const float* __restrict__ w, T* __restrict__ dx) {
+  constexpr int V = VecOf<KS>::value;
+  pdl_wait();
+  pdl_trigger();
+  const int CVn = g.C / V;
+  const int64_t total = (int64_t)g.N * g.Hi * g.Wi * CVn;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int cv = (int)(idx % CVn);
+    const int64_t pix = idx / CVn;
+    const int ix = (int)(pix % g.Wi);
+    const int iy = (int)((pix / g.Wi) % g.Hi);
+    const int n = (int)(pix / ((int64_t)g.Wi * g.Hi));
+    const int c = cv * V;
+    float acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+#pragma unroll
+    for (int ky = 0; ky < KS; ++ky) {
+      const int ty = iy + g.pt - ky;
+      if (ty < 0 || (ty & 1) || (ty >> 1) >= g.Ho) continue;
+#pragma unroll
+      for (int kx = 0; kx < KS; ++kx) {
+        const int tx = ix + g.pl - kx;
+        if (tx < 0 || (tx & 1) || (tx >> 1) >= g.Wo) continue;
+        RV<T, V> v;
+        v.ldg(dz + (((size_t)n * g.Ho + (ty >> 1)) * g.Wo + (tx >> 1)) * g.C + c);
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = fmaf(v.get(i), __ldg(w + (size_t)(ky * KS + kx) * g.C + c + i), acc[i]);
+      }
+    }
+    stv<V>(dx + pix * g.C + c, acc);
+  }
+}
+
+// ---------------------------------------------------------------- planning
+struct Plan {
+  RingP p;
+  int threads, grid;
+  size_t smem;
+};
+
+size_t rnd128(size_t b) { return (b + 127) & ~size_t(127); }
+
+int pick_cb(int C, int V, int esz) {
+  for (int d = std::min(C, 128); d >= V; --d)
+    if (C % d == 0 && d % V == 0 && (d * esz) % 16 == 0) return d;
+  return 0;
+}
+
+// in grid (Hi, Wi) -> out grid (Ho, Wo) with (pt, pl): the correlation this launch computes
+bool make_plan(int N, int Hi, int Wi, int Ho, int Wo, int C, int ks, int s, int pt, int pl, int esz, int mode,
+               Plan* pl_out) {
+  (void)Hi;
+  (void)Wi;
+  if (ks != 3 && ks != 5) return false;
+  if (s != 1 && s != 2) return false;
+  if ((C * esz) % 16 != 0) return false;
+  const int V = ks == 3 ? 4 : 2;
+  const int K = ks + 2 * s;
+  const int Cb = pick_cb(C, V, esz);
+  if (!Cb) return false;
+  const int CVn = Cb / V;
+  if (CVn > kMaxThreads) return false;
+  auto smem_of = [&](int wt) {
+    const size_t in_slot = rnd128((size_t)((wt - 1) * s + ks) * Cb * esz);
+    const size_t io_slot = rnd128((size_t)wt * Cb * esz);
+    return K * in_slot + (mode == MODE_DZW ? 4 * io_slot : 0) + (K + 2) * 8 + 128;
+  };
+  int Wt = std::min(Wo, std::min(256, (256 - ks) / s + 1));
+  while (Wt > 1 && smem_of(Wt) > kSmemBudget) --Wt;
+  if (smem_of(Wt) > kSmemBudget) return false;
+  const int nwt = (Wo + Wt - 1) / Wt;
+  Wt = (Wo + nwt - 1) / nwt;
+  const int nseg_max = kMaxThreads / CVn;
+  const int L = (Wt + nseg_max - 1) / nseg_max;
+  const int nseg = (Wt + L - 1) / L;
+  RingP p{};
+  p.Ho = Ho;
+  p.Wo = Wo;
+  p.C = C;
+  p.pt = pt;
+  p.pl = pl;
+  p.Cb = Cb;
+  p.Wt = Wt;
+  p.Wb = (Wt - 1) * s + ks;
+  p.ncb = C / Cb;
+  p.nwt = nwt;
+  p.nseg = nseg;
+  p.L = L;
+  p.in_slot = (uint32_t)rnd128((size_t)p.Wb * Cb * esz);
+  p.io_slot = (uint32_t)rnd128((size_t)Wt * Cb * esz);
+  // reduction scratch must fit in the ring
+  const size_t red = (size_t)nseg * (1 + 2 * Cb) * 4;
+  if (red > (size_t)K * p.in_slot) return false;
+  // band height: fewest waves x rows per CTA (2 CTAs per SM)
+  const long slots = 2L * num_sms();
+  long best = -1;
+  int bestR = Ho;
+  for (int R = 1; R <= Ho; ++R) {
+    const int nb = (Ho + R - 1) / R;
+    if ((Ho + nb - 1) / nb != R) continue;
+    const long ctas = (long)N * nb * nwt * p.ncb;
+    const long waves = (ctas + slots - 1) / slots;
+    const long cost = waves * ((long)(R - 1) * s + ks + 4);
+    if (best < 0 || cost < best) {
+      best = cost;
+      bestR = R;
+    }
+  }
+  p.R = bestR;
+  p.nbands = (Ho + bestR - 1) / bestR;
+  pl_out->p = p;
+  pl_out->threads = CVn * nseg;
+  pl_out->grid = N * p.nbands * nwt * p.ncb;
+  pl_out->smem = smem_of(Wt);
+  return true;
+}
+
+int tmap(CUtensorMap* m, const void* base, int esz, int N, int H, int W, int C, int Cb, int box_w) {
+  return make_map(m, base, esz, (uint64_t)C, (uint64_t)W, C, H, (int64_t)W * C, N, (int64_t)H * W * C, (uint32_t)Cb,
+                  (uint32_t)box_w, false);
+}
+
+template <typename T, int KS, int S, int MODE>
+int launch_ring(const Plan& pl, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const float* w,
+                void* out, float* part, const DzConsts& dk, cudaStream_t st) {
+  auto k = dw_ring_kernel<T, KS, S, MODE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  launch_k(k, pl.grid, pl.threads, pl.smem, st, a, b, c, pl.p, w, (T*)out, part, dk);
+  DFX_LAUNCH_CHECK("dwconv ring kernel");
+  return DFX_OK;
+}
+
+template <typename T, int MODE>
+int dispatch_ring(int ks, int s, const Plan& pl, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                  const float* w, void* out, float* part, const DzConsts& dk, cudaStream_t st) {
+  if (ks == 3 && s == 1) return launch_ring<T, 3, 1, MODE>(pl, a, b, c, w, out, part, dk, st);
+  if (ks == 3 && s == 2) return launch_ring<T, 3, 2, MODE>(pl, a, b, c, w, out, part, dk, st);
+  if (ks == 5 && s == 1) return launch_ring<T, 5, 1, MODE>(pl, a, b, c, w, out, part, dk, st);
+  if (ks == 5 && s == 2) return launch_ring<T, 5, 2, MODE>(pl, a, b, c, w, out, part, dk, st);
+  return fail(DFX_ERR_UNSUPPORTED, "dwconv: kernel size must be 3 or 5, stride 1 or 2");
+}
+
+int esz_of(int dtype) { return dtype == DFX_BF16 ? 2 : 4; }
+
+}  // namespace
+
+bool dw_ring_ok(const DwShape& g, int esz) {
+  Plan a, b, c;
+  return make_plan(g.N, g.Hi, g.Wi, g.Ho, g.Wo, g.C, g.ks, g.s, g.pt, g.pl, esz, MODE_STATS, &a) &&
+         make_plan(g.N, g.Hi, g.Wi, g.Ho, g.Wo, g.C, g.ks, g.s, g.pt, g.pl, esz, MODE_DZW, &b) &&
+         (g.s == 2 || make_plan(g.N, g.Ho, g.Wo, g.Hi, g.Wi, g.C, g.ks, 1, g.ks - 1 - g.pt, g.ks - 1 - g.pl, esz,
+                                MODE_CONV, &c));
+}
+
+size_t dw_stat_tiles(const DwShape& g, int esz) {
+  Plan pl;
+  if (!make_plan(g.N, g.Hi, g.Wi, g.Ho, g.Wo, g.C, g.ks, g.s, g.pt, g.pl, esz, MODE_STATS, &pl)) return 0;
+  return (size_t)g.N * pl.p.nbands * pl.p.nwt;
+}
+
+size_t dw_dzw_tiles(const DwShape& g, int esz) {
+  Plan pl;
+  if (!make_plan(g.N, g.Hi, g.Wi, g.Ho, g.Wo, g.C, g.ks, g.s, g.pt, g.pl, esz, MODE_DZW, &pl)) return 0;
+  return (size_t)g.N * pl.p.nbands * pl.p.nwt;
+}
+
+int dw_conv_stats(int dtype, const DwShape& g, const void* x, const float* w, void* z, float* part,
+                  float* stats_out, cudaStream_t st) {
+  const int esz = esz_of(dtype);
+  Plan pl;
+  if (!make_plan(g.N, g.Hi, g.Wi, g.Ho, g.Wo, g.C, g.ks, g.s, g.pt, g.pl, esz, MODE_STATS, &pl))
+    return fail(DFX_ERR_UNSUPPORTED, "dwconv: shape not supported by the TMA ring path");
+  CUtensorMap mx;
+  if (int rc = tmap(&mx, x, esz, g.N, g.Hi, g.Wi, g.C, pl.p.Cb, pl.p.Wb)) return rc;
+  DzConsts none{};
+  int rc = dtype == DFX_BF16 ? dispatch_ring<__nv_bfloat16, MODE_STATS>(g.ks, g.s, pl, mx, mx, mx, w, z, part, none, st)
+                             : dispatch_ring<float, MODE_STATS>(g.ks, g.s, pl, mx, mx, mx, w, z, part, none, st);
+  if (rc) return rc;
+  launch_k(stats_merge_kernel, g.C, 256, 0, st, (int)((size_t)g.N * pl.p.nbands * pl.p.nwt), g.C, part, stats_out);
+  DFX_LAUNCH_CHECK("dwconv stats merge");
+  return DFX_OK;
+}
+
+int dw_dz_dw(int dtype, const DwShape& g, const void* x, const void* dy, const void* z, const DzConsts& k, void* dz,
+             float* part, float* dw_out, cudaStream_t st) {
+  const int esz = esz_of(dtype);
+  Plan pl;
+  if (!make_plan(g.N, g.Hi, g.Wi, g.Ho, g.Wo, g.C, g.ks, g.s, g.pt, g.pl, esz, MODE_DZW, &pl))
+    return fail(DFX_ERR_UNSUPPORTED, "dwconv: shape not supported by the TMA ring path");
+  CUtensorMap mx, mdy, mz;
+  if (int rc = tmap(&mx, x, esz, g.N, g.Hi, g.Wi, g.C, pl.p.Cb, pl.p.Wb)) return rc;
+  if (int rc = tmap(&mdy, dy, esz, g.N, g.Ho, g.Wo, g.C, pl.p.Cb, pl.p.Wt)) return rc;
+  if (int rc = tmap(&mz, z, esz, g.N, g.Ho, g.Wo, g.C, pl.p.Cb, pl.p.Wt)) return rc;
+  int rc = dtype == DFX_BF16 ? dispatch_ring<__nv_bfloat16, MODE_DZW>(g.ks, g.s, pl, mx, mdy, mz, nullptr, dz, part, k, st)
+                             : dispatch_ring<float, MODE_DZW>(g.ks, g.s, pl, mx, mdy, mz, nullptr, dz, part, k, st);
+  if (rc) return rc;
+  const int taps = g.ks * g.ks;
+  launch_k(taps_sum_kernel, dim3((unsigned)((g.C + 31) / 32), (unsigned)taps), 256, 0, st,
+           (int)((size_t)g.N * pl.p.nbands * pl.p.nwt), taps, g.C, part, dw_out);
+  DFX_LAUNCH_CHECK("dwconv dw sum");
+  return DFX_OK;
+}
+
+int dw_dx(int dtype, const DwShape& g, const void* dz, const float* w, void* dx, cudaStream_t st) {
+  const int esz = esz_of(dtype);
+  if (g.s == 2) {
+    const int V = g.ks == 3 ? 4 : 2;
+    if (g.C % V) return fail(DFX_ERR_UNSUPPORTED, "dwconv dx: channels must be a multiple of the vector width");
+    const int64_t total = (int64_t)g.N * g.Hi * g.Wi * (g.C / V);
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+    if (dtype == DFX_BF16) {
+      if (g.ks == 3) launch_k(dw_dx_s2_kernel<__nv_bfloat16, 3>, grid, 256, 0, st, g, (const __nv_bfloat16*)dz, w, (__nv_bfloat16*)dx);
+      else launch_k(dw_dx_s2_kernel<__nv_bfloat16, 5>, grid, 256, 0, st, g, (const __nv_bfloat16*)dz, w, (__nv_bfloat16*)dx);
+    } else {
+      if (g.ks == 3) launch_k(dw_dx_s2_kernel<float, 3>, grid, 256, 0, st, g, (const float*)dz, w, (float*)dx);
+      else launch_k(dw_dx_s2_kernel<float, 5>, grid, 256, 0, st, g, (const float*)dz, w, (float*)dx);
+    }
+    DFX_LAUNCH_CHECK("dwconv dx (stride 2)");
+    return DFX_OK;
+  }
+  Plan pl;
+  const int pt = g.ks - 1 - g.pt, pleft = g.ks - 1 - g.pl;
+  if (!make_plan(g.N, g.Ho, g.Wo, g.Hi, g.Wi, g.C, g.ks, 1, pt, pleft, esz, MODE_CONV, &pl))
+    return fail(DFX_ERR_UNSUPPORTED, "dwconv dx: shape not supported by the TMA ring path");
+  pl.p.flip = 1;
+  CUtensorMap mdz;
+  if (int rc = tmap(&mdz, dz, esz, g.N, g.Ho, g.Wo, g.C, pl.p.Cb, pl.p.Wb)) return rc;
+  DzConsts none{};
+  return dtype == DFX_BF16 ? dispatch_ring<__nv_bfloat16, MODE_CONV>(g.ks, 1, pl, mdz, mdz, mdz, w, dx, nullptr, none, st)
+                           : dispatch_ring<float, MODE_CONV>(g.ks, 1, pl, mdz, mdz, mdz, w, dx, nullptr, none, st);
+}
+
+}  // namespace dfx

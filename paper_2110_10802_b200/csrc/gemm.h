@@ -1,5 +1,6 @@
 // gemm.h — internal entry points of the two contraction paths.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "dfx.h"
@@ -12,4 +13,7 @@ bool gemm_tc_supported(const dfx_gemm_args& p);
 int gemm_tc(const dfx_gemm_args& p, cudaStream_t st);
 size_t gemm_tc_workspace(const dfx_gemm_args& p);
 void gemm_tc_set_trace(void* buf);
+// 4-D TMA tensor map (gemm_tc.cu): dims (inner..outer) = {d0, d1, nb2, nb1}, strides in elements
+int make_map(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t d1, int64_t s1, int64_t nb2,
+             int64_t sb2, int64_t nb1, int64_t sb1, uint32_t box0, uint32_t box1, bool swizzle128);
 }  // namespace dfx

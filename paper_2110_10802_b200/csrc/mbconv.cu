@@ -27,7 +27,10 @@
 // Only two full-tensor backward passes read (dy, z) + (dy, z, x) and one
 // writes dx.  All reductions are fixed-order (Welford/Chan merges, no float
 // atomics): results are bitwise reproducible.
+#include <algorithm>
+
 #include "common.cuh"
+#include "dwconv.h"
 
 namespace dfx {
 namespace {
@@ -687,298 +690,6 @@ __global__ void dw_finalize_kernel(int nparts, int C, const float* __restrict__ 
   dw[idx] = acc;
 }
 
-// ---------------------------------------------------------------- stride-1 fast path
-// 3x3 depthwise correlation at stride 1, NHWC.  Thread = (4-channel group,
-// output column); it walks down a band of rows keeping a 3x3 window of
-// input vectors in registers (raw bf16 / f32), so each output row costs 3
-// new 8-byte (bf16) loads instead of 9, and the horizontal neighbours are L1
-// hits from the adjacent threads (channel groups are fastest in a warp:
-// every load instruction of a warp covers ~2.7 consecutive pixels = fully
-// coalesced).
-//   FWD: out = z[oy,ox] = sum in[oy+ky-pt, ox+kx-pl] w[ky][kx], in = x,
-//        + per-CTA BN partial statistics (count, mean, M2) per channel
-//   BWD: out = dx[iy,ix] = sum dz[iy+ky-(2-pt), ix+kx-(2-pl)] w[2-ky][2-kx]
-//        (the transposed conv of the lowered loop nest, lowering.py:930-1004)
-//        and dw[2-ky][2-kx] += x[iy,ix] * dz[...] — both from the same window.
-struct S1Args {
-  int N, Hi, Wi, Ho, Wo, C;
-  int pt, pl;       // top/left padding of the correlation on `in`
-  int rows_per_band, bands, xb;
-};
-
-template <typename T> struct Raw4;
-template <> struct Raw4<__nv_bfloat16> {
-  uint2 r;
-  __device__ __forceinline__ void load(const __nv_bfloat16* p) { r = __ldg(reinterpret_cast<const uint2*>(p)); }
-  __device__ __forceinline__ void zero() { r = make_uint2(0, 0); }
-  __device__ __forceinline__ float get(int i) const {
-    const uint32_t w = i < 2 ? r.x : r.y;
-    return __uint_as_float((i & 1) ? (w & 0xFFFF0000u) : (w << 16));
-  }
-};
-template <> struct Raw4<float> {
-  float4 r;
-  __device__ __forceinline__ void load(const float* p) { r = __ldg(reinterpret_cast<const float4*>(p)); }
-  __device__ __forceinline__ void zero() { r = make_float4(0.f, 0.f, 0.f, 0.f); }
-  __device__ __forceinline__ float get(int i) const { return i == 0 ? r.x : (i == 1 ? r.y : (i == 2 ? r.z : r.w)); }
-};
-__device__ __forceinline__ void store4(__nv_bfloat16* p, const float (&v)[4]) {
-  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
-  *reinterpret_cast<uint2*>(p) = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
-}
-__device__ __forceinline__ void store4(float* p, const float (&v)[4]) {
-  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-}
-
-template <typename T, bool BWD>
-__global__ void __launch_bounds__(256, 2) dw3x3_s1_kernel(S1Args a, const T* __restrict__ in, const float* __restrict__ w,
-                                                           T* __restrict__ out, const T* __restrict__ xin,
-                                                           float* __restrict__ part) {
-  pdl_trigger();
-  pdl_wait();
-  extern __shared__ float sm[];
-  const int CG = a.C / 4;
-  const int cg = threadIdx.x % CG, xl = threadIdx.x / CG;
-  const int n = blockIdx.x / a.bands, band = blockIdx.x % a.bands;
-  const int ox = blockIdx.y * a.xb + xl;
-  const bool act = xl < a.xb && ox < a.Wo;
-  const int oy0 = band * a.rows_per_band, oy1 = min(oy0 + a.rows_per_band, a.Ho);
-  const int c0 = cg * 4;
-  float wr[9][4];
-#pragma unroll
-  for (int t = 0; t < 9; ++t) {
-    const float4 v = act ? __ldg(reinterpret_cast<const float4*>(w + (BWD ? 8 - t : t) * a.C + c0))
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-    wr[t][0] = v.x; wr[t][1] = v.y; wr[t][2] = v.z; wr[t][3] = v.w;
-  }
-  int ixk[3];
-  bool vk[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    ixk[k] = ox + k - a.pl;
-    vk[k] = act && ixk[k] >= 0 && ixk[k] < a.Wi;
-  }
-  const T* img = in + (size_t)n * a.Hi * a.Wi * a.C + c0;
-  auto load_row = [&](int iy, Raw4<T>(&r)[3]) {
-    const bool rv = iy >= 0 && iy < a.Hi;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      if (rv && vk[k]) r[k].load(img + ((size_t)iy * a.Wi + ixk[k]) * a.C);
-      else r[k].zero();
-    }
-  };
-  auto load_x = [&](int oy, Raw4<T>& r) {
-    if (BWD && act && oy < oy1) r.load(xin + (((size_t)n * a.Ho + oy) * a.Wo + ox) * a.C + c0);
-    else r.zero();
-  };
-  // window rows w0..w2 plus two prefetched rows p1, p2 (loads issued two
-  // output rows before use, so each warp keeps ~6 loads in flight)
-  Raw4<T> w0[3], w1[3], w2[3], p1[3], p2[3], x1, x2;
-  load_row(oy0 - a.pt, w0);
-  load_row(oy0 - a.pt + 1, w1);
-  load_row(oy0 - a.pt + 2, p1);
-  load_row(oy0 - a.pt + 3, p2);
-  load_x(oy0, x1);
-  load_x(oy0 + 1, x2);
-  // FWD: shifted sums for BN statistics; BWD: dw accumulators
-  float st0[4], st1[4], shift[4], dwa[BWD ? 9 : 1][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) { st0[i] = 0.f; st1[i] = 0.f; shift[i] = 0.f; }
-#pragma unroll
-  for (int t = 0; t < (BWD ? 9 : 1); ++t)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) dwa[t][i] = 0.f;
-  int cnt = 0;
-  for (int oy = oy0; oy < oy1; ++oy) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { w2[k] = p1[k]; p1[k] = p2[k]; }
-    load_row(oy - a.pt + 4, p2);
-    const Raw4<T> xc = x1;
-    if (BWD) {
-      x1 = x2;
-      load_x(oy + 2, x2);
-    }
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int kx = 0; kx < 3; ++kx)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float v0 = w0[kx].get(i), v1 = w1[kx].get(i), v2 = w2[kx].get(i);
-        acc[i] = fmaf(v0, wr[kx][i], acc[i]);
-        acc[i] = fmaf(v1, wr[3 + kx][i], acc[i]);
-        acc[i] = fmaf(v2, wr[6 + kx][i], acc[i]);
-        if (BWD) {
-          const float xv = xc.get(i);
-          dwa[kx][i] = fmaf(xv, v0, dwa[kx][i]);
-          dwa[3 + kx][i] = fmaf(xv, v1, dwa[3 + kx][i]);
-          dwa[6 + kx][i] = fmaf(xv, v2, dwa[6 + kx][i]);
-        }
-      }
-    if (act) {
-      store4(out + (((size_t)n * a.Ho + oy) * a.Wo + ox) * a.C + c0, acc);
-      if (!BWD) {
-        // statistics of the unrounded conv output (as the oracle's storage model)
-        if (cnt == 0) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) shift[i] = acc[i];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float d = acc[i] - shift[i];
-          st0[i] += d;
-          st1[i] = fmaf(d, d, st1[i]);
-        }
-        ++cnt;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { w0[k] = w1[k]; w1[k] = w2[k]; }
-  }
-  const int XB = a.xb;
-  const int tile = blockIdx.x * gridDim.y + blockIdx.y;
-  if (!BWD) {
-    // per-thread (n, mean, M2) -> fixed-order Chan merge over the CTA's columns
-    float* s_n = sm;                  // [XB]
-    float* s_mean = sm + XB;          // [XB][C]
-    float* s_m2 = s_mean + XB * a.C;  // [XB][C]
-    if (xl < XB) {
-      const float fn = (float)cnt;
-      if (cg == 0) s_n[xl] = fn;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float m = cnt ? st0[i] / fn : 0.f;
-        s_mean[xl * a.C + c0 + i] = shift[i] + m;
-        s_m2[xl * a.C + c0 + i] = cnt ? fmaxf(st1[i] - st0[i] * m, 0.f) : 0.f;
-      }
-    }
-    __syncthreads();
-    for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
-      Welford acc = {0.f, 0.f, 0.f};
-      for (int j = 0; j < XB; ++j) acc = merge(acc, Welford{s_n[j], s_mean[j * a.C + c], s_m2[j * a.C + c]});
-      part[((size_t)tile * 3 + 0) * a.C + c] = acc.n;
-      part[((size_t)tile * 3 + 1) * a.C + c] = acc.mean;
-      part[((size_t)tile * 3 + 2) * a.C + c] = acc.m2;
-    }
-  } else {
-    // dw partials of this CTA, fixed order over its columns, tap by tap
-    for (int t = 0; t < 9; ++t) {
-      if (xl < XB) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) sm[xl * a.C + c0 + i] = dwa[t][i];
-      }
-      __syncthreads();
-      for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
-        float acc = 0.f;
-        for (int j = 0; j < XB; ++j) acc += sm[j * a.C + c];
-        part[((size_t)tile * 9 + (8 - t)) * a.C + c] = acc;
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// BN statistics merge over CTA partials [tiles][3][C] -> out [3][C] (fixed order)
-__global__ void __launch_bounds__(kThreads) bn_merge3_kernel(int ntiles, int C, const float* __restrict__ part,
-                                                             float* __restrict__ out) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float sn[kThreads], smn[kThreads], sm2[kThreads];
-  const int c = blockIdx.x;
-  Welford acc = {0.f, 0.f, 0.f};
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x)
-    acc = merge(acc, Welford{part[((size_t)t * 3) * C + c], part[((size_t)t * 3 + 1) * C + c],
-                             part[((size_t)t * 3 + 2) * C + c]});
-  sn[threadIdx.x] = acc.n; smn[threadIdx.x] = acc.mean; sm2[threadIdx.x] = acc.m2;
-  __syncthreads();
-  for (int sd = blockDim.x / 2; sd > 0; sd >>= 1) {
-    if (threadIdx.x < sd) {
-      Welford m = merge(Welford{sn[threadIdx.x], smn[threadIdx.x], sm2[threadIdx.x]},
-                        Welford{sn[threadIdx.x + sd], smn[threadIdx.x + sd], sm2[threadIdx.x + sd]});
-      sn[threadIdx.x] = m.n; smn[threadIdx.x] = m.mean; sm2[threadIdx.x] = m.m2;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    out[c] = sn[0];
-    out[C + c] = smn[0];
-    out[2 * C + c] = sm2[0];
-  }
-}
-
-// dw[t][c] = sum over CTA partials [parts][9][C]: block = 32 channels x 8
-// part lanes (coalesced 128-byte rows), fixed-order combine (deterministic).
-__global__ void __launch_bounds__(256) dw_sum_kernel(int nparts, int C, const float* __restrict__ part,
-                                                     float* __restrict__ dw) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float red[8][33];
-  const int lane = threadIdx.x & 31, pl = threadIdx.x >> 5;
-  const int t = blockIdx.y, c = blockIdx.x * 32 + lane;
-  float acc = 0.f;
-  if (c < C) {
-#pragma unroll 4
-    for (int b = pl; b < nparts; b += 8) acc += part[((size_t)b * 9 + t) * C + c];
-  }
-  red[pl][lane] = acc;
-  __syncthreads();
-  if (pl == 0 && c < C) {
-    float s2 = 0.f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s2 += red[j][lane];
-    dw[t * C + c] = s2;
-  }
-}
-
-// dz = dBN(dswish(dy * s + dpool)) elementwise (BN VJP autodiff.py:1557-1617 in
-// the closed form dz = A*du + B + Cz*z, du = (dy*s + dpool) * swish'(z*P + Q)).
-template <typename T, int V>
-__global__ void __launch_bounds__(kThreads) dz_kernel(Geo g, const T* __restrict__ dy, const T* __restrict__ z,
-                                                      BnParams bn, const float* __restrict__ s,
-                                                      const float* __restrict__ dpool, const float* __restrict__ bnsum,
-                                                      float inv_count, T* __restrict__ dz) {
-  pdl_trigger();
-  pdl_wait();
-  const int CV = g.C / V;
-  const int PY = blockDim.x / CV;
-  const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
-  if (py >= PY) return;
-  const int tile = blockIdx.x;
-  const int n = tile / g.tiles_per_img;
-  const int r0 = (tile % g.tiles_per_img) * g.tile_rows;
-  const int r1 = min(r0 + g.tile_rows, g.Ho);
-  const int c0 = cv * V;
-  float P[V], Q[V], A[V], Bc[V], Cz[V], sv[V], dp[V];
-#pragma unroll
-  for (int i = 0; i < V; ++i) {
-    const int c = c0 + i;
-    const float rs = bn.rstd[c], gm = bn.gamma[c], mu = bn.mean[c];
-    P[i] = gm * rs;
-    Q[i] = bn.beta[c] - mu * P[i];
-    const float mdu = bnsum[c] * inv_count, mdux = bnsum[g.C + c] * inv_count;
-    A[i] = P[i];
-    Cz[i] = -P[i] * rs * mdux;
-    Bc[i] = -P[i] * mdu - Cz[i] * mu;
-    sv[i] = s[(size_t)n * g.C + c];
-    dp[i] = dpool[(size_t)n * g.C + c];
-  }
-  const size_t base = ((size_t)n * g.Ho + r0) * g.Wo * g.C + c0;
-  const int npix = (r1 - r0) * g.Wo;
-  for (int p = py; p < npix; p += PY) {
-    Vec<T, V> dv, zv, o;
-    dv.load(dy + base + (size_t)p * g.C);
-    zv.load(z + base + (size_t)p * g.C);
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const float u = fmaf(zv.v[i], P[i], Q[i]);
-      const float sg = sigm<T>(u);
-      const float swp = sg * fmaf(u, 1.f - sg, 1.f);
-      const float du = fmaf(dv.v[i], sv[i], dp[i]) * swp;
-      o.v[i] = fmaf(A[i], du, fmaf(Cz[i], zv.v[i], Bc[i]));
-    }
-    o.store(dz + base + (size_t)p * g.C);
-  }
-}
-
 // ---------------------------------------------------------------- host
 int make_geo(int64_t N, int64_t H, int64_t W, int64_t C, int stride, const int* pads, int vec, Geo* g,
              const char* op) {
@@ -1001,30 +712,15 @@ int make_geo(int64_t N, int64_t H, int64_t W, int64_t C, int stride, const int* 
 
 template <typename T> constexpr int vec_of() { return MbVec<T>::value; }
 
-// stride-1 fast path geometry: CTA = (image, band of rows) x column tile
-constexpr int kS1BandFwd = 32, kS1BandBwd = 56;
-inline bool s1_ok(const Geo& g) { return g.stride == 1 && g.C % 4 == 0 && g.C / 4 <= 256; }
-inline S1Args s1_args(const Geo& g, bool bwd) {
-  S1Args a;
-  a.N = g.N; a.C = g.C;
-  if (!bwd) {
-    a.Hi = g.H; a.Wi = g.W; a.Ho = g.Ho; a.Wo = g.Wo; a.pt = g.pt; a.pl = g.pl;
-  } else {  // dx over the input grid from dz over the output grid
-    a.Hi = g.Ho; a.Wi = g.Wo; a.Ho = g.H; a.Wo = g.W; a.pt = 2 - g.pt; a.pl = 2 - g.pl;
-  }
-  a.xb = std::max(1, 256 / (g.C / 4));
-  const int band = bwd ? kS1BandBwd : kS1BandFwd;
-  a.rows_per_band = std::min(band, a.Ho);
-  a.bands = (a.Ho + a.rows_per_band - 1) / a.rows_per_band;
-  return a;
-}
-inline dim3 s1_grid(const S1Args& a) { return dim3((unsigned)(a.N * a.bands), (unsigned)((a.Wo + a.xb - 1) / a.xb)); }
-inline size_t s1_tiles(const S1Args& a) { const dim3 gr = s1_grid(a); return (size_t)gr.x * gr.y; }
-// float offset of the dz buffer in the workspace: past the generic scratch
-// (`fl` floats, computed with SE = 1) and the fast-path partials, 256-B aligned
-inline size_t s1_dz_offset(const Geo& g, size_t fl) {
-  const size_t f3 = s1_tiles(s1_args(g, false)) * 3 * g.C, b9 = s1_tiles(s1_args(g, true)) * 9 * g.C;
-  return (std::max(fl, std::max(f3, b9)) + 63) / 64 * 64;
+// TMA ring path (dwconv.cu) geometry of this block: 3x3 taps
+inline DwShape dw_shape(const Geo& g) { return DwShape{g.N, g.H, g.W, g.Ho, g.Wo, g.C, 3, g.stride, g.pt, g.pl}; }
+inline bool ring_ok(const Geo& g) { return dw_ring_ok(dw_shape(g), 2) && dw_ring_ok(dw_shape(g), 4); }
+// ring-path scratch (floats): partials [tiles][9][C] (>= [tiles][3][C]) then dz
+inline size_t ring_part_floats(const Geo& g) {
+  const DwShape d = dw_shape(g);
+  size_t t = 0;
+  for (int esz : {2, 4}) t = std::max(t, std::max(dw_stat_tiles(d, esz) * 3, dw_dzw_tiles(d, esz) * 9));
+  return (t * g.C + 63) / 64 * 64;
 }
 
 }  // namespace
@@ -1038,17 +734,7 @@ template <typename T>
 int mb_forward(const Geo& g, const void* x, const float* w, void* z, float* bn_part, float* bn_local,
                cudaStream_t st) {
   constexpr int V = vec_of<T>();
-  if (s1_ok(g)) {
-    const S1Args a = s1_args(g, false);
-    const size_t sm = (size_t)(a.xb + 2 * a.xb * g.C) * sizeof(float);
-    auto k = dw3x3_s1_kernel<T, false>;
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_k(k, s1_grid(a), (g.C / 4) * a.xb, sm, st, a, (const T*)x, w, (T*)z, (const T*)nullptr, bn_part);
-    DFX_LAUNCH_CHECK("dfx_mbconv_fwd dwconv (s1)");
-    launch_k(bn_merge3_kernel, g.C, kThreads, 0, st, (int)s1_tiles(a), g.C, bn_part, bn_local);
-    DFX_LAUNCH_CHECK("dfx_mbconv_fwd bn_merge");
-    return DFX_OK;
-  }
+  if (ring_ok(g)) return dw_conv_stats(sizeof(T) == 2 ? DFX_BF16 : DFX_F32, dw_shape(g), x, w, z, bn_part, bn_local, st);
   const int CV = g.C / V, PY = kThreads / CV, threads = CV * PY;
   const int ntiles = g.N * g.tiles_per_img;
   const size_t sm1 = (size_t)(PY + 2 * PY * g.C) * sizeof(float);
@@ -1074,10 +760,10 @@ size_t dfx_mbconv_workspace(int64_t N, int64_t H, int64_t W, int64_t C, int stri
   // bn_part 2C*tiles | pool_part C*tiles | bwd_part 5C*tiles | de N*C | dr N*SE | nsum 2NC | dw_part 9C*grid
   size_t fl = ntiles * 2 * C + ntiles * C + ntiles * 5 * C + (size_t)N * C + (size_t)N * SE + 2 * (size_t)N * C +
               9 * (size_t)C * nsm;
-  if (s1_ok(g)) {
-    // fast path: fwd partials [tiles][3][C] and bwd [tiles][9][C] reuse the
-    // scratch head; dz (f32-sized, [N, Ho, Wo, C]) follows the whole scratch
-    fl = s1_dz_offset(g, fl) + (size_t)g.N * g.Ho * g.Wo * C;
+  if (ring_ok(g)) {
+    // ring path: partials at the head (the generic scratch is not live across
+    // the dwconv calls), dz ([N, Ho, Wo, C], f32-sized) after everything
+    fl = (std::max(fl, ring_part_floats(g)) + 63) / 64 * 64 + (size_t)g.N * g.Ho * g.Wo * C;
   }
   return sizeof(float) * fl + 256;
 }
@@ -1208,44 +894,16 @@ int dfx_mbconv_bwd_dx(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
   DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, pads, 1), DFX_ERR_WORKSPACE,
               "dfx_mbconv_bwd_dx: workspace too small");
   cudaStream_t st = as_stream(stream);
-  // bf16 keeps the fused path: a bf16-rounded dz breaks the BN-VJP
-  // orthogonality (sum dz = sum dz*z = 0) that dw = sum x*dz cancels against
-  if (s1_ok(g) && dtype == DFX_F32) {
-    // dz (elementwise, stored) -> dx = transposed conv of dz, dw from the same window
-    const S1Args a = s1_args(g, true);
-    // dz sits after every scratch region this call or the SE=1 layout uses
+  if (ring_ok(g)) {
+    // dz (stored) + dw from the x window, then dx = transposed conv of dz
+    const DwShape d = dw_shape(g);
     const size_t nt = (size_t)g.N * g.tiles_per_img, nsm = (size_t)4 * num_sms();
     const size_t fl1 = nt * 8 * C + (size_t)N * C + (size_t)N + 2 * (size_t)N * C + 9 * (size_t)C * nsm;
-    float* part9 = (float*)workspace;
-    void* dzb = (float*)workspace + s1_dz_offset(g, fl1);
-    BnParams bnp{mean, rstd, gamma, beta};
-    const float icount = (float)(1.0 / count);
-    const int ntl = g.N * g.tiles_per_img;
-    const size_t sm = (size_t)a.xb * g.C * sizeof(float);
-    if (dtype == DFX_BF16) {
-      const int CV = g.C / 8, threads = CV * (kThreads / CV);
-      launch_k(dz_kernel<__nv_bfloat16, 8>, ntl, threads, 0, st, g, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)z,
-               bnp, s, dpool, bnsum, icount, (__nv_bfloat16*)dzb);
-      DFX_LAUNCH_CHECK("dfx_mbconv_bwd_dx dz");
-      auto k = dw3x3_s1_kernel<__nv_bfloat16, true>;
-      if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      launch_k(k, s1_grid(a), (g.C / 4) * a.xb, sm, st, a, (const __nv_bfloat16*)dzb, w_dw, (__nv_bfloat16*)dx,
-               (const __nv_bfloat16*)x, part9);
-    } else if (dtype == DFX_F32) {
-      const int CV = g.C / 4, threads = CV * (kThreads / CV);
-      launch_k(dz_kernel<float, 4>, ntl, threads, 0, st, g, (const float*)dy, (const float*)z, bnp, s, dpool, bnsum,
-               icount, (float*)dzb);
-      DFX_LAUNCH_CHECK("dfx_mbconv_bwd_dx dz");
-      auto k = dw3x3_s1_kernel<float, true>;
-      if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      launch_k(k, s1_grid(a), (g.C / 4) * a.xb, sm, st, a, (const float*)dzb, w_dw, (float*)dx, (const float*)x, part9);
-    } else {
-      return fail(DFX_ERR_DTYPE, "dfx_mbconv_bwd_dx: dtype must be f32 or bf16");
-    }
-    DFX_LAUNCH_CHECK("dfx_mbconv_bwd_dx conv (s1)");
-    launch_k(dw_sum_kernel, dim3((unsigned)((C + 31) / 32), 9), 256, 0, st, (int)s1_tiles(a), (int)C, part9, dw_dw);
-    DFX_LAUNCH_CHECK("dfx_mbconv_bwd_dx dw");
-    return DFX_OK;
+    float* part = (float*)workspace;
+    void* dzb = (float*)workspace + (std::max(fl1, ring_part_floats(g)) + 63) / 64 * 64;  // TMA: 16-B aligned
+    const DzConsts k{mean, rstd, gamma, beta, s, dpool, bnsum, (float)(1.0 / count)};
+    if (int rc = dw_dz_dw(dtype, d, x, dy, z, k, dzb, part, dw_dw, st)) return rc;
+    return dw_dx(dtype, d, dzb, w_dw, dx, st);
   }
   const int ntiles_conv = g.N * ((g.Ho + TO - 1) / TO) * ((g.Wo + TO - 1) / TO);
   const int grid = std::min(ntiles_conv, 4 * num_sms());
