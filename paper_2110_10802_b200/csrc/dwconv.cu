@@ -31,6 +31,8 @@
 //   CONV (backward, stride 1): dx = conv(dz, flipped w) with the transposed
 //       padding (KS-1-pt, KS-1-pl).  Stride 2 uses a direct gather kernel.
 #include <algorithm>
+#include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 #include "dwconv.h"
@@ -39,6 +41,15 @@
 
 namespace dfx {
 namespace {
+
+template <int... Is, typename F>
+__device__ __forceinline__ void unroll_impl(std::integer_sequence<int, Is...>, F&& f) {
+  (f(std::integral_constant<int, Is>{}), ...);
+}
+// f(integral_constant<int, 0..N-1>): compile-time loop index
+template <int N, typename F> __device__ __forceinline__ void unroll_for(F&& f) {
+  unroll_impl(std::make_integer_sequence<int, N>{}, f);
+}
 
 enum { MODE_CONV = 0, MODE_STATS = 1, MODE_DZW = 2 };
 constexpr int kMaxThreads = 256;
@@ -93,6 +104,41 @@ template <int V> __device__ __forceinline__ void stv(float* p, const float (&v)[
     *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
 }
 
+using F2 = float2;
+__device__ __forceinline__ F2 bf2_to_f2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+// V channels from shared memory, unpacked to V/2 float pairs
+template <typename T, int V> __device__ __forceinline__ void ld_f2(const T* p, F2 (&o)[V / 2]);
+template <> __device__ __forceinline__ void ld_f2<__nv_bfloat16, 4>(const __nv_bfloat16* p, F2 (&o)[2]) {
+  const uint2 r = *reinterpret_cast<const uint2*>(p);
+  o[0] = bf2_to_f2(r.x);
+  o[1] = bf2_to_f2(r.y);
+}
+template <> __device__ __forceinline__ void ld_f2<__nv_bfloat16, 2>(const __nv_bfloat16* p, F2 (&o)[1]) {
+  o[0] = bf2_to_f2(*reinterpret_cast<const uint32_t*>(p));
+}
+template <> __device__ __forceinline__ void ld_f2<float, 4>(const float* p, F2 (&o)[2]) {
+  const float4 r = *reinterpret_cast<const float4*>(p);
+  o[0] = make_float2(r.x, r.y);
+  o[1] = make_float2(r.z, r.w);
+}
+template <> __device__ __forceinline__ void ld_f2<float, 2>(const float* p, F2 (&o)[1]) {
+  o[0] = *reinterpret_cast<const float2*>(p);
+}
+template <int V> __device__ __forceinline__ void st_f2(__nv_bfloat16* p, const F2 (&v)[V / 2]) {
+  if constexpr (V == 4)
+    *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf2(v[0].x, v[0].y), pack_bf2(v[1].x, v[1].y));
+  else
+    *reinterpret_cast<uint32_t*>(p) = pack_bf2(v[0].x, v[0].y);
+}
+template <int V> __device__ __forceinline__ void st_f2(float* p, const F2 (&v)[V / 2]) {
+  if constexpr (V == 4)
+    *reinterpret_cast<float4*>(p) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+  else
+    *reinterpret_cast<float2*>(p) = v[0];
+}
+
 __device__ __forceinline__ float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -122,6 +168,7 @@ struct RingP {
   int ncb, nwt, nbands;
   int nseg, L;
   uint32_t in_slot, io_slot;  // bytes per ring slot (128-B multiples)
+  int K;                      // ring slots
   int flip;                   // CONV: w[KS*KS-1-t] (transposed conv)
 };
 
@@ -131,10 +178,13 @@ __global__ void __launch_bounds__(kMaxThreads, 2)
                    const __grid_constant__ CUtensorMap z_map, const RingP p, const float* __restrict__ w,
                    T* __restrict__ out, float* __restrict__ part, const DzConsts dk) {
   constexpr int V = VecOf<KS>::value;
-  constexpr int K = KS + 2 * S;
+  const int K = p.K;  // ring slots (planner: KS + 2s .. KS + 4s)
   constexpr int T2 = KS * KS;
-  extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+  constexpr int V2 = V / 2;
+  // dynamic shared memory starts the CTA's window (no static smem here), so
+  // it is 1024-B aligned; indexing it directly keeps the compiler in the
+  // shared state space (LDS, 32-bit addresses) instead of generic loads
+  extern __shared__ __align__(1024) uint8_t sm[];
   T* ring = reinterpret_cast<T*>(sm);
   T* dyr = reinterpret_cast<T*>(sm + K * p.in_slot);
   T* zr = reinterpret_cast<T*>(sm + K * p.in_slot + 2 * p.io_slot);
@@ -155,7 +205,10 @@ __global__ void __launch_bounds__(kMaxThreads, 2)
   const uint32_t in_el = p.in_slot / sizeof(T), io_el = p.io_slot / sizeof(T);
   const uint32_t in_bytes = (uint32_t)(p.Wb * p.Cb * sizeof(T)), io_bytes = (uint32_t)(p.Wt * p.Cb * sizeof(T));
 
+  uint32_t* cnts = reinterpret_cast<uint32_t*>(bars + K + 2);  // per-row release counters (r % 16)
+  const uint32_t nwarps = (blockDim.x + 31) / 32;
   if (tid == 0) {
+    for (int i = 0; i < 16; ++i) cnts[i] = 0;
     for (int i = 0; i < K + 2; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -185,12 +238,17 @@ __global__ void __launch_bounds__(kMaxThreads, 2)
   const bool act = xs < xe;
   const int cc = c0 + cv * V;
 
-  float wr[MODE == MODE_DZW ? 1 : T2][V];
+  // weights / window / accumulators as float2 pairs: FFMA2 (sm_100 packed
+  // f32 FMA) does two channels per instruction
+  F2 wr[MODE == MODE_DZW ? 1 : T2][V2];
   if constexpr (MODE != MODE_DZW) {
 #pragma unroll
     for (int t = 0; t < T2; ++t)
 #pragma unroll
-      for (int i = 0; i < V; ++i) wr[t][i] = __ldg(w + (size_t)(p.flip ? T2 - 1 - t : t) * p.C + cc + i);
+      for (int i = 0; i < V2; ++i) {
+        const float* wp = w + (size_t)(p.flip ? T2 - 1 - t : t) * p.C + cc + 2 * i;
+        wr[t][i] = make_float2(__ldg(wp), __ldg(wp + 1));
+      }
   }
   // DZW: dz = P*du + Cz*z + Bc, du = (dy*sv + dp) * swish'(z*P + Q)
   float kP[V], kQ[V], kCz[V], kB[V], kS[V], kD[V];
@@ -208,19 +266,40 @@ __global__ void __launch_bounds__(kMaxThreads, 2)
       kD[i] = dk.dpool[(size_t)n * p.C + c];
     }
   }
-  float st0[V], st1[V], shf[V];
-  float dwa[MODE == MODE_DZW ? T2 : 1][V];
+  F2 st0[V2], st1[V2], nsh[V2];
+  F2 dwa[MODE == MODE_DZW ? T2 : 1][V2];
 #pragma unroll
-  for (int i = 0; i < V; ++i) {
-    st0[i] = 0.f;
-    st1[i] = 0.f;
-    shf[i] = 0.f;
+  for (int i = 0; i < V2; ++i) {
+    st0[i] = make_float2(0.f, 0.f);
+    st1[i] = make_float2(0.f, 0.f);
+    nsh[i] = make_float2(0.f, 0.f);
   }
 #pragma unroll
   for (int t = 0; t < (MODE == MODE_DZW ? T2 : 1); ++t)
 #pragma unroll
-    for (int i = 0; i < V; ++i) dwa[t][i] = 0.f;
+    for (int i = 0; i < V2; ++i) dwa[t][i] = make_float2(0.f, 0.f);
   int cnt = 0;
+
+  if constexpr (MODE == MODE_STATS) {
+    if (act) {
+#pragma unroll
+      for (int ky = 0; ky < KS; ++ky) mbar_wait(&bars[ky], 0);
+      F2 acc[V2];
+#pragma unroll
+      for (int i = 0; i < V2; ++i) acc[i] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int ky = 0; ky < KS; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < KS; ++kx) {
+          F2 v[V2];
+          ld_f2<T, V>(ring + ky * in_el + cv * V + (xs * S + kx) * p.Cb, v);
+#pragma unroll
+          for (int i = 0; i < V2; ++i) acc[i] = __ffma2_rn(v[i], wr[ky * KS + kx][i], acc[i]);
+        }
+#pragma unroll
+      for (int i = 0; i < V2; ++i) nsh[i] = make_float2(-acc[i].x, -acc[i].y);
+    }
+  }
 
   for (int r = 0; r < nrows; ++r) {
 #pragma unroll
@@ -233,83 +312,107 @@ __global__ void __launch_bounds__(kMaxThreads, 2)
       const T* rows[KS];
 #pragma unroll
       for (int ky = 0; ky < KS; ++ky) rows[ky] = ring + ((r * S + ky) % K) * in_el + cv * V;
-      RV<T, V> win[KS][KS];
-#pragma unroll
-      for (int ky = 0; ky < KS; ++ky)
-#pragma unroll
-        for (int kx = 0; kx < KS; ++kx) win[ky][kx].ld(rows[ky] + (xs * S + kx) * p.Cb);
       T* orow = out + (((size_t)n * p.Ho + oy0 + r) * p.Wo + ox0) * p.C + cc;
       const T* dyrow = dyr + (r & 1) * io_el + cv * V;
       const T* zrow = zr + (r & 1) * io_el + cv * V;
-      for (int x = xs; x < xe; ++x) {
-        if (x > xs) {
+      // window = KS column slots x KS rows; input column q (relative to the
+      // segment) lives in slot q % KS.  Unrolling the column walk by KS makes
+      // every slot index a compile-time constant: no register shuffling.
+      F2 win[KS][KS][V2];
 #pragma unroll
-          for (int ky = 0; ky < KS; ++ky) {
+      for (int q = 0; q < KS - S; ++q)
 #pragma unroll
-            for (int kx = 0; kx < KS - S; ++kx) win[ky][kx] = win[ky][kx + S];
+        for (int ky = 0; ky < KS; ++ky) ld_f2<T, V>(rows[ky] + (xs * S + q) * p.Cb, win[q][ky]);
+      auto step = [&](auto uc, int x) {
+        constexpr int u = decltype(uc)::value;
 #pragma unroll
-            for (int kx = KS - S; kx < KS; ++kx) win[ky][kx].ld(rows[ky] + (x * S + kx) * p.Cb);
-          }
-        }
+        for (int jn = 0; jn < S; ++jn)
+#pragma unroll
+          for (int ky = 0; ky < KS; ++ky)
+            ld_f2<T, V>(rows[ky] + (x * S + KS - S + jn) * p.Cb, win[(u * S + KS - S + jn) % KS][ky]);
         if constexpr (MODE != MODE_DZW) {
-          float acc[V];
-#pragma unroll
-          for (int i = 0; i < V; ++i) acc[i] = 0.f;
+          // one partial sum per tap row: KS independent FFMA2 chains
+          F2 pr[KS][V2];
 #pragma unroll
           for (int ky = 0; ky < KS; ++ky)
 #pragma unroll
-            for (int kx = 0; kx < KS; ++kx)
+            for (int i = 0; i < V2; ++i) {
+              pr[ky][i] = __fmul2_rn(win[(u * S) % KS][ky][i], wr[ky * KS][i]);
 #pragma unroll
-              for (int i = 0; i < V; ++i) acc[i] = fmaf(win[ky][kx].get(i), wr[ky * KS + kx][i], acc[i]);
-          stv<V>(orow + (size_t)x * p.C, acc);
-          if constexpr (MODE == MODE_STATS) {
-            // shifted sums of the unrounded conv output
-            if (cnt == 0) {
-#pragma unroll
-              for (int i = 0; i < V; ++i) shf[i] = acc[i];
+              for (int kx = 1; kx < KS; ++kx)
+                pr[ky][i] = __ffma2_rn(win[(u * S + kx) % KS][ky][i], wr[ky * KS + kx][i], pr[ky][i]);
             }
+          F2 acc[V2];
 #pragma unroll
-            for (int i = 0; i < V; ++i) {
-              const float d = acc[i] - shf[i];
-              st0[i] += d;
-              st1[i] = fmaf(d, d, st1[i]);
+          for (int i = 0; i < V2; ++i) {
+            acc[i] = pr[0][i];
+#pragma unroll
+            for (int ky = 1; ky < KS; ++ky) acc[i] = __fadd2_rn(acc[i], pr[ky][i]);
+          }
+          st_f2<V>(orow + (size_t)x * p.C, acc);
+          if constexpr (MODE == MODE_STATS) {
+            // shifted sums of the unrounded conv output (shift = the
+            // thread's first output, computed before the row loop)
+#pragma unroll
+            for (int i = 0; i < V2; ++i) {
+              const F2 d = __fadd2_rn(acc[i], nsh[i]);
+              st0[i] = __fadd2_rn(st0[i], d);
+              st1[i] = __ffma2_rn(d, d, st1[i]);
             }
             ++cnt;
           }
         } else {
-          RV<T, V> dv, zv;
-          dv.ld(dyrow + x * p.Cb);
-          zv.ld(zrow + x * p.Cb);
-          float dz[V];
+          F2 dv[V2], zv[V2], dz[V2];
+          ld_f2<T, V>(dyrow + x * p.Cb, dv);
+          ld_f2<T, V>(zrow + x * p.Cb, zv);
 #pragma unroll
           for (int i = 0; i < V; ++i) {
-            const float zz = zv.get(i);
-            const float u = fmaf(zz, kP[i], kQ[i]);
-            const float sgm = sigm<T>(u);
-            const float swp = sgm * fmaf(u, 1.f - sgm, 1.f);
-            const float du = fmaf(dv.get(i), kS[i], kD[i]) * swp;
-            dz[i] = fmaf(kP[i], du, fmaf(kCz[i], zz, kB[i]));
+            const float zz = (i & 1) ? zv[i >> 1].y : zv[i >> 1].x;
+            const float dd = (i & 1) ? dv[i >> 1].y : dv[i >> 1].x;
+            const float u_ = fmaf(zz, kP[i], kQ[i]);
+            const float sgm = sigm<T>(u_);
+            const float swp = sgm * fmaf(u_, 1.f - sgm, 1.f);
+            const float du = fmaf(dd, kS[i], kD[i]) * swp;
+            const float o = fmaf(kP[i], du, fmaf(kCz[i], zz, kB[i]));
+            if (i & 1) dz[i >> 1].y = o;
+            else dz[i >> 1].x = o;
           }
-          stv<V>(orow + (size_t)x * p.C, dz);
+          st_f2<V>(orow + (size_t)x * p.C, dz);
 #pragma unroll
           for (int ky = 0; ky < KS; ++ky)
 #pragma unroll
             for (int kx = 0; kx < KS; ++kx)
 #pragma unroll
-              for (int i = 0; i < V; ++i) dwa[ky * KS + kx][i] = fmaf(win[ky][kx].get(i), dz[i], dwa[ky * KS + kx][i]);
+              for (int i = 0; i < V2; ++i)
+                dwa[ky * KS + kx][i] = __ffma2_rn(win[(u * S + kx) % KS][ky][i], dz[i], dwa[ky * KS + kx][i]);
         }
-      }
+      };
+      // whole groups of KS columns unguarded (the compiler interleaves the
+      // independent outputs), then the guarded remainder
+      int xb = xs;
+      for (; xb + KS <= xe; xb += KS) unroll_for<KS>([&](auto uc) { step(uc, xb + decltype(uc)::value); });
+      unroll_for<KS>([&](auto uc) {
+        if (xb + decltype(uc)::value < xe) step(uc, xb + decltype(uc)::value);
+      });
     }
-    __syncthreads();  // every thread is done with the rows that leave the window
-    if (tid == 0) {
+    // release: the warp is done with the rows leaving the window; the last
+    // warp to arrive refills them (no CTA-wide barrier per row)
+    __syncwarp();
+    if ((tid & 31) == 0) {
+      __threadfence_block();
+      // a warp leads the slowest by at most (K - KS) / s <= 4 rows: 16 counters never alias
+      const uint32_t old = atomicAdd(&cnts[r & 15], 1u);
+      if (old == (uint32_t)((r >> 4) + 1) * nwarps - 1) {
 #pragma unroll
-      for (int q = 0; q < S; ++q) {
-        const int jn = r * S + q + K;
-        if (jn < NR) issue_in(jn);
+        for (int q = 0; q < S; ++q) {
+          const int jn = r * S + q + K;
+          if (jn < NR) issue_in(jn);
+        }
+        if (MODE == MODE_DZW && r + 2 < nrows) issue_io(r + 2);
       }
-      if (MODE == MODE_DZW && r + 2 < nrows) issue_io(r + 2);
     }
   }
+  __syncthreads();
 
   // ------------------------------------------------------------ CTA partials
   // every issued load has been consumed: the ring is free scratch now
@@ -322,9 +425,11 @@ __global__ void __launch_bounds__(kMaxThreads, 2)
     if (cv == 0) s_n[sg] = (float)cnt;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      const float m = cnt ? st0[i] / (float)cnt : 0.f;
-      s_mean[sg * p.Cb + cv * V + i] = shf[i] + m;
-      s_m2[sg * p.Cb + cv * V + i] = cnt ? fmaxf(st1[i] - st0[i] * m, 0.f) : 0.f;
+      const float a0 = (i & 1) ? st0[i >> 1].y : st0[i >> 1].x, a1 = (i & 1) ? st1[i >> 1].y : st1[i >> 1].x;
+      const float sh = -((i & 1) ? nsh[i >> 1].y : nsh[i >> 1].x);
+      const float m = cnt ? a0 / (float)cnt : 0.f;
+      s_mean[sg * p.Cb + cv * V + i] = sh + m;
+      s_m2[sg * p.Cb + cv * V + i] = cnt ? fmaxf(a1 - a0 * m, 0.f) : 0.f;
     }
     __syncthreads();
     for (int c = tid; c < p.Cb; c += blockDim.x) {
@@ -338,7 +443,10 @@ __global__ void __launch_bounds__(kMaxThreads, 2)
 #pragma unroll
     for (int t = 0; t < T2; ++t) {
 #pragma unroll
-      for (int i = 0; i < V; ++i) red[sg * p.Cb + cv * V + i] = dwa[t][i];
+      for (int i = 0; i < V2; ++i) {
+        red[sg * p.Cb + cv * V + 2 * i] = dwa[t][i].x;
+        red[sg * p.Cb + cv * V + 2 * i + 1] = dwa[t][i].y;
+      }
       __syncthreads();
       for (int c = tid; c < p.Cb; c += blockDim.x) {
         float acc = 0.f;
@@ -468,19 +576,28 @@ bool make_plan(int N, int Hi, int Wi, int Ho, int Wo, int C, int ks, int s, int 
   if (s != 1 && s != 2) return false;
   if ((C * esz) % 16 != 0) return false;
   const int V = ks == 3 ? 4 : 2;
-  const int K = ks + 2 * s;
   const int Cb = pick_cb(C, V, esz);
   if (!Cb) return false;
   const int CVn = Cb / V;
   if (CVn > kMaxThreads) return false;
-  auto smem_of = [&](int wt) {
+  auto smem_of = [&](int wt, int k) {
     const size_t in_slot = rnd128((size_t)((wt - 1) * s + ks) * Cb * esz);
     const size_t io_slot = rnd128((size_t)wt * Cb * esz);
-    return K * in_slot + (mode == MODE_DZW ? 4 * io_slot : 0) + (K + 2) * 8 + 128;
+    return k * in_slot + (mode == MODE_DZW ? 4 * io_slot : 0) + (k + 2) * 8 + 64;
   };
-  int Wt = std::min(Wo, std::min(256, (256 - ks) / s + 1));
-  while (Wt > 1 && smem_of(Wt) > kSmemBudget) --Wt;
-  if (smem_of(Wt) > kSmemBudget) return false;
+  // widest tile first (fewer halo columns, fewer per-row overheads): a deeper
+  // ring (up to 4 output rows of lookahead) only when the whole row still fits
+  const int wmax = std::min(Wo, std::min(256, (256 - ks) / s + 1));
+  int K = 0, Wt = 0;
+  for (int k = ks + 4 * s; k >= ks + 2 * s && !K; --k) {
+    int w = wmax;
+    while (w > 1 && smem_of(w, k) > kSmemBudget) --w;
+    if (smem_of(w, k) <= kSmemBudget && (w == wmax || k == ks + 2 * s)) {
+      K = k;
+      Wt = w;
+    }
+  }
+  if (!K) return false;
   const int nwt = (Wo + Wt - 1) / Wt;
   Wt = (Wo + nwt - 1) / nwt;
   const int nseg_max = kMaxThreads / CVn;
@@ -502,6 +619,7 @@ bool make_plan(int N, int Hi, int Wi, int Ho, int Wo, int C, int ks, int s, int 
   p.in_slot = (uint32_t)rnd128((size_t)p.Wb * Cb * esz);
   p.io_slot = (uint32_t)rnd128((size_t)Wt * Cb * esz);
   // reduction scratch must fit in the ring
+  p.K = K;
   const size_t red = (size_t)nseg * (1 + 2 * Cb) * 4;
   if (red > (size_t)K * p.in_slot) return false;
   // band height: fewest waves x rows per CTA (2 CTAs per SM)
@@ -524,7 +642,7 @@ bool make_plan(int N, int Hi, int Wi, int Ho, int Wo, int C, int ks, int s, int 
   pl_out->p = p;
   pl_out->threads = CVn * nseg;
   pl_out->grid = N * p.nbands * nwt * p.ncb;
-  pl_out->smem = smem_of(Wt);
+  pl_out->smem = smem_of(Wt, K);
   return true;
 }
 

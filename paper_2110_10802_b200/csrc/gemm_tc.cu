@@ -527,13 +527,13 @@ Plan plan(const dfx_gemm_args& p) {
     if (sscanf(force, "%d,%d", &fcg, &fbn) == 2 && (fcg == 1 || fcg == 2) && (fbn == 64 || fbn == 128 || fbn == 256) &&
         !(fcg == 2 && (fbn == 64 || p.m < 256))) {
       const int64_t z = p.batch1 * p.batch2;
-      const int64_t kb = p.k / BK;
+      const int64_t kb = (p.k + BK - 1) / BK;  // K tail: TMA zero-fills past k
       const int64_t units = z * ((p.m + BM * fcg - 1) / (BM * fcg)) * ((p.n + fbn - 1) / fbn);
       return Plan{fbn, fcg, 1, (int)kb, units};
     }
   }
   const int64_t z = p.batch1 * p.batch2;
-  const int64_t kb = p.k / BK;
+  const int64_t kb = (p.k + BK - 1) / BK;  // K tail: TMA zero-fills past k
   struct Cand { int bn, cg; double thr; };
   const Cand cands[] = {{256, 2, 1.5}, {128, 2, 1.0}, {256, 1, 1.0}, {128, 1, 0.8}, {64, 1, 0.6}};
   Plan best{64, 1, 1, (int)kb, 0};
@@ -554,7 +554,7 @@ Plan plan(const dfx_gemm_args& p) {
   if (best.cg == 1 && p.epilogue == DFX_EPI_NONE && best.tiles * 2 <= sms && kb >= 8) {
     if (best.bn == 256) {
       best.bn = 128;
-      best.tiles = z * (p.m / BM) * ((p.n + 127) / 128);
+      best.tiles = z * ((p.m + BM - 1) / BM) * ((p.n + 127) / 128);
     }
     int64_t s = std::min<int64_t>(sms / std::max<int64_t>(best.tiles, 1), kb / 4);
     s = std::min<int64_t>(s, 8);
@@ -622,7 +622,7 @@ bool gemm_tc_supported(const dfx_gemm_args& p) {
   if (p.force_simt || p.in_dtype != DFX_BF16) return false;
   if (p.out_dtype != DFX_BF16 && p.out_dtype != DFX_F32) return false;
   if (p.m <= 0 || p.n <= 0 || p.k <= 0) return false;
-  if (p.m % BM || p.k % BK) return false;
+  // M and K tails: TMA zero-fills out-of-range rows/k, the epilogue clips rows
   const bool a_k = p.a_stride_k == 1, a_m = p.a_stride_m == 1;
   const bool b_k = p.b_stride_k == 1, b_n = p.b_stride_n == 1;
   if (!(a_k || a_m) || !(b_k || b_n)) return false;
@@ -641,7 +641,7 @@ bool gemm_tc_supported(const dfx_gemm_args& p) {
   if (p.aux_out && (p.aux_out_stride_m % ovec || !aligned16(p.aux_out) ||
                     (p.batch2 > 1 && p.aux_out_stride_b2 % ovec) || (p.batch1 > 1 && p.aux_out_stride_b1 % ovec)))
     return false;
-  if (p.batch1 * p.batch2 * (p.m / BM) * ((p.n + 63) / 64) * 8 > (1ll << 31)) return false;
+  if (p.batch1 * p.batch2 * ((p.m + BM - 1) / BM) * ((p.n + 63) / 64) * 8 > (1ll << 31)) return false;
   return true;
 }
 
@@ -674,7 +674,7 @@ int gemm_tc(const dfx_gemm_args& p, cudaStream_t st) {
   tp.m = p.m; tp.n = p.n; tp.k = p.k; tp.batch2 = p.batch2;
   tp.m_tiles = (int)((p.m + BM * pl.cg - 1) / (BM * pl.cg));
   tp.n_tiles = (int)((p.n + bn - 1) / bn);
-  tp.k_blocks = (int)(p.k / BK);
+  tp.k_blocks = (int)((p.k + BK - 1) / BK);
   tp.splits = pl.splits;
   tp.kb_per_split = pl.kb_per_split;
   tp.num_tiles = (int)pl.tiles;

@@ -247,13 +247,26 @@ __global__ void __launch_bounds__(kThreads) bn_swish_pool_kernel(Geo g, const T*
     }
     const T* base = z + ((size_t)n * g.Ho + r0) * g.Wo * g.C + c0;
     const int npix = (r1 - r0) * g.Wo;
-    for (int p = py; p < npix; p += PY) {
+    int p = py;
+    for (; p + 3 * PY < npix; p += 4 * PY) {  // 4 loads in flight per thread
+      Vec<T, V> zv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) zv[q].load(base + (size_t)(p + q * PY) * g.C);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const float u = fmaf(zv[q].v[i], sc[i], sh[i]);
+          acc[i] = fmaf(u, sigm<T>(u), acc[i]);
+        }
+    }
+    for (; p < npix; p += PY) {
       Vec<T, V> zv;
       zv.load(base + (size_t)p * g.C);
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         const float u = fmaf(zv.v[i], sc[i], sh[i]);
-        acc[i] += u * sigm<T>(u);
+        acc[i] = fmaf(u, sigm<T>(u), acc[i]);
       }
     }
     for (int i = 0; i < V; ++i) sm[py * g.C + c0 + i] = acc[i];
@@ -384,25 +397,50 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geo g, const T* __
     for (int i = 0; i < V; ++i) {
       mu[i] = bn.mean[c0 + i]; rs[i] = bn.rstd[c0 + i]; gm[i] = bn.gamma[c0 + i]; bt[i] = bn.beta[c0 + i];
     }
+    float P[V], Q[V], R[V], M[V];  // u = z*P + Q, xhat = z*R + M
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      P[i] = gm[i] * rs[i];
+      Q[i] = bt[i] - mu[i] * P[i];
+      R[i] = rs[i];
+      M[i] = -mu[i] * rs[i];
+    }
     const size_t base = ((size_t)n * g.Ho + r0) * g.Wo * g.C + c0;
     const int npix = (r1 - r0) * g.Wo;
-    for (int p = py; p < npix; p += PY) {
+    auto body = [&](const Vec<T, V>& dv, const Vec<T, V>& zv) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const float zz = zv.v[i];
+        const float xh = fmaf(zz, R[i], M[i]);
+        const float u = fmaf(zz, P[i], Q[i]);
+        const float sg = sigm<T>(u);
+        const float swp = sg * fmaf(u, 1.f - sg, 1.f);
+        const float d = dv.v[i];
+        const float dswp = d * swp;
+        a[0][i] = fmaf(d * u, sg, a[0][i]);
+        a[1][i] += dswp;
+        a[2][i] += swp;
+        a[3][i] = fmaf(dswp, xh, a[3][i]);
+        a[4][i] = fmaf(swp, xh, a[4][i]);
+      }
+    };
+    // four pixels per iteration: 8 independent 128-bit loads in flight per thread
+    int p = py;
+    for (; p + 3 * PY < npix; p += 4 * PY) {
+      Vec<T, V> dv[4], zv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        dv[q].load(dy + base + (size_t)(p + q * PY) * g.C);
+        zv[q].load(z + base + (size_t)(p + q * PY) * g.C);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) body(dv[q], zv[q]);
+    }
+    for (; p < npix; p += PY) {
       Vec<T, V> dv, zv;
       dv.load(dy + base + (size_t)p * g.C);
       zv.load(z + base + (size_t)p * g.C);
-#pragma unroll
-      for (int i = 0; i < V; ++i) {
-        const float xh = (zv.v[i] - mu[i]) * rs[i];
-        const float u = fmaf(xh, gm[i], bt[i]);
-        const float sg = sigm<T>(u);
-        const float swp = sg + u * sg * (1.f - sg);
-        const float d = dv.v[i];
-        a[0][i] += d * u * sg;
-        a[1][i] += d * swp;
-        a[2][i] += swp;
-        a[3][i] += d * swp * xh;
-        a[4][i] += swp * xh;
-      }
+      body(dv, zv);
     }
   }
   for (int k = 0; k < 5; ++k) {

@@ -175,3 +175,17 @@ def test_tc_ragged_n(n):
     kk.gemm(a, b, d, _lib.EPI_BIAS, bias=bias)
     torch.cuda.synchronize()
     _check(d, _ref(a, b) + bias.double().cpu().numpy(), 1e-2)
+
+
+@pytest.mark.parametrize("m,n,k,la,lb", [(4704, 40, 24, "k", "k"), (300, 96, 16, "k", "k"), (1000, 144, 24, "m", "k"),
+                                         (24, 40, 4704, "m", "m"), (130, 1152, 192, "k", "k")])
+def test_tc_ragged_m_k(m, n, k, la, lb):
+    """M and K not multiples of the 128 x 64 tile (the EfficientNet-B0 1x1
+    convolutions: K = 16/24/40 channels, M = N*H*W pixels, wgrad K = pixels)."""
+    kk = K()
+    a, b = _operands(m, n, k, la, lb, torch.bfloat16, m + n + k)
+    d = torch.full((m, n), 7.0, dtype=torch.bfloat16, device="cuda")
+    assert kk.gemm_uses_tensor_cores(a, b, d)
+    kk.gemm(a, b, d)
+    torch.cuda.synchronize()
+    _check(d, _ref(a, b), 1e-2)
