@@ -195,9 +195,10 @@ size_t dfx_gemm_workspace(const dfx_gemm_args* args);
 int dfx_gemm_uses_tensor_cores(const dfx_gemm_args* args);
 
 /* ---- a9-a13: EfficientNet-B0 MBConv block, NHWC ---------------------------
- * x [N,H,W,C] (f32 or bf16, C % 4 (f32) / C % 8 (bf16) == 0); depthwise 3x3
- * weight stored [3][3][C] f32 (the reference's (C,1,3,3) transposed);
- * pads = {top, left, bottom, right} in [0,2]; stride 1 or 2.
+ * x [N,H,W,C] (f32 or bf16, C % 4 (f32) / C % 8 (bf16) == 0); depthwise
+ * ksize x ksize (3 or 5; EfficientNet-B0 uses both) weight stored [k][k][C]
+ * f32 (the reference's (C,1,k,k) transposed); pads = {top, left, bottom,
+ * right} in [0, ksize-1]; stride 1 or 2.
  *   Conv group=C (frontend.py:598-678; depthwise check 608-635)
  *   BatchNormalization, training mode (frontend.py:544-591): biased variance,
  *     running = running*momentum + batch*(1-momentum)
@@ -207,12 +208,12 @@ int dfx_gemm_uses_tensor_cores(const dfx_gemm_args* args);
  * Backward: BN VJP autodiff.py:1557-1617, depthwise conv VJP of the lowered
  * loop nest (lowering.py:930-1004 + tasklet VJPs, autodiff.py:1623-1629).
  * One workspace (dfx_mbconv_workspace) serves every call of a step. */
-size_t dfx_mbconv_workspace(int64_t N, int64_t H, int64_t W, int64_t C, int stride, const int* pads,
-                            int SE);
+size_t dfx_mbconv_workspace(int64_t N, int64_t H, int64_t W, int64_t C, int stride, int ksize,
+                            const int* pads, int SE);
 /* z = dwconv(x); bn_local[3][C] = per-channel (count, mean, M2) of z on this
  * rank (Welford, fixed order).  SyncBN gathers bn_local of every rank. */
 int dfx_mbconv_fwd_stats(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride,
-                         const int* pads, const void* x, const float* w_dw, void* z, float* bn_local,
+                         int ksize, const int* pads, const void* x, const float* w_dw, void* z, float* bn_local,
                          void* workspace, size_t ws_bytes, void* stream);
 /* Merge nsets (count, mean, M2) sets in order -> mean, var (biased), rstd and
  * the running-statistic update (any output but rstd may be NULL). */
@@ -221,7 +222,7 @@ int dfx_bn_finalize(int64_t C, int nsets, const float* sets, float eps, float mo
 /* pooled[N][C] = mean_hw swish(BN(z)); r[N][SE] = Wr pooled + br;
  * s[N][C] = sigmoid(We swish(r) + be); y = swish(BN(z)) * s. */
 int dfx_mbconv_fwd_se(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride,
-                      const int* pads, int64_t SE, const void* z, const float* mean, const float* rstd,
+                      int ksize, const int* pads, int64_t SE, const void* z, const float* mean, const float* rstd,
                       const float* gamma, const float* beta, const float* w_r, const float* b_r,
                       const float* w_e, const float* b_e, float* pooled, float* r, float* s, void* y,
                       void* workspace, size_t ws_bytes, void* stream);
@@ -230,7 +231,7 @@ int dfx_mbconv_fwd_se(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
  * the pool); bnsum[2][C] = (sum du, sum du*xhat) = (dbeta, dgamma) of this
  * rank — SyncBN allreduces bnsum before part 2. */
 int dfx_mbconv_bwd_reduce(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride,
-                          const int* pads, int64_t SE, const void* dy, const void* z,
+                          int ksize, const int* pads, int64_t SE, const void* dy, const void* z,
                           const float* mean, const float* rstd, const float* gamma,
                           const float* beta, const float* s, const float* r, const float* pooled,
                           const float* w_r, const float* w_e, float* dw_e, float* db_e, float* dw_r,
@@ -239,7 +240,7 @@ int dfx_mbconv_bwd_reduce(int dtype, int64_t N, int64_t H, int64_t W, int64_t C,
 /* Backward part 2: dx and dw_dw [3][3][C]; count = number of elements each
  * BN channel normalises over (all ranks). */
 int dfx_mbconv_bwd_dx(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride,
-                      const int* pads, const void* dy, const void* z, const void* x,
+                      int ksize, const int* pads, const void* dy, const void* z, const void* x,
                       const float* w_dw, const float* mean, const float* rstd, const float* gamma,
                       const float* beta, const float* s, const float* dpool, const float* bnsum,
                       double count, void* dx, float* dw_dw, void* workspace, size_t ws_bytes,

@@ -72,22 +72,22 @@ _SIGS = [
     ("dfx_gemm", c_int, [POINTER(GemmArgs), c_void_p]),
     ("dfx_gemm_uses_tensor_cores", c_int, [POINTER(GemmArgs)]),
     ("dfx_gemm_workspace", c_size_t, [POINTER(GemmArgs)]),
-    ("dfx_mbconv_workspace", c_size_t, [c_int64, c_int64, c_int64, c_int64, c_int, c_void_p, c_int]),
-    ("dfx_mbconv_fwd_stats", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_void_p,
+    ("dfx_mbconv_workspace", c_size_t, [c_int64, c_int64, c_int64, c_int64, c_int, c_int, c_void_p, c_int]),
+    ("dfx_mbconv_fwd_stats", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_int, c_void_p,
                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                      c_void_p]),
     ("dfx_bn_finalize", c_int, [c_int64, c_int, c_void_p, c_float, c_float, c_void_p, c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_void_p]),
-    ("dfx_mbconv_fwd_se", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_void_p, c_int64,
+    ("dfx_mbconv_fwd_se", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_int, c_void_p, c_int64,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_size_t, c_void_p]),
-    ("dfx_mbconv_bwd_reduce", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_void_p,
+    ("dfx_mbconv_bwd_reduce", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_int, c_void_p,
                                       c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_size_t, c_void_p]),
-    ("dfx_mbconv_bwd_dx", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_void_p,
+    ("dfx_mbconv_bwd_dx", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_int, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, ctypes.c_double,
                                   c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),

@@ -44,6 +44,7 @@ struct Geo {
   int N, H, W, C;        // input
   int Ho, Wo;            // output
   int stride, pt, pl;    // stride, top/left pad
+  int ks;                // taps per side (3 or 5)
   int tile_rows;         // output rows per tile
   int tiles_per_img;
 };
@@ -729,18 +730,20 @@ __global__ void dw_finalize_kernel(int nparts, int C, const float* __restrict__ 
 }
 
 // ---------------------------------------------------------------- host
-int make_geo(int64_t N, int64_t H, int64_t W, int64_t C, int stride, const int* pads, int vec, Geo* g,
+int make_geo(int64_t N, int64_t H, int64_t W, int64_t C, int stride, int ks, const int* pads, int vec, Geo* g,
              const char* op) {
   DFX_REQUIRE(N > 0 && H > 0 && W > 0 && C > 0, DFX_ERR_SHAPE, std::string(op) + ": empty tensor");
   DFX_REQUIRE(stride == 1 || stride == 2, DFX_ERR_UNSUPPORTED, std::string(op) + ": stride must be 1 or 2");
+  DFX_REQUIRE(ks == 3 || ks == 5, DFX_ERR_UNSUPPORTED, std::string(op) + ": kernel size must be 3 or 5");
   DFX_REQUIRE(C % vec == 0, DFX_ERR_SHAPE, std::string(op) + ": channels must be a multiple of " + std::to_string(vec));
   DFX_REQUIRE(C / vec <= kThreads, DFX_ERR_SHAPE, std::string(op) + ": too many channels");
   for (int i = 0; i < 4; ++i)
-    DFX_REQUIRE(pads[i] >= 0 && pads[i] <= 2, DFX_ERR_UNSUPPORTED, std::string(op) + ": pads must be in [0, 2]");
+    DFX_REQUIRE(pads[i] >= 0 && pads[i] <= ks - 1, DFX_ERR_UNSUPPORTED,
+                std::string(op) + ": pads must be in [0, ksize-1]");
   g->N = (int)N; g->H = (int)H; g->W = (int)W; g->C = (int)C;
-  g->stride = stride; g->pt = pads[0]; g->pl = pads[1];
-  g->Ho = (int)((H + pads[0] + pads[2] - 3) / stride + 1);
-  g->Wo = (int)((W + pads[1] + pads[3] - 3) / stride + 1);
+  g->stride = stride; g->pt = pads[0]; g->pl = pads[1]; g->ks = ks;
+  g->Ho = (int)((H + pads[0] + pads[2] - ks) / stride + 1);
+  g->Wo = (int)((W + pads[1] + pads[3] - ks) / stride + 1);
   DFX_REQUIRE(g->Ho > 0 && g->Wo > 0, DFX_ERR_SHAPE, std::string(op) + ": output would be empty");
   g->tile_rows = std::max(1, 2048 / g->Wo);
   if (g->tile_rows > g->Ho) g->tile_rows = g->Ho;
@@ -751,7 +754,7 @@ int make_geo(int64_t N, int64_t H, int64_t W, int64_t C, int stride, const int* 
 template <typename T> constexpr int vec_of() { return MbVec<T>::value; }
 
 // TMA ring path (dwconv.cu) geometry of this block: 3x3 taps
-inline DwShape dw_shape(const Geo& g) { return DwShape{g.N, g.H, g.W, g.Ho, g.Wo, g.C, 3, g.stride, g.pt, g.pl}; }
+inline DwShape dw_shape(const Geo& g) { return DwShape{g.N, g.H, g.W, g.Ho, g.Wo, g.C, g.ks, g.stride, g.pt, g.pl}; }
 inline bool ring_ok(const Geo& g) { return dw_ring_ok(dw_shape(g), 2) && dw_ring_ok(dw_shape(g), 4); }
 // ring-path scratch (floats): partials [tiles][9][C] (>= [tiles][3][C]) then dz
 inline size_t ring_part_floats(const Geo& g) {
@@ -773,6 +776,7 @@ int mb_forward(const Geo& g, const void* x, const float* w, void* z, float* bn_p
                cudaStream_t st) {
   constexpr int V = vec_of<T>();
   if (ring_ok(g)) return dw_conv_stats(sizeof(T) == 2 ? DFX_BF16 : DFX_F32, dw_shape(g), x, w, z, bn_part, bn_local, st);
+  DFX_REQUIRE(g.ks == 3, DFX_ERR_UNSUPPORTED, "dfx_mbconv_fwd_stats: 5x5 needs the TMA ring path (C % 8 == 0)");
   const int CV = g.C / V, PY = kThreads / CV, threads = CV * PY;
   const int ntiles = g.N * g.tiles_per_img;
   const size_t sm1 = (size_t)(PY + 2 * PY * g.C) * sizeof(float);
@@ -790,9 +794,10 @@ int mb_forward(const Geo& g, const void* x, const float* w, void* z, float* bn_p
 extern "C" {
 
 /* Workspace sizes (floats) are computed by dfx_mbconv_workspace. */
-size_t dfx_mbconv_workspace(int64_t N, int64_t H, int64_t W, int64_t C, int stride, const int* pads, int SE) {
+size_t dfx_mbconv_workspace(int64_t N, int64_t H, int64_t W, int64_t C, int stride, int ksize, const int* pads,
+                            int SE) {
   Geo g;
-  if (make_geo(N, H, W, C, stride, pads, 4, &g, "dfx_mbconv_workspace")) return 0;
+  if (make_geo(N, H, W, C, stride, ksize, pads, 4, &g, "dfx_mbconv_workspace")) return 0;
   const size_t ntiles = (size_t)g.N * g.tiles_per_img;
   const size_t nsm = (size_t)4 * num_sms();
   // bn_part 2C*tiles | pool_part C*tiles | bwd_part 5C*tiles | de N*C | dr N*SE | nsum 2NC | dw_part 9C*grid
@@ -806,14 +811,15 @@ size_t dfx_mbconv_workspace(int64_t N, int64_t H, int64_t W, int64_t C, int stri
   return sizeof(float) * fl + 256;
 }
 
-int dfx_mbconv_fwd_stats(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride, const int* pads,
+int dfx_mbconv_fwd_stats(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride, int ksize,
+    const int* pads,
                          const void* x, const float* w_dw, void* z, float* bn_local, void* workspace,
                          size_t ws_bytes, void* stream) {
   const int V = dtype == DFX_BF16 ? 8 : 4;
   Geo g;
-  if (int rc = make_geo(N, H, W, C, stride, pads, V, &g, "dfx_mbconv_fwd_stats")) return rc;
+  if (int rc = make_geo(N, H, W, C, stride, ksize, pads, V, &g, "dfx_mbconv_fwd_stats")) return rc;
   DFX_REQUIRE(x && w_dw && z && bn_local && workspace, DFX_ERR_SHAPE, "dfx_mbconv_fwd_stats: null pointer");
-  DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, pads, 1), DFX_ERR_WORKSPACE,
+  DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, ksize, pads, 1), DFX_ERR_WORKSPACE,
               "dfx_mbconv_fwd_stats: workspace too small");
   float* bn_part = (float*)workspace;
   if (dtype == DFX_BF16)
@@ -832,16 +838,17 @@ int dfx_bn_finalize(int64_t C, int nsets, const float* sets, float eps, float mo
   return DFX_OK;
 }
 
-int dfx_mbconv_fwd_se(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride, const int* pads, int64_t SE,
+int dfx_mbconv_fwd_se(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride, int ksize,
+    const int* pads, int64_t SE,
                       const void* z, const float* mean, const float* rstd, const float* gamma, const float* beta,
                       const float* w_r, const float* b_r, const float* w_e, const float* b_e, float* pooled,
                       float* r, float* s, void* y, void* workspace, size_t ws_bytes, void* stream) {
   const int V = dtype == DFX_BF16 ? 8 : 4;
   Geo g;
-  if (int rc = make_geo(N, H, W, C, stride, pads, V, &g, "dfx_mbconv_fwd_se")) return rc;
+  if (int rc = make_geo(N, H, W, C, stride, ksize, pads, V, &g, "dfx_mbconv_fwd_se")) return rc;
   DFX_REQUIRE(SE > 0 && z && mean && rstd && gamma && beta && w_r && b_r && w_e && b_e && pooled && r && s && y,
               DFX_ERR_SHAPE, "dfx_mbconv_fwd_se: null pointer");
-  DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, pads, (int)SE), DFX_ERR_WORKSPACE,
+  DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, ksize, pads, (int)SE), DFX_ERR_WORKSPACE,
               "dfx_mbconv_fwd_se: workspace too small");
   cudaStream_t st = as_stream(stream);
   const int ntiles = g.N * g.tiles_per_img;
@@ -873,7 +880,8 @@ int dfx_mbconv_fwd_se(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
   return DFX_OK;
 }
 
-int dfx_mbconv_bwd_reduce(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride, const int* pads,
+int dfx_mbconv_bwd_reduce(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride, int ksize,
+    const int* pads,
                           int64_t SE, const void* dy, const void* z, const float* mean, const float* rstd,
                           const float* gamma, const float* beta, const float* s, const float* r,
                           const float* pooled, const float* w_r, const float* w_e, float* dw_e, float* db_e,
@@ -881,11 +889,11 @@ int dfx_mbconv_bwd_reduce(int dtype, int64_t N, int64_t H, int64_t W, int64_t C,
                           void* stream) {
   const int V = dtype == DFX_BF16 ? 8 : 4;
   Geo g;
-  if (int rc = make_geo(N, H, W, C, stride, pads, V, &g, "dfx_mbconv_bwd_reduce")) return rc;
+  if (int rc = make_geo(N, H, W, C, stride, ksize, pads, V, &g, "dfx_mbconv_bwd_reduce")) return rc;
   DFX_REQUIRE(dy && z && mean && rstd && gamma && beta && s && r && pooled && w_r && w_e && dw_e && db_e && dw_r &&
                   db_r && dpool && bnsum,
               DFX_ERR_SHAPE, "dfx_mbconv_bwd_reduce: null pointer");
-  DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, pads, (int)SE), DFX_ERR_WORKSPACE,
+  DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, ksize, pads, (int)SE), DFX_ERR_WORKSPACE,
               "dfx_mbconv_bwd_reduce: workspace too small");
   cudaStream_t st = as_stream(stream);
   const int ntiles = g.N * g.tiles_per_img;
@@ -918,18 +926,19 @@ int dfx_mbconv_bwd_reduce(int dtype, int64_t N, int64_t H, int64_t W, int64_t C,
   return DFX_OK;
 }
 
-int dfx_mbconv_bwd_dx(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride, const int* pads,
+int dfx_mbconv_bwd_dx(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride, int ksize,
+    const int* pads,
                       const void* dy, const void* z, const void* x, const float* w_dw, const float* mean,
                       const float* rstd, const float* gamma, const float* beta, const float* s, const float* dpool,
                       const float* bnsum, double count, void* dx, float* dw_dw, void* workspace, size_t ws_bytes,
                       void* stream) {
   const int V = dtype == DFX_BF16 ? 8 : 4;
   Geo g;
-  if (int rc = make_geo(N, H, W, C, stride, pads, V, &g, "dfx_mbconv_bwd_dx")) return rc;
+  if (int rc = make_geo(N, H, W, C, stride, ksize, pads, V, &g, "dfx_mbconv_bwd_dx")) return rc;
   DFX_REQUIRE(dy && z && x && w_dw && mean && rstd && gamma && beta && s && dpool && bnsum && dx && dw_dw,
               DFX_ERR_SHAPE, "dfx_mbconv_bwd_dx: null pointer");
   DFX_REQUIRE(count > 0, DFX_ERR_SHAPE, "dfx_mbconv_bwd_dx: count must be positive");
-  DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, pads, 1), DFX_ERR_WORKSPACE,
+  DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, ksize, pads, 1), DFX_ERR_WORKSPACE,
               "dfx_mbconv_bwd_dx: workspace too small");
   cudaStream_t st = as_stream(stream);
   if (ring_ok(g)) {
@@ -943,6 +952,7 @@ int dfx_mbconv_bwd_dx(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
     if (int rc = dw_dz_dw(dtype, d, x, dy, z, k, dzb, part, dw_dw, st)) return rc;
     return dw_dx(dtype, d, dzb, w_dw, dx, st);
   }
+  DFX_REQUIRE(g.ks == 3, DFX_ERR_UNSUPPORTED, "dfx_mbconv_bwd_dx: 5x5 needs the TMA ring path (C % 8 == 0)");
   const int ntiles_conv = g.N * ((g.Ho + TO - 1) / TO) * ((g.Wo + TO - 1) / TO);
   const int grid = std::min(ntiles_conv, 4 * num_sms());
   const size_t ntiles = (size_t)g.N * g.tiles_per_img;

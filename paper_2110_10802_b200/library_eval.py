@@ -227,18 +227,19 @@ def _conv(attrs, inputs):
     if x.ndim != 4 or w.ndim != 4:
         raise ShapeError("Conv: X and W must be rank 4 (N, C, H, W)")
     N, C, H, W = x.shape
-    if int(attrs["group"]) != C or w.shape != (C, 1, 3, 3):
-        raise UnsupportedOp("Conv: only depthwise 3x3 (group = C, weight (C,1,3,3)) runs on the B200 path")
+    k = w.shape[-1]
+    if int(attrs["group"]) != C or w.shape != (C, 1, k, k) or k not in (3, 5):
+        raise UnsupportedOp("Conv: only depthwise 3x3 / 5x5 (group = C, weight (C,1,k,k)) runs on the B200 path")
     stride, pads = _pads_strides(attrs)
     tx = _dev(np.moveaxis(x, 1, -1))
-    tw = _dev(w.reshape(C, 9).T)
-    Ho = (H + pads[0] + pads[2] - 3) // stride + 1
-    Wo = (W + pads[1] + pads[3] - 3) // stride + 1
+    tw = _dev(w.reshape(C, k * k).T)
+    Ho = (H + pads[0] + pads[2] - k) // stride + 1
+    Wo = (W + pads[1] + pads[3] - k) // stride + 1
     z = torch.empty(N, Ho, Wo, C, device="cuda")
     local = torch.empty(3, C, device="cuda")
     pc = (ctypes.c_int * 4)(*pads)
-    ws = K.WORKSPACE.get(_lib.load().dfx_mbconv_workspace(N, H, W, C, stride, pc, 1))
-    _lib.call("dfx_mbconv_fwd_stats", _lib.DFX_F32, N, H, W, C, stride, pc, tx.data_ptr(), tw.data_ptr(),
+    ws = K.WORKSPACE.get(_lib.load().dfx_mbconv_workspace(N, H, W, C, stride, k, pc, 1))
+    _lib.call("dfx_mbconv_fwd_stats", _lib.DFX_F32, N, H, W, C, stride, k, pc, tx.data_ptr(), tw.data_ptr(),
               z.data_ptr(), local.data_ptr(), ws.data_ptr(), ws.numel(), K._stream())
     return [np.moveaxis(_host(z, x), -1, 1)]
 

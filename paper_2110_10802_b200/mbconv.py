@@ -41,6 +41,7 @@ class MBConvConfig:
     se: int = 4
     stride: int = 1
     pads: tuple = (1, 1, 1, 1)
+    ksize: int = 3
     eps: float = 1e-3
     momentum: float = 0.99
     dtype: torch.dtype = torch.float32
@@ -48,7 +49,7 @@ class MBConvConfig:
 
 def _specs(c: MBConvConfig):
     C, SE = c.channels, c.se
-    return [("wdw", (3, 3, C)), ("g", (C,)), ("b", (C,)), ("wr", (SE, C)), ("br", (SE,)),
+    return [("wdw", (c.ksize, c.ksize, C)), ("g", (C,)), ("b", (C,)), ("wr", (SE, C)), ("br", (SE,)),
             ("we", (C, SE)), ("be", (C,))]
 
 
@@ -70,7 +71,7 @@ class MBConvBlock:
         self._bufs = {}
         g = torch.Generator(device="cpu").manual_seed(seed)
         self.load_params({
-            "wdw": 0.3 * torch.randn(C, 1, 3, 3, generator=g),
+            "wdw": 0.3 * torch.randn(C, 1, cfg.ksize, cfg.ksize, generator=g),
             "g": 1 + 0.1 * torch.randn(C, generator=g), "b": 0.1 * torch.randn(C, generator=g),
             "wr": 0.3 * torch.randn(cfg.se, C, generator=g), "br": 0.1 * torch.randn(cfg.se, generator=g),
             "we": 0.3 * torch.randn(C, cfg.se, generator=g), "be": 0.1 * torch.randn(C, generator=g)})
@@ -82,7 +83,8 @@ class MBConvBlock:
         for name, _ in _specs(self.cfg):
             v = torch.as_tensor(vals[name], dtype=torch.float32)
             if name == "wdw":
-                v = v.reshape(self.cfg.channels, 3, 3).permute(1, 2, 0)
+                k = self.cfg.ksize
+                v = v.reshape(self.cfg.channels, k, k).permute(1, 2, 0)
             self.master[name].copy_(v.to(self.device))
         if "rm" in vals:
             self.running_mean.copy_(torch.as_tensor(vals["rm"], dtype=torch.float32))
@@ -91,7 +93,8 @@ class MBConvBlock:
 
     def grads_numpy(self):
         out = {k: v.detach().cpu().double().numpy() for k, v in self.grad.views.items()}
-        out["wdw"] = out["wdw"].transpose(2, 0, 1).reshape(self.cfg.channels, 1, 3, 3)
+        k = self.cfg.ksize
+        out["wdw"] = out["wdw"].transpose(2, 0, 1).reshape(self.cfg.channels, 1, k, k)
         return out
 
     # ------------------------------------------------------------ buffers
@@ -100,8 +103,9 @@ class MBConvBlock:
         if C != self.cfg.channels:
             raise ShapeError(f"MBConvBlock: expected {self.cfg.channels} channels, got {C}")
         p = self.cfg.pads
-        Ho = (H + p[0] + p[2] - 3) // self.cfg.stride + 1
-        Wo = (W + p[1] + p[3] - 3) // self.cfg.stride + 1
+        k = self.cfg.ksize
+        Ho = (H + p[0] + p[2] - k) // self.cfg.stride + 1
+        Wo = (W + p[1] + p[3] - k) // self.cfg.stride + 1
         return N, H, W, C, Ho, Wo
 
     def buffers(self, x_shape):
@@ -111,7 +115,7 @@ class MBConvBlock:
             N, H, W, C, Ho, Wo = self._geo(x_shape)
             dev, dt = self.device, c.dtype
             f = lambda *s: torch.empty(s, dtype=torch.float32, device=dev)  # noqa: E731
-            ws = _lib.load().dfx_mbconv_workspace(N, H, W, C, c.stride, self._pads(), c.se)
+            ws = _lib.load().dfx_mbconv_workspace(N, H, W, C, c.stride, c.ksize, self._pads(), c.se)
             self._bufs[key] = dict(
                 z=torch.empty(N, Ho, Wo, C, dtype=dt, device=dev),
                 y=torch.empty(N, Ho, Wo, C, dtype=dt, device=dev),
@@ -143,7 +147,7 @@ class MBConvBlock:
         self._saved = x
         esz = x.element_size()
         with K._span("mbconv.dwconv_stats", "hbm", lambda: (N * H * W + N * Ho * Wo) * C * esz):
-            _lib.call("dfx_mbconv_fwd_stats", dt, N, H, W, C, c.stride, pads, x.data_ptr(),
+            _lib.call("dfx_mbconv_fwd_stats", dt, N, H, W, C, c.stride, c.ksize, pads, x.data_ptr(),
                       P["wdw"].data_ptr(), b["z"].data_ptr(), b["bn_local"].data_ptr(), ws.data_ptr(),
                       ws.numel(), st)
         if self.world > 1:
@@ -156,7 +160,7 @@ class MBConvBlock:
                       b["mean"].data_ptr(), b["var"].data_ptr(), b["rstd"].data_ptr(),
                       self.running_mean.data_ptr(), self.running_var.data_ptr(), st)
         with K._span("mbconv.bn_swish_se_excite", "hbm", lambda: 3 * N * Ho * Wo * C * esz):
-            _lib.call("dfx_mbconv_fwd_se", dt, N, H, W, C, c.stride, pads, c.se, b["z"].data_ptr(),
+            _lib.call("dfx_mbconv_fwd_se", dt, N, H, W, C, c.stride, c.ksize, pads, c.se, b["z"].data_ptr(),
                       b["mean"].data_ptr(), b["rstd"].data_ptr(), P["g"].data_ptr(), P["b"].data_ptr(),
                       P["wr"].data_ptr(), P["br"].data_ptr(), P["we"].data_ptr(), P["be"].data_ptr(),
                       b["pooled"].data_ptr(), b["r"].data_ptr(), b["s"].data_ptr(), b["y"].data_ptr(),
@@ -178,7 +182,7 @@ class MBConvBlock:
         ws = b["ws"]
         esz = x.element_size()
         with K._span("mbconv.bwd_reduce", "hbm", lambda: 2 * N * Ho * Wo * C * esz):
-            _lib.call("dfx_mbconv_bwd_reduce", dt, N, H, W, C, c.stride, pads, c.se, dy.data_ptr(),
+            _lib.call("dfx_mbconv_bwd_reduce", dt, N, H, W, C, c.stride, c.ksize, pads, c.se, dy.data_ptr(),
                       b["z"].data_ptr(), b["mean"].data_ptr(), b["rstd"].data_ptr(), P["g"].data_ptr(),
                       P["b"].data_ptr(), b["s"].data_ptr(), b["r"].data_ptr(), b["pooled"].data_ptr(),
                       P["wr"].data_ptr(), P["we"].data_ptr(), G["we"].data_ptr(), G["be"].data_ptr(),
@@ -191,7 +195,7 @@ class MBConvBlock:
             allreduce_sum(b["bnsum"], group=self.pg)
         count = float(N * Ho * Wo * self.world)
         with K._span("mbconv.dwconv_bwd", "hbm", lambda: (2 * N * Ho * Wo + 2 * N * H * W) * C * esz):
-            _lib.call("dfx_mbconv_bwd_dx", dt, N, H, W, C, c.stride, pads, dy.data_ptr(), b["z"].data_ptr(),
+            _lib.call("dfx_mbconv_bwd_dx", dt, N, H, W, C, c.stride, c.ksize, pads, dy.data_ptr(), b["z"].data_ptr(),
                       x.data_ptr(), P["wdw"].data_ptr(), b["mean"].data_ptr(), b["rstd"].data_ptr(),
                       P["g"].data_ptr(), P["b"].data_ptr(), b["s"].data_ptr(), b["dpool"].data_ptr(),
                       b["bnsum"].data_ptr(), count, b["dx"].data_ptr(), G["wdw"].data_ptr(), ws.data_ptr(),

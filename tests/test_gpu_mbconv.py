@@ -100,6 +100,35 @@ def test_vs_oracle(dtype, stride, pads, hw):
     _check(errs, 1e-4 if dtype == torch.float32 else 2e-2)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("stride,hw,C", [(1, 14, 48), (2, 15, 40), (1, 7, 1152 // 8)])
+def test_5x5_vs_oracle(dtype, stride, hw, C):
+    """5x5 depthwise (EfficientNet-B0 stages 3, 5, 6) through the TMA ring path."""
+    rng = np.random.default_rng(hw * 7 + stride + C)
+    N, SE, k, pads = 3, 8, 5, (2, 2, 2, 2)
+    prm, x = _rand_case(rng, N, C, hw, hw, SE)
+    prm["wdw"] = 0.2 * rng.standard_normal((C, 1, k, k))
+    if dtype == torch.bfloat16:
+        x = O.round_bf16(x).astype(np.float64)
+    rnd = (lambda a: O.round_bf16(a).astype(np.float64)) if dtype == torch.bfloat16 else None
+    y_w, rm_w, rv_w, cache = O.mbconv_fwd(prm, x, stride, 1e-3, 0.99, rnd=rnd, pads=pads)
+    dy = rng.standard_normal(y_w.shape)
+    if dtype == torch.bfloat16:
+        dy = O.round_bf16(dy).astype(np.float64)
+    gw = O.mbconv_bwd(prm, cache, dy)
+    from paper_2110_10802_b200.mbconv import MBConvBlock, MBConvConfig
+
+    blk = MBConvBlock(MBConvConfig(channels=C, se=SE, stride=stride, pads=pads, ksize=k, dtype=dtype), seed=5)
+    blk.load_params(prm)
+    y, dx = _run(blk, x, dy, dtype)
+    errs = {"y": O.compare(y, y_w), "dx": O.compare(dx, gw["x"]),
+            "rm": O.compare(blk.running_mean.cpu().numpy(), rm_w)}
+    gr = blk.grads_numpy()
+    for kk in GRADS[1:]:
+        errs[kk] = O.compare(gr[kk], gw[kk])
+    _check(errs, 1e-4 if dtype == torch.float32 else 2e-2)
+
+
 def test_syncbn_merge_equals_global_batch():
     """SyncBN statistics: merging the per-rank (count, mean, M2) sets of two
     half batches equals BatchNorm over the concatenated batch."""
@@ -116,9 +145,9 @@ def test_syncbn_merge_equals_global_batch():
     def stats(xx):
         z = torch.empty_like(xx)
         loc = torch.empty(3, C, device="cuda")
-        ws = torch.empty(lib.dfx_mbconv_workspace(xx.shape[0], H, H, C, 1, pads, 4), dtype=torch.uint8,
+        ws = torch.empty(lib.dfx_mbconv_workspace(xx.shape[0], H, H, C, 1, 3, pads, 4), dtype=torch.uint8,
                          device="cuda")
-        _lib.check(lib.dfx_mbconv_fwd_stats(0, xx.shape[0], H, H, C, 1, pads, xx.data_ptr(),
+        _lib.check(lib.dfx_mbconv_fwd_stats(0, xx.shape[0], H, H, C, 1, 3, pads, xx.data_ptr(),
                                             blk.master["wdw"].data_ptr(), z.data_ptr(), loc.data_ptr(),
                                             ws.data_ptr(), ws.numel(), st))
         return loc
