@@ -279,6 +279,22 @@ int dfx_batchnorm_act_bwd_dx(int dtype, int64_t rows, int64_t C, const void* dy,
                              const float* beta, int act, const float* bnsum, double count, void* dx,
                              void* stream);
 
+/* ---- C5: EfficientNet-B0 training-step glue (NHWC) ------------------------
+ * stem im2col for a 3x3 conv (frontend.py:598-678): cols [N*Ho*Wo, Kp] with
+ *   k = (ky*3 + kx)*Cin + c, zeros for padding taps and k >= 9*Cin;
+ * GlobalAveragePool (frontend.py:681-706) and its VJP over [N, HW, C];
+ * softmax cross-entropy: loss = mean_n(logsumexp(z_n) - z_n[label_n]) (the
+ *   Softmax of frontend.py:488-501 + the log-likelihood of the label),
+ *   dlogits = (softmax(z) - onehot) / N;
+ * residual Add (frontend.py:291): out = a + b (out may alias a or b). */
+int dfx_im2col3x3(int dtype, int64_t N, int64_t H, int64_t W, int64_t Cin, int stride, const int* pads,
+                  int64_t Kp, const void* x, void* cols, void* stream);
+int dfx_avgpool_fwd(int dtype, int64_t N, int64_t HW, int64_t C, const void* x, void* pooled, void* stream);
+int dfx_avgpool_bwd(int dtype, int64_t N, int64_t HW, int64_t C, const void* dpooled, void* dx, void* stream);
+int dfx_softmax_xent(int64_t N, int64_t classes, const float* logits, const int32_t* labels, float* loss,
+                     float* loss_rows, int grad_dtype, void* dlogits, void* stream);
+int dfx_add(int dtype, int64_t n, const void* a, const void* b, void* out, void* stream);
+
 /* ---- optimizer (the user-written SGD step of the training loop) --
  * master -= lr * grad (f32); if weights_bf16 != NULL also refresh the bf16 copy. */
 int dfx_sgd_update(int64_t n, float* master, const float* grad, float lr, void* weights_bf16,

@@ -797,7 +797,7 @@ extern "C" {
 size_t dfx_mbconv_workspace(int64_t N, int64_t H, int64_t W, int64_t C, int stride, int ksize, const int* pads,
                             int SE) {
   Geo g;
-  if (make_geo(N, H, W, C, stride, ksize, pads, 4, &g, "dfx_mbconv_workspace")) return 0;
+  if (make_geo(N, H, W, C, stride, ksize, pads, C % 8 == 0 ? 8 : 4, &g, "dfx_mbconv_workspace")) return 0;
   const size_t ntiles = (size_t)g.N * g.tiles_per_img;
   const size_t nsm = (size_t)4 * num_sms();
   // bn_part 2C*tiles | pool_part C*tiles | bwd_part 5C*tiles | de N*C | dr N*SE | nsum 2NC | dw_part 9C*grid
