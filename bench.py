@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-extra", action="store_true", help="skip the C3 / C5 workload measurements")
     return ap.parse_args()
 
 
@@ -203,6 +204,158 @@ def peaks():
             "source": "fallback (B200_PROFILING.md)"}
 
 
+def _kernel_rows(timer, steps, pk):
+    rows = []
+    for r in timer.summary():
+        per_call_ms = r["ms"] / r["calls"]
+        work = r["work"] / r["calls"]
+        if r["kind"] == "hbm":
+            ach, peak, unit = work / (per_call_ms * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
+        else:
+            ach, peak, unit = work / (per_call_ms * 1e-3) / 1e12, pk["tflops"], "TFLOP/s"
+        rows.append({"kernel": r["label"], "bound": "hbm" if r["kind"] == "hbm" else "tensor",
+                     "calls_per_step": r["calls"] / steps, "us_per_call": round(per_call_ms * 1e3, 2),
+                     "share": 0.0, "achieved": round(ach, 1), "unit": unit, "frac": round(ach / peak, 3),
+                     "work_per_call": work})
+    tot = sum(r["us_per_call"] * r["calls_per_step"] for r in rows) or 1.0
+    for r in rows:
+        r["share"] = round(r["us_per_call"] * r["calls_per_step"] / tot, 3)
+    rows.sort(key=lambda r: -r["share"])
+    return rows
+
+
+def _timed_graph(step, k, flush):
+    import torch
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+    torch.cuda.synchronize()
+    for i in range(k):
+        flush.zero_()
+        evs[i][0].record()
+        step()
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs) / k
+
+
+def measure_mbconv_c3(steps, flush, pk):
+    """BASELINE.json configs[2]: one MBConv block (dw3x3 + BN + swish + SE),
+    N=96 x 112x112 x 96 channels, bf16, fwd + bwd as a CUDA graph."""
+    import torch
+
+    from paper_2110_10802_b200 import kernels as K
+    from paper_2110_10802_b200.graphs import CapturedStep
+    from paper_2110_10802_b200.mbconv import MBConvBlock, MBConvConfig
+
+    N, HW, C = 96, 112, 96
+    blk = MBConvBlock(MBConvConfig(channels=C, dtype=torch.bfloat16), device="cuda", seed=1)
+    g = torch.Generator(device="cpu").manual_seed(7)
+    x = torch.randn(N, HW, HW, C, generator=g).bfloat16().cuda()
+    dy = torch.randn(N, HW, HW, C, generator=g).bfloat16().cuda()
+
+    def fn():
+        blk.forward(x)
+        blk.backward(dy)
+
+    cs = CapturedStep(fn)
+    timer = K.KernelTimer()
+    with timer:
+        inst = CapturedStep(fn, warmup=0)
+    ms = _timed_graph(cs.replay, steps, flush)
+    timer.totals = {}
+    for _ in range(max(3, steps // 4)):
+        flush.zero_()
+        inst.replay()
+        timer.collect()
+    rows = _kernel_rows(timer, max(3, steps // 4), pk)
+    elems = N * HW * HW * C
+    # compulsory traffic of the schedule: fwd conv (x, z) + pool (z) + excite (z, y);
+    # bwd reduce (dy, z) + dz/dw (x, dy, z, dz) + dx (dz, dx) = 13 tensor passes
+    traffic = 13 * elems * 2
+    return {"metric": "MBConv block fwd+bwd throughput (bf16, N=96, 112x112, C=96, dw3x3+BN+swish+SE)",
+            "value": round(N * 1e3 / ms, 1), "unit": "images/s", "ms_per_step": round(ms, 4),
+            "config": {"workload": "mbconv_block (BASELINE.json configs[2])", "batch": N, "hw": HW,
+                       "channels": C, "stride": 1, "se": 4, "dtype": "bf16"},
+            "hbm_gbs_effective": round(traffic / (ms * 1e-3) / 1e9, 1),
+            "hbm_frac_effective": round(traffic / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], 3),
+            "kernels": rows[:10]}
+
+
+def measure_effnet_c5(steps, flush, pk, world, rank, local, dist):
+    """BASELINE.json configs[4]: full EfficientNet-B0 training step, 96 images
+    of 224x224 per GPU, SyncBN + gradient allreduce when world > 1."""
+    import torch
+
+    from paper_2110_10802_b200 import kernels as K
+    from paper_2110_10802_b200.efficientnet import EfficientNetB0, EffNetConfig
+
+    N = 96
+    pg = dist.group.WORLD if world > 1 else None
+    net = EfficientNetB0(EffNetConfig(), device=f"cuda:{local}", seed=11, process_group=pg)
+    g = torch.Generator(device="cpu").manual_seed(200 + rank)
+    xh = torch.randn(N, 224, 224, 3, generator=g).bfloat16().pin_memory()
+    lh = torch.randint(0, 1000, (N,), generator=g, dtype=torch.int32).pin_memory()
+    dev = net.device_inputs(N)
+    dev["x"].copy_(xh)
+    dev["labels"].copy_(lh)
+    lr = 1e-3
+    rows = []
+    if world == 1:
+        from paper_2110_10802_b200.graphs import CapturedStep
+
+        cs = net.capture_step(N, lr)
+        step = cs.replay
+
+        timer = K.KernelTimer()
+        with timer:
+            inst = CapturedStep(lambda: net.train_step(dev["x"], dev["labels"], lr), warmup=0)
+        timer.totals = {}
+        for _ in range(3):
+            flush.zero_()
+            inst.replay()
+            timer.collect()
+        rows = _kernel_rows(timer, 3, pk)
+    else:
+        def step():
+            net.train_step(dev["x"], dev["labels"], None)
+            dist.all_reduce(net.grad.flat)
+            net.sgd_step(lr / world)
+    for _ in range(3):
+        step()
+    if world > 1:
+        dist.barrier()
+    ms = _timed_graph(step, steps, flush)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    loss_h = torch.empty(1).pin_memory()
+
+    def host_step():
+        net.train_step_host(xh, lh, lr=None if world > 1 else lr, loss_host=loss_h,
+                            graph=cs if world == 1 else None)
+        if world > 1:
+            dist.all_reduce(net.grad.flat)
+            net.sgd_step(lr / world)
+
+    e2e_ms = _timed_graph(host_step, max(3, steps // 2), flush)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d, d2h = net.host_inputs_bytes(N)
+    return {"metric": "EfficientNet-B0 training step throughput (bf16, 96 images/GPU, 224x224)",
+            "value": round(world * N * 1e3 / ms, 1), "unit": "images/s", "ms_per_step": round(ms, 3),
+            "n_gpus": world, "scaling": "weak",
+            "config": {"workload": "efficientnet_b0_train_step (BASELINE.json configs[4])", "batch_per_gpu": N,
+                       "image": 224, "params": net.num_params, "parallelism": f"dp{world}",
+                       "syncbn": world > 1, "step": "fwd + bwd + SGD" + (" + NCCL allreduce" if world > 1 else ""),
+                       "execution": "CUDA graph" if world == 1 else "eager (SyncBN collectives)"},
+            "e2e": {"value": round(world * N * 1e3 / e2e_ms, 1), "unit": "images/s", "ms_per_step": round(e2e_ms, 3),
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "kernels": rows[:12]}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -332,6 +485,13 @@ def run_ours(args):
     flops = bert_layer_flops(B, S, H, NH, FF)
     gemm_tflops = flops / (gemm_us * 1e-6) / 1e12
 
+    workloads = {}
+    if not args.no_extra:
+        if rank == 0 and world == 1:
+            workloads["mbconv_c3"] = measure_mbconv_c3(max(10, args.steps // 4), flush, pk)
+        workloads["efficientnet_b0_c5"] = measure_effnet_c5(max(5, args.steps // 20), flush, pk, world, rank,
+                                                            local, dist)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, reps, el = cpu_reference_sample(args.cpu_seconds)
@@ -357,6 +517,7 @@ def run_ours(args):
             "kernels": rows,
             "cpu_baseline": cpu,
             "clocks": clocks,
+            "workloads": workloads,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

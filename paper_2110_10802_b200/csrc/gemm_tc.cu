@@ -448,20 +448,37 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   }
 }
 
-// Fixed-order split-K reduction: D = sum_s part[s] (f32 workspace).
+// Fixed-order split-K reduction: D = sum_s part[s] (f32 workspace).  Block =
+// 32 output elements x 8 split lanes (warp w sums splits w, w+8, ...; the 8
+// lane sums combine in order), so a 148-way split of a tiny weight gradient
+// is 19 loads deep per thread instead of 148.
 template <typename TO>
-__global__ void splitk_reduce_kernel(int splits, int64_t Z, int64_t m, int64_t n, const float* __restrict__ part,
-                                     TO* __restrict__ d, int64_t d_stride_m, int64_t d_stride_b1,
-                                     int64_t d_stride_b2, int64_t batch2) {
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(int splits, int64_t Z, int64_t m, int64_t n,
+                                                            const float* __restrict__ part, TO* __restrict__ d,
+                                                            int64_t d_stride_m, int64_t d_stride_b1,
+                                                            int64_t d_stride_b2, int64_t batch2) {
   pdl_trigger();
   pdl_wait();
+  __shared__ float red[8][33];
   const int64_t total = Z * m * n;
-  const int64_t per_split = total;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < total; base += (int64_t)gridDim.x * 32) {
+    const int64_t i = base + lane;
     float acc = 0.f;
-    for (int s = 0; s < splits; ++s) acc += part[s * per_split + i];
-    const int64_t col = i % n, row = (i / n) % m, z = i / (n * m);
-    d[(z / batch2) * d_stride_b1 + (z % batch2) * d_stride_b2 + row * d_stride_m + col] = from_f<TO>(acc);
+    if (i < total) {
+#pragma unroll 4
+      for (int s = w; s < splits; s += 8) acc += part[s * total + i];
+    }
+    red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && i < total) {
+      float v = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v += red[j][lane];
+      const int64_t col = i % n, row = (i / n) % m, z = i / (n * m);
+      d[(z / batch2) * d_stride_b1 + (z % batch2) * d_stride_b2 + row * d_stride_m + col] = from_f<TO>(v);
+    }
+    __syncthreads();
   }
 }
 
@@ -557,7 +574,11 @@ Plan plan(const dfx_gemm_args& p) {
       best.tiles = z * ((p.m + BM - 1) / BM) * ((p.n + 127) / 128);
     }
     int64_t s = std::min<int64_t>(sms / std::max<int64_t>(best.tiles, 1), kb / 4);
-    s = std::min<int64_t>(s, 8);
+    // few-tile, long-K weight gradients (EfficientNet 1x1 convs: K = N*H*W
+    // pixels, a 16..1152-square output) take up to one split per SM; the f32
+    // partials stay under 64 MB
+    const int64_t cap = std::max<int64_t>(8, (64ll << 20) / std::max<int64_t>(z * p.m * p.n * 4, 1));
+    s = std::min<int64_t>(s, cap);
     if (s >= 2) best.splits = (int)s;
   }
   best.kb_per_split = (int)((kb + best.splits - 1) / best.splits);
@@ -691,7 +712,7 @@ int gemm_tc(const dfx_gemm_args& p, cudaStream_t st) {
   rc = f32 ? launch_tc_any<float>(bn, pl.cg, ma, mb, tp, st) : launch_tc_any<__nv_bfloat16>(bn, pl.cg, ma, mb, tp, st);
   if (rc || pl.splits <= 1) return rc;
   const int64_t total = Z * p.m * p.n;
-  const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+  const int grid = (int)std::min<int64_t>((total + 31) / 32, (int64_t)num_sms() * 8);
   if (p.out_dtype == DFX_F32)
     launch_k(splitk_reduce_kernel<float>, grid, 256, 0, st, pl.splits, Z, p.m, p.n, part, (float*)p.d, p.d_stride_m,
                                                       p.d_stride_b1, p.d_stride_b2, p.batch2);

@@ -36,7 +36,11 @@ __device__ __forceinline__ Wf wmerge(Wf a, Wf b) {
 template <typename T> struct NV { static constexpr int value = 8; };
 template <> struct NV<float> { static constexpr int value = 4; };
 
-// block b handles rows [b*rpb, min((b+1)*rpb, rows)); thread (cv, py)
+// block b handles rows [b*rpb, min((b+1)*rpb, rows)); thread (cv, py) owns
+// channel vector cv and every PY-th row; rows are loaded four at a time (four
+// 128-bit loads in flight per thread).  Statistics are shifted sums (shift =
+// the thread's first row: no per-element division, no cancellation), turned
+// into a Welford (n, mean, M2) set per thread and merged in a fixed order.
 template <typename T, int V>
 __global__ void __launch_bounds__(kThreads) bn_stats_kernel(int64_t rows, int C, int64_t rpb, const T* __restrict__ x,
                                                            float* __restrict__ part /*[blocks][3][C]*/) {
@@ -47,29 +51,53 @@ __global__ void __launch_bounds__(kThreads) bn_stats_kernel(int64_t rows, int C,
   const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
   const int c0 = cv * V;
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, rows);
-  float cnt = 0.f, mean[V], m2[V];
-#pragma unroll
-  for (int i = 0; i < V; ++i) { mean[i] = 0.f; m2[i] = 0.f; }
-  for (int64_t r = r0 + py; r < r1; r += PY) {
+  float sh[V], s1[V], s2[V];
+  int cnt = 0;
+  int64_t r = r0 + py;
+  {
     Vec<T, V> v;
-    v.load(x + r * C + c0);
-    cnt += 1.f;
-    const float inv = 1.f / cnt;
+    if (r < r1) v.load(x + r * C + c0);
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      const float d = v.v[i] - mean[i];
-      mean[i] += d * inv;
-      m2[i] += d * (v.v[i] - mean[i]);
+      sh[i] = r < r1 ? v.v[i] : 0.f;
+      s1[i] = 0.f;
+      s2[i] = 0.f;
     }
+  }
+  for (; r + 3 * PY < r1; r += 4 * PY) {
+    Vec<T, V> v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q].load(x + (r + q * PY) * C + c0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const float d = v[q].v[i] - sh[i];
+        s1[i] += d;
+        s2[i] = fmaf(d, d, s2[i]);
+      }
+    cnt += 4;
+  }
+  for (; r < r1; r += PY) {
+    Vec<T, V> v;
+    v.load(x + r * C + c0);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float d = v.v[i] - sh[i];
+      s1[i] += d;
+      s2[i] = fmaf(d, d, s2[i]);
+    }
+    ++cnt;
   }
   float* s_n = sm;
   float* s_mean = sm + PY;
   float* s_m2 = s_mean + PY * C;
-  if (cv == 0) s_n[py] = cnt;
+  if (cv == 0) s_n[py] = (float)cnt;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    s_mean[py * C + c0 + i] = mean[i];
-    s_m2[py * C + c0 + i] = m2[i];
+    const float m = cnt ? s1[i] / (float)cnt : 0.f;
+    s_mean[py * C + c0 + i] = sh[i] + m;
+    s_m2[py * C + c0 + i] = cnt ? fmaxf(s2[i] - s1[i] * m, 0.f) : 0.f;
   }
   __syncthreads();
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
@@ -105,25 +133,57 @@ __global__ void __launch_bounds__(kThreads) bn_merge_kernel(int nparts, int C, c
   if (threadIdx.x == 0) { out[c] = sn[0]; out[C + c] = smn[0]; out[2 * C + c] = sm2[0]; }
 }
 
+// swish'(u) = s + u s (1 - s); bf16 storage uses the one-MUFU sigmoid
+template <typename T> __device__ __forceinline__ float sig_t(float u) {
+  if constexpr (sizeof(T) == 2) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(0.5f * u));
+    return fmaf(0.5f, y, 0.5f);
+  } else {
+    return sigmoid_f(u);
+  }
+}
+
+// rows-chunk grid, thread (cv, py): the per-channel constants live in
+// registers (u = x*P + Q), four rows in flight per thread
 template <typename T, int V, int ACT>
-__global__ void __launch_bounds__(kThreads) bn_apply_kernel(int64_t nvec, int C, const T* __restrict__ x,
+__global__ void __launch_bounds__(kThreads) bn_apply_kernel(int64_t rows, int C, int64_t rpb, const T* __restrict__ x,
                                                            const float* __restrict__ mean, const float* __restrict__ rstd,
                                                            const float* __restrict__ gamma, const float* __restrict__ beta,
                                                            T* __restrict__ y) {
   pdl_trigger();
   pdl_wait();
-  const int CV = C / V;
-  for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec; vi += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(vi % CV) * V;
-    Vec<T, V> xv, yv;
-    xv.load(x + vi * V);
+  const int CV = C / V, PY = blockDim.x / CV;
+  const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
+  const int c0 = cv * V;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, rows);
+  float P[V], Q[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    P[i] = rstd[c0 + i] * gamma[c0 + i];
+    Q[i] = beta[c0 + i] - mean[c0 + i] * P[i];
+  }
+  auto f = [&](const Vec<T, V>& xv, T* out) {
+    Vec<T, V> yv;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      const int c = c0 + i;
-      const float u = (xv.v[i] - mean[c]) * rstd[c] * gamma[c] + beta[c];
-      yv.v[i] = ACT ? u * sigmoid_f(u) : u;
+      const float u = fmaf(xv.v[i], P[i], Q[i]);
+      yv.v[i] = ACT ? u * sig_t<T>(u) : u;
     }
-    yv.store(y + vi * V);
+    yv.store(out);
+  };
+  int64_t r = r0 + py;
+  for (; r + 3 * PY < r1; r += 4 * PY) {
+    Vec<T, V> v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q].load(x + (r + q * PY) * C + c0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f(v[q], y + (r + q * PY) * C + c0);
+  }
+  for (; r < r1; r += PY) {
+    Vec<T, V> v;
+    v.load(x + r * C + c0);
+    f(v, y + r * C + c0);
   }
 }
 
@@ -142,37 +202,55 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(int64_t rows, i
   const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
   const int c0 = cv * V;
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, rows);
-  float mu[V], rs[V], gm[V], bt[V], s1[V], s2[V];
+  float P[V], Q[V], R[V], M[V], s1[V], s2[V];  // u = x*P + Q, xhat = x*R + M
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    mu[i] = mean[c0 + i]; rs[i] = rstd[c0 + i]; gm[i] = gamma[c0 + i]; bt[i] = beta[c0 + i];
-    s1[i] = 0.f; s2[i] = 0.f;
+    R[i] = rstd[c0 + i];
+    M[i] = -mean[c0 + i] * R[i];
+    P[i] = gamma[c0 + i] * R[i];
+    Q[i] = beta[c0 + i] - mean[c0 + i] * P[i];
+    s1[i] = 0.f;
+    s2[i] = 0.f;
   }
-  for (int64_t r = r0 + py; r < r1; r += PY) {
+  auto f = [&](const Vec<T, V>& dv, const Vec<T, V>& xv) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float xh = fmaf(xv.v[i], R[i], M[i]);
+      float du = dv.v[i];
+      if (ACT) {
+        const float u = fmaf(xv.v[i], P[i], Q[i]);
+        const float sg = sig_t<T>(u);
+        du *= sg * fmaf(u, 1.f - sg, 1.f);
+      }
+      s1[i] += du;
+      s2[i] = fmaf(du, xh, s2[i]);
+    }
+  };
+  int64_t r = r0 + py;
+  for (; r + 3 * PY < r1; r += 4 * PY) {
+    Vec<T, V> dv[4], xv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      dv[q].load(dy + (r + q * PY) * C + c0);
+      xv[q].load(x + (r + q * PY) * C + c0);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f(dv[q], xv[q]);
+  }
+  for (; r < r1; r += PY) {
     Vec<T, V> dv, xv;
     dv.load(dy + r * C + c0);
     xv.load(x + r * C + c0);
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const float xh = (xv.v[i] - mu[i]) * rs[i];
-      float du = dv.v[i];
-      if (ACT) {
-        const float u = xh * gm[i] + bt[i];
-        const float sg = sigmoid_f(u);
-        du *= sg + u * sg * (1.f - sg);
-      }
-      s1[i] += du;
-      s2[i] += du * xh;
-    }
+    f(dv, xv);
   }
   for (int q = 0; q < 2; ++q) {
 #pragma unroll
     for (int i = 0; i < V; ++i) sm[py * C + c0 + i] = q == 0 ? s1[i] : s2[i];
     __syncthreads();
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
-      float acc = 0.f;
+      double acc = 0.0;  // the cross-lane / cross-block merges run in f64
       for (int j = 0; j < PY; ++j) acc += sm[j * C + c];
-      part[((size_t)blockIdx.x * 2 + q) * C + c] = acc;
+      part[((size_t)blockIdx.x * 2 + q) * C + c] = (float)acc;
     }
     __syncthreads();
   }
@@ -183,13 +261,15 @@ __global__ void bn_sum_parts_kernel(int nparts, int C, const float* __restrict__
   pdl_wait();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= 2 * C) return;
-  float acc = 0.f;
+  double acc = 0.0;
   for (int b = 0; b < nparts; ++b) acc += part[(size_t)b * 2 * C + idx];
-  out[idx] = acc;
+  out[idx] = (float)acc;
 }
 
+// dx = A*du + Cx*x + B with A = gamma*rstd and the BN-VJP means folded into
+// per-channel constants (autodiff.py:1557-1617)
 template <typename T, int V, int ACT>
-__global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(int64_t nvec, int C, const T* __restrict__ dy,
+__global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(int64_t rows, int C, int64_t rpb, const T* __restrict__ dy,
                                                             const T* __restrict__ x, const float* __restrict__ mean,
                                                             const float* __restrict__ rstd,
                                                             const float* __restrict__ gamma,
@@ -198,25 +278,52 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(int64_t nvec, int C
                                                             T* __restrict__ dx) {
   pdl_trigger();
   pdl_wait();
-  const int CV = C / V;
-  for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec; vi += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(vi % CV) * V;
-    Vec<T, V> dv, xv, o;
-    dv.load(dy + vi * V);
-    xv.load(x + vi * V);
+  const int CV = C / V, PY = blockDim.x / CV;
+  const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
+  const int c0 = cv * V;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, rows);
+  float A[V], Cx[V], B[V], P[V], Q[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = c0 + i;
+    const float rs = rstd[c], mu = mean[c];
+    A[i] = gamma[c] * rs;
+    const float mdu = sums[c] * inv_count, mdux = sums[C + c] * inv_count;
+    Cx[i] = -A[i] * mdux * rs;
+    B[i] = -A[i] * mdu + A[i] * mdux * rs * mu;
+    P[i] = A[i];
+    Q[i] = beta[c] - mu * A[i];
+  }
+  auto f = [&](const Vec<T, V>& dv, const Vec<T, V>& xv, T* out) {
+    Vec<T, V> o;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      const int c = c0 + i;
-      const float xh = (xv.v[i] - mean[c]) * rstd[c];
       float du = dv.v[i];
       if (ACT) {
-        const float u = xh * gamma[c] + beta[c];
-        const float sg = sigmoid_f(u);
-        du *= sg + u * sg * (1.f - sg);
+        const float u = fmaf(xv.v[i], P[i], Q[i]);
+        const float sg = sig_t<T>(u);
+        du *= sg * fmaf(u, 1.f - sg, 1.f);
       }
-      o.v[i] = gamma[c] * rstd[c] * (du - sums[c] * inv_count - xh * sums[C + c] * inv_count);
+      o.v[i] = fmaf(A[i], du, fmaf(Cx[i], xv.v[i], B[i]));
     }
-    o.store(dx + vi * V);
+    o.store(out);
+  };
+  int64_t r = r0 + py;
+  for (; r + 3 * PY < r1; r += 4 * PY) {
+    Vec<T, V> dv[4], xv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      dv[q].load(dy + (r + q * PY) * C + c0);
+      xv[q].load(x + (r + q * PY) * C + c0);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f(dv[q], xv[q], dx + (r + q * PY) * C + c0);
+  }
+  for (; r < r1; r += PY) {
+    Vec<T, V> dv, xv;
+    dv.load(dy + r * C + c0);
+    xv.load(x + r * C + c0);
+    f(dv, xv, dx + r * C + c0);
   }
 }
 
@@ -246,6 +353,15 @@ int check_bn(int dtype, int64_t rows, int64_t C, const char* op) {
     }                                                                           \
   } while (0)
 
+// elementwise passes: >= 8 rows per thread lane, at most 8 blocks per SM
+void stream_blocks(int64_t rows, int PY, int64_t* rpb, int* nb) {
+  int64_t b = std::min<int64_t>((int64_t)num_sms() * 8, (rows + 8 * PY - 1) / (8 * PY));
+  if (b < 1) b = 1;
+  *rpb = (rows + b - 1) / b;
+  *nb = (int)((rows + *rpb - 1) / *rpb);
+}
+
+// reductions: partial sets per block (<= kMaxBlocks), >= 4 rows per thread lane
 void blocks_for(int64_t rows, int64_t* rpb, int* nb) {
   int64_t b = std::min<int64_t>(kMaxBlocks, (rows + 63) / 64);
   if (b < 1) b = 1;
@@ -298,9 +414,11 @@ int dfx_batchnorm_act_apply(int dtype, int64_t rows, int64_t C, const void* x, c
   DFX_REQUIRE(act == 0 || act == 1, DFX_ERR_UNSUPPORTED, "dfx_batchnorm_act_apply: act must be 0 or 1");
   cudaStream_t st = as_stream(stream);
   const int V = vec_width(dtype, C);
-  const int64_t nvec = rows * C / V;
-  const int grid = (int)std::min<int64_t>((nvec + 255) / 256, (int64_t)num_sms() * 16);
-#define A(TT, VV, ACT) { launch_k(bn_apply_kernel<TT, VV, ACT>, grid, 256, 0, st, nvec, (int)C, (const TT*)x, mean, rstd, gamma, beta, (TT*)y); }
+  const int CV = (int)C / V, PY = kThreads / CV;
+  int64_t rpb;
+  int nb;
+  stream_blocks(rows, PY, &rpb, &nb);
+#define A(TT, VV, ACT) { launch_k(bn_apply_kernel<TT, VV, ACT>, nb, CV * PY, 0, st, rows, (int)C, rpb, (const TT*)x, mean, rstd, gamma, beta, (TT*)y); }
   BN_DISPATCH(A, act);
 #undef A
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_apply");
@@ -346,11 +464,13 @@ int dfx_batchnorm_act_bwd_dx(int dtype, int64_t rows, int64_t C, const void* dy,
   DFX_REQUIRE(count > 0, DFX_ERR_SHAPE, "dfx_batchnorm_act_bwd_dx: count must be positive");
   cudaStream_t st = as_stream(stream);
   const int V = vec_width(dtype, C);
-  const int64_t nvec = rows * C / V;
-  const int grid = (int)std::min<int64_t>((nvec + 255) / 256, (int64_t)num_sms() * 16);
+  const int CV = (int)C / V, PY = kThreads / CV;
+  int64_t rpb;
+  int nb;
+  stream_blocks(rows, PY, &rpb, &nb);
   const float ic = (float)(1.0 / count);
 #define D(TT, VV, ACT) \
-  { launch_k(bn_bwd_dx_kernel<TT, VV, ACT>, grid, 256, 0, st, nvec, (int)C, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, bnsum, ic, (TT*)dx); }
+  { launch_k(bn_bwd_dx_kernel<TT, VV, ACT>, nb, CV * PY, 0, st, rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, bnsum, ic, (TT*)dx); }
   BN_DISPATCH(D, act);
 #undef D
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_dx");

@@ -153,9 +153,14 @@ _NULL = _Null()
 _LABEL = [None]
 
 
+_LABEL_NEST = False  # profiling tools: "outer/inner" call-site labels
+
+
 def _span(default_label, kind, work_fn):
     if _TIMER is None:
         return _NULL
+    if _LABEL_NEST and _LABEL[0]:
+        return _Span(f"{_LABEL[0]}/{default_label}", kind, work_fn())
     return _Span(_LABEL[0] or default_label, kind, work_fn())
 
 
@@ -167,7 +172,7 @@ class label:
 
     def __enter__(self):
         self.prev = _LABEL[0]
-        _LABEL[0] = self.name
+        _LABEL[0] = f"{self.prev}/{self.name}" if (_LABEL_NEST and self.prev) else self.name
 
     def __exit__(self, *exc):
         _LABEL[0] = self.prev
