@@ -514,26 +514,35 @@ __global__ void __launch_bounds__(256) taps_sum_kernel(int nparts, int taps, int
 }
 
 // dx for stride 2 (a gather: each input pixel receives the taps whose
-// output position has the right parity), V channels per thread
+// output position has the right parity), V channels per thread.  The launch
+// keeps (grid x block) a multiple of C/V, so a thread's channel group never
+// changes: its KS*KS*V weights are loaded once into registers.
 template <typename T, int KS>
-__global__ void __launch_bounds__(256) dw_dx_s2_kernel(const DwShape g, const T* __restrict__ dz,
+__global__ void __launch_bounds__(512) dw_dx_s2_kernel(const DwShape g, const T* __restrict__ dz,
                                                        const float* __restrict__ w, T* __restrict__ dx) {
   constexpr int V = VecOf<KS>::value;
   pdl_wait();
   pdl_trigger();
   const int CVn = g.C / V;
-  const int64_t total = (int64_t)g.N * g.Hi * g.Wi * CVn;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int cv = (int)(idx % CVn);
-    const int64_t pix = idx / CVn;
-    const int ix = (int)(pix % g.Wi);
-    const int iy = (int)((pix / g.Wi) % g.Hi);
-    const int n = (int)(pix / ((int64_t)g.Wi * g.Hi));
-    const int c = cv * V;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride_pix = (gridDim.x * blockDim.x) / CVn;
+  const int cv = tid % CVn;
+  const int c = cv * V;
+  float wr[KS * KS][V];
+#pragma unroll
+  for (int t = 0; t < KS * KS; ++t)
+#pragma unroll
+    for (int i = 0; i < V; ++i) wr[t][i] = __ldg(w + (size_t)t * g.C + c + i);
+  const int npix = g.N * g.Hi * g.Wi;
+  for (int pix = tid / CVn; pix < npix; pix += stride_pix) {
+    const int ix = pix % g.Wi;
+    const int t2 = pix / g.Wi;
+    const int iy = t2 % g.Hi;
+    const int n = t2 / g.Hi;
     float acc[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    const T* dzn = dz + (size_t)n * g.Ho * g.Wo * g.C + c;
 #pragma unroll
     for (int ky = 0; ky < KS; ++ky) {
       const int ty = iy + g.pt - ky;
@@ -543,12 +552,86 @@ __global__ void __launch_bounds__(256) dw_dx_s2_kernel(const DwShape g, const T*
         const int tx = ix + g.pl - kx;
         if (tx < 0 || (tx & 1) || (tx >> 1) >= g.Wo) continue;
         RV<T, V> v;
-        v.ldg(dz + (((size_t)n * g.Ho + (ty >> 1)) * g.Wo + (tx >> 1)) * g.C + c);
+        v.ldg(dzn + ((size_t)(ty >> 1) * g.Wo + (tx >> 1)) * g.C);
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[i] = fmaf(v.get(i), __ldg(w + (size_t)(ky * KS + kx) * g.C + c + i), acc[i]);
+        for (int i = 0; i < V; ++i) acc[i] = fmaf(v.get(i), wr[ky * KS + kx][i], acc[i]);
       }
     }
-    stv<V>(dx + pix * g.C + c, acc);
+    stv<V>(dx + (size_t)pix * g.C + c, acc);
+  }
+}
+
+// dx for stride 2 with the symmetric "same" padding pt = pl = KS/2 (every
+// EfficientNet stride-2 block): a thread owns a 2x2 block of input pixels
+// (2a..2a+1, 2b..2b+1) and one channel group; with the padding a compile-time
+// constant, the tap parities are compile-time too, so the block's dz window
+// (2x2 for k3, 3x3 for k5) is loaded once and every tap is one FMA — no
+// per-tap parity tests, one index decomposition per 4 outputs.
+template <typename T, int KS>
+__global__ void __launch_bounds__(512) dw_dx_s2_same_kernel(const DwShape g, const T* __restrict__ dz,
+                                                            const float* __restrict__ w, T* __restrict__ dx) {
+  constexpr int V = VecOf<KS>::value;
+  constexpr int PT = KS / 2;
+  constexpr int OMIN = -((KS - 1 - PT) / 2), OMAX = (1 + PT) / 2;  // dz offsets relative to (a, b)
+  constexpr int RW = OMAX - OMIN + 1;
+  pdl_wait();
+  pdl_trigger();
+  const int CVn = g.C / V;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride_blk = (gridDim.x * blockDim.x) / CVn;
+  const int c = (tid % CVn) * V;
+  float wr[KS * KS][V];
+#pragma unroll
+  for (int t = 0; t < KS * KS; ++t)
+#pragma unroll
+    for (int i = 0; i < V; ++i) wr[t][i] = __ldg(w + (size_t)t * g.C + c + i);
+  const int BH = (g.Hi + 1) / 2, BW = (g.Wi + 1) / 2;
+  const int nblk = g.N * BH * BW;
+  for (int blk = tid / CVn; blk < nblk; blk += stride_blk) {
+    const int b = blk % BW;
+    const int t2 = blk / BW;
+    const int a = t2 % BH;
+    const int n = t2 / BH;
+    const T* dzn = dz + (size_t)n * g.Ho * g.Wo * g.C + c;
+    float win[RW][RW][V];
+#pragma unroll
+    for (int oy = 0; oy < RW; ++oy)
+#pragma unroll
+      for (int ox = 0; ox < RW; ++ox) {
+        const int y = a + OMIN + oy, x = b + OMIN + ox;
+        RV<T, V> v;
+        if (y >= 0 && y < g.Ho && x >= 0 && x < g.Wo) {
+          v.ldg(dzn + ((size_t)y * g.Wo + x) * g.C);
+#pragma unroll
+          for (int i = 0; i < V; ++i) win[oy][ox][i] = v.get(i);
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) win[oy][ox][i] = 0.f;
+        }
+      }
+#pragma unroll
+    for (int dyy = 0; dyy < 2; ++dyy)
+#pragma unroll
+      for (int dxx = 0; dxx < 2; ++dxx) {
+        const int iy = 2 * a + dyy, ix = 2 * b + dxx;
+        if (iy >= g.Hi || ix >= g.Wi) continue;
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+#pragma unroll
+        for (int ky = 0; ky < KS; ++ky) {
+          if ((dyy + PT - ky) & 1) continue;  // compile-time after unrolling
+          const int oy = (dyy + PT - ky) / 2 - OMIN;
+#pragma unroll
+          for (int kx = 0; kx < KS; ++kx) {
+            if ((dxx + PT - kx) & 1) continue;
+            const int ox = (dxx + PT - kx) / 2 - OMIN;
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] = fmaf(win[oy][ox][i], wr[ky * KS + kx][i], acc[i]);
+          }
+        }
+        stv<V>(dx + (((size_t)n * g.Hi + iy) * g.Wi + ix) * g.C + c, acc);
+      }
   }
 }
 
@@ -737,14 +820,31 @@ int dw_dx(int dtype, const DwShape& g, const void* dz, const float* w, void* dx,
   if (g.s == 2) {
     const int V = g.ks == 3 ? 4 : 2;
     if (g.C % V) return fail(DFX_ERR_UNSUPPORTED, "dwconv dx: channels must be a multiple of the vector width");
-    const int64_t total = (int64_t)g.N * g.Hi * g.Wi * (g.C / V);
-    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+    const int CVn = g.C / V;
+    const int per_block = CVn <= 256 ? (256 / CVn) * CVn : (CVn <= 512 ? CVn : 0);
+    if (!per_block) return fail(DFX_ERR_UNSUPPORTED, "dwconv dx: too many channels for the stride-2 gather");
+    const int64_t total = (int64_t)g.N * g.Hi * g.Wi * CVn;
+    const int grid = (int)std::min<int64_t>((total + per_block - 1) / per_block, (int64_t)num_sms() * 8);
+    const bool same = g.pt == g.ks / 2 && g.pl == g.ks / 2;
+    if (same) {
+      const int64_t blocks = (int64_t)g.N * ((g.Hi + 1) / 2) * ((g.Wi + 1) / 2) * CVn;
+      const int grid2 = (int)std::min<int64_t>((blocks + per_block - 1) / per_block, (int64_t)num_sms() * 8);
+      if (dtype == DFX_BF16) {
+        if (g.ks == 3) launch_k(dw_dx_s2_same_kernel<__nv_bfloat16, 3>, grid2, per_block, 0, st, g, (const __nv_bfloat16*)dz, w, (__nv_bfloat16*)dx);
+        else launch_k(dw_dx_s2_same_kernel<__nv_bfloat16, 5>, grid2, per_block, 0, st, g, (const __nv_bfloat16*)dz, w, (__nv_bfloat16*)dx);
+      } else {
+        if (g.ks == 3) launch_k(dw_dx_s2_same_kernel<float, 3>, grid2, per_block, 0, st, g, (const float*)dz, w, (float*)dx);
+        else launch_k(dw_dx_s2_same_kernel<float, 5>, grid2, per_block, 0, st, g, (const float*)dz, w, (float*)dx);
+      }
+      DFX_LAUNCH_CHECK("dwconv dx (stride 2, same padding)");
+      return DFX_OK;
+    }
     if (dtype == DFX_BF16) {
-      if (g.ks == 3) launch_k(dw_dx_s2_kernel<__nv_bfloat16, 3>, grid, 256, 0, st, g, (const __nv_bfloat16*)dz, w, (__nv_bfloat16*)dx);
-      else launch_k(dw_dx_s2_kernel<__nv_bfloat16, 5>, grid, 256, 0, st, g, (const __nv_bfloat16*)dz, w, (__nv_bfloat16*)dx);
+      if (g.ks == 3) launch_k(dw_dx_s2_kernel<__nv_bfloat16, 3>, grid, per_block, 0, st, g, (const __nv_bfloat16*)dz, w, (__nv_bfloat16*)dx);
+      else launch_k(dw_dx_s2_kernel<__nv_bfloat16, 5>, grid, per_block, 0, st, g, (const __nv_bfloat16*)dz, w, (__nv_bfloat16*)dx);
     } else {
-      if (g.ks == 3) launch_k(dw_dx_s2_kernel<float, 3>, grid, 256, 0, st, g, (const float*)dz, w, (float*)dx);
-      else launch_k(dw_dx_s2_kernel<float, 5>, grid, 256, 0, st, g, (const float*)dz, w, (float*)dx);
+      if (g.ks == 3) launch_k(dw_dx_s2_kernel<float, 3>, grid, per_block, 0, st, g, (const float*)dz, w, (float*)dx);
+      else launch_k(dw_dx_s2_kernel<float, 5>, grid, per_block, 0, st, g, (const float*)dz, w, (float*)dx);
     }
     DFX_LAUNCH_CHECK("dwconv dx (stride 2)");
     return DFX_OK;

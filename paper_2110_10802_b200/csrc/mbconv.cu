@@ -228,18 +228,21 @@ __global__ void __launch_bounds__(kThreads) bn_swish_pool_kernel(Geo g, const T*
   pdl_trigger();
   pdl_wait();
   extern __shared__ float sm[];
-  const int CV = g.C / V;
-  const int PY = blockDim.x / CV;
-  const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
+  // channel chunks across gridDim.y (wide C at small H x W: enough CTAs/lanes)
+  const int CVt = g.C / V, CVc = (CVt + gridDim.y - 1) / gridDim.y, PY = blockDim.x / CVc;
+  const int lcv = threadIdx.x % CVc, py = threadIdx.x / CVc;
+  const int cv = blockIdx.y * CVc + lcv;
+  const bool on = cv < CVt;
+  const int cbeg = blockIdx.y * CVc * V, cend = min(cbeg + CVc * V, g.C);
   const int tile = blockIdx.x;
   const int n = tile / g.tiles_per_img;
   const int r0 = (tile % g.tiles_per_img) * g.tile_rows;
   const int r1 = min(r0 + g.tile_rows, g.Ho);
-  const int c0 = cv * V;
+  const int c0 = (on ? cv : 0) * V;
   float acc[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) acc[i] = 0.f;
-  if (py < PY) {
+  if (py < PY && on) {
     float sc[V], sh[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) {
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(kThreads) bn_swish_pool_kernel(Geo g, const T*
     for (int i = 0; i < V; ++i) sm[py * g.C + c0 + i] = acc[i];
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < g.C; c += blockDim.x) {
+  for (int c = cbeg + threadIdx.x; c < cend; c += blockDim.x) {
     float s = 0.f;
     for (int j = 0; j < PY; ++j) s += sm[j * g.C + c];
     part[(size_t)tile * g.C + c] = s;
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(kThreads) bn_swish_pool_kernel(Geo g, const T*
 
 // ---------------------------------------------------------------- K5
 // one block per sample.  Wr [SE][C], We [C][SE] (Gemm transB=1 layout).
-__global__ void __launch_bounds__(kThreads) se_fwd_kernel(Geo g, int SE, const float* __restrict__ part,
+__global__ void __launch_bounds__(1024) se_fwd_kernel(Geo g, int SE, const float* __restrict__ part,
                                                           const float* __restrict__ wr, const float* __restrict__ br,
                                                           const float* __restrict__ we, const float* __restrict__ be,
                                                           float* __restrict__ pooled, float* __restrict__ r_out,
@@ -296,6 +299,7 @@ __global__ void __launch_bounds__(kThreads) se_fwd_kernel(Geo g, int SE, const f
   const float inv_hw = 1.f / (float)(g.Ho * g.Wo);
   for (int c = threadIdx.x; c < g.C; c += blockDim.x) {
     float s = 0.f;
+#pragma unroll 4
     for (int t = 0; t < g.tiles_per_img; ++t) s += part[((size_t)n * g.tiles_per_img + t) * g.C + c];
     p[c] = s * inv_hw;
     pooled[(size_t)n * g.C + c] = s * inv_hw;
@@ -304,6 +308,7 @@ __global__ void __launch_bounds__(kThreads) se_fwd_kernel(Geo g, int SE, const f
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int j = warp; j < SE; j += nw) {
     float acc = 0.f;
+#pragma unroll 8
     for (int c = lane; c < g.C; c += 32) acc += wr[(size_t)j * g.C + c] * p[c];
     acc = warp_sum(acc) + br[j];
     if (lane == 0) {
@@ -314,6 +319,7 @@ __global__ void __launch_bounds__(kThreads) se_fwd_kernel(Geo g, int SE, const f
   __syncthreads();
   for (int c = threadIdx.x; c < g.C; c += blockDim.x) {
     float e = be[c];
+#pragma unroll 8
     for (int j = 0; j < SE; ++j) e += we[(size_t)c * SE + j] * r2[j];
     s_out[(size_t)n * g.C + c] = sigmoidf_(e);
   }
@@ -327,15 +333,18 @@ __global__ void __launch_bounds__(kThreads) excite_kernel(Geo g, const T* __rest
                                                           const float* __restrict__ s, T* __restrict__ y) {
   pdl_trigger();
   pdl_wait();
-  const int CV = g.C / V;
-  const int PY = blockDim.x / CV;
-  const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
-  if (py >= PY) return;
+  // channel chunks across gridDim.y (wide C at small H x W: enough CTAs/lanes)
+  const int CVt = g.C / V, CVc = (CVt + gridDim.y - 1) / gridDim.y, PY = blockDim.x / CVc;
+  const int lcv = threadIdx.x % CVc, py = threadIdx.x / CVc;
+  const int cv = blockIdx.y * CVc + lcv;
+  const bool on = cv < CVt;
+  const int cbeg = blockIdx.y * CVc * V, cend = min(cbeg + CVc * V, g.C);
+  if (py >= PY || !on) return;
   const int tile = blockIdx.x;
   const int n = tile / g.tiles_per_img;
   const int r0 = (tile % g.tiles_per_img) * g.tile_rows;
   const int r1 = min(r0 + g.tile_rows, g.Ho);
-  const int c0 = cv * V;
+  const int c0 = (on ? cv : 0) * V;
   float sc[V], sh[V], se[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) {
@@ -379,20 +388,23 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geo g, const T* __
   pdl_trigger();
   pdl_wait();
   extern __shared__ float sm[];
-  const int CV = g.C / V;
-  const int PY = blockDim.x / CV;
-  const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
+  // channel chunks across gridDim.y (wide C at small H x W: enough CTAs/lanes)
+  const int CVt = g.C / V, CVc = (CVt + gridDim.y - 1) / gridDim.y, PY = blockDim.x / CVc;
+  const int lcv = threadIdx.x % CVc, py = threadIdx.x / CVc;
+  const int cv = blockIdx.y * CVc + lcv;
+  const bool on = cv < CVt;
+  const int cbeg = blockIdx.y * CVc * V, cend = min(cbeg + CVc * V, g.C);
   const int tile = blockIdx.x;
   const int n = tile / g.tiles_per_img;
   const int r0 = (tile % g.tiles_per_img) * g.tile_rows;
   const int r1 = min(r0 + g.tile_rows, g.Ho);
-  const int c0 = cv * V;
+  const int c0 = (on ? cv : 0) * V;
   float a[5][V];
 #pragma unroll
   for (int k = 0; k < 5; ++k)
 #pragma unroll
     for (int i = 0; i < V; ++i) a[k][i] = 0.f;
-  if (py < PY) {
+  if (py < PY && on) {
     float mu[V], rs[V], gm[V], bt[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) {
@@ -445,12 +457,12 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geo g, const T* __
     }
   }
   for (int k = 0; k < 5; ++k) {
-    if (py < PY) {
+    if (py < PY && on) {
 #pragma unroll
       for (int i = 0; i < V; ++i) sm[py * g.C + c0 + i] = a[k][i];
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < g.C; c += blockDim.x) {
+    for (int c = cbeg + threadIdx.x; c < cend; c += blockDim.x) {
       float s = 0.f;
       for (int j = 0; j < PY; ++j) s += sm[j * g.C + c];
       part[((size_t)tile * 5 + k) * g.C + c] = s;
@@ -461,7 +473,7 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geo g, const T* __
 
 // ---------------------------------------------------------------- B2
 // one block per sample: SE VJP + per-sample BN-VJP sums.
-__global__ void __launch_bounds__(kThreads) se_bwd_kernel(Geo g, int SE, const float* __restrict__ part,
+__global__ void __launch_bounds__(1024) se_bwd_kernel(Geo g, int SE, const float* __restrict__ part,
                                                           const float* __restrict__ s, const float* __restrict__ r,
                                                           const float* __restrict__ wr, const float* __restrict__ we,
                                                           float* __restrict__ de_out /*[N][C]*/,
@@ -478,6 +490,7 @@ __global__ void __launch_bounds__(kThreads) se_bwd_kernel(Geo g, int SE, const f
   for (int idx = threadIdx.x; idx < 5 * g.C; idx += blockDim.x) {
     const int k = idx / g.C, c = idx % g.C;
     float acc = 0.f;
+#pragma unroll 4
     for (int t = 0; t < g.tiles_per_img; ++t) acc += part[(((size_t)n * g.tiles_per_img + t) * 5 + k) * g.C + c];
     A[idx] = acc;
   }
@@ -492,6 +505,7 @@ __global__ void __launch_bounds__(kThreads) se_bwd_kernel(Geo g, int SE, const f
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int j = warp; j < SE; j += nw) {
     float acc = 0.f;
+#pragma unroll 8
     for (int c = lane; c < g.C; c += 32) acc += we[(size_t)c * SE + j] * de[c];
     acc = warp_sum(acc);
     if (lane == 0) {
@@ -506,6 +520,7 @@ __global__ void __launch_bounds__(kThreads) se_bwd_kernel(Geo g, int SE, const f
   const float inv_hw = 1.f / (float)(g.Ho * g.Wo);
   for (int c = threadIdx.x; c < g.C; c += blockDim.x) {
     float dp = 0.f;
+#pragma unroll 8
     for (int j = 0; j < SE; ++j) dp += wr[(size_t)j * g.C + c] * dr[j];
     dp *= inv_hw;  // d loss / d a contribution per pixel
     dpool[(size_t)n * g.C + c] = dp;
@@ -516,54 +531,50 @@ __global__ void __launch_bounds__(kThreads) se_bwd_kernel(Geo g, int SE, const f
 }
 
 // ---------------------------------------------------------------- B3
-// grid: (C + SE*C + 2C ...) — one thread per output scalar, fixed-order sum over samples.
-__global__ void se_bwd_reduce_kernel(int N, int C, int SE, const float* __restrict__ de, const float* __restrict__ dr,
-                                     const float* __restrict__ r, const float* __restrict__ pooled,
-                                     const float* __restrict__ nsum, float* __restrict__ dwe /*[C][SE]*/,
-                                     float* __restrict__ dbe, float* __restrict__ dwr /*[SE][C]*/,
-                                     float* __restrict__ dbr, float* __restrict__ bnsum /*[2][C]*/) {
+// one WARP per output scalar: lanes stride the samples (n = lane, lane+32,
+// ...), then a fixed-order warp sum — deterministic, and every sample's load
+// is in flight at once instead of an N-long serial chain per thread.
+__global__ void __launch_bounds__(256) se_bwd_reduce_kernel(int N, int C, int SE, const float* __restrict__ de,
+                                                            const float* __restrict__ dr, const float* __restrict__ r,
+                                                            const float* __restrict__ pooled,
+                                                            const float* __restrict__ nsum, float* __restrict__ dwe /*[C][SE]*/,
+                                                            float* __restrict__ dbe, float* __restrict__ dwr /*[SE][C]*/,
+                                                            float* __restrict__ dbr, float* __restrict__ bnsum /*[2][C]*/) {
   pdl_trigger();
   pdl_wait();
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int n_we = C * SE, n_wr = SE * C;
-  if (idx < n_we) {
-    const int c = idx / SE, j = idx % SE;
+  const int lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)C * SE * 2 + C + SE + 2 * C;
+  for (int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; idx < total;
+       idx += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t n_we = (int64_t)C * SE, n_wr = (int64_t)SE * C;
     float acc = 0.f;
-    for (int n = 0; n < N; ++n) {
-      const float rv = r[(size_t)n * SE + j];
-      acc += de[(size_t)n * C + c] * rv * sigmoidf_(rv);
+    float* out;
+    int64_t k = idx;
+    if (k < n_we) {
+      const int c = (int)(k / SE), j = (int)(k % SE);
+      for (int n = lane; n < N; n += 32) {
+        const float rv = r[(size_t)n * SE + j];
+        acc += de[(size_t)n * C + c] * rv * sigmoidf_(rv);
+      }
+      out = dwe + k;
+    } else if ((k -= n_we) < C) {
+      for (int n = lane; n < N; n += 32) acc += de[(size_t)n * C + k];
+      out = dbe + k;
+    } else if ((k -= C) < n_wr) {
+      const int j = (int)(k / C), c = (int)(k % C);
+      for (int n = lane; n < N; n += 32) acc += dr[(size_t)n * SE + j] * pooled[(size_t)n * C + c];
+      out = dwr + k;
+    } else if ((k -= n_wr) < SE) {
+      for (int n = lane; n < N; n += 32) acc += dr[(size_t)n * SE + k];
+      out = dbr + k;
+    } else {
+      k -= SE;
+      const int q = (int)(k / C), c = (int)(k % C);
+      for (int n = lane; n < N; n += 32) acc += nsum[((size_t)n * 2 + q) * C + c];
+      out = bnsum + k;
     }
-    dwe[idx] = acc;
-    return;
-  }
-  int k = idx - n_we;
-  if (k < C) {
-    float acc = 0.f;
-    for (int n = 0; n < N; ++n) acc += de[(size_t)n * C + k];
-    dbe[k] = acc;
-    return;
-  }
-  k -= C;
-  if (k < n_wr) {
-    const int j = k / C, c = k % C;
-    float acc = 0.f;
-    for (int n = 0; n < N; ++n) acc += dr[(size_t)n * SE + j] * pooled[(size_t)n * C + c];
-    dwr[k] = acc;
-    return;
-  }
-  k -= n_wr;
-  if (k < SE) {
-    float acc = 0.f;
-    for (int n = 0; n < N; ++n) acc += dr[(size_t)n * SE + k];
-    dbr[k] = acc;
-    return;
-  }
-  k -= SE;
-  if (k < 2 * C) {
-    const int q = k / C, c = k % C;
-    float acc = 0.f;
-    for (int n = 0; n < N; ++n) acc += nsum[((size_t)n * 2 + q) * C + c];
-    bnsum[k] = acc;
+    acc = warp_sum(acc);
+    if (lane == 0) *out = acc;
   }
 }
 
@@ -753,6 +764,17 @@ int make_geo(int64_t N, int64_t H, int64_t W, int64_t C, int stride, int ks, con
 
 template <typename T> constexpr int vec_of() { return MbVec<T>::value; }
 
+// channel chunking of the stream kernels: <= 64 vectors per CTA row
+struct Lanes {
+  int nch, cvc, py;
+};
+inline Lanes lanes_for(int C, int V) {
+  const int cvt = C / V;
+  const int nch = cvt > 64 ? (cvt + 63) / 64 : 1;
+  const int cvc = (cvt + nch - 1) / nch;
+  return Lanes{nch, cvc, kThreads / cvc};
+}
+
 // TMA ring path (dwconv.cu) geometry of this block: 3x3 taps
 inline DwShape dw_shape(const Geo& g) { return DwShape{g.N, g.H, g.W, g.Ho, g.Wo, g.C, g.ks, g.stride, g.pt, g.pl}; }
 inline bool ring_ok(const Geo& g) { return dw_ring_ok(dw_shape(g), 2) && dw_ring_ok(dw_shape(g), 4); }
@@ -854,28 +876,30 @@ int dfx_mbconv_fwd_se(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
   const int ntiles = g.N * g.tiles_per_img;
   float* pool_part = (float*)workspace + (size_t)ntiles * 2 * C;
   BnParams bn{mean, rstd, gamma, beta};
-  const int CV = g.C / V, PY = kThreads / CV, threads = CV * PY;
+  const Lanes ln = lanes_for(g.C, V);
+  const int PY = ln.py, threads = ln.cvc * ln.py;
+  const dim3 grid2((unsigned)ntiles, (unsigned)ln.nch);
   const size_t sm4 = (size_t)PY * g.C * sizeof(float);
   if (dtype == DFX_BF16) {
     auto k4 = bn_swish_pool_kernel<__nv_bfloat16, 8>;
     if (sm4 > 48 * 1024) cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
-    launch_k(k4, ntiles, threads, sm4, st, g, (const __nv_bfloat16*)z, bn, pool_part);
+    launch_k(k4, grid2, threads, sm4, st, g, (const __nv_bfloat16*)z, bn, pool_part);
   } else if (dtype == DFX_F32) {
     auto k4 = bn_swish_pool_kernel<float, 4>;
     if (sm4 > 48 * 1024) cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
-    launch_k(k4, ntiles, threads, sm4, st, g, (const float*)z, bn, pool_part);
+    launch_k(k4, grid2, threads, sm4, st, g, (const float*)z, bn, pool_part);
   } else {
     return fail(DFX_ERR_DTYPE, "dfx_mbconv_fwd_se: dtype must be f32 or bf16");
   }
   DFX_LAUNCH_CHECK("dfx_mbconv_fwd_se pool");
-  launch_k(se_fwd_kernel, g.N, kThreads, (size_t)(g.C + SE) * sizeof(float), st, g, (int)SE, pool_part, w_r, b_r, w_e, b_e,
+  launch_k(se_fwd_kernel, g.N, 1024, (size_t)(g.C + SE) * sizeof(float), st, g, (int)SE, pool_part, w_r, b_r, w_e, b_e,
                                                                            pooled, r, s);
   DFX_LAUNCH_CHECK("dfx_mbconv_fwd_se se");
   if (dtype == DFX_BF16)
-    launch_k(excite_kernel<__nv_bfloat16, 8>, ntiles, threads, 0, st, g, (const __nv_bfloat16*)z, bn, s,
+    launch_k(excite_kernel<__nv_bfloat16, 8>, grid2, threads, 0, st, g, (const __nv_bfloat16*)z, bn, s,
              (__nv_bfloat16*)y);
   else
-    launch_k(excite_kernel<float, 4>, ntiles, threads, 0, st, g, (const float*)z, bn, s, (float*)y);
+    launch_k(excite_kernel<float, 4>, grid2, threads, 0, st, g, (const float*)z, bn, s, (float*)y);
   DFX_LAUNCH_CHECK("dfx_mbconv_fwd_se excite");
   return DFX_OK;
 }
@@ -902,26 +926,29 @@ int dfx_mbconv_bwd_reduce(int dtype, int64_t N, int64_t H, int64_t W, int64_t C,
   float* dr = de + (size_t)N * C;
   float* nsum = dr + (size_t)N * SE;
   BnParams bn{mean, rstd, gamma, beta};
-  const int CV = g.C / V, PY = kThreads / CV, threads = CV * PY;
+  const Lanes ln = lanes_for(g.C, V);
+  const int PY = ln.py, threads = ln.cvc * ln.py;
+  const dim3 grid2((unsigned)ntiles, (unsigned)ln.nch);
   const size_t sm = (size_t)PY * g.C * sizeof(float);
   if (dtype == DFX_BF16) {
     auto k = bwd_reduce_kernel<__nv_bfloat16, 8>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_k(k, ntiles, threads, sm, st, g, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)z, bn, bwd_part);
+    launch_k(k, grid2, threads, sm, st, g, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)z, bn, bwd_part);
   } else if (dtype == DFX_F32) {
     auto k = bwd_reduce_kernel<float, 4>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_k(k, ntiles, threads, sm, st, g, (const float*)dy, (const float*)z, bn, bwd_part);
+    launch_k(k, grid2, threads, sm, st, g, (const float*)dy, (const float*)z, bn, bwd_part);
   } else {
     return fail(DFX_ERR_DTYPE, "dfx_mbconv_bwd_reduce: dtype must be f32 or bf16");
   }
   DFX_LAUNCH_CHECK("dfx_mbconv_bwd_reduce reduce");
-  launch_k(se_bwd_kernel, g.N, kThreads, (size_t)(6 * g.C + SE) * sizeof(float), st, g, (int)SE, bwd_part, s, r, w_r, w_e,
+  launch_k(se_bwd_kernel, g.N, 1024, (size_t)(6 * g.C + SE) * sizeof(float), st, g, (int)SE, bwd_part, s, r, w_r, w_e,
                                                                                 de, dr, dpool, nsum);
   DFX_LAUNCH_CHECK("dfx_mbconv_bwd_reduce se_bwd");
-  const int total = (int)(C * SE + C + SE * C + SE + 2 * C);
-  launch_k(se_bwd_reduce_kernel, (total + 255) / 256, 256, 0, st, g.N, g.C, (int)SE, de, dr, r, pooled, nsum, dw_e, db_e,
-                                                             dw_r, db_r, bnsum);
+  const int64_t total = (int64_t)C * SE * 2 + C + SE + 2 * C;
+  const int grid5 = (int)std::min<int64_t>((total * 32 + 255) / 256, (int64_t)num_sms() * 16);
+  launch_k(se_bwd_reduce_kernel, grid5, 256, 0, st, g.N, g.C, (int)SE, de, dr, r, pooled, nsum, dw_e, db_e,
+           dw_r, db_r, bnsum);
   DFX_LAUNCH_CHECK("dfx_mbconv_bwd_reduce se_reduce");
   return DFX_OK;
 }

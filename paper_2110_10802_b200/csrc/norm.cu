@@ -47,13 +47,17 @@ __global__ void __launch_bounds__(kThreads) bn_stats_kernel(int64_t rows, int C,
   pdl_trigger();
   pdl_wait();
   extern __shared__ float sm[];
-  const int CV = C / V, PY = blockDim.x / CV;
-  const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
-  const int c0 = cv * V;
+  // channel chunks across gridDim.y (wide C, few rows: enough CTAs and lanes)
+  const int CVt = C / V, CVc = (CVt + gridDim.y - 1) / gridDim.y, PY = blockDim.x / CVc;
+  const int lcv = threadIdx.x % CVc, py = threadIdx.x / CVc;
+  const int cv = blockIdx.y * CVc + lcv;
+  const bool on = cv < CVt;
+  const int c0 = (on ? cv : 0) * V;
+  const int cbeg = blockIdx.y * CVc * V, cend = min(cbeg + CVc * V, C);
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, rows);
   float sh[V], s1[V], s2[V];
   int cnt = 0;
-  int64_t r = r0 + py;
+  int64_t r = on ? r0 + py : r1;
   {
     Vec<T, V> v;
     if (r < r1) v.load(x + r * C + c0);
@@ -92,15 +96,17 @@ __global__ void __launch_bounds__(kThreads) bn_stats_kernel(int64_t rows, int C,
   float* s_n = sm;
   float* s_mean = sm + PY;
   float* s_m2 = s_mean + PY * C;
-  if (cv == 0) s_n[py] = (float)cnt;
+  if (lcv == 0) s_n[py] = (float)cnt;
+  if (on) {
 #pragma unroll
-  for (int i = 0; i < V; ++i) {
-    const float m = cnt ? s1[i] / (float)cnt : 0.f;
-    s_mean[py * C + c0 + i] = sh[i] + m;
-    s_m2[py * C + c0 + i] = cnt ? fmaxf(s2[i] - s1[i] * m, 0.f) : 0.f;
+    for (int i = 0; i < V; ++i) {
+      const float m = cnt ? s1[i] / (float)cnt : 0.f;
+      s_mean[py * C + c0 + i] = sh[i] + m;
+      s_m2[py * C + c0 + i] = cnt ? fmaxf(s2[i] - s1[i] * m, 0.f) : 0.f;
+    }
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+  for (int c = cbeg + threadIdx.x; c < cend; c += blockDim.x) {
     Wf acc = {0.f, 0.f, 0.f};
     for (int j = 0; j < PY; ++j) acc = wmerge(acc, Wf{s_n[j], s_mean[j * C + c], s_m2[j * C + c]});
     part[((size_t)blockIdx.x * 3 + 0) * C + c] = acc.n;
@@ -153,9 +159,13 @@ __global__ void __launch_bounds__(kThreads) bn_apply_kernel(int64_t rows, int C,
                                                            T* __restrict__ y) {
   pdl_trigger();
   pdl_wait();
-  const int CV = C / V, PY = blockDim.x / CV;
-  const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
-  const int c0 = cv * V;
+  // channel chunks across gridDim.y (wide C, few rows: enough CTAs and lanes)
+  const int CVt = C / V, CVc = (CVt + gridDim.y - 1) / gridDim.y, PY = blockDim.x / CVc;
+  const int lcv = threadIdx.x % CVc, py = threadIdx.x / CVc;
+  const int cv = blockIdx.y * CVc + lcv;
+  const bool on = cv < CVt;
+  const int c0 = (on ? cv : 0) * V;
+  const int cbeg = blockIdx.y * CVc * V, cend = min(cbeg + CVc * V, C);
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, rows);
   float P[V], Q[V];
 #pragma unroll
@@ -172,7 +182,7 @@ __global__ void __launch_bounds__(kThreads) bn_apply_kernel(int64_t rows, int C,
     }
     yv.store(out);
   };
-  int64_t r = r0 + py;
+  int64_t r = on ? r0 + py : r1;
   for (; r + 3 * PY < r1; r += 4 * PY) {
     Vec<T, V> v[4];
 #pragma unroll
@@ -198,9 +208,13 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(int64_t rows, i
   pdl_trigger();
   pdl_wait();
   extern __shared__ float sm[];
-  const int CV = C / V, PY = blockDim.x / CV;
-  const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
-  const int c0 = cv * V;
+  // channel chunks across gridDim.y (wide C, few rows: enough CTAs and lanes)
+  const int CVt = C / V, CVc = (CVt + gridDim.y - 1) / gridDim.y, PY = blockDim.x / CVc;
+  const int lcv = threadIdx.x % CVc, py = threadIdx.x / CVc;
+  const int cv = blockIdx.y * CVc + lcv;
+  const bool on = cv < CVt;
+  const int c0 = (on ? cv : 0) * V;
+  const int cbeg = blockIdx.y * CVc * V, cend = min(cbeg + CVc * V, C);
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, rows);
   float P[V], Q[V], R[V], M[V], s1[V], s2[V];  // u = x*P + Q, xhat = x*R + M
 #pragma unroll
@@ -226,7 +240,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(int64_t rows, i
       s2[i] = fmaf(du, xh, s2[i]);
     }
   };
-  int64_t r = r0 + py;
+  int64_t r = on ? r0 + py : r1;
   for (; r + 3 * PY < r1; r += 4 * PY) {
     Vec<T, V> dv[4], xv[4];
 #pragma unroll
@@ -244,10 +258,12 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(int64_t rows, i
     f(dv, xv);
   }
   for (int q = 0; q < 2; ++q) {
+    if (on) {
 #pragma unroll
-    for (int i = 0; i < V; ++i) sm[py * C + c0 + i] = q == 0 ? s1[i] : s2[i];
+      for (int i = 0; i < V; ++i) sm[py * C + c0 + i] = q == 0 ? s1[i] : s2[i];
+    }
     __syncthreads();
-    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    for (int c = cbeg + threadIdx.x; c < cend; c += blockDim.x) {
       double acc = 0.0;  // the cross-lane / cross-block merges run in f64
       for (int j = 0; j < PY; ++j) acc += sm[j * C + c];
       part[((size_t)blockIdx.x * 2 + q) * C + c] = (float)acc;
@@ -256,14 +272,28 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(int64_t rows, i
   }
 }
 
-__global__ void bn_sum_parts_kernel(int nparts, int C, const float* __restrict__ part, float* __restrict__ out) {
+// out[i] = sum_b part[b][i] (i over 2C): block = 32 outputs x 8 part lanes,
+// fixed-order f64 combine
+__global__ void __launch_bounds__(256) bn_sum_parts_kernel(int nparts, int C, const float* __restrict__ part,
+                                                           float* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= 2 * C) return;
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, pl = threadIdx.x >> 5;
+  const int idx = blockIdx.x * 32 + lane;
   double acc = 0.0;
-  for (int b = 0; b < nparts; ++b) acc += part[(size_t)b * 2 * C + idx];
-  out[idx] = (float)acc;
+  if (idx < 2 * C) {
+#pragma unroll 4
+    for (int b = pl; b < nparts; b += 8) acc += part[(size_t)b * 2 * C + idx];
+  }
+  red[pl][lane] = acc;
+  __syncthreads();
+  if (pl == 0 && idx < 2 * C) {
+    double v = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v += red[j][lane];
+    out[idx] = (float)v;
+  }
 }
 
 // dx = A*du + Cx*x + B with A = gamma*rstd and the BN-VJP means folded into
@@ -278,9 +308,13 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(int64_t rows, int C
                                                             T* __restrict__ dx) {
   pdl_trigger();
   pdl_wait();
-  const int CV = C / V, PY = blockDim.x / CV;
-  const int cv = threadIdx.x % CV, py = threadIdx.x / CV;
-  const int c0 = cv * V;
+  // channel chunks across gridDim.y (wide C, few rows: enough CTAs and lanes)
+  const int CVt = C / V, CVc = (CVt + gridDim.y - 1) / gridDim.y, PY = blockDim.x / CVc;
+  const int lcv = threadIdx.x % CVc, py = threadIdx.x / CVc;
+  const int cv = blockIdx.y * CVc + lcv;
+  const bool on = cv < CVt;
+  const int c0 = (on ? cv : 0) * V;
+  const int cbeg = blockIdx.y * CVc * V, cend = min(cbeg + CVc * V, C);
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, rows);
   float A[V], Cx[V], B[V], P[V], Q[V];
 #pragma unroll
@@ -308,7 +342,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(int64_t rows, int C
     }
     o.store(out);
   };
-  int64_t r = r0 + py;
+  int64_t r = on ? r0 + py : r1;
   for (; r + 3 * PY < r1; r += 4 * PY) {
     Vec<T, V> dv[4], xv[4];
 #pragma unroll
@@ -336,7 +370,7 @@ int vec_width(int dtype, int64_t C) {
 int check_bn(int dtype, int64_t rows, int64_t C, const char* op) {
   DFX_REQUIRE(dtype == DFX_BF16 || dtype == DFX_F32, DFX_ERR_DTYPE, std::string(op) + ": dtype must be f32 or bf16");
   DFX_REQUIRE(rows > 0 && C > 0, DFX_ERR_SHAPE, std::string(op) + ": empty tensor");
-  DFX_REQUIRE(C / vec_width(dtype, C) <= kThreads, DFX_ERR_SHAPE, std::string(op) + ": too many channels");
+  DFX_REQUIRE(C / vec_width(dtype, C) <= 64 * kThreads, DFX_ERR_SHAPE, std::string(op) + ": too many channels");
   return DFX_OK;
 }
 
@@ -362,6 +396,17 @@ void stream_blocks(int64_t rows, int PY, int64_t* rpb, int* nb) {
 }
 
 // reductions: partial sets per block (<= kMaxBlocks), >= 4 rows per thread lane
+// channel chunking: <= 64 vectors per CTA row so a wide C still gets >= 4 row lanes
+struct Lanes {
+  int nch, cvc, py;
+};
+Lanes lanes_for(int64_t C, int V) {
+  const int cvt = (int)C / V;
+  const int nch = cvt > 64 ? (cvt + 63) / 64 : 1;
+  const int cvc = (cvt + nch - 1) / nch;
+  return Lanes{nch, cvc, kThreads / cvc};
+}
+
 void blocks_for(int64_t rows, int64_t* rpb, int* nb) {
   int64_t b = std::min<int64_t>(kMaxBlocks, (rows + 63) / 64);
   if (b < 1) b = 1;
@@ -391,13 +436,14 @@ int dfx_batchnorm_stats(int dtype, int64_t rows, int64_t C, const void* x, float
   int nb;
   blocks_for(rows, &rpb, &nb);
   const int V = vec_width(dtype, C);
-  const int CV = (int)C / V, PY = kThreads / CV;
+  const Lanes ln = lanes_for(C, V);
+  const int PY = ln.py;
   const size_t sm = (size_t)(PY + 2 * PY * C) * sizeof(float);
 #define S(TT, VV, ACT)                                                                                    \
   {                                                                                                       \
     auto k = bn_stats_kernel<TT, VV>;                                                                     \
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);   \
-    launch_k(k, nb, CV * PY, sm, st, rows, (int)C, rpb, (const TT*)x, (float*)workspace);                       \
+    launch_k(k, dim3(nb, ln.nch), ln.cvc * PY, sm, st, rows, (int)C, rpb, (const TT*)x, (float*)workspace);     \
   }
   BN_DISPATCH(S, 0);
 #undef S
@@ -414,11 +460,11 @@ int dfx_batchnorm_act_apply(int dtype, int64_t rows, int64_t C, const void* x, c
   DFX_REQUIRE(act == 0 || act == 1, DFX_ERR_UNSUPPORTED, "dfx_batchnorm_act_apply: act must be 0 or 1");
   cudaStream_t st = as_stream(stream);
   const int V = vec_width(dtype, C);
-  const int CV = (int)C / V, PY = kThreads / CV;
+  const Lanes ln = lanes_for(C, V);
   int64_t rpb;
   int nb;
-  stream_blocks(rows, PY, &rpb, &nb);
-#define A(TT, VV, ACT) { launch_k(bn_apply_kernel<TT, VV, ACT>, nb, CV * PY, 0, st, rows, (int)C, rpb, (const TT*)x, mean, rstd, gamma, beta, (TT*)y); }
+  stream_blocks(rows, ln.py * ln.nch, &rpb, &nb);
+#define A(TT, VV, ACT) { launch_k(bn_apply_kernel<TT, VV, ACT>, dim3(nb, ln.nch), ln.cvc * ln.py, 0, st, rows, (int)C, rpb, (const TT*)x, mean, rstd, gamma, beta, (TT*)y); }
   BN_DISPATCH(A, act);
 #undef A
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_apply");
@@ -438,19 +484,20 @@ int dfx_batchnorm_act_bwd_reduce(int dtype, int64_t rows, int64_t C, const void*
   int nb;
   blocks_for(rows, &rpb, &nb);
   const int V = vec_width(dtype, C);
-  const int CV = (int)C / V, PY = kThreads / CV;
+  const Lanes ln = lanes_for(C, V);
+  const int PY = ln.py;
   const size_t sm = (size_t)PY * C * sizeof(float);
 #define R(TT, VV, ACT)                                                                                      \
   {                                                                                                         \
     auto k = bn_bwd_reduce_kernel<TT, VV, ACT>;                                                             \
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
-    launch_k(k, nb, CV * PY, sm, st, rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta,     \
+    launch_k(k, dim3(nb, ln.nch), ln.cvc * PY, sm, st, rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, \
                                (float*)workspace);                                                          \
   }
   BN_DISPATCH(R, act);
 #undef R
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_reduce");
-  launch_k(bn_sum_parts_kernel, (unsigned)((2 * C + 255) / 256), 256, 0, st, nb, (int)C, (const float*)workspace, bnsum);
+  launch_k(bn_sum_parts_kernel, (unsigned)((2 * C + 31) / 32), 256, 0, st, nb, (int)C, (const float*)workspace, bnsum);
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_reduce sum");
   return DFX_OK;
 }
@@ -464,13 +511,13 @@ int dfx_batchnorm_act_bwd_dx(int dtype, int64_t rows, int64_t C, const void* dy,
   DFX_REQUIRE(count > 0, DFX_ERR_SHAPE, "dfx_batchnorm_act_bwd_dx: count must be positive");
   cudaStream_t st = as_stream(stream);
   const int V = vec_width(dtype, C);
-  const int CV = (int)C / V, PY = kThreads / CV;
+  const Lanes ln = lanes_for(C, V);
   int64_t rpb;
   int nb;
-  stream_blocks(rows, PY, &rpb, &nb);
+  stream_blocks(rows, ln.py * ln.nch, &rpb, &nb);
   const float ic = (float)(1.0 / count);
 #define D(TT, VV, ACT) \
-  { launch_k(bn_bwd_dx_kernel<TT, VV, ACT>, nb, CV * PY, 0, st, rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, bnsum, ic, (TT*)dx); }
+  { launch_k(bn_bwd_dx_kernel<TT, VV, ACT>, dim3(nb, ln.nch), ln.cvc * ln.py, 0, st, rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, bnsum, ic, (TT*)dx); }
   BN_DISPATCH(D, act);
 #undef D
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_dx");
