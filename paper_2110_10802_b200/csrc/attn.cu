@@ -135,8 +135,9 @@ __device__ __forceinline__ uint32_t p_chunk(uint32_t base, int c) {
 __global__ void __launch_bounds__(kAttnThreads, 1)
 attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams p) {
   pdl_trigger();
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // dynamic smem opens the CTA's window (no static smem in this kernel): it is
+  // 1024-B aligned, and indexing it directly keeps every access LDS/STS
+  extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FwdSmem::BAR);
   uint64_t *bar_qk = bar, *bar_v = bar + 1, *bar_s = bar + 2, *bar_p = bar + 3, *bar_o = bar + 4;
@@ -423,8 +424,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
                    const AttnBwdParams p) {
   pdl_trigger();
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // dynamic smem opens the CTA's window (no static smem in this kernel): it is
+  // 1024-B aligned, and indexing it directly keeps every access LDS/STS
+  extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + DqSmem::BAR);
   uint64_t *bar_q = bar, *bar_s = bar + 1, *bar_tfree = bar + 2, *bar_ds = bar + 3, *bar_dsfree = bar + 4;
@@ -584,8 +586,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
                      const AttnBwdParams p) {
   pdl_trigger();
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // dynamic smem opens the CTA's window (no static smem in this kernel): it is
+  // 1024-B aligned, and indexing it directly keeps every access LDS/STS
+  extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + DkvSmem::BAR);
   uint64_t *bar_a = bar, *bar_s = bar + 1, *bar_tfree = bar + 2, *bar_pds = bar + 3, *bar_pdsfree = bar + 4;

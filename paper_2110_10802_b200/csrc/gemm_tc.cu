@@ -46,11 +46,12 @@ template <int BN, int CG = 1> struct TcCfg {
   // epilogue staging (TMA store source) per epilogue warp, and the smem ring
   // depth: both sized so the CTA uses <= 227 KB
   static constexpr int EPI_WARP_BYTES = 4096;  // output unit + aux unit, 32 rows x 64 B each
-  static constexpr int STAGES = CG == 2 ? (BN == 256 ? 5 : 6) : (BN == 256 ? 3 : (BN == 128 ? 5 : 6));
+  static constexpr int STAGES = CG == 2 ? (BN >= 192 ? 5 : 6) : (BN == 256 ? 3 : (BN == 192 ? 4 : (BN == 128 ? 5 : 6)));
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN / CG * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  // two accumulator buffers, rounded up to the power-of-two allocation unit
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : (BN == 192 ? 512 : 2 * BN);
   static constexpr int EPI_BYTES = kEpiWarps * EPI_WARP_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -332,7 +333,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int part = ew >> 2;         // which quarter of the tile's columns
     constexpr int WCOLS = BN / 4;     // columns per warp
     constexpr int ESZ = (int)sizeof(TO);
-    constexpr int UB = WCOLS * ESZ >= 64 ? 64 : WCOLS * ESZ;  // bytes per row per unit
+    // bytes per row per unit: 64 when the warp's columns tile by it (BN = 192 bf16: 32)
+    constexpr int UB = (WCOLS * ESZ) % 64 == 0 ? 64 : ((WCOLS * ESZ) % 32 == 0 ? 32 : 16);
     constexpr int L = UB / 16;
     constexpr int UCOLS = UB / ESZ;   // columns per unit (bf16 32, f32 16)
     static_assert(WCOLS % UCOLS == 0, "warp columns must hold whole units");
@@ -482,6 +484,23 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(int splits, int64_t 
   }
 }
 
+// few splits (the 768-wide BERT weight gradients): one element per thread
+template <typename TO>
+__global__ void __launch_bounds__(256) splitk_reduce_few_kernel(int splits, int64_t Z, int64_t m, int64_t n,
+                                                                const float* __restrict__ part, TO* __restrict__ d,
+                                                                int64_t d_stride_m, int64_t d_stride_b1,
+                                                                int64_t d_stride_b2, int64_t batch2) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t total = Z * m * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) acc += part[s * total + i];
+    const int64_t col = i % n, row = (i / n) % m, z = i / (n * m);
+    d[(z / batch2) * d_stride_b1 + (z % batch2) * d_stride_b2 + row * d_stride_m + col] = from_f<TO>(acc);
+  }
+}
+
 // ----------------------------------------------------------------- host side
 }  // namespace
 
@@ -538,10 +557,11 @@ unsigned long long* g_trace = nullptr;
 
 Plan plan(const dfx_gemm_args& p) {
   const int sms = num_sms();
-  static const char* force = getenv("DFX_GEMM_FORCE");  // "cg,bn" (tuning only)
+  const char* force = getenv("DFX_GEMM_FORCE");  // "cg,bn" (tuning / tests only)
   if (force) {
     int fcg = 1, fbn = 256;
-    if (sscanf(force, "%d,%d", &fcg, &fbn) == 2 && (fcg == 1 || fcg == 2) && (fbn == 64 || fbn == 128 || fbn == 256) &&
+    if (sscanf(force, "%d,%d", &fcg, &fbn) == 2 && (fcg == 1 || fcg == 2) && (fbn == 64 || fbn == 128 || fbn == 192 || fbn == 256) &&
+        !(fcg == 2 && fbn == 192 && p.b_stride_k != 1) &&  // pair-192 loads B in 96-row K-major boxes only
         !(fcg == 2 && (fbn == 64 || p.m < 256))) {
       const int64_t z = p.batch1 * p.batch2;
       const int64_t kb = (p.k + BK - 1) / BK;  // K tail: TMA zero-fills past k
@@ -552,11 +572,15 @@ Plan plan(const dfx_gemm_args& p) {
   const int64_t z = p.batch1 * p.batch2;
   const int64_t kb = (p.k + BK - 1) / BK;  // K tail: TMA zero-fills past k
   struct Cand { int bn, cg; double thr; };
-  const Cand cands[] = {{256, 2, 1.5}, {128, 2, 1.0}, {256, 1, 1.0}, {128, 1, 0.8}, {64, 1, 0.6}};
+  // 192-wide single-CTA tiles fill the SMs on the narrow (768-wide) outputs:
+  // 32 x 4 = 128 tiles in one wave instead of 16 x 3 pairs on 96 SMs
+  // (measured: out 11.2 -> 9.6 us, ffn2 22.4 -> 20.0 us; tools/gemm_force_sweep.sh)
+  const Cand cands[] = {{256, 2, 1.5}, {128, 2, 1.0}, {256, 1, 1.0}, {192, 1, 1.2}, {128, 1, 0.8}, {64, 1, 0.6}};
   Plan best{64, 1, 1, (int)kb, 0};
   double best_cost = 1e30;
   for (const Cand& c : cands) {
     if (c.cg == 2 && (p.m < 256 || sms < 2)) continue;
+    if (c.bn == 192 && p.n > 1024) continue;
     const int64_t units = z * ((p.m + BM * c.cg - 1) / (BM * c.cg)) * ((p.n + c.bn - 1) / c.bn);
     const int64_t slots = sms / c.cg;
     const double waves = (double)((units + slots - 1) / slots);
@@ -621,9 +645,11 @@ int launch_tc_any(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& mb, 
                   cudaStream_t st) {
   if (cg == 2) {
     if (bn == 256) return launch_tc<256, TO, 2>(ma, mb, tp, st);
+    if (bn == 192) return launch_tc<192, TO, 2>(ma, mb, tp, st);
     return launch_tc<128, TO, 2>(ma, mb, tp, st);
   }
   if (bn == 256) return launch_tc<256, TO, 1>(ma, mb, tp, st);
+  if (bn == 192) return launch_tc<192, TO, 1>(ma, mb, tp, st);
   if (bn == 128) return launch_tc<128, TO, 1>(ma, mb, tp, st);
   return launch_tc<64, TO, 1>(ma, mb, tp, st);
 }
@@ -670,6 +696,7 @@ int gemm_tc(const dfx_gemm_args& p, cudaStream_t st) {
   const Plan pl = plan(p);
   const int bn = pl.bn;
   const bool a_mn = p.a_stride_k != 1, b_mn = p.b_stride_k != 1;
+  DFX_REQUIRE(!(pl.cg == 2 && bn == 192 && b_mn), DFX_ERR_UNSUPPORTED, "dfx_gemm: 2-CTA 192 tile needs K-major B");
   CUtensorMap ma, mb;
   int rc;
   if (a_mn)
@@ -712,13 +739,23 @@ int gemm_tc(const dfx_gemm_args& p, cudaStream_t st) {
   rc = f32 ? launch_tc_any<float>(bn, pl.cg, ma, mb, tp, st) : launch_tc_any<__nv_bfloat16>(bn, pl.cg, ma, mb, tp, st);
   if (rc || pl.splits <= 1) return rc;
   const int64_t total = Z * p.m * p.n;
-  const int grid = (int)std::min<int64_t>((total + 31) / 32, (int64_t)num_sms() * 8);
-  if (p.out_dtype == DFX_F32)
-    launch_k(splitk_reduce_kernel<float>, grid, 256, 0, st, pl.splits, Z, p.m, p.n, part, (float*)p.d, p.d_stride_m,
-                                                      p.d_stride_b1, p.d_stride_b2, p.batch2);
-  else
-    launch_k(splitk_reduce_kernel<__nv_bfloat16>, grid, 256, 0, st, pl.splits, Z, p.m, p.n, part, (__nv_bfloat16*)p.d,
-                                                              p.d_stride_m, p.d_stride_b1, p.d_stride_b2, p.batch2);
+  if (pl.splits <= 8) {
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+    if (p.out_dtype == DFX_F32)
+      launch_k(splitk_reduce_few_kernel<float>, grid, 256, 0, st, pl.splits, Z, p.m, p.n, part, (float*)p.d,
+               p.d_stride_m, p.d_stride_b1, p.d_stride_b2, p.batch2);
+    else
+      launch_k(splitk_reduce_few_kernel<__nv_bfloat16>, grid, 256, 0, st, pl.splits, Z, p.m, p.n, part,
+               (__nv_bfloat16*)p.d, p.d_stride_m, p.d_stride_b1, p.d_stride_b2, p.batch2);
+  } else {
+    const int grid = (int)std::min<int64_t>((total + 31) / 32, (int64_t)num_sms() * 8);
+    if (p.out_dtype == DFX_F32)
+      launch_k(splitk_reduce_kernel<float>, grid, 256, 0, st, pl.splits, Z, p.m, p.n, part, (float*)p.d,
+               p.d_stride_m, p.d_stride_b1, p.d_stride_b2, p.batch2);
+    else
+      launch_k(splitk_reduce_kernel<__nv_bfloat16>, grid, 256, 0, st, pl.splits, Z, p.m, p.n, part,
+               (__nv_bfloat16*)p.d, p.d_stride_m, p.d_stride_b1, p.d_stride_b2, p.batch2);
+  }
   DFX_LAUNCH_CHECK("dfx_gemm split-K reduce");
   return DFX_OK;
 }

@@ -189,3 +189,26 @@ def test_tc_ragged_m_k(m, n, k, la, lb):
     kk.gemm(a, b, d)
     torch.cuda.synchronize()
     _check(d, _ref(a, b), 1e-2)
+
+
+@pytest.mark.parametrize("force", ["2,192", "1,192"])
+@pytest.mark.parametrize("la,lb,epi", [("k", "k", "none"), ("k", "n", "none"), ("m", "k", "bias"), ("k", "k", "gelu")])
+def test_tc_192_tiles(force, la, lb, epi, monkeypatch):
+    """The 192-column tiles (768-wide BERT outputs) on every epilogue path with
+    K- and MN-major operands, forced through DFX_GEMM_FORCE (read per call)."""
+    from paper_2110_10802_b200 import _lib
+
+    monkeypatch.setenv("DFX_GEMM_FORCE", force)
+    kk = K()
+    a, b = _operands(512, 768, 320, la, lb, torch.bfloat16, 11)
+    d = torch.empty(512, 768, dtype=torch.bfloat16, device="cuda")
+    bias = _rand((768,), torch.float32, 3, 0.1)
+    e = {"none": _lib.EPI_NONE, "bias": _lib.EPI_BIAS, "gelu": _lib.EPI_BIAS_GELU}[epi]
+    kk.gemm(a, b, d, e, bias=bias if e != _lib.EPI_NONE else None)
+    torch.cuda.synchronize()
+    want = _ref(a, b)
+    if e != _lib.EPI_NONE:
+        want = want + bias.double().cpu().numpy()
+    if e == _lib.EPI_BIAS_GELU:
+        want = 0.5 * want * (1 + np.tanh(0.7978845608028654 * (want + 0.044715 * want ** 3)))
+    _check(d, want, 2e-2)

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Time each BERT C2 GEMM shape under every forced tile config (DFX_GEMM_FORCE=cg,bn).
 cd "${GRAFT_REPO_ROOT:-.}"
-for f in "" 2,256 2,128 1,256 1,128 1,64; do
+for f in "" 2,256 2,192 2,128 1,256 1,192 1,128; do
   echo "== force '$f'"
   DFX_GEMM_FORCE=$f python - <<'PY'
 import os, sys
