@@ -378,7 +378,10 @@ def run_ours(args):
     keep_attn = (torch.rand(B, NH, S, S, generator=gen) >= P_DROP).to(torch.uint8)
     keep1 = (torch.rand(T, H, generator=gen) >= P_DROP).to(torch.uint8)
     keep2 = (torch.rand(T, H, generator=gen) >= P_DROP).to(torch.uint8)
-    host = {k: v.pin_memory() for k, v in dict(x=x, dout=dout, add_mask=am, keep_attn=keep_attn,
+    # the attention dropout mask is supplied bit-packed (the fused kernels' native
+    # form: 3.1 MB instead of 25 MB of u8 flags per step over PCIe and HBM)
+    keep_attn_bits = K.pack_keep_bits(keep_attn)
+    host = {k: v.pin_memory() for k, v in dict(x=x, dout=dout, add_mask=am, keep_attn=keep_attn_bits,
                                                  keep1=keep1, keep2=keep2).items()}
     dev = layer.device_inputs(B, S)
     for k, v in host.items():

@@ -117,7 +117,10 @@ int dfx_softmax_bwd(int dtype, int64_t rows, int64_t cols, const void* dpd, cons
  *   lse[b,h,s]          = log2 sum_t exp2(log2e*(S/divisor + mask))  (f32)
  *   keep_bits_row[b,h,s,t/32] bit t%32 = keep[b,h,s,t]; keep_bits_col[b,h,t,s/32]
  *   bit s%32 = keep[b,h,s,t] — the packed dropout masks the backward reads
- *   (each [B,NH,S,S/32] u32; pass both or neither; keep may be NULL = no dropout). */
+ *   (each [B,NH,S,S/32] u32; pass both or neither; keep may be NULL = no dropout).
+ *   keep == NULL with keep_bits_row != NULL: the keep flags are supplied
+ *   PACKED in keep_bits_row (an input, 1/8 of the u8 bytes); only
+ *   keep_bits_col is written. */
 int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t head_dim, const void* qkv,
                  int64_t ld_qkv, const float* add_mask, const uint8_t* keep, float keep_scale,
                  float inv_divisor, void* ctx, int64_t ld_ctx, float* lse, uint32_t* keep_bits_row,

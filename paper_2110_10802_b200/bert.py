@@ -207,7 +207,9 @@ class BertEncoderLayer:
     # ------------------------------------------------------------ forward
     def forward(self, x, add_mask, keep_attn, keep1, keep2):
         """x [T, H] (T = B*S); add_mask f32 [B, S]; keep_* u8 dropout keep flags
-        ([B, NH, S, S], [T, H], [T, H]).  Returns the layer output [T, H]."""
+        ([B, NH, S, S], [T, H], [T, H]); keep_attn may instead be the packed
+        int32 [B, NH, S, S/32] form (kernels.pack_keep_bits, fused path only).
+        Returns the layer output [T, H]."""
         c = self.cfg
         B, S = add_mask.shape
         T = B * S
@@ -217,13 +219,18 @@ class BertEncoderLayer:
         b = self.buffers(B, S)
         P = self.master
         self._saved = (x, add_mask, keep_attn, keep1, keep2, B, S)
+        packed = keep_attn.dtype == torch.int32
+        if packed and not self._fused(S):
+            raise ShapeError("packed keep_attn needs the fused (bf16) attention path")
+        # the backward reads the row-major packed flags: the input itself when packed
+        self._kb_row = keep_attn if packed else b.get("kbits_row")
         L = K.label
         with L("fwd.qkv_gemm+bias"):
             K.gemm(x, self.weight("wqkv"), b["qkv"], EPI_BIAS, bias=P["bqkv"])
         if self._fused(S):
             with L("fwd.attention"):
-                K.attn_fwd(b["qkv"], B, S, c.heads, add_mask, keep_attn, ks, 1.0 / (c.head_dim ** 0.5), b["ctx"],
-                           b["lse"], b["kbits_row"], b["kbits_col"])
+                K.attn_fwd(b["qkv"], B, S, c.heads, add_mask, None if packed else keep_attn, ks,
+                           1.0 / (c.head_dim ** 0.5), b["ctx"], b["lse"], self._kb_row, b["kbits_col"])
         else:
             q, k, v = (self._heads(b["qkv"], B, S, i) for i in range(3))
             with L("fwd.scores_gemm"):
@@ -279,7 +286,7 @@ class BertEncoderLayer:
         # attention
         if self._fused(S):
             with L("bwd.attention"):
-                K.attn_bwd(b["qkv"], b["ctx"], b["dctx"], B, S, c.heads, add_mask, b["lse"], b["kbits_row"],
+                K.attn_bwd(b["qkv"], b["ctx"], b["dctx"], B, S, c.heads, add_mask, b["lse"], self._kb_row,
                            b["kbits_col"], ks, 1.0 / (c.head_dim ** 0.5), b["dqkv"])
         else:
             self._attn_bwd_unfused(b, B, S, keep_attn, ks)
@@ -325,7 +332,8 @@ class BertEncoderLayer:
         c = self.cfg
         T, H = B * S, c.hidden
         esz = torch.tensor([], dtype=c.dtype).element_size()
-        h2d = 2 * T * H * esz + B * S * 4 + B * c.heads * S * S + 2 * T * H
+        attn_keep = B * c.heads * S * S // 8 if self._fused(S) else B * c.heads * S * S
+        h2d = 2 * T * H * esz + B * S * 4 + attn_keep + 2 * T * H
         return h2d, T * H * esz
 
     def train_step_host(self, host: dict, lr=None, dx_host=None, graph=True):
@@ -364,7 +372,9 @@ class BertEncoderLayer:
                 x=torch.empty(T, H, dtype=c.dtype, device=dev),
                 dout=torch.empty(T, H, dtype=c.dtype, device=dev),
                 add_mask=torch.empty(B, S, dtype=torch.float32, device=dev),
-                keep_attn=torch.empty(B, NH, S, S, dtype=u8, device=dev),
+                # fused path: the attention keep flags travel packed (1 bit each)
+                keep_attn=(torch.empty(B, NH, S, S // 32, dtype=torch.int32, device=dev) if self._fused(S)
+                           else torch.empty(B, NH, S, S, dtype=u8, device=dev)),
                 keep1=torch.empty(T, H, dtype=u8, device=dev),
                 keep2=torch.empty(T, H, dtype=u8, device=dev))
         return self._bufs[key]

@@ -111,8 +111,9 @@ struct AttnFwdParams {
   float sc2;              // inv_divisor * log2(e)
   __nv_bfloat16* ctx;
   float* lse;             // [B, NH, S], log2 domain
-  uint32_t* kb_row;       // [B, NH, S, S/32] or null
+  uint32_t* kb_row;       // [B, NH, S, S/32] or null (written, or READ when kb_in)
   uint32_t* kb_col;       // [B, NH, S(key), S/32] or null
+  int kb_in;              // keep flags arrive packed (kb_row is the input, keep is null)
 };
 
 // shared-memory plan of the forward kernel (bytes from a 1024-aligned base)
@@ -140,8 +141,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FwdSmem::BAR);
-  uint64_t *bar_qk = bar, *bar_v = bar + 1, *bar_s = bar + 2, *bar_p = bar + 3, *bar_o = bar + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
+  // bar_p[j]: P of key chunk j (128 keys) complete in smem -> PV MMA of chunk j
+  uint64_t *bar_qk = bar, *bar_v = bar + 1, *bar_s = bar + 2, *bar_o = bar + 4, *bar_p = bar + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
   float* mask2 = reinterpret_cast<float*>(smem + FwdSmem::MASK);
   float* red_max = reinterpret_cast<float*>(smem + FwdSmem::RED);
   float* red_sum = red_max + 4 * QT;
@@ -158,7 +160,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
     mbar_init(bar_qk, 1);
     mbar_init(bar_v, 1);
     mbar_init(bar_s, 1);
-    mbar_init(bar_p, kSoftWarps);
+    for (int j = 0; j < 4; ++j) mbar_init(&bar_p[j], kSoftWarps);
     mbar_init(bar_o, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
@@ -204,25 +206,32 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
           tc_mma_cg<1>(tmem + nb * 128, qdesc + 2 * kk, kdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
       }
       tc_commit_cg<1>(bar_s);
-      mbar_wait(bar_p, 0);
-      ATRACE(5);
       mbar_wait(bar_v, 0);
-      tc_fence_after();
+      // O = P·V chunk by chunk as the softmax warps finish each 128-key chunk:
+      // the PV MMAs of chunk j overlap the exp pass of chunk j+1.  O lives in
+      // TMEM columns [0, 64) — S chunk 0, consumed before bar_p[0] fires.
       const uint32_t idesc_o = make_idesc(DH, QT, 0, 1);
       const uint64_t vdesc = make_sdesc(sbase + FwdSmem::V, 8 * KB, 1024);
-      for (int kc = 0; kc < S / 16; ++kc) {
-        const uint64_t pdesc = make_sdesc(p_chunk(sbase, kc >> 2), 16, 1024);
-        tc_mma_cg<1>(tmem, pdesc + 2 * (kc & 3), vdesc + (uint64_t)(kc * (2048 >> 4)), idesc_o, kc > 0 ? 1u : 0u);
+      for (int j = 0; j < S / 128; ++j) {
+        mbar_wait(&bar_p[j], 0);
+        tc_fence_after();
+#pragma unroll
+        for (int kc = j * 8; kc < j * 8 + 8; ++kc) {
+          const uint64_t pdesc = make_sdesc(p_chunk(sbase, kc >> 2), 16, 1024);
+          tc_mma_cg<1>(tmem, pdesc + 2 * (kc & 3), vdesc + (uint64_t)(kc * (2048 >> 4)), idesc_o, kc > 0 ? 1u : 0u);
+        }
       }
+      ATRACE(5);
       tc_commit_cg<1>(bar_o);
     }
   } else {
     // ------------------------------------------------------------ softmax warps
     const int sw = warp - 2;
     const int q = warp & 3;          // TMEM lane quadrant
-    const int part = sw >> 2;        // column quarter
-    const int cpp = S / 4;           // columns per part (<= 128)
-    const int c0 = part * cpp;
+    const int part = sw >> 2;        // 32-column slice of every 128-key chunk
+    // chunk j of this thread's row: columns j*128 + part*32 .. +31 (all 16
+    // warps finish chunk j together, so its PV MMA can start early)
+    auto colof = [part](int j) { return j * 128 + part * 32; };
     const int rl = q * 32 + lane;    // row within the strip
     const int grow = q0 + rl;        // query index
     const int st = threadIdx.x - 64; // 0..511
@@ -230,9 +239,18 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
       mask2[i] = p.add_mask ? p.add_mask[(size_t)b * S + i] * kLog2e : 0.f;
     // dropout keep flags of this thread's row segment, 32 bytes per chunk
     const size_t rowoff = ((size_t)bh * S + grow) * S;
-    const uint4* kp = reinterpret_cast<const uint4*>(p.keep + rowoff + c0);
+    const uint4* kp = reinterpret_cast<const uint4*>(p.keep + rowoff);  // 16 columns per uint4
     const uint4 ones = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
-    uint4 kv0 = p.keep ? __ldg(kp) : ones, kv1 = p.keep ? __ldg(kp + 1) : ones;
+    uint4 kv0 = p.keep ? __ldg(kp + colof(0) / 16) : ones, kv1 = p.keep ? __ldg(kp + colof(0) / 16 + 1) : ones;
+    // packed keep flags (one word per 32-column chunk slice): all of this
+    // thread's words are fetched up front, off the exp pass's critical path
+    uint32_t kbw[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    if (p.kb_in) {
+      const uint32_t* kr = p.kb_row + ((size_t)bh * S + grow) * (S / 32);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < S / 128) kbw[j] = __ldg(kr + colof(j) / 32);
+    }
     named_bar(1, kSoftWarps * 32);
     const float4* mask4 = reinterpret_cast<const float4*>(mask2);
     if (sw == 0 && lane == 0) ATRACE(2);
@@ -243,17 +261,17 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
     // pass 1: row max of t = S*c*log2e + mask*log2e (TMEM load of chunk j+1
     // in flight while chunk j is reduced)
     float mx = -INFINITY;
-    const int nj = cpp / 32;
+    const int nj = S / 128;
     {
       float v[2][32];
-      tmem_ld32(trow + c0, v[0]);
+      tmem_ld32(trow + colof(0), v[0]);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (j >= nj) break;
-        if (j + 1 < nj) tmem_ld32_nowait(trow + c0 + (j + 1) * 32, v[(j + 1) & 1]);
+        if (j + 1 < nj) tmem_ld32_nowait(trow + colof(j + 1), v[(j + 1) & 1]);
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
-          const float4 m = mask4[(c0 + j * 32 + i) >> 2];
+          const float4 m = mask4[(colof(j) + i) >> 2];
           const float* w = v[j & 1];
           mx = fmax3(mx, fmaf(w[i], p.sc2, m.x), fmaf(w[i + 1], p.sc2, m.y));
           mx = fmax3(mx, fmaf(w[i + 2], p.sc2, m.z), fmaf(w[i + 3], p.sc2, m.w));
@@ -272,46 +290,60 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
 #pragma unroll 1
     for (int j = 0; j < nj; ++j) {
       float w[32];
-      tmem_ld32_nowait(trow + c0 + j * 32, w);
+      tmem_ld32_nowait(trow + colof(j), w);
       const uint32_t kw[8] = {kv0.x, kv0.y, kv0.z, kv0.w, kv1.x, kv1.y, kv1.z, kv1.w};
       if (j + 1 < nj && p.keep) {  // next chunk's keep flags
-        kv0 = __ldg(kp + 2 * (j + 1));
-        kv1 = __ldg(kp + 2 * (j + 1) + 1);
+        kv0 = __ldg(kp + colof(j + 1) / 16);
+        kv1 = __ldg(kp + colof(j + 1) / 16 + 1);
       }
       tmem_wait_ld();
       uint32_t pk[16];
       uint32_t bits = 0;
+      const uint32_t kbj = j == 0 ? kbw[0] : (j == 1 ? kbw[1] : (j == 2 ? kbw[2] : kbw[3]));
+      // packed fp32 (FFMA2 / FADD2): t = s*c*log2e + (mask*log2e - max), two
+      // columns per instruction; the exps stay on the MUFU pipe
+      const float2 sc2x2 = make_float2(p.sc2, p.sc2), nmx2 = make_float2(-mx, -mx);
+      float2 sacc = make_float2(0.f, 0.f);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {  // 4 columns per keep word
-        const float4 m = mask4[(c0 + j * 32 + 4 * u) >> 2];
-        const float e0 = ex2(fmaf(w[4 * u], p.sc2, m.x) - mx);
-        const float e1 = ex2(fmaf(w[4 * u + 1], p.sc2, m.y) - mx);
-        const float e2 = ex2(fmaf(w[4 * u + 2], p.sc2, m.z) - mx);
-        const float e3 = ex2(fmaf(w[4 * u + 3], p.sc2, m.w) - mx);
-        sum += (e0 + e1) + (e2 + e3);
-        const uint32_t ff = kw[u] * 0xFFu;  // bytes 0x00 / 0xFF
-        pk[2 * u] = pack_bf16x2(e0, e1) & __byte_perm(ff, 0, 0x1100);
-        pk[2 * u + 1] = pack_bf16x2(e2, e3) & __byte_perm(ff, 0, 0x3322);
-        bits |= keep_nibble(kw[u]) << (4 * u);
+        const float4 m = mask4[(colof(j) + 4 * u) >> 2];
+        const float2 ta = __ffma2_rn(make_float2(w[4 * u], w[4 * u + 1]), sc2x2, __fadd2_rn(make_float2(m.x, m.y), nmx2));
+        const float2 tb = __ffma2_rn(make_float2(w[4 * u + 2], w[4 * u + 3]), sc2x2, __fadd2_rn(make_float2(m.z, m.w), nmx2));
+        const float e0 = ex2(ta.x), e1 = ex2(ta.y), e2 = ex2(tb.x), e3 = ex2(tb.y);
+        sacc = __fadd2_rn(sacc, __fadd2_rn(make_float2(e0, e1), make_float2(e2, e3)));
+        if (p.kb_in) {  // bit pair -> 2 x 16-bit lane masks (PRMT from the {0, ~0} byte pool)
+          const uint32_t nib = kbj >> (4 * u);
+          const uint32_t s01 = ((nib & 1u) * 0x0044u) | (((nib >> 1) & 1u) * 0x4400u);
+          const uint32_t s23 = (((nib >> 2) & 1u) * 0x0044u) | (((nib >> 3) & 1u) * 0x4400u);
+          pk[2 * u] = pack_bf16x2(e0, e1) & __byte_perm(0u, 0xFFFFFFFFu, s01);
+          pk[2 * u + 1] = pack_bf16x2(e2, e3) & __byte_perm(0u, 0xFFFFFFFFu, s23);
+        } else {
+          const uint32_t ff = kw[u] * 0xFFu;  // bytes 0x00 / 0xFF
+          pk[2 * u] = pack_bf16x2(e0, e1) & __byte_perm(ff, 0, 0x1100);
+          pk[2 * u + 1] = pack_bf16x2(e2, e3) & __byte_perm(ff, 0, 0x3322);
+          bits |= keep_nibble(kw[u]) << (4 * u);
+        }
       }
-      const int col = c0 + j * 32;
+      if (p.kb_in) bits = kbj;
+      sum += sacc.x + sacc.y;
+      const int col = colof(j);
       const uint32_t tile = p_chunk(sbase, col >> 6);
       const int ch0 = (col & 63) >> 3;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         st_sw128(tile, rl, ch0 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
       if (p.kb_row) {
-        p.kb_row[((size_t)bh * S + grow) * words + (col >> 5)] = bits;
+        if (!p.kb_in) p.kb_row[((size_t)bh * S + grow) * words + (col >> 5)] = bits;
         // transposed: bit i of word [key][q/32] = keep of query (32-row group base + i)
         const uint32_t colword = warp_transpose32(bits, lane);
         p.kb_col[((size_t)bh * S + col + lane) * words + (grow >> 5)] = colword;
       }
+      // chunk j of P̃d complete in smem -> the MMA warp may issue its PV MMAs
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_p[j]);
     }
-    // P̃d complete in smem -> the MMA warp may issue O = P̃d·V (and reuse TMEM)
-    fence_async_smem();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar_p);
     red_sum[part * QT + rl] = sum;
     named_bar(1, kSoftWarps * 32);
     const float tot = red_sum[rl] + red_sum[QT + rl] + red_sum[2 * QT + rl] + red_sum[3 * QT + rl];
@@ -789,7 +821,9 @@ extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   DFX_REQUIRE(!keep || aligned16(keep), DFX_ERR_ALIGN, "dfx_attn_fwd: keep must be 16-byte aligned");
   DFX_REQUIRE((keep_bits_row == nullptr) == (keep_bits_col == nullptr), DFX_ERR_SHAPE,
               "dfx_attn_fwd: pass both packed keep-bit outputs or neither");
-  DFX_REQUIRE(!keep_bits_row || keep, DFX_ERR_SHAPE, "dfx_attn_fwd: keep bits need keep flags");
+  // keep == NULL with keep_bits_row set: the keep flags arrive PACKED in
+  // keep_bits_row (input; only keep_bits_col is written)
+  const bool kb_in = !keep && keep_bits_row;
   CUtensorMap map;
   const int64_t T = batch * seq;
   rc = make_map(&map, qkv, 2, (uint64_t)ld_qkv, (uint64_t)T, ld_qkv, 1, 0, 1, 0, 64, 64, true);
@@ -800,7 +834,8 @@ extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   p.ld_ctx = ld_ctx;
   p.add_mask = add_mask;
   p.keep = keep;
-  p.ks = keep ? keep_scale : 1.f;
+  p.ks = (keep || kb_in) ? keep_scale : 1.f;
+  p.kb_in = kb_in ? 1 : 0;
   p.sc2 = inv_divisor * kLog2e;
   p.ctx = reinterpret_cast<__nv_bfloat16*>(ctx);
   p.lse = lse;

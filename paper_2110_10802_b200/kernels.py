@@ -261,10 +261,22 @@ def softmax_bwd(dpd, p, keep, keep_scale, inv_divisor, out=None):
 # fused attention (QKᵀ -> scale + mask -> softmax -> dropout -> PV)
 
 
+def pack_keep_bits(keep):
+    """u8/bool keep flags [..., S] -> int32 [..., S/32], bit i of word w = keep[32w + i]
+    (the packed layout dfx_attn_fwd / dfx_attn_bwd read)."""
+    *lead, S = keep.shape
+    if S % 32:
+        raise ShapeError("pack_keep_bits: last dim must be a multiple of 32")
+    k = keep.reshape(*lead, S // 32, 32).to(torch.int64)
+    w = (k << torch.arange(32, device=keep.device, dtype=torch.int64)).sum(-1)
+    return torch.where(w >= 2 ** 31, w - 2 ** 32, w).to(torch.int32)
+
+
 def attn_fwd(qkv, B, S, heads, add_mask, keep, keep_scale, inv_divisor, ctx, lse, kbits_row=None,
              kbits_col=None):
     """qkv bf16 [B*S, >=3H] (Q|K|V blocks); ctx bf16 [B*S, >=H]; lse f32 [B, NH, S];
-    keep u8 [B, NH, S, S] or None; kbits_* int32 [B, NH, S, S/32] (packed keep flags)."""
+    keep u8 [B, NH, S, S] or None; kbits_* int32 [B, NH, S, S/32] (packed keep flags).
+    keep None with kbits_row given: the flags arrive packed in kbits_row (input)."""
     if qkv.dtype != torch.bfloat16 or ctx.dtype != torch.bfloat16:
         raise ShapeError("attn_fwd: qkv and ctx must be bfloat16")
     if qkv.stride(1) != 1 or ctx.stride(1) != 1:

@@ -151,3 +151,31 @@ def test_layer_fused_matches_unfused():
     assert O.compare_scaled(d1, d2) <= 2e-2
     for name in ("wq", "wk", "wv", "bq", "wo", "w1"):
         assert O.compare_scaled(g1[name], g2[name]) <= 2e-2, name
+
+
+def test_packed_keep_input_matches_u8():
+    """The attention dropout mask supplied bit-packed (kernels.pack_keep_bits,
+    the bench / e2e input form) gives bitwise the same layer outputs and
+    gradients as the u8 keep flags."""
+    import torch
+
+    from paper_2110_10802_b200 import kernels as K
+    from paper_2110_10802_b200.bert import BertEncoderLayer, BertLayerConfig
+
+    B, S, H, NH = 2, 256, 768, 12
+    g = torch.Generator(device="cpu").manual_seed(4)
+    x = torch.randn(B * S, H, generator=g).bfloat16().cuda()
+    dout = torch.randn(B * S, H, generator=g).bfloat16().cuda()
+    am = torch.where(torch.rand(B, S, generator=g) < 0.1, -10000.0, 0.0).cuda()
+    ka = (torch.rand(B, NH, S, S, generator=g) >= 0.1).to(torch.uint8).cuda()
+    k1 = (torch.rand(B * S, H, generator=g) >= 0.1).to(torch.uint8).cuda()
+    k2 = (torch.rand(B * S, H, generator=g) >= 0.1).to(torch.uint8).cuda()
+    outs = []
+    for keep in (ka, K.pack_keep_bits(ka)):
+        layer = BertEncoderLayer(BertLayerConfig(dtype=torch.bfloat16), seed=9)
+        out = layer.forward(x, am, keep, k1, k2).clone()
+        dx = layer.backward(dout).clone()
+        torch.cuda.synchronize()
+        outs.append((out, dx, layer.grad.flat.clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
