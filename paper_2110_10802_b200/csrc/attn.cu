@@ -565,6 +565,14 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
     if (part == 0) p.delta[rowi] = D;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const int words = S / 32;
+    // this thread's packed keep words for every chunk, fetched before the
+    // first S chunk lands (not a global-latency stall per chunk)
+    uint32_t kbw[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    if (p.kb_row) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < nch) kbw[j] = __ldg(p.kb_row + rowi * words + ((j * CH + part * 32) >> 5));
+    }
     for (int j = 0; j < nch; ++j) {
       mbar_wait(bar_s, j & 1);
       tc_fence_after();
@@ -575,7 +583,7 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_tfree);
       const int key0 = j * CH + part * 32;
-      const uint32_t bits = p.kb_row ? p.kb_row[rowi * words + (key0 >> 5)] : 0xFFFFFFFFu;
+      const uint32_t bits = j == 0 ? kbw[0] : (j == 1 ? kbw[1] : (j == 2 ? kbw[2] : kbw[3]));
       const float4* m4 = reinterpret_cast<const float4*>(mask2 + key0);
       uint32_t pk[16];
 #pragma unroll
@@ -733,6 +741,12 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const int words = S / 32;
     const size_t keyi = (size_t)bh * S + key;
+    uint32_t kbw[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};  // prefetched (see dq)
+    if (p.kb_col) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < nch) kbw[j] = __ldg(p.kb_col + keyi * words + ((j * CH + part * 32) >> 5));
+    }
     for (int j = 0; j < nch; ++j) {
       mbar_wait(bar_s, j & 1);
       tc_fence_after();
@@ -743,7 +757,7 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_tfree);
       const int qc0 = j * CH + part * 32;
-      const uint32_t bits = p.kb_col ? p.kb_col[keyi * words + (qc0 >> 5)] : 0xFFFFFFFFu;
+      const uint32_t bits = j == 0 ? kbw[0] : (j == 1 ? kbw[1] : (j == 2 ? kbw[2] : kbw[3]));
       const float4* l4 = reinterpret_cast<const float4*>(lse_s + qc0);
       const float4* d4 = reinterpret_cast<const float4*>(del_s + qc0);
       uint32_t pkp[16], pks[16];
