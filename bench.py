@@ -238,6 +238,69 @@ def _timed_graph(step, k, flush):
     return sum(a.elapsed_time(b) for a, b in evs) / k
 
 
+def measure_bert_c1(steps, flush, pk):
+    """BASELINE.json configs[0]: one BERT-base encoder layer, fp32, B=2 x S=128,
+    fwd + bwd + SGD (the reference's CPU-oracle workload; CUDA-core fp32 GEMMs
+    for the 1e-4 parity bar) as a CUDA graph, next to the oracle on the host."""
+    import torch
+
+    from paper_2110_10802_b200.bert import BertEncoderLayer, BertLayerConfig
+
+    b1, s1 = 2, 128
+    layer = BertEncoderLayer(BertLayerConfig(dtype=torch.float32), device="cuda", seed=3)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    dev = layer.device_inputs(b1, s1)
+    dev["x"].copy_(torch.randn(b1 * s1, H, generator=g))
+    dev["dout"].copy_(torch.randn(b1 * s1, H, generator=g))
+    dev["add_mask"].zero_()
+    for k in ("keep_attn", "keep1", "keep2"):
+        dev[k].copy_((torch.rand(dev[k].shape, generator=g) >= P_DROP).to(dev[k].dtype))
+    cs = layer.capture_step(b1, s1, 1e-4)
+    ms = _timed_graph(cs.replay, steps, flush)
+    v, reps, el = cpu_reference_sample(3.0, seq=s1)
+    return {"metric": "BERT-base encoder layer fwd+bwd+SGD, fp32, B=2 x S=128 (C1)",
+            "value": round(b1 * 1e3 / ms, 1), "unit": "samples/s", "ms_per_step": round(ms, 4),
+            "config": {"workload": "bert_base_encoder_layer_train_step fp32 (BASELINE.json configs[0])",
+                       "global_batch": b1, "seq_len": s1, "dtype": "f32"},
+            "cpu_oracle": {"value": round(v * 1.0, 3), "unit": "samples/s", "sample": f"{reps} x one sequence S={s1}",
+                           "cores": os.cpu_count()},
+            "note": "launch-bound: every kernel moves 1-5 MB (SURVEY.md §7 hard parts)"}
+
+
+def measure_norm_sweep_c4(steps, flush, pk):
+    """BASELINE.json configs[3]: LayerNorm vs BatchNorm (+ swish) over the
+    channel axis of channels-last 4D [32,56,56,64] and 5D [8,16,56,56,32]
+    bf16 tensors, fwd + bwd each; effective HBM GB/s over the compulsory
+    passes (LN: fwd read x + write y, bwd read dy, x + write dx; BN: fwd 2 reads
+    + 1 write, bwd 3 reads + 1 write)."""
+    import torch
+
+    from paper_2110_10802_b200.graphs import CapturedStep
+    from paper_2110_10802_b200.norms import BatchNormAct, LayerNormAct
+
+    out = {}
+    for name, shape in (("4d", (32, 56, 56, 64)), ("5d", (8, 16, 56, 56, 32))):
+        C = shape[-1]
+        g = torch.Generator(device="cpu").manual_seed(9)
+        x = torch.randn(shape, generator=g).bfloat16().cuda()
+        dy = torch.randn(shape, generator=g).bfloat16().cuda()
+        n = x.numel() * 2
+        for kind, mod, passes in (("layernorm_swish", LayerNormAct(C, act="swish"), 5),
+                                  ("batchnorm_swish", BatchNormAct(C, act="swish"), 7)):
+            def fn(m=mod):
+                m.forward(x)
+                m.backward(dy)
+
+            cs = CapturedStep(fn)
+            ms = _timed_graph(cs.replay, steps, flush)
+            gbs = passes * n / (ms * 1e-3) / 1e9
+            out[f"{kind}_{name}"] = {"shape": list(shape), "us_fwd_bwd": round(ms * 1e3, 2),
+                                     "hbm_gbs_effective": round(gbs, 1),
+                                     "hbm_frac_effective": round(gbs / pk["hbm_gbs"], 3)}
+    return {"metric": "normalisation sweep fwd+bwd (LN vs BN + swish, channels-last bf16) (C4)",
+            "config": {"workload": "norm_sweep (BASELINE.json configs[3])"}, "cases": out}
+
+
 def measure_mbconv_c3(steps, flush, pk):
     """BASELINE.json configs[2]: one MBConv block (dw3x3 + BN + swish + SE),
     N=96 x 112x112 x 96 channels, bf16, fwd + bwd as a CUDA graph."""
@@ -491,7 +554,9 @@ def run_ours(args):
     workloads = {}
     if not args.no_extra:
         if rank == 0 and world == 1:
+            workloads["bert_c1_fp32"] = measure_bert_c1(max(10, args.steps // 4), flush, pk)
             workloads["mbconv_c3"] = measure_mbconv_c3(max(10, args.steps // 4), flush, pk)
+            workloads["norm_sweep_c4"] = measure_norm_sweep_c4(max(10, args.steps // 4), flush, pk)
         workloads["efficientnet_b0_c5"] = measure_effnet_c5(max(5, args.steps // 20), flush, pk, world, rank,
                                                             local, dist)
 

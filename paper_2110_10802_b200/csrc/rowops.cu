@@ -18,6 +18,7 @@
 // through shared memory and finish with a fixed-order pass over blocks — no
 // float atomics, so results are bitwise reproducible.
 #include "common.cuh"
+#include "lnsmall.h"
 
 namespace dfx {
 namespace {
@@ -1002,6 +1003,8 @@ int dfx_layernorm_act_fwd(int dtype, int64_t rows, int64_t cols, const void* x, 
                           const float* beta, float eps, int act, void* y, void* stream) {
   DFX_REQUIRE(x && gamma && beta && y, DFX_ERR_SHAPE, "dfx_layernorm_act_fwd: null pointer");
   DFX_REQUIRE(act == 0 || act == 1, DFX_ERR_UNSUPPORTED, "dfx_layernorm_act_fwd: act must be 0 (none) or 1 (swish)");
+  if ((dtype == DFX_BF16 || dtype == DFX_F32) && ln_small_ok(dtype, cols))  // C4's short rows
+    return ln_small_fwd(dtype, rows, cols, x, gamma, beta, eps, act, y, as_stream(stream));
   if (dtype == DFX_BF16)
     return bdrln_fwd_t_any<__nv_bfloat16>(cols, rows, cols, x, nullptr, nullptr, 1.f, nullptr, gamma, beta, eps, y, nullptr,
                                       nullptr, nullptr, as_stream(stream), act);
@@ -1016,6 +1019,11 @@ int dfx_layernorm_act_bwd(int dtype, int64_t rows, int64_t cols, const void* dy,
                           float* dbeta, void* workspace, size_t ws_bytes, void* stream) {
   DFX_REQUIRE(dy && x && gamma && beta && dx, DFX_ERR_SHAPE, "dfx_layernorm_act_bwd: null pointer");
   DFX_REQUIRE(act == 0 || act == 1, DFX_ERR_UNSUPPORTED, "dfx_layernorm_act_bwd: act must be 0 (none) or 1 (swish)");
+  if ((dtype == DFX_BF16 || dtype == DFX_F32) && ln_small_ok(dtype, cols)) {
+    DFX_REQUIRE(dgamma && dbeta && workspace, DFX_ERR_SHAPE, "dfx_layernorm_act_bwd: dgamma/dbeta/workspace required");
+    return ln_small_bwd(dtype, rows, cols, dy, x, gamma, beta, eps, act, dx, dgamma, dbeta, workspace, ws_bytes,
+                        as_stream(stream));
+  }
   if (dtype == DFX_BF16)
     return bdrln_bwd_t_any<__nv_bfloat16>(cols, rows, cols, dy, x, gamma, nullptr, 1.f, eps, dx, nullptr, dgamma, dbeta, nullptr,
                                       workspace, ws_bytes, as_stream(stream), act, beta);
