@@ -101,6 +101,7 @@ class BertEncoderLayer:
         self.grad = FlatArena(specs, torch.float32, self.device)
         self.wlow = FlatArena(specs, torch.bfloat16, self.device) if cfg.dtype == torch.bfloat16 else None
         self._bufs = {}
+        self.slot = 0  # activation / input buffer set (see train_step_host_async)
         self._init_params(seed)
 
     # ------------------------------------------------------------ parameters
@@ -166,7 +167,8 @@ class BertEncoderLayer:
 
     # ------------------------------------------------------------ activations
     def buffers(self, B: int, S: int):
-        key = (B, S)
+        # one activation set per pipeline slot (train_step_host_async double-buffers)
+        key = (B, S, self.slot)
         if key not in self._bufs:
             c = self.cfg
             T, H, F, NH = B * S, c.hidden, c.ffn, c.heads
@@ -348,7 +350,7 @@ class BertEncoderLayer:
         for k in ("x", "add_mask", "keep_attn", "keep1", "keep2", "dout"):
             dev[k].copy_(host[k], non_blocking=True)
         if graph:
-            key = ("graph", B, S, lr)
+            key = ("graph", B, S, lr, self.slot)
             if key not in self._bufs:
                 self._bufs[key] = self.capture_step(B, S, lr)
             self._bufs[key].replay()
@@ -363,7 +365,7 @@ class BertEncoderLayer:
         return dx_host
 
     def _dev_inputs(self, B, S):
-        key = ("in", B, S)
+        key = ("in", B, S, self.slot)
         if key not in self._bufs:
             c = self.cfg
             T, H, NH, dev = B * S, c.hidden, c.heads, self.device
@@ -380,6 +382,53 @@ class BertEncoderLayer:
         return self._bufs[key]
 
     # ------------------------------------------------------------ CUDA graphs
+    def train_step_host_async(self, host: dict, lr=None, dx_host=None):
+        """Pipelined form of ``train_step_host``: two device input/activation
+        sets alternate, so step i+1's H2D copy (its own stream) and step i's
+        D2H of dx (another stream) overlap step i's CUDA-graph replay — the
+        prefetching a data loader does.  Every step still copies its own inputs
+        from pinned host memory and reads its own dx back; ``finish_host()``
+        joins the copy streams into the compute stream."""
+        B, S = host["add_mask"].shape
+        if not hasattr(self, "_pipe"):
+            self._pipe = {"h2d": torch.cuda.Stream(device=self.device), "d2h": torch.cuda.Stream(device=self.device),
+                          "free": [None, None]}
+        pp = self._pipe
+        slot = self.slot
+        comp = torch.cuda.current_stream(self.device)
+        dev = self._dev_inputs(B, S)
+        key = ("graph", B, S, lr, slot)
+        if key not in self._bufs:
+            torch.cuda.synchronize(self.device)
+            self._bufs[key] = self.capture_step(B, S, lr)
+        with torch.cuda.stream(pp["h2d"]):
+            if pp["free"][slot] is not None:
+                pp["h2d"].wait_event(pp["free"][slot])  # slot's previous step fully drained
+            for k in ("x", "add_mask", "keep_attn", "keep1", "keep2", "dout"):
+                dev[k].copy_(host[k], non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(pp["h2d"])
+        comp.wait_event(ev_in)
+        self._bufs[key].replay()
+        ev_done = torch.cuda.Event()
+        ev_done.record(comp)
+        with torch.cuda.stream(pp["d2h"]):
+            pp["d2h"].wait_event(ev_done)
+            if dx_host is not None:
+                dx_host.copy_(self.buffers(B, S)["dx"], non_blocking=True)
+            ev_free = torch.cuda.Event()
+            ev_free.record(pp["d2h"])
+        pp["free"][slot] = ev_free
+        self.slot ^= 1
+        return dx_host
+
+    def finish_host(self):
+        """Make the current stream wait for every pipelined copy."""
+        if hasattr(self, "_pipe"):
+            comp = torch.cuda.current_stream(self.device)
+            comp.wait_stream(self._pipe["h2d"])
+            comp.wait_stream(self._pipe["d2h"])
+
     def capture_step(self, B: int, S: int, lr=None, timer=None):
         """Capture forward + backward (+ SGD) on the static device input
         buffers (``device_inputs``) into a CUDA graph; returns a

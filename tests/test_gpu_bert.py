@@ -141,3 +141,35 @@ def test_bert_c2_properties():
     torch.cuda.synchronize()
     assert torch.isfinite(dx.float()).all()
     assert torch.isfinite(layer.grad.flat).all()
+
+
+def test_pipelined_host_steps_match_synchronous():
+    """train_step_host_async (double-buffered, H2D/D2H overlapping compute)
+    returns for every step exactly the dx the synchronous host API returns."""
+    from paper_2110_10802_b200 import kernels as K
+    from paper_2110_10802_b200.bert import BertEncoderLayer, BertLayerConfig
+
+    B, S, H, NH = 2, 128, 768, 12
+    g = torch.Generator(device="cpu").manual_seed(11)
+    hosts = []
+    for _ in range(4):
+        ka = (torch.rand(B, NH, S, S, generator=g) >= 0.1).to(torch.uint8)
+        hosts.append({k: v.pin_memory() for k, v in dict(
+            x=torch.randn(B * S, H, generator=g).bfloat16(), dout=torch.randn(B * S, H, generator=g).bfloat16(),
+            add_mask=torch.zeros(B, S), keep_attn=K.pack_keep_bits(ka),
+            keep1=(torch.rand(B * S, H, generator=g) >= 0.1).to(torch.uint8),
+            keep2=(torch.rand(B * S, H, generator=g) >= 0.1).to(torch.uint8)).items()})
+    outs = {}
+    for mode in ("sync", "async"):
+        layer = BertEncoderLayer(BertLayerConfig(dtype=torch.bfloat16), seed=2)
+        res = [torch.empty(B * S, H, dtype=torch.bfloat16).pin_memory() for _ in hosts]
+        for h, r in zip(hosts, res):
+            if mode == "sync":
+                layer.train_step_host(h, lr=None, dx_host=r)
+            else:
+                layer.train_step_host_async(h, lr=None, dx_host=r)
+        layer.finish_host()
+        torch.cuda.synchronize()
+        outs[mode] = res
+    for a, b in zip(outs["sync"], outs["async"]):
+        assert torch.equal(a, b)
