@@ -558,9 +558,16 @@ def run_ours(args):
     for r in rows:
         r["share"] = round(r["us_per_call"] * r["calls_per_step"] / tot, 3)
     dom = max(rows, key=lambda r: r["us_per_call"] * r["calls_per_step"])
+    # DRAM bytes per launch of the dominant kernel from the committed ncu --set
+    # full capture (profiles/r01_traffic.json, tools/gpu_profile.sh); null if absent
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom["kernel"])
     roofline = {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"],
                 "peak": pk["hbm_gbs"] if dom["bound"] == "hbm" else pk["tflops"], "unit": dom["unit"],
-                "frac": dom["frac"], "traffic": None, "peak_source": pk["source"]}
+                "frac": dom["frac"], "traffic": traffic, "traffic_source": "profiles/r01_traffic.json (ncu --set full)",
+                "peak_source": pk["source"]}
     gemm_us = sum(r["us_per_call"] * r["calls_per_step"] for r in rows if r["bound"] == "tensor")
     from oracle.oracle import bert_layer_flops  # algorithmic flop count only
 
