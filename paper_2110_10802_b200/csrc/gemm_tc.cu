@@ -501,6 +501,23 @@ __global__ void __launch_bounds__(256) splitk_reduce_few_kernel(int splits, int6
   }
 }
 
+// few splits, one contiguous f32 output matrix (the BERT / EfficientNet weight
+// gradients): 16-byte vectors, 32-bit indices, fixed split order
+__global__ void __launch_bounds__(256) splitk_reduce_vec4_kernel(int splits, int total4, int stride4,
+                                                                 const float4* __restrict__ part,
+                                                                 float4* __restrict__ d) {
+  pdl_trigger();
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += gridDim.x * blockDim.x) {
+    float4 acc = part[i];
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = part[(size_t)s * stride4 + i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    d[i] = acc;
+  }
+}
+
 // ----------------------------------------------------------------- host side
 }  // namespace
 
@@ -575,7 +592,9 @@ Plan plan(const dfx_gemm_args& p) {
   // 192-wide single-CTA tiles fill the SMs on the narrow (768-wide) outputs:
   // 32 x 4 = 128 tiles in one wave instead of 16 x 3 pairs on 96 SMs
   // (measured: out 11.2 -> 9.6 us, ffn2 22.4 -> 20.0 us; tools/gemm_force_sweep.sh)
-  const Cand cands[] = {{256, 2, 1.5}, {128, 2, 1.0}, {256, 1, 1.0}, {192, 1, 1.2}, {128, 1, 0.8}, {64, 1, 0.6}};
+  // relative per-SM throughputs measured on the BERT shapes (tools/gemm_force_sweep.sh,
+  // tools/wgrad_sweep.py): the 128-wide pair tile loses to the single-CTA one
+  const Cand cands[] = {{256, 2, 1.5}, {128, 2, 0.75}, {256, 1, 1.0}, {192, 1, 1.2}, {128, 1, 0.85}, {64, 1, 0.6}};
   Plan best{64, 1, 1, (int)kb, 0};
   double best_cost = 1e30;
   for (const Cand& c : cands) {
@@ -739,7 +758,13 @@ int gemm_tc(const dfx_gemm_args& p, cudaStream_t st) {
   rc = f32 ? launch_tc_any<float>(bn, pl.cg, ma, mb, tp, st) : launch_tc_any<__nv_bfloat16>(bn, pl.cg, ma, mb, tp, st);
   if (rc || pl.splits <= 1) return rc;
   const int64_t total = Z * p.m * p.n;
-  if (pl.splits <= 8) {
+  if (pl.splits <= 8 && p.out_dtype == DFX_F32 && Z == 1 && p.d_stride_m == p.n && p.n % 4 == 0 &&
+      aligned16(p.d) && total / 4 < (1ll << 31)) {
+    const int total4 = (int)(total / 4);
+    const int grid = (int)std::min<int64_t>((total4 + 255) / 256, (int64_t)num_sms() * 4);
+    launch_k(splitk_reduce_vec4_kernel, grid, 256, 0, st, pl.splits, total4, total4, (const float4*)part,
+             (float4*)p.d);
+  } else if (pl.splits <= 8) {
     const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
     if (p.out_dtype == DFX_F32)
       launch_k(splitk_reduce_few_kernel<float>, grid, 256, 0, st, pl.splits, Z, p.m, p.n, part, (float*)p.d,
