@@ -301,6 +301,15 @@ def measure_norm_sweep_c4(steps, flush, pk):
             "config": {"workload": "norm_sweep (BASELINE.json configs[3])"}, "cases": out}
 
 
+def _mbconv_vs_unfused(ours):
+    path = os.path.join(ROOT, "tests", "golden", "movement_volume.json")
+    if not os.path.exists(path):
+        return None
+    ref = json.load(open(path))["mbconv_c3"]["fwd_bwd_library_bytes"] / 2
+    return {"ours_bytes_per_step": ours, "reference_unfused_bytes_per_step_bf16": int(ref),
+            "ratio": round(ours / ref, 4)}
+
+
 def measure_mbconv_c3(steps, flush, pk):
     """BASELINE.json configs[2]: one MBConv block (dw3x3 + BN + swish + SE),
     N=96 x 112x112 x 96 channels, bf16, fwd + bwd as a CUDA graph."""
@@ -340,6 +349,7 @@ def measure_mbconv_c3(steps, flush, pk):
             "config": {"workload": "mbconv_block (BASELINE.json configs[2])", "batch": N, "hw": HW,
                        "channels": C, "stride": 1, "se": 4, "dtype": "bf16"},
             "hbm_gbs_effective": round(traffic / (ms * 1e-3) / 1e9, 1),
+            "bytes_vs_unfused": _mbconv_vs_unfused(traffic),
             "hbm_frac_effective": round(traffic / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], 3),
             "kernels": rows[:10]}
 
@@ -583,6 +593,20 @@ def run_ours(args):
         workloads["efficientnet_b0_c5"] = measure_effnet_c5(max(5, args.steps // 20), flush, pk, world, rank,
                                                             local, dist)
 
+    # the fused schedule's compulsory bytes vs the reference's unfused graph
+    # (ir.movement_volume of the autodiff graph, oracle/movement_volume.py; f32 -> bf16 halved)
+    mv_path = os.path.join(ROOT, "tests", "golden", "movement_volume.json")
+    bytes_vs_unfused = None
+    if os.path.exists(mv_path):
+        mv = json.load(open(mv_path))
+        ref_b = mv["bert_c2"]["fwd_bwd_library_bytes"] / 2
+        ours_b = layer.step_bytes(B, S)
+        bytes_vs_unfused = {"ours_bytes_per_step": ours_b, "reference_unfused_bytes_per_step_bf16": int(ref_b),
+                            "ratio": round(ours_b / ref_b, 4),
+                            "reference": "dfir ir.movement_volume of differentiate_graph(BERT layer) "
+                                         "(library-node form, f32 halved to bf16)",
+                            "achieved_gbs": round(ours_b / (ms_step * 1e-3) / 1e9, 1)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, reps, el = cpu_reference_sample(args.cpu_seconds)
@@ -609,6 +633,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "clocks": clocks,
             "workloads": workloads,
+            "bytes_vs_unfused": bytes_vs_unfused,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -329,6 +329,28 @@ class BertEncoderLayer:
         return out, dx
 
     # ------------------------------------------------------------ host-buffer API
+    def step_bytes(self, B: int, S: int) -> int:
+        """Compulsory HBM bytes of one fused training step (fused attention,
+        SGD included): every kernel's tensor arguments read once and written
+        once — the schedule's own data movement, compared in bench.py with the
+        reference's ``ir.movement_volume`` of the unfused graph."""
+        c = self.cfg
+        T, H, F, NH = B * S, c.hidden, c.ffn, c.heads
+        e = torch.tensor([], dtype=c.dtype).element_size()
+        th, tf, t3 = T * H * e, T * F * e, T * 3 * H * e
+        bits = B * NH * S * S // 8
+        w = lambda n, k: n * k * e  # noqa: E731  (bf16 weight operand)
+        g32 = lambda n, k: n * k * 4  # noqa: E731  (f32 weight gradient)
+        fwd = (th + w(3 * H, H) + t3) + (t3 + bits + th + bits + B * NH * S * 4) + (th + w(H, H) + th) \
+            + (2 * th + T * H + 2 * th) + (th + w(F, H) + 2 * tf) + (tf + w(H, F) + th) + (2 * th + T * H + 2 * th)
+        bwd = (2 * th + T * H + 2 * th) + (th + w(H, F) + tf + tf) + (th + tf + g32(H, F)) + tf \
+            + (tf + w(F, H) + th + th) + (tf + th + g32(F, H)) + (2 * th + T * H + 2 * th) + (th + w(H, H) + th) \
+            + (2 * th + g32(H, H)) + (t3 + 2 * th + B * NH * S * 4 + 2 * bits + t3) + t3 \
+            + (t3 + w(3 * H, H) + th + th) + (t3 + th + g32(3 * H, H))
+        nparam = sum(v.numel() for v in self.master.views.values())
+        sgd = nparam * (4 + 4 + 4 + (2 if self.wlow is not None else 0))
+        return int(fwd + bwd + sgd)
+
     def host_inputs_bytes(self, B: int, S: int) -> tuple[int, int]:
         """(H2D, D2H) bytes per train_step_host call."""
         c = self.cfg

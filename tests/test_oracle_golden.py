@@ -194,3 +194,17 @@ def test_bf16_flip_sensitivity():
     scaled = max(O.compare_scaled(g2[k], g1[k]) for k in O.BERT_WEIGHTS)
     assert scaled < 1e-2
     assert elem > scaled  # the element-wise metric over-reacts to flips
+
+
+def test_movement_volume_fixture():
+    """The reference's unfused byte accounting (oracle/movement_volume.py,
+    committed fixture) that bench.py compares the fused schedules against:
+    the MBConv forward lowered bytes reproduce SURVEY §8a row a14 (6.47 GB)."""
+    import json
+    import os
+
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "movement_volume.json")))
+    assert abs(d["mbconv_c3"]["fwd_lowered_bytes"] / 1e9 - 6.47) < 0.01
+    assert abs(d["mbconv_c3"]["fwd_library_bytes"] / 1e9 - 5.55) < 0.01
+    for k in ("bert_c2", "mbconv_c3"):
+        assert d[k]["fwd_bwd_library_bytes"] > d[k]["fwd_library_bytes"] > 0
