@@ -493,6 +493,7 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // setup above overlapped the previous kernel's tail
+  if (threadIdx.x == 0) ATRACE(0);
   constexpr uint32_t T_S = 0, T_DP = 128, T_DQ = 256;
 
   if (warp == 0) {
@@ -521,6 +522,7 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
       const uint64_t dodesc = make_sdesc(sbase + DqSmem::DO, 16, 1024);
       mbar_wait(bar_q, 0);
       tc_fence_after();
+      ATRACE(1);
       auto issue_dq = [&](int j) {  // dQ += dS_j · K_j   (K_j read MN-major)
         mbar_wait(bar_ds, j & 1);
         tc_fence_after();
@@ -576,6 +578,7 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
     for (int j = 0; j < nch; ++j) {
       mbar_wait(bar_s, j & 1);
       tc_fence_after();
+      if (sw == 0 && lane == 0 && j < 4) ATRACE(2 + j);
       float s[32], dp[32];
       tmem_ld32(trow + T_S + part * 32, s);
       tmem_ld32(trow + T_DP + part * 32, dp);
@@ -584,21 +587,21 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
       if (lane == 0) mbar_arrive(bar_tfree);
       const int key0 = j * CH + part * 32;
       const uint32_t bits = j == 0 ? kbw[0] : (j == 1 ? kbw[1] : (j == 2 ? kbw[2] : kbw[3]));
-      const float4* m4 = reinterpret_cast<const float4*>(mask2 + key0);
       uint32_t pk[16];
+      // packed fp32 pairs: P' = exp2(s*c + mask - lse') ; dS = P' * (dPd*keep*ks - D)
+      const float2 sc2x2 = make_float2(p.sc2, p.sc2), nl2 = make_float2(-lse_c, -lse_c);
+      const float2 ks2 = make_float2(p.ks, p.ks), nD2 = make_float2(-D, -D);
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        const float4 m = m4[i >> 2];
-        const float mm[4] = {m.x, m.y, m.z, m.w};
-        float d[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          // P' = scale * P ; dS = P' * (dPd * keep * ks - D)
-          const float P = ex2(fmaf(s[i + e], p.sc2, mm[e]) - lse_c);
-          d[e] = P * (((bits >> (i + e)) & 1u) ? fmaf(dp[i + e], p.ks, -D) : -D);
-        }
-        pk[i >> 1] = pack_bf16x2(d[0], d[1]);
-        pk[(i >> 1) + 1] = pack_bf16x2(d[2], d[3]);
+      for (int i = 0; i < 32; i += 2) {
+        const float2 m = reinterpret_cast<const float2*>(mask2 + key0)[i >> 1];
+        const float2 t = __ffma2_rn(make_float2(s[i], s[i + 1]), sc2x2, __fadd2_rn(m, nl2));
+        const float2 P = make_float2(ex2(t.x), ex2(t.y));
+        // dPd * keep: the dropped lanes' bits zeroed (0 * ks - D = -D)
+        const uint32_t k0 = 0u - ((bits >> i) & 1u), k1 = 0u - ((bits >> (i + 1)) & 1u);
+        const float2 dpm = make_float2(__uint_as_float(__float_as_uint(dp[i]) & k0),
+                                       __uint_as_float(__float_as_uint(dp[i + 1]) & k1));
+        const float2 d = __fmul2_rn(P, __ffma2_rn(dpm, ks2, nD2));
+        pk[i >> 1] = pack_bf16x2(d.x, d.y);
       }
       if (j > 0) mbar_wait(bar_dsfree, (j - 1) & 1);
       st_row32(sbase + DqSmem::DS, rl, part * 32, pk);
@@ -606,8 +609,10 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_ds);
+      if (sw == 0 && lane == 0 && j < 4) ATRACE(6 + j);
     }
     mbar_wait(bar_dsfree, (nch - 1) & 1);
+    if (sw == 0 && lane == 0) ATRACE(10);
     tc_fence_after();
     float o[16];
     tmem_ld16(trow + T_DQ + part * 16, o);
@@ -615,6 +620,7 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ATRACE(11);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
@@ -758,27 +764,23 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
       if (lane == 0) mbar_arrive(bar_tfree);
       const int qc0 = j * CH + part * 32;
       const uint32_t bits = j == 0 ? kbw[0] : (j == 1 ? kbw[1] : (j == 2 ? kbw[2] : kbw[3]));
-      const float4* l4 = reinterpret_cast<const float4*>(lse_s + qc0);
-      const float4* d4 = reinterpret_cast<const float4*>(del_s + qc0);
       uint32_t pkp[16], pks[16];
+      // packed fp32 pairs.  P' = P / divisor; Pd' = P' * keep (dV is rescaled
+      // by ks * divisor); dS = P' * (dPd * keep * ks - D)
+      const float2 sc2x2 = make_float2(p.sc2, p.sc2), mrow2 = make_float2(mrow, mrow), ks2 = make_float2(p.ks, p.ks);
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        const float4 l = l4[i >> 2], dd = d4[i >> 2];
-        const float ll[4] = {l.x, l.y, l.z, l.w}, DD[4] = {dd.x, dd.y, dd.z, dd.w};
-        float pd[4], ds[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          // P' = P / divisor; Pd' = P' * keep (dV is rescaled by ks * divisor);
-          // dS = P' * (dPd * keep * ks - D)
-          const float P = ex2(fmaf(s[i + e], p.sc2, mrow) - ll[e]);
-          const bool kept = (bits >> (i + e)) & 1u;
-          pd[e] = kept ? P : 0.f;
-          ds[e] = P * (kept ? fmaf(dp[i + e], p.ks, -DD[e]) : -DD[e]);
-        }
-        pkp[i >> 1] = pack_bf16x2(pd[0], pd[1]);
-        pkp[(i >> 1) + 1] = pack_bf16x2(pd[2], pd[3]);
-        pks[i >> 1] = pack_bf16x2(ds[0], ds[1]);
-        pks[(i >> 1) + 1] = pack_bf16x2(ds[2], ds[3]);
+      for (int i = 0; i < 32; i += 2) {
+        const float2 l = reinterpret_cast<const float2*>(lse_s + qc0)[i >> 1];
+        const float2 dd = reinterpret_cast<const float2*>(del_s + qc0)[i >> 1];
+        const float2 t = __ffma2_rn(make_float2(s[i], s[i + 1]), sc2x2, __fadd2_rn(mrow2, make_float2(-l.x, -l.y)));
+        const float2 P = make_float2(ex2(t.x), ex2(t.y));
+        const uint32_t k0 = 0u - ((bits >> i) & 1u), k1 = 0u - ((bits >> (i + 1)) & 1u);
+        const float2 pd = make_float2(__uint_as_float(__float_as_uint(P.x) & k0), __uint_as_float(__float_as_uint(P.y) & k1));
+        const float2 dpm = make_float2(__uint_as_float(__float_as_uint(dp[i]) & k0),
+                                       __uint_as_float(__float_as_uint(dp[i + 1]) & k1));
+        const float2 ds = __fmul2_rn(P, __ffma2_rn(dpm, ks2, make_float2(-dd.x, -dd.y)));
+        pkp[i >> 1] = pack_bf16x2(pd.x, pd.y);
+        pks[i >> 1] = pack_bf16x2(ds.x, ds.y);
       }
       if (j > 0) mbar_wait(bar_pdsfree, (j - 1) & 1);
       st_row32(sbase + DkvSmem::PD, rl, part * 32, pkp);
@@ -912,8 +914,10 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
     attr = true;
   }
   const int grid = (int)(batch * heads * (seq / QT));
+  p.trace = g_attn_trace;  // debug timeline of the dq kernel (tools/attn_trace.py --bwd)
   launch_k(attn_bwd_dq_kernel, grid, kAttnThreads, DqSmem::TOTAL, as_stream(stream), mqkv, mdo, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dq)");
+  p.trace = nullptr;
   launch_k(attn_bwd_dkdv_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dk, dv)");
   return DFX_OK;

@@ -31,6 +31,26 @@ else:
 for _ in range(3):
     run()
 ncta = B * NH * S // 128
+if "--bwd" in sys.argv:  # dq kernel timeline: 0 start, 1 Q/dO landed (MMA), 2-5 S_j ready, 6-9 dS_j done, 10 dQ done, 11 exit
+    run()
+    dctx = torch.randn_like(ctx)
+    dqkv = torch.empty_like(qkv)
+    bwd = lambda: K.attn_bwd(qkv, ctx, dctx, B, S, NH, am, lse, kr, kc, 1 / 0.9, 0.125, dqkv)  # noqa: E731
+    for _ in range(3):
+        bwd()
+    tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
+    fn(tr.data_ptr())
+    bwd()
+    torch.cuda.synchronize()
+    fn(None)
+    t = tr.view(ncta, 16).cpu().double()
+    rel = (t - t[:, 0].min()) / 1e3
+    d = rel[:, 1:12] - rel[:, 0:11]
+    names = ["start->qdo", "qdo->S0", "S0->S1", "S1->S2", "S2->S3", "S3->dS0", "dS0->dS1", "dS1->dS2", "dS2->dS3",
+             "dS3->dQ", "dQ->exit"]
+    print("dq mean phase durations (us):", {n: round(d[:, i].mean().item(), 2) for i, n in enumerate(names)})
+    print("dq per-CTA total mean", (rel[:, 11] - rel[:, 0]).mean().item(), "kernel span", rel[:, 11].max().item())
+    sys.exit(0)
 tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
 fn(tr.data_ptr())
 run()
