@@ -16,27 +16,42 @@ namespace dfx {
 namespace {
 
 // stem: cols[m][k] for a 3x3 conv with Cin input channels, k = (ky*3+kx)*Cin + c,
-// zero for padding taps and for k in [9*Cin, Kp) (Kp = GEMM K, a multiple of 8)
-template <typename T>
+// zero for padding taps and for k in [9*Cin, Kp) (Kp = GEMM K, a multiple of 8).
+// One thread per output pixel: the 9*Cin taps are gathered into registers and
+// the Kp-wide row leaves as 16-byte stores (one index decomposition per pixel).
+template <typename T, int KP>
 __global__ void __launch_bounds__(256) im2col3x3_kernel(int N, int H, int W, int Cin, int Ho, int Wo, int stride,
-                                                        int pt, int pl, int Kp, const T* __restrict__ x,
+                                                        int pt, int pl, const T* __restrict__ x,
                                                         T* __restrict__ cols) {
   pdl_wait();
   pdl_trigger();
-  const int64_t total = (int64_t)N * Ho * Wo * Kp;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(i % Kp);
-    const int64_t m = i / Kp;
+  constexpr int EPV = 16 / sizeof(T);
+  const int64_t total = (int64_t)N * Ho * Wo;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < total; m += (int64_t)gridDim.x * blockDim.x) {
     const int ox = (int)(m % Wo);
-    const int oy = (int)((m / Wo) % Ho);
-    const int n = (int)(m / ((int64_t)Wo * Ho));
-    float v = 0.f;
-    if (k < 9 * Cin) {
-      const int t = k / Cin, c = k % Cin;
+    const int64_t t2 = m / Wo;
+    const int oy = (int)(t2 % Ho);
+    const int n = (int)(t2 / Ho);
+    float v[KP];
+#pragma unroll
+    for (int k = 0; k < KP; ++k) v[k] = 0.f;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
       const int iy = oy * stride + t / 3 - pt, ix = ox * stride + t % 3 - pl;
-      if (iy >= 0 && iy < H && ix >= 0 && ix < W) v = to_f(x[(((size_t)n * H + iy) * W + ix) * Cin + c]);
+      if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
+        const T* px = x + (((size_t)n * H + iy) * W + ix) * Cin;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[t * 3 + c] = to_f(px[c]);  // Cin == 3 (host-checked)
+      }
     }
-    cols[i] = from_f<T>(v);
+    T* out = cols + m * KP;
+#pragma unroll
+    for (int q = 0; q < KP / EPV; ++q) {
+      Vec<T, EPV> o;
+#pragma unroll
+      for (int i = 0; i < EPV; ++i) o.v[i] = v[q * EPV + i];
+      o.store(out + q * EPV);
+    }
   }
 }
 
@@ -165,13 +180,14 @@ int dfx_im2col3x3(int dtype, int64_t N, int64_t H, int64_t W, int64_t Cin, int s
   const int64_t Ho = (H + pads[0] + pads[2] - 3) / stride + 1, Wo = (W + pads[1] + pads[3] - 3) / stride + 1;
   DFX_REQUIRE(Ho > 0 && Wo > 0, DFX_ERR_SHAPE, "dfx_im2col3x3: empty output");
   cudaStream_t st = as_stream(stream);
-  const int grid = grid_for(N * Ho * Wo * Kp);
+  DFX_REQUIRE(Kp == 32 && Cin == 3, DFX_ERR_UNSUPPORTED, "dfx_im2col3x3: the stem layout (Cin = 3, Kp = 32)");
+  const int grid = grid_for(N * Ho * Wo);
   if (dtype == DFX_BF16)
-    launch_k(im2col3x3_kernel<__nv_bfloat16>, grid, 256, 0, st, (int)N, (int)H, (int)W, (int)Cin, (int)Ho, (int)Wo,
-             stride, pads[0], pads[1], (int)Kp, (const __nv_bfloat16*)x, (__nv_bfloat16*)cols);
+    launch_k(im2col3x3_kernel<__nv_bfloat16, 32>, grid, 256, 0, st, (int)N, (int)H, (int)W, (int)Cin, (int)Ho,
+             (int)Wo, stride, pads[0], pads[1], (const __nv_bfloat16*)x, (__nv_bfloat16*)cols);
   else if (dtype == DFX_F32)
-    launch_k(im2col3x3_kernel<float>, grid, 256, 0, st, (int)N, (int)H, (int)W, (int)Cin, (int)Ho, (int)Wo, stride,
-             pads[0], pads[1], (int)Kp, (const float*)x, (float*)cols);
+    launch_k(im2col3x3_kernel<float, 32>, grid, 256, 0, st, (int)N, (int)H, (int)W, (int)Cin, (int)Ho, (int)Wo,
+             stride, pads[0], pads[1], (const float*)x, (float*)cols);
   else
     return fail(DFX_ERR_DTYPE, "dfx_im2col3x3: dtype must be f32 or bf16");
   DFX_LAUNCH_CHECK("dfx_im2col3x3");
