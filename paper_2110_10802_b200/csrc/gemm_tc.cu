@@ -50,8 +50,12 @@ template <int BN, int CG = 1> struct TcCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN / CG * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // two accumulator buffers, rounded up to the power-of-two allocation unit
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : (BN == 192 ? 512 : 2 * BN);
+  // TMEM accumulator buffers: narrow tiles (BN <= 128) keep FOUR so the
+  // mainloop runs up to three tiles ahead of the epilogue, and the 16
+  // epilogue warps split into four groups that each drain a whole tile
+  // (skinny GEMMs are epilogue-bound); wide tiles keep two.
+  static constexpr int NACC = BN <= 128 ? 4 : 2;
+  static constexpr int TMEM_COLS = NACC * BN < 32 ? 32 : (BN == 192 ? 512 : NACC * BN);
   static constexpr int EPI_BYTES = kEpiWarps * EPI_WARP_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -203,9 +207,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   uint8_t* epi_smem = smem + STAGES * Cfg::STAGE_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + Cfg::EPI_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;  // [2]
-  uint64_t* tempty = tfull + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  constexpr int NACC = Cfg::NACC;
+  constexpr int EPI_GROUP_WARPS = NACC == 4 ? 4 : kEpiWarps;  // warps draining one tile
+  uint64_t* tfull = empty + STAGES;  // [NACC]
+  uint64_t* tempty = tfull + NACC;   // [NACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TRACE(0);
@@ -217,7 +223,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * kEpiWarps); }
+    for (int a = 0; a < NACC; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * EPI_GROUP_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -297,8 +303,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const TileIdx ti = tile_of(t, p);
         const int kb0 = ti.split * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
-        const int acc = lt & 1;
-        const uint32_t aph = (lt >> 1) & 1;
+        const int acc = (int)(lt % NACC);
+        const uint32_t aph = (lt / NACC) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
@@ -330,8 +336,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // 16-byte global stores (and the mirror path for the aux operand).
     const int ew = warp - 2;          // 0..15
     const int q = warp & 3;           // TMEM lane quadrant this warp may access
-    const int part = ew >> 2;         // which quarter of the tile's columns
-    constexpr int WCOLS = BN / 4;     // columns per warp
+    // NACC == 4: group ew>>2 drains every 4th tile, each warp all BN columns
+    // of its quadrant; NACC == 2: all 16 warps share a tile, a quarter each
+    const int grp = NACC == 4 ? (ew >> 2) : 0;
+    const int part = NACC == 4 ? 0 : ew >> 2;
+    constexpr int WCOLS = NACC == 4 ? BN : BN / 4;  // columns per warp
     constexpr int ESZ = (int)sizeof(TO);
     // bytes per row per unit: 64 when the warp's columns tile by it (BN = 192 bf16: 32)
     constexpr int UB = (WCOLS * ESZ) % 64 == 0 ? 64 : ((WCOLS * ESZ) % 32 == 0 ? 32 : 16);
@@ -345,9 +354,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const bool unit_alpha = p.alpha == 1.f;
     uint32_t lt = 0;
     for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++lt) {
+      if (NACC == 4 && (int)(lt & 3) != grp) continue;  // another group's tile
       const TileIdx ti = tile_of(t, p);
-      const int acc = lt & 1;
-      const uint32_t aph = (lt >> 1) & 1;
+      const int acc = (int)(lt % NACC);
+      const uint32_t aph = (lt / NACC) & 1;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       if (ew == 0 && lane == 0 && lt < 8) TRACE(11 + lt);
@@ -609,6 +619,14 @@ Plan plan(const dfx_gemm_args& p) {
       best_cost = cost;
       best = Plan{c.bn, c.cg, 1, (int)kb, units};
     }
+  }
+  // one k-block (K <= 64: the EfficientNet expand / stem / project 1x1 convs
+  // with 16-40 input channels): the GEMM is a pure epilogue stream, and the
+  // pair tile halves the tile count (tools/skinny_sweep.py: 161 -> 107 us on
+  // the 1.2M x 96 x 16 expand)
+  if (z == 1 && kb == 1 && p.m >= 256 && sms >= 2 && p.epilogue == DFX_EPI_NONE) {
+    const int64_t units = (p.m + 255) / 256 * ((p.n + 127) / 128);
+    best = Plan{128, 2, 1, (int)kb, units};
   }
   // split K when a 1-CTA plan leaves most SMs idle (the 768-wide wgrads)
   if (best.cg == 1 && p.epilogue == DFX_EPI_NONE && best.tiles * 2 <= sms && kb >= 8) {
