@@ -263,28 +263,47 @@ class BertEncoderLayer:
         b = self.buffers(B, S)
         P, G = self.master, self.grad
         L = K.label
+        # Weight-gradient GEMMs and bias column sums do not feed the dgrad
+        # chain: they run on a second stream (forked after their inputs exist,
+        # joined before returning), so their CTAs fill the wave-quantisation
+        # tails of the dgrad GEMMs and the attention kernels.  The CUDA graph
+        # captures the fork/join as parallel branches.
+        main = torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream(device=self.device)
+        side = self._side
+
+        def fork():
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            return torch.cuda.stream(side)
+
         with L("bwd.bdrln2"):
             K.bdrln_bwd(dout, b["s2"], P["g2"], keep2, ks, c.eps, ds=b["ds2"], dh=b["da2"],
                         dgamma=G["g2"], dbeta=G["be2"], dbias=G["b2"])
+        with fork():
+            with L("bwd.ffn2_wgrad"):
+                K.gemm(b["da2"].t(), b["g"].t(), G["w2"])
         # FFN2: dgrad with the GELU-backward epilogue, wgrad straight into f32 grads
         with L("bwd.ffn2_dgrad+gelu_bwd"):
             K.gemm(b["da2"], self.weight("w2").t(), b["dpre"], EPI_GELU_BWD, aux=b["pre"])
-        with L("bwd.ffn2_wgrad"):
-            K.gemm(b["da2"].t(), b["g"].t(), G["w2"])
-        with L("bwd.ffn1_bias_grad"):
-            K.colsum(b["dpre"], G["b1"])
+        with fork():
+            with L("bwd.ffn1_bias_grad"):
+                K.colsum(b["dpre"], G["b1"])
+            with L("bwd.ffn1_wgrad"):
+                K.gemm(b["dpre"].t(), b["ln1"].t(), G["w1"])
         # FFN1: dgrad + residual gradient from LN2
         with L("bwd.ffn1_dgrad+residual"):
             K.gemm(b["dpre"], self.weight("w1").t(), b["dln1"], EPI_ADD, aux=b["ds2"])
-        with L("bwd.ffn1_wgrad"):
-            K.gemm(b["dpre"].t(), b["ln1"].t(), G["w1"])
         with L("bwd.bdrln1"):
             K.bdrln_bwd(b["dln1"], b["s1"], P["g1"], keep1, ks, c.eps, ds=b["ds1"], dh=b["da1"],
                         dgamma=G["g1"], dbeta=G["be1"], dbias=G["bo"])
+        with fork():
+            with L("bwd.out_wgrad"):
+                K.gemm(b["da1"].t(), b["ctx"].t(), G["wo"])
         with L("bwd.out_dgrad"):
             K.gemm(b["da1"], self.weight("wo").t(), b["dctx"])
-        with L("bwd.out_wgrad"):
-            K.gemm(b["da1"].t(), b["ctx"].t(), G["wo"])
         # attention
         if self._fused(S):
             with L("bwd.attention"):
@@ -292,12 +311,14 @@ class BertEncoderLayer:
                            b["kbits_col"], ks, 1.0 / (c.head_dim ** 0.5), b["dqkv"])
         else:
             self._attn_bwd_unfused(b, B, S, keep_attn, ks)
-        with L("bwd.qkv_bias_grad"):
-            K.colsum(b["dqkv"], G["bqkv"])
+        with fork():
+            with L("bwd.qkv_bias_grad"):
+                K.colsum(b["dqkv"], G["bqkv"])
+            with L("bwd.qkv_wgrad"):
+                K.gemm(b["dqkv"].t(), x.t(), G["wqkv"])
         with L("bwd.qkv_dgrad+residual"):
             K.gemm(b["dqkv"], self.weight("wqkv").t(), b["dx"], EPI_ADD, aux=b["ds1"])
-        with L("bwd.qkv_wgrad"):
-            K.gemm(b["dqkv"].t(), x.t(), G["wqkv"])
+        main.wait_stream(side)  # join: every gradient is complete on the caller's stream
         return b["dx"]
 
     def _attn_bwd_unfused(self, b, B, S, keep_attn, ks):
