@@ -173,16 +173,18 @@ class _Block:
         dy = torch.empty_like(self.y)
         with K.label("block.project_dgrad"):
             _gemm(dp.view(-1, self.co), self.w("wp").t(), dy.view(-1, self.cx))
-        with K.label("block.project_wgrad"):
-            _gemm(dp.view(-1, self.co).t(), y2.t(), G[self.p + "wp"])
+        with self.net.fork():
+            with K.label("block.project_wgrad"):
+                _gemm(dp.view(-1, self.co).t(), y2.t(), G[self.p + "wp"])
         da = self.mb.backward(dy)
         if self.e != 1:
             dh = self.bn1.backward(da)
             dx = torch.empty_like(self.x)
             with K.label("block.expand_dgrad"):
                 _gemm(dh.view(-1, self.cx), self.w("we").t(), dx.view(-1, self.ci))
-            with K.label("block.expand_wgrad"):
-                _gemm(dh.view(-1, self.cx).t(), self.x.view(-1, self.ci).t(), G[self.p + "we"])
+            with self.net.fork():
+                with K.label("block.expand_wgrad"):
+                    _gemm(dh.view(-1, self.cx).t(), self.x.view(-1, self.ci).t(), G[self.p + "we"])
         else:
             dx = da  # the MBConv block's own dx buffer (no residual on expand-ratio-1 blocks)
         if self.residual:
@@ -298,16 +300,29 @@ class EfficientNetB0:
         self.dlogits = dlogits
         return self.loss
 
+    def fork(self):
+        """Run the enclosed launches on the side stream after everything queued
+        so far on the main stream (weight gradients: off the dgrad chain)."""
+        main = torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream(device=self.device)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self._side.wait_event(ev)
+        return torch.cuda.stream(self._side)
+
     def backward(self):
         """Gradients of the mean loss w.r.t. every parameter (this rank's
-        batch; the data-parallel sum is the caller's allreduce)."""
+        batch; the data-parallel sum is the caller's allreduce).  Weight
+        gradients run on a forked stream joined at the end."""
         c, G = self.cfg, self.grad
         N = self.pooled.shape[0]
         dt, st = K.dfx_dtype(self.pooled), K._stream()
         dl = self.dlogits
-        with K.label("fc.wgrad"):
-            _gemm(dl.t(), self.pooled.t(), G["fc.w"])
-        K.colsum(dl, G["fc.b"])
+        with self.fork():
+            with K.label("fc.wgrad"):
+                _gemm(dl.t(), self.pooled.t(), G["fc.w"])
+            K.colsum(dl, G["fc.b"])
         dpooled = torch.empty_like(self.pooled)
         with K.label("fc.dgrad"):
             _gemm(dl, self.w("fc.w").t(), dpooled)
@@ -320,13 +335,16 @@ class EfficientNetB0:
         dcur = torch.empty_like(self.last)
         with K.label("head.dgrad"):
             _gemm(dhh.view(-1, c.head), self.w("head.w").t(), dcur.view(-1, Cl))
-        with K.label("head.wgrad"):
-            _gemm(dhh.view(-1, c.head).t(), self.last.view(-1, Cl).t(), G["head.w"])
+        with self.fork():
+            with K.label("head.wgrad"):
+                _gemm(dhh.view(-1, c.head).t(), self.last.view(-1, Cl).t(), G["head.w"])
         for b in reversed(self.blocks):
             dcur = b.backward(dcur)
         dh = self.stem_bn.backward(dcur)
-        with K.label("stem.wgrad"):
-            _gemm(dh.view(-1, c.stem).t(), self.cols.t(), G["stem.w"])
+        with self.fork():
+            with K.label("stem.wgrad"):
+                _gemm(dh.view(-1, c.stem).t(), self.cols.t(), G["stem.w"])
+        torch.cuda.current_stream(self.device).wait_stream(self._side)  # join
 
     def sgd_step(self, lr: float):
         with K.label("sgd_update"):
