@@ -173,7 +173,7 @@ class _Block:
         dy = torch.empty_like(self.y)
         with K.label("block.project_dgrad"):
             _gemm(dp.view(-1, self.co), self.w("wp").t(), dy.view(-1, self.cx))
-        with self.net.fork():
+        with self.net.fork(dp):
             with K.label("block.project_wgrad"):
                 _gemm(dp.view(-1, self.co).t(), y2.t(), G[self.p + "wp"])
         da = self.mb.backward(dy)
@@ -182,7 +182,7 @@ class _Block:
             dx = torch.empty_like(self.x)
             with K.label("block.expand_dgrad"):
                 _gemm(dh.view(-1, self.cx), self.w("we").t(), dx.view(-1, self.ci))
-            with self.net.fork():
+            with self.net.fork(dh):
                 with K.label("block.expand_wgrad"):
                     _gemm(dh.view(-1, self.cx).t(), self.x.view(-1, self.ci).t(), G[self.p + "we"])
         else:
@@ -300,15 +300,20 @@ class EfficientNetB0:
         self.dlogits = dlogits
         return self.loss
 
-    def fork(self):
+    def fork(self, *uses):
         """Run the enclosed launches on the side stream after everything queued
-        so far on the main stream (weight gradients: off the dgrad chain)."""
+        so far on the main stream (weight gradients: off the dgrad chain).
+        ``uses``: freshly allocated tensors the side stream reads — recorded on
+        it so the caching allocator cannot hand their memory to a later
+        main-stream allocation while the side stream still reads them."""
         main = torch.cuda.current_stream(self.device)
         if not hasattr(self, "_side"):
             self._side = torch.cuda.Stream(device=self.device)
         ev = torch.cuda.Event()
         ev.record(main)
         self._side.wait_event(ev)
+        for t in uses:
+            t.record_stream(self._side)
         return torch.cuda.stream(self._side)
 
     def backward(self):
@@ -335,13 +340,13 @@ class EfficientNetB0:
         dcur = torch.empty_like(self.last)
         with K.label("head.dgrad"):
             _gemm(dhh.view(-1, c.head), self.w("head.w").t(), dcur.view(-1, Cl))
-        with self.fork():
+        with self.fork(dhh):
             with K.label("head.wgrad"):
                 _gemm(dhh.view(-1, c.head).t(), self.last.view(-1, Cl).t(), G["head.w"])
         for b in reversed(self.blocks):
             dcur = b.backward(dcur)
         dh = self.stem_bn.backward(dcur)
-        with self.fork():
+        with self.fork(dh):
             with K.label("stem.wgrad"):
                 _gemm(dh.view(-1, c.stem).t(), self.cols.t(), G["stem.w"])
         torch.cuda.current_stream(self.device).wait_stream(self._side)  # join
