@@ -88,6 +88,12 @@ int dfx_bdrln_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const v
                   const float* gamma, const uint8_t* keep, float keep_scale, float eps,
                   void* ds, void* dh, float* dgamma, float* dbeta, float* dbias, void* workspace,
                   size_t ws_bytes, void* stream);
+/* The parameter-gradient half of dfx_bdrln_bwd as its own launch: call
+ * dfx_bdrln_bwd with dgamma = dbeta = dbias = NULL (it leaves the per-block
+ * partial sums in `workspace`), then this — possibly on another stream, after
+ * an event — to reduce them (fixed order) into dgamma / dbeta / dbias. */
+int dfx_bdrln_bwd_finalize(int dtype, int64_t rows, int64_t cols, const void* workspace, size_t ws_bytes,
+                           float* dgamma, float* dbeta, float* dbias, void* stream);
 
 /* ---- a4/a5: scaled + masked softmax + dropout (forward) -------------------
  * rows are [batch, heads, q] (row-major), cols = k.

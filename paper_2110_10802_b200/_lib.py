@@ -120,6 +120,8 @@ _SIGS = [
     ("dfx_softmax_xent", c_int, [c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
                                  c_void_p]),
     ("dfx_add", c_int, [c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("dfx_bdrln_bwd_finalize", c_int, [c_int, c_int64, c_int64, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p,
+                                       c_void_p]),
     ("dfx_sgd_update", c_int, [c_int64, c_void_p, c_void_p, c_float, c_void_p, c_void_p]),
     ("dfx_scale_f32", c_int, [c_int64, c_void_p, c_float, c_void_p]),
     ("dfx_cast", c_int, [c_int64, c_int, c_void_p, c_int, c_void_p, c_void_p]),

@@ -279,10 +279,13 @@ class BertEncoderLayer:
             side.wait_event(ev)
             return torch.cuda.stream(side)
 
+        # BDRLN backward: the dx half stays on the critical path; the
+        # parameter-gradient finalize (partials in a per-site workspace) forks
+        wsb = self._bdrln_ws(B, S)
         with L("bwd.bdrln2"):
-            K.bdrln_bwd(dout, b["s2"], P["g2"], keep2, ks, c.eps, ds=b["ds2"], dh=b["da2"],
-                        dgamma=G["g2"], dbeta=G["be2"], dbias=G["b2"])
+            K.bdrln_bwd(dout, b["s2"], P["g2"], keep2, ks, c.eps, ds=b["ds2"], dh=b["da2"], ws=wsb[0])
         with fork():
+            K.bdrln_bwd_finalize(dout, wsb[0], G["g2"], G["be2"], G["b2"])
             with L("bwd.ffn2_wgrad"):
                 K.gemm(b["da2"].t(), b["g"].t(), G["w2"])
         # FFN2: dgrad with the GELU-backward epilogue, wgrad straight into f32 grads
@@ -297,9 +300,9 @@ class BertEncoderLayer:
         with L("bwd.ffn1_dgrad+residual"):
             K.gemm(b["dpre"], self.weight("w1").t(), b["dln1"], EPI_ADD, aux=b["ds2"])
         with L("bwd.bdrln1"):
-            K.bdrln_bwd(b["dln1"], b["s1"], P["g1"], keep1, ks, c.eps, ds=b["ds1"], dh=b["da1"],
-                        dgamma=G["g1"], dbeta=G["be1"], dbias=G["bo"])
+            K.bdrln_bwd(b["dln1"], b["s1"], P["g1"], keep1, ks, c.eps, ds=b["ds1"], dh=b["da1"], ws=wsb[1])
         with fork():
+            K.bdrln_bwd_finalize(b["dln1"], wsb[1], G["g1"], G["be1"], G["bo"])
             with L("bwd.out_wgrad"):
                 K.gemm(b["da1"].t(), b["ctx"].t(), G["wo"])
         with L("bwd.out_dgrad"):
@@ -320,6 +323,15 @@ class BertEncoderLayer:
             K.gemm(b["dqkv"], self.weight("wqkv").t(), b["dx"], EPI_ADD, aux=b["ds1"])
         main.wait_stream(side)  # join: every gradient is complete on the caller's stream
         return b["dx"]
+
+    def _bdrln_ws(self, B, S):
+        """Two persistent BDRLN-backward workspaces (one per call site): their
+        partial sums are reduced on the side stream while the main stream runs on."""
+        key = ("bdrln_ws", B, S, self.slot)
+        if key not in self._bufs:
+            n = _lib.load().dfx_bdrln_bwd_workspace(B * S, self.cfg.hidden)
+            self._bufs[key] = [torch.empty(n, dtype=torch.uint8, device=self.device) for _ in range(2)]
+        return self._bufs[key]
 
     def _attn_bwd_unfused(self, b, B, S, keep_attn, ks):
         c, L = self.cfg, K.label

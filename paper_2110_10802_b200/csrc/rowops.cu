@@ -766,6 +766,13 @@ int bdrln_bwd_launch(int nch, int grid, size_t smem, int64_t rows, int64_t cols,
   return DFX_OK;
 }
 
+// partial-set count of the backward (the finalize must use the same one)
+template <typename T, int V> int bdrln_bwd_grid(int64_t rows, int64_t cols, int act) {
+  const int nch = pick_nch((int)(cols / V));
+  const bool wave = sizeof(T) == 2 && act == 0 && rows <= 16 * (int64_t)kMaxColBlocks && nch <= 3;
+  return wave ? (int)((rows + 15) / 16) : grid_for(rows, kWarps, kMaxColBlocks);
+}
+
 template <typename T, int V>
 int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const float* gamma,
                 const uint8_t* keep, float ks, float eps, void* ds, void* dh, float* dgamma,
@@ -906,6 +913,22 @@ int dfx_bdrln_fwd(int dtype, int64_t rows, int64_t cols, const void* h, const fl
 
 size_t dfx_bdrln_bwd_workspace(int64_t rows, int64_t cols) {
   return 3 * colsum_ws_bytes(rows, cols);
+}
+
+int dfx_bdrln_bwd_finalize(int dtype, int64_t rows, int64_t cols, const void* workspace, size_t ws_bytes,
+                           float* dgamma, float* dbeta, float* dbias, void* stream) {
+  DFX_REQUIRE(workspace && rows > 0 && cols > 0, DFX_ERR_SHAPE, "dfx_bdrln_bwd_finalize: bad arguments");
+  int grid;
+  if (dtype == DFX_BF16) grid = bdrln_bwd_grid<__nv_bfloat16, 8>(rows, cols, 0);
+  else if (dtype == DFX_F32) grid = bdrln_bwd_grid<float, 4>(rows, cols, 0);
+  else return fail(DFX_ERR_DTYPE, "dfx_bdrln_bwd_finalize: dtype must be f32 or bf16");
+  DFX_REQUIRE(ws_bytes >= 3 * (size_t)grid * cols * sizeof(float), DFX_ERR_WORKSPACE,
+              "dfx_bdrln_bwd_finalize: workspace too small");
+  if (!(dgamma || dbeta || dbias)) return DFX_OK;
+  launch_k(finalize_colsum_kernel, dim3((unsigned)((cols + 31) / 32), 3), kFinWarps * 32, 0, as_stream(stream), grid,
+           (int)cols, (const float*)workspace, dgamma, dbeta, dbias, 0);
+  DFX_LAUNCH_CHECK("dfx_bdrln_bwd_finalize");
+  return DFX_OK;
 }
 
 int dfx_bdrln_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const void* s_stash,

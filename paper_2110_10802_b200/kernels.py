@@ -203,14 +203,19 @@ def bdrln_fwd(h, bias, keep, keep_scale, residual, gamma, beta, eps, y=None, s=N
 
 
 def bdrln_bwd(dy, s, gamma, keep, keep_scale, eps, ds=None, dh=None, dgamma=None, dbeta=None,
-              dbias=None):
+              dbias=None, ws=None):
+    """``ws``: an explicit workspace (>= dfx_bdrln_bwd_workspace bytes) whose
+    partial sums bdrln_bwd_finalize reduces later (dgamma/dbeta/dbias None)."""
     _contig(dy, "dy")
     cols = dy.shape[-1]
     rows = dy.numel() // cols
     if s.shape != dy.shape or s.dtype != dy.dtype:
         raise ShapeError("bdrln_bwd: stash must match dy")
     ws_n = _lib.load().dfx_bdrln_bwd_workspace(rows, cols)
-    ws = WORKSPACE.get(ws_n)
+    if ws is None:
+        ws = WORKSPACE.get(ws_n)
+    elif ws.numel() < ws_n:
+        raise ShapeError("bdrln_bwd: workspace too small")
     esz = dy.element_size()
     work = lambda: rows * cols * (esz * (2 + (ds is not None) + (dh is not None))  # noqa: E731
                                   + (keep is not None)) + 4 * cols * 4
@@ -219,6 +224,15 @@ def bdrln_bwd(dy, s, gamma, keep, keep_scale, eps, ds=None, dh=None, dgamma=None
                   _vec(gamma, cols, "gamma").data_ptr(), _ptr(_u8(keep, dy.numel(), "keep")),
                   float(keep_scale), float(eps), _ptr(ds), _ptr(dh), _ptr(dgamma), _ptr(dbeta),
                   _ptr(dbias), ws.data_ptr(), ws.numel(), _stream())
+
+
+def bdrln_bwd_finalize(dy_like, ws, dgamma, dbeta, dbias):
+    """dgamma / dbeta / dbias from the partial sums a bdrln_bwd(..., ws=ws) left."""
+    cols = dy_like.shape[-1]
+    rows = dy_like.numel() // cols
+    with _span("bdrln_bwd_finalize", "hbm", lambda: 3 * cols * 4 * 256):
+        _lib.call("dfx_bdrln_bwd_finalize", dfx_dtype(dy_like), rows, cols, ws.data_ptr(), ws.numel(),
+                  _ptr(dgamma), _ptr(dbeta), _ptr(dbias), _stream())
 
 
 # ---------------------------------------------------------------------------
