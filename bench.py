@@ -380,8 +380,10 @@ def measure_effnet_c5(steps, flush, pk, world, rank, local, dist):
         step = cs.replay
 
         timer = K.KernelTimer()
+        net.concurrent = False  # single-stream twin: per-kernel times without branch contention
         with timer:
             inst = CapturedStep(lambda: net.train_step(dev["x"], dev["labels"], lr), warmup=0)
+        net.concurrent = True
         timer.totals = {}
         for _ in range(3):
             flush.zero_()

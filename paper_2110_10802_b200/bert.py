@@ -23,6 +23,7 @@ data-parallel allreduce and the SGD step each touch a single buffer.
 
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass
 
 import torch
@@ -102,6 +103,7 @@ class BertEncoderLayer:
         self.wlow = FlatArena(specs, torch.bfloat16, self.device) if cfg.dtype == torch.bfloat16 else None
         self._bufs = {}
         self.slot = 0  # activation / input buffer set (see train_step_host_async)
+        self.concurrent = True  # weight gradients on a forked stream (backward)
         self._init_params(seed)
 
     # ------------------------------------------------------------ parameters
@@ -274,6 +276,8 @@ class BertEncoderLayer:
         side = self._side
 
         def fork():
+            if not self.concurrent:  # the per-kernel attribution twin runs one stream
+                return contextlib.nullcontext()
             ev = torch.cuda.Event()
             ev.record(main)
             side.wait_event(ev)
@@ -321,7 +325,8 @@ class BertEncoderLayer:
                 K.gemm(b["dqkv"].t(), x.t(), G["wqkv"])
         with L("bwd.qkv_dgrad+residual"):
             K.gemm(b["dqkv"], self.weight("wqkv").t(), b["dx"], EPI_ADD, aux=b["ds1"])
-        main.wait_stream(side)  # join: every gradient is complete on the caller's stream
+        if self.concurrent:
+            main.wait_stream(side)  # join: every gradient is complete on the caller's stream
         return b["dx"]
 
     def _bdrln_ws(self, B, S):
@@ -501,9 +506,15 @@ class BertEncoderLayer:
         if timer is None:
             return CapturedStep(fn)
         cs = CapturedStep(fn)  # warm-up/capture without events, then an instrumented twin
+        # the twin is single-stream: each kernel's events then time that kernel
+        # alone, not its contention with the forked weight-gradient branch
         timer.reset_records()
-        with timer:
-            inst = CapturedStep(fn, warmup=0)
+        self.concurrent = False
+        try:
+            with timer:
+                inst = CapturedStep(fn, warmup=0)
+        finally:
+            self.concurrent = True
         return cs, inst
 
     def device_inputs(self, B: int, S: int) -> dict:

@@ -31,6 +31,7 @@ With a process group every BatchNorm is SyncBN (dp.py).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass
 
@@ -221,6 +222,7 @@ class EfficientNetB0:
         _bind_bn(self.head_bn, self.master, self.grad, "head.g", "head.b")
         self.loss = torch.zeros(1, device=self.device)
         self._pads = (ctypes.c_int * 4)(1, 1, 1, 1)
+        self.concurrent = True  # weight gradients on a forked stream (backward)
         self._bufs = {}
 
     # ------------------------------------------------------------ parameters
@@ -309,6 +311,8 @@ class EfficientNetB0:
         main = torch.cuda.current_stream(self.device)
         if not hasattr(self, "_side"):
             self._side = torch.cuda.Stream(device=self.device)
+        if not self.concurrent:  # per-kernel attribution: one stream
+            return contextlib.nullcontext()
         ev = torch.cuda.Event()
         ev.record(main)
         self._side.wait_event(ev)
@@ -349,7 +353,8 @@ class EfficientNetB0:
         with self.fork(dh):
             with K.label("stem.wgrad"):
                 _gemm(dh.view(-1, c.stem).t(), self.cols.t(), G["stem.w"])
-        torch.cuda.current_stream(self.device).wait_stream(self._side)  # join
+        if self.concurrent:
+            torch.cuda.current_stream(self.device).wait_stream(self._side)  # join
 
     def sgd_step(self, lr: float):
         with K.label("sgd_update"):
