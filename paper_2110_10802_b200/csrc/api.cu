@@ -73,7 +73,10 @@ int dfx_gemm_uses_tensor_cores(const dfx_gemm_args* args) {
 /* debug: per-CTA timeline of the tensor-core GEMM (32 u64 per CTA; NULL = off). */
 __attribute__((visibility("default"))) void dfx_debug_gemm_trace(void* buf) { gemm_tc_set_trace(buf); }
 
-size_t dfx_gemm_workspace(const dfx_gemm_args* args) { return args ? gemm_tc_workspace(*args) : 0; }
+size_t dfx_gemm_workspace(const dfx_gemm_args* args) {
+  if (!args) return 0;
+  return gemm_tc_supported(*args) ? gemm_tc_workspace(*args) : gemm_simt_workspace(*args);
+}
 
 int dfx_gemm(const dfx_gemm_args* args, void* stream) {
   DFX_REQUIRE(args, DFX_ERR_SHAPE, "dfx_gemm: null args");

@@ -7,6 +7,7 @@
 
 namespace dfx {
 int gemm_simt(const dfx_gemm_args& p, cudaStream_t st);
+size_t gemm_simt_workspace(const dfx_gemm_args& p);
 // Returns DFX_OK after launching, or DFX_ERR_UNSUPPORTED (no error recorded)
 // when the shape/layout does not tile for tcgen05.
 bool gemm_tc_supported(const dfx_gemm_args& p);
