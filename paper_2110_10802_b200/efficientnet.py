@@ -369,7 +369,7 @@ class EfficientNetB0:
 
     # ------------------------------------------------------------ graph / host API
     def device_inputs(self, N: int):
-        key = ("in", N)
+        key = ("in", N, getattr(self, "slot", 0))
         if key not in self._bufs:
             s = self.cfg.image
             self._bufs[key] = {"x": torch.zeros(N, s, s, 3, dtype=self.cfg.dtype, device=self.device),
@@ -395,6 +395,49 @@ class EfficientNetB0:
         with timer:
             inst = CapturedStep(fn, warmup=0)
         return cs, inst
+
+    def train_step_host_async(self, x_host, labels_host, lr=None, loss_host=None):
+        """Pipelined host-buffer step (single process): two input sets and two
+        captured graphs alternate, so step i+1's H2D and step i's loss D2H
+        overlap step i's compute.  ``finish_host()`` joins the copy streams."""
+        N = x_host.shape[0]
+        if not hasattr(self, "_pipe"):
+            self._pipe = {"h2d": torch.cuda.Stream(device=self.device), "d2h": torch.cuda.Stream(device=self.device),
+                          "free": [None, None], "graphs": {}}
+        pp = self._pipe
+        slot = getattr(self, "slot", 0)
+        comp = torch.cuda.current_stream(self.device)
+        key = (N, lr, slot)
+        if key not in pp["graphs"]:
+            torch.cuda.synchronize(self.device)
+            pp["graphs"][key] = self.capture_step(N, lr)
+        dev = self.device_inputs(N)
+        with torch.cuda.stream(pp["h2d"]):
+            if pp["free"][slot] is not None:
+                pp["h2d"].wait_event(pp["free"][slot])
+            dev["x"].copy_(x_host, non_blocking=True)
+            dev["labels"].copy_(labels_host, non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(pp["h2d"])
+        comp.wait_event(ev_in)
+        pp["graphs"][key].replay()
+        ev_done = torch.cuda.Event()
+        ev_done.record(comp)
+        with torch.cuda.stream(pp["d2h"]):
+            pp["d2h"].wait_event(ev_done)
+            if loss_host is not None:
+                loss_host.copy_(self.loss, non_blocking=True)
+            ev_free = torch.cuda.Event()
+            ev_free.record(pp["d2h"])
+        pp["free"][slot] = ev_free
+        self.slot = slot ^ 1
+        return loss_host
+
+    def finish_host(self):
+        if hasattr(self, "_pipe"):
+            comp = torch.cuda.current_stream(self.device)
+            comp.wait_stream(self._pipe["h2d"])
+            comp.wait_stream(self._pipe["d2h"])
 
     def host_inputs_bytes(self, N: int):
         s = self.cfg.image
