@@ -34,6 +34,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -83,6 +84,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// keep nibble (4 flags) -> 4 floats {0, v}: the flags enter the packed fp32
+// math as multipliers, one LDS.128 per 4 columns instead of a shift / sign /
+// AND chain per column
+__device__ __forceinline__ void fill_keep_lut(float4* lut, int t, float v) {
+  if (t < 16) lut[t] = make_float4(t & 1 ? v : 0.f, t & 2 ? v : 0.f, t & 4 ? v : 0.f, t & 8 ? v : 0.f);
+}
+
 // Store 8 consecutive bf16 (16 bytes) of row `r`, 16-byte chunk `ch` (0..7)
 // of a [rows x 64] K-major SWIZZLE_128B tile at `tile`.
 __device__ __forceinline__ void st_sw128(uint32_t tile, int r, int ch, uint4 v) {
@@ -124,7 +132,8 @@ struct FwdSmem {
   static constexpr int P2 = V + kMaxSeq * 128;      // P chunks 4..7 (0..3 reuse K)
   static constexpr int MASK = P2 + 4 * QT * 128;    // S floats
   static constexpr int RED = MASK + kMaxSeq * 4;    // [2][4][128] floats
-  static constexpr int BAR = RED + 2 * 4 * QT * 4;  // mbarriers
+  static constexpr int LUT = RED + 2 * 4 * QT * 4;  // keep byte -> 4 bf16-pair masks
+  static constexpr int BAR = LUT + 256 * 16;        // mbarriers
   static constexpr int TOTAL = BAR + 128 + KB;      // + alignment slack
 };
 static_assert(FwdSmem::TOTAL <= 227 * 1024, "attention forward exceeds shared memory");
@@ -237,6 +246,16 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
     const int st = threadIdx.x - 64; // 0..511
     for (int i = st; i < S; i += kSoftWarps * 32)
       mask2[i] = p.add_mask ? p.add_mask[(size_t)b * S + i] * kLog2e : 0.f;
+    // packed keep byte (8 columns) -> AND masks of its 4 bf16 pairs: one
+    // LDS.128 expands 8 flags (instead of per-bit shift/select chains)
+    uint4* klut = reinterpret_cast<uint4*>(smem + FwdSmem::LUT);
+    if (st < 256) {
+      uint32_t m[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        m[w] = (((st >> (2 * w)) & 1) ? 0x0000FFFFu : 0u) | (((st >> (2 * w + 1)) & 1) ? 0xFFFF0000u : 0u);
+      klut[st] = make_uint4(m[0], m[1], m[2], m[3]);
+    }
     // dropout keep flags of this thread's row segment, 32 bytes per chunk
     const size_t rowoff = ((size_t)bh * S + grow) * S;
     const uint4* kp = reinterpret_cast<const uint4*>(p.keep + rowoff);  // 16 columns per uint4
@@ -287,12 +306,17 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
     // applied to O) -> bf16 swizzled smem; keep flags -> packed bits
     float sum = 0.f;
     const int words = S / 32;
+    // the keep-flag format is a compile-time branch: a uniform branch inside
+    // the column loop would split it into basic blocks the scheduler cannot
+    // interleave (each MUFU result then stalls its own block)
+    auto pass2 = [&](auto kbin_c) {
+    constexpr bool KBIN = decltype(kbin_c)::value;
 #pragma unroll 1
     for (int j = 0; j < nj; ++j) {
       float w[32];
       tmem_ld32_nowait(trow + colof(j), w);
       const uint32_t kw[8] = {kv0.x, kv0.y, kv0.z, kv0.w, kv1.x, kv1.y, kv1.z, kv1.w};
-      if (j + 1 < nj && p.keep) {  // next chunk's keep flags
+      if (!KBIN && j + 1 < nj && p.keep) {  // next chunk's keep flags
         kv0 = __ldg(kp + colof(j + 1) / 16);
         kv1 = __ldg(kp + colof(j + 1) / 16 + 1);
       }
@@ -304,6 +328,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
       // columns per instruction; the exps stay on the MUFU pipe
       const float2 sc2x2 = make_float2(p.sc2, p.sc2), nmx2 = make_float2(-mx, -mx);
       float2 sacc = make_float2(0.f, 0.f);
+      uint4 lm;  // masks of the current keep byte (KBIN)
 #pragma unroll
       for (int u = 0; u < 8; ++u) {  // 4 columns per keep word
         const float4 m = mask4[(colof(j) + 4 * u) >> 2];
@@ -311,12 +336,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
         const float2 tb = __ffma2_rn(make_float2(w[4 * u + 2], w[4 * u + 3]), sc2x2, __fadd2_rn(make_float2(m.z, m.w), nmx2));
         const float e0 = ex2(ta.x), e1 = ex2(ta.y), e2 = ex2(tb.x), e3 = ex2(tb.y);
         sacc = __fadd2_rn(sacc, __fadd2_rn(make_float2(e0, e1), make_float2(e2, e3)));
-        if (p.kb_in) {  // bit pair -> 2 x 16-bit lane masks (PRMT from the {0, ~0} byte pool)
-          const uint32_t nib = kbj >> (4 * u);
-          const uint32_t s01 = ((nib & 1u) * 0x0044u) | (((nib >> 1) & 1u) * 0x4400u);
-          const uint32_t s23 = (((nib >> 2) & 1u) * 0x0044u) | (((nib >> 3) & 1u) * 0x4400u);
-          pk[2 * u] = pack_bf16x2(e0, e1) & __byte_perm(0u, 0xFFFFFFFFu, s01);
-          pk[2 * u + 1] = pack_bf16x2(e2, e3) & __byte_perm(0u, 0xFFFFFFFFu, s23);
+        if constexpr (KBIN) {
+          if ((u & 1) == 0) lm = klut[(kbj >> (8 * (u >> 1))) & 0xFFu];
+          pk[2 * u] = pack_bf16x2(e0, e1) & ((u & 1) ? lm.z : lm.x);
+          pk[2 * u + 1] = pack_bf16x2(e2, e3) & ((u & 1) ? lm.w : lm.y);
         } else {
           const uint32_t ff = kw[u] * 0xFFu;  // bytes 0x00 / 0xFF
           pk[2 * u] = pack_bf16x2(e0, e1) & __byte_perm(ff, 0, 0x1100);
@@ -324,7 +347,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
           bits |= keep_nibble(kw[u]) << (4 * u);
         }
       }
-      if (p.kb_in) bits = kbj;
+      if constexpr (KBIN) bits = kbj;
       sum += sacc.x + sacc.y;
       const int col = colof(j);
       const uint32_t tile = p_chunk(sbase, col >> 6);
@@ -333,7 +356,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
       for (int u = 0; u < 4; ++u)
         st_sw128(tile, rl, ch0 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
       if (p.kb_row) {
-        if (!p.kb_in) p.kb_row[((size_t)bh * S + grow) * words + (col >> 5)] = bits;
+        if constexpr (!KBIN) p.kb_row[((size_t)bh * S + grow) * words + (col >> 5)] = bits;
         // transposed: bit i of word [key][q/32] = keep of query (32-row group base + i)
         const uint32_t colword = warp_transpose32(bits, lane);
         p.kb_col[((size_t)bh * S + col + lane) * words + (grow >> 5)] = colword;
@@ -344,6 +367,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_p[j]);
     }
+    };
+    if (p.kb_in)
+      pass2(std::true_type{});
+    else
+      pass2(std::false_type{});
     red_sum[part * QT + rl] = sum;
     named_bar(1, kSoftWarps * 32);
     const float tot = red_sum[rl] + red_sum[QT + rl] + red_sum[2 * QT + rl] + red_sum[3 * QT + rl];
@@ -397,7 +425,8 @@ struct DqSmem {
   static constexpr int DS = V + kMaxSeq * 128;      // [128 x 128] bf16 as 2 x [128 x 64]
   static constexpr int MASK = DS + QT * CH * 2;
   static constexpr int RED = MASK + kMaxSeq * 4;
-  static constexpr int BAR = RED + 4 * QT * 4;
+  static constexpr int LUT = RED + 4 * QT * 4;   // keep nibble -> 4 x {0, ks}
+  static constexpr int BAR = LUT + 16 * 16;
   static constexpr int TOTAL = BAR + 256 + KB;
 };
 static_assert(DqSmem::TOTAL <= 227 * 1024, "attention dq exceeds shared memory");
@@ -411,7 +440,8 @@ struct DkvSmem {
   static constexpr int DS = PD + QT * CH * 2;
   static constexpr int LSE = DS + QT * CH * 2;
   static constexpr int DEL = LSE + kMaxSeq * 4;
-  static constexpr int BAR = DEL + kMaxSeq * 4;
+  static constexpr int LUT = DEL + kMaxSeq * 4;  // keep nibble -> 4 x {0, 1}
+  static constexpr int BAR = LUT + 16 * 16;
   static constexpr int TOTAL = BAR + 256 + KB;
 };
 static_assert(DkvSmem::TOTAL <= 227 * 1024, "attention dkdv exceeds shared memory");
@@ -561,6 +591,8 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
     // D = rowsum(dO ∘ O): each of the 4 warps of a quadrant sums 16 of the 64
     const size_t goff = (size_t)(row0 + grow) * p.ld_ctx + h * DH + part * 16;
     red[part * QT + rl] = dot16_bf16(p.dctx + goff, p.ctx + goff);
+    const float4* klut = reinterpret_cast<const float4*>(smem + DqSmem::LUT);
+    fill_keep_lut(reinterpret_cast<float4*>(smem + DqSmem::LUT), st, p.ks);
     const float lse_c = p.lse[rowi] - __log2f(p.scale);  // folds the 1/divisor into P
     named_bar(1, kSoftWarps * 32);
     const float D = red[rl] + red[QT + rl] + red[2 * QT + rl] + red[3 * QT + rl];
@@ -590,17 +622,17 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
       uint32_t pk[16];
       // packed fp32 pairs: P' = exp2(s*c + mask - lse') ; dS = P' * (dPd*keep*ks - D)
       const float2 sc2x2 = make_float2(p.sc2, p.sc2), nl2 = make_float2(-lse_c, -lse_c);
-      const float2 ks2 = make_float2(p.ks, p.ks), nD2 = make_float2(-D, -D);
+      const float2 nD2 = make_float2(-D, -D);
+      float4 kf;
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         const float2 m = reinterpret_cast<const float2*>(mask2 + key0)[i >> 1];
         const float2 t = __ffma2_rn(make_float2(s[i], s[i + 1]), sc2x2, __fadd2_rn(m, nl2));
         const float2 P = make_float2(ex2(t.x), ex2(t.y));
-        // dPd * keep: the dropped lanes' bits zeroed (0 * ks - D = -D)
-        const uint32_t k0 = 0u - ((bits >> i) & 1u), k1 = 0u - ((bits >> (i + 1)) & 1u);
-        const float2 dpm = make_float2(__uint_as_float(__float_as_uint(dp[i]) & k0),
-                                       __uint_as_float(__float_as_uint(dp[i + 1]) & k1));
-        const float2 d = __fmul2_rn(P, __ffma2_rn(dpm, ks2, nD2));
+        // dPd * keep * ks - D with keep*ks in {0, ks} (dropped: 0 - D = -D)
+        if ((i & 3) == 0) kf = klut[(bits >> i) & 15u];
+        const float2 kk = (i & 3) ? make_float2(kf.z, kf.w) : make_float2(kf.x, kf.y);
+        const float2 d = __fmul2_rn(P, __ffma2_rn(make_float2(dp[i], dp[i + 1]), kk, nD2));
         pk[i >> 1] = pack_bf16x2(d.x, d.y);
       }
       if (j > 0) mbar_wait(bar_dsfree, (j - 1) & 1);
@@ -743,6 +775,8 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
       del_s[i] = p.delta[(size_t)bh * S + i];
     }
     const float mrow = p.add_mask ? p.add_mask[(size_t)b * S + key] * kLog2e : 0.f;
+    const float4* klut = reinterpret_cast<const float4*>(smem + DkvSmem::LUT);
+    fill_keep_lut(reinterpret_cast<float4*>(smem + DkvSmem::LUT), st, 1.f);
     named_bar(1, kSoftWarps * 32);
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const int words = S / 32;
@@ -768,16 +802,17 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
       // packed fp32 pairs.  P' = P / divisor; Pd' = P' * keep (dV is rescaled
       // by ks * divisor); dS = P' * (dPd * keep * ks - D)
       const float2 sc2x2 = make_float2(p.sc2, p.sc2), mrow2 = make_float2(mrow, mrow), ks2 = make_float2(p.ks, p.ks);
+      float4 kf;
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         const float2 l = reinterpret_cast<const float2*>(lse_s + qc0)[i >> 1];
         const float2 dd = reinterpret_cast<const float2*>(del_s + qc0)[i >> 1];
         const float2 t = __ffma2_rn(make_float2(s[i], s[i + 1]), sc2x2, __fadd2_rn(mrow2, make_float2(-l.x, -l.y)));
         const float2 P = make_float2(ex2(t.x), ex2(t.y));
-        const uint32_t k0 = 0u - ((bits >> i) & 1u), k1 = 0u - ((bits >> (i + 1)) & 1u);
-        const float2 pd = make_float2(__uint_as_float(__float_as_uint(P.x) & k0), __uint_as_float(__float_as_uint(P.y) & k1));
-        const float2 dpm = make_float2(__uint_as_float(__float_as_uint(dp[i]) & k0),
-                                       __uint_as_float(__float_as_uint(dp[i + 1]) & k1));
+        if ((i & 3) == 0) kf = klut[(bits >> i) & 15u];
+        const float2 kk = (i & 3) ? make_float2(kf.z, kf.w) : make_float2(kf.x, kf.y);  // keep in {0, 1}
+        const float2 pd = __fmul2_rn(P, kk);
+        const float2 dpm = __fmul2_rn(make_float2(dp[i], dp[i + 1]), kk);
         const float2 ds = __fmul2_rn(P, __ffma2_rn(dpm, ks2, make_float2(-dd.x, -dd.y)));
         pkp[i >> 1] = pack_bf16x2(pd.x, pd.y);
         pks[i >> 1] = pack_bf16x2(ds.x, ds.y);

@@ -17,4 +17,6 @@ void gemm_tc_set_trace(void* buf);
 // 4-D TMA tensor map (gemm_tc.cu): dims (inner..outer) = {d0, d1, nb2, nb1}, strides in elements
 int make_map(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t d1, int64_t s1, int64_t nb2,
              int64_t sb2, int64_t nb1, int64_t sb1, uint32_t box0, uint32_t box1, bool swizzle128);
+int make_map_sw(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t d1, int64_t s1, int64_t nb2,
+                int64_t sb2, int64_t nb1, int64_t sb1, uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz);
 }  // namespace dfx

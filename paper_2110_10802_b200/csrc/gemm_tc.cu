@@ -42,6 +42,13 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle atom row
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = (2 + kEpiWarps) * 32;
+// Epilogue unit geometry (shared with the host, which builds the bulk-store
+// tensor maps): columns per epilogue warp, and bytes per staged unit row.
+__host__ __device__ constexpr int epi_wcols(int bn) { return bn <= 128 ? bn : bn / 4; }
+__host__ __device__ constexpr int epi_ub(int bn, int esz) {
+  return (epi_wcols(bn) * esz) % 64 == 0 ? 64 : ((epi_wcols(bn) * esz) % 32 == 0 ? 32 : 16);
+}
+
 template <int BN, int CG = 1> struct TcCfg {
   // epilogue staging (TMA store source) per epilogue warp, and the smem ring
   // depth: both sized so the CTA uses <= 227 KB
@@ -122,13 +129,19 @@ template <typename TO> __device__ __forceinline__ float gelu_grad_epi(float x) {
 
 // Stage this thread's 16 fp32 values (row `lane`, element offset `e0` within
 // the unit) as TO / read them back.
+// 16-byte chunk permutation of row r: the TMA SWIZZLE_64B (L = 4) / 32B
+// (L = 2) pattern, so a staged unit is also a bulk-tensor-store source; both
+// the row-per-lane writes and the row-wise reads are bank-conflict free.
+template <int L> __device__ __forceinline__ int swz(int r) {
+  return L == 4 ? ((r >> 1) & 3) : (L == 2 ? ((r >> 2) & 1) : 0);
+}
 template <typename TO, int L>
 __device__ __forceinline__ void stage16(uint32_t base, int lane, int e0, const float (&v)[16]) {
   constexpr int EPC = 16 / (int)sizeof(TO);
 #pragma unroll
   for (int j = 0; j < 16 / EPC; ++j) {
     const int chunk = e0 / EPC + j;
-    sts128(base + lane * (L * 16) + ((chunk ^ (lane % L)) * 16), pack4<TO>(&v[j * EPC]));
+    sts128(base + lane * (L * 16) + ((chunk ^ swz<L>(lane)) * 16), pack4<TO>(&v[j * EPC]));
   }
 }
 template <typename TO, int L>
@@ -137,21 +150,7 @@ __device__ __forceinline__ void unstage16(uint32_t base, int lane, int e0, float
 #pragma unroll
   for (int j = 0; j < 16 / EPC; ++j) {
     const int chunk = e0 / EPC + j;
-    unpack4<TO>(lds128(base + lane * (L * 16) + ((chunk ^ (lane % L)) * 16)), &v[j * EPC]);
-  }
-}
-template <typename TO, int L>
-__device__ __forceinline__ void store_unit(uint32_t base, int lane, TO* g, int64_t ld, int64_t m0, int64_t m,
-                                           int64_t n0, int64_t n) {
-  constexpr int EPC = 16 / (int)sizeof(TO);
-  constexpr int RPI = 32 / L;  // rows per instruction
-  const int c = lane % L;
-#pragma unroll
-  for (int it = 0; it < L; ++it) {
-    const int r = it * RPI + lane / L;
-    const uint4 v = lds128(base + r * (L * 16) + ((c ^ (r % L)) * 16));
-    const int64_t gm = m0 + r, gn = n0 + c * EPC;
-    if (gm < m && gn < n) *reinterpret_cast<uint4*>(g + gm * ld + gn) = v;
+    unpack4<TO>(lds128(base + lane * (L * 16) + ((chunk ^ swz<L>(lane)) * 16)), &v[j * EPC]);
   }
 }
 // Coalesced copy global rows -> staged unit (zeros out of range).
@@ -167,7 +166,7 @@ __device__ __forceinline__ void load_unit(uint32_t base, int lane, const TO* g, 
     const int64_t gm = m0 + r, gn = n0 + c * EPC;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (gm < m && gn < n) v = __ldg(reinterpret_cast<const uint4*>(g + gm * ld + gn));
-    sts128(base + r * (L * 16) + ((c ^ (r % L)) * 16), v);
+    sts128(base + r * (L * 16) + ((c ^ swz<L>(r)) * 16), v);
   }
 }
 
@@ -197,6 +196,7 @@ __device__ __forceinline__ TileIdx tile_of(int t, const TcParams& p) {
 template <int BN, typename TO, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+               const __grid_constant__ CUtensorMap map_d, const __grid_constant__ CUtensorMap map_o,
                const TcParams p) {
   pdl_trigger();
   using Cfg = TcCfg<BN, CG>;
@@ -340,10 +340,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // of its quadrant; NACC == 2: all 16 warps share a tile, a quarter each
     const int grp = NACC == 4 ? (ew >> 2) : 0;
     const int part = NACC == 4 ? 0 : ew >> 2;
-    constexpr int WCOLS = NACC == 4 ? BN : BN / 4;  // columns per warp
+    constexpr int WCOLS = epi_wcols(BN);  // columns per warp
+    static_assert(WCOLS == (NACC == 4 ? BN : BN / 4), "epilogue split");
     constexpr int ESZ = (int)sizeof(TO);
     // bytes per row per unit: 64 when the warp's columns tile by it (BN = 192 bf16: 32)
-    constexpr int UB = (WCOLS * ESZ) % 64 == 0 ? 64 : ((WCOLS * ESZ) % 32 == 0 ? 32 : 16);
+    constexpr int UB = epi_ub(BN, ESZ);
     constexpr int L = UB / 16;
     constexpr int UCOLS = UB / ESZ;   // columns per unit (bf16 32, f32 16)
     static_assert(WCOLS % UCOLS == 0, "warp columns must hold whole units");
@@ -352,7 +353,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t st_out = smem_u32(epi_smem + ew * Cfg::EPI_WARP_BYTES);
     const uint32_t st_aux = st_out + 32 * UB;
     const bool unit_alpha = p.alpha == 1.f;
-    uint32_t lt = 0;
+    uint32_t lt = 0, ucount = 0;
     for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++lt) {
       if (NACC == 4 && (int)(lt & 3) != grp) continue;  // another group's tile
       const TileIdx ti = tile_of(t, p);
@@ -362,26 +363,29 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       tc_fence_after();
       if (ew == 0 && lane == 0 && lt < 8) TRACE(11 + lt);
       const int64_t m0 = (int64_t)ti.mb * BM * CG + (int)rank * BM + q * 32;
-      TO* dbase;
-      int64_t dld;
-      if (split_out) {
-        const int64_t nz = p.num_tiles / (p.m_tiles * p.n_tiles * p.splits);
-        dbase = reinterpret_cast<TO*>(p.part + ((int64_t)ti.split * nz + ti.z) * p.m * p.n);
-        dld = p.n;
-      } else {
-        dbase = (TO*)p.d + ti.b1 * p.d_stride_b1 + ti.b2 * p.d_stride_b2;
-        dld = p.d_stride_m;
-      }
+      // bulk-store coordinates beyond (n, m): batch (b2, b1), or (z, split)
+      // of the split-K partials [split][z][m][n]
+      const int sc2 = split_out ? ti.z : ti.b2, sc3 = split_out ? ti.split : ti.b1;
       const TO* xbase = p.aux ? (const TO*)p.aux + ti.b1 * p.aux_stride_b1 + ti.b2 * p.aux_stride_b2 : nullptr;
-      TO* obase = p.aux_out ? (TO*)p.aux_out + ti.b1 * p.aux_out_stride_b1 + ti.b2 * p.aux_out_stride_b2 : nullptr;
       const bool use_aux = !split_out && (p.epilogue == DFX_EPI_GELU_BWD || p.epilogue == DFX_EPI_ADD);
       const bool gelu = !split_out && p.epilogue == DFX_EPI_BIAS_GELU;
       const bool biased = !split_out && (p.epilogue == DFX_EPI_BIAS || gelu) && p.bias != nullptr;
       const bool store_pre = gelu && p.has_aux_out;
+      // output-only units alternate between the warp's two staging slots, so
+      // staging unit u+1 overlaps the bulk store of unit u
+      const bool dbl = !use_aux && !store_pre;
 #pragma unroll 1
-      for (int u = 0; u < UNITS; ++u) {
+      for (int u = 0; u < UNITS; ++u, ++ucount) {
         const int64_t n0 = (int64_t)ti.nb * BN + part * WCOLS + u * UCOLS;
         if (n0 >= p.n) break;
+        const uint32_t so = (dbl && (ucount & 1)) ? st_aux : st_out;
+        if (lane == 0) {  // the slot's previous bulk store has read its source
+          if (dbl)
+            bulk_wait_read<1>();
+          else
+            bulk_wait_read<0>();
+        }
+        __syncwarp();
         if (use_aux) {
           load_unit<TO, L>(st_aux, lane, xbase, p.aux_stride_m, m0, p.m, n0, p.n);
           __syncwarp();
@@ -424,12 +428,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = gelu_epi<TO>(v[i]);
           }
-          stage16<TO, L>(st_out, lane, hc * 16, v);
+          stage16<TO, L>(so, lane, hc * 16, v);
         }
+        // staged unit -> one bulk tensor store (the TMA clips rows >= m / cols >= n)
+        fence_async_smem();
         __syncwarp();
-        if (store_pre) store_unit<TO, L>(st_aux, lane, obase, p.aux_out_stride_m, m0, p.m, n0, p.n);
-        store_unit<TO, L>(st_out, lane, dbase, dld, m0, p.m, n0, p.n);
-        __syncwarp();
+        if (lane == 0) {
+          if (store_pre) tma_store_4d(&map_o, st_aux, (int)n0, (int)m0, sc2, sc3);
+          tma_store_4d(&map_d, so, (int)n0, (int)m0, sc2, sc3);
+          bulk_commit();
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -442,6 +450,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       }
     }
   }
+  if (warp >= 2 && lane == 0) bulk_wait_all();  // this warp's bulk stores are complete
   tc_fence_before();
   if constexpr (CG == 2) {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -551,6 +560,12 @@ EncodeTiledFn encode_fn() {
 // 4-D tensor map: dims (inner..outer) = {d0, d1, nb2, nb1}; strides in elements.
 int make_map(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t d1, int64_t s1, int64_t nb2,
              int64_t sb2, int64_t nb1, int64_t sb1, uint32_t box0, uint32_t box1, bool swizzle128) {
+  return make_map_sw(map, base, esz, d0, d1, s1, nb2, sb2, nb1, sb1, box0, box1,
+                     swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+int make_map_sw(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t d1, int64_t s1, int64_t nb2,
+                int64_t sb2, int64_t nb1, int64_t sb1, uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(DFX_ERR_CUDA, "dfx_gemm: cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[4] = {d0, d1, (cuuint64_t)nb2, (cuuint64_t)nb1};
@@ -561,8 +576,7 @@ int make_map(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t 
   cuuint32_t box[4] = {box0, box1, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(map, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
-                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(DFX_ERR_CUDA, "dfx_gemm: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -649,7 +663,8 @@ Plan plan(const dfx_gemm_args& p) {
 }
 
 template <int BN, typename TO, int CG>
-int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& tp, cudaStream_t st) {
+int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, const CUtensorMap& mo,
+              const TcParams& tp, cudaStream_t st) {
   auto kfn = tc_gemm_kernel<BN, TO, CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -671,24 +686,24 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& tp, 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, tp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, md, mo, tp);
   if (e != cudaSuccess) return fail(DFX_ERR_CUDA, std::string("dfx_gemm (tcgen05) launch: ") + cudaGetErrorString(e));
   DFX_LAUNCH_CHECK("dfx_gemm (tcgen05)");
   return DFX_OK;
 }
 
 template <typename TO>
-int launch_tc_any(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& tp,
-                  cudaStream_t st) {
+int launch_tc_any(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
+                  const CUtensorMap& mo, const TcParams& tp, cudaStream_t st) {
   if (cg == 2) {
-    if (bn == 256) return launch_tc<256, TO, 2>(ma, mb, tp, st);
-    if (bn == 192) return launch_tc<192, TO, 2>(ma, mb, tp, st);
-    return launch_tc<128, TO, 2>(ma, mb, tp, st);
+    if (bn == 256) return launch_tc<256, TO, 2>(ma, mb, md, mo, tp, st);
+    if (bn == 192) return launch_tc<192, TO, 2>(ma, mb, md, mo, tp, st);
+    return launch_tc<128, TO, 2>(ma, mb, md, mo, tp, st);
   }
-  if (bn == 256) return launch_tc<256, TO, 1>(ma, mb, tp, st);
-  if (bn == 192) return launch_tc<192, TO, 1>(ma, mb, tp, st);
-  if (bn == 128) return launch_tc<128, TO, 1>(ma, mb, tp, st);
-  return launch_tc<64, TO, 1>(ma, mb, tp, st);
+  if (bn == 256) return launch_tc<256, TO, 1>(ma, mb, md, mo, tp, st);
+  if (bn == 192) return launch_tc<192, TO, 1>(ma, mb, md, mo, tp, st);
+  if (bn == 128) return launch_tc<128, TO, 1>(ma, mb, md, mo, tp, st);
+  return launch_tc<64, TO, 1>(ma, mb, md, mo, tp, st);
 }
 
 }  // namespace
@@ -773,7 +788,29 @@ int gemm_tc(const dfx_gemm_args& p, cudaStream_t st) {
   tp.part = part;
   tp.trace = g_trace;
   const bool f32 = pl.splits > 1 || p.out_dtype == DFX_F32;
-  rc = f32 ? launch_tc_any<float>(bn, pl.cg, ma, mb, tp, st) : launch_tc_any<__nv_bfloat16>(bn, pl.cg, ma, mb, tp, st);
+  // bulk-store maps of the output (or the split-K partials) and the
+  // pre-activation stash: one 32-row x UB-byte unit per box, swizzled like
+  // the epilogue's staging
+  const int esz = f32 ? 4 : 2;
+  const int ub = epi_ub(bn, esz);
+  const CUtensorMapSwizzle oswz =
+      ub == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : (ub == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE);
+  CUtensorMap md, mo;
+  if (pl.splits > 1)
+    rc = make_map_sw(&md, part, 4, p.n, p.m, p.n, Z, p.m * p.n, pl.splits, Z * p.m * p.n, ub / esz, 32, oswz);
+  else
+    rc = make_map_sw(&md, p.d, esz, p.n, p.m, p.d_stride_m, p.batch2, p.d_stride_b2, p.batch1, p.d_stride_b1,
+                     ub / esz, 32, oswz);
+  if (rc) return rc;
+  if (p.aux_out) {
+    rc = make_map_sw(&mo, p.aux_out, esz, p.n, p.m, p.aux_out_stride_m, p.batch2, p.aux_out_stride_b2, p.batch1,
+                     p.aux_out_stride_b1, ub / esz, 32, oswz);
+    if (rc) return rc;
+  } else {
+    mo = md;
+  }
+  rc = f32 ? launch_tc_any<float>(bn, pl.cg, ma, mb, md, mo, tp, st)
+           : launch_tc_any<__nv_bfloat16>(bn, pl.cg, ma, mb, md, mo, tp, st);
   if (rc || pl.splits <= 1) return rc;
   const int64_t total = Z * p.m * p.n;
   if (pl.splits <= 8 && p.out_dtype == DFX_F32 && Z == 1 && p.d_stride_m == p.n && p.n % 4 == 0 &&

@@ -24,7 +24,11 @@ ctx = torch.empty(B * S, H, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(B, NH, S, device="cuda")
 kr = torch.empty(B, NH, S, S // 32, device="cuda", dtype=torch.int32)
 kc = torch.empty_like(kr)
-if os.environ.get("ATTN_NOKEEP"):  # isolate the dropout-flag traffic
+if os.environ.get("ATTN_KBIN"):  # packed keep flags as input (the BERT step's mode)
+    K.attn_fwd(qkv, B, S, NH, am, keep, 1 / 0.9, 0.125, ctx, lse, kr, kc)
+    kr_in = kr.clone()
+    run = lambda: K.attn_fwd(qkv, B, S, NH, am, None, 1 / 0.9, 0.125, ctx, lse, kr_in, kc)  # noqa: E731
+elif os.environ.get("ATTN_NOKEEP"):  # isolate the dropout-flag traffic
     run = lambda: K.attn_fwd(qkv, B, S, NH, am, None, 1.0, 0.125, ctx, lse, None, None)  # noqa: E731
 else:
     run = lambda: K.attn_fwd(qkv, B, S, NH, am, keep, 1 / 0.9, 0.125, ctx, lse, kr, kc)  # noqa: E731

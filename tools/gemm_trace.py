@@ -25,7 +25,7 @@ for _ in range(3):
     K.gemm(a, b, d)
 tr = torch.zeros(148 * 32, dtype=torch.int64, device="cuda")
 fn(tr.data_ptr())
-K.gemm(a, b, d)
+K.gemm(a, b, d, beta=float(os.environ.get("GT_BETA", "1.0")))
 torch.cuda.synchronize()
 fn(None)
 t = tr.view(148, 32).cpu()
@@ -40,4 +40,4 @@ for c in list(range(0, 148, 16)) + [147]:
     es = [f"{rel(v):6.2f}" for v in r[11:19] if v > 0]
     ee = [f"{rel(v):6.2f}" for v in r[19:27] if v > 0]
     print(f"{c:3d} {rel(r[0]):6.2f} {rel(r[1]):6.2f} {rel(r[2]):6.2f} | {' '.join(mma)} | {' '.join(es)} | "
-          f"{' '.join(ee)} | {rel(r[27]):6.2f}")
+          f"{' '.join(ee)} | {rel(r[27]):6.2f} | t0 epi: ld {rel(r[28]):6.2f} units {rel(r[29]):6.2f} {rel(r[30]):6.2f} {rel(r[31]):6.2f}")
