@@ -64,7 +64,7 @@ template <int BN, int CG = 1> struct TcCfg {
   static constexpr int NACC = BN <= 128 ? 4 : 2;
   static constexpr int TMEM_COLS = NACC * BN < 32 ? 32 : (BN == 192 ? 512 : NACC * BN);
   static constexpr int EPI_BYTES = kEpiWarps * EPI_WARP_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 struct TcParams {
@@ -153,23 +153,6 @@ __device__ __forceinline__ void unstage16(uint32_t base, int lane, int e0, float
     unpack4<TO>(lds128(base + lane * (L * 16) + ((chunk ^ swz<L>(lane)) * 16)), &v[j * EPC]);
   }
 }
-// Coalesced copy global rows -> staged unit (zeros out of range).
-template <typename TO, int L>
-__device__ __forceinline__ void load_unit(uint32_t base, int lane, const TO* g, int64_t ld, int64_t m0, int64_t m,
-                                          int64_t n0, int64_t n) {
-  constexpr int EPC = 16 / (int)sizeof(TO);
-  constexpr int RPI = 32 / L;
-  const int c = lane % L;
-#pragma unroll
-  for (int it = 0; it < L; ++it) {
-    const int r = it * RPI + lane / L;
-    const int64_t gm = m0 + r, gn = n0 + c * EPC;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (gm < m && gn < n) v = __ldg(reinterpret_cast<const uint4*>(g + gm * ld + gn));
-    sts128(base + r * (L * 16) + ((c ^ swz<L>(r)) * 16), v);
-  }
-}
-
 // Decompose a linear tile index: n fastest, then m, then batch, then split.
 struct TileIdx {
   int nb, mb, b1, b2, z, split;
@@ -197,7 +180,7 @@ template <int BN, typename TO, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const __grid_constant__ CUtensorMap map_d, const __grid_constant__ CUtensorMap map_o,
-               const TcParams p) {
+               const __grid_constant__ CUtensorMap map_x, const TcParams p) {
   pdl_trigger();
   using Cfg = TcCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
@@ -211,7 +194,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   constexpr int EPI_GROUP_WARPS = NACC == 4 ? 4 : kEpiWarps;  // warps draining one tile
   uint64_t* tfull = empty + STAGES;  // [NACC]
   uint64_t* tempty = tfull + NACC;   // [NACC]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
+  uint64_t* xbar = tempty + NACC;    // [kEpiWarps]: aux-operand unit landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TRACE(0);
@@ -224,6 +208,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < NACC; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * EPI_GROUP_WARPS); }
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(&xbar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -353,12 +338,29 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t st_out = smem_u32(epi_smem + ew * Cfg::EPI_WARP_BYTES);
     const uint32_t st_aux = st_out + 32 * UB;
     const bool unit_alpha = p.alpha == 1.f;
+    const bool use_aux = p.splits <= 1 && (p.epilogue == DFX_EPI_GELU_BWD || p.epilogue == DFX_EPI_ADD);
+    uint64_t* my_xbar = &xbar[ew];
+    uint32_t xph = 0;  // parity of this warp's next aux unit
+    // aux unit (32 rows x UB bytes) -> st_aux by bulk tensor load; it lands
+    // in the staging layout unstage16 reads
+    auto fetch_aux = [&](int64_t n0, int64_t m0, const TileIdx& ti) {
+      if (lane == 0) {
+        fence_async_smem();  // the slot's previous reads precede the async write
+        mbar_expect_tx(my_xbar, 32 * (uint32_t)UB);
+        tma_load_4d_cg<1>(&map_x, smem_u32(my_xbar), epi_smem + ew * Cfg::EPI_WARP_BYTES + 32 * UB, (int)n0, (int)m0,
+                          ti.b2, ti.b1);
+      }
+    };
     uint32_t lt = 0, ucount = 0;
     for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++lt) {
       if (NACC == 4 && (int)(lt & 3) != grp) continue;  // another group's tile
       const TileIdx ti = tile_of(t, p);
       const int acc = (int)(lt % NACC);
       const uint32_t aph = (lt / NACC) & 1;
+      // the first aux unit does not depend on the accumulator: fetch it
+      // while the tile's MMAs finish
+      if (use_aux && (int64_t)ti.nb * BN + part * WCOLS < p.n)
+        fetch_aux((int64_t)ti.nb * BN + part * WCOLS, (int64_t)ti.mb * BM * CG + (int)rank * BM + q * 32, ti);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       if (ew == 0 && lane == 0 && lt < 8) TRACE(11 + lt);
@@ -366,8 +368,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       // bulk-store coordinates beyond (n, m): batch (b2, b1), or (z, split)
       // of the split-K partials [split][z][m][n]
       const int sc2 = split_out ? ti.z : ti.b2, sc3 = split_out ? ti.split : ti.b1;
-      const TO* xbase = p.aux ? (const TO*)p.aux + ti.b1 * p.aux_stride_b1 + ti.b2 * p.aux_stride_b2 : nullptr;
-      const bool use_aux = !split_out && (p.epilogue == DFX_EPI_GELU_BWD || p.epilogue == DFX_EPI_ADD);
       const bool gelu = !split_out && p.epilogue == DFX_EPI_BIAS_GELU;
       const bool biased = !split_out && (p.epilogue == DFX_EPI_BIAS || gelu) && p.bias != nullptr;
       const bool store_pre = gelu && p.has_aux_out;
@@ -379,6 +379,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const int64_t n0 = (int64_t)ti.nb * BN + part * WCOLS + u * UCOLS;
         if (n0 >= p.n) break;
         const uint32_t so = (dbl && (ucount & 1)) ? st_aux : st_out;
+        // the unit's accumulator columns: loads issued first, so their latency
+        // overlaps the staging-slot wait and the aux fetch
+        float vu[UCOLS];
+        {
+          const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + part * WCOLS + u * UCOLS;
+#pragma unroll
+          for (int hc = 0; hc < UCOLS / 16; ++hc) tmem_ld16_nowait(ta + hc * 16, vu + hc * 16);
+        }
         if (lane == 0) {  // the slot's previous bulk store has read its source
           if (dbl)
             bulk_wait_read<1>();
@@ -387,14 +395,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
         __syncwarp();
         if (use_aux) {
-          load_unit<TO, L>(st_aux, lane, xbase, p.aux_stride_m, m0, p.m, n0, p.n);
-          __syncwarp();
+          mbar_wait(my_xbar, xph);
+          xph ^= 1;
         }
+        tmem_wait_ld();
 #pragma unroll
         for (int hc = 0; hc < UCOLS / 16; ++hc) {
           const int col = part * WCOLS + u * UCOLS + hc * 16;  // column within the tile
           float v[16];
-          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = vu[hc * 16 + i];
           if (!unit_alpha) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] *= p.alpha;
@@ -438,6 +448,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
           tma_store_4d(&map_d, so, (int)n0, (int)m0, sc2, sc3);
           bulk_commit();
         }
+        // st_aux has been read: the next unit's aux streams in under this store
+        if (use_aux && u + 1 < UNITS && n0 + UCOLS < p.n) fetch_aux(n0 + UCOLS, m0, ti);
       }
       tc_fence_before();
       __syncwarp();
@@ -664,7 +676,7 @@ Plan plan(const dfx_gemm_args& p) {
 
 template <int BN, typename TO, int CG>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, const CUtensorMap& mo,
-              const TcParams& tp, cudaStream_t st) {
+              const CUtensorMap& mx, const TcParams& tp, cudaStream_t st) {
   auto kfn = tc_gemm_kernel<BN, TO, CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -686,7 +698,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& m
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, md, mo, tp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, md, mo, mx, tp);
   if (e != cudaSuccess) return fail(DFX_ERR_CUDA, std::string("dfx_gemm (tcgen05) launch: ") + cudaGetErrorString(e));
   DFX_LAUNCH_CHECK("dfx_gemm (tcgen05)");
   return DFX_OK;
@@ -694,16 +706,16 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& m
 
 template <typename TO>
 int launch_tc_any(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
-                  const CUtensorMap& mo, const TcParams& tp, cudaStream_t st) {
+                  const CUtensorMap& mo, const CUtensorMap& mx, const TcParams& tp, cudaStream_t st) {
   if (cg == 2) {
-    if (bn == 256) return launch_tc<256, TO, 2>(ma, mb, md, mo, tp, st);
-    if (bn == 192) return launch_tc<192, TO, 2>(ma, mb, md, mo, tp, st);
-    return launch_tc<128, TO, 2>(ma, mb, md, mo, tp, st);
+    if (bn == 256) return launch_tc<256, TO, 2>(ma, mb, md, mo, mx, tp, st);
+    if (bn == 192) return launch_tc<192, TO, 2>(ma, mb, md, mo, mx, tp, st);
+    return launch_tc<128, TO, 2>(ma, mb, md, mo, mx, tp, st);
   }
-  if (bn == 256) return launch_tc<256, TO, 1>(ma, mb, md, mo, tp, st);
-  if (bn == 192) return launch_tc<192, TO, 1>(ma, mb, md, mo, tp, st);
-  if (bn == 128) return launch_tc<128, TO, 1>(ma, mb, md, mo, tp, st);
-  return launch_tc<64, TO, 1>(ma, mb, md, mo, tp, st);
+  if (bn == 256) return launch_tc<256, TO, 1>(ma, mb, md, mo, mx, tp, st);
+  if (bn == 192) return launch_tc<192, TO, 1>(ma, mb, md, mo, mx, tp, st);
+  if (bn == 128) return launch_tc<128, TO, 1>(ma, mb, md, mo, mx, tp, st);
+  return launch_tc<64, TO, 1>(ma, mb, md, mo, mx, tp, st);
 }
 
 }  // namespace
@@ -737,6 +749,8 @@ bool gemm_tc_supported(const dfx_gemm_args& p) {
   if (p.n % ovec || p.d_stride_m % ovec) return false;  // TMA store: 16-byte row strides
   if ((p.batch2 > 1 && p.d_stride_b2 % ovec) || (p.batch1 > 1 && p.d_stride_b1 % ovec)) return false;
   if (p.aux && ((p.aux_stride_m * osz) % 16 || !aligned16(p.aux))) return false;
+  if (p.aux && ((p.batch2 > 1 && p.aux_stride_b2 % ovec) || (p.batch1 > 1 && p.aux_stride_b1 % ovec)))
+    return false;  // bulk-tensor aux loads: 16-byte batch strides
   if (p.aux_out && (p.aux_out_stride_m % ovec || !aligned16(p.aux_out) ||
                     (p.batch2 > 1 && p.aux_out_stride_b2 % ovec) || (p.batch1 > 1 && p.aux_out_stride_b1 % ovec)))
     return false;
@@ -809,8 +823,14 @@ int gemm_tc(const dfx_gemm_args& p, cudaStream_t st) {
   } else {
     mo = md;
   }
-  rc = f32 ? launch_tc_any<float>(bn, pl.cg, ma, mb, md, mo, tp, st)
-           : launch_tc_any<__nv_bfloat16>(bn, pl.cg, ma, mb, md, mo, tp, st);
+  CUtensorMap mx = md;  // aux operand (residual / GELU input), read per unit by bulk tensor loads
+  if (p.aux && pl.splits <= 1 && (p.epilogue == DFX_EPI_GELU_BWD || p.epilogue == DFX_EPI_ADD)) {
+    rc = make_map_sw(&mx, p.aux, esz, p.n, p.m, p.aux_stride_m, p.batch2, p.aux_stride_b2, p.batch1,
+                     p.aux_stride_b1, ub / esz, 32, oswz);
+    if (rc) return rc;
+  }
+  rc = f32 ? launch_tc_any<float>(bn, pl.cg, ma, mb, md, mo, mx, tp, st)
+           : launch_tc_any<__nv_bfloat16>(bn, pl.cg, ma, mb, md, mo, mx, tp, st);
   if (rc || pl.splits <= 1) return rc;
   const int64_t total = Z * p.m * p.n;
   if (pl.splits <= 8 && p.out_dtype == DFX_F32 && Z == 1 && p.d_stride_m == p.n && p.n % 4 == 0 &&
