@@ -464,27 +464,10 @@ __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* g, const float (&o)
   dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
-__device__ __forceinline__ float dot16_bf16(const __nv_bfloat16* a, const __nv_bfloat16* b) {
-  float s = 0.f;
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const uint4 x = __ldg(reinterpret_cast<const uint4*>(a) + u), y = __ldg(reinterpret_cast<const uint4*>(b) + u);
-    const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&x);
-    const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&y);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 fx = __bfloat1622float2(hx[i]), fy = __bfloat1622float2(hy[i]);
-      s = fmaf(fx.x, fy.x, s);
-      s = fmaf(fx.y, fy.y, s);
-    }
-  }
-  return s;
-}
-
 // dQ strip: CTA = (b, h, 128-query block); loops over 128-key chunks.
 __global__ void __launch_bounds__(kAttnThreads, 1)
 attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
-                   const AttnBwdParams p) {
+                   const __grid_constant__ CUtensorMap map_o, const AttnBwdParams p) {
   pdl_trigger();
   // dynamic smem opens the CTA's window (no static smem in this kernel): it is
   // 1024-B aligned, and indexing it directly keeps every access LDS/STS
@@ -528,13 +511,18 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(bar_q, 2 * QT * 128);
+      // Q, dO, and O (parked in the dS buffer until D = rowsum(dO∘O) is formed)
+      mbar_expect_tx(bar_q, 3 * QT * 128);
       const uint32_t bq = smem_u32(bar_q);
       for (int u = 0; u < 2; ++u) {
         tma_load_4d_cg<1>(&map_qkv, bq, smem + DqSmem::Q + u * 8 * KB, h * DH, row0 + q0 + 64 * u, 0, 0);
         tma_load_4d_cg<1>(&map_do, bq, smem + DqSmem::DO + u * 8 * KB, h * DH, row0 + q0 + 64 * u, 0, 0);
+        tma_load_4d_cg<1>(&map_o, bq, smem + DqSmem::DS + u * 8 * KB, h * DH, row0 + q0 + 64 * u, 0, 0);
       }
       for (int j = 0; j < nch; ++j) {
+        // at most two K/V chunks in flight: the first chunk is not slowed by
+        // the rest of the strip's loads (every SM fetches at once at start)
+        if (j >= 2) mbar_wait(&bar_kv[j - 2], 0);
         mbar_expect_tx(&bar_kv[j], 2 * CH * 128);
         const uint32_t bk = smem_u32(&bar_kv[j]);
         for (int u = 0; u < 2; ++u) {
@@ -586,17 +574,35 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
     const int rl = q * 32 + lane, grow = q0 + rl;
     const int st = threadIdx.x - 64;
     const size_t rowi = (size_t)bh * S + grow;
+    const float lse_c = p.lse[rowi] - __log2f(p.scale);  // folds the 1/divisor into P
     for (int i = st; i < S; i += kSoftWarps * 32)
       mask2[i] = p.add_mask ? p.add_mask[(size_t)b * S + i] * kLog2e : 0.f;
-    // D = rowsum(dO ∘ O): each of the 4 warps of a quadrant sums 16 of the 64
-    const size_t goff = (size_t)(row0 + grow) * p.ld_ctx + h * DH + part * 16;
-    red[part * QT + rl] = dot16_bf16(p.dctx + goff, p.ctx + goff);
     const float4* klut = reinterpret_cast<const float4*>(smem + DqSmem::LUT);
     fill_keep_lut(reinterpret_cast<float4*>(smem + DqSmem::LUT), st, p.ks);
-    const float lse_c = p.lse[rowi] - __log2f(p.scale);  // folds the 1/divisor into P
+    // D = rowsum(dO ∘ O) from the TMA-staged tiles (SW128 rows): each of the
+    // 4 warps of a quadrant sums 16 of the 64 columns (chunks 2*part, +1)
+    mbar_wait(bar_q, 0);
+    {
+      float dsum = 0.f;
+#pragma unroll
+      for (int c = 2 * part; c < 2 * part + 2; ++c) {
+        const uint32_t off = rl * 128 + ((c ^ (rl & 7)) << 4);
+        const uint4 x = lds128(sbase + DqSmem::DO + off), y = lds128(sbase + DqSmem::DS + off);
+        const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&x);
+        const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 fx = __bfloat1622float2(hx[i]), fy = __bfloat1622float2(hy[i]);
+          dsum = fmaf(fx.x, fy.x, dsum);
+          dsum = fmaf(fx.y, fy.y, dsum);
+        }
+      }
+      red[part * QT + rl] = dsum;
+    }
     named_bar(1, kSoftWarps * 32);
     const float D = red[rl] + red[QT + rl] + red[2 * QT + rl] + red[3 * QT + rl];
     if (part == 0) p.delta[rowi] = D;
+    if (sw == 0 && lane == 0) ATRACE(12);
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const int words = S / 32;
     // this thread's packed keep words for every chunk, fetched before the
@@ -924,10 +930,12 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   DFX_REQUIRE(workspace && ws_bytes >= dfx_attn_bwd_workspace(batch, heads, seq) && aligned16(workspace),
               DFX_ERR_WORKSPACE, "dfx_attn_bwd: needs dfx_attn_bwd_workspace() bytes of workspace");
   const int64_t T = batch * seq;
-  CUtensorMap mqkv, mdo;
+  CUtensorMap mqkv, mdo, mo;
   rc = make_map(&mqkv, qkv, 2, (uint64_t)ld_qkv, (uint64_t)T, ld_qkv, 1, 0, 1, 0, 64, 64, true);
   if (rc) return rc;
   rc = make_map(&mdo, dctx, 2, (uint64_t)ld_ctx, (uint64_t)T, ld_ctx, 1, 0, 1, 0, 64, 64, true);
+  if (rc) return rc;
+  rc = make_map(&mo, ctx, 2, (uint64_t)ld_ctx, (uint64_t)T, ld_ctx, 1, 0, 1, 0, 64, 64, true);
   if (rc) return rc;
   AttnBwdParams p;
   p.trace = nullptr;
@@ -950,7 +958,7 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   }
   const int grid = (int)(batch * heads * (seq / QT));
   p.trace = g_attn_trace;  // debug timeline of the dq kernel (tools/attn_trace.py --bwd)
-  launch_k(attn_bwd_dq_kernel, grid, kAttnThreads, DqSmem::TOTAL, as_stream(stream), mqkv, mdo, p);
+  launch_k(attn_bwd_dq_kernel, grid, kAttnThreads, DqSmem::TOTAL, as_stream(stream), mqkv, mdo, mo, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dq)");
   p.trace = nullptr;
   launch_k(attn_bwd_dkdv_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, p);

@@ -53,6 +53,8 @@ if "--bwd" in sys.argv:  # dq kernel timeline: 0 start, 1 Q/dO landed (MMA), 2-5
     names = ["start->qdo", "qdo->S0", "S0->S1", "S1->S2", "S2->S3", "S3->dS0", "dS0->dS1", "dS1->dS2", "dS2->dS3",
              "dS3->dQ", "dQ->exit"]
     print("dq mean phase durations (us):", {n: round(d[:, i].mean().item(), 2) for i, n in enumerate(names)})
+    print("dq softmax prologue done (us after start):", round((rel[:, 12] - rel[:, 0]).mean().item(), 2),
+          "MMA saw Q/dO:", round((rel[:, 1] - rel[:, 0]).mean().item(), 2))
     print("dq per-CTA total mean", (rel[:, 11] - rel[:, 0]).mean().item(), "kernel span", rel[:, 11].max().item())
     sys.exit(0)
 tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
