@@ -434,9 +434,10 @@ static_assert(DqSmem::TOTAL <= 227 * 1024, "attention dq exceeds shared memory")
 struct DkvSmem {
   static constexpr int K = 0;
   static constexpr int V = K + QT * 128;
-  static constexpr int RING = V + QT * 128;          // 2 stages x (Q_j, dO_j)
+  static constexpr int NST = 2;                      // ring depth (3 measured slower)
+  static constexpr int RING = V + QT * 128;          // NST stages x (Q_j, dO_j)
   static constexpr int STAGE = 2 * CH * 128;
-  static constexpr int PD = RING + 2 * STAGE;
+  static constexpr int PD = RING + NST * STAGE;
   static constexpr int DS = PD + QT * CH * 2;
   static constexpr int LSE = DS + QT * CH * 2;
   static constexpr int DEL = LSE + kMaxSeq * 4;
@@ -574,6 +575,15 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
     const int rl = q * 32 + lane, grow = q0 + rl;
     const int st = threadIdx.x - 64;
     const size_t rowi = (size_t)bh * S + grow;
+    const int words = S / 32;
+    // this thread's packed keep words for every chunk, issued first: their
+    // latency overlaps the prologue (not a global-latency stall per chunk)
+    uint32_t kbw[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    if (p.kb_row) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < nch) kbw[j] = __ldg(p.kb_row + rowi * words + ((j * CH + part * 32) >> 5));
+    }
     const float lse_c = p.lse[rowi] - __log2f(p.scale);  // folds the 1/divisor into P
     for (int i = st; i < S; i += kSoftWarps * 32)
       mask2[i] = p.add_mask ? p.add_mask[(size_t)b * S + i] * kLog2e : 0.f;
@@ -604,15 +614,6 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
     if (part == 0) p.delta[rowi] = D;
     if (sw == 0 && lane == 0) ATRACE(12);
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    const int words = S / 32;
-    // this thread's packed keep words for every chunk, fetched before the
-    // first S chunk lands (not a global-latency stall per chunk)
-    uint32_t kbw[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    if (p.kb_row) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < nch) kbw[j] = __ldg(p.kb_row + rowi * words + ((j * CH + part * 32) >> 5));
-    }
     for (int j = 0; j < nch; ++j) {
       mbar_wait(bar_s, j & 1);
       tc_fence_after();
@@ -676,9 +677,10 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + DkvSmem::BAR);
   uint64_t *bar_a = bar, *bar_s = bar + 1, *bar_tfree = bar + 2, *bar_pds = bar + 3, *bar_pdsfree = bar + 4;
-  uint64_t* full = bar + 8;    // [2]
-  uint64_t* empty = bar + 10;  // [2]
+  uint64_t* full = bar + 8;    // [NST]
+  uint64_t* empty = bar + 12;  // [NST]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  constexpr int NST = DkvSmem::NST;
   float* lse_s = reinterpret_cast<float*>(smem + DkvSmem::LSE);
   float* del_s = reinterpret_cast<float*>(smem + DkvSmem::DEL);
 
@@ -695,7 +697,7 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
     mbar_init(bar_tfree, kSoftWarps);
     mbar_init(bar_pds, kSoftWarps);
     mbar_init(bar_pdsfree, 1);
-    for (int s = 0; s < 2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -708,19 +710,23 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // setup above overlapped the previous kernel's tail
+  if (threadIdx.x == 0) ATRACE(0);
   constexpr uint32_t T_S = 0, T_DP = 128, T_DK = 256, T_DV = 320;
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(bar_a, 2 * QT * 128);
+      // K, V strips and the head's lse / D rows (bulk copies)
+      mbar_expect_tx(bar_a, 2 * QT * 128 + 2 * S * 4);
       const uint32_t ba = smem_u32(bar_a);
+      bulk_g2s(lse_s, p.lse + (size_t)bh * S, S * 4, ba);
+      bulk_g2s(del_s, p.delta + (size_t)bh * S, S * 4, ba);
       for (int u = 0; u < 2; ++u) {
         tma_load_4d_cg<1>(&map_qkv, ba, smem + DkvSmem::K + u * 8 * KB, p.H + h * DH, row0 + k0 + 64 * u, 0, 0);
         tma_load_4d_cg<1>(&map_qkv, ba, smem + DkvSmem::V + u * 8 * KB, 2 * p.H + h * DH, row0 + k0 + 64 * u, 0, 0);
       }
       for (int j = 0; j < nch; ++j) {
-        const int s = j & 1;
-        mbar_wait(&empty[s], ((j >> 1) & 1) ^ 1);
+        const int s = j % NST;
+        mbar_wait(&empty[s], ((j / NST) & 1) ^ 1);
         mbar_expect_tx(&full[s], DkvSmem::STAGE);
         const uint32_t bf = smem_u32(&full[s]);
         uint8_t* stq = smem + DkvSmem::RING + s * DkvSmem::STAGE;
@@ -737,10 +743,11 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
       const uint64_t kdesc = make_sdesc(sbase + DkvSmem::K, 16, 1024);
       const uint64_t vdesc = make_sdesc(sbase + DkvSmem::V, 16, 1024);
       mbar_wait(bar_a, 0);
+      ATRACE(1);
       auto issue_grads = [&](int j) {  // dV += Pdᵀ·dO_j ; dK += dSᵀ·Q_j   (B operands MN-major)
         mbar_wait(bar_pds, j & 1);
         tc_fence_after();
-        const uint32_t stq = sbase + DkvSmem::RING + (j & 1) * DkvSmem::STAGE;
+        const uint32_t stq = sbase + DkvSmem::RING + (j % NST) * DkvSmem::STAGE;
         const uint64_t qmn = make_sdesc(stq, 8 * KB, 1024);
         const uint64_t domn = make_sdesc(stq + CH * 128, 8 * KB, 1024);
 #pragma unroll
@@ -751,14 +758,14 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
           tc_mma_cg<1>(tmem + T_DV, pd + 2 * (kc & 3), domn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
           tc_mma_cg<1>(tmem + T_DK, ds + 2 * (kc & 3), qmn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
         }
-        tc_commit_cg<1>(&empty[j & 1]);
+        tc_commit_cg<1>(&empty[j % NST]);
         tc_commit_cg<1>(bar_pdsfree);
       };
       for (int j = 0; j < nch; ++j) {
-        mbar_wait(&full[j & 1], (j >> 1) & 1);
+        mbar_wait(&full[j % NST], (j / NST) & 1);
         if (j > 0) mbar_wait(bar_tfree, (j - 1) & 1);
         tc_fence_after();
-        const uint32_t stq = sbase + DkvSmem::RING + (j & 1) * DkvSmem::STAGE;
+        const uint32_t stq = sbase + DkvSmem::RING + (j % NST) * DkvSmem::STAGE;
         const uint64_t qdesc = make_sdesc(stq, 16, 1024);
         const uint64_t dodesc = make_sdesc(stq + CH * 128, 16, 1024);
 #pragma unroll
@@ -775,26 +782,27 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
     const int sw = warp - 2, q = warp & 3, part = sw >> 2;
     const int rl = q * 32 + lane, key = k0 + rl;
     const int st = threadIdx.x - 64;
-    const float lsc = __log2f(p.scale);
-    for (int i = st; i < S; i += kSoftWarps * 32) {
-      lse_s[i] = p.lse[(size_t)bh * S + i] - lsc;  // P' = P / divisor
-      del_s[i] = p.delta[(size_t)bh * S + i];
-    }
-    const float mrow = p.add_mask ? p.add_mask[(size_t)b * S + key] * kLog2e : 0.f;
-    const float4* klut = reinterpret_cast<const float4*>(smem + DkvSmem::LUT);
-    fill_keep_lut(reinterpret_cast<float4*>(smem + DkvSmem::LUT), st, 1.f);
-    named_bar(1, kSoftWarps * 32);
-    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const int words = S / 32;
     const size_t keyi = (size_t)bh * S + key;
-    uint32_t kbw[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};  // prefetched (see dq)
+    // packed keep words, issued first so their latency overlaps the prologue
+    uint32_t kbw[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
     if (p.kb_col) {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (j < nch) kbw[j] = __ldg(p.kb_col + keyi * words + ((j * CH + part * 32) >> 5));
     }
+    const float mraw = p.add_mask ? __ldg(p.add_mask + (size_t)b * S + key) : 0.f;  // consumed after the waits
+    const float4* klut = reinterpret_cast<const float4*>(smem + DkvSmem::LUT);
+    fill_keep_lut(reinterpret_cast<float4*>(smem + DkvSmem::LUT), st, 1.f);
+    named_bar(1, kSoftWarps * 32);
+    mbar_wait(bar_a, 0);  // lse / D rows landed (with K, V)
+    // P' = P / divisor: the divisor's log2 folds into the row mask term
+    const float mrow = mraw * kLog2e + __log2f(p.scale);
+    if (sw == 0 && lane == 0) ATRACE(12);
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     for (int j = 0; j < nch; ++j) {
       mbar_wait(bar_s, j & 1);
+      if (sw == 0 && lane == 0 && j < 4) ATRACE(2 + j);
       tc_fence_after();
       float s[32], dp[32];
       tmem_ld32(trow + T_S + part * 32, s);
@@ -830,8 +838,10 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_pds);
+      if (sw == 0 && lane == 0 && j < 4) ATRACE(6 + j);
     }
     mbar_wait(bar_pdsfree, (nch - 1) & 1);
+    if (sw == 0 && lane == 0) ATRACE(10);
     tc_fence_after();
     float o[16];
     __nv_bfloat16* grow_ptr = p.dqkv + (size_t)(row0 + key) * p.ld_dqkv + h * DH + part * 16;
@@ -957,10 +967,12 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
     attr = true;
   }
   const int grid = (int)(batch * heads * (seq / QT));
-  p.trace = g_attn_trace;  // debug timeline of the dq kernel (tools/attn_trace.py --bwd)
+  // debug timeline of the dq kernel, or of dkdv with DFX_ATTN_TRACE_DKDV set (tools/attn_trace.py)
+  const bool trace_dkdv = getenv("DFX_ATTN_TRACE_DKDV") != nullptr;
+  p.trace = trace_dkdv ? nullptr : g_attn_trace;
   launch_k(attn_bwd_dq_kernel, grid, kAttnThreads, DqSmem::TOTAL, as_stream(stream), mqkv, mdo, mo, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dq)");
-  p.trace = nullptr;
+  p.trace = trace_dkdv ? g_attn_trace : nullptr;
   launch_k(attn_bwd_dkdv_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dk, dv)");
   return DFX_OK;

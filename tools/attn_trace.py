@@ -35,6 +35,9 @@ else:
 for _ in range(3):
     run()
 ncta = B * NH * S // 128
+if "--dkdv" in sys.argv:  # dkdv timeline: 0 start, 1 K/V landed (MMA), 2-5 S_j ready, 6-9 Pd/dS_j stored, 10 grads done
+    os.environ["DFX_ATTN_TRACE_DKDV"] = "1"
+    sys.argv.append("--bwd")
 if "--bwd" in sys.argv:  # dq kernel timeline: 0 start, 1 Q/dO landed (MMA), 2-5 S_j ready, 6-9 dS_j done, 10 dQ done, 11 exit
     run()
     dctx = torch.randn_like(ctx)
