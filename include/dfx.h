@@ -78,6 +78,15 @@ int dfx_bdrln_fwd(int dtype, int64_t rows, int64_t cols, const void* h, const fl
                   const float* gamma, const float* beta, float eps, void* y, void* s_stash,
                   float* mean, float* rstd, void* stream);
 
+/* Same, with the keep flags bit-packed: bit e % 32 of keep_bits[e / 32] is the
+ * keep flag of flat element e = row * cols + col (kernels.pack_keep_bits over
+ * the last axis; rows * cols % 32 == 0).  8x fewer mask bytes over PCIe and
+ * HBM than the u8 form; results are identical. */
+int dfx_bdrln_fwd_kb(int dtype, int64_t rows, int64_t cols, const void* h, const float* bias,
+                     const uint32_t* keep_bits, float keep_scale, const void* residual,
+                     const float* gamma, const float* beta, float eps, void* y, void* s_stash,
+                     float* mean, float* rstd, void* stream);
+
 /* ---- a3: backward of the above -------------------------------------------
  * LN VJP (autodiff.py:1490-1545): ds = rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat))
  * dh = ds * keep * keep_scale ; dgamma = sum_rows dy*xhat ; dbeta = sum_rows dy ;
@@ -88,6 +97,11 @@ int dfx_bdrln_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const v
                   const float* gamma, const uint8_t* keep, float keep_scale, float eps,
                   void* ds, void* dh, float* dgamma, float* dbeta, float* dbias, void* workspace,
                   size_t ws_bytes, void* stream);
+/* dfx_bdrln_bwd with bit-packed keep flags (layout as dfx_bdrln_fwd_kb). */
+int dfx_bdrln_bwd_kb(int dtype, int64_t rows, int64_t cols, const void* dy, const void* s_stash,
+                     const float* gamma, const uint32_t* keep_bits, float keep_scale, float eps,
+                     void* ds, void* dh, float* dgamma, float* dbeta, float* dbias, void* workspace,
+                     size_t ws_bytes, void* stream);
 /* The parameter-gradient half of dfx_bdrln_bwd as its own launch: call
  * dfx_bdrln_bwd with dgamma = dbeta = dbias = NULL (it leaves the per-block
  * partial sums in `workspace`), then this — possibly on another stream, after

@@ -54,7 +54,13 @@ _SIGS = [
     ("dfx_bdrln_fwd", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_float,
                               c_void_p, c_void_p, c_void_p, c_float, c_void_p, c_void_p, c_void_p,
                               c_void_p, c_void_p]),
+    ("dfx_bdrln_fwd_kb", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_float,
+                                 c_void_p, c_void_p, c_void_p, c_float, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_void_p]),
     ("dfx_bdrln_bwd_workspace", c_size_t, [c_int64, c_int64]),
+    ("dfx_bdrln_bwd_kb", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_float, c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_size_t, c_void_p]),
     ("dfx_bdrln_bwd", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                               c_float, c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                               c_void_p, c_size_t, c_void_p]),

@@ -81,6 +81,16 @@ class FlatArena:
         return self.views[name]
 
 
+def _check_host(dev: dict, host: dict):
+    """Host input buffers must already be in the device buffers' form: a u8
+    mask copied into a packed int32 buffer would be converted, not packed."""
+    for k, d in dev.items():
+        h = host[k]
+        if h.dtype != d.dtype or h.shape != d.shape:
+            hint = " (pack keep flags with kernels.pack_keep_bits)" if d.dtype == torch.int32 else ""
+            raise ShapeError(f"host input {k}: expected {d.dtype} {tuple(d.shape)}, got {h.dtype} {tuple(h.shape)}{hint}")
+
+
 def _numel(shape):
     n = 1
     for d in shape:
@@ -212,7 +222,8 @@ class BertEncoderLayer:
     def forward(self, x, add_mask, keep_attn, keep1, keep2):
         """x [T, H] (T = B*S); add_mask f32 [B, S]; keep_* u8 dropout keep flags
         ([B, NH, S, S], [T, H], [T, H]); keep_attn may instead be the packed
-        int32 [B, NH, S, S/32] form (kernels.pack_keep_bits, fused path only).
+        int32 [B, NH, S, S/32] form (kernels.pack_keep_bits, fused path only),
+        keep1 / keep2 the packed int32 [T, H/32] form (any path).
         Returns the layer output [T, H]."""
         c = self.cfg
         B, S = add_mask.shape
@@ -377,12 +388,13 @@ class BertEncoderLayer:
         e = torch.tensor([], dtype=c.dtype).element_size()
         th, tf, t3 = T * H * e, T * F * e, T * 3 * H * e
         bits = B * NH * S * S // 8
+        kb = T * H // 8 if self._fused(S) and H % 32 == 0 else T * H  # BDRLN keep flags (packed or u8)
         w = lambda n, k: n * k * e  # noqa: E731  (bf16 weight operand)
         g32 = lambda n, k: n * k * 4  # noqa: E731  (f32 weight gradient)
         fwd = (th + w(3 * H, H) + t3) + (t3 + bits + th + bits + B * NH * S * 4) + (th + w(H, H) + th) \
-            + (2 * th + T * H + 2 * th) + (th + w(F, H) + 2 * tf) + (tf + w(H, F) + th) + (2 * th + T * H + 2 * th)
-        bwd = (2 * th + T * H + 2 * th) + (th + w(H, F) + tf + tf) + (th + tf + g32(H, F)) + tf \
-            + (tf + w(F, H) + th + th) + (tf + th + g32(F, H)) + (2 * th + T * H + 2 * th) + (th + w(H, H) + th) \
+            + (2 * th + kb + 2 * th) + (th + w(F, H) + 2 * tf) + (tf + w(H, F) + th) + (2 * th + kb + 2 * th)
+        bwd = (2 * th + kb + 2 * th) + (th + w(H, F) + tf + tf) + (th + tf + g32(H, F)) + tf \
+            + (tf + w(F, H) + th + th) + (tf + th + g32(F, H)) + (2 * th + kb + 2 * th) + (th + w(H, H) + th) \
             + (2 * th + g32(H, H)) + (t3 + 2 * th + B * NH * S * 4 + 2 * bits + t3) + t3 \
             + (t3 + w(3 * H, H) + th + th) + (t3 + th + g32(3 * H, H))
         nparam = sum(v.numel() for v in self.master.views.values())
@@ -394,8 +406,8 @@ class BertEncoderLayer:
         c = self.cfg
         T, H = B * S, c.hidden
         esz = torch.tensor([], dtype=c.dtype).element_size()
-        attn_keep = B * c.heads * S * S // 8 if self._fused(S) else B * c.heads * S * S
-        h2d = 2 * T * H * esz + B * S * 4 + attn_keep + 2 * T * H
+        # counted from the device input buffers every step copies into
+        h2d = sum(t.numel() * t.element_size() for t in self._dev_inputs(B, S).values())
         return h2d, T * H * esz
 
     def train_step_host(self, host: dict, lr=None, dx_host=None, graph=True):
@@ -407,6 +419,7 @@ class BertEncoderLayer:
         ``interp.execute`` likewise takes host arrays (interp.py:1301-1317)."""
         B, S = host["add_mask"].shape
         dev = self._dev_inputs(B, S)
+        _check_host(dev, host)
         for k in ("x", "add_mask", "keep_attn", "keep1", "keep2", "dout"):
             dev[k].copy_(host[k], non_blocking=True)
         if graph:
@@ -430,6 +443,7 @@ class BertEncoderLayer:
             c = self.cfg
             T, H, NH, dev = B * S, c.hidden, c.heads, self.device
             u8 = torch.uint8
+            packed = self._fused(S) and H % 32 == 0
             self._bufs[key] = dict(
                 x=torch.empty(T, H, dtype=c.dtype, device=dev),
                 dout=torch.empty(T, H, dtype=c.dtype, device=dev),
@@ -437,8 +451,11 @@ class BertEncoderLayer:
                 # fused path: the attention keep flags travel packed (1 bit each)
                 keep_attn=(torch.empty(B, NH, S, S // 32, dtype=torch.int32, device=dev) if self._fused(S)
                            else torch.empty(B, NH, S, S, dtype=u8, device=dev)),
-                keep1=torch.empty(T, H, dtype=u8, device=dev),
-                keep2=torch.empty(T, H, dtype=u8, device=dev))
+                # the BDRLN keep flags travel packed as well (0.4 MB instead of 3.1 MB each)
+                keep1=(torch.empty(T, H // 32, dtype=torch.int32, device=dev) if packed
+                       else torch.empty(T, H, dtype=u8, device=dev)),
+                keep2=(torch.empty(T, H // 32, dtype=torch.int32, device=dev) if packed
+                       else torch.empty(T, H, dtype=u8, device=dev)))
         return self._bufs[key]
 
     # ------------------------------------------------------------ CUDA graphs
@@ -462,6 +479,7 @@ class BertEncoderLayer:
             torch.cuda.synchronize(self.device)
             self._bufs[key] = self.capture_step(B, S, lr)
         with torch.cuda.stream(pp["h2d"]):
+            _check_host(dev, host)
             if pp["free"][slot] is not None:
                 pp["h2d"].wait_event(pp["free"][slot])  # slot's previous step fully drained
             for k in ("x", "add_mask", "keep_attn", "keep1", "keep2", "dout"):

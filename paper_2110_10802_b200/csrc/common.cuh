@@ -177,6 +177,16 @@ __device__ __forceinline__ void load_keep(const uint8_t* p, float scale, float (
   }
 }
 
+// Bit-packed keep flags (bit e % 8 of byte e / 8 = keep of flat element e,
+// the little-endian byte view of kernels.pack_keep_bits' int32 words): the V
+// flags of elements e .. e+V-1 (e % V == 0, V <= 8) -> {0, scale}.
+template <int V>
+__device__ __forceinline__ void load_keep_bits(const uint8_t* kb, size_t e, float scale, float (&m)[V]) {
+  const uint32_t bits = (uint32_t)__ldg(kb + (e >> 3)) >> (e & 7);
+#pragma unroll
+  for (int i = 0; i < V; ++i) m[i] = ((bits >> i) & 1u) ? scale : 0.f;
+}
+
 __device__ __forceinline__ float sigmoid_f(float u) { return 1.f / (1.f + __expf(-u)); }
 
 __device__ __forceinline__ float gelu_f(float x) {

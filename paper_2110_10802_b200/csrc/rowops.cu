@@ -35,7 +35,7 @@ template <> struct VecWidth<float> { static constexpr int value = 4; };
 template <typename T, int V, int NCH, int ACT = 0>
 __global__ void __launch_bounds__(256, 4) bdrln_fwd_kernel(
     int64_t rows, int cols, const T* __restrict__ h, const float* __restrict__ bias,
-    const uint8_t* __restrict__ keep, float ks, const T* __restrict__ res,
+    const uint8_t* __restrict__ keep, const uint8_t* __restrict__ kbits, float ks, const T* __restrict__ res,
     const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
     T* __restrict__ y, T* __restrict__ s_out, float* __restrict__ mean_out,
     float* __restrict__ rstd_out) {
@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(256, 4) bdrln_fwd_kernel(
         }
         float m[V], r[V];
         if (keep) load_keep<V>(keep + base + col, ks, m);
+        else if (kbits) load_keep_bits<V>(kbits, base + col, ks, m);
         else {
 #pragma unroll
           for (int i = 0; i < V; ++i) m[i] = 1.f;
@@ -159,7 +160,7 @@ template <typename T, int V, int NCH, int ACT = 0>
 __global__ void __launch_bounds__(256, 2) bdrln_bwd_kernel(
     int64_t rows, int cols, const T* __restrict__ dy, const T* __restrict__ s,
     const float* __restrict__ gamma, const float* __restrict__ beta,
-    const uint8_t* __restrict__ keep, float ks, float eps,
+    const uint8_t* __restrict__ keep, const uint8_t* __restrict__ kbits, float ks, float eps,
     T* __restrict__ ds_out, T* __restrict__ dh_out, float* __restrict__ part_g,
     float* __restrict__ part_b, float* __restrict__ part_h) {
   pdl_trigger();
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(256, 2) bdrln_bwd_kernel(
         const int col = vi * V;
         float m[V];
         if (keep) load_keep<V>(keep + base + col, ks, m);
+        else if (kbits) load_keep_bits<V>(kbits, base + col, ks, m);
         else {
 #pragma unroll
           for (int i = 0; i < V; ++i) m[i] = 1.f;
@@ -290,8 +292,9 @@ __device__ __forceinline__ void bf8(const uint4& r, float (&f)[8]) {
 template <int NCH>
 __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     int64_t rows, int cols, const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ s,
-    const float* __restrict__ gamma, const uint8_t* __restrict__ keep, float ks, float eps,
-    __nv_bfloat16* __restrict__ ds_out, __nv_bfloat16* __restrict__ dh_out, float* __restrict__ part /*[3][grid][cols]*/) {
+    const float* __restrict__ gamma, const uint8_t* __restrict__ keep, const uint8_t* __restrict__ kbits, float ks,
+    float eps, __nv_bfloat16* __restrict__ ds_out, __nv_bfloat16* __restrict__ dh_out,
+    float* __restrict__ part /*[3][grid][cols]*/) {
   pdl_trigger();
   pdl_wait();
   constexpr int V = 8;
@@ -310,7 +313,14 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     const bool on = valid && vi < nvec;
     sr[c] = on ? *reinterpret_cast<const uint4*>(s + base + vi * V) : make_uint4(0, 0, 0, 0);
     dr[c] = on ? *reinterpret_cast<const uint4*>(dy + base + vi * V) : make_uint4(0, 0, 0, 0);
-    kr[c] = (on && keep) ? *reinterpret_cast<const uint2*>(keep + base + vi * V) : make_uint2(0x01010101u, 0x01010101u);
+    if (on && keep) {
+      kr[c] = *reinterpret_cast<const uint2*>(keep + base + vi * V);
+    } else if (on && kbits) {  // one byte = the lane's 8 flags -> 8 bytes of 0/1
+      const uint32_t b = __ldg(kbits + ((base + vi * V) >> 3));
+      kr[c] = make_uint2(((b & 15u) * 0x204081u) & 0x01010101u, ((b >> 4) * 0x204081u) & 0x01010101u);
+    } else {
+      kr[c] = make_uint2(0x01010101u, 0x01010101u);
+    }
   }
   float sum = 0.f;
 #pragma unroll
@@ -726,7 +736,7 @@ size_t colsum_ws_bytes(int64_t rows, int64_t cols) {
 
 template <typename T, int V>
 int bdrln_fwd_t(int64_t rows, int64_t cols, const void* h, const float* bias, const uint8_t* keep,
-                float ks, const void* res, const float* gamma, const float* beta, float eps, void* y,
+                const uint8_t* kbits, float ks, const void* res, const float* gamma, const float* beta, float eps, void* y,
                 void* s_out, float* mean, float* rstd, cudaStream_t st, int act = 0) {
   if (int rc = check_row_shape<T, V>(cols, "dfx_bdrln_fwd")) return rc;
   const int nch = pick_nch((int)(cols / V));
@@ -735,11 +745,11 @@ int bdrln_fwd_t(int64_t rows, int64_t cols, const void* h, const float* bias, co
 #define L(N)                                                                                        \
   if (nch == N) {                                                                                   \
     if (act)                                                                                        \
-      launch_k(bdrln_fwd_kernel<T, V, N, 1>, grid, 256, 0, st, rows, (int)cols, (const T*)h, bias, keep, ks, \
+      launch_k(bdrln_fwd_kernel<T, V, N, 1>, grid, 256, 0, st, rows, (int)cols, (const T*)h, bias, keep, kbits, ks, \
                                                          (const T*)res, gamma, beta, eps, (T*)y,    \
                                                          (T*)s_out, mean, rstd);                   \
     else                                                                                            \
-      launch_k(bdrln_fwd_kernel<T, V, N, 0>, grid, 256, 0, st, rows, (int)cols, (const T*)h, bias, keep, ks, \
+      launch_k(bdrln_fwd_kernel<T, V, N, 0>, grid, 256, 0, st, rows, (int)cols, (const T*)h, bias, keep, kbits, ks, \
                                                          (const T*)res, gamma, beta, eps, (T*)y,    \
                                                          (T*)s_out, mean, rstd);                   \
   }
@@ -751,13 +761,13 @@ int bdrln_fwd_t(int64_t rows, int64_t cols, const void* h, const float* bias, co
 
 template <typename T, int V, int ACT>
 int bdrln_bwd_launch(int nch, int grid, size_t smem, int64_t rows, int64_t cols, const void* dy, const void* s,
-                     const float* gamma, const float* beta, const uint8_t* keep, float ks, float eps, void* ds,
-                     void* dh, float* pg, float* pb, float* ph, cudaStream_t st) {
+                     const float* gamma, const float* beta, const uint8_t* keep, const uint8_t* kbits, float ks,
+                     float eps, void* ds, void* dh, float* pg, float* pb, float* ph, cudaStream_t st) {
 #define L(N)                                                                                       \
   if (nch == N) {                                                                                  \
     auto kfn = bdrln_bwd_kernel<T, V, N, ACT>;                                                     \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    launch_k(kfn, grid, 256, smem, st, rows, (int)cols, (const T*)dy, (const T*)s, gamma, beta, keep, ks, eps, \
+    launch_k(kfn, grid, 256, smem, st, rows, (int)cols, (const T*)dy, (const T*)s, gamma, beta, keep, kbits, ks, eps, \
                                  (T*)ds, (T*)dh, pg, pb, ph);                                      \
   }
   DFX_NCH_LIST(L)
@@ -775,7 +785,7 @@ template <typename T, int V> int bdrln_bwd_grid(int64_t rows, int64_t cols, int 
 
 template <typename T, int V>
 int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const float* gamma,
-                const uint8_t* keep, float ks, float eps, void* ds, void* dh, float* dgamma,
+                const uint8_t* keep, const uint8_t* kbits, float ks, float eps, void* ds, void* dh, float* dgamma,
                 float* dbeta, float* dbias, void* ws, size_t ws_bytes, cudaStream_t st, int act = 0,
                 const float* beta = nullptr) {
   if (int rc = check_row_shape<T, V>(cols, "dfx_bdrln_bwd")) return rc;
@@ -795,7 +805,7 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
   if (nch == N) {                                                                                  \
     auto kfn = bdrln_bwd_wave_kernel<N>;                                                           \
     if (wsm > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm); \
-    launch_k(kfn, grid, 512, wsm, st, rows, (int)cols, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)s, gamma, keep, \
+    launch_k(kfn, grid, 512, wsm, st, rows, (int)cols, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)s, gamma, keep, kbits, \
                                 ks, eps, (__nv_bfloat16*)ds, (__nv_bfloat16*)dh, pg);              \
   }
     LW(1) LW(2) LW(3)
@@ -809,9 +819,9 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
     return DFX_OK;
   }
   const size_t smem = (size_t)kWarps * cols * sizeof(float);
-  rc = act ? bdrln_bwd_launch<T, V, 1>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, ks, eps, ds, dh,
+  rc = act ? bdrln_bwd_launch<T, V, 1>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, kbits, ks, eps, ds, dh,
                                         pg, pb, ph, st)
-               : bdrln_bwd_launch<T, V, 0>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, ks, eps, ds, dh,
+               : bdrln_bwd_launch<T, V, 0>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, kbits, ks, eps, ds, dh,
                                         pg, pb, ph, st);
   if (rc) return rc;
   if (dgamma || dbeta || dbias) {
@@ -897,18 +907,36 @@ using namespace dfx;
 
 extern "C" {
 
+static int bdrln_fwd_entry(int dtype, int64_t rows, int64_t cols, const void* h, const float* bias,
+                           const uint8_t* keep, const uint8_t* kbits, float keep_scale, const void* residual,
+                           const float* gamma, const float* beta, float eps, void* y, void* s_stash, float* mean,
+                           float* rstd, void* stream) {
+  DFX_REQUIRE(h && gamma && beta && y, DFX_ERR_SHAPE, "dfx_bdrln_fwd: null required pointer");
+  if (dtype == DFX_BF16)
+    return bdrln_fwd_t_any<__nv_bfloat16>(cols, rows, cols, h, bias, keep, kbits, keep_scale, residual, gamma, beta,
+                                      eps, y, s_stash, mean, rstd, as_stream(stream));
+  if (dtype == DFX_F32)
+    return bdrln_fwd_t_any<float>(cols, rows, cols, h, bias, keep, kbits, keep_scale, residual, gamma, beta, eps, y,
+                              s_stash, mean, rstd, as_stream(stream));
+  return fail(DFX_ERR_DTYPE, "dfx_bdrln_fwd: dtype must be f32 or bf16");
+}
+
 int dfx_bdrln_fwd(int dtype, int64_t rows, int64_t cols, const void* h, const float* bias,
                   const uint8_t* keep, float keep_scale, const void* residual, const float* gamma,
                   const float* beta, float eps, void* y, void* s_stash, float* mean, float* rstd,
                   void* stream) {
-  DFX_REQUIRE(h && gamma && beta && y, DFX_ERR_SHAPE, "dfx_bdrln_fwd: null required pointer");
-  if (dtype == DFX_BF16)
-    return bdrln_fwd_t_any<__nv_bfloat16>(cols, rows, cols, h, bias, keep, keep_scale, residual, gamma, beta,
-                                      eps, y, s_stash, mean, rstd, as_stream(stream));
-  if (dtype == DFX_F32)
-    return bdrln_fwd_t_any<float>(cols, rows, cols, h, bias, keep, keep_scale, residual, gamma, beta, eps, y,
-                              s_stash, mean, rstd, as_stream(stream));
-  return fail(DFX_ERR_DTYPE, "dfx_bdrln_fwd: dtype must be f32 or bf16");
+  return bdrln_fwd_entry(dtype, rows, cols, h, bias, keep, nullptr, keep_scale, residual, gamma, beta, eps, y,
+                         s_stash, mean, rstd, stream);
+}
+
+int dfx_bdrln_fwd_kb(int dtype, int64_t rows, int64_t cols, const void* h, const float* bias,
+                     const uint32_t* keep_bits, float keep_scale, const void* residual, const float* gamma,
+                     const float* beta, float eps, void* y, void* s_stash, float* mean, float* rstd,
+                     void* stream) {
+  DFX_REQUIRE(keep_bits && (rows * cols) % 32 == 0, DFX_ERR_SHAPE,
+              "dfx_bdrln_fwd_kb: keep_bits required and rows*cols must be a multiple of 32");
+  return bdrln_fwd_entry(dtype, rows, cols, h, bias, nullptr, reinterpret_cast<const uint8_t*>(keep_bits), keep_scale,
+                         residual, gamma, beta, eps, y, s_stash, mean, rstd, stream);
 }
 
 size_t dfx_bdrln_bwd_workspace(int64_t rows, int64_t cols) {
@@ -931,18 +959,36 @@ int dfx_bdrln_bwd_finalize(int dtype, int64_t rows, int64_t cols, const void* wo
   return DFX_OK;
 }
 
+static int bdrln_bwd_entry(int dtype, int64_t rows, int64_t cols, const void* dy, const void* s_stash,
+                           const float* gamma, const uint8_t* keep, const uint8_t* kbits, float keep_scale, float eps,
+                           void* ds, void* dh, float* dgamma, float* dbeta, float* dbias, void* workspace,
+                           size_t ws_bytes, void* stream) {
+  DFX_REQUIRE(dy && s_stash && gamma, DFX_ERR_SHAPE, "dfx_bdrln_bwd: null required pointer");
+  if (dtype == DFX_BF16)
+    return bdrln_bwd_t_any<__nv_bfloat16>(cols, rows, cols, dy, s_stash, gamma, keep, kbits, keep_scale, eps, ds, dh,
+                                      dgamma, dbeta, dbias, workspace, ws_bytes, as_stream(stream));
+  if (dtype == DFX_F32)
+    return bdrln_bwd_t_any<float>(cols, rows, cols, dy, s_stash, gamma, keep, kbits, keep_scale, eps, ds, dh, dgamma,
+                              dbeta, dbias, workspace, ws_bytes, as_stream(stream));
+  return fail(DFX_ERR_DTYPE, "dfx_bdrln_bwd: dtype must be f32 or bf16");
+}
+
 int dfx_bdrln_bwd(int dtype, int64_t rows, int64_t cols, const void* dy, const void* s_stash,
                   const float* gamma, const uint8_t* keep, float keep_scale, float eps, void* ds,
                   void* dh, float* dgamma, float* dbeta, float* dbias, void* workspace,
                   size_t ws_bytes, void* stream) {
-  DFX_REQUIRE(dy && s_stash && gamma, DFX_ERR_SHAPE, "dfx_bdrln_bwd: null required pointer");
-  if (dtype == DFX_BF16)
-    return bdrln_bwd_t_any<__nv_bfloat16>(cols, rows, cols, dy, s_stash, gamma, keep, keep_scale, eps, ds, dh,
-                                      dgamma, dbeta, dbias, workspace, ws_bytes, as_stream(stream));
-  if (dtype == DFX_F32)
-    return bdrln_bwd_t_any<float>(cols, rows, cols, dy, s_stash, gamma, keep, keep_scale, eps, ds, dh, dgamma,
-                              dbeta, dbias, workspace, ws_bytes, as_stream(stream));
-  return fail(DFX_ERR_DTYPE, "dfx_bdrln_bwd: dtype must be f32 or bf16");
+  return bdrln_bwd_entry(dtype, rows, cols, dy, s_stash, gamma, keep, nullptr, keep_scale, eps, ds, dh, dgamma, dbeta,
+                         dbias, workspace, ws_bytes, stream);
+}
+
+int dfx_bdrln_bwd_kb(int dtype, int64_t rows, int64_t cols, const void* dy, const void* s_stash,
+                     const float* gamma, const uint32_t* keep_bits, float keep_scale, float eps, void* ds,
+                     void* dh, float* dgamma, float* dbeta, float* dbias, void* workspace,
+                     size_t ws_bytes, void* stream) {
+  DFX_REQUIRE(keep_bits && (rows * cols) % 32 == 0, DFX_ERR_SHAPE,
+              "dfx_bdrln_bwd_kb: keep_bits required and rows*cols must be a multiple of 32");
+  return bdrln_bwd_entry(dtype, rows, cols, dy, s_stash, gamma, nullptr, reinterpret_cast<const uint8_t*>(keep_bits),
+                         keep_scale, eps, ds, dh, dgamma, dbeta, dbias, workspace, ws_bytes, stream);
 }
 
 int dfx_softmax_fwd(int dtype, int64_t batch, int64_t heads, int64_t q, int64_t cols,
@@ -1029,10 +1075,10 @@ int dfx_layernorm_act_fwd(int dtype, int64_t rows, int64_t cols, const void* x, 
   if ((dtype == DFX_BF16 || dtype == DFX_F32) && ln_small_ok(dtype, cols))  // C4's short rows
     return ln_small_fwd(dtype, rows, cols, x, gamma, beta, eps, act, y, as_stream(stream));
   if (dtype == DFX_BF16)
-    return bdrln_fwd_t_any<__nv_bfloat16>(cols, rows, cols, x, nullptr, nullptr, 1.f, nullptr, gamma, beta, eps, y, nullptr,
+    return bdrln_fwd_t_any<__nv_bfloat16>(cols, rows, cols, x, nullptr, nullptr, nullptr, 1.f, nullptr, gamma, beta, eps, y, nullptr,
                                       nullptr, nullptr, as_stream(stream), act);
   if (dtype == DFX_F32)
-    return bdrln_fwd_t_any<float>(cols, rows, cols, x, nullptr, nullptr, 1.f, nullptr, gamma, beta, eps, y, nullptr, nullptr,
+    return bdrln_fwd_t_any<float>(cols, rows, cols, x, nullptr, nullptr, nullptr, 1.f, nullptr, gamma, beta, eps, y, nullptr, nullptr,
                               nullptr, as_stream(stream), act);
   return fail(DFX_ERR_DTYPE, "dfx_layernorm_act_fwd: dtype must be f32 or bf16");
 }
@@ -1048,10 +1094,10 @@ int dfx_layernorm_act_bwd(int dtype, int64_t rows, int64_t cols, const void* dy,
                         as_stream(stream));
   }
   if (dtype == DFX_BF16)
-    return bdrln_bwd_t_any<__nv_bfloat16>(cols, rows, cols, dy, x, gamma, nullptr, 1.f, eps, dx, nullptr, dgamma, dbeta, nullptr,
+    return bdrln_bwd_t_any<__nv_bfloat16>(cols, rows, cols, dy, x, gamma, nullptr, nullptr, 1.f, eps, dx, nullptr, dgamma, dbeta, nullptr,
                                       workspace, ws_bytes, as_stream(stream), act, beta);
   if (dtype == DFX_F32)
-    return bdrln_bwd_t_any<float>(cols, rows, cols, dy, x, gamma, nullptr, 1.f, eps, dx, nullptr, dgamma, dbeta, nullptr,
+    return bdrln_bwd_t_any<float>(cols, rows, cols, dy, x, gamma, nullptr, nullptr, 1.f, eps, dx, nullptr, dgamma, dbeta, nullptr,
                               workspace, ws_bytes, as_stream(stream), act, beta);
   return fail(DFX_ERR_DTYPE, "dfx_layernorm_act_bwd: dtype must be f32 or bf16");
 }

@@ -50,6 +50,16 @@ def _vec(t, n, name):
     return _contig(t, name)
 
 
+def _keep_arg(t, numel, name):
+    """(entry-point suffix, tensor): u8/bool flags, or int32 words bit-packed by
+    pack_keep_bits (bit e % 32 of word e // 32 = flag of flat element e)."""
+    if t is not None and t.dtype == torch.int32:
+        if t.numel() * 32 != numel:
+            raise ShapeError(f"{name}: expected {numel // 32} packed int32 keep words")
+        return "_kb", _contig(t, name)
+    return "", _u8(t, numel, name)
+
+
 def _u8(t, numel, name):
     if t is None:
         return None
@@ -191,11 +201,13 @@ def bdrln_fwd(h, bias, keep, keep_scale, residual, gamma, beta, eps, y=None, s=N
     if residual is not None and (residual.shape != h.shape or residual.dtype != h.dtype):
         raise ShapeError("bdrln: residual must match h")
     esz = h.element_size()
+    sfx, keep = _keep_arg(keep, h.numel(), "keep")
+    kbytes = 0 if keep is None else (1 if sfx == "" else 0.125)
     work = lambda: rows * cols * (esz * (2 + (residual is not None) + (s is not None))  # noqa: E731
-                                  + (keep is not None)) + rows * 8 * (mean is not None) + 3 * cols * 4
+                                  + kbytes) + rows * 8 * (mean is not None) + 3 * cols * 4
     with _span("bdrln_fwd", "hbm", work):
-        _lib.call("dfx_bdrln_fwd", dfx_dtype(h), rows, cols, h.data_ptr(), _ptr(_vec(bias, cols, "bias")),
-                  _ptr(_u8(keep, h.numel(), "keep")), float(keep_scale),
+        _lib.call("dfx_bdrln_fwd" + sfx, dfx_dtype(h), rows, cols, h.data_ptr(), _ptr(_vec(bias, cols, "bias")),
+                  _ptr(keep), float(keep_scale),
                   _ptr(None if residual is None else _contig(residual, "residual")),
                   _ptr(_vec(gamma, cols, "gamma")), _ptr(_vec(beta, cols, "beta")), float(eps),
                   _contig(y, "y").data_ptr(), _ptr(s), _ptr(mean), _ptr(rstd), _stream())
@@ -217,11 +229,13 @@ def bdrln_bwd(dy, s, gamma, keep, keep_scale, eps, ds=None, dh=None, dgamma=None
     elif ws.numel() < ws_n:
         raise ShapeError("bdrln_bwd: workspace too small")
     esz = dy.element_size()
+    sfx, keep = _keep_arg(keep, dy.numel(), "keep")
+    kbytes = 0 if keep is None else (1 if sfx == "" else 0.125)
     work = lambda: rows * cols * (esz * (2 + (ds is not None) + (dh is not None))  # noqa: E731
-                                  + (keep is not None)) + 4 * cols * 4
+                                  + kbytes) + 4 * cols * 4
     with _span("bdrln_bwd", "hbm", work):
-        _lib.call("dfx_bdrln_bwd", dfx_dtype(dy), rows, cols, dy.data_ptr(), _contig(s, "s").data_ptr(),
-                  _vec(gamma, cols, "gamma").data_ptr(), _ptr(_u8(keep, dy.numel(), "keep")),
+        _lib.call("dfx_bdrln_bwd" + sfx, dfx_dtype(dy), rows, cols, dy.data_ptr(), _contig(s, "s").data_ptr(),
+                  _vec(gamma, cols, "gamma").data_ptr(), _ptr(keep),
                   float(keep_scale), float(eps), _ptr(ds), _ptr(dh), _ptr(dgamma), _ptr(dbeta),
                   _ptr(dbias), ws.data_ptr(), ws.numel(), _stream())
 

@@ -157,8 +157,8 @@ def test_pipelined_host_steps_match_synchronous():
         hosts.append({k: v.pin_memory() for k, v in dict(
             x=torch.randn(B * S, H, generator=g).bfloat16(), dout=torch.randn(B * S, H, generator=g).bfloat16(),
             add_mask=torch.zeros(B, S), keep_attn=K.pack_keep_bits(ka),
-            keep1=(torch.rand(B * S, H, generator=g) >= 0.1).to(torch.uint8),
-            keep2=(torch.rand(B * S, H, generator=g) >= 0.1).to(torch.uint8)).items()})
+            keep1=K.pack_keep_bits((torch.rand(B * S, H, generator=g) >= 0.1).to(torch.uint8)),
+            keep2=K.pack_keep_bits((torch.rand(B * S, H, generator=g) >= 0.1).to(torch.uint8))).items()})
     outs = {}
     for mode in ("sync", "async"):
         layer = BertEncoderLayer(BertLayerConfig(dtype=torch.bfloat16), seed=2)

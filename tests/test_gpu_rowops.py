@@ -78,6 +78,30 @@ def test_bdrln(dtype, rows, cols):
     assert_close(host(dbi), wb["dbias"], tol, "dbias")
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("rows,cols", [(4096, 768), (37, 64), (300, 2048), (5, 96)])
+def test_bdrln_packed_keep_identical(dtype, rows, cols):
+    """Bit-packed keep flags (dfx_bdrln_{fwd,bwd}_kb) give bitwise the u8 results."""
+    from paper_2110_10802_b200 import kernels as KK
+    k = K()
+    g = torch.Generator(device="cpu").manual_seed(rows + cols)
+    h, r, dy = (torch.randn(rows, cols, generator=g).to(dtype).cuda() for _ in range(3))
+    bias, gm, be = (torch.randn(cols, generator=g).cuda() for _ in range(3))
+    keep = (torch.rand(rows, cols, generator=g) >= 0.1).to(torch.uint8).cuda()
+    kb = KK.pack_keep_bits(keep)
+    outs = []
+    for kk in (keep, kb):
+        y, s = torch.empty_like(h), torch.empty_like(h)
+        k.bdrln_fwd(h, bias, kk, 1 / 0.9, r, gm, be, 1e-12, y=y, s=s)
+        ds, dh = torch.empty_like(h), torch.empty_like(h)
+        dg, dbe, dbi = (torch.empty(cols, device="cuda") for _ in range(3))
+        k.bdrln_bwd(dy, s, gm, kk, 1 / 0.9, 1e-12, ds=ds, dh=dh, dgamma=dg, dbeta=dbe, dbias=dbi)
+        outs.append((y, s, ds, dh, dg, dbe, dbi))
+    torch.cuda.synchronize()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
 def test_bdrln_golden_f32():
     """Straight against the reference's own outputs (tests/golden)."""
     k = K()
