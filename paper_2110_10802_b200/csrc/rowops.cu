@@ -277,16 +277,17 @@ __global__ void __launch_bounds__(256, 2) bdrln_bwd_kernel(
 // grid-stride kernel above is latency-bound there), and nothing is carried
 // across rows.  The row stays in registers as raw bf16 (24 registers for s
 // and dy at 768 columns) and is unpacked on each use, which keeps the kernel
-// at 64 registers = 2 CTAs x 16 warps per SM without spills.  The CTA's 16
-// rows are reduced per column in a fixed order through shared memory, one
-// quantity at a time (dbias, dgamma, dbeta partials).
-__device__ __forceinline__ void bf8(const uint4& r, float (&f)[8]) {
-  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    f[2 * i] = __uint_as_float(w[i] << 16);
-    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-  }
+// at 64 registers = 2 CTAs x 16 warps per SM without spills.  All arithmetic
+// is packed fp32 (FADD2 / FMUL2 / FFMA2 on column pairs): one wave of this
+// kernel is instruction-issue bound, not HBM bound.  The CTA's 16 rows are
+// reduced per column in a fixed order through two shared-memory planes
+// (dbias and dgamma staged by the output pass, then dbeta).
+__device__ __forceinline__ float2 bf2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+__device__ __forceinline__ uint32_t pk_bf2(float2 v) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
+  return *reinterpret_cast<uint32_t*>(&h);
 }
 
 template <int NCH>
@@ -294,134 +295,150 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     int64_t rows, int cols, const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ s,
     const float* __restrict__ gamma, const uint8_t* __restrict__ keep, const uint8_t* __restrict__ kbits, float ks,
     float eps, __nv_bfloat16* __restrict__ ds_out, __nv_bfloat16* __restrict__ dh_out,
-    float* __restrict__ part /*[3][grid][cols]*/) {
+    float* __restrict__ part /*[3][grid][cols]*/, int rpc /* rows per CTA, <= 16 */) {
   pdl_trigger();
   pdl_wait();
   constexpr int V = 8;
-  extern __shared__ float red[];  // [16][cols]
+  extern __shared__ float red[];  // [2][16][cols]
+  float* red2 = red + 16 * cols;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvec = cols / V;
   const float inv_n = 1.f / (float)cols;
-  const int64_t row = (int64_t)blockIdx.x * 16 + warp;
-  const bool valid = row < rows;
+  const int64_t row = (int64_t)blockIdx.x * rpc + warp;
+  const bool valid = warp < rpc && row < rows;
   const size_t base = (size_t)(valid ? row : 0) * cols;
   uint4 sr[NCH], dr[NCH];
-  uint2 kr[NCH];
+  uint32_t kb[NCH];  // the lane's 8 keep flags of each chunk as bits
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int vi = lane + c * 32;
     const bool on = valid && vi < nvec;
     sr[c] = on ? *reinterpret_cast<const uint4*>(s + base + vi * V) : make_uint4(0, 0, 0, 0);
     dr[c] = on ? *reinterpret_cast<const uint4*>(dy + base + vi * V) : make_uint4(0, 0, 0, 0);
-    if (on && keep) {
-      kr[c] = *reinterpret_cast<const uint2*>(keep + base + vi * V);
-    } else if (on && kbits) {  // one byte = the lane's 8 flags -> 8 bytes of 0/1
-      const uint32_t b = __ldg(kbits + ((base + vi * V) >> 3));
-      kr[c] = make_uint2(((b & 15u) * 0x204081u) & 0x01010101u, ((b >> 4) * 0x204081u) & 0x01010101u);
+    if (on && keep) {  // 8 bytes of 0/1 -> 8 bits (byte k -> bit k, no carries)
+      const uint2 k2 = *reinterpret_cast<const uint2*>(keep + base + vi * V);
+      kb[c] = ((k2.x * 0x01020408u) >> 24) | (((k2.y * 0x01020408u) >> 24) << 4);
+    } else if (on && kbits) {
+      kb[c] = __ldg(kbits + ((base + vi * V) >> 3));
     } else {
-      kr[c] = make_uint2(0x01010101u, 0x01010101u);
+      kb[c] = 0xFFu;
     }
   }
-  float sum = 0.f;
+  // mean, then variance (two passes over the registers)
+  float2 a2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
-    float x[8];
-    bf8(sr[c], x);
+    const uint32_t w[4] = {sr[c].x, sr[c].y, sr[c].z, sr[c].w};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sum += x[i];
+    for (int i = 0; i < 4; ++i) a2 = __fadd2_rn(a2, bf2(w[i]));
   }
-  const float mu = warp_sum(sum) * inv_n;
-  float sq = 0.f;
+  const float mu = warp_sum(a2.x + a2.y) * inv_n;
+  const float2 nmu2 = make_float2(-mu, -mu);
+  a2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     if (lane + c * 32 < nvec) {
-      float x[8];
-      bf8(sr[c], x);
+      const uint32_t w[4] = {sr[c].x, sr[c].y, sr[c].z, sr[c].w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) { const float d = x[i] - mu; sq += d * d; }
+      for (int i = 0; i < 4; ++i) {
+        const float2 d = __fadd2_rn(bf2(w[i]), nmu2);
+        a2 = __ffma2_rn(d, d, a2);
+      }
     }
   }
-  const float rstd = rsqrtf(warp_sum(sq) * inv_n + eps);
-  float m1 = 0.f, m2 = 0.f;
+  const float rstd = rsqrtf(warp_sum(a2.x + a2.y) * inv_n + eps);
+  const float2 rstd2 = make_float2(rstd, rstd);
+  // m1 = mean(dy*g), m2 = mean(dy*g*xhat)
+  float2 m1a = make_float2(0.f, 0.f), m2a = make_float2(0.f, 0.f);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int vi = lane + c * 32;
     if (vi < nvec) {
-      Vec<float, V> gv;
-      gv.load(gamma + vi * V);
-      float x[8], g[8];
-      bf8(sr[c], x);
-      bf8(dr[c], g);
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + vi * V));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + vi * V) + 1);
+      const float2 gg[4] = {make_float2(g0.x, g0.y), make_float2(g0.z, g0.w), make_float2(g1.x, g1.y),
+                            make_float2(g1.z, g1.w)};
+      const uint32_t ws[4] = {sr[c].x, sr[c].y, sr[c].z, sr[c].w};
+      const uint32_t wd[4] = {dr[c].x, dr[c].y, dr[c].z, dr[c].w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float dyg = g[i] * gv.v[i];
-        m1 += dyg;
-        m2 += dyg * (x[i] - mu) * rstd;
+      for (int i = 0; i < 4; ++i) {
+        const float2 dyg = __fmul2_rn(bf2(wd[i]), gg[i]);
+        const float2 xh = __fmul2_rn(__fadd2_rn(bf2(ws[i]), nmu2), rstd2);
+        m1a = __fadd2_rn(m1a, dyg);
+        m2a = __ffma2_rn(dyg, xh, m2a);
       }
     }
   }
-  m1 = warp_sum(m1) * inv_n;
-  m2 = warp_sum(m2) * inv_n;
-  const int64_t nparts = gridDim.x;
-  // ds, dh -> HBM; dh (the dbias contribution) also -> the reduction buffer
+  const float m1 = warp_sum(m1a.x + m1a.y) * inv_n, m2 = warp_sum(m2a.x + m2a.y) * inv_n;
+  const float2 nm1v = make_float2(-m1, -m1), nm2v = make_float2(-m2, -m2);
+  // ds = rstd * (dy*g - (xhat*m2 + m1)) and dh = ds * keep * ks -> HBM;
+  // dh (the dbias contribution) and dy*xhat (dgamma) -> the two planes
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int vi = lane + c * 32;
     if (vi < nvec) {
       const int col = vi * V;
-      Vec<float, V> dhv;
-      Vec<float, V> gv;
-      gv.load(gamma + col);
-      float x[8], g[8];
-      bf8(sr[c], x);
-      bf8(dr[c], g);
-      const uint32_t kw[2] = {kr[c].x, kr[c].y};
-      Vec<__nv_bfloat16, V> dsv, dhs;
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + col));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + col) + 1);
+      const float2 gg[4] = {make_float2(g0.x, g0.y), make_float2(g0.z, g0.w), make_float2(g1.x, g1.y),
+                            make_float2(g1.z, g1.w)};
+      const uint32_t ws[4] = {sr[c].x, sr[c].y, sr[c].z, sr[c].w};
+      const uint32_t wd[4] = {dr[c].x, dr[c].y, dr[c].z, dr[c].w};
+      uint32_t pds[4], pdh[4];
+      float2* r1 = reinterpret_cast<float2*>(red + warp * cols + col);
+      float2* r2 = reinterpret_cast<float2*>(red2 + warp * cols + col);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float dsi = rstd * (g[i] * gv.v[i] - m1 - (x[i] - mu) * rstd * m2);
-        dsv.v[i] = dsi;
-        dhv.v[i] = ((kw[i >> 2] >> (8 * (i & 3))) & 0xFFu) ? dsi * ks : 0.f;
-        dhs.v[i] = dhv.v[i];
+      for (int i = 0; i < 4; ++i) {
+        const float2 y = bf2(wd[i]);
+        const float2 dyg = __fmul2_rn(y, gg[i]);
+        const float2 xh = __fmul2_rn(__fadd2_rn(bf2(ws[i]), nmu2), rstd2);
+        const float2 ds = __fmul2_rn(__ffma2_rn(xh, nm2v, __fadd2_rn(dyg, nm1v)), rstd2);
+        const float2 kf = make_float2((kb[c] >> (2 * i)) & 1u ? ks : 0.f, (kb[c] >> (2 * i + 1)) & 1u ? ks : 0.f);
+        const float2 dh = __fmul2_rn(ds, kf);
+        pds[i] = pk_bf2(ds);
+        pdh[i] = pk_bf2(dh);
+        // invalid rows (the grid's tail) stage zeros
+        r1[i] = valid ? dh : make_float2(0.f, 0.f);
+        r2[i] = valid ? __fmul2_rn(y, xh) : make_float2(0.f, 0.f);
       }
       if (valid) {
-        if (ds_out) dsv.store(ds_out + base + col);
-        if (dh_out) dhs.store(dh_out + base + col);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dhv.v[i] = 0.f;
+        if (ds_out) *reinterpret_cast<uint4*>(ds_out + base + col) = make_uint4(pds[0], pds[1], pds[2], pds[3]);
+        if (dh_out) *reinterpret_cast<uint4*>(dh_out + base + col) = make_uint4(pdh[0], pdh[1], pdh[2], pdh[3]);
       }
-      dhv.store(red + warp * cols + col);
     }
   }
-  // column partials of the CTA's 16 rows in fixed order: dbias (staged
-  // above), then dgamma (dy * xhat), then dbeta (dy)
-#pragma unroll 1
-  for (int step = 0; step < 3; ++step) {
-    const int q = step == 0 ? 2 : step - 1;
-    if (step > 0) {
+  const int64_t nparts = gridDim.x;
+  // column partials of the CTA's 16 rows, rows summed in fixed order:
+  // dbias (plane 1) and dgamma (plane 2), then dbeta (dy, plane 1 again)
+  __syncthreads();
+  for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+    float th = 0.f, tg = 0.f;
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const int vi = lane + c * 32;
-        if (vi < nvec) {
-          float x[8], g[8];
-          bf8(sr[c], x);
-          bf8(dr[c], g);
-          Vec<float, V> v;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) v.v[i] = q == 0 ? g[i] * (x[i] - mu) * rstd : g[i];
-          v.store(red + warp * cols + vi * V);
-        }
-      }
+    for (int w = 0; w < 16; ++w) {
+      th += red[w * cols + col];
+      tg += red2[w * cols + col];
     }
-    __syncthreads();
-    for (int col = threadIdx.x; col < cols; col += blockDim.x) {
-      float t = 0.f;
+    part[((size_t)2 * nparts + blockIdx.x) * cols + col] = th;
+    part[((size_t)0 * nparts + blockIdx.x) * cols + col] = tg;
+  }
+  __syncthreads();
 #pragma unroll
-      for (int w = 0; w < 16; ++w) t += red[w * cols + col];
-      part[((size_t)q * nparts + blockIdx.x) * cols + col] = t;
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      const uint32_t wd[4] = {dr[c].x, dr[c].y, dr[c].z, dr[c].w};
+      float4* r1 = reinterpret_cast<float4*>(red + warp * cols + vi * V);
+      const float2 y0 = bf2(wd[0]), y1 = bf2(wd[1]), y2 = bf2(wd[2]), y3 = bf2(wd[3]);
+      r1[0] = make_float4(y0.x, y0.y, y1.x, y1.y);
+      r1[1] = make_float4(y2.x, y2.y, y3.x, y3.y);
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) t += red[w * cols + col];
+    part[((size_t)1 * nparts + blockIdx.x) * cols + col] = t;
   }
 }
 
@@ -777,10 +794,20 @@ int bdrln_bwd_launch(int nch, int grid, size_t smem, int64_t rows, int64_t cols,
 }
 
 // partial-set count of the backward (the finalize must use the same one)
+// rows per CTA of the one-wave backward: two CTAs on every SM with an even
+// share of the rows (<= 16, one per warp), so no SM runs a second CTA while
+// others idle (256 CTAs of 16 rows left 40 SMs with one CTA at C2)
+inline int bdrln_wave_rpc(int64_t rows) {
+  const int64_t slots = std::min<int64_t>(2 * (int64_t)num_sms(), kMaxColBlocks);  // <= the workspace's partial sets
+  return (int)std::min<int64_t>(16, std::max<int64_t>(1, (rows + slots - 1) / slots));
+}
+
 template <typename T, int V> int bdrln_bwd_grid(int64_t rows, int64_t cols, int act) {
   const int nch = pick_nch((int)(cols / V));
   const bool wave = sizeof(T) == 2 && act == 0 && rows <= 16 * (int64_t)kMaxColBlocks && nch <= 3;
-  return wave ? (int)((rows + 15) / 16) : grid_for(rows, kWarps, kMaxColBlocks);
+  if (!wave) return grid_for(rows, kWarps, kMaxColBlocks);
+  const int rpc = bdrln_wave_rpc(rows);
+  return (int)((rows + rpc - 1) / rpc);
 }
 
 template <typename T, int V>
@@ -792,7 +819,7 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
   if (rows == 0) return DFX_OK;
   const int nch = pick_nch((int)(cols / V));
   const bool wave = sizeof(T) == 2 && act == 0 && rows <= 16 * (int64_t)kMaxColBlocks && nch <= 3;
-  const int grid = wave ? (int)((rows + 15) / 16) : grid_for(rows, kWarps, kMaxColBlocks);
+  const int grid = bdrln_bwd_grid<T, V>(rows, cols, act);
   const size_t need = 3 * (size_t)grid * cols * sizeof(float);
   DFX_REQUIRE(ws_bytes >= need, DFX_ERR_WORKSPACE, "dfx_bdrln_bwd: workspace too small");
   float* pg = (float*)ws;
@@ -800,13 +827,13 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
   float* ph = pb + (size_t)grid * cols;
   int rc;
   if (wave) {
-    const size_t wsm = (size_t)16 * cols * sizeof(float);
+    const size_t wsm = (size_t)2 * 16 * cols * sizeof(float);  // two staging planes
 #define LW(N)                                                                                      \
   if (nch == N) {                                                                                  \
     auto kfn = bdrln_bwd_wave_kernel<N>;                                                           \
     if (wsm > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm); \
     launch_k(kfn, grid, 512, wsm, st, rows, (int)cols, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)s, gamma, keep, kbits, \
-                                ks, eps, (__nv_bfloat16*)ds, (__nv_bfloat16*)dh, pg);              \
+                                ks, eps, (__nv_bfloat16*)ds, (__nv_bfloat16*)dh, pg, bdrln_wave_rpc(rows)); \
   }
     LW(1) LW(2) LW(3)
 #undef LW

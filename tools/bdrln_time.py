@@ -9,7 +9,7 @@ import torch  # noqa: E402
 from paper_2110_10802_b200 import kernels as K  # noqa: E402
 from tools.gemm_vs_cublas import timeit  # noqa: E402
 
-T, H = 4096, 768
+T, H = int(os.environ.get("BDRLN_T", "4096")), 768
 g = torch.Generator(device="cuda").manual_seed(0)
 bf = torch.bfloat16
 h = torch.randn(T, H, device="cuda", generator=g).to(bf)
