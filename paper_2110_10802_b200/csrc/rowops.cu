@@ -272,6 +272,8 @@ __global__ void __launch_bounds__(256, 2) bdrln_bwd_kernel(
 }
 
 
+unsigned long long* g_row_trace = nullptr;  // debug timeline of the one-wave BDRLN backward
+
 // One-wave variant (bf16, rows <= 16 * kMaxColBlocks — the BERT C2 shape):
 // every warp owns exactly ONE row, so all rows are in flight at once (the
 // grid-stride kernel above is latency-bound there), and nothing is carried
@@ -295,12 +297,22 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     int64_t rows, int cols, const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ s,
     const float* __restrict__ gamma, const uint8_t* __restrict__ keep, const uint8_t* __restrict__ kbits, float ks,
     float eps, __nv_bfloat16* __restrict__ ds_out, __nv_bfloat16* __restrict__ dh_out,
-    float* __restrict__ part /*[3][grid][cols]*/, int rpc /* rows per CTA, <= 16 */) {
+    float* __restrict__ part /*[3][grid][cols]*/, int rpc /* rows per CTA, <= 16 */,
+    unsigned long long* trace /* debug timeline (tools/bdrln_trace.py), normally null */) {
   pdl_trigger();
   pdl_wait();
+#define RTRACE(k)                                                                                  \
+  do {                                                                                             \
+    if (trace && threadIdx.x == 0) {                                                               \
+      unsigned long long t_;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+      trace[blockIdx.x * 8 + (k)] = t_;                                                            \
+    }                                                                                              \
+  } while (0)
   constexpr int V = 8;
-  extern __shared__ float red[];  // [2][16][cols]
+  extern __shared__ float red[];  // [2][16][cols] staging planes, then gamma [cols]
   float* red2 = red + 16 * cols;
+  float* gam = red2 + 16 * cols;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvec = cols / V;
   const float inv_n = 1.f / (float)cols;
@@ -324,6 +336,12 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
       kb[c] = 0xFFu;
     }
   }
+  // gamma -> smem once per CTA: the per-chunk reads below are then LDS, not
+  // one dependent L2 round trip per chunk (1.5 us of the kernel, measured)
+  for (int i = threadIdx.x * 4; i < cols; i += blockDim.x * 4)
+    *reinterpret_cast<float4*>(gam + i) = __ldg(reinterpret_cast<const float4*>(gamma + i));
+  __syncthreads();
+  RTRACE(0);
   // mean, then variance (two passes over the registers)
   float2 a2 = make_float2(0.f, 0.f);
 #pragma unroll
@@ -333,6 +351,7 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     for (int i = 0; i < 4; ++i) a2 = __fadd2_rn(a2, bf2(w[i]));
   }
   const float mu = warp_sum(a2.x + a2.y) * inv_n;
+  RTRACE(1);
   const float2 nmu2 = make_float2(-mu, -mu);
   a2 = make_float2(0.f, 0.f);
 #pragma unroll
@@ -347,6 +366,7 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     }
   }
   const float rstd = rsqrtf(warp_sum(a2.x + a2.y) * inv_n + eps);
+  RTRACE(2);
   const float2 rstd2 = make_float2(rstd, rstd);
   // m1 = mean(dy*g), m2 = mean(dy*g*xhat)
   float2 m1a = make_float2(0.f, 0.f), m2a = make_float2(0.f, 0.f);
@@ -354,8 +374,8 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
   for (int c = 0; c < NCH; ++c) {
     const int vi = lane + c * 32;
     if (vi < nvec) {
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + vi * V));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + vi * V) + 1);
+      const float4 g0 = reinterpret_cast<const float4*>(gam + vi * V)[0];
+      const float4 g1 = reinterpret_cast<const float4*>(gam + vi * V)[1];
       const float2 gg[4] = {make_float2(g0.x, g0.y), make_float2(g0.z, g0.w), make_float2(g1.x, g1.y),
                             make_float2(g1.z, g1.w)};
       const uint32_t ws[4] = {sr[c].x, sr[c].y, sr[c].z, sr[c].w};
@@ -370,6 +390,7 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     }
   }
   const float m1 = warp_sum(m1a.x + m1a.y) * inv_n, m2 = warp_sum(m2a.x + m2a.y) * inv_n;
+  RTRACE(3);
   const float2 nm1v = make_float2(-m1, -m1), nm2v = make_float2(-m2, -m2);
   // ds = rstd * (dy*g - (xhat*m2 + m1)) and dh = ds * keep * ks -> HBM;
   // dh (the dbias contribution) and dy*xhat (dgamma) -> the two planes
@@ -378,8 +399,8 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     const int vi = lane + c * 32;
     if (vi < nvec) {
       const int col = vi * V;
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + col));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + col) + 1);
+      const float4 g0 = reinterpret_cast<const float4*>(gam + col)[0];
+      const float4 g1 = reinterpret_cast<const float4*>(gam + col)[1];
       const float2 gg[4] = {make_float2(g0.x, g0.y), make_float2(g0.z, g0.w), make_float2(g1.x, g1.y),
                             make_float2(g1.z, g1.w)};
       const uint32_t ws[4] = {sr[c].x, sr[c].y, sr[c].z, sr[c].w};
@@ -408,9 +429,11 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     }
   }
   const int64_t nparts = gridDim.x;
+  RTRACE(4);
   // column partials of the CTA's 16 rows, rows summed in fixed order:
   // dbias (plane 1) and dgamma (plane 2), then dbeta (dy, plane 1 again)
   __syncthreads();
+  RTRACE(5);
   for (int col = threadIdx.x; col < cols; col += blockDim.x) {
     float th = 0.f, tg = 0.f;
 #pragma unroll
@@ -421,6 +444,7 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     part[((size_t)2 * nparts + blockIdx.x) * cols + col] = th;
     part[((size_t)0 * nparts + blockIdx.x) * cols + col] = tg;
   }
+  RTRACE(6);
   __syncthreads();
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
@@ -440,6 +464,8 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     for (int w = 0; w < 16; ++w) t += red[w * cols + col];
     part[((size_t)1 * nparts + blockIdx.x) * cols + col] = t;
   }
+  RTRACE(7);
+#undef RTRACE
 }
 
 // out_q[col] (+)= sum_b part[q][b][col] for q = blockIdx.y.  Warp w sums
@@ -827,13 +853,13 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
   float* ph = pb + (size_t)grid * cols;
   int rc;
   if (wave) {
-    const size_t wsm = (size_t)2 * 16 * cols * sizeof(float);  // two staging planes
+    const size_t wsm = (size_t)(2 * 16 + 1) * cols * sizeof(float);  // two staging planes + gamma
 #define LW(N)                                                                                      \
   if (nch == N) {                                                                                  \
     auto kfn = bdrln_bwd_wave_kernel<N>;                                                           \
     if (wsm > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm); \
     launch_k(kfn, grid, 512, wsm, st, rows, (int)cols, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)s, gamma, keep, kbits, \
-                                ks, eps, (__nv_bfloat16*)ds, (__nv_bfloat16*)dh, pg, bdrln_wave_rpc(rows)); \
+                                ks, eps, (__nv_bfloat16*)ds, (__nv_bfloat16*)dh, pg, bdrln_wave_rpc(rows), g_row_trace); \
   }
     LW(1) LW(2) LW(3)
 #undef LW
@@ -1158,3 +1184,7 @@ int dfx_cast(int64_t n, int sd, const void* src, int dd, void* dst, void* stream
 }
 
 }  // extern "C"
+
+extern "C" __attribute__((visibility("default"))) void dfx_debug_bdrln_trace(void* buf) {
+  dfx::g_row_trace = reinterpret_cast<unsigned long long*>(buf);
+}
