@@ -155,6 +155,12 @@ int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t head_dim, co
                  const float* add_mask, const float* lse, const uint32_t* keep_bits_row,
                  const uint32_t* keep_bits_col, float keep_scale, float inv_divisor, void* dqkv,
                  int64_t ld_dqkv, void* workspace, size_t ws_bytes, void* stream);
+/* The qkv bias gradient dbias[3*NH*64] (+)= column sums of dQ | dK | dV, from
+ * the per-strip partial sums dfx_attn_bwd leaves in its workspace (fixed
+ * order; the unrounded fp32 gradients).  Replaces a column-sum pass over the
+ * [B*S, 3H] dqkv tensor (Gemm C-input VJP, autodiff.py:1416-1459). */
+int dfx_attn_bwd_bias_grad(int64_t batch, int64_t heads, int64_t seq, const void* workspace,
+                           size_t ws_bytes, float* dbias, int accumulate, void* stream);
 
 /* ---- a7: bias + tanh-GELU -------------------------------------------------
  * pre = f + bias ; y = 0.5*pre*(1+tanh(0.7978845608*(pre+0.044715*pre^3)))

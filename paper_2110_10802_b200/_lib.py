@@ -119,6 +119,7 @@ _SIGS = [
     ("dfx_attn_bwd", c_int, [c_int64, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                              c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_float, c_void_p,
                              c_int64, c_void_p, c_size_t, c_void_p]),
+    ("dfx_attn_bwd_bias_grad", c_int, [c_int64, c_int64, c_int64, c_void_p, c_size_t, c_void_p, c_int, c_void_p]),
     ("dfx_im2col3x3", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_void_p, c_int64, c_void_p,
                               c_void_p, c_void_p]),
     ("dfx_avgpool_fwd", c_int, [c_int, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),

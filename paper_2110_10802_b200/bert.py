@@ -326,12 +326,15 @@ class BertEncoderLayer:
         if self._fused(S):
             with L("bwd.attention"):
                 K.attn_bwd(b["qkv"], b["ctx"], b["dctx"], B, S, c.heads, add_mask, b["lse"], self._kb_row,
-                           b["kbits_col"], ks, 1.0 / (c.head_dim ** 0.5), b["dqkv"])
+                           b["kbits_col"], ks, 1.0 / (c.head_dim ** 0.5), b["dqkv"], ws=self._attn_ws(B, S))
         else:
             self._attn_bwd_unfused(b, B, S, keep_attn, ks)
         with fork():
             with L("bwd.qkv_bias_grad"):
-                K.colsum(b["dqkv"], G["bqkv"])
+                if self._fused(S):  # the attention backward left per-strip column sums
+                    K.attn_bwd_bias_grad(B, S, c.heads, self._attn_ws(B, S), G["bqkv"])
+                else:
+                    K.colsum(b["dqkv"], G["bqkv"])
             with L("bwd.qkv_wgrad"):
                 K.gemm(b["dqkv"].t(), x.t(), G["wqkv"])
         with L("bwd.qkv_dgrad+residual"):
@@ -339,6 +342,14 @@ class BertEncoderLayer:
         if self.concurrent:
             main.wait_stream(side)  # join: every gradient is complete on the caller's stream
         return b["dx"]
+
+    def _attn_ws(self, B, S):
+        """Persistent attention-backward workspace (delta and the qkv-bias
+        partial sums the side stream reduces)."""
+        key = ("attn_ws", B, S)
+        if key not in self._bufs:
+            self._bufs[key] = K.attn_bwd_workspace(B, S, self.cfg.heads)
+        return self._bufs[key]
 
     def _bdrln_ws(self, B, S):
         """Two persistent BDRLN-backward workspaces (one per call site): their

@@ -399,6 +399,18 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
   }
 }
 
+// qkv bias gradient: out[col] (+)= sum over the strip partials, fixed order
+__global__ void __launch_bounds__(256) attn_bias_reduce_kernel(int nparts, int cols, const float* __restrict__ part,
+                                                               float* __restrict__ out, int accumulate) {
+  pdl_trigger();
+  pdl_wait();
+  const int col = blockIdx.x * 256 + threadIdx.x;
+  if (col >= cols) return;
+  float t = 0.f;
+  for (int r = 0; r < nparts; ++r) t += part[(size_t)r * cols + col];
+  out[col] = accumulate ? out[col] + t : t;
+}
+
 // --------------------------------------------------------------------- backward
 struct AttnBwdParams {
   unsigned long long* trace;
@@ -413,6 +425,7 @@ struct AttnBwdParams {
   const uint32_t* kb_col;
   float ks, sc2, scale;       // keep scale, inv_divisor*log2e, inv_divisor
   __nv_bfloat16* dqkv;        // [T, ld_dqkv]: dQ | dK | dV column blocks
+  float* bias_part;           // [B*S/128][3H]: per-strip column sums of dQ | dK | dV (qkv bias gradient)
 };
 
 constexpr int CH = 128;  // keys (dq) / queries (dkdv) per chunk
@@ -454,6 +467,46 @@ __device__ __forceinline__ void st_row32(uint32_t buf, int r, int col0, const ui
   const int ch0 = (col0 & 63) >> 3;
 #pragma unroll
   for (int u = 0; u < 4; ++u) st_sw128(tile, r, ch0 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+}
+
+// Column sums of NT 128 x 64 fp32 tiles whose rows are spread one 16-column
+// slice per softmax thread (row rl, columns c0..c0+15), in a fixed order:
+// staged in smem, 8 groups of 16 rows, then the 8 group sums -> out_t[0..63].
+// 16-byte chunk c of row r lives at chunk c ^ (r & 15): the row-per-lane
+// writes and the column reads are both bank-conflict free.
+template <int NT>
+__device__ __forceinline__ void tile_colsum_128x64(float* const (&stage)[NT], float* const (&scratch)[NT], int rl,
+                                                   int c0, const float (&v)[NT][16], int st,
+                                                   float* const (&out)[NT]) {
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    float4* d = reinterpret_cast<float4*>(stage[t] + rl * 64);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      d[((c0 >> 2) + i) ^ (rl & 15)] = make_float4(v[t][4 * i], v[t][4 * i + 1], v[t][4 * i + 2], v[t][4 * i + 3]);
+  }
+  named_bar(1, kSoftWarps * 32);
+  const int col = st & 63, grp = st >> 6;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int row = grp * 16 + r;
+      acc += stage[t][row * 64 + (((col >> 2) ^ (row & 15)) << 2) + (col & 3)];
+    }
+    scratch[t][grp * 64 + col] = acc;
+  }
+  named_bar(1, kSoftWarps * 32);
+  if (st < 64) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      float u = 0.f;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) u += scratch[t][g * 64 + st];
+      out[t][st] = u;
+    }
+  }
 }
 
 __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* g, const float (&o)[16]) {
@@ -656,6 +709,13 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
     float o[16];
     tmem_ld16(trow + T_DQ + part * 16, o);
     store_bf16x16(p.dqkv + (size_t)(row0 + grow) * p.ld_dqkv + h * DH + part * 16, o);
+    if (p.bias_part) {  // this strip's dQ column sums (the dS buffer is free now)
+      float* const stg[1] = {reinterpret_cast<float*>(smem + DqSmem::DS)};
+      float* const scr[1] = {red};
+      float* const dst[1] = {p.bias_part + (size_t)(b * (S / QT) + qb) * 3 * p.H + h * DH};
+      const float (&vv)[1][16] = *reinterpret_cast<const float(*)[1][16]>(&o);
+      tile_colsum_128x64<1>(stg, scr, rl, part * 16, vv, st, dst);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -843,15 +903,22 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
     mbar_wait(bar_pdsfree, (nch - 1) & 1);
     if (sw == 0 && lane == 0) ATRACE(10);
     tc_fence_after();
-    float o[16];
     __nv_bfloat16* grow_ptr = p.dqkv + (size_t)(row0 + key) * p.ld_dqkv + h * DH + part * 16;
-    tmem_ld16(trow + T_DK + part * 16, o);
-    store_bf16x16(grow_ptr + p.H, o);
-    tmem_ld16(trow + T_DV + part * 16, o);
+    float g2[2][16];  // dK, dV rows of this thread
+    tmem_ld16(trow + T_DK + part * 16, g2[0]);
+    store_bf16x16(grow_ptr + p.H, g2[0]);
+    tmem_ld16(trow + T_DV + part * 16, g2[1]);
     const float dvs = p.ks / p.scale;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) o[i] *= dvs;
-    store_bf16x16(grow_ptr + 2 * p.H, o);
+    for (int i = 0; i < 16; ++i) g2[1][i] *= dvs;
+    store_bf16x16(grow_ptr + 2 * p.H, g2[1]);
+    if (p.bias_part) {  // dK / dV column sums of this key strip (Pd / dS buffers and lse / D rows are free now)
+      float* bp = p.bias_part + (size_t)(b * (S / QT) + kb) * 3 * p.H + h * DH;
+      float* const stg[2] = {reinterpret_cast<float*>(smem + DkvSmem::DS), reinterpret_cast<float*>(smem + DkvSmem::PD)};
+      float* const scr[2] = {lse_s, del_s};
+      float* const dst[2] = {bp + p.H, bp + 2 * p.H};
+      tile_colsum_128x64<2>(stg, scr, rl, part * 16, g2, st, dst);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -919,8 +986,13 @@ extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   return DFX_OK;
 }
 
+// delta D [B, NH, S] f32, then (256-byte aligned) the qkv-bias column partials
+// [B*S/128][3*NH*64] f32 that dfx_attn_bwd_bias_grad reduces
+static size_t attn_delta_bytes(int64_t batch, int64_t heads, int64_t seq) {
+  return ((size_t)(batch * heads * seq) * sizeof(float) + 255) & ~(size_t)255;
+}
 extern "C" size_t dfx_attn_bwd_workspace(int64_t batch, int64_t heads, int64_t seq) {
-  return (size_t)(batch * heads * seq) * sizeof(float) + 256;
+  return attn_delta_bytes(batch, heads, seq) + (size_t)(batch * (seq / QT)) * 3 * heads * DH * sizeof(float) + 256;
 }
 
 extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t head_dim, const void* qkv,
@@ -955,6 +1027,7 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   p.dctx = reinterpret_cast<const __nv_bfloat16*>(dctx);
   p.add_mask = add_mask; p.lse = lse;
   p.delta = reinterpret_cast<float*>(workspace);
+  p.bias_part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + attn_delta_bytes(batch, heads, seq));
   p.kb_row = keep_bits_row; p.kb_col = keep_bits_col;
   p.ks = keep_bits_row ? keep_scale : 1.f;
   p.sc2 = inv_divisor * kLog2e;
@@ -975,6 +1048,20 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   p.trace = trace_dkdv ? g_attn_trace : nullptr;
   launch_k(attn_bwd_dkdv_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dk, dv)");
+  return DFX_OK;
+}
+
+extern "C" int dfx_attn_bwd_bias_grad(int64_t batch, int64_t heads, int64_t seq, const void* workspace,
+                                      size_t ws_bytes, float* dbias, int accumulate, void* stream) {
+  DFX_REQUIRE(dbias && workspace && ws_bytes >= dfx_attn_bwd_workspace(batch, heads, seq), DFX_ERR_WORKSPACE,
+              "dfx_attn_bwd_bias_grad: pass the workspace of the preceding dfx_attn_bwd");
+  DFX_REQUIRE(seq % QT == 0, DFX_ERR_SHAPE, "dfx_attn_bwd_bias_grad: seq must be a multiple of 128");
+  const int cols = (int)(3 * heads * DH);
+  const float* part = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(workspace) +
+                                                     attn_delta_bytes(batch, heads, seq));
+  launch_k(attn_bias_reduce_kernel, (cols + 255) / 256, 256, 0, as_stream(stream), (int)(batch * (seq / QT)), cols,
+           part, dbias, accumulate);
+  DFX_LAUNCH_CHECK("dfx_attn_bwd_bias_grad");
   return DFX_OK;
 }
 

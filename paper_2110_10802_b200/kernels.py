@@ -320,14 +320,26 @@ def attn_fwd(qkv, B, S, heads, add_mask, keep, keep_scale, inv_divisor, ctx, lse
     return ctx
 
 
-def attn_bwd(qkv, ctx, dctx, B, S, heads, add_mask, lse, kbits_row, kbits_col, keep_scale, inv_divisor, dqkv):
-    """Writes dQ | dK | dV into dqkv (bf16 [B*S, >=3H])."""
+def attn_bwd_workspace(B, S, heads):
+    """A dedicated workspace for attn_bwd whose qkv-bias partial sums
+    attn_bwd_bias_grad reduces later (possibly on another stream)."""
+    return torch.empty(_lib.load().dfx_attn_bwd_workspace(B, heads, S), dtype=torch.uint8, device="cuda")
+
+
+def attn_bwd(qkv, ctx, dctx, B, S, heads, add_mask, lse, kbits_row, kbits_col, keep_scale, inv_divisor, dqkv,
+             ws=None):
+    """Writes dQ | dK | dV into dqkv (bf16 [B*S, >=3H]); ``ws`` (attn_bwd_workspace)
+    keeps the per-strip qkv-bias column sums for attn_bwd_bias_grad."""
     for t, nm in ((qkv, "qkv"), (ctx, "ctx"), (dctx, "dctx"), (dqkv, "dqkv")):
         if t.dtype != torch.bfloat16 or t.stride(1) != 1:
             raise ShapeError(f"attn_bwd: {nm} must be bfloat16 with contiguous rows")
     if ctx.stride(0) != dctx.stride(0):
         raise ShapeError("attn_bwd: ctx and dctx must share a row stride")
-    ws = WORKSPACE.get(_lib.load().dfx_attn_bwd_workspace(B, heads, S))
+    need = _lib.load().dfx_attn_bwd_workspace(B, heads, S)
+    if ws is None:
+        ws = WORKSPACE.get(need)
+    elif ws.numel() < need:
+        raise ShapeError("attn_bwd: workspace too small")
     flops = 8.0 * B * heads * S * S * 64  # algorithmic: dPd, dV, dQ, dK (the S recomputes are extra)
     with _span("attn_bwd", "tensor", lambda: flops):
         _lib.call("dfx_attn_bwd", B, heads, S, 64, qkv.data_ptr(), qkv.stride(0), ctx.data_ptr(), dctx.data_ptr(),
@@ -335,6 +347,15 @@ def attn_bwd(qkv, ctx, dctx, B, S, heads, add_mask, lse, kbits_row, kbits_col, k
                   float(keep_scale), float(inv_divisor), dqkv.data_ptr(), dqkv.stride(0), ws.data_ptr(),
                   ws.numel(), _stream())
     return dqkv
+
+
+def attn_bwd_bias_grad(B, S, heads, ws, dbias, accumulate=False):
+    """dbias [3*heads*64] (+)= column sums of the dQ | dK | dV an attn_bwd(..., ws=ws) produced."""
+    _vec(dbias, 3 * heads * 64, "dbias")
+    with _span("attn_bwd_bias_grad", "hbm", lambda: B * (S // 128) * 3 * heads * 64 * 4):
+        _lib.call("dfx_attn_bwd_bias_grad", B, heads, S, ws.data_ptr(), ws.numel(), dbias.data_ptr(),
+                  int(bool(accumulate)), _stream())
+    return dbias
 
 
 # ---------------------------------------------------------------------------

@@ -90,6 +90,41 @@ def test_attention_vs_oracle(B, NH, S):
         assert err <= 2e-2, f"d{nm}: {err:.3e}"
 
 
+@pytest.mark.parametrize("B,NH,S", [(2, 2, 128), (2, 12, 512), (1, 3, 384)])
+def test_qkv_bias_grad_from_strip_partials(B, NH, S):
+    """dfx_attn_bwd_bias_grad (per-strip fp32 column sums left by the backward)
+    against the oracle's column sums of dQ | dK | dV, and against a column sum
+    of the bf16 dqkv the same call wrote."""
+    from paper_2110_10802_b200 import kernels as KK
+    qkv, am, keep, dctx = _case(B, NH, S, seed=3 * S + NH)
+    H = NH * 64
+    t_qkv = torch.as_tensor(qkv, dtype=torch.float32).bfloat16().cuda()
+    t_am = torch.as_tensor(am, dtype=torch.float32).cuda()
+    t_keep = torch.as_tensor(keep.astype(np.uint8)).cuda()
+    ctx = torch.empty(B * S, H, dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty(B, NH, S, dtype=torch.float32, device="cuda")
+    kr = torch.empty(B, NH, S, S // 32, dtype=torch.int32, device="cuda")
+    kc = torch.empty_like(kr)
+    ks = 1.0 / (1.0 - P_DROP)
+    KK.attn_fwd(t_qkv, B, S, NH, t_am, t_keep, ks, 0.125, ctx, lse, kr, kc)
+    t_do = torch.as_tensor(dctx, dtype=torch.float32).bfloat16().cuda()
+    dqkv = torch.zeros(B * S, 3 * H, dtype=torch.bfloat16, device="cuda")
+    ws = KK.attn_bwd_workspace(B, S, NH)
+    KK.attn_bwd(t_qkv, ctx, t_do, B, S, NH, t_am, lse, kr, kc, ks, 0.125, dqkv, ws=ws)
+    db = torch.full((3 * H,), 7.0, device="cuda")
+    KK.attn_bwd_bias_grad(B, S, NH, ws, db)
+    db2 = torch.ones(3 * H, device="cuda")
+    KK.attn_bwd_bias_grad(B, S, NH, ws, db2, accumulate=True)
+    torch.cuda.synchronize()
+    got = db.cpu().numpy().astype(np.float64)
+    _, _, w_dqkv = _oracle(qkv, am, keep, dctx, B, S, NH)
+    want = w_dqkv.sum(0)
+    assert O.compare_scaled(got, want) <= 2e-2, O.compare_scaled(got, want)
+    from_bf16 = dqkv.float().sum(0).cpu().numpy()
+    assert np.abs(got - from_bf16).max() <= 1e-2 * max(1.0, np.abs(from_bf16).max())
+    assert np.allclose(db2.cpu().numpy(), got + 1.0, rtol=1e-6, atol=1e-5)
+
+
 def test_attention_no_dropout_no_mask():
     B, NH, S = 1, 2, 256
     qkv, am, keep, dctx = _case(B, NH, S, seed=7, dropout=False, masked=False)
