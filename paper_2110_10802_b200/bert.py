@@ -113,6 +113,10 @@ class BertEncoderLayer:
         self.wlow = FlatArena(specs, torch.bfloat16, self.device) if cfg.dtype == torch.bfloat16 else None
         self._bufs = {}
         self.slot = 0  # activation / input buffer set (see train_step_host_async)
+        # three sets: step i+3's H2D may start once step i's dx has left
+        # (D2H), i.e. with two compute periods of slack (two sets stalled
+        # every step on H2D(i+2) waiting for D2H(i): tools/e2e_probe.py)
+        self.nslots = 3
         self.concurrent = True  # weight gradients on a forked stream (backward)
         self._init_params(seed)
 
@@ -179,7 +183,7 @@ class BertEncoderLayer:
 
     # ------------------------------------------------------------ activations
     def buffers(self, B: int, S: int):
-        # one activation set per pipeline slot (train_step_host_async double-buffers)
+        # one activation set per pipeline slot (train_step_host_async rotates them)
         key = (B, S, self.slot)
         if key not in self._bufs:
             c = self.cfg
@@ -471,16 +475,16 @@ class BertEncoderLayer:
 
     # ------------------------------------------------------------ CUDA graphs
     def train_step_host_async(self, host: dict, lr=None, dx_host=None):
-        """Pipelined form of ``train_step_host``: two device input/activation
-        sets alternate, so step i+1's H2D copy (its own stream) and step i's
-        D2H of dx (another stream) overlap step i's CUDA-graph replay — the
+        """Pipelined form of ``train_step_host``: ``nslots`` device input /
+        activation sets rotate, so step i+1's H2D copy (its own stream) and step
+        i's D2H of dx (another stream) overlap step i's CUDA-graph replay — the
         prefetching a data loader does.  Every step still copies its own inputs
         from pinned host memory and reads its own dx back; ``finish_host()``
         joins the copy streams into the compute stream."""
         B, S = host["add_mask"].shape
         if not hasattr(self, "_pipe"):
             self._pipe = {"h2d": torch.cuda.Stream(device=self.device), "d2h": torch.cuda.Stream(device=self.device),
-                          "free": [None, None]}
+                          "free": [None] * self.nslots}
         pp = self._pipe
         slot = self.slot
         comp = torch.cuda.current_stream(self.device)
@@ -508,7 +512,7 @@ class BertEncoderLayer:
             ev_free = torch.cuda.Event()
             ev_free.record(pp["d2h"])
         pp["free"][slot] = ev_free
-        self.slot ^= 1
+        self.slot = (self.slot + 1) % self.nslots
         return dx_host
 
     def finish_host(self):
