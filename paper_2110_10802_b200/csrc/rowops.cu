@@ -739,6 +739,43 @@ __global__ void sgd_kernel(int64_t n, float* __restrict__ w, const float* __rest
   }
 }
 
+// 16-byte form (n4 float4 groups, 16-byte aligned w / g, 8-byte aligned wb):
+// two groups per thread per iteration, so each thread keeps 64 bytes of loads
+// in flight (the scalar form streamed at ~5.5 TB/s)
+__global__ void sgd4_kernel(int64_t n4, float4* __restrict__ w, const float4* __restrict__ g, float lr,
+                            uint2* __restrict__ wb) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const float2 nl = make_float2(-lr, -lr);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += 2 * stride) {
+    const bool two = i + stride < n4;
+    const float4 w0 = w[i], g0 = g[i];
+    float4 w1 = make_float4(0.f, 0.f, 0.f, 0.f), g1 = w1;
+    if (two) { w1 = w[i + stride]; g1 = g[i + stride]; }
+    float4 v[2] = {w0, w1};
+    const float4 gg[2] = {g0, g1};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const float2 a = __ffma2_rn(make_float2(gg[u].x, gg[u].y), nl, make_float2(v[u].x, v[u].y));
+      const float2 b = __ffma2_rn(make_float2(gg[u].z, gg[u].w), nl, make_float2(v[u].z, v[u].w));
+      v[u] = make_float4(a.x, a.y, b.x, b.y);
+    }
+    w[i] = v[0];
+    if (wb) {
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0].x, v[0].y), h1 = __floats2bfloat162_rn(v[0].z, v[0].w);
+      wb[i] = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+    }
+    if (two) {
+      w[i + stride] = v[1];
+      if (wb) {
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[1].x, v[1].y), h1 = __floats2bfloat162_rn(v[1].z, v[1].w);
+        wb[i + stride] = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+      }
+    }
+  }
+}
+
 __global__ void scale_kernel(int64_t n, float* __restrict__ x, float s) {
   pdl_trigger();
   pdl_wait();
@@ -1172,7 +1209,15 @@ int dfx_sgd_update(int64_t n, float* master, const float* grad, float lr, void* 
                    void* stream) {
   DFX_REQUIRE(master && grad, DFX_ERR_SHAPE, "dfx_sgd_update: null pointer");
   if (n == 0) return DFX_OK;
-  launch_k(sgd_kernel, grid_for(n, 256, 148 * 8), 256, 0, as_stream(stream), n, master, grad, lr, (__nv_bfloat16*)weights_bf16);
+  if (n % 4 == 0 && aligned16(master) && aligned16(grad) && (reinterpret_cast<uintptr_t>(weights_bf16) & 7) == 0) {
+    const int64_t n4 = n / 4;
+    launch_k(sgd4_kernel, grid_for((n4 + 1) / 2, 256, 148 * 8), 256, 0, as_stream(stream), n4,
+             reinterpret_cast<float4*>(master), reinterpret_cast<const float4*>(grad), lr,
+             reinterpret_cast<uint2*>(weights_bf16));
+  } else {
+    launch_k(sgd_kernel, grid_for(n, 256, 148 * 8), 256, 0, as_stream(stream), n, master, grad, lr,
+             (__nv_bfloat16*)weights_bf16);
+  }
   DFX_LAUNCH_CHECK("dfx_sgd_update");
   return DFX_OK;
 }

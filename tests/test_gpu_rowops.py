@@ -242,3 +242,22 @@ def test_odd_widths_scalar_lanes():
                         dev(b, torch.float32), 1e-5)
         torch.cuda.synchronize()
         assert_close(host(y), O.layernorm(x, g, b, 1e-5), 1e-4, f"cols={cols}")
+
+
+@pytest.mark.parametrize("n,off", [(7_087_872, 0), (4096 * 3 + 4, 0), (1001, 0), (4096, 1)])
+def test_sgd_update_vector_and_scalar_paths(n, off):
+    """dfx_sgd_update: the 16-byte path (n % 4 == 0, aligned) and the scalar
+    path (odd n / misaligned views) give w - lr*g as one fma, and the bf16
+    shadow is its round-to-nearest copy."""
+    from paper_2110_10802_b200 import kernels as KK
+    g = torch.Generator(device="cpu").manual_seed(n)
+    w0 = torch.randn(n + off, generator=g).cuda()
+    gr = torch.randn(n + off, generator=g).cuda()
+    w, gg = w0[off:], gr[off:]
+    ref = torch.addcmul(w.double(), gg.double(), torch.full_like(gg.double(), -1e-3)).float()
+    wb = torch.empty(n + off, dtype=torch.bfloat16, device="cuda")[off:]
+    wk = w.clone() if off == 0 else w  # misaligned view stays a view
+    KK.sgd_update(wk, gg, 1e-3, wb)
+    torch.cuda.synchronize()
+    assert torch.allclose(wk, ref, rtol=0, atol=1e-6 * max(1.0, ref.abs().max().item()))
+    assert torch.equal(wb, wk.bfloat16())
