@@ -612,14 +612,19 @@ Plan plan(const dfx_gemm_args& p) {
   const int sms = num_sms();
   const char* force = getenv("DFX_GEMM_FORCE");  // "cg,bn" (tuning / tests only)
   if (force) {
-    int fcg = 1, fbn = 256;
-    if (sscanf(force, "%d,%d", &fcg, &fbn) == 2 && (fcg == 1 || fcg == 2) && (fbn == 64 || fbn == 128 || fbn == 192 || fbn == 256) &&
+    int fcg = 1, fbn = 256, fsp = 1;
+    const int nf = sscanf(force, "%d,%d,%d", &fcg, &fbn, &fsp);
+    if (nf >= 2 && (fcg == 1 || fcg == 2) && (fbn == 64 || fbn == 128 || fbn == 192 || fbn == 256) &&
         !(fcg == 2 && fbn == 192 && p.b_stride_k != 1) &&  // pair-192 loads B in 96-row K-major boxes only
-        !(fcg == 2 && (fbn == 64 || p.m < 256))) {
+        !(fcg == 2 && (fbn == 64 || p.m < 256)) && (fsp == 1 || p.epilogue == DFX_EPI_NONE)) {
       const int64_t z = p.batch1 * p.batch2;
       const int64_t kb = (p.k + BK - 1) / BK;  // K tail: TMA zero-fills past k
       const int64_t units = z * ((p.m + BM * fcg - 1) / (BM * fcg)) * ((p.n + fbn - 1) / fbn);
-      return Plan{fbn, fcg, 1, (int)kb, units};
+      Plan f{fbn, fcg, std::max(1, fsp), (int)kb, units};
+      f.kb_per_split = (int)((kb + f.splits - 1) / f.splits);
+      f.splits = (int)((kb + f.kb_per_split - 1) / f.kb_per_split);
+      f.tiles = units * f.splits;
+      return f;
     }
   }
   const int64_t z = p.batch1 * p.batch2;
@@ -653,6 +658,28 @@ Plan plan(const dfx_gemm_args& p) {
   if (z == 1 && kb == 1 && p.m >= 256 && sms >= 2 && p.epilogue == DFX_EPI_NONE) {
     const int64_t units = (p.m + 255) / 256 * ((p.n + 127) / 128);
     best = Plan{128, 2, 1, (int)kb, units};
+  }
+  // a 1-CTA plan that fills most but not all SMs (qkv wgrad: 18 x 6 = 108
+  // tiles) runs better as a split-K-2 plan that fills one wave: 192-wide
+  // single-CTA tiles, else 256-wide pairs (tools/gemm_mc_sweep.py: qkv wgrad
+  // 24.8 -> 19.5 us, ffn2 wgrad 24.4 -> 22.6 us)
+  if (best.cg == 1 && p.epilogue == DFX_EPI_NONE && z == 1 && best.tiles * 2 > sms && best.tiles < sms &&
+      kb >= 16) {
+    const int64_t u192 = ((p.m + BM - 1) / BM) * ((p.n + 191) / 192);
+    const int64_t u256p = ((p.m + 2 * BM - 1) / (2 * BM)) * ((p.n + 255) / 256);
+    const bool b_k = p.b_stride_k == 1;
+    if (u192 * 2 <= sms) {
+      best = Plan{192, 1, 2, 0, u192};
+    } else if (p.m >= 256 && u256p * 2 <= sms / 2) {
+      best = Plan{256, 2, 2, 0, u256p};
+    }
+    (void)b_k;
+    if (best.splits == 2) {
+      best.kb_per_split = (int)((kb + 1) / 2);
+      best.splits = (int)((kb + best.kb_per_split - 1) / best.kb_per_split);
+      best.tiles *= best.splits;
+      return best;
+    }
   }
   // split K when a 1-CTA plan leaves most SMs idle (the 768-wide wgrads)
   if (best.cg == 1 && p.epilogue == DFX_EPI_NONE && best.tiles * 2 <= sms && kb >= 8) {

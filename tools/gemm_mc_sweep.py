@@ -1,6 +1,5 @@
-"""BERT C2 GEMM shapes under forced tile configs (DFX_GEMM_FORCE=cg,bn,mc),
-including the A-multicast clusters (mc = 2): max error vs a float reference and
-graph-replay time per call."""
+"""BERT C2 GEMM shapes under forced tile configs (DFX_GEMM_FORCE=cg,bn[,splits]):
+max error vs a float reference and graph-replay time per call."""
 import os
 import sys
 
@@ -14,7 +13,8 @@ T, H, F = 4096, 768, 3072
 SHAPES = [("qkv", T, 3 * H, H, False, False, torch.bfloat16), ("out", T, H, H, False, False, torch.bfloat16),
           ("ffn1", T, F, H, False, False, torch.bfloat16), ("ffn2", T, H, F, False, False, torch.bfloat16),
           ("ffn2_dgrad", T, F, H, False, True, torch.bfloat16), ("ffn1_dgrad", T, H, F, False, True, torch.bfloat16),
-          ("ffn2_wgrad", H, F, T, True, True, torch.float32), ("qkv_wgrad", 3 * H, H, T, True, True, torch.float32)]
+          ("ffn2_wgrad", H, F, T, True, True, torch.float32), ("qkv_wgrad", 3 * H, H, T, True, True, torch.float32),
+          ("ffn1_wgrad", F, H, T, True, True, torch.float32), ("out_wgrad", H, H, T, True, True, torch.float32)]
 CONFIGS = sys.argv[1:] or ["", "2,256", "2,192", "2,128", "1,256", "1,192", "1,128"]
 
 for name, m, n, k, a_t, b_t, out in SHAPES:
