@@ -659,28 +659,10 @@ Plan plan(const dfx_gemm_args& p) {
     const int64_t units = (p.m + 255) / 256 * ((p.n + 127) / 128);
     best = Plan{128, 2, 1, (int)kb, units};
   }
-  // a 1-CTA plan that fills most but not all SMs (qkv wgrad: 18 x 6 = 108
-  // tiles) runs better as a split-K-2 plan that fills one wave: 192-wide
-  // single-CTA tiles, else 256-wide pairs (tools/gemm_mc_sweep.py: qkv wgrad
-  // 24.8 -> 19.5 us, ffn2 wgrad 24.4 -> 22.6 us)
-  if (best.cg == 1 && p.epilogue == DFX_EPI_NONE && z == 1 && best.tiles * 2 > sms && best.tiles < sms &&
-      kb >= 16) {
-    const int64_t u192 = ((p.m + BM - 1) / BM) * ((p.n + 191) / 192);
-    const int64_t u256p = ((p.m + 2 * BM - 1) / (2 * BM)) * ((p.n + 255) / 256);
-    const bool b_k = p.b_stride_k == 1;
-    if (u192 * 2 <= sms) {
-      best = Plan{192, 1, 2, 0, u192};
-    } else if (p.m >= 256 && u256p * 2 <= sms / 2) {
-      best = Plan{256, 2, 2, 0, u256p};
-    }
-    (void)b_k;
-    if (best.splits == 2) {
-      best.kb_per_split = (int)((kb + 1) / 2);
-      best.splits = (int)((kb + best.kb_per_split - 1) / best.kb_per_split);
-      best.tiles *= best.splits;
-      return best;
-    }
-  }
+  // (tried: split-K-2 one-wave plans for the near-full-wave weight gradients —
+  // faster alone, qkv wgrad 24.8 -> 19.6 us, but the BERT step 0.400 -> 0.409 ms
+  // and the C5 step 11.17 -> 11.37 ms in context: extra partial traffic and a
+  // reduce launch on the forked branch)
   // split K when a 1-CTA plan leaves most SMs idle (the 768-wide wgrads)
   if (best.cg == 1 && p.epilogue == DFX_EPI_NONE && best.tiles * 2 <= sms && kb >= 8) {
     if (best.bn == 256) {
