@@ -334,15 +334,19 @@ class BertEncoderLayer:
         else:
             self._attn_bwd_unfused(b, B, S, keep_attn, ks)
         with fork():
-            with L("bwd.qkv_bias_grad"):
-                if self._fused(S):  # the attention backward left per-strip column sums
-                    K.attn_bwd_bias_grad(B, S, c.heads, self._attn_ws(B, S), G["bqkv"])
-                else:
+            if not self._fused(S):
+                with L("bwd.qkv_bias_grad"):
                     K.colsum(b["dqkv"], G["bqkv"])
             with L("bwd.qkv_wgrad"):
                 K.gemm(b["dqkv"].t(), x.t(), G["wqkv"])
         with L("bwd.qkv_dgrad+residual"):
             K.gemm(b["dqkv"], self.weight("wqkv").t(), b["dx"], EPI_ADD, aux=b["ds1"])
+        if self._fused(S):
+            # the attention backward left per-strip column sums: the tiny reduce
+            # rides the main stream after the dgrad (shorter than the forked
+            # weight-gradient GEMM), keeping it off the step's tail
+            with L("bwd.qkv_bias_grad"):
+                K.attn_bwd_bias_grad(B, S, c.heads, self._attn_ws(B, S), G["bqkv"])
         if self.concurrent:
             main.wait_stream(side)  # join: every gradient is complete on the caller's stream
         return b["dx"]
