@@ -407,7 +407,15 @@ __global__ void __launch_bounds__(256) attn_bias_reduce_kernel(int nparts, int c
   const int col = blockIdx.x * 256 + threadIdx.x;
   if (col >= cols) return;
   float t = 0.f;
-  for (int r = 0; r < nparts; ++r) t += part[(size_t)r * cols + col];
+  int r = 0;
+  for (; r + 8 <= nparts; r += 8) {  // eight partial rows in flight (not one L2 round trip per row)
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(part + (size_t)(r + u) * cols + col);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t += v[u];
+  }
+  for (; r < nparts; ++r) t += __ldg(part + (size_t)r * cols + col);
   out[col] = accumulate ? out[col] + t : t;
 }
 
