@@ -332,6 +332,9 @@ int dfx_sgd_update(int64_t n, float* master, const float* grad, float lr, void* 
 int dfx_scale_f32(int64_t n, float* x, float scale, void* stream);
 /* bf16 <-> f32 casts of flat buffers. */
 int dfx_cast(int64_t n, int src_dtype, const void* src, int dst_dtype, void* dst, void* stream);
+/* dst0 = cast(src0), dst1 = cast(src1) (n elements each) in one launch. */
+int dfx_cast2(int64_t n, int src_dtype, const void* src0, const void* src1, int dst_dtype, void* dst0,
+              void* dst1, void* stream);
 
 #ifdef __cplusplus
 }

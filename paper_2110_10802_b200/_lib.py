@@ -132,6 +132,7 @@ _SIGS = [
     ("dfx_sgd_update", c_int, [c_int64, c_void_p, c_void_p, c_float, c_void_p, c_void_p]),
     ("dfx_scale_f32", c_int, [c_int64, c_void_p, c_float, c_void_p]),
     ("dfx_cast", c_int, [c_int64, c_int, c_void_p, c_int, c_void_p, c_void_p]),
+    ("dfx_cast2", c_int, [c_int64, c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGS]

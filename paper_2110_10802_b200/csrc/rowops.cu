@@ -784,6 +784,21 @@ __global__ void scale_kernel(int64_t n, float* __restrict__ x, float s) {
     x[i] *= s;
 }
 
+// two equal-length casts in one launch (the BN parameter gradients dbeta and
+// dgamma of every normalisation layer: one tiny launch instead of two)
+template <typename S, typename D>
+__global__ void cast2_kernel(int64_t n, const S* __restrict__ s0, const S* __restrict__ s1, D* __restrict__ d0,
+                             D* __restrict__ d1) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n)
+      d0[i] = from_f<D>(to_f<S>(s0[i]));
+    else
+      d1[i - n] = from_f<D>(to_f<S>(s1[i - n]));
+  }
+}
+
 template <typename S, typename D>
 __global__ void cast_kernel(int64_t n, const S* __restrict__ s, D* __restrict__ d) {
   pdl_trigger();
@@ -1238,6 +1253,25 @@ int dfx_cast(int64_t n, int sd, const void* src, int dd, void* dst, void* stream
   else if (sd == DFX_F32 && dd == DFX_F32) launch_k(cast_kernel<float, float>, g, 256, 0, st, n, (const float*)src, (float*)dst);
   else return fail(DFX_ERR_DTYPE, "dfx_cast: unsupported dtype pair");
   DFX_LAUNCH_CHECK("dfx_cast");
+  return DFX_OK;
+}
+
+int dfx_cast2(int64_t n, int sd, const void* src0, const void* src1, int dd, void* dst0, void* dst1, void* stream) {
+  if (n == 0) return DFX_OK;
+  cudaStream_t st = as_stream(stream);
+  const int g = grid_for(2 * n, 256, 148 * 8);
+  if (sd == DFX_F32 && dd == DFX_F32)
+    launch_k(cast2_kernel<float, float>, g, 256, 0, st, n, (const float*)src0, (const float*)src1, (float*)dst0,
+             (float*)dst1);
+  else if (sd == DFX_F32 && dd == DFX_BF16)
+    launch_k(cast2_kernel<float, __nv_bfloat16>, g, 256, 0, st, n, (const float*)src0, (const float*)src1,
+             (__nv_bfloat16*)dst0, (__nv_bfloat16*)dst1);
+  else if (sd == DFX_BF16 && dd == DFX_F32)
+    launch_k(cast2_kernel<__nv_bfloat16, float>, g, 256, 0, st, n, (const __nv_bfloat16*)src0,
+             (const __nv_bfloat16*)src1, (float*)dst0, (float*)dst1);
+  else
+    return fail(DFX_ERR_DTYPE, "dfx_cast2: unsupported dtype pair");
+  DFX_LAUNCH_CHECK("dfx_cast2");
   return DFX_OK;
 }
 

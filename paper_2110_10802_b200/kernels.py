@@ -501,6 +501,17 @@ def cast(src, dst):
     return dst
 
 
+def cast2(src0, dst0, src1, dst1):
+    """dst0 = src0 and dst1 = src1 (equal sizes, dtype-converting) in one launch."""
+    n = src0.numel()
+    if src1.numel() != n or dst0.numel() != n or dst1.numel() != n:
+        raise ShapeError("cast2: size mismatch")
+    if src0.dtype != src1.dtype or dst0.dtype != dst1.dtype:
+        raise ShapeError("cast2: both pairs must share dtypes")
+    _lib.call("dfx_cast2", n, dfx_dtype(src0), src0.data_ptr(), src1.data_ptr(), dfx_dtype(dst0), dst0.data_ptr(),
+              dst1.data_ptr(), _stream())
+
+
 def launch_count() -> int:
     return int(_lib.load().dfx_launch_count())
 

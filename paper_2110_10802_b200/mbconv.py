@@ -189,8 +189,7 @@ class MBConvBlock:
                       G["wr"].data_ptr(), G["br"].data_ptr(), b["dpool"].data_ptr(), b["bnsum"].data_ptr(),
                       ws.data_ptr(), ws.numel(), st)
         # local BN parameter gradients (dbeta = sum du, dgamma = sum du*xhat)
-        K.cast(b["bnsum"][0], G["b"])
-        K.cast(b["bnsum"][1], G["g"])
+        K.cast2(b["bnsum"][0], G["b"], b["bnsum"][1], G["g"])
         if self.world > 1:  # SyncBN: global sums for the input gradient
             allreduce_sum(b["bnsum"], group=self.pg)
         count = float(N * Ho * Wo * self.world)

@@ -108,8 +108,7 @@ class BatchNormAct:
             _lib.call("dfx_batchnorm_act_bwd_reduce", dt, rows, self.C, dy.data_ptr(), x.data_ptr(),
                       self.mean.data_ptr(), self.rstd.data_ptr(), self.gamma.data_ptr(), self.beta.data_ptr(),
                       self.act, self.bnsum.data_ptr(), ws.data_ptr(), ws.numel(), st)
-        K.cast(self.bnsum[0], self.dbeta)   # local parameter gradients
-        K.cast(self.bnsum[1], self.dgamma)
+        K.cast2(self.bnsum[0], self.dbeta, self.bnsum[1], self.dgamma)  # local parameter gradients
         if self.world > 1:
             allreduce_sum(self.bnsum, group=self.pg)
         with K._span("bn_act_bwd_dx", "hbm", lambda: 3 * x.numel() * x.element_size()):
