@@ -267,7 +267,10 @@ int dfx_mbconv_bwd_reduce(int dtype, int64_t N, int64_t H, int64_t W, int64_t C,
                           float* db_r, float* dpool, float* bnsum, void* workspace, size_t ws_bytes,
                           void* stream);
 /* Backward part 2: dx and dw_dw [3][3][C]; count = number of elements each
- * BN channel normalises over (all ranks). */
+ * BN channel normalises over (all ranks), or 0 for SyncBN: bnsum is then
+ * [3][C] and bnsum[2][c] holds the allreduced per-channel count (each rank
+ * contributes its own local count, so unequal per-rank batches normalise
+ * exactly as the forward's merged statistics do). */
 int dfx_mbconv_bwd_dx(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride,
                       int ksize, const int* pads, const void* dy, const void* z, const void* x,
                       const float* w_dw, const float* mean, const float* rstd, const float* gamma,
@@ -292,7 +295,8 @@ int dfx_layernorm_act_bwd(int dtype, int64_t rows, int64_t cols, const void* dy,
  *          (nsets = #ranks for SyncBN)
  *   apply: y = act((x - mean) * rstd * gamma + beta)
  *   bwd_reduce: bnsum[2][C] = (sum du, sum du*xhat) = (dbeta, dgamma)
- *   bwd_dx: dx = gamma*rstd*(du - bnsum[0]/count - xhat*bnsum[1]/count) */
+ *   bwd_dx: dx = gamma*rstd*(du - bnsum[0]/count - xhat*bnsum[1]/count);
+ *           count = 0 (SyncBN): per-channel count read from bnsum[2][C] */
 size_t dfx_batchnorm_workspace(int64_t rows, int64_t C);
 int dfx_batchnorm_stats(int dtype, int64_t rows, int64_t C, const void* x, float* local,
                         void* workspace, size_t ws_bytes, void* stream);

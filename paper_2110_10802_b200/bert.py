@@ -540,9 +540,10 @@ class BertEncoderLayer:
             if lr is not None:
                 self.sgd_step(lr)
 
+        keep = self.training_state()
         if timer is None:
-            return CapturedStep(fn)
-        cs = CapturedStep(fn)  # warm-up/capture without events, then an instrumented twin
+            return CapturedStep(fn, preserve=keep)
+        cs = CapturedStep(fn, preserve=keep)  # warm-up/capture without events, then an instrumented twin
         # the twin is single-stream: each kernel's events then time that kernel
         # alone, not its contention with the forked weight-gradient branch
         timer.reset_records()
@@ -553,6 +554,11 @@ class BertEncoderLayer:
         finally:
             self.concurrent = True
         return cs, inst
+
+    def training_state(self) -> list:
+        """Tensors a step mutates beyond its activations (restored around a
+        capture's warm-up, graphs.CapturedStep)."""
+        return [t.flat for t in (self.master, self.grad, self.wlow) if t is not None]
 
     def device_inputs(self, B: int, S: int) -> dict:
         """Static device buffers a captured step reads (fill before replay)."""

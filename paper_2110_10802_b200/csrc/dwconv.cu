@@ -259,7 +259,8 @@ __global__ void __launch_bounds__(kMaxThreads, 2)
       const float rs = dk.rstd[c], mu = dk.mean[c];
       kP[i] = dk.gamma[c] * rs;
       kQ[i] = dk.beta[c] - mu * kP[i];
-      const float mdu = dk.bnsum[c] * dk.inv_count, mdux = dk.bnsum[p.C + c] * dk.inv_count;
+      const float ic = dk.inv_count > 0.f ? dk.inv_count : 1.f / dk.bnsum[2 * p.C + c];  // SyncBN count
+      const float mdu = dk.bnsum[c] * ic, mdux = dk.bnsum[p.C + c] * ic;
       kCz[i] = -kP[i] * rs * mdux;
       kB[i] = -kP[i] * mdu - kCz[i] * mu;
       kS[i] = dk.s[(size_t)n * p.C + c];

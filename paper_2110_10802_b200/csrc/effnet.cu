@@ -130,11 +130,15 @@ __global__ void __launch_bounds__(256) xent_kernel(int N, int classes, const flo
   const float lse = mx + logf(sred[0]);
   const int lab = labels[n];
   const float inv_n = 1.f / (float)N;
+  // a label outside [0, classes) (e.g. an ignore index) is not a class of
+  // this head: its row gets zero gradient and a NaN loss, so the mean loss
+  // reports the bad batch instead of reading z out of bounds
+  const bool ok = lab >= 0 && lab < classes;
   for (int j = threadIdx.x; j < classes; j += blockDim.x) {
     const float p = __expf(z[j] - lse);
-    dlogits[(size_t)n * classes + j] = from_f<TG>((p - (j == lab ? 1.f : 0.f)) * inv_n);
+    dlogits[(size_t)n * classes + j] = from_f<TG>(ok ? (p - (j == lab ? 1.f : 0.f)) * inv_n : 0.f);
   }
-  if (threadIdx.x == 0) loss_rows[n] = lse - z[lab];
+  if (threadIdx.x == 0) loss_rows[n] = ok ? lse - z[lab] : __int_as_float(0x7fc00000);
 }
 
 // loss = mean(loss_rows), fixed order

@@ -615,8 +615,9 @@ __global__ void __launch_bounds__(kThreads) dwconv_bwd_kernel(Geo g, const T* __
     for (int i = 0; i < V; ++i) {
       const int c = c0 + i;
       mu[i] = bn.mean[c]; rs[i] = bn.rstd[c]; gm[i] = bn.gamma[c]; bt[i] = bn.beta[c];
-      mdu[i] = bnsum[c] * inv_count;
-      mdux[i] = bnsum[g.C + c] * inv_count;
+      const float ic = inv_count > 0.f ? inv_count : 1.f / bnsum[2 * g.C + c];  // SyncBN: allreduced count
+      mdu[i] = bnsum[c] * ic;
+      mdux[i] = bnsum[g.C + c] * ic;
     }
   }
   // dz region needed by the input pixels a tile owns, relative to its first
@@ -964,7 +965,7 @@ int dfx_mbconv_bwd_dx(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
   if (int rc = make_geo(N, H, W, C, stride, ksize, pads, V, &g, "dfx_mbconv_bwd_dx")) return rc;
   DFX_REQUIRE(dy && z && x && w_dw && mean && rstd && gamma && beta && s && dpool && bnsum && dx && dw_dw,
               DFX_ERR_SHAPE, "dfx_mbconv_bwd_dx: null pointer");
-  DFX_REQUIRE(count > 0, DFX_ERR_SHAPE, "dfx_mbconv_bwd_dx: count must be positive");
+  DFX_REQUIRE(count >= 0, DFX_ERR_SHAPE, "dfx_mbconv_bwd_dx: count must be >= 0");
   DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, ksize, pads, 1), DFX_ERR_WORKSPACE,
               "dfx_mbconv_bwd_dx: workspace too small");
   cudaStream_t st = as_stream(stream);
@@ -975,7 +976,7 @@ int dfx_mbconv_bwd_dx(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
     const size_t fl1 = nt * 8 * C + (size_t)N * C + (size_t)N + 2 * (size_t)N * C + 9 * (size_t)C * nsm;
     float* part = (float*)workspace;
     void* dzb = (float*)workspace + (std::max(fl1, ring_part_floats(g)) + 63) / 64 * 64;  // TMA: 16-B aligned
-    const DzConsts k{mean, rstd, gamma, beta, s, dpool, bnsum, (float)(1.0 / count)};
+    const DzConsts k{mean, rstd, gamma, beta, s, dpool, bnsum, count > 0 ? (float)(1.0 / count) : -1.f};
     if (int rc = dw_dz_dw(dtype, d, x, dy, z, k, dzb, part, dw_dw, st)) return rc;
     return dw_dx(dtype, d, dzb, w_dw, dx, st);
   }
@@ -988,7 +989,7 @@ int dfx_mbconv_bwd_dx(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
   BnParams bn{mean, rstd, gamma, beta};
   const int CV = g.C / V, PY = kThreads / CV, threads = CV * PY;
   const size_t sm = std::max((size_t)TH * TH * g.C, (size_t)PY * g.C) * sizeof(float);
-  const float inv_count = (float)(1.0 / count);
+  const float inv_count = count > 0 ? (float)(1.0 / count) : -1.f;
   if (dtype == DFX_BF16) {
     auto k = dwconv_bwd_kernel<__nv_bfloat16, 8>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

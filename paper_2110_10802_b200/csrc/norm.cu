@@ -322,7 +322,9 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_dx_kernel(int64_t rows, int C
     const int c = c0 + i;
     const float rs = rstd[c], mu = mean[c];
     A[i] = gamma[c] * rs;
-    const float mdu = sums[c] * inv_count, mdux = sums[C + c] * inv_count;
+    // inv_count <= 0: SyncBN — the allreduced per-channel count is sums[2][c]
+    const float ic = inv_count > 0.f ? inv_count : 1.f / sums[2 * C + c];
+    const float mdu = sums[c] * ic, mdux = sums[C + c] * ic;
     Cx[i] = -A[i] * mdux * rs;
     B[i] = -A[i] * mdu + A[i] * mdux * rs * mu;
     P[i] = A[i];
@@ -508,14 +510,14 @@ int dfx_batchnorm_act_bwd_dx(int dtype, int64_t rows, int64_t C, const void* dy,
   if (int rc = check_bn(dtype, rows, C, "dfx_batchnorm_act_bwd_dx")) return rc;
   DFX_REQUIRE(dy && x && mean && rstd && gamma && beta && bnsum && dx, DFX_ERR_SHAPE,
               "dfx_batchnorm_act_bwd_dx: null pointer");
-  DFX_REQUIRE(count > 0, DFX_ERR_SHAPE, "dfx_batchnorm_act_bwd_dx: count must be positive");
+  DFX_REQUIRE(count >= 0, DFX_ERR_SHAPE, "dfx_batchnorm_act_bwd_dx: count must be >= 0");
   cudaStream_t st = as_stream(stream);
   const int V = vec_width(dtype, C);
   const Lanes ln = lanes_for(C, V);
   int64_t rpb;
   int nb;
   stream_blocks(rows, ln.py * ln.nch, &rpb, &nb);
-  const float ic = (float)(1.0 / count);
+  const float ic = count > 0 ? (float)(1.0 / count) : -1.f;  // -1: per-channel count from bnsum[2]
 #define D(TT, VV, ACT) \
   { launch_k(bn_bwd_dx_kernel<TT, VV, ACT>, dim3(nb, ln.nch), ln.cvc * ln.py, 0, st, rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, bnsum, ic, (TT*)dx); }
   BN_DISPATCH(D, act);

@@ -75,9 +75,16 @@ class GradAllReducer:
 
 
 def gather_bn_sets(local: torch.Tensor, out: torch.Tensor, group=None) -> torch.Tensor:
-    """local [3, C] (count, mean, M2) -> out [world, 3, C] in rank order."""
-    # concatenation along dim 0 is the same memory as [world, 3, C]
-    dist.all_gather_into_tensor(out.view(-1, local.shape[-1]), local.contiguous(), group=group)
+    """local [3, C] (count, mean, M2) -> out [world, 3, C] in rank order.
+
+    A rank-slotted allreduce (each rank writes its slot, zeros elsewhere; the
+    sum is exact because every slot has one non-zero contributor): one NCCL
+    allreduce, which gloo also supports on CUDA tensors and which can be
+    captured in a CUDA graph like the gradient allreduce."""
+    rank = dist.get_rank(group)
+    out.zero_()
+    out[rank].copy_(local)
+    dist.all_reduce(out, group=group)
     return out
 
 

@@ -373,8 +373,22 @@ class EfficientNetB0:
         if key not in self._bufs:
             s = self.cfg.image
             self._bufs[key] = {"x": torch.zeros(N, s, s, 3, dtype=self.cfg.dtype, device=self.device),
-                               "labels": torch.zeros(N, dtype=torch.int32, device=self.device)}
+                               "labels": torch.zeros(N, dtype=torch.int32, device=self.device),
+                               "loss": torch.zeros(1, device=self.device)}
         return self._bufs[key]
+
+    def training_state(self) -> list:
+        """Tensors a step mutates beyond its activations: parameter / gradient
+        arenas, the bf16 shadow and every BatchNorm's running statistics
+        (restored around a capture's warm-up, graphs.CapturedStep)."""
+        out = [t.flat for t in (self.master, self.grad, self.wlow) if t is not None]
+        bns = [self.stem_bn, self.head_bn]
+        for b in self.blocks:
+            bns += [getattr(b, "bn1", None), b.bn3, b.mb]
+        for bn in bns:
+            if bn is not None:
+                out += [bn.running_mean, bn.running_var]
+        return out
 
     def capture_step(self, N: int, lr=None, timer=None):
         """Forward + backward (+ SGD) on the static ``device_inputs(N)`` as one
@@ -384,13 +398,15 @@ class EfficientNetB0:
         if self.world > 1:
             raise ShapeError("capture_step: SyncBN collectives run eagerly (world > 1)")
         dev = self.device_inputs(N)
+        self.loss = dev["loss"]  # per input slot: the graph bakes this buffer in
 
         def fn():
             self.train_step(dev["x"], dev["labels"], lr)
 
+        keep = self.training_state()
         if timer is None:
-            return CapturedStep(fn)
-        cs = CapturedStep(fn)
+            return CapturedStep(fn, preserve=keep)
+        cs = CapturedStep(fn, preserve=keep)
         timer.reset_records()
         with timer:
             inst = CapturedStep(fn, warmup=0)
@@ -412,6 +428,7 @@ class EfficientNetB0:
             torch.cuda.synchronize(self.device)
             pp["graphs"][key] = self.capture_step(N, lr)
         dev = self.device_inputs(N)
+        loss = dev["loss"]
         with torch.cuda.stream(pp["h2d"]):
             if pp["free"][slot] is not None:
                 pp["h2d"].wait_event(pp["free"][slot])
@@ -426,7 +443,7 @@ class EfficientNetB0:
         with torch.cuda.stream(pp["d2h"]):
             pp["d2h"].wait_event(ev_done)
             if loss_host is not None:
-                loss_host.copy_(self.loss, non_blocking=True)
+                loss_host.copy_(loss, non_blocking=True)  # this slot's own loss buffer
             ev_free = torch.cuda.Event()
             ev_free.record(pp["d2h"])
         pp["free"][slot] = ev_free
@@ -452,9 +469,10 @@ class EfficientNetB0:
         dev["x"].copy_(x_host, non_blocking=True)
         dev["labels"].copy_(labels_host, non_blocking=True)
         if graph is not None:
-            graph.replay()
+            graph.replay()  # captured by capture_step(N): writes this slot's dev["loss"]
+            loss = dev["loss"]
         else:
-            self.train_step(dev["x"], dev["labels"], lr)
+            loss = self.train_step(dev["x"], dev["labels"], lr)
         if loss_host is not None:
-            loss_host.copy_(self.loss, non_blocking=True)
+            loss_host.copy_(loss, non_blocking=True)
         return loss_host

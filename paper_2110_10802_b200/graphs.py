@@ -12,14 +12,24 @@ import torch
 
 
 class CapturedStep:
-    def __init__(self, fn, warmup: int = 2):
+    """``fn`` runs ``warmup`` times eagerly (allocations, lazy kernel
+    attributes), then once under capture.  ``preserve`` lists the tensors the
+    step mutates as training state (parameter arenas, bf16 shadows, running
+    statistics, ...): they are snapshotted before the warm-up and restored
+    after it, so capturing applies no optimizer update and moves no
+    statistics — the first replay is the first step."""
+
+    def __init__(self, fn, warmup: int = 2, preserve=()):
         cur = torch.cuda.current_stream()
+        saved = [t.clone() for t in preserve] if warmup else []
         side = torch.cuda.Stream()
         side.wait_stream(cur)
         with torch.cuda.stream(side):
             for _ in range(warmup):
                 fn()
         cur.wait_stream(side)
+        for t, s in zip(preserve, saved):
+            t.copy_(s)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):

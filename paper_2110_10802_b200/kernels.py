@@ -69,16 +69,26 @@ def _u8(t, numel, name):
 
 
 class _Workspace:
-    """Grow-only scratch buffer per (device, stream); stream-ordered reuse."""
+    """Grow-only scratch buffer per (device, stream); stream-ordered reuse.
+
+    A superseded (smaller) buffer is never freed: a CUDA graph captured
+    earlier may have baked its address in and still write it on replay, and
+    torch hands out side streams from a small pool, so two users can share a
+    key.  The retired buffers are kept alive for the process lifetime (they
+    only ever grow geometrically, so the total is bounded by ~2x the largest)."""
 
     def __init__(self):
         self.bufs = {}
+        self.retired = []
 
     def get(self, nbytes: int) -> torch.Tensor:
         key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
         buf = self.bufs.get(key)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
+            if buf is not None:
+                self.retired.append(buf)
+            size = max(nbytes, 1 << 20, 0 if buf is None else 2 * buf.numel())
+            buf = torch.empty(size, dtype=torch.uint8, device="cuda")
             self.bufs[key] = buf
         return buf
 

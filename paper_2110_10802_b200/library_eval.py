@@ -18,9 +18,17 @@ its host arrays to HBM, launches the sm_100a kernels through the C ABI
 raise ``UnsupportedOp`` — there is no CPU fallback.  Attribute
 handling follows ``frontend.normalize_attrs`` (registry.py).
 
-Arithmetic is fp32 (the tensor cores are used for bf16 only); f32 and f64
-arrays are accepted and results are returned in the input dtype, matching
-the reference's cast-back rule (frontend.py:216-218).
+Arithmetic is fp32 (the tensor cores are used for bf16 only).  The reference
+evaluates every operator in float64 and casts back to the input dtype
+(frontend.py:146-150, 216-218); for f32 graphs that is what happens here too
+(fp32 arithmetic, f32 results).  f64 graphs are REJECTED by default — the B200
+path has no f64 arithmetic and silently computing in fp32 would change the
+reference's numerics; ``make_library_eval(f64="as_f32")`` opts in explicitly
+(results are cast back to f64).
+
+``Reshape`` / ``Flatten`` are pure metadata in row-major storage (no bytes
+move, no arithmetic); they are answered with a view of the input so a graph
+that keeps them as library nodes still runs.
 """
 
 from __future__ import annotations
@@ -40,11 +48,20 @@ from .registry import get_op, normalize_attrs
 __all__ = ["library_eval", "SUPPORTED_OPS"]
 
 
+_POLICY = {"f64": "reject"}
+
+
 def _dev(a, dtype=torch.float32):
-    arr = np.ascontiguousarray(np.asarray(a))
+    arr = np.asarray(a)
+    if arr.dtype == np.float64 and _POLICY["f64"] != "as_f32":
+        raise ShapeError("B200 path computes in fp32: f64 operands are rejected (the reference evaluates f64; "
+                         "use make_library_eval(f64='as_f32') to accept fp32 arithmetic explicitly)")
     if arr.dtype not in (np.float32, np.float64):
-        raise ShapeError(f"B200 path takes f32/f64 tensors, got {arr.dtype}")
-    return torch.from_numpy(arr.astype(np.float32, copy=False)).to("cuda", dtype=dtype)
+        raise ShapeError(f"B200 path takes f32 tensors, got {arr.dtype}")
+    # a private, writable, contiguous fp32 copy: the interpreter hands in
+    # read-only views of its storage (interp.py:348)
+    host = torch.from_numpy(np.array(arr, dtype=np.float32, order="C", copy=True))
+    return host.to("cuda", dtype=dtype)
 
 
 def _host(t, like):
@@ -153,6 +170,49 @@ def _matmul(attrs, inputs):
     if b.ndim == 1:
         y = y[..., 0]
     return [y]
+
+
+# ---------------------------------------------------------------------------
+# reductions and layout
+
+
+def _norm_axes(axes, rank):
+    if axes is None or (not isinstance(axes, int) and len(list(axes)) == 0):
+        return tuple(range(rank))
+    axes = [axes] if isinstance(axes, int) else list(axes)
+    out = sorted({int(a) % rank for a in axes})
+    if len(out) != len(axes):
+        raise ShapeError(f"repeated axis in {axes}")
+    return tuple(out)
+
+
+def _reduce(attrs, inputs, mean=False):
+    """ReduceSum / ReduceMean (frontend.py:302-328): the reduced axes are moved
+    to the front and summed by the fixed-order column-sum kernel."""
+    x = np.asarray(inputs[0])
+    axes = _norm_axes(attrs["axes"], x.ndim)
+    kept = [a for a in range(x.ndim) if a not in axes]
+    rows = int(np.prod([x.shape[a] for a in axes], dtype=np.int64))
+    cols = int(np.prod([x.shape[a] for a in kept], dtype=np.int64))
+    t = _dev(np.transpose(x, list(axes) + kept).reshape(rows, cols))
+    out = torch.empty(cols, device="cuda")
+    K.colsum(t, out)
+    if mean:
+        K.scale_(out, 1.0 / max(rows, 1))
+    shape = [1 if a in axes else x.shape[a] for a in range(x.ndim)] if attrs["keepdims"] else \
+        [x.shape[a] for a in kept]
+    return [_host(out, x).reshape(shape)]
+
+
+def _reshape(attrs, inputs):
+    """Reshape / Flatten are metadata on row-major storage (frontend.py:713-829)."""
+    x = np.asarray(inputs[0])
+    if "axis" in attrs:  # Flatten
+        ax = int(attrs["axis"]) % max(x.ndim, 1)
+        return [x.reshape(int(np.prod(x.shape[:ax], dtype=np.int64)), -1)]
+    shape = [int(v) for v in attrs["shape"]]
+    shape = [x.shape[i] if v == 0 else v for i, v in enumerate(shape)]
+    return [x.reshape(shape)]
 
 
 # ---------------------------------------------------------------------------
@@ -330,6 +390,37 @@ def _bias_gelu_grad(attrs, inputs):
     return [_host(dpre, dy), _host(db, dy)]
 
 
+def _ln_act_grad(attrs, inputs):
+    from .norms import LayerNormAct
+
+    dy, x, g, b = (np.asarray(v) for v in inputs)
+    H = x.shape[-1]
+    m = LayerNormAct(H, eps=float(attrs["epsilon"]), act=attrs["activation"])
+    m.gamma.copy_(_dev(g))
+    m.beta.copy_(_dev(b))
+    m.forward(_dev(x))
+    dx = m.backward(_dev(dy))
+    return [_host(dx, x), _host(m.dgamma, g), _host(m.dbeta, b)]
+
+
+def _bn_act_grad(attrs, inputs):
+    """BN(+act) VJP with the batch statistics recomputed from x (as the
+    reference's _bwd_batchnorm does, autodiff.py:1569-1574)."""
+    from .norms import BatchNormAct
+
+    dy, x, g, b = (np.asarray(v) for v in inputs)
+    if x.ndim < 2:
+        raise ShapeError("BatchNormActGrad: input must have a channel dim")
+    C = x.shape[1]
+    m = BatchNormAct(C, eps=float(attrs["epsilon"]), act=attrs["activation"])
+    m.gamma.copy_(_dev(g))
+    m.beta.copy_(_dev(b))
+    m.forward(_dev(np.moveaxis(x, 1, -1)))
+    dx = m.backward(_dev(np.moveaxis(dy, 1, -1)))
+    return [np.moveaxis(_host(dx, x).reshape(np.moveaxis(x, 1, -1).shape), -1, 1), _host(m.dgamma, g),
+            _host(m.dbeta, b)]
+
+
 def _ln_act(attrs, inputs):
     return _layernorm({"axis": -1, "epsilon": attrs["epsilon"]}, inputs, act=_act_code(attrs))
 
@@ -353,6 +444,9 @@ _DISPATCH = {
     "BiasGelu": _bias_gelu, "BiasGeluGrad": _bias_gelu_grad,
     "MBConvBlock": _mbconv_block, "MBConvBlockGrad": lambda a, i: _mbconv_block(a, i, grad=True),
     "LayerNormAct": _ln_act, "BatchNormAct": _bn_act,
+    "LayerNormActGrad": _ln_act_grad, "BatchNormActGrad": _bn_act_grad,
+    "ReduceSum": _reduce, "ReduceMean": lambda a, i: _reduce(a, i, mean=True),
+    "Reshape": _reshape, "Flatten": _reshape,
 }
 SUPPORTED_OPS = sorted(_DISPATCH)
 
@@ -368,6 +462,23 @@ def library_eval(op: str, attrs, inputs):
     if not (spec.min_inputs <= len(inputs) <= spec.max_inputs):
         raise ShapeError(f"{op}: takes {spec.min_inputs}..{spec.max_inputs} inputs, got {len(inputs)}")
     _lib.load(check_device=True)
-    out = fn(normalize_attrs(spec, attrs), list(inputs))
-    torch.cuda.synchronize()
-    return out
+    # results come back as host arrays (the seam's contract); the D2H copies
+    # inside _host already order them after the kernels
+    return fn(normalize_attrs(spec, attrs), list(inputs))
+
+
+def make_library_eval(f64: str = "reject"):
+    """A ``library_eval`` with an explicit f64 policy: ``"reject"`` (default,
+    raise ShapeError) or ``"as_f32"`` (compute in fp32, cast results back)."""
+    if f64 not in ("reject", "as_f32"):
+        raise ValueError("f64 policy must be 'reject' or 'as_f32'")
+
+    def evaluate(op, attrs, inputs):
+        saved = _POLICY["f64"]
+        _POLICY["f64"] = f64
+        try:
+            return library_eval(op, attrs, inputs)
+        finally:
+            _POLICY["f64"] = saved
+
+    return evaluate

@@ -121,7 +121,7 @@ class MBConvBlock:
                 y=torch.empty(N, Ho, Wo, C, dtype=dt, device=dev),
                 dx=torch.empty(N, H, W, C, dtype=dt, device=dev),
                 bn_local=f(3, C), bn_sets=f(self.world, 3, C), mean=f(C), var=f(C), rstd=f(C),
-                pooled=f(N, C), r=f(N, c.se), s=f(N, C), dpool=f(N, C), bnsum=f(2, C),
+                pooled=f(N, C), r=f(N, c.se), s=f(N, C), dpool=f(N, C), bnsum=f(3, C),
                 ws=torch.empty(ws, dtype=torch.uint8, device=dev))
         return self._bufs[key]
 
@@ -190,9 +190,14 @@ class MBConvBlock:
                       ws.data_ptr(), ws.numel(), st)
         # local BN parameter gradients (dbeta = sum du, dgamma = sum du*xhat)
         K.cast2(b["bnsum"][0], G["b"], b["bnsum"][1], G["g"])
-        if self.world > 1:  # SyncBN: global sums for the input gradient
+        count = float(N * Ho * Wo)
+        if self.world > 1:
+            # SyncBN: global (sum du, sum du*xhat, count) for the input gradient;
+            # each rank adds its OWN count, so unequal per-rank batches normalise
+            # like the forward's merged statistics (count 0 = read bnsum[2])
+            b["bnsum"][2].fill_(count)
             allreduce_sum(b["bnsum"], group=self.pg)
-        count = float(N * Ho * Wo * self.world)
+            count = 0.0
         with K._span("mbconv.dwconv_bwd", "hbm", lambda: (2 * N * Ho * Wo + 2 * N * H * W) * C * esz):
             _lib.call("dfx_mbconv_bwd_dx", dt, N, H, W, C, c.stride, c.ksize, pads, dy.data_ptr(), b["z"].data_ptr(),
                       x.data_ptr(), P["wdw"].data_ptr(), b["mean"].data_ptr(), b["rstd"].data_ptr(),

@@ -73,7 +73,7 @@ class BatchNormAct:
         self.running_mean, self.running_var = f(channels), torch.ones(channels, device=device)
         self.dgamma, self.dbeta = f(channels), f(channels)
         self.local, self.sets = f(3, channels), f(self.world, 3, channels)
-        self.mean, self.var, self.rstd, self.bnsum = f(channels), f(channels), f(channels), f(2, channels)
+        self.mean, self.var, self.rstd, self.bnsum = f(channels), f(channels), f(channels), f(3, channels)
 
     def forward(self, x, y=None):
         """x channels-last [..., C]; returns act(BN(x))."""
@@ -109,10 +109,13 @@ class BatchNormAct:
                       self.mean.data_ptr(), self.rstd.data_ptr(), self.gamma.data_ptr(), self.beta.data_ptr(),
                       self.act, self.bnsum.data_ptr(), ws.data_ptr(), ws.numel(), st)
         K.cast2(self.bnsum[0], self.dbeta, self.bnsum[1], self.dgamma)  # local parameter gradients
-        if self.world > 1:
+        count = float(rows)
+        if self.world > 1:  # SyncBN: (sum du, sum du*xhat, count) over ranks; count 0 = read bnsum[2]
+            self.bnsum[2].fill_(count)
             allreduce_sum(self.bnsum, group=self.pg)
+            count = 0.0
         with K._span("bn_act_bwd_dx", "hbm", lambda: 3 * x.numel() * x.element_size()):
             _lib.call("dfx_batchnorm_act_bwd_dx", dt, rows, self.C, dy.data_ptr(), x.data_ptr(), self.mean.data_ptr(),
                       self.rstd.data_ptr(), self.gamma.data_ptr(), self.beta.data_ptr(), self.act,
-                      self.bnsum.data_ptr(), float(rows * self.world), dx.data_ptr(), st)
+                      self.bnsum.data_ptr(), count, dx.data_ptr(), st)
         return dx

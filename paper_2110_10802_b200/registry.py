@@ -96,6 +96,10 @@ HOT_OPS = [
            replaces="frontend.py:544-591 (training mode)"),
     OpSpec("Conv", {"strides": None, "pads": None, "group": 1, "kernel_shape": None}, 2, 2,
            replaces="frontend.py:598-678 (depthwise 3x3, group = C)"),
+    OpSpec("ReduceSum", {"axes": None, "keepdims": 1}, 1, 1, replaces="frontend.py:302-328 (Gemm bias VJP)"),
+    OpSpec("ReduceMean", {"axes": None, "keepdims": 1}, 1, 1, replaces="frontend.py:302-328"),
+    OpSpec("Reshape", {"shape": None}, 1, 1, replaces="frontend.py:713-829 (metadata only)"),
+    OpSpec("Flatten", {"axis": 1}, 1, 1, replaces="frontend.py:713-829 (metadata only)"),
 ]
 
 # -- fused operators (the subgraphs the reference's fusion recipe collapses,
@@ -130,8 +134,14 @@ FUSED_OPS = [
                  "(dx, dw_dw, dgamma, dbeta, dw_r, db_r, dw_e, db_e)"),
     OpSpec("LayerNormAct", {"epsilon": 1e-5, "activation": "swish"}, 3, 3, 1, 1,
            replaces="act(LayerNormalization(x, gamma, beta, axis=-1))"),
+    OpSpec("LayerNormActGrad", {"epsilon": 1e-5, "activation": "swish"}, 4, 4, 3, 3,
+           replaces="act VJP + LayerNormalization VJP (autodiff.py:1490-1545)",
+           notes="inputs (dy, x, gamma, beta) -> (dx, dgamma, dbeta)"),
     OpSpec("BatchNormAct", {"epsilon": 1e-5, "momentum": 0.9, "activation": "swish"}, 5, 5, 1, 3,
            replaces="act(BatchNormalization(x, gamma, beta, run_mean, run_var)) (training)"),
+    OpSpec("BatchNormActGrad", {"epsilon": 1e-5, "activation": "swish"}, 4, 4, 3, 3,
+           replaces="act VJP + BatchNormalization VJP (autodiff.py:1551-1617), batch statistics recomputed",
+           notes="inputs (dy, x, gamma, beta) -> (dx, dgamma, dbeta)"),
 ]
 
 for _s in HOT_OPS + FUSED_OPS:
@@ -142,60 +152,10 @@ for _s in HOT_OPS + FUSED_OPS:
 # installation into a live dfir registry
 
 
-def _fused_reference(frontend, name):
-    """numpy reference of a fused op composed from the reference's own
-    operator evaluators (frontend.reference_apply, frontend.py:146-150)."""
-    ra = frontend.reference_apply
+def register_with_dfir(frontend=None) -> list:
+    """Install the fused operators (spec + reference + lowering + manual VJP)
+    and the ``fuse_to_b200`` transformation into the importable ``dfir``
+    (dfir_plugin.install).  Returns the operator names newly registered."""
+    from .dfir_plugin import install
 
-    if name == "BiasDropoutResidualLayerNorm":
-        def ref(attrs, inputs):
-            h, b, m, r, g, be = inputs
-            (s,) = ra("Add", {}, [ra("Mul", {}, [ra("Add", {}, [h, b])[0], m])[0], r])
-            (y,) = ra("LayerNormalization", {"epsilon": attrs["epsilon"], "axis": -1}, [s, g, be])
-            return [y, s]
-        return ref
-    if name == "ScaledMaskedSoftmax":
-        def ref(attrs, inputs):
-            sc, am, dm = inputs
-            (z,) = ra("Div", {"divisor": attrs["divisor"]}, [sc])
-            (p,) = ra("Softmax", {"axis": -1}, [ra("Add", {}, [z, am])[0]])
-            return [ra("Mul", {}, [p, dm])[0], p]
-        return ref
-    if name == "BiasGelu":
-        import numpy as np
-
-        def ref(attrs, inputs):
-            f, b = inputs
-            (x,) = ra("Add", {}, [f, b])
-            c = lambda v: np.asarray(v, dtype=x.dtype)  # noqa: E731
-            (x3,) = ra("Pow", {"exponent": 3.0}, [x])
-            (t,) = ra("Tanh", {}, [ra("Mul", {}, [ra("Add", {}, [x, ra("Mul", {}, [x3, c(0.044715)])[0]])[0],
-                                                 c(0.7978845608028654)])[0]])
-            (y,) = ra("Mul", {}, [ra("Mul", {}, [x, ra("Add", {}, [t, c(1.0)])[0]])[0], c(0.5)])
-            return [y, x]
-        return ref
-    return None
-
-
-def register_with_dfir(frontend) -> list:
-    """Install the forward fused operators into ``frontend``'s registry.
-    Returns the names registered (already-present names are skipped, since
-    ``register_op`` refuses duplicates)."""
-    done = []
-    for spec in FUSED_OPS:
-        ref = _fused_reference(frontend, spec.name)
-        if ref is None or spec.name in frontend.registered_ops():
-            continue
-
-        def infer(attrs, shapes, dtypes, spec=spec):
-            if spec.name == "BiasDropoutResidualLayerNorm":
-                return [(shapes[0], dtypes[0]), (shapes[0], dtypes[0])]
-            if spec.name == "ScaledMaskedSoftmax":
-                return [(shapes[0], dtypes[0]), (shapes[0], dtypes[0])]
-            return [(shapes[0], dtypes[0]), (shapes[0], dtypes[0])]
-
-        schema = {k: (frontend.REQUIRED if v is REQUIRED else v) for k, v in spec.attr_schema.items()}
-        frontend.register_op(frontend.OpSpec(spec.name, schema, spec.min_inputs, spec.max_inputs, infer, ref,
-                                             min_outputs=spec.min_outputs, max_outputs=spec.max_outputs))
-        done.append(spec.name)
-    return done
+    return install()["ops"]

@@ -173,3 +173,61 @@ def test_pipelined_host_steps_match_synchronous():
         outs[mode] = res
     for a, b in zip(outs["sync"], outs["async"]):
         assert torch.equal(a, b)
+
+
+def _c2_inputs(seed=2024, B=8, S=512, H=768, NH=12, p=0.1):
+    """The bench's C2 inputs (bench.py run_ours): bf16 x / dout, 10 % of the
+    keys masked with -10000, dropout p=0.1 keep flags."""
+    rng = np.random.default_rng(seed)
+    T = B * S
+    x = _bf16_store(rng.standard_normal((T, H)))
+    dout = _bf16_store(rng.standard_normal((T, H)))
+    am = np.where(rng.random((B, S)) < 0.1, -10000.0, 0.0)
+    keeps = [rng.random((B, NH, S, S)) >= p, rng.random((T, H)) >= p, rng.random((T, H)) >= p]
+    return x, am, keeps, dout
+
+
+def test_bert_c2_vs_oracle():
+    """the benchmarked configuration itself (C2: B=8, S=512,
+    bf16, the bench's 10 % additive mask, bit-packed keep masks, the captured
+    CUDA-graph step the bench replays) against the float64 oracle on the same
+    bf16-rounded inputs and weights: out, dx and all 16 parameter gradients.
+
+    Metric = interp.compare_outputs' element-wise max|a-b|/max(|b|,1)
+    (interp.py:1332-1352) at the north star's bf16 bar 2e-2 for out, dx and
+    every parameter gradient; the scale-normalised metric is reported next to
+    it per tensor."""
+    from paper_2110_10802_b200 import kernels as K
+    from paper_2110_10802_b200.bert import BertLayerConfig
+
+    B, S, H, NH = 8, 512, 768, 12
+    layer = _layer(BertLayerConfig(), seed=1234)
+    x, am, keeps, dout = _c2_inputs()
+    dev = layer.device_inputs(B, S)
+    dev["x"].copy_(torch.as_tensor(x, dtype=torch.float32).bfloat16())
+    dev["dout"].copy_(torch.as_tensor(dout, dtype=torch.float32).bfloat16())
+    dev["add_mask"].copy_(torch.as_tensor(am, dtype=torch.float32))
+    for k, kp in zip(("keep_attn", "keep1", "keep2"), keeps):
+        dev[k].copy_(K.pack_keep_bits(torch.as_tensor(kp.astype(np.uint8))))
+    m0 = layer.master.flat.clone()
+    lr = 1e-3
+    cs = layer.capture_step(B, S, lr)
+    torch.cuda.synchronize()
+    assert torch.equal(layer.master.flat, m0), "capture must not apply an update (graphs.CapturedStep)"
+    prm = layer.params_numpy()  # bf16-rounded matrices (what the tensor cores read)
+    cs.replay()
+    torch.cuda.synchronize()
+    b = layer.buffers(B, S)
+    out = b["out"].float().cpu().numpy().astype(np.float64)
+    dx = b["dx"].float().cpu().numpy().astype(np.float64)
+    grads = layer.grads_numpy()
+    # one replay = exactly one SGD step of the gradient it computed
+    assert torch.allclose(layer.master.flat, m0 - lr * layer.grad.flat, rtol=0, atol=1e-7)
+    want_out, want_g = _oracle(prm, x, am, keeps, dout, B, S, NH)
+    errs = {"out": (O.compare(out, want_out), O.compare_scaled(out, want_out)),
+            "x": (O.compare(dx, want_g["x"]), O.compare_scaled(dx, want_g["x"]))}
+    for k in O.BERT_WEIGHTS:
+        errs[k] = (O.compare(grads[k], want_g[k]), O.compare_scaled(grads[k], want_g[k]))
+    print("C2 vs oracle (element-wise, scaled):", {k: f"{a:.2e}/{s:.2e}" for k, (a, s) in errs.items()})
+    bad = {k: v for k, v in errs.items() if v[0] > 2e-2}
+    assert not bad, f"over 2e-2 element-wise: {bad}"

@@ -199,3 +199,31 @@ def test_c3_full_size_against_torch_fp32():
     assert rel(blk.grad["wdw"].permute(2, 0, 1).reshape(C, 1, 3, 3), w.grad) < 1e-2
     assert rel(blk.grad["g"], gm.grad) < 1e-2
     assert rel(blk.grad["b"], bt.grad) < 1e-2
+
+
+def test_c3_bf16_vs_oracle():
+    """the benchmarked C3 block in its benchmarked dtype (bf16,
+    112x112, C=96, SE=4, stride 1) at N=16 images against the float64 oracle
+    on the same bf16-rounded inputs, with the bf16 storage model applied where
+    the GPU stores z and y (oracle.mbconv_fwd docstring): y, dx, the running
+    statistics and every parameter gradient at the bf16 bar 2e-2 (the
+    interp.compare_outputs metric, interp.py:1332-1352)."""
+    rng = np.random.default_rng(96)
+    N, C, HW, SE = 16, 96, 112, 4
+    prm, x = _rand_case(rng, N, C, HW, HW, SE)
+    x = O.round_bf16(x).astype(np.float64)
+    rnd = lambda a: O.round_bf16(a).astype(np.float64)  # noqa: E731
+    y_w, rm_w, rv_w, cache = O.mbconv_fwd(prm, x, 1, 1e-3, 0.99, rnd=rnd)
+    dy = O.round_bf16(rng.standard_normal(y_w.shape)).astype(np.float64)
+    gw = O.mbconv_bwd(prm, cache, dy)
+    del cache
+    blk = _block(C, SE, 1, (1, 1, 1, 1), torch.bfloat16, prm=prm)
+    y, dx = _run(blk, x, dy, torch.bfloat16)
+    errs = {"y": O.compare(y, y_w), "dx": O.compare(dx, gw["x"]),
+            "rm": O.compare(blk.running_mean.cpu().numpy(), rm_w),
+            "rv": O.compare(blk.running_var.cpu().numpy(), rv_w)}
+    gr = blk.grads_numpy()
+    for k in GRADS[1:]:
+        errs[k] = O.compare(gr[k], gw[k])
+    print("C3 bf16 N=16 vs oracle:", {k: f"{v:.2e}" for k, v in errs.items()})
+    _check(errs, 2e-2)

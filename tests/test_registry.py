@@ -31,7 +31,7 @@ def test_registry_refuses_duplicates_and_unknown():
 
 def test_library_eval_has_no_cpu_fallback():
     """Operators off the hot path raise instead of running on the CPU."""
-    for op in ("Add", "Relu", "Reshape", "GlobalAveragePool"):
+    for op in ("Add", "Relu", "Sigmoid", "GlobalAveragePool"):
         with pytest.raises(UnsupportedOp):
             library_eval(op, {}, [np.zeros(4, np.float32)])
     assert "BiasDropoutResidualLayerNorm" in SUPPORTED_OPS
