@@ -420,6 +420,15 @@ class BertEncoderLayer:
         sgd = nparam * (4 + 4 + 4 + (2 if self.wlow is not None else 0))
         return int(fwd + bwd + sgd)
 
+    def step_flops(self, B: int, S: int) -> int:
+        """Algorithmic contraction FLOPs of one fwd+bwd step (SURVEY.md §8a row
+        a8): QKV, QKᵀ, PV, out-proj, FFN1, FFN2 forward, x3 for the backward."""
+        c = self.cfg
+        T = B * S
+        fwd = 2 * T * c.hidden * (3 * c.hidden) + 2 * 2 * B * c.heads * S * S * c.head_dim \
+            + 2 * T * c.hidden * c.hidden + 2 * 2 * T * c.hidden * c.ffn
+        return 3 * fwd
+
     def host_inputs_bytes(self, B: int, S: int) -> tuple[int, int]:
         """(H2D, D2H) bytes per train_step_host call."""
         c = self.cfg

@@ -125,12 +125,13 @@ class KernelTimer:
 
     def collect(self):
         torch.cuda.synchronize()
-        for label, kind, work, e0, e1 in self.records:
+        for label, kind, work, nbytes, e0, e1 in self.records:
             a = self.totals.setdefault(label, {"label": label, "kind": kind, "calls": 0, "ms": 0.0,
-                                               "work": 0.0})
+                                               "work": 0.0, "bytes": 0.0})
             a["calls"] += 1
             a["ms"] += e0.elapsed_time(e1)
             a["work"] += work
+            a["bytes"] += nbytes if nbytes is not None else (work if kind == "hbm" else 0.0)
 
     def reset_records(self):
         self.records = []
@@ -145,10 +146,10 @@ _TIMER = None
 
 
 class _Span:
-    __slots__ = ("label", "kind", "work", "e0")
+    __slots__ = ("label", "kind", "work", "nbytes", "e0")
 
-    def __init__(self, label, kind, work):
-        self.label, self.kind, self.work = label, kind, work
+    def __init__(self, label, kind, work, nbytes=None):
+        self.label, self.kind, self.work, self.nbytes = label, kind, work, nbytes
 
     def __enter__(self):
         self.e0 = torch.cuda.Event(enable_timing=True, external=True)
@@ -158,7 +159,7 @@ class _Span:
         e1 = torch.cuda.Event(enable_timing=True, external=True)
         e1.record()
         if _TIMER is not None:
-            _TIMER.records.append((self.label, self.kind, self.work, self.e0, e1))
+            _TIMER.records.append((self.label, self.kind, self.work, self.nbytes, self.e0, e1))
 
 
 class _Null:
@@ -176,12 +177,16 @@ _LABEL = [None]
 _LABEL_NEST = False  # profiling tools: "outer/inner" call-site labels
 
 
-def _span(default_label, kind, work_fn):
+def _span(default_label, kind, work_fn, bytes_fn=None):
+    """``work_fn``: algorithmic bytes (kind "hbm") or flops (contractions);
+    ``bytes_fn`` (contractions): compulsory operand bytes, so a contraction
+    whose arithmetic intensity is below the ridge point is judged against HBM."""
     if _TIMER is None:
         return _NULL
+    nb = bytes_fn() if bytes_fn is not None else None
     if _LABEL_NEST and _LABEL[0]:
-        return _Span(f"{_LABEL[0]}/{default_label}", kind, work_fn())
-    return _Span(_LABEL[0] or default_label, kind, work_fn())
+        return _Span(f"{_LABEL[0]}/{default_label}", kind, work_fn(), nb)
+    return _Span(_LABEL[0] or default_label, kind, work_fn(), nb)
 
 
 class label:
@@ -478,7 +483,13 @@ def gemm(a, b, d, epilogue=_lib.EPI_NONE, alpha=1.0, beta=1.0, bias=None, aux=No
         _lib.check(lib.dfx_gemm(g, _stream()), "dfx_gemm")
         return d
     kind = "tensor" if lib.dfx_gemm_uses_tensor_cores(g) else "simt"
-    with _span("gemm", kind, lambda: 2.0 * g.m * g.n * g.k * g.batch1 * g.batch2):
+
+    def nbytes():  # A, B read once, D written once (+ the aux operand read)
+        z = g.batch1 * g.batch2
+        return z * (g.m * g.k * a.element_size() + g.n * g.k * b.element_size()
+                    + g.m * g.n * d.element_size() * (1 + (aux is not None) + (aux_out is not None)))
+
+    with _span("gemm", kind, lambda: 2.0 * g.m * g.n * g.k * g.batch1 * g.batch2, nbytes):
         _lib.check(lib.dfx_gemm(g, _stream()), "dfx_gemm")
     return d
 

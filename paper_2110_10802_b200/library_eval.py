@@ -194,9 +194,12 @@ def _reduce(attrs, inputs, mean=False):
     kept = [a for a in range(x.ndim) if a not in axes]
     rows = int(np.prod([x.shape[a] for a in axes], dtype=np.int64))
     cols = int(np.prod([x.shape[a] for a in kept], dtype=np.int64))
-    t = _dev(np.transpose(x, list(axes) + kept).reshape(rows, cols))
-    out = torch.empty(cols, device="cuda")
+    xt = np.transpose(x, list(axes) + kept).reshape(rows, cols)
+    pad = -cols % 8  # the column-sum kernel reads 16-byte vectors: pad with zero columns
+    t = _dev(np.pad(xt, ((0, 0), (0, pad))) if pad else xt)
+    out = torch.empty(cols + pad, device="cuda")
     K.colsum(t, out)
+    out = out[:cols]
     if mean:
         K.scale_(out, 1.0 / max(rows, 1))
     shape = [1 if a in axes else x.shape[a] for a in range(x.ndim)] if attrs["keepdims"] else \
