@@ -1,0 +1,3 @@
+cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 120 python tools/attn_trace.py --fused
