@@ -38,6 +38,23 @@ ncta = B * NH * S // 128
 if "--dkdv" in sys.argv:  # dkdv timeline: 0 start, 1 K/V landed (MMA), 2-5 S_j ready, 6-9 Pd/dS_j stored, 10 grads done
     os.environ["DFX_ATTN_TRACE_DKDV"] = "1"
     sys.argv.append("--bwd")
+if "--fwd2" in sys.argv:  # online-softmax forward: 0 start, 1 Q landed, 2-5 S_j ready, 6-9 P_j stored, 10 O done, 11 exit
+    tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
+    fn(tr.data_ptr())
+    run()
+    torch.cuda.synchronize()
+    fn(None)
+    t = tr.view(ncta, 16).cpu().double()
+    rel = (t - t[:, 0].min()) / 1e3
+    names = ["start->Q", "Q->S0", "S0->P0", "P0->S1", "S1->P1", "P1->S2", "S2->P2", "P2->S3", "S3->P3", "P3->O", "O->exit"]
+    order = [0, 1, 2, 6, 3, 7, 4, 8, 5, 9, 10, 11]
+    d = [rel[:, order[i + 1]] - rel[:, order[i]] for i in range(len(order) - 1)]
+    print("fwd2 mean phase durations (us):", {n: round(x.mean().item(), 2) for n, x in zip(names, d)})
+    print("per-CTA total mean", round((rel[:, 11] - rel[:, 0]).mean().item(), 2), "kernel span",
+          round(rel[:, 11].max().item(), 2))
+    starts = sorted(rel[:, 0].tolist())
+    print("CTA start quantiles:", [round(starts[int(q * (len(starts) - 1))], 2) for q in (0, .25, .5, .75, 1)])
+    sys.exit(0)
 if "--fused" in sys.argv:  # fused backward: 0 start, 1 K/V/O landed, 2 D exchanged, 3-6 S_j ready, 7-10 dQ_j reduced, 11 epilogue, 12 exit
     run()
     dctx = torch.randn_like(ctx)

@@ -1,3 +1,4 @@
+#!/bin/bash
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 120 python tools/attn_trace.py --fused
+timeout 120 python tools/attn_trace.py ${TRACE_ARGS:---fused}
