@@ -712,7 +712,6 @@ struct AttnBwdParams {
   float ks, sc2, scale;       // keep scale, inv_divisor*log2e, inv_divisor
   __nv_bfloat16* dqkv;        // [T, ld_dqkv]: dQ | dK | dV column blocks
   float* bias_part;           // [B*S/128][3H]: per-strip column sums of dQ | dK | dV (qkv bias gradient)
-  uint32_t dq_lbo, dq_sbo;    // UMMA descriptor strides of the MN-major dS operand (fused backward)
 };
 
 constexpr int CH = 128;  // keys (dq) / queries (dkdv) per chunk
@@ -1215,389 +1214,6 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
   }
 }
 
-// ------------------------------------------------- fused backward (one kernel)
-// CTA = (b, h, 128-key strip); the S/128 key strips of one head form a thread
-// block CLUSTER.  Per 128-query chunk j the CTA computes, from K/V (resident)
-// and Q_j / dO_j (TMA ring):
-//   Sᵀ = K·Q_jᵀ, dPdᵀ = V·dO_jᵀ                      (TMEM, once per tile pair)
-//   P = exp2(Sᵀ·c + mask - lse), dS = P∘(dPd∘keep·ks - D), Pd = P∘keep  (smem)
-//   dV += Pdᵀ·dO_j, dK += dSᵀ·Q_j                     (TMEM accumulators)
-//   dQ_j(partial) = dS_j·K                           (TMEM, double-buffered)
-// i.e. the five MMAs of attention's backward with ONE exp pass (the previous
-// dq + dk/dv kernel pair recomputed S and dPd in each: 7 MMAs, 2 exp passes).
-// The dQ_j partials of the cluster's CTAs are summed through distributed
-// shared memory in a FIXED rank order (each CTA reduces 32 of the chunk's 128
-// rows) — deterministic, no atomics.  D = rowsum(dO∘O) is formed in-cluster:
-// CTA r computes it for query block r and the others read it over DSMEM.
-constexpr int kDqWarps = 4;
-constexpr int kBwdWarps = 2 + kSoftWarps + kDqWarps;
-constexpr int kBwdThreads = kBwdWarps * 32;
-
-struct BwdSmem {
-  static constexpr int K = 0;
-  static constexpr int V = K + QT * 128;
-  static constexpr int NST = 2;
-  static constexpr int STAGE = 2 * CH * 128;          // Q_j | dO_j
-  static constexpr int RING = V + QT * 128;
-  static constexpr int PD = RING + NST * STAGE;
-  static constexpr int DS = PD + QT * CH * 2;
-  static constexpr int DQP = DS + QT * CH * 2;        // fp32 [128 q][64] dQ partial (prologue: O_r | dO_r)
-  static constexpr int LSE = DQP + CH * DH * 4;
-  static constexpr int DEL = LSE + kMaxSeq * 4;
-  static constexpr int RED = DEL + kMaxSeq * 4;       // [4][128] floats
-  static constexpr int SCR = RED + 4 * QT * 4;        // 2 x [8][64] floats (column-sum scratch)
-  static constexpr int LUT = SCR + 2 * 8 * 64 * 4;
-  static constexpr int BAR = LUT + 16 * 16;
-  static constexpr int TOTAL = BAR + 256 + KB;
-};
-static_assert(BwdSmem::TOTAL <= 227 * 1024, "attention backward exceeds shared memory");
-
-// Warp roles: 0 TMA producer, 1 MMA issuer, 2..17 softmax (P, dS, Pd; four per
-// TMEM lane quadrant, 32 query columns each), 18..21 dQ (drain the dQ_j
-// partial from TMEM, exchange it over DSMEM, reduce 128/nch rows of it).
-// Cross-CTA signalling uses mbarriers with the CUTLASS ClusterBarrier
-// semantics (remote arrive / local try_wait at their default CTA scope): a
-// cluster-scope release / acquire compiles to a memory barrier + L1
-// invalidate per poll, which cost more than the whole exchange.
-__global__ void __launch_bounds__(kBwdThreads, 1)
-attn_bwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
-                const __grid_constant__ CUtensorMap map_o, const AttnBwdParams p) {
-  pdl_trigger();
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const uint32_t sbase = smem_u32(smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BwdSmem::BAR);
-  uint64_t *bar_a = bar, *bar_s = bar + 1, *bar_tfree = bar + 2, *bar_pds = bar + 3, *bar_pdsfree = bar + 4;
-  uint64_t* full = bar + 5;         // [NST]
-  uint64_t* empty = bar + 7;        // [NST]
-  uint64_t* bar_dq = bar + 9;       // [2] dQ chunk in TMEM buffer
-  uint64_t* bar_dqfree = bar + 11;  // [2]
-  uint64_t* bar_ready = bar + 13;   // partials of every CTA stored (cluster)
-  uint64_t* bar_used = bar + 14;    // every CTA read my partial (cluster)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-  constexpr int NST = BwdSmem::NST;
-  float* lse_s = reinterpret_cast<float*>(smem + BwdSmem::LSE);
-  float* del_s = reinterpret_cast<float*>(smem + BwdSmem::DEL);
-  float* red = reinterpret_cast<float*>(smem + BwdSmem::RED);
-
-  const int S = p.S, nch = S / CH;             // query chunks = key strips = cluster size
-  const uint32_t kb = cluster_rank();          // this CTA's key strip
-  const int bh = blockIdx.x / nch;
-  const int b = bh / p.NH, h = bh % p.NH;
-  const int k0 = kb * QT, row0 = b * S;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    mbar_init(bar_a, 1);
-    mbar_init(bar_s, 1);
-    mbar_init(bar_tfree, kSoftWarps);
-    mbar_init(bar_pds, kSoftWarps);
-    mbar_init(bar_pdsfree, 1);
-    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&bar_dq[s], 1); mbar_init(&bar_dqfree[s], kDqWarps); }
-    mbar_init(bar_ready, nch * kDqWarps);
-    mbar_init(bar_used, nch * kDqWarps);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  cluster_arrive();  // phase 1: every CTA's barriers are initialised before any remote arrive
-  cluster_wait();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_wait();
-  if (threadIdx.x == 64) ATRACE(0);
-  constexpr uint32_t T_S = 0, T_DP = 128, T_DK = 256, T_DV = 320, T_DQ = 384;
-  const int qd = warp & 3;  // TMEM lane quadrant this warp may access
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // K, V strips, the head's lse row, and O / dO of query block kb (for D)
-      mbar_expect_tx(bar_a, 4 * QT * 128 + S * 4);
-      const uint32_t ba = smem_u32(bar_a);
-      bulk_g2s(lse_s, p.lse + (size_t)bh * S, S * 4, ba);
-      for (int u = 0; u < 2; ++u) {
-        const int r = row0 + k0 + 64 * u;
-        tma_load_4d_cg<1>(&map_qkv, ba, smem + BwdSmem::K + u * 8 * KB, p.H + h * DH, r, 0, 0);
-        tma_load_4d_cg<1>(&map_qkv, ba, smem + BwdSmem::V + u * 8 * KB, 2 * p.H + h * DH, r, 0, 0);
-        tma_load_4d_cg<1>(&map_o, ba, smem + BwdSmem::DQP + u * 8 * KB, h * DH, r, 0, 0);
-        tma_load_4d_cg<1>(&map_do, ba, smem + BwdSmem::DQP + 16 * KB + u * 8 * KB, h * DH, r, 0, 0);
-      }
-    }
-    __syncwarp();
-    cluster_arrive();  // phase 2 (nothing to publish)
-    if (lane == 0) {
-      for (int j = 0; j < nch; ++j) {
-        const int s = j % NST;
-        mbar_wait(&empty[s], ((j / NST) & 1) ^ 1);
-        mbar_expect_tx(&full[s], BwdSmem::STAGE);
-        const uint32_t bf = smem_u32(&full[s]);
-        uint8_t* stq = smem + BwdSmem::RING + s * BwdSmem::STAGE;
-        for (int u = 0; u < 2; ++u) {
-          tma_load_4d_cg<1>(&map_qkv, bf, stq + u * 8 * KB, h * DH, row0 + j * CH + 64 * u, 0, 0);
-          tma_load_4d_cg<1>(&map_do, bf, stq + CH * 128 + u * 8 * KB, h * DH, row0 + j * CH + 64 * u, 0, 0);
-        }
-      }
-    }
-    __syncwarp();
-    cluster_wait();
-  } else if (warp == 1) {
-    cluster_arrive();  // phase 2
-    if (lane == 0) {
-      const uint32_t idesc_s = make_idesc(CH, QT, 0, 0);
-      const uint32_t idesc_g = make_idesc(DH, QT, 0, 1);
-      const uint32_t idesc_q = make_idesc(DH, CH, 1, 1);  // dQ: A = dS (MN-major view of dSᵀ), B = K (MN-major)
-      const uint64_t kdesc = make_sdesc(sbase + BwdSmem::K, 16, 1024);
-      const uint64_t vdesc = make_sdesc(sbase + BwdSmem::V, 16, 1024);
-      mbar_wait(bar_a, 0);
-      auto issue_grads = [&](int c) {
-        mbar_wait(bar_pds, c & 1);
-        tc_fence_after();
-        const uint32_t stq = sbase + BwdSmem::RING + (c % NST) * BwdSmem::STAGE;
-        const uint64_t qmn = make_sdesc(stq, 8 * KB, 1024);
-        const uint64_t domn = make_sdesc(stq + CH * 128, 8 * KB, 1024);
-#pragma unroll
-        for (int kc = 0; kc < CH / 16; ++kc) {  // dV += Pdᵀ·dO_c ; dK += dSᵀ·Q_c
-          const uint64_t pd = make_sdesc(sbase + BwdSmem::PD + (kc >> 2) * 16 * KB, 16, 1024);
-          const uint64_t ds = make_sdesc(sbase + BwdSmem::DS + (kc >> 2) * 16 * KB, 16, 1024);
-          const uint32_t acc = (c > 0 || kc > 0) ? 1u : 0u;
-          tc_mma_cg<1>(tmem + T_DV, pd + 2 * (kc & 3), domn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
-          tc_mma_cg<1>(tmem + T_DK, ds + 2 * (kc & 3), qmn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
-        }
-        tc_commit_cg<1>(&empty[c % NST]);
-        // dQ_c = dS_c · K   (contraction over this strip's 128 keys)
-        if (c >= 2) mbar_wait(&bar_dqfree[c & 1], ((c >> 1) + 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kc = 0; kc < QT / 16; ++kc) {
-          const uint64_t adesc = make_sdesc(sbase + BwdSmem::DS + kc * 2048, p.dq_lbo, p.dq_sbo);
-          const uint64_t bdesc = make_sdesc(sbase + BwdSmem::K + kc * 2048, 8 * KB, 1024);
-          tc_mma_cg<1>(tmem + T_DQ + (c & 1) * DH, adesc, bdesc, idesc_q, kc > 0 ? 1u : 0u);
-        }
-        tc_commit_cg<1>(bar_pdsfree);
-        tc_commit_cg<1>(&bar_dq[c & 1]);
-      };
-      for (int j = 0; j < nch; ++j) {
-        mbar_wait(&full[j % NST], (j / NST) & 1);
-        if (j > 0) mbar_wait(bar_tfree, (j - 1) & 1);
-        tc_fence_after();
-        const uint32_t stq = sbase + BwdSmem::RING + (j % NST) * BwdSmem::STAGE;
-        const uint64_t qdesc = make_sdesc(stq, 16, 1024);
-        const uint64_t dodesc = make_sdesc(stq + CH * 128, 16, 1024);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          tc_mma_cg<1>(tmem + T_S, kdesc + 2 * kk, qdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
-          tc_mma_cg<1>(tmem + T_DP, vdesc + 2 * kk, dodesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
-        }
-        tc_commit_cg<1>(bar_s);
-        if (j > 0) issue_grads(j - 1);
-      }
-      issue_grads(nch - 1);
-    }
-    __syncwarp();
-    cluster_wait();
-  } else if (warp < 2 + kSoftWarps) {
-    // ------------------------------------------------------------- softmax warps
-    const int sw = warp - 2, part = sw >> 2;
-    const int rl = qd * 32 + lane, key = k0 + rl;
-    const int st = threadIdx.x - 64;
-    fill_keep_lut(reinterpret_cast<float4*>(smem + BwdSmem::LUT), st, 1.f);
-    mbar_wait(bar_a, 0);
-    if (sw == 0 && lane == 0) ATRACE(1);
-    // D = rowsum(dO∘O) for query block kb (rows of the O / dO tiles staged in DQP)
-    {
-      float dsum = 0.f;
-#pragma unroll
-      for (int c = 2 * part; c < 2 * part + 2; ++c) {
-        const uint32_t off = (rl >> 6) * 8 * KB + (rl & 63) * 128 + ((c ^ (rl & 7)) << 4);
-        const uint4 x = lds128(sbase + BwdSmem::DQP + 16 * KB + off), y = lds128(sbase + BwdSmem::DQP + off);
-        const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&x);
-        const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&y);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 fx = __bfloat1622float2(hx[i]), fy = __bfloat1622float2(hy[i]);
-          dsum = fmaf(fx.x, fy.x, dsum);
-          dsum = fmaf(fx.y, fy.y, dsum);
-        }
-      }
-      red[part * QT + rl] = dsum;
-    }
-    named_bar(1, kSoftWarps * 32);
-    if (part == 0) del_s[k0 + rl] = red[rl] + red[QT + rl] + red[2 * QT + rl] + red[3 * QT + rl];
-    // D slices of every CTA complete (cluster barrier phase 2); then each CTA
-    // copies the other blocks' D over DSMEM.  The DQP staging is free again.
-    cluster_arrive();
-    cluster_wait();
-    for (int i = st; i < S; i += kSoftWarps * 32)
-      if (i / QT != (int)kb) del_s[i] = ld_cluster_f32(mapa_u32(smem_u32(del_s + i), i / QT));
-    const int words = S / 32;
-    const size_t keyi = (size_t)bh * S + key;
-    uint32_t kbw[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    if (p.kb_col) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < nch) kbw[j] = __ldg(p.kb_col + keyi * words + ((j * CH + part * 32) >> 5));
-    }
-    const float mraw = p.add_mask ? __ldg(p.add_mask + (size_t)b * S + key) : 0.f;
-    const float mrow = mraw * kLog2e + __log2f(p.scale);  // P' = P / divisor
-    const float4* klut = reinterpret_cast<const float4*>(smem + BwdSmem::LUT);
-    named_bar(1, kSoftWarps * 32);
-    if (sw == 0 && lane == 0) ATRACE(2);
-    const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
-    float rsum = 0.f;  // sum over queries of dS' (this key row): the dQ bias column sums
-    const float2 sc2x2 = make_float2(p.sc2, p.sc2), mrow2 = make_float2(mrow, mrow), ks2 = make_float2(p.ks, p.ks);
-    for (int j = 0; j < nch; ++j) {
-      mbar_wait(bar_s, j & 1);
-      if (sw == 0 && lane == 0 && j < 4) ATRACE(3 + j);
-      tc_fence_after();
-      const uint32_t bits = j == 0 ? kbw[0] : (j == 1 ? kbw[1] : (j == 2 ? kbw[2] : kbw[3]));
-      // two 16-column halves: fewer live registers (22 warps share the file)
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        float s[16], dp[16];
-        tmem_ld16_nowait(trow + T_S + part * 32 + 16 * hf, s);
-        tmem_ld16_nowait(trow + T_DP + part * 32 + 16 * hf, dp);
-        tmem_wait_ld();
-        if (hf == 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar_tfree);
-        }
-        const int qc0 = j * CH + part * 32 + 16 * hf;
-        uint32_t pkp[8], pks[8];
-        float2 racc = make_float2(0.f, 0.f);
-        float4 kf;
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const float2 l = reinterpret_cast<const float2*>(lse_s + qc0)[i >> 1];
-          const float2 dd = reinterpret_cast<const float2*>(del_s + qc0)[i >> 1];
-          const float2 t = __ffma2_rn(make_float2(s[i], s[i + 1]), sc2x2, __fadd2_rn(mrow2, make_float2(-l.x, -l.y)));
-          const float2 P = make_float2(ex2(t.x), ex2(t.y));
-          if ((i & 3) == 0) kf = klut[(bits >> (16 * hf + i)) & 15u];
-          const float2 kk = (i & 3) ? make_float2(kf.z, kf.w) : make_float2(kf.x, kf.y);
-          const float2 pd = __fmul2_rn(P, kk);
-          const float2 dpm = __fmul2_rn(make_float2(dp[i], dp[i + 1]), kk);
-          const float2 ds = __fmul2_rn(P, __ffma2_rn(dpm, ks2, make_float2(-dd.x, -dd.y)));
-          racc = __fadd2_rn(racc, ds);
-          pkp[i >> 1] = pack_bf16x2(pd.x, pd.y);
-          pks[i >> 1] = pack_bf16x2(ds.x, ds.y);
-        }
-        rsum += racc.x + racc.y;
-        if (hf == 0 && j > 0) mbar_wait(bar_pdsfree, (j - 1) & 1);
-        // 16 columns = 2 x 16-byte chunks of row rl in the two SW128 tiles
-        const int col0 = part * 32 + 16 * hf;
-        const uint32_t tp = sbase + BwdSmem::PD + (col0 >> 6) * (QT * 128);
-        const uint32_t ts = sbase + BwdSmem::DS + (col0 >> 6) * (QT * 128);
-        const int ch0 = (col0 & 63) >> 3;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          st_sw128(tp, rl, ch0 + u, make_uint4(pkp[4 * u], pkp[4 * u + 1], pkp[4 * u + 2], pkp[4 * u + 3]));
-          st_sw128(ts, rl, ch0 + u, make_uint4(pks[4 * u], pks[4 * u + 1], pks[4 * u + 2], pks[4 * u + 3]));
-        }
-      }
-      fence_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_pds);
-    }
-    mbar_wait(bar_pdsfree, (nch - 1) & 1);  // every MMA of the CTA complete
-    tc_fence_after();
-    __nv_bfloat16* grow_ptr = p.dqkv + (size_t)(row0 + key) * p.ld_dqkv + h * DH + part * 16;
-    float g2[2][16];
-    tmem_ld16(trow + T_DK + part * 16, g2[0]);
-    store_bf16x16(grow_ptr + p.H, g2[0]);
-    tmem_ld16(trow + T_DV + part * 16, g2[1]);
-    const float dvs = p.ks / p.scale;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) g2[1][i] *= dvs;
-    store_bf16x16(grow_ptr + 2 * p.H, g2[1]);
-    if (p.bias_part) {
-      // qkv bias gradient partials of this key strip: dK / dV column sums, and
-      // the dQ column sums of the whole head through this strip's keys:
-      // sum_q dQ[q][d] = sum_k (sum_q dS'[q][k]) K[k][d]
-      float* bp = p.bias_part + (size_t)(b * nch + kb) * 3 * p.H + h * DH;
-      red[part * QT + rl] = rsum;
-      float* scr0 = reinterpret_cast<float*>(smem + BwdSmem::SCR);
-      float* const stg[2] = {reinterpret_cast<float*>(smem + BwdSmem::DS), reinterpret_cast<float*>(smem + BwdSmem::PD)};
-      float* const scr[2] = {scr0, scr0 + 8 * 64};
-      float* const dst[2] = {bp + p.H, bp + 2 * p.H};
-      tile_colsum_128x64<2>(stg, scr, rl, part * 16, g2, st, dst);  // (its barriers also publish red[])
-      if (st < 64) {
-        float acc = 0.f;
-        for (int k = 0; k < QT; ++k) {
-          const float rk = red[k] + red[QT + k] + red[2 * QT + k] + red[3 * QT + k];
-          const uint32_t off = BwdSmem::K + (k >> 6) * 8 * KB + (k & 63) * 128 + (((st >> 3) ^ (k & 7)) << 4) +
-                               (st & 7) * 2;
-          acc = fmaf(rk, __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(smem + off)), acc);
-        }
-        bp[st] = acc;
-      }
-    }
-    if (sw == 0 && lane == 0) ATRACE(11);
-  } else {
-    // ------------------------------------------------------------- dQ warps
-    cluster_arrive();  // phase 2 (nothing to publish)
-    cluster_wait();
-    const int dt = threadIdx.x - (2 + kSoftWarps) * 32;  // 0..127
-    const int rl = qd * 32 + lane;                        // query row of the chunk = TMEM lane
-    const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
-    const uint32_t dqp = sbase + BwdSmem::DQP;
-    for (int c = 0; c < nch; ++c) {
-      mbar_wait(&bar_dq[c & 1], (c >> 1) & 1);
-      tc_fence_after();
-      float o[2][32];
-      tmem_ld32_nowait(trow + T_DQ + (c & 1) * DH, o[0]);
-      tmem_ld32_nowait(trow + T_DQ + (c & 1) * DH + 32, o[1]);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_dqfree[c & 1]);
-      if (c >= 1) mbar_wait(bar_used, (c - 1) & 1);  // every CTA finished reading chunk c-1
-#pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
-        const float* v = &o[ch >> 3][(ch & 7) * 4];
-        sts128(dqp + rl * 256 + ((ch ^ (rl & 15)) << 4),
-               make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])));
-      }
-      __syncwarp();
-      if (lane < nch) mbar_arrive_remote_cta(bar_ready, lane);
-      mbar_wait(bar_ready, c & 1);
-      if (c == 1 && dt == 0) ATRACE(13);
-      // rows r of dQ_c with r % nch == kb, summed over the partials in rank order
-      const int nrows = (QT - (int)kb + nch - 1) / nch;
-      for (int idx = dt; idx < nrows * 16; idx += kDqWarps * 32) {
-        const int row = (idx >> 4) * nch + (int)kb, ch = idx & 15;
-        const uint32_t off = dqp + row * 256 + ((ch ^ (row & 15)) << 4);
-        float4 v[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (r < nch) v[r] = ld_cluster_f4(mapa_u32(off, r));
-        float4 acc = v[0];
-#pragma unroll
-        for (int r = 1; r < 4; ++r)
-          if (r < nch) { acc.x += v[r].x; acc.y += v[r].y; acc.z += v[r].z; acc.w += v[r].w; }
-        const uint2 w2 = make_uint2(pack_bf16x2(acc.x, acc.y), pack_bf16x2(acc.z, acc.w));
-        *reinterpret_cast<uint2*>(p.dqkv + (size_t)(row0 + c * CH + row) * p.ld_dqkv + h * DH + ch * 4) = w2;
-      }
-      __syncwarp();
-      if (lane < nch) mbar_arrive_remote_cta(bar_used, lane);
-      if (dt == 0 && c < 4) ATRACE(7 + c);
-    }
-  }
-  tc_fence_before();
-  // no CTA leaves while a cluster peer may still read its shared memory
-  cluster_arrive();
-  cluster_wait();
-  if (threadIdx.x == 64) ATRACE(12);
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-  }
-}
-
 int check_common(int64_t B, int64_t NH, int64_t S, int64_t dh, const void* qkv, int64_t ld_qkv) {
   DFX_REQUIRE(B >= 1 && NH >= 1, DFX_ERR_SHAPE, "dfx_attn: batch and heads must be >= 1");
   DFX_REQUIRE(dh == DH, DFX_ERR_UNSUPPORTED, "dfx_attn: head_dim must be 64");
@@ -1712,35 +1328,9 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   if (!attr) {
     cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem::TOTAL);
     cudaFuncSetAttribute(attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvSmem::TOTAL);
-    cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem::TOTAL);
     attr = true;
   }
   const int grid = (int)(batch * heads * (seq / QT));
-  static const bool legacy = getenv("DFX_ATTN_BWD_LEGACY") != nullptr;  // A/B: the two-kernel form
-  if (!legacy) {
-    // one fused kernel; the S/128 key strips of a head form a cluster
-    static const bool swap = getenv("DFX_ATTN_DQ_SWAP") != nullptr;
-    p.dq_lbo = swap ? 1024 : 16 * KB;
-    p.dq_sbo = swap ? 16 * KB : 1024;
-    p.trace = g_attn_trace;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kBwdThreads);
-    cfg.dynamicSmemBytes = BwdSmem::TOTAL;
-    cfg.stream = as_stream(stream);
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)(seq / QT);
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = getenv("DFX_NO_PDL") ? 1 : 2;
-    cudaLaunchKernelEx(&cfg, attn_bwd_kernel, mqkv, mdo, mo, p);
-    DFX_LAUNCH_CHECK("dfx_attn_bwd");
-    return DFX_OK;
-  }
   // debug timeline of the dq kernel, or of dkdv with DFX_ATTN_TRACE_DKDV set (tools/attn_trace.py)
   const bool trace_dkdv = getenv("DFX_ATTN_TRACE_DKDV") != nullptr;
   p.trace = trace_dkdv ? nullptr : g_attn_trace;

@@ -55,32 +55,6 @@ if "--fwd2" in sys.argv:  # online-softmax forward: 0 start, 1 Q landed, 2-5 S_j
     starts = sorted(rel[:, 0].tolist())
     print("CTA start quantiles:", [round(starts[int(q * (len(starts) - 1))], 2) for q in (0, .25, .5, .75, 1)])
     sys.exit(0)
-if "--fused" in sys.argv:  # fused backward: 0 start, 1 K/V/O landed, 2 D exchanged, 3-6 S_j ready, 7-10 dQ_j reduced, 11 epilogue, 12 exit
-    run()
-    dctx = torch.randn_like(ctx)
-    dqkv = torch.empty_like(qkv)
-    bwd = lambda: K.attn_bwd(qkv, ctx, dctx, B, S, NH, am, lse, kr, kc, 1 / 0.9, 0.125, dqkv)  # noqa: E731
-    for _ in range(3):
-        bwd()
-    tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
-    fn(tr.data_ptr())
-    bwd()
-    torch.cuda.synchronize()
-    fn(None)
-    t = tr.view(ncta, 16).cpu().double()
-    rel = (t - t[:, 0].min()) / 1e3
-    d = rel[:, 1:13] - rel[:, 0:12]
-    names = ["start->kv", "kv->D", "D->S0", "S0->S1", "S1->S2", "S2->S3", "S3->dQ0", "dQ0->dQ1", "dQ1->dQ2",
-             "dQ2->dQ3", "dQ3->epi", "epi->exit"]
-    print("fused bwd mean phase durations (us):", {n: round(d[:, i].mean().item(), 2) for i, n in enumerate(names)})
-    print("chunk-1 drain: S2->dq ld", round((rel[:, 13] - rel[:, 5]).mean().item(), 2), "-> partial stored",
-          round((rel[:, 14] - rel[:, 13]).mean().item(), 2), "-> ready", round((rel[:, 15] - rel[:, 14]).mean().item(), 2),
-          "-> reduced", round((rel[:, 8] - rel[:, 15]).mean().item(), 2))
-    print("per-CTA total mean", round((rel[:, 12] - rel[:, 0]).mean().item(), 2), "kernel span",
-          round(rel[:, 12].max().item(), 2))
-    starts = sorted(rel[:, 0].tolist())
-    print("CTA start times (us) quantiles:", [round(starts[int(q * (len(starts) - 1))], 2) for q in (0, .25, .5, .75, 1)])
-    sys.exit(0)
 if "--bwd" in sys.argv:  # dq kernel timeline: 0 start, 1 Q/dO landed (MMA), 2-5 S_j ready, 6-9 dS_j done, 10 dQ done, 11 exit
     run()
     dctx = torch.randn_like(ctx)
