@@ -6,14 +6,20 @@ container), builds ``dfm-0.1`` models made exclusively of registry operators
 (the survey's Appendix B recipe, SURVEY.md:500-514), runs the forward pass with
 ``dfir.interp.execute`` (interp.py:1301-1317) and the backward pass with
 ``dfir.autodiff.differentiate_graph(..., seed="input")`` (autodiff.py:1760-1841)
-followed by ``execute``, and stores inputs + outputs + gradients as compressed
-``.npz`` fixtures under ``tests/golden/``.
+followed by ``execute``, and stores inputs + outputs + gradients as DTNS
+containers written by the reference's OWN encoder (``dfir.dtns.encode``,
+dtns.py:52-70) — one ``tests/golden/<case>/<tensor>.dtns`` per array — next to
+the case's ``dfm-0.1`` model documents: ``model.json`` (the registry-operator
+graph the reference executed) and, where the B200 path has fused operators,
+``model_fused.json`` (the same computation as fused operators; pinned to the
+reference by tests/test_dfir_plugin.py and executed device-resident by
+tests/test_gpu_dfm.py).
 
 The fixtures pin ``oracle/oracle.py`` (tests/test_oracle_golden.py) so the
 numpy restatement that travels to the GPU box is checked against the reference
 itself.  Regenerate with::
 
-    python oracle/make_golden.py            # writes tests/golden/*.npz
+    python oracle/make_golden.py            # writes tests/golden/<case>/*.dtns + model*.json
 
 Every random draw uses ``numpy.random.default_rng(seed)`` with the seed stored
 in the fixture.
@@ -99,11 +105,28 @@ def _drop_mask(rng, shape, p, dtype):
     return keep, (keep.astype(np.float64) * (1.0 / (1.0 - p))).astype(dtype)
 
 
-def _save(name, **arrays):
-    os.makedirs(OUT_DIR, exist_ok=True)
-    path = os.path.join(OUT_DIR, name + ".npz")
-    np.savez_compressed(path, **arrays)
-    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+def _save(name, model=None, fused=None, **arrays):
+    """One DTNS container per array (reference encoder) + the model documents."""
+    import json
+
+    sys.path.insert(0, REF_SRC)
+    from dfir import dtns  # noqa: WPS433
+
+    d = os.path.join(OUT_DIR, name)
+    os.makedirs(d, exist_ok=True)
+    for key, val in arrays.items():
+        arr = np.asarray(val)
+        if arr.dtype == np.int32 or (arr.dtype.kind in "iu" and arr.dtype != np.int64):
+            arr = arr.astype(np.int64)
+        if isinstance(val, float):
+            arr = np.float64(val)
+        with open(os.path.join(d, key + ".dtns"), "wb") as fh:
+            fh.write(dtns.encode(np.asarray(arr)))
+    for fname, doc in (("model.json", model), ("model_fused.json", fused)):
+        if doc is not None:
+            with open(os.path.join(d, fname), "w") as fh:
+                json.dump(doc, fh, indent=1)
+    print(f"wrote {d} ({len(arrays)} tensors)")
 
 
 # ---------------------------------------------------------------------------
@@ -128,8 +151,14 @@ def golden_bdrln(seed=11, T=24, H=40, p=0.1, eps=1e-12, dtype="f64"):
               "g": (1 + 0.1 * rng.standard_normal(H)).astype(npdt),
               "be": (0.1 * rng.standard_normal(H)).astype(npdt)}
     fwd, dy, grads = _run(mb.doc, inputs, [y], ["h", "b", "r", "g", "be"])
-    _save(f"bdrln_{dtype}", seed=seed, p=p, eps=eps, keep=keep, **inputs, y=fwd[y], dy=dy,
-          **{"d" + k: v for k, v in grads.items()})
+    fz = ModelBuilder("bdrln_fused", dtype)
+    for k, v in inputs.items():
+        fz.inp(k, v.shape)
+    fz.doc["nodes"].append({"op": "BiasDropoutResidualLayerNorm", "attrs": {"epsilon": eps},
+                            "inputs": ["h", "b", "m", "r", "g", "be"], "outputs": ["y", "s"]})
+    fz.output("y")
+    _save(f"bdrln_{dtype}", model=mb.doc, fused=fz.doc, seed=seed, p=p, eps=eps, keep=keep, **inputs, y=fwd[y],
+          dy=dy, **{"d" + k: v for k, v in grads.items()})
 
 
 def golden_softmax(seed=12, B=2, NH=3, S=16, p=0.1, divisor=8.0, dtype="f64"):
@@ -147,7 +176,14 @@ def golden_softmax(seed=12, B=2, NH=3, S=16, p=0.1, divisor=8.0, dtype="f64"):
     amask = np.where(rng.random((B, 1, 1, S)) < 0.1, -10000.0, 0.0).astype(npdt)
     inputs = {"sc": (3.0 * rng.standard_normal((B, NH, S, S))).astype(npdt), "am": amask, "dm": dmask}
     fwd, dy, grads = _run(mb.doc, inputs, [pd, pr], ["sc"])
-    _save(f"softmax_{dtype}", seed=seed, p=p, divisor=divisor, keep=keep, **inputs,
+    fz = ModelBuilder("scaled_masked_softmax_fused", dtype)
+    for k, v in inputs.items():
+        fz.inp(k, v.shape)
+    fz.doc["nodes"].append({"op": "ScaledMaskedSoftmax", "attrs": {"divisor": divisor},
+                            "inputs": ["sc", "am", "dm"], "outputs": ["pd", "p_out"]})
+    fz.output("pd")
+    fz.output("p_out")
+    _save(f"softmax_{dtype}", model=mb.doc, fused=fz.doc, seed=seed, p=p, divisor=divisor, keep=keep, **inputs,
           pd=fwd[pd], p_out=fwd[pr], dy=dy, dsc=grads["sc"])
 
 
@@ -173,7 +209,13 @@ def golden_bias_gelu(seed=13, T=20, F=48, dtype="f64"):
     inputs = {"f": (2.0 * rng.standard_normal((T, F))).astype(npdt),
               "b": (0.1 * rng.standard_normal(F)).astype(npdt)}
     fwd, dy, grads = _run(mb.doc, inputs, [y], ["f", "b"])
-    _save(f"bias_gelu_{dtype}", seed=seed, **inputs, y=fwd[y], dy=dy, df=grads["f"], db=grads["b"])
+    fz = ModelBuilder("bias_gelu_fused", dtype)
+    for k, v in inputs.items():
+        fz.inp(k, v.shape)
+    fz.doc["nodes"].append({"op": "BiasGelu", "attrs": {}, "inputs": ["f", "b"], "outputs": ["y", "pre"]})
+    fz.output("y")
+    _save(f"bias_gelu_{dtype}", model=mb.doc, fused=fz.doc, seed=seed, **inputs, y=fwd[y], dy=dy, df=grads["f"],
+          db=grads["b"])
 
 
 def bert_layer_model(B, S, H, NH, FF, eps, dtype):
@@ -216,6 +258,39 @@ def bert_layer_model(B, S, H, NH, FF, eps, dtype):
     return mb.doc, out, list(w)
 
 
+def bert_layer_model_fused(B, S, H, NH, FF, eps, dtype):
+    """The same layer with the B200 path's fused operators (registry.py
+    FUSED_OPS): what dfir_plugin.fuse_to_b200 makes of bert_layer_model."""
+    dh = H // NH
+    T = B * S
+    mb = ModelBuilder("bert_layer_fused", dtype)
+    x = mb.inp("x", (T, H))
+    for nm, shp in [("am", (B, 1, 1, S)), ("dm", (B, NH, S, S)), ("m1", (T, H)), ("m2", (T, H)),
+                    ("wq", (H, H)), ("wk", (H, H)), ("wv", (H, H)), ("wo", (H, H)), ("w1", (FF, H)),
+                    ("w2", (H, FF))]:
+        mb.inp(nm, shp)
+    for nm, n in [("bq", H), ("bk", H), ("bv", H), ("bo", H), ("b1", FF), ("b2", H),
+                  ("g1", H), ("be1", H), ("g2", H), ("be2", H)]:
+        mb.inp(nm, (n,))
+    heads = {}
+    for t in "qkv":
+        lin = mb.node("Gemm", [x, "w" + t, "b" + t], transB=1)
+        heads[t] = mb.node("Reshape", [lin], shape=[B, S, NH, dh])
+    sc = mb.node("Einsum", [heads["q"], heads["k"]], equation="bsnd,btnd->bnst")
+    pd, _ = mb.node("ScaledMaskedSoftmax", [sc, "am", "dm"], n_out=2, divisor=float(np.sqrt(dh)))
+    c4 = mb.node("Einsum", [pd, heads["v"]], equation="bnst,btnd->bsnd")
+    ctx = mb.node("Reshape", [c4], shape=[T, H])
+    a1 = mb.node("Gemm", [ctx, "wo"], transB=1)
+    ln1, _ = mb.node("BiasDropoutResidualLayerNorm", [a1, "bo", "m1", x, "g1", "be1"], n_out=2, epsilon=eps)
+    f = mb.node("Gemm", [ln1, "w1"], transB=1)
+    gl, _ = mb.node("BiasGelu", [f, "b1"], n_out=2)
+    a2 = mb.node("Gemm", [gl, "w2"], transB=1)
+    mb.doc["nodes"].append({"op": "BiasDropoutResidualLayerNorm", "attrs": {"epsilon": eps},
+                            "inputs": [a2, "b2", "m2", ln1, "g2", "be2"], "outputs": ["out", "s2"]})
+    mb.output("out")
+    return mb.doc
+
+
 def bert_layer_inputs(rng, B, S, H, NH, FF, p, npdt):
     T = B * S
     inp = {"x": rng.standard_normal((T, H))}
@@ -242,8 +317,9 @@ def golden_bert_layer(seed=14, B=2, S=8, H=32, NH=2, FF=64, p=0.1, eps=1e-12, dt
     inputs, keeps = bert_layer_inputs(rng, B, S, H, NH, FF, p, npdt)
     wrt = ["x"] + wnames
     fwd, dy, grads = _run(doc, inputs, [out], wrt)
-    _save(f"bert_layer_{dtype}", seed=seed, B=B, S=S, H=H, NH=NH, FF=FF, p=p, eps=eps,
-          **keeps, **inputs, out=fwd[out], dy=dy, **{"d_" + k: v for k, v in grads.items()})
+    _save(f"bert_layer_{dtype}", model=doc, fused=bert_layer_model_fused(B, S, H, NH, FF, eps, dtype), seed=seed,
+          B=B, S=S, H=H, NH=NH, FF=FF, p=p, eps=eps, **keeps, **inputs, out=fwd[out], dy=dy,
+          **{"d_" + k: v for k, v in grads.items()})
 
 
 def mbconv_model(N, C, Hh, Ww, SE, stride, eps, momentum, dtype):
@@ -285,8 +361,17 @@ def golden_mbconv(seed=15, N=2, C=8, Hh=7, Ww=7, SE=2, stride=1, eps=1e-3, momen
               "we": 0.3 * rng.standard_normal((C, SE)), "be": 0.1 * rng.standard_normal(C)}
     inputs = {k: v.astype(npdt) for k, v in inputs.items()}
     fwd, dy, grads = _run(doc, inputs, [y, nrm, nrv], wrt)
-    _save(f"mbconv_s{stride}_{dtype}", seed=seed, N=N, C=C, H=Hh, W=Ww, SE=SE, stride=stride,
-          eps=eps, momentum=momentum, **inputs, y=fwd[y], new_rm=fwd[nrm], new_rv=fwd[nrv],
+    fz = ModelBuilder("mbconv_fused", dtype)
+    for k, v in inputs.items():
+        fz.inp(k, v.shape)
+    fz.doc["nodes"].append({"op": "MBConvBlock", "attrs": {"strides": [stride, stride], "pads": [1, 1, 1, 1],
+                                                            "epsilon": eps, "momentum": momentum},
+                            "inputs": ["x", "wdw", "g", "b", "rm", "rv", "wr", "br", "we", "be"],
+                            "outputs": ["y", "new_rm", "new_rv"]})
+    for o in ("y", "new_rm", "new_rv"):
+        fz.output(o)
+    _save(f"mbconv_s{stride}_{dtype}", model=doc, fused=fz.doc, seed=seed, N=N, C=C, H=Hh, W=Ww, SE=SE,
+          stride=stride, eps=eps, momentum=momentum, **inputs, y=fwd[y], new_rm=fwd[nrm], new_rv=fwd[nrv],
           dy=dy, **{"d_" + k: v for k, v in grads.items()})
 
 
