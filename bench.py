@@ -139,6 +139,14 @@ class DfirReference:
         return time.perf_counter() - t0
 
 
+_T0 = time.time()
+
+
+def _progress(what):
+    """stderr breadcrumbs (the JSON line alone goes to stdout)."""
+    print(f"[bench {time.time() - _T0:7.1f} s] {what}", file=sys.stderr, flush=True)
+
+
 def reference_sample(seconds: float):
     """Bounded cpu_baseline reading: the reference package (``kind``
     "reference") when installed, else the numpy port.  Returns
@@ -483,12 +491,13 @@ def measure_effnet_c5(steps, flush, pk, world, rank, local, dist):
     dev["labels"].copy_(lh)
     lr = 1e-3
     rows = []
+    from paper_2110_10802_b200.graphs import CapturedStep
+
+    # one CUDA graph per step; data parallel, the SyncBN statistics
+    # collectives and the group-aligned gradient buckets are NCCL nodes of it
+    cs = net.capture_step(N, lr)
+    step = cs.replay
     if world == 1:
-        from paper_2110_10802_b200.graphs import CapturedStep
-
-        cs = net.capture_step(N, lr)
-        step = cs.replay
-
         timer = K.KernelTimer()
         net.concurrent = False  # single-stream twin: per-kernel times without branch contention
         with timer:
@@ -500,11 +509,6 @@ def measure_effnet_c5(steps, flush, pk, world, rank, local, dist):
             inst.replay()
             timer.collect()
         rows = _kernel_rows(timer, 3, pk)
-    else:
-        def step():
-            net.train_step(dev["x"], dev["labels"], None)
-            dist.all_reduce(net.grad.flat)
-            net.sgd_step(lr / world)
     for _ in range(3):
         step()
     if world > 1:
@@ -531,9 +535,7 @@ def measure_effnet_c5(steps, flush, pk, world, rank, local, dist):
         e2e_ms = e0.elapsed_time(e1) / ke
     else:
         def host_step():
-            net.train_step_host(xh, lh, lr=None, loss_host=loss_h)
-            dist.all_reduce(net.grad.flat)
-            net.sgd_step(lr / world)
+            net.train_step_host(xh, lh, lr=lr, loss_host=loss_h, graph=cs)
 
         e2e_ms = _timed_graph(host_step, ke, flush)
     if world > 1:
@@ -546,8 +548,8 @@ def measure_effnet_c5(steps, flush, pk, world, rank, local, dist):
             "n_gpus": world, "scaling": "weak",
             "config": {"workload": "efficientnet_b0_train_step (BASELINE.json configs[4])", "batch_per_gpu": N,
                        "image": 224, "params": net.num_params, "parallelism": f"dp{world}",
-                       "syncbn": world > 1, "step": "fwd + bwd + SGD" + (" + NCCL allreduce" if world > 1 else ""),
-                       "execution": "CUDA graph" if world == 1 else "eager (SyncBN collectives)"},
+                       "syncbn": world > 1, "step": "fwd + bwd + SGD" + (" + bucketed NCCL allreduce" if world > 1 else ""),
+                       "execution": "CUDA graph" + (" (SyncBN + gradient buckets as NCCL nodes)" if world > 1 else "")},
             "e2e": {"value": round(world * N * 1e3 / e2e_ms, 1), "unit": "images/s", "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "kernels": rows[:12]}
@@ -595,21 +597,20 @@ def run_ours(args):
     K.reset_launch_count()
     timer = K.KernelTimer()
     if world > 1:
-        g_step, g_inst = layer.capture_step(B, S, None, timer)
-    else:
-        g_step, g_inst = layer.capture_step(B, S, lr, timer)
+        # data parallel: the backward all-reduces the gradient arena in four
+        # group-aligned buckets as the groups complete (overlapping the rest
+        # of the backward); the buckets are NCCL nodes of the step's graph
+        layer.attach_process_group(dist.group.WORLD)
+    g_step, g_inst = layer.capture_step(B, S, lr, timer)
     K.reset_launch_count()  # count one eager step's launches (the graph replays the same set)
-    layer.forward(dev["x"], dev["add_mask"], dev["keep_attn"], dev["keep1"], dev["keep2"])
-    layer.backward(dev["dout"])
-    if world == 1:
-        layer.sgd_step(lr)
+    saved = [t.clone() for t in layer.training_state()]
+    layer.train_step(dev["x"], dev["add_mask"], dev["keep_attn"], dev["keep1"], dev["keep2"], dev["dout"], lr)
+    for t, v in zip(layer.training_state(), saved):
+        t.copy_(v)
     launches_per_step = K.launch_count()
 
     def step(g=g_step):
         g.replay()
-        if world > 1:
-            dist.all_reduce(layer.grad.flat)  # NCCL sum; averaging folded into the lr
-            layer.sgd_step(lr / world)
 
     def timed(fn, k, per_step=None):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
@@ -633,6 +634,7 @@ def run_ours(args):
             ms = float(t.item())
         return ms
 
+    _progress("bert c2 captured; timing")
     sampler = ClockSampler(local)
     with sampler:
         for _ in range(max(3, args.warmup)):
@@ -666,10 +668,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / ke
     else:
-        def host_step():
-            layer.train_step_host(host, lr=None, dx_host=dx_host)
-            dist.all_reduce(layer.grad.flat)
-            layer.sgd_step(lr / world)
+        def host_step():  # captured step (gradient buckets inside) from host buffers
+            layer.train_step_host(host, lr=lr, dx_host=dx_host)
 
         for _ in range(3):
             host_step()
@@ -697,11 +697,16 @@ def run_ours(args):
     workloads = {}
     if not args.no_extra:
         if rank == 0 and world == 1:
+            _progress("bert_c1_fp32")
             workloads["bert_c1_fp32"] = measure_bert_c1(max(10, args.steps // 4), flush, pk)
+            _progress("mbconv_c3")
             workloads["mbconv_c3"] = measure_mbconv_c3(max(10, args.steps // 4), flush, pk)
+            _progress("norm_sweep_c4")
             workloads["norm_sweep_c4"] = measure_norm_sweep_c4(max(10, args.steps // 4), flush, pk)
+        _progress("efficientnet_b0_c5")
         workloads["efficientnet_b0_c5"] = measure_effnet_c5(max(5, args.steps // 20), flush, pk, world, rank,
                                                             local, dist)
+        _progress("workloads done")
 
     # the fused schedule's compulsory bytes vs the reference's unfused graph
     # (ir.movement_volume of the autodiff graph, oracle/movement_volume.py; f32 -> bf16 halved)
@@ -718,6 +723,7 @@ def run_ours(args):
                             "achieved_gbs": round(ours_b / (ms_step * 1e-3) / 1e9, 1)}
 
     cpu = None
+    _progress("cpu baseline")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sample, kind = reference_sample(args.cpu_seconds)
         cpu = {"value": round(v, 4), "unit": UNIT, "cores": os.cpu_count(), "kind": kind, "sample": sample}

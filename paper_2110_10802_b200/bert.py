@@ -51,11 +51,24 @@ class BertLayerConfig:
         return self.hidden // self.heads
 
 
-def _param_specs(c: BertLayerConfig):
+def _model_specs(c: BertLayerConfig):
     H, F = c.hidden, c.ffn
     return [("wqkv", (3 * H, H)), ("wo", (H, H)), ("w1", (F, H)), ("w2", (H, F)),
             ("bqkv", (3 * H,)), ("bo", (H,)), ("g1", (H,)), ("be1", (H,)), ("b1", (F,)),
             ("b2", (H,)), ("g2", (H,)), ("be2", (H,))]
+
+
+# Arena order = the order backward() finishes the gradients (LN2 / FFN2 group
+# first, the QKV group last), so a bucketed data-parallel allreduce
+# (dp.GradAllReducer) can reduce the front of the arena while the backward is
+# still producing the rest.  GRAD_GROUP_ENDS close each group.
+PRODUCTION_ORDER = ("g2", "be2", "b2", "w2", "b1", "w1", "g1", "be1", "bo", "wo", "wqkv", "bqkv")
+GRAD_GROUP_ENDS = ("w2", "w1", "wo", "bqkv")
+
+
+def _param_specs(c: BertLayerConfig):
+    shapes = dict(_model_specs(c))
+    return [(n, shapes[n]) for n in PRODUCTION_ORDER]
 
 
 MATRICES = ("wqkv", "wo", "w1", "w2")
@@ -118,14 +131,31 @@ class BertEncoderLayer:
         # every step on H2D(i+2) waiting for D2H(i): tools/e2e_probe.py)
         self.nslots = 3
         self.concurrent = True  # weight gradients on a forked stream (backward)
+        self.reducer = None  # dp.GradAllReducer once attach_process_group() is called
+        self.world = 1
         self._init_params(seed)
+
+    def attach_process_group(self, group=None, bucket_bytes: int = 8 << 20):
+        """Data-parallel replica: the backward all-reduces (SUM) the gradient
+        arena bucket by bucket as each parameter group completes, and
+        ``train_step`` / the captured step fold the 1/world average into the
+        SGD learning rate.  Under NCCL the buckets are captured into the step's
+        CUDA graph with everything else."""
+        import torch.distributed as dist
+
+        from .dp import GradAllReducer
+
+        ends = [self.grad.offsets[n][0] + _numel(self.grad.offsets[n][1]) for n in GRAD_GROUP_ENDS]
+        self.reducer = GradAllReducer(self.grad.flat, group, bucket_bytes, boundaries=ends)
+        self.world = dist.get_world_size(group)
+        return self.reducer
 
     # ------------------------------------------------------------ parameters
     def _init_params(self, seed):
         g = torch.Generator(device="cpu").manual_seed(seed)
         H = self.cfg.hidden
         vals = {}
-        for name, shape in _param_specs(self.cfg):
+        for name, shape in _model_specs(self.cfg):  # draw order fixed (independent of the arena order)
             if name.startswith("w"):
                 vals[name] = 0.02 * torch.randn(shape, generator=g)
             elif name.startswith("g"):
@@ -298,6 +328,11 @@ class BertEncoderLayer:
             side.wait_event(ev)
             return torch.cuda.stream(side)
 
+        def ready(name):  # gradient group complete: its allreduce bucket may start
+            if self.reducer is not None:
+                off, shape = G.offsets[name]
+                self.reducer.mark_ready(off + _numel(shape), (main, side) if self.concurrent else (main,))
+
         # BDRLN backward: the dx half stays on the critical path; the
         # parameter-gradient finalize (partials in a per-site workspace) forks
         wsb = self._bdrln_ws(B, S)
@@ -307,6 +342,7 @@ class BertEncoderLayer:
             K.bdrln_bwd_finalize(dout, wsb[0], G["g2"], G["be2"], G["b2"])
             with L("bwd.ffn2_wgrad"):
                 K.gemm(b["da2"].t(), b["g"].t(), G["w2"])
+        ready("w2")
         # FFN2: dgrad with the GELU-backward epilogue, wgrad straight into f32 grads
         with L("bwd.ffn2_dgrad+gelu_bwd"):
             K.gemm(b["da2"], self.weight("w2").t(), b["dpre"], EPI_GELU_BWD, aux=b["pre"])
@@ -315,6 +351,7 @@ class BertEncoderLayer:
                 K.colsum(b["dpre"], G["b1"])
             with L("bwd.ffn1_wgrad"):
                 K.gemm(b["dpre"].t(), b["ln1"].t(), G["w1"])
+        ready("w1")
         # FFN1: dgrad + residual gradient from LN2
         with L("bwd.ffn1_dgrad+residual"):
             K.gemm(b["dpre"], self.weight("w1").t(), b["dln1"], EPI_ADD, aux=b["ds2"])
@@ -324,6 +361,7 @@ class BertEncoderLayer:
             K.bdrln_bwd_finalize(b["dln1"], wsb[1], G["g1"], G["be1"], G["bo"])
             with L("bwd.out_wgrad"):
                 K.gemm(b["da1"].t(), b["ctx"].t(), G["wo"])
+        ready("wo")
         with L("bwd.out_dgrad"):
             K.gemm(b["da1"], self.weight("wo").t(), b["dctx"])
         # attention
@@ -389,11 +427,19 @@ class BertEncoderLayer:
             K.sgd_update(self.master.flat, self.grad.flat, lr,
                          None if self.wlow is None else self.wlow.flat)
 
+    def reduce_gradients(self):
+        """Data parallel: finish the bucketed allreduce the backward started
+        (no-op for a single replica).  Returns the world size."""
+        return self.reducer.finish() if self.reducer is not None else 1
+
     def train_step(self, x, add_mask, keep_attn, keep1, keep2, dout, lr=None):
+        """fwd + bwd (+ gradient allreduce over the attached process group)
+        (+ SGD with the gradient averaged over the replicas)."""
         out = self.forward(x, add_mask, keep_attn, keep1, keep2)
         dx = self.backward(dout)
+        world = self.reduce_gradients()
         if lr is not None:
-            self.sgd_step(lr)
+            self.sgd_step(lr / world)
         return out, dx
 
     # ------------------------------------------------------------ host-buffer API
@@ -402,32 +448,10 @@ class BertEncoderLayer:
         SGD included): every kernel's tensor arguments read once and written
         once — the schedule's own data movement, compared in bench.py with the
         reference's ``ir.movement_volume`` of the unfused graph."""
-        c = self.cfg
-        T, H, F, NH = B * S, c.hidden, c.ffn, c.heads
-        e = torch.tensor([], dtype=c.dtype).element_size()
-        th, tf, t3 = T * H * e, T * F * e, T * 3 * H * e
-        bits = B * NH * S * S // 8
-        kb = T * H // 8 if self._fused(S) and H % 32 == 0 else T * H  # BDRLN keep flags (packed or u8)
-        w = lambda n, k: n * k * e  # noqa: E731  (bf16 weight operand)
-        g32 = lambda n, k: n * k * 4  # noqa: E731  (f32 weight gradient)
-        fwd = (th + w(3 * H, H) + t3) + (t3 + bits + th + bits + B * NH * S * 4) + (th + w(H, H) + th) \
-            + (2 * th + kb + 2 * th) + (th + w(F, H) + 2 * tf) + (tf + w(H, F) + th) + (2 * th + kb + 2 * th)
-        bwd = (2 * th + kb + 2 * th) + (th + w(H, F) + tf + tf) + (th + tf + g32(H, F)) + tf \
-            + (tf + w(F, H) + th + th) + (tf + th + g32(F, H)) + (2 * th + kb + 2 * th) + (th + w(H, H) + th) \
-            + (2 * th + g32(H, H)) + (t3 + 2 * th + B * NH * S * 4 + 2 * bits + t3) + t3 \
-            + (t3 + w(3 * H, H) + th + th) + (t3 + th + g32(3 * H, H))
-        nparam = sum(v.numel() for v in self.master.views.values())
-        sgd = nparam * (4 + 4 + 4 + (2 if self.wlow is not None else 0))
-        return int(fwd + bwd + sgd)
+        return fused_step_bytes(self.cfg, B, S)
 
     def step_flops(self, B: int, S: int) -> int:
-        """Algorithmic contraction FLOPs of one fwd+bwd step (SURVEY.md §8a row
-        a8): QKV, QKᵀ, PV, out-proj, FFN1, FFN2 forward, x3 for the backward."""
-        c = self.cfg
-        T = B * S
-        fwd = 2 * T * c.hidden * (3 * c.hidden) + 2 * 2 * B * c.heads * S * S * c.head_dim \
-            + 2 * T * c.hidden * c.hidden + 2 * 2 * T * c.hidden * c.ffn
-        return 3 * fwd
+        return fused_step_flops(self.cfg, B, S)
 
     def host_inputs_bytes(self, B: int, S: int) -> tuple[int, int]:
         """(H2D, D2H) bytes per train_step_host call."""
@@ -457,10 +481,8 @@ class BertEncoderLayer:
             self._bufs[key].replay()
             dx = self.buffers(B, S)["dx"]
         else:
-            self.forward(dev["x"], dev["add_mask"], dev["keep_attn"], dev["keep1"], dev["keep2"])
-            dx = self.backward(dev["dout"])
-            if lr is not None:
-                self.sgd_step(lr)
+            _, dx = self.train_step(dev["x"], dev["add_mask"], dev["keep_attn"], dev["keep1"], dev["keep2"],
+                                    dev["dout"], lr)
         if dx_host is not None:
             dx_host.copy_(dx, non_blocking=True)
         return dx_host
@@ -543,11 +565,8 @@ class BertEncoderLayer:
 
         dev = self._dev_inputs(B, S)
 
-        def fn():
-            self.forward(dev["x"], dev["add_mask"], dev["keep_attn"], dev["keep1"], dev["keep2"])
-            self.backward(dev["dout"])
-            if lr is not None:
-                self.sgd_step(lr)
+        def fn():  # fwd + bwd (+ bucketed NCCL allreduce when data parallel) (+ SGD)
+            self.train_step(dev["x"], dev["add_mask"], dev["keep_attn"], dev["keep1"], dev["keep2"], dev["dout"], lr)
 
         keep = self.training_state()
         if timer is None:
@@ -573,3 +592,38 @@ class BertEncoderLayer:
         """Static device buffers a captured step reads (fill before replay)."""
         return self._dev_inputs(B, S)
 
+
+
+def fused_step_bytes(c: BertLayerConfig, B: int, S: int) -> int:
+    """Compulsory HBM bytes of one fused training step (bf16 fused attention
+    path, SGD included): every kernel's tensor arguments read once and written
+    once, as scheduled by BertEncoderLayer.forward / backward / sgd_step."""
+    T, H, F, NH = B * S, c.hidden, c.ffn, c.heads
+    e = torch.tensor([], dtype=c.dtype).element_size()
+    th, tf, t3 = T * H * e, T * F * e, T * 3 * H * e
+    fused = c.fused_attention and c.dtype == torch.bfloat16 and c.head_dim == 64 and S % 128 == 0 and S <= 512
+    bits = B * NH * S * S // 8
+    lse = B * NH * S * 4
+    kb = T * H // 8 if fused and H % 32 == 0 else T * H  # BDRLN keep flags (packed or u8)
+    w = lambda n, k: n * k * e  # noqa: E731  (bf16 weight operand)
+    g32 = lambda n, k: n * k * 4  # noqa: E731  (f32 weight gradient)
+    ds = B * NH * S * S * e  # dSᵀ, written by the key-strip kernel, read by the dQ GEMM
+    attn_bwd = (2 * th + lse) + (t3 + th + 2 * lse + bits + ds + 2 * t3 // 3) + (ds + t3 // 3 + t3 // 3)
+    fwd = (th + w(3 * H, H) + t3) + (t3 + bits + th + bits + lse) + (th + w(H, H) + th) \
+        + (2 * th + kb + 2 * th) + (th + w(F, H) + 2 * tf) + (tf + w(H, F) + th) + (2 * th + kb + 2 * th)
+    bwd = (2 * th + kb + 2 * th) + (th + w(H, F) + tf + tf) + (th + tf + g32(H, F)) + tf \
+        + (tf + w(F, H) + th + th) + (tf + th + g32(F, H)) + (2 * th + kb + 2 * th) + (th + w(H, H) + th) \
+        + (2 * th + g32(H, H)) + attn_bwd \
+        + (t3 + w(3 * H, H) + th + th) + (t3 + th + g32(3 * H, H))
+    nparam = sum(_numel(sh) for _, sh in _param_specs(c))
+    sgd = nparam * (4 + 4 + 4 + (2 if c.dtype == torch.bfloat16 else 0))
+    return int(fwd + bwd + sgd)
+
+
+def fused_step_flops(c: BertLayerConfig, B: int, S: int) -> int:
+    """Algorithmic contraction FLOPs of one fwd+bwd step (SURVEY.md §8a row
+    a8): QKV, QKᵀ, PV, out-proj, FFN1, FFN2 forward, x3 for the backward."""
+    T = B * S
+    fwd = 2 * T * c.hidden * (3 * c.hidden) + 2 * 2 * B * c.heads * S * S * c.head_dim \
+        + 2 * T * c.hidden * c.hidden + 2 * 2 * T * c.hidden * c.ffn
+    return 3 * fwd

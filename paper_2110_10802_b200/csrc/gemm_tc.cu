@@ -181,7 +181,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const __grid_constant__ CUtensorMap map_d, const __grid_constant__ CUtensorMap map_o,
                const __grid_constant__ CUtensorMap map_x, const TcParams p) {
-  pdl_trigger();
   using Cfg = TcCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int BN_LOAD = BN / CG;  // B columns each CTA loads
@@ -234,6 +233,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // dependents launch only once this CTA holds its TMEM: a dependent grid's CTA
+  // allocating first on this SM would block our alloc while it waits on us
+  pdl_trigger();
   pdl_wait();  // setup above overlapped the previous kernel's tail
   if (threadIdx.x == 0) TRACE(1);
 

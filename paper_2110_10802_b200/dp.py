@@ -5,10 +5,12 @@ gradient (paper-only, SPEC.md:8 scopes it out of the
 reference).  Here one process drives one GPU; gradients live in one flat f32
 arena per model (bert.FlatArena), ordered so that the buckets at the front
 complete first during the backward pass.  ``GradAllReducer`` splits the
-arena into ~25 MB buckets and all-reduces each on a dedicated communication
-stream as soon as ``mark_ready(offset)`` says the backward has produced
-everything below ``offset`` — so NCCL traffic over NVLink overlaps the rest
-of the backward.  Averaging is folded into the optimizer's learning rate (no
+arena into buckets aligned to parameter-group boundaries and all-reduces each
+on a dedicated communication stream as soon as ``mark_ready(offset)`` says
+the backward has produced everything below ``offset`` — so NCCL traffic over
+NVLink overlaps the rest of the backward (bert.py / efficientnet.py call it
+after each weight-gradient group; the whole step, collectives included, is
+one CUDA graph under NCCL).  Averaging is folded into the optimizer's learning rate (no
 extra pass over the gradients).
 
 SyncBN (MBConv): ``gather_bn_sets`` all-gathers each rank's per-channel
@@ -27,48 +29,81 @@ import torch.distributed as dist
 
 
 class GradAllReducer:
-    def __init__(self, flat: torch.Tensor, group=None, bucket_bytes: int = 25 << 20):
+    """Bucketed SUM-allreduce of a flat gradient arena, overlapped with the
+    backward pass.
+
+    ``boundaries`` (optional) are arena offsets at which the backward
+    finishes a parameter group (the models order their arenas by gradient
+    production, bert._param_specs / efficientnet.param_specs): buckets are
+    then unions of whole groups of up to ``bucket_bytes``, so a bucket never
+    waits on a group the backward has not reached.  Without boundaries the
+    arena is cut every ``bucket_bytes``.
+
+    ``mark_ready(offset, streams)``: everything in [0, offset) is final once
+    the work queued so far on ``streams`` (the compute stream and the forked
+    weight-gradient stream) has run; every bucket below ``offset`` is then
+    all-reduced on the communication stream behind an event of each of those
+    streams.  ``finish()`` launches the rest and joins the communication
+    stream back into the current stream.  All of it is stream-ordered (no
+    host waits on CUDA), so a whole step — backward, NCCL buckets, SGD — can
+    be captured in one CUDA graph."""
+
+    def __init__(self, flat: torch.Tensor, group=None, bucket_bytes: int = 25 << 20, boundaries=None):
         if flat.dim() != 1:
             raise ValueError("GradAllReducer: expects a flat 1-D gradient arena")
         self.flat = flat
         self.group = group
         self.world = dist.get_world_size(group)
         per = max(1, bucket_bytes // flat.element_size())
-        self.buckets = [(o, min(o + per, flat.numel())) for o in range(0, flat.numel(), per)]
+        n = flat.numel()
+        if boundaries is None:
+            self.buckets = [(o, min(o + per, n)) for o in range(0, n, per)]
+        else:
+            cuts = sorted({int(b) for b in boundaries if 0 < int(b) < n}) + [n]
+            self.buckets, lo, prev = [], 0, 0
+            for c in cuts:
+                if c - lo > per and prev > lo:  # close the bucket at the previous group end
+                    self.buckets.append((lo, prev))
+                    lo = prev
+                prev = c
+            self.buckets.append((lo, n))
         self.cuda = flat.is_cuda
         self.stream = torch.cuda.Stream(device=flat.device) if self.cuda else None
+        self.launched = 0  # collectives issued (bench / tests)
         self.reset()
 
     def reset(self):
         self.next = 0
         self.works = []
 
-    def _launch(self, lo, hi):
+    def _launch(self, lo, hi, streams):
         view = self.flat[lo:hi]
+        self.launched += 1
         if self.cuda:
-            ev = torch.cuda.Event()
-            ev.record()  # gradients below `hi` were produced on the compute stream
-            with torch.cuda.stream(self.stream):
+            for s in streams or (torch.cuda.current_stream(self.flat.device),):
+                ev = torch.cuda.Event()
+                ev.record(s)  # gradients below `hi` were produced on these streams
                 self.stream.wait_event(ev)
+            with torch.cuda.stream(self.stream):
                 self.works.append(dist.all_reduce(view, group=self.group, async_op=True))
         else:
             self.works.append(dist.all_reduce(view, group=self.group, async_op=True))
 
-    def mark_ready(self, offset: int):
-        """All gradient elements in [0, offset) are final: launch every bucket
-        that lies entirely below ``offset``."""
+    def mark_ready(self, offset: int, streams=None):
+        """All gradient elements in [0, offset) are final (after the work
+        queued so far on ``streams``): launch every bucket entirely below it."""
         while self.next < len(self.buckets) and self.buckets[self.next][1] <= offset:
-            self._launch(*self.buckets[self.next])
+            self._launch(*self.buckets[self.next], streams)
             self.next += 1
 
-    def finish(self):
-        """Launch the remaining buckets and make the compute stream wait for
+    def finish(self, streams=None):
+        """Launch the remaining buckets and make the current stream wait for
         all of them.  Returns the world size (the gradient is a SUM)."""
-        self.mark_ready(self.flat.numel())
+        self.mark_ready(self.flat.numel(), streams)
         for w in self.works:
             w.wait()
         if self.cuda:
-            torch.cuda.current_stream().wait_stream(self.stream)
+            torch.cuda.current_stream(self.flat.device).wait_stream(self.stream)
         self.works = []
         self.next = 0
         return self.world

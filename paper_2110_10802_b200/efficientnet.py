@@ -90,6 +90,33 @@ STEM_K = 32  # 3x3x3 = 27 im2col taps, padded to a 16-byte multiple
 
 
 def param_specs(c: EffNetConfig):
+    """Arena order = the order ``EfficientNetB0.backward`` finishes the
+    gradients (classifier and head first, then the blocks from last to first,
+    the stem last; inside a block: project BN, project weight, the MBConv
+    parameters, expand BN, expand weight), so the bucketed data-parallel
+    allreduce (dp.GradAllReducer) reduces the front of the arena while the
+    backward is still producing the rest."""
+    model = dict(model_specs(c))
+    order = ["fc.w", "fc.b", "head.g", "head.b", "head.w"]
+    for i in reversed(range(len(c.blocks()))):
+        p = f"b{i}."
+        order += [p + n for n in ("g3", "b3", "wp", "wdw", "g", "b", "wr", "br", "wse", "bse", "g1", "b1", "we")
+                  if p + n in model]
+    order += ["stem.g", "stem.b", "stem.w"]
+    assert sorted(order) == sorted(model)
+    return [(n, model[n]) for n in order]
+
+
+def grad_group_ends(c: EffNetConfig):
+    """Last arena entry of each gradient group (head, every block, stem)."""
+    ends = ["head.w"]
+    for i in reversed(range(len(c.blocks()))):
+        ends.append(f"b{i}." + ("we" if c.blocks()[i][0] != 1 else "bse"))
+    return ends + ["stem.w"]
+
+
+def model_specs(c: EffNetConfig):
+    """Parameters in model order (initialisation draws in this order)."""
     specs = [("stem.w", (c.stem, STEM_K)), ("stem.g", (c.stem,)), ("stem.b", (c.stem,))]
     for i, (e, k, s, ci, cx, co, se) in enumerate(c.blocks()):
         p = f"b{i}."
@@ -224,11 +251,33 @@ class EfficientNetB0:
         self._pads = (ctypes.c_int * 4)(1, 1, 1, 1)
         self.concurrent = True  # weight gradients on a forked stream (backward)
         self._bufs = {}
+        self.reducer = None
+        if process_group is not None and self.world > 1:
+            self.attach_process_group(process_group)
+
+    def attach_process_group(self, group=None, bucket_bytes: int = 4 << 20):
+        """Data parallel: the backward all-reduces (SUM) the gradient arena
+        bucket by bucket as the head, each block and the stem finish their
+        gradients; ``train_step`` folds the 1/world average into the SGD
+        learning rate."""
+        from .dp import GradAllReducer
+
+        G = self.grad
+        ends = [G.offsets[n][0] + G[n].numel() for n in grad_group_ends(self.cfg)]
+        self.reducer = GradAllReducer(G.flat, group, bucket_bytes, boundaries=ends)
+        return self.reducer
+
+    def _ready(self, name):
+        if self.reducer is not None:
+            off, _ = self.grad.offsets[name]
+            main = torch.cuda.current_stream(self.device)
+            streams = (main, self._side) if self.concurrent and hasattr(self, "_side") else (main,)
+            self.reducer.mark_ready(off + self.grad[name].numel(), streams)
 
     # ------------------------------------------------------------ parameters
     def _init(self, seed):
         g = torch.Generator(device="cpu").manual_seed(seed)
-        for name, (off, shape) in self.master.offsets.items():
+        for name, shape in model_specs(self.cfg):  # draw order independent of the arena order
             v = self.master[name]
             leaf = name.split(".")[-1]
             if leaf in ("g", "g1", "g3"):
@@ -347,8 +396,11 @@ class EfficientNetB0:
         with self.fork(dhh):
             with K.label("head.wgrad"):
                 _gemm(dhh.view(-1, c.head).t(), self.last.view(-1, Cl).t(), G["head.w"])
-        for b in reversed(self.blocks):
+        self._ready("head.w")
+        for i in reversed(range(len(self.blocks))):
+            b = self.blocks[i]
             dcur = b.backward(dcur)
+            self._ready(b.p + ("we" if b.e != 1 else "bse"))
         dh = self.stem_bn.backward(dcur)
         with self.fork(dh):
             with K.label("stem.wgrad"):
@@ -360,11 +412,18 @@ class EfficientNetB0:
         with K.label("sgd_update"):
             K.sgd_update(self.master.flat, self.grad.flat, lr, None if self.wlow is None else self.wlow.flat)
 
+    def reduce_gradients(self):
+        """Finish the bucketed gradient allreduce the backward started (data
+        parallel; no-op for one replica).  Returns the world size."""
+        return self.reducer.finish() if self.reducer is not None else 1
+
     def train_step(self, x, labels, lr=None):
+        """fwd + bwd (+ bucketed gradient allreduce) (+ SGD on the replica-averaged gradient)."""
         loss = self.forward(x, labels)
         self.backward()
+        world = self.reduce_gradients()
         if lr is not None:
-            self.sgd_step(lr)
+            self.sgd_step(lr / world)
         return loss
 
     # ------------------------------------------------------------ graph / host API
@@ -392,11 +451,10 @@ class EfficientNetB0:
 
     def capture_step(self, N: int, lr=None, timer=None):
         """Forward + backward (+ SGD) on the static ``device_inputs(N)`` as one
-        CUDA graph (single process: SyncBN collectives cannot sit inside)."""
+        CUDA graph.  Data parallel, the SyncBN statistics collectives and the
+        gradient buckets are captured with it (NCCL; gloo cannot be captured)."""
         from .graphs import CapturedStep
 
-        if self.world > 1:
-            raise ShapeError("capture_step: SyncBN collectives run eagerly (world > 1)")
         dev = self.device_inputs(N)
         self.loss = dev["loss"]  # per input slot: the graph bakes this buffer in
 

@@ -107,3 +107,23 @@ def _syncbn_case(rank, world):
 
 def test_syncbn_statistics_protocol():
     _run(_syncbn_case)
+
+
+def _group_bucket_case(rank, world):
+    from paper_2110_10802_b200.dp import GradAllReducer
+
+    n = 1000
+    flat = torch.ones(n) * (rank + 1)
+    # parameter groups end at 100, 300, 350, 900; buckets of <= 300 elements
+    red = GradAllReducer(flat, bucket_bytes=300 * 4, boundaries=[100, 300, 350, 900])
+    assert red.buckets == [(0, 300), (300, 350), (350, 900), (900, 1000)], red.buckets
+    red.mark_ready(120)  # first group done: its bucket still waits for the second group
+    assert red.launched == 0
+    red.mark_ready(350)
+    assert red.launched == 2
+    assert red.finish() == world and red.launched == 4
+    assert torch.equal(flat, torch.full((n,), float(sum(r + 1 for r in range(world)))))
+
+
+def test_group_aligned_buckets():
+    _run(_group_bucket_case)

@@ -76,7 +76,7 @@ def _run(qkv, am, keep, dctx, B, S, NH, dropout=True):
     return f(ctx), f(lse), f(dqkv), kr, kc
 
 
-@pytest.mark.parametrize("B,NH,S", [(2, 2, 128), (1, 3, 256), (2, 2, 384), (2, 12, 512)])
+@pytest.mark.parametrize("B,NH,S", [(2, 2, 128), (1, 3, 256), (2, 2, 384), (2, 12, 512), (8, 12, 512)])
 def test_attention_vs_oracle(B, NH, S):
     qkv, am, keep, dctx = _case(B, NH, S, seed=S + NH)
     ctx, lse, dqkv, _, _ = _run(qkv, am, keep, dctx, B, S, NH)
@@ -131,6 +131,26 @@ def test_attention_no_dropout_no_mask():
     ctx, _, dqkv, _, _ = _run(qkv, am, keep, dctx, B, S, NH, dropout=False)
     w_ctx, _, w_dqkv = _oracle(qkv, am, keep, dctx, B, S, NH, p_drop=0.0)
     assert O.compare(ctx, w_ctx) <= 2e-2
+    assert O.compare_scaled(dqkv, w_dqkv) <= 2e-2
+
+
+def test_attention_online_rescale():
+    """Key chunks whose scores exceed the first chunk's max by far more than
+    2^8 (a large additive mask on the first 128 keys of some sequences, and
+    one sequence where only some rows see it): the forward's lazily rescaled
+    reference max must move, warp-uniformly, for exactly those rows."""
+    B, NH, S = 2, 3, 512
+    qkv, am, keep, dctx = _case(B, NH, S, seed=21)
+    am[0, :128] = -30.0  # every row of sequence 0: chunk 0 is ~2^43 below the rest
+    qkv = qkv.copy()
+    H = NH * 64
+    # sequence 1: large keys in chunk 2 for head 0, so rows with large q see a jump there
+    qkv[S + 256:S + 384, H:H + 64] *= 6.0
+    qkv = O.round_bf16(qkv).astype(np.float64)
+    ctx, lse, dqkv, _, _ = _run(qkv, am, keep, dctx, B, S, NH)
+    w_ctx, w_lse, w_dqkv = _oracle(qkv, am, keep, dctx, B, S, NH)
+    assert O.compare(ctx, w_ctx) <= 2e-2, O.compare(ctx, w_ctx)
+    assert np.abs(lse - w_lse).max() <= 1e-2 * max(1.0, np.abs(w_lse).max())
     assert O.compare_scaled(dqkv, w_dqkv) <= 2e-2
 
 

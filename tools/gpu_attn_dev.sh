@@ -4,11 +4,11 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
-timeout 300 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_attention.py > gpurun_out/attn_test.log 2>&1
-echo "tests rc=$?"; tail -3 gpurun_out/attn_test.log
+timeout 300 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_attention.py ${EXTRA_TESTS} > gpurun_out/attn_test.log 2>&1
+echo "tests rc=$?"; tail -15 gpurun_out/attn_test.log
 timeout 120 python tools/attn_time.py > gpurun_out/attn_time.txt 2>&1; echo "new rc=$?"; cat gpurun_out/attn_time.txt
-DFX_ATTN_FWD_LEGACY=1 timeout 120 python tools/attn_time.py > gpurun_out/attn_time_legacy.txt 2>&1; echo "legacy"; cat gpurun_out/attn_time_legacy.txt
-for v in "X=1" "DFX_ATTN_FWD_LEGACY=1"; do
+DFX_ATTN_BWD_LEGACY=1 timeout 120 python tools/attn_time.py > gpurun_out/attn_time_legacy.txt 2>&1; echo "legacy"; cat gpurun_out/attn_time_legacy.txt
+for v in "X=1" "DFX_ATTN_BWD_LEGACY=1"; do
   env $v timeout 240 python bench.py --steps 30 --warmup 5 --no-extra --no-cpu-baseline > gpurun_out/b_ab.json 2> gpurun_out/b_ab.err
   echo "[$v] rc=$?"
   python - <<'P'
