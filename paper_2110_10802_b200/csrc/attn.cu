@@ -584,8 +584,9 @@ attn_fwd2_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParam
         mref = cmax;
       } else if (__any_sync(0xffffffffu, cmax > mref + 8.f)) {
         // rare: a row's reference max moves up; O (after PV_{j-1}) and the row
-        // sum rescale.  The TMEM load / store are warp-collective (.sync.aligned),
-        // so the whole warp takes this branch; rows that keep their max use f = 1
+        // sum rescale.  The TMEM load / store are warp-collective (.sync.aligned):
+        // the whole warp takes this branch (a lane-divergent tcgen05.ld hung the
+        // GPU), rows that keep their max use f = 1
         const bool up = cmax > mref + 8.f;
         const float f = up ? ex2(mref - cmax) : 1.f;
         mbar_wait(bar_pv, (j - 1) & 1);
@@ -1225,322 +1226,6 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
   }
 }
 
-// ------------------------------------------------ backward, single exp pass
-// The dq and dkdv strip kernels above both recompute S and dPd (7 MMAs and two
-// exp passes per tile pair).  Here ONE key-strip kernel does the exp pass once
-// and also forms this strip's dQ contribution per 128-query chunk,
-//     dQp[kb][q_j] = dS_j · K_kb          (M = 128 queries, N = 64, K = 128 keys)
-// with dS_j read from the same shared-memory tile the dK MMA consumes (as an
-// MN-major A operand) into 64 spare TMEM columns; the fp32 partial leaves
-// through the softmax warps.  A small fixed-order reduce sums the S/128 strip
-// partials per query (deterministic, no atomics) and emits dQ in bf16 plus the
-// query-bias column sums.  D = rowsum(dO∘O) comes from a tiny pre-pass.
-//   delta   D                                   (reads O, dO: 12.6 MB at C2)
-//   dkdv3   dK, dV, dQ partials, key/value-bias column sums
-//   dqred   dQ = Σ_kb dQp[kb] (+ query-bias column sums)
-
-// D = rowsum(dO ∘ O): four threads per (row, head) slice of 64, 16 bytes of
-// each operand in flight twice per thread, a 4-lane shuffle reduction
-__global__ void __launch_bounds__(256) attn_bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
-                                                             const __nv_bfloat16* __restrict__ dout, int64_t ld,
-                                                             int T, int S, int NH, float* __restrict__ delta) {
-  pdl_trigger();
-  pdl_wait();
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int slice = t >> 2, qtr = t & 3;
-  const bool live = slice < T * NH;
-  const int row = live ? slice / NH : 0, h = live ? slice - row * NH : 0;
-  float2 acc = make_float2(0.f, 0.f);
-  if (live) {
-    const uint4* a = reinterpret_cast<const uint4*>(o + (size_t)row * ld + h * DH + qtr * 16);
-    const uint4* g = reinterpret_cast<const uint4*>(dout + (size_t)row * ld + h * DH + qtr * 16);
-    const uint4 va0 = __ldg(a), va1 = __ldg(a + 1), vg0 = __ldg(g), vg1 = __ldg(g + 1);
-    const __nv_bfloat162* x0 = reinterpret_cast<const __nv_bfloat162*>(&va0);
-    const __nv_bfloat162* x1 = reinterpret_cast<const __nv_bfloat162*>(&va1);
-    const __nv_bfloat162* y0 = reinterpret_cast<const __nv_bfloat162*>(&vg0);
-    const __nv_bfloat162* y1 = reinterpret_cast<const __nv_bfloat162*>(&vg1);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      acc = __ffma2_rn(__bfloat1622float2(x0[e]), __bfloat1622float2(y0[e]), acc);
-      acc = __ffma2_rn(__bfloat1622float2(x1[e]), __bfloat1622float2(y1[e]), acc);
-    }
-  }
-  float v = acc.x + acc.y;
-  v += __shfl_xor_sync(0xffffffffu, v, 1);
-  v += __shfl_xor_sync(0xffffffffu, v, 2);
-  if (live && qtr == 0) {
-    const int b = row / S, srow = row - b * S;
-    delta[((size_t)b * NH + h) * S + srow] = v;
-  }
-}
-
-// dK / dV strip + dQ partials: CTA = (b, h, 128-key block); loops over
-// 128-query chunks.  TMEM: Sᵀ 128 | dPdᵀ 128 | dK 64 | dV 64 | dQp 64.
-__global__ void __maxnreg__(112)
-attn_bwd_dkdv3_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
-                      const AttnBwdParams p, float* __restrict__ dqp) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const uint32_t sbase = smem_u32(smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + DkvSmem::BAR);
-  uint64_t *bar_a = bar, *bar_s = bar + 1, *bar_tfree = bar + 2, *bar_pds = bar + 3, *bar_pdsfree = bar + 4;
-  uint64_t* bar_dqfree = bar + 5;
-  uint64_t* full = bar + 8;    // [NST]
-  uint64_t* empty = bar + 12;  // [NST]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-  constexpr int NST = DkvSmem::NST;
-  float* lse_s = reinterpret_cast<float*>(smem + DkvSmem::LSE);
-  float* del_s = reinterpret_cast<float*>(smem + DkvSmem::DEL);
-
-  const int S = p.S, nch = S / CH;
-  const int kb = blockIdx.x % (S / QT);
-  const int bh = blockIdx.x / (S / QT);
-  const int b = bh / p.NH, h = bh % p.NH;
-  const int k0 = kb * QT, row0 = b * S;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    mbar_init(bar_a, 1);
-    mbar_init(bar_s, 1);
-    mbar_init(bar_tfree, kSoftWarps);
-    mbar_init(bar_pds, kSoftWarps);
-    mbar_init(bar_pdsfree, 1);
-    mbar_init(bar_dqfree, kSoftWarps);
-    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_do)) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // dependents launch only once this CTA holds its TMEM (see attn_fwd_kernel)
-  pdl_trigger();
-  pdl_wait();  // setup above overlapped the delta kernel
-  if (threadIdx.x == 0) ATRACE(0);
-  constexpr uint32_t T_S = 0, T_DP = 128, T_DK = 256, T_DV = 320, T_DQ = 384;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(bar_a, 2 * QT * 128 + 2 * S * 4);
-      const uint32_t ba = smem_u32(bar_a);
-      bulk_g2s(lse_s, p.lse + (size_t)bh * S, S * 4, ba);
-      bulk_g2s(del_s, p.delta + (size_t)bh * S, S * 4, ba);
-      for (int u = 0; u < 2; ++u) {
-        tma_load_4d_cg<1>(&map_qkv, ba, smem + DkvSmem::K + u * 8 * KB, p.H + h * DH, row0 + k0 + 64 * u, 0, 0);
-        tma_load_4d_cg<1>(&map_qkv, ba, smem + DkvSmem::V + u * 8 * KB, 2 * p.H + h * DH, row0 + k0 + 64 * u, 0, 0);
-      }
-      for (int j = 0; j < nch; ++j) {
-        const int s = j % NST;
-        mbar_wait(&empty[s], ((j / NST) & 1) ^ 1);
-        mbar_expect_tx(&full[s], DkvSmem::STAGE);
-        const uint32_t bf = smem_u32(&full[s]);
-        uint8_t* stq = smem + DkvSmem::RING + s * DkvSmem::STAGE;
-        for (int u = 0; u < 2; ++u) {
-          tma_load_4d_cg<1>(&map_qkv, bf, stq + u * 8 * KB, h * DH, row0 + j * CH + 64 * u, 0, 0);
-          tma_load_4d_cg<1>(&map_do, bf, stq + CH * 128 + u * 8 * KB, h * DH, row0 + j * CH + 64 * u, 0, 0);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc_s = make_idesc(CH, QT, 0, 0);
-      const uint32_t idesc_g = make_idesc(DH, QT, 0, 1);
-      const uint32_t idesc_q = make_idesc(DH, CH, 1, 1);  // A = dS (queries x keys) MN-major, B = K MN-major
-      const uint64_t kdesc = make_sdesc(sbase + DkvSmem::K, 16, 1024);
-      const uint64_t vdesc = make_sdesc(sbase + DkvSmem::V, 16, 1024);
-      const uint64_t kmn = make_sdesc(sbase + DkvSmem::K, 8 * KB, 1024);
-      // dSᵀ tile = two [128 keys x 64 queries] SW128 tiles, 16 KB apart: as an
-      // MN-major A (M = queries) the two 64-query atoms are 16 KB apart (LBO)
-      const uint64_t dsmn = make_sdesc(sbase + DkvSmem::DS, 16 * KB, 1024);
-      mbar_wait(bar_a, 0);
-      ATRACE(1);
-      auto issue_grads = [&](int j) {  // dV += Pdᵀ·dO_j ; dK += dSᵀ·Q_j ; dQp_j = dS_j·K
-        mbar_wait(bar_pds, j & 1);
-        tc_fence_after();
-        const uint32_t stq = sbase + DkvSmem::RING + (j % NST) * DkvSmem::STAGE;
-        const uint64_t qmn = make_sdesc(stq, 8 * KB, 1024);
-        const uint64_t domn = make_sdesc(stq + CH * 128, 8 * KB, 1024);
-#pragma unroll
-        for (int kc = 0; kc < CH / 16; ++kc) {
-          const uint64_t pd = make_sdesc(sbase + DkvSmem::PD + (kc >> 2) * 16 * KB, 16, 1024);
-          const uint64_t ds = make_sdesc(sbase + DkvSmem::DS + (kc >> 2) * 16 * KB, 16, 1024);
-          const uint32_t acc = (j > 0 || kc > 0) ? 1u : 0u;
-          tc_mma_cg<1>(tmem + T_DV, pd + 2 * (kc & 3), domn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
-          tc_mma_cg<1>(tmem + T_DK, ds + 2 * (kc & 3), qmn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
-        }
-        tc_commit_cg<1>(&empty[j % NST]);
-        if (j > 0) mbar_wait(bar_dqfree, (j - 1) & 1);  // softmax warps read dQp_{j-1}
-        tc_fence_after();
-#pragma unroll
-        for (int kc = 0; kc < QT / 16; ++kc)  // K dim = the strip's 128 keys
-          tc_mma_cg<1>(tmem + T_DQ, dsmn + (uint64_t)(kc * (2048 >> 4)), kmn + (uint64_t)(kc * (2048 >> 4)),
-                       idesc_q, kc > 0 ? 1u : 0u);
-        tc_commit_cg<1>(bar_pdsfree);
-      };
-      for (int j = 0; j < nch; ++j) {
-        mbar_wait(&full[j % NST], (j / NST) & 1);
-        if (j > 0) mbar_wait(bar_tfree, (j - 1) & 1);
-        tc_fence_after();
-        const uint32_t stq = sbase + DkvSmem::RING + (j % NST) * DkvSmem::STAGE;
-        const uint64_t qdesc = make_sdesc(stq, 16, 1024);
-        const uint64_t dodesc = make_sdesc(stq + CH * 128, 16, 1024);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          tc_mma_cg<1>(tmem + T_S, kdesc + 2 * kk, qdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
-          tc_mma_cg<1>(tmem + T_DP, vdesc + 2 * kk, dodesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
-        }
-        tc_commit_cg<1>(bar_s);
-        if (j > 0) issue_grads(j - 1);
-      }
-      issue_grads(nch - 1);
-    }
-  } else {
-    const int sw = warp - 2, q = warp & 3, part = sw >> 2;
-    const int rl = q * 32 + lane, key = k0 + rl;
-    const int st = threadIdx.x - 64;
-    const int words = S / 32;
-    const size_t keyi = (size_t)bh * S + key;
-    uint32_t kbw[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    if (p.kb_col) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < nch) kbw[j] = __ldg(p.kb_col + keyi * words + ((j * CH + part * 32) >> 5));
-    }
-    const float mraw = p.add_mask ? __ldg(p.add_mask + (size_t)b * S + key) : 0.f;
-    const float4* klut = reinterpret_cast<const float4*>(smem + DkvSmem::LUT);
-    fill_keep_lut(reinterpret_cast<float4*>(smem + DkvSmem::LUT), st, 1.f);
-    named_bar(1, kSoftWarps * 32);
-    mbar_wait(bar_a, 0);
-    const float mrow = mraw * kLog2e + __log2f(p.scale);
-    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    // this thread's dQ-partial row slice: query q0 + rl of chunk j, columns 16 part .. +15
-    float* dqrow = dqp + (((size_t)bh * (S / QT) + kb) * S + rl) * DH + part * 16;
-    for (int j = 0; j < nch; ++j) {
-      mbar_wait(bar_s, j & 1);
-      tc_fence_after();
-      float s[32], dp[32];
-      tmem_ld32(trow + T_S + part * 32, s);
-      tmem_ld32(trow + T_DP + part * 32, dp);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_tfree);
-      const int qc0 = j * CH + part * 32;
-      const uint32_t bits = j == 0 ? kbw[0] : (j == 1 ? kbw[1] : (j == 2 ? kbw[2] : kbw[3]));
-      uint32_t pkp[16], pks[16];
-      const float2 sc2x2 = make_float2(p.sc2, p.sc2), mrow2 = make_float2(mrow, mrow), ks2 = make_float2(p.ks, p.ks);
-      float4 kf;
-#pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        const float2 l = reinterpret_cast<const float2*>(lse_s + qc0)[i >> 1];
-        const float2 dd = reinterpret_cast<const float2*>(del_s + qc0)[i >> 1];
-        const float2 t = __ffma2_rn(make_float2(s[i], s[i + 1]), sc2x2, __fadd2_rn(mrow2, make_float2(-l.x, -l.y)));
-        const float2 P = make_float2(ex2(t.x), ex2(t.y));
-        if ((i & 3) == 0) kf = klut[(bits >> i) & 15u];
-        const float2 kk = (i & 3) ? make_float2(kf.z, kf.w) : make_float2(kf.x, kf.y);
-        const float2 pd = __fmul2_rn(P, kk);
-        const float2 dpm = __fmul2_rn(make_float2(dp[i], dp[i + 1]), kk);
-        const float2 ds = __fmul2_rn(P, __ffma2_rn(dpm, ks2, make_float2(-dd.x, -dd.y)));
-        pkp[i >> 1] = pack_bf16x2(pd.x, pd.y);
-        pks[i >> 1] = pack_bf16x2(ds.x, ds.y);
-      }
-      if (j > 0) {
-        // grads_{j-1} (and dQp_{j-1}) done: PD / DS free; move dQp_{j-1} out of TMEM
-        mbar_wait(bar_pdsfree, (j - 1) & 1);
-        tc_fence_after();
-        float o[16];
-        tmem_ld16(trow + T_DQ + part * 16, o);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_dqfree);
-        float4* d4 = reinterpret_cast<float4*>(dqrow + (size_t)(j - 1) * CH * DH);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) d4[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
-      }
-      st_row32(sbase + DkvSmem::PD, rl, part * 32, pkp);
-      st_row32(sbase + DkvSmem::DS, rl, part * 32, pks);
-      fence_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_pds);
-    }
-    mbar_wait(bar_pdsfree, (nch - 1) & 1);
-    tc_fence_after();
-    {
-      float o[16];
-      tmem_ld16(trow + T_DQ + part * 16, o);
-      float4* d4 = reinterpret_cast<float4*>(dqrow + (size_t)(nch - 1) * CH * DH);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) d4[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
-    }
-    __nv_bfloat16* grow_ptr = p.dqkv + (size_t)(row0 + key) * p.ld_dqkv + h * DH + part * 16;
-    float g2[2][16];
-    tmem_ld16(trow + T_DK + part * 16, g2[0]);
-    store_bf16x16(grow_ptr + p.H, g2[0]);
-    tmem_ld16(trow + T_DV + part * 16, g2[1]);
-    const float dvs = p.ks / p.scale;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) g2[1][i] *= dvs;
-    store_bf16x16(grow_ptr + 2 * p.H, g2[1]);
-    if (p.bias_part) {
-      float* bp = p.bias_part + (size_t)(b * (S / QT) + kb) * 3 * p.H + h * DH;
-      float* const stg[2] = {reinterpret_cast<float*>(smem + DkvSmem::DS), reinterpret_cast<float*>(smem + DkvSmem::PD)};
-      float* const scr[2] = {lse_s, del_s};
-      float* const dst[2] = {bp + p.H, bp + 2 * p.H};
-      tile_colsum_128x64<2>(stg, scr, rl, part * 16, g2, st, dst);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-  }
-}
-
-// dQ = Σ_kb dQp[kb] in strip order (deterministic), bf16 into dqkv's Q block;
-// CTA = (b, h, 128-query block), 256 threads x (8 rows x 4 columns); also the
-// block's query-bias column sums (fp32 before rounding) into bias_part
-__global__ void __launch_bounds__(256) attn_bwd_dq_reduce_kernel(const float* __restrict__ dqp, int S, int NH,
-                                                                 __nv_bfloat16* __restrict__ dqkv, int64_t ld_dqkv,
-                                                                 float* __restrict__ bias_part, int H) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float red[16][64];
-  const int nst = S / QT;
-  const int qb = blockIdx.x % nst, bh = blockIdx.x / nst;
-  const int b = bh / NH, h = bh - b * NH;
-  const int c4 = threadIdx.x & 15, r0 = threadIdx.x >> 4;
-  float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 2
-  for (int i = 0; i < 8; ++i) {
-    const int qr = qb * QT + r0 + 16 * i;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int kb = 0; kb < nst; ++kb) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(dqp + (((size_t)bh * nst + kb) * S + qr) * DH) + c4);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-    }
-    cs.x += acc.x; cs.y += acc.y; cs.z += acc.z; cs.w += acc.w;
-    uint2 w = make_uint2(pack_bf16x2(acc.x, acc.y), pack_bf16x2(acc.z, acc.w));
-    *reinterpret_cast<uint2*>(dqkv + (size_t)(b * S + qr) * ld_dqkv + h * DH + 4 * c4) = w;
-  }
-  if (bias_part) {
-    red[r0][4 * c4] = cs.x; red[r0][4 * c4 + 1] = cs.y; red[r0][4 * c4 + 2] = cs.z; red[r0][4 * c4 + 3] = cs.w;
-    __syncthreads();
-    if (threadIdx.x < 64) {
-      float u = 0.f;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) u += red[r][threadIdx.x];
-      bias_part[(size_t)(b * nst + qb) * 3 * H + h * DH + threadIdx.x] = u;
-    }
-  }
-}
-
 int check_common(int64_t B, int64_t NH, int64_t S, int64_t dh, const void* qkv, int64_t ld_qkv) {
   DFX_REQUIRE(B >= 1 && NH >= 1, DFX_ERR_SHAPE, "dfx_attn: batch and heads must be >= 1");
   DFX_REQUIRE(dh == DH, DFX_ERR_UNSUPPORTED, "dfx_attn: head_dim must be 64");
@@ -1591,7 +1276,7 @@ extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem::TOTAL);
-    cudaFuncSetAttribute(attn_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * KB);
+    cudaFuncSetAttribute(attn_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F2Smem::TOTAL);
     attr = true;
   }
   const int grid = (int)(batch * heads * (seq / QT));
@@ -1599,11 +1284,7 @@ extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   if (legacy)
     launch_k(attn_fwd_kernel, grid, kAttnThreads, FwdSmem::TOTAL, as_stream(stream), map, p);
   else
-  {
-    // DFX_ATTN_FWD2_ONE=1: one CTA per SM (debug A/B of the two-CTA residency)
-    static const int one = getenv("DFX_ATTN_FWD2_ONE") ? 1 : 0;
-    launch_k(attn_fwd2_kernel, grid, kF2Threads, one ? 160 * KB : F2Smem::TOTAL, as_stream(stream), map, p);
-  }
+    launch_k(attn_fwd2_kernel, grid, kF2Threads, F2Smem::TOTAL, as_stream(stream), map, p);
   DFX_LAUNCH_CHECK("dfx_attn_fwd");
   return DFX_OK;
 }
@@ -1613,13 +1294,8 @@ extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
 static size_t attn_delta_bytes(int64_t batch, int64_t heads, int64_t seq) {
   return ((size_t)(batch * heads * seq) * sizeof(float) + 255) & ~(size_t)255;
 }
-static size_t attn_part_bytes(int64_t batch, int64_t heads, int64_t seq) {
-  return ((size_t)(batch * (seq / QT)) * 3 * heads * DH * sizeof(float) + 255) & ~(size_t)255;
-}
-// ... then the dQ partials [B*NH][S/128 key strips][S][64] f32 of attn_bwd_dkdv3
 extern "C" size_t dfx_attn_bwd_workspace(int64_t batch, int64_t heads, int64_t seq) {
-  return attn_delta_bytes(batch, heads, seq) + attn_part_bytes(batch, heads, seq) +
-         (size_t)(batch * heads) * (seq / QT) * seq * DH * sizeof(float) + 256;
+  return attn_delta_bytes(batch, heads, seq) + (size_t)(batch * (seq / QT)) * 3 * heads * DH * sizeof(float) + 256;
 }
 
 extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t head_dim, const void* qkv,
@@ -1664,26 +1340,9 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   if (!attr) {
     cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem::TOTAL);
     cudaFuncSetAttribute(attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvSmem::TOTAL);
-    cudaFuncSetAttribute(attn_bwd_dkdv3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvSmem::TOTAL);
     attr = true;
   }
   const int grid = (int)(batch * heads * (seq / QT));
-  static const bool legacy = getenv("DFX_ATTN_BWD_LEGACY") != nullptr;  // A/B: dq + dkdv strip kernels
-  if (!legacy) {
-    const int nthr = (int)(T * heads * 4);
-    launch_k(attn_bwd_delta_kernel, (nthr + 255) / 256, 256, 0, as_stream(stream), p.ctx, p.dctx, ld_ctx, (int)T,
-             (int)seq, (int)heads, p.delta);
-    DFX_LAUNCH_CHECK("dfx_attn_bwd (delta)");
-    float* dqp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + attn_delta_bytes(batch, heads, seq) +
-                                          attn_part_bytes(batch, heads, seq));
-    p.trace = g_attn_trace;
-    launch_k(attn_bwd_dkdv3_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, p, dqp);
-    DFX_LAUNCH_CHECK("dfx_attn_bwd (dk, dv, dq partials)");
-    launch_k(attn_bwd_dq_reduce_kernel, grid, 256, 0, as_stream(stream), (const float*)dqp, (int)seq, (int)heads,
-             p.dqkv, ld_dqkv, p.bias_part, p.H);
-    DFX_LAUNCH_CHECK("dfx_attn_bwd (dq reduce)");
-    return DFX_OK;
-  }
   // debug timeline of the dq kernel, or of dkdv with DFX_ATTN_TRACE_DKDV set (tools/attn_trace.py)
   const bool trace_dkdv = getenv("DFX_ATTN_TRACE_DKDV") != nullptr;
   p.trace = trace_dkdv ? nullptr : g_attn_trace;

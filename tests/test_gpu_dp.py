@@ -57,8 +57,11 @@ def _effnet(pg):
 
     # f32: the comparison below isolates the data-parallel machinery from bf16
     # rounding (the last stages normalise 2x2 maps over a 4-image batch)
-    return EfficientNetB0(EffNetConfig(image=64, classes=40, dtype=torch.float32), device="cuda:0", seed=5,
-                          process_group=pg)
+    m = EfficientNetB0(EffNetConfig(image=64, classes=40, width=0.25, dtype=torch.float32), device="cuda:0", seed=5,
+                       process_group=pg)
+    if pg is not None:  # small buckets: several group-aligned buckets even at width 0.25
+        m.attach_process_group(pg, bucket_bytes=64 << 10)
+    return m
 
 
 def _effnet_inputs(rank, n=2):

@@ -73,12 +73,18 @@ def steps(launches):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("csv")
-    ap.add_argument("--block", type=int, default=-2, help="which flush-delimited block is the step (default: "
-                    "second to last = last plain replay before the instrumented twin's final one)")
+    ap.add_argument("--block", type=int, default=None, help="index of the flush-delimited block to use (default: "
+                    "the last block of the most common length = one timed replay of the step)")
     ap.add_argument("--slack", type=float, default=1.5)
     a = ap.parse_args()
     blocks = [b for b in steps(load(a.csv)) if len(b) > 20]
-    step = blocks[a.block]
+    if a.block is None:
+        import collections
+
+        n = collections.Counter(len(b) for b in blocks).most_common(1)[0][0]
+        step = [b for b in blocks if len(b) == n][-1]
+    else:
+        step = blocks[a.block]
     rd = sum(d.get("dram__bytes_read.sum", 0.0) for d in step)
     wr = sum(d.get("dram__bytes_write.sum", 0.0) for d in step)
     us = sum(d.get("gpu__time_duration.sum", 0.0) for d in step) / 1e3

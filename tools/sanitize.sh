@@ -18,6 +18,7 @@ SEL=(
   "tests/test_gpu_gemm.py::test_simt_f32[130-70-33]"
   "tests/test_gpu_attention.py::test_attention_vs_oracle[2-2-128]"
   "tests/test_gpu_attention.py::test_qkv_bias_grad_from_strip_partials[2-2-128]"
+  "tests/test_gpu_attention.py::test_attention_online_rescale"
   "tests/test_gpu_rowops.py::test_bdrln[37-64-dtype0]"
   "tests/test_gpu_rowops.py::test_bdrln[256-768-dtype1]"
   "tests/test_gpu_rowops.py::test_bdrln_packed_keep_identical[37-64-dtype1]"
