@@ -222,6 +222,17 @@ int dfx_gemm(const dfx_gemm_args* args, void* stream);
 size_t dfx_gemm_workspace(const dfx_gemm_args* args);
 /* 1 if the call would take the tcgen05 path. */
 int dfx_gemm_uses_tensor_cores(const dfx_gemm_args* args);
+/* SE excite folded into an MBConv block's project 1x1 conv (bf16 only):
+ *   d[m][n] = sum_k y[m][k] w[n][k],
+ *   y[m][k] = swish(z[m][k] * rstd[k]*gamma[k] + beta[k] - mean[k]*rstd[k]*gamma[k]) * gate[m / hw][k]
+ * with y formed in shared memory from the TMA-loaded z tiles (tcgen05 GEMM with
+ * A-transform warps); y is also written to y_out when non-NULL (the weight
+ * gradient's operand).  Replaces excite (dfx_mbconv_fwd_se's last pass) +
+ * the project dfx_gemm: one read of z instead of read z, write y, read y.
+ * Reference: Conv 1x1 (frontend.py:598-678) of Mul(a, Sigmoid(...)) (frontend.py:293). */
+int dfx_gemm_excite(int64_t m, int64_t k, int64_t n, const void* z, int64_t hw, const float* mean,
+                    const float* rstd, const float* gamma, const float* beta, const float* gate,
+                    const void* w, void* d, void* y_out, void* stream);
 
 /* ---- a9-a13: EfficientNet-B0 MBConv block, NHWC ---------------------------
  * x [N,H,W,C] (f32 or bf16, C % 4 (f32) / C % 8 (bf16) == 0); depthwise
@@ -249,7 +260,8 @@ int dfx_mbconv_fwd_stats(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, 
 int dfx_bn_finalize(int64_t C, int nsets, const float* sets, float eps, float momentum, float* mean,
                     float* var, float* rstd, float* run_mean, float* run_var, void* stream);
 /* pooled[N][C] = mean_hw swish(BN(z)); r[N][SE] = Wr pooled + br;
- * s[N][C] = sigmoid(We swish(r) + be); y = swish(BN(z)) * s. */
+ * s[N][C] = sigmoid(We swish(r) + be); y = swish(BN(z)) * s.  y == NULL
+ * skips the excite pass (its consumer, dfx_gemm_excite, forms y itself). */
 int dfx_mbconv_fwd_se(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int stride,
                       int ksize, const int* pads, int64_t SE, const void* z, const float* mean, const float* rstd,
                       const float* gamma, const float* beta, const float* w_r, const float* b_r,

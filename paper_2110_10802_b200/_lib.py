@@ -78,6 +78,8 @@ _SIGS = [
     ("dfx_gemm", c_int, [POINTER(GemmArgs), c_void_p]),
     ("dfx_gemm_uses_tensor_cores", c_int, [POINTER(GemmArgs)]),
     ("dfx_gemm_workspace", c_size_t, [POINTER(GemmArgs)]),
+    ("dfx_gemm_excite", c_int, [c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("dfx_mbconv_workspace", c_size_t, [c_int64, c_int64, c_int64, c_int64, c_int, c_int, c_void_p, c_int]),
     ("dfx_mbconv_fwd_stats", c_int, [c_int, c_int64, c_int64, c_int64, c_int64, c_int, c_int, c_void_p,
                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,

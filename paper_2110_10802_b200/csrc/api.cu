@@ -78,6 +78,12 @@ size_t dfx_gemm_workspace(const dfx_gemm_args* args) {
   return gemm_tc_supported(*args) ? gemm_tc_workspace(*args) : gemm_simt_workspace(*args);
 }
 
+int dfx_gemm_excite(int64_t m, int64_t k, int64_t n, const void* z, int64_t hw, const float* mean,
+                    const float* rstd, const float* gamma, const float* beta, const float* gate, const void* w,
+                    void* d, void* y_out, void* stream) {
+  return gemm_excite(m, k, n, z, hw, mean, rstd, gamma, beta, gate, w, d, y_out, as_stream(stream));
+}
+
 int dfx_gemm(const dfx_gemm_args* args, void* stream) {
   DFX_REQUIRE(args, DFX_ERR_SHAPE, "dfx_gemm: null args");
   if (int rc = check_gemm_args(*args)) return rc;

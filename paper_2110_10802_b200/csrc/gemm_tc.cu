@@ -42,6 +42,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle atom row
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = (2 + kEpiWarps) * 32;
+constexpr int kXfThreads = 128;  // A-operand transform warps of the XF = 1 (excite-folded) instantiation
 // Epilogue unit geometry (shared with the host, which builds the bulk-store
 // tensor maps): columns per epilogue warp, and bytes per staged unit row.
 __host__ __device__ constexpr int epi_wcols(int bn) { return bn <= 128 ? bn : bn / 4; }
@@ -85,6 +86,14 @@ struct TcParams {
   int64_t aux_out_stride_m, aux_out_stride_b1, aux_out_stride_b2;
   float* part;  // split-K partials [split][z][m][n]
   unsigned long long* trace;  // debug timeline (tools/gemm_trace.py), normally null
+  // XF = 1 (dfx_gemm_excite): the K-major A operand is a BatchNorm input z;
+  // the transform warps turn each landed A stage into
+  //   y = swish(z * rstd*gamma + (beta - mean*rstd*gamma)) * gate[row / x_hw][k]
+  // in place before the MMA reads it, and (optionally) write y to x_y [m][k]
+  const float *x_mean, *x_rstd, *x_gamma, *x_beta;  // [k]
+  const float* x_gate;                               // [images][k]
+  int64_t x_hw;                                      // A rows per image
+  __nv_bfloat16* x_y;                                // [m][k] or null
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -176,8 +185,8 @@ __device__ __forceinline__ TileIdx tile_of(int t, const TcParams& p) {
 // leader issues tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' shared
 // memory, and each CTA's TMEM receives its 128 accumulator rows.  Halving B
 // traffic per SM raises the flop-per-L2-byte ratio from 85 to 128.
-template <int BN, typename TO, int CG>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, typename TO, int CG, int XF = 0>
+__global__ void __launch_bounds__(kThreads + XF * kXfThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const __grid_constant__ CUtensorMap map_d, const __grid_constant__ CUtensorMap map_o,
                const __grid_constant__ CUtensorMap map_x, const TcParams p) {
@@ -194,7 +203,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   uint64_t* tfull = empty + STAGES;  // [NACC]
   uint64_t* tempty = tfull + NACC;   // [NACC]
   uint64_t* xbar = tempty + NACC;    // [kEpiWarps]: aux-operand unit landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + kEpiWarps);
+  uint64_t* xfull = xbar + kEpiWarps;  // [STAGES] (XF): A stage transformed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + (XF ? STAGES : 0));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TRACE(0);
@@ -208,6 +218,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < NACC; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * EPI_GROUP_WARPS); }
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(&xbar[w], 1);
+    if constexpr (XF != 0)
+      for (int s = 0; s < STAGES; ++s) mbar_init(&xfull[s], kXfThreads / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -298,7 +310,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&full[s], ph);
+          mbar_wait(XF ? &xfull[s] : &full[s], ph);
           tc_fence_after();
           if (it == 0) TRACE(2);
           const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
@@ -315,7 +327,63 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         if (lt < 8) TRACE(3 + lt);
       }
     }
-  } else {
+  } else if (XF != 0 && warp >= 2 + kEpiWarps) {
+    // ------------------------------------------------- A transform (XF = 1)
+    // Thread = one 16-byte chunk column (8 channels, fixed per stage) x 8 rows
+    // (r0 + 16 i) of each landed [128 x 64] A stage: the per-channel BN
+    // constants are loaded once per stage, the SE gate per row's image.  Rows
+    // past m and channels past k become zeros (TMA zero-fill would otherwise
+    // turn into swish(shift) * gate).  Same arithmetic as excite_kernel
+    // (mbconv.cu), so y is bitwise the unfused path's.
+    const int tt = threadIdx.x - (2 + kEpiWarps) * 32;
+    const int ch = tt & 7, r0 = tt >> 3;
+    uint32_t it = 0;
+    for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+      const TileIdx ti = tile_of(t, p);
+      const int64_t m0 = (int64_t)ti.mb * BM;
+      for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        const int64_t k = (int64_t)kb * BK + ch * 8;
+        const bool kin = k < p.k;  // k % 8 == 0 (host check)
+        float sc[8], sh[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          sc[i] = kin ? __ldg(p.x_rstd + k + i) * __ldg(p.x_gamma + k + i) : 0.f;
+          sh[i] = kin ? __ldg(p.x_beta + k + i) - __ldg(p.x_mean + k + i) * sc[i] : 0.f;
+        }
+        mbar_wait(&full[s], ph);
+        const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
+#pragma unroll 2
+        for (int i = 0; i < 8; ++i) {
+          const int r = r0 + 16 * i;
+          const int64_t gm = m0 + r;
+          const uint32_t addr = sa + r * 128 + ((ch ^ (r & 7)) << 4);
+          uint4 out = make_uint4(0u, 0u, 0u, 0u);
+          if (kin && gm < p.m) {
+            const uint4 zv = lds128(addr);
+            const float* gp = p.x_gate + (gm / p.x_hw) * p.k + k;
+            const float4 g0 = __ldg(reinterpret_cast<const float4*>(gp));
+            const float4 g1 = __ldg(reinterpret_cast<const float4*>(gp) + 1);
+            const float se[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            float zf[8], yv[8];
+            unpack4<__nv_bfloat16>(zv, zf);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float u = fmaf(zf[e], sc[e], sh[e]);
+              yv[e] = u * fmaf(0.5f, tanh_fast(0.5f * u), 0.5f) * se[e];
+            }
+            out = pack4<__nv_bfloat16>(yv);
+            if (p.x_y) *reinterpret_cast<uint4*>(p.x_y + gm * p.k + k) = out;
+          }
+          sts128(addr, out);
+        }
+        fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xfull[s]);
+      }
+    }
+  } else if (warp >= 2 && warp < 2 + kEpiWarps) {
     // -------------------------------------------------------------- epilogue
     // Four warps per TMEM lane quadrant (32 rows), each owning a quarter of
     // the tile's columns.  Per staging unit (32 rows x 64 bytes):
@@ -464,7 +532,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       }
     }
   }
-  if (warp >= 2 && lane == 0) bulk_wait_all();  // this warp's bulk stores are complete
+  if (warp >= 2 && warp < 2 + kEpiWarps && lane == 0) bulk_wait_all();  // this warp's bulk stores are complete
   tc_fence_before();
   if constexpr (CG == 2) {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -685,10 +753,10 @@ Plan plan(const dfx_gemm_args& p) {
   return best;
 }
 
-template <int BN, typename TO, int CG>
+template <int BN, typename TO, int CG, int XF = 0>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, const CUtensorMap& mo,
               const CUtensorMap& mx, const TcParams& tp, cudaStream_t st) {
-  auto kfn = tc_gemm_kernel<BN, TO, CG>;
+  auto kfn = tc_gemm_kernel<BN, TO, CG, XF>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN, CG>::SMEM);
@@ -697,7 +765,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& m
   const int clusters = std::min(tp.num_tiles, num_sms() / CG);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(clusters * CG);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kThreads + XF * kXfThreads);
   cfg.dynamicSmemBytes = TcCfg<BN, CG>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
@@ -732,6 +800,59 @@ int launch_tc_any(int bn, int cg, const CUtensorMap& ma, const CUtensorMap& mb, 
 }  // namespace
 
 void gemm_tc_set_trace(void* buf) { g_trace = reinterpret_cast<unsigned long long*>(buf); }
+
+// D[m][n] = y · Wᵀ with y = swish(BN(z)) * gate formed on the fly from the
+// K-major A operand z (the SE excite folded into the project 1x1 GEMM of an
+// MBConv block); y itself is also written when y_out is set (the weight
+// gradient reads it).  Single-CTA tiles (the transform warps own one CTA's A).
+int gemm_excite(int64_t m, int64_t k, int64_t n, const void* z, int64_t hw, const float* mean, const float* rstd,
+                const float* gamma, const float* beta, const float* gate, const void* w, void* d, void* y_out,
+                cudaStream_t st) {
+  DFX_REQUIRE(m > 0 && n > 0 && k > 0 && hw > 0, DFX_ERR_SHAPE, "dfx_gemm_excite: empty extent");
+  DFX_REQUIRE(k % 8 == 0 && n % 8 == 0, DFX_ERR_SHAPE, "dfx_gemm_excite: k and n must be multiples of 8");
+  DFX_REQUIRE(z && w && d && mean && rstd && gamma && beta && gate, DFX_ERR_SHAPE, "dfx_gemm_excite: null operand");
+  DFX_REQUIRE(aligned16(z) && aligned16(w) && aligned16(d) && aligned16(gate) && (!y_out || aligned16(y_out)),
+              DFX_ERR_ALIGN, "dfx_gemm_excite: operands must be 16-byte aligned");
+  dfx_gemm_args g{};
+  g.in_dtype = DFX_BF16; g.out_dtype = DFX_BF16; g.epilogue = DFX_EPI_NONE;
+  g.m = m; g.n = n; g.k = k; g.batch1 = 1; g.batch2 = 1;
+  g.a = z; g.a_stride_m = k; g.a_stride_k = 1;
+  g.b = w; g.b_stride_n = k; g.b_stride_k = 1;
+  g.d = d; g.d_stride_m = n;
+  g.alpha = 1.f;
+  Plan pl = plan(g);
+  const int bn = pl.cg == 2 ? (n > 128 ? 256 : 128) : pl.bn;  // one CTA per tile
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, z, 2, k, m, k, 1, 0, 1, 0, 64, BM, true);
+  if (rc) return rc;
+  rc = make_map(&mb, w, 2, k, n, k, 1, 0, 1, 0, 64, bn, true);
+  if (rc) return rc;
+  TcParams tp{};
+  tp.m = m; tp.n = n; tp.k = k; tp.batch2 = 1;
+  tp.m_tiles = (int)((m + BM - 1) / BM);
+  tp.n_tiles = (int)((n + bn - 1) / bn);
+  tp.k_blocks = (int)((k + BK - 1) / BK);
+  tp.splits = 1; tp.kb_per_split = tp.k_blocks;
+  tp.num_tiles = tp.m_tiles * tp.n_tiles;
+  tp.a_mn = 0; tp.b_mn = 0;
+  tp.epilogue = DFX_EPI_NONE;
+  tp.alpha = 1.f; tp.beta = 0.f;
+  tp.d = d; tp.d_stride_m = n;
+  tp.trace = g_trace;
+  tp.x_mean = mean; tp.x_rstd = rstd; tp.x_gamma = gamma; tp.x_beta = beta; tp.x_gate = gate; tp.x_hw = hw;
+  tp.x_y = reinterpret_cast<__nv_bfloat16*>(y_out);
+  const int ub = epi_ub(bn, 2);
+  const CUtensorMapSwizzle oswz =
+      ub == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : (ub == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE);
+  CUtensorMap md;
+  rc = make_map_sw(&md, d, 2, n, m, n, 1, 0, 1, 0, ub / 2, 32, oswz);
+  if (rc) return rc;
+  using T = __nv_bfloat16;
+  if (bn == 256) return launch_tc<256, T, 1, 1>(ma, mb, md, md, md, tp, st);
+  if (bn == 192) return launch_tc<192, T, 1, 1>(ma, mb, md, md, md, tp, st);
+  if (bn == 128) return launch_tc<128, T, 1, 1>(ma, mb, md, md, md, tp, st);
+  return launch_tc<64, T, 1, 1>(ma, mb, md, md, md, tp, st);
+}
 
 size_t gemm_tc_workspace(const dfx_gemm_args& p) {
   if (!gemm_tc_supported(p)) return 0;

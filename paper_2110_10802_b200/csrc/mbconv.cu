@@ -869,7 +869,7 @@ int dfx_mbconv_fwd_se(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
   const int V = dtype == DFX_BF16 ? 8 : 4;
   Geo g;
   if (int rc = make_geo(N, H, W, C, stride, ksize, pads, V, &g, "dfx_mbconv_fwd_se")) return rc;
-  DFX_REQUIRE(SE > 0 && z && mean && rstd && gamma && beta && w_r && b_r && w_e && b_e && pooled && r && s && y,
+  DFX_REQUIRE(SE > 0 && z && mean && rstd && gamma && beta && w_r && b_r && w_e && b_e && pooled && r && s,
               DFX_ERR_SHAPE, "dfx_mbconv_fwd_se: null pointer");
   DFX_REQUIRE(ws_bytes >= dfx_mbconv_workspace(N, H, W, C, stride, ksize, pads, (int)SE), DFX_ERR_WORKSPACE,
               "dfx_mbconv_fwd_se: workspace too small");
@@ -896,6 +896,7 @@ int dfx_mbconv_fwd_se(int dtype, int64_t N, int64_t H, int64_t W, int64_t C, int
   launch_k(se_fwd_kernel, g.N, 1024, (size_t)(g.C + SE) * sizeof(float), st, g, (int)SE, pool_part, w_r, b_r, w_e, b_e,
                                                                            pooled, r, s);
   DFX_LAUNCH_CHECK("dfx_mbconv_fwd_se se");
+  if (!y) return DFX_OK;  // excite folded into the consumer (dfx_gemm_excite)
   if (dtype == DFX_BF16)
     launch_k(excite_kernel<__nv_bfloat16, 8>, grid2, threads, 0, st, g, (const __nv_bfloat16*)z, bn, s,
              (__nv_bfloat16*)y);

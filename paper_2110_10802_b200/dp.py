@@ -13,8 +13,10 @@ after each weight-gradient group; the whole step, collectives included, is
 one CUDA graph under NCCL).  Averaging is folded into the optimizer's learning rate (no
 extra pass over the gradients).
 
-SyncBN (MBConv): ``gather_bn_sets`` all-gathers each rank's per-channel
-(count, mean, M2) so every rank merges them in rank order (mbconv.py);
+SyncBN (MBConv, BatchNormAct): the statistics kernels write each rank's
+per-channel (count, mean, M2) straight into its slot of a [world, 3, C]
+buffer and ``exchange_bn_sets`` all-gathers the slots in place, so every rank
+merges them in rank order (dfx_bn_finalize);
 ``allreduce_sum`` combines the backward BN sums.  Both are tiny, latency-bound
 messages.
 
@@ -121,6 +123,25 @@ def gather_bn_sets(local: torch.Tensor, out: torch.Tensor, group=None) -> torch.
     out[rank].copy_(local)
     dist.all_reduce(out, group=group)
     return out
+
+
+def bn_slot(sets: torch.Tensor, group=None) -> torch.Tensor:
+    """This rank's [3, C] slot of a [world, 3, C] SyncBN set buffer: the
+    statistics kernel writes its (count, mean, M2) straight into it, so the
+    exchange below needs no staging copy."""
+    return sets[dist.get_rank(group)]
+
+
+def exchange_bn_sets(sets: torch.Tensor, group=None) -> torch.Tensor:
+    """Complete a [world, 3, C] SyncBN set buffer whose own slot is filled:
+    under NCCL one in-place all-gather (each rank's slot is the send buffer —
+    no zeroing, no copy; a graph node like the gradient buckets); other
+    backends (gloo, CPU tests) the rank-slotted all-reduce."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(sets, bn_slot(sets, group), group=group)
+        return sets
+    mine = bn_slot(sets, group).clone()
+    return gather_bn_sets(mine, sets, group)
 
 
 def allreduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:

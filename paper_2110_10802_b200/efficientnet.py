@@ -66,6 +66,9 @@ class EffNetConfig:
     eps: float = 1e-5
     momentum: float = 0.9
     dtype: torch.dtype = torch.bfloat16
+    # bf16: the SE excite is folded into the project 1x1 GEMM (kernels.gemm_excite:
+    # y = swish(BN(z)) * s formed from z inside the tcgen05 GEMM, SURVEY §8f row 2)
+    fold_excite: bool = True
 
     def blocks(self):
         """[(expand, k, stride, cin, cexp, cout, se)] for the 16 blocks."""
@@ -183,12 +186,24 @@ class _Block:
         else:
             a = x
         self.a = a
-        y = self.mb.forward(a)
+        if self.net.cfg.fold_excite and x.dtype == torch.bfloat16:
+            # excite + project as one GEMM over z; y is still written for the weight gradient
+            self.mb.forward(a, excite=False)
+            mbb = self.mb.buffers(a.shape)
+            y = mbb["y"]
+            No, Ho, Wo, _ = y.shape
+            pr = torch.empty(No, Ho, Wo, self.co, dtype=x.dtype, device=x.device)
+            with K.label("block.excite_project_gemm"):
+                K.gemm_excite(mbb["z"].view(-1, self.cx), Ho * Wo, mbb["mean"], mbb["rstd"], self.mb.master["g"],
+                              self.mb.master["b"], mbb["s"], self.w("wp"), pr.view(-1, self.co),
+                              y_out=y.view(-1, self.cx))
+        else:
+            y = self.mb.forward(a)
+            No, Ho, Wo, _ = y.shape
+            pr = torch.empty(No, Ho, Wo, self.co, dtype=x.dtype, device=x.device)
+            with K.label("block.project_gemm"):
+                _gemm(y.view(-1, self.cx), self.w("wp"), pr.view(-1, self.co))
         self.y = y
-        No, Ho, Wo, _ = y.shape
-        pr = torch.empty(No, Ho, Wo, self.co, dtype=x.dtype, device=x.device)
-        with K.label("block.project_gemm"):
-            _gemm(y.view(-1, self.cx), self.w("wp"), pr.view(-1, self.co))
         o = self.bn3.forward(pr)
         if self.residual:
             _lib.call("dfx_add", K.dfx_dtype(o), o.numel(), o.data_ptr(), x.data_ptr(), o.data_ptr(), K._stream())

@@ -494,6 +494,35 @@ def gemm(a, b, d, epilogue=_lib.EPI_NONE, alpha=1.0, beta=1.0, bias=None, aux=No
     return d
 
 
+def gemm_excite(z, hw, mean, rstd, gamma, beta, gate, w, d, y_out=None):
+    """d [M, N] = y · wᵀ with y = swish(BN(z)) * gate[row // hw] formed inside
+    the tcgen05 GEMM from z [M, K] (the MBConv SE excite folded into the
+    project 1x1 conv, dfx_gemm_excite); y_out [M, K] receives y when given."""
+    for t, nm in ((z, "z"), (w, "w"), (d, "d")):
+        if t.dtype != torch.bfloat16 or t.dim() != 2 or not t.is_contiguous():
+            raise ShapeError(f"gemm_excite: {nm} must be a contiguous 2-D bfloat16 tensor")
+    M, Kc = z.shape
+    N = w.shape[0]
+    if w.shape[1] != Kc or d.shape != (M, N):
+        raise ShapeError("gemm_excite: shape mismatch")
+    if y_out is not None and (y_out.shape != z.shape or y_out.dtype != torch.bfloat16 or not y_out.is_contiguous()):
+        raise ShapeError("gemm_excite: y_out must match z")
+    for t, nm in ((mean, "mean"), (rstd, "rstd"), (gamma, "gamma"), (beta, "beta")):
+        _vec(t, Kc, nm)
+    if gate.dtype != torch.float32 or gate.dim() != 2 or gate.shape[1] != Kc or gate.shape[0] * hw < M:
+        raise ShapeError("gemm_excite: gate must be f32 [images, K] covering every row")
+    esz = 2
+
+    def nbytes():  # z and w read once, d written once (+ y written)
+        return M * Kc * esz + N * Kc * esz + M * N * esz + (M * Kc * esz if y_out is not None else 0)
+
+    with _span("gemm_excite", "tensor", lambda: 2.0 * M * N * Kc, nbytes):
+        _lib.call("dfx_gemm_excite", M, Kc, N, z.data_ptr(), hw, mean.data_ptr(), rstd.data_ptr(), gamma.data_ptr(),
+                  beta.data_ptr(), _contig(gate, "gate").data_ptr(), w.data_ptr(), d.data_ptr(), _ptr(y_out),
+                  _stream())
+    return d
+
+
 def gemm_uses_tensor_cores(a, b, d, **kw) -> bool:
     return bool(_lib.load().dfx_gemm_uses_tensor_cores(gemm_args(a, b, d, **kw)))
 

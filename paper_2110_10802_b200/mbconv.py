@@ -31,7 +31,7 @@ import torch
 from . import _lib
 from . import kernels as K
 from .bert import FlatArena
-from .dp import allreduce_sum, gather_bn_sets
+from .dp import allreduce_sum, bn_slot, exchange_bn_sets
 from .errors import ShapeError
 
 
@@ -132,8 +132,11 @@ class MBConvBlock:
         return self._pads_c
 
     # ------------------------------------------------------------ forward
-    def forward(self, x):
-        """x [N, H, W, C] (NHWC) -> y [N, Ho, Wo, C]; updates running stats."""
+    def forward(self, x, excite: bool = True):
+        """x [N, H, W, C] (NHWC) -> y [N, Ho, Wo, C]; updates running stats.
+        ``excite=False`` stops after the SE gate ``s`` (buffers()["s"]): the
+        caller folds y = swish(BN(z)) * s into its consumer
+        (kernels.gemm_excite) and None is returned."""
         c = self.cfg
         if x.dtype != c.dtype or x.dim() != 4 or not x.is_contiguous():
             raise ShapeError(f"MBConvBlock: x must be a contiguous NHWC {c.dtype} tensor")
@@ -146,26 +149,25 @@ class MBConvBlock:
         ws = b["ws"]
         self._saved = x
         esz = x.element_size()
+        # SyncBN: the statistics land directly in this rank's slot of the exchange buffer
+        stats = bn_slot(b["bn_sets"], self.pg) if self.world > 1 else b["bn_local"]
         with K._span("mbconv.dwconv_stats", "hbm", lambda: (N * H * W + N * Ho * Wo) * C * esz):
             _lib.call("dfx_mbconv_fwd_stats", dt, N, H, W, C, c.stride, c.ksize, pads, x.data_ptr(),
-                      P["wdw"].data_ptr(), b["z"].data_ptr(), b["bn_local"].data_ptr(), ws.data_ptr(),
+                      P["wdw"].data_ptr(), b["z"].data_ptr(), stats.data_ptr(), ws.data_ptr(),
                       ws.numel(), st)
-        if self.world > 1:
-            gather_bn_sets(b["bn_local"], b["bn_sets"], group=self.pg)
-            sets = b["bn_sets"]
-        else:
-            sets = b["bn_local"]
+        sets = exchange_bn_sets(b["bn_sets"], group=self.pg) if self.world > 1 else b["bn_local"]
         with K._span("mbconv.bn_finalize", "hbm", lambda: 8 * C * 4):
             _lib.call("dfx_bn_finalize", C, self.world, sets.data_ptr(), float(c.eps), float(c.momentum),
                       b["mean"].data_ptr(), b["var"].data_ptr(), b["rstd"].data_ptr(),
                       self.running_mean.data_ptr(), self.running_var.data_ptr(), st)
-        with K._span("mbconv.bn_swish_se_excite", "hbm", lambda: 3 * N * Ho * Wo * C * esz):
+        with K._span("mbconv.bn_swish_se_excite" if excite else "mbconv.bn_swish_se", "hbm",
+                     lambda: (3 if excite else 1) * N * Ho * Wo * C * esz):
             _lib.call("dfx_mbconv_fwd_se", dt, N, H, W, C, c.stride, c.ksize, pads, c.se, b["z"].data_ptr(),
                       b["mean"].data_ptr(), b["rstd"].data_ptr(), P["g"].data_ptr(), P["b"].data_ptr(),
                       P["wr"].data_ptr(), P["br"].data_ptr(), P["we"].data_ptr(), P["be"].data_ptr(),
-                      b["pooled"].data_ptr(), b["r"].data_ptr(), b["s"].data_ptr(), b["y"].data_ptr(),
-                      ws.data_ptr(), ws.numel(), st)
-        return b["y"]
+                      b["pooled"].data_ptr(), b["r"].data_ptr(), b["s"].data_ptr(),
+                      b["y"].data_ptr() if excite else None, ws.data_ptr(), ws.numel(), st)
+        return b["y"] if excite else None
 
     # ------------------------------------------------------------ backward
     def backward(self, dy):

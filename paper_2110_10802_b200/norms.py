@@ -15,7 +15,7 @@ import torch
 
 from . import _lib
 from . import kernels as K
-from .dp import allreduce_sum, gather_bn_sets
+from .dp import allreduce_sum, bn_slot, exchange_bn_sets
 from .errors import ShapeError
 
 ACTS = {"none": 0, "swish": 1}
@@ -84,12 +84,12 @@ class BatchNormAct:
         dt, st = K.dfx_dtype(x), K._stream()
         ws = K.WORKSPACE.get(_lib.load().dfx_batchnorm_workspace(rows, self.C))
         y = torch.empty_like(x) if y is None else y
+        # SyncBN: the statistics land directly in this rank's slot of the exchange buffer
+        stats = bn_slot(self.sets, self.pg) if self.world > 1 else self.local
         with K._span("bn_stats", "hbm", lambda: x.numel() * x.element_size()):
-            _lib.call("dfx_batchnorm_stats", dt, rows, self.C, x.data_ptr(), self.local.data_ptr(), ws.data_ptr(),
+            _lib.call("dfx_batchnorm_stats", dt, rows, self.C, x.data_ptr(), stats.data_ptr(), ws.data_ptr(),
                       ws.numel(), st)
-        sets = self.local
-        if self.world > 1:
-            sets = gather_bn_sets(self.local, self.sets, group=self.pg)
+        sets = exchange_bn_sets(self.sets, group=self.pg) if self.world > 1 else self.local
         _lib.call("dfx_bn_finalize", self.C, self.world, sets.data_ptr(), float(self.eps), float(self.momentum),
                   self.mean.data_ptr(), self.var.data_ptr(), self.rstd.data_ptr(), self.running_mean.data_ptr(),
                   self.running_var.data_ptr(), st)

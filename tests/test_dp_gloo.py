@@ -127,3 +127,17 @@ def _group_bucket_case(rank, world):
 
 def test_group_aligned_buckets():
     _run(_group_bucket_case)
+
+
+def _bn_exchange_case(rank, world):
+    from paper_2110_10802_b200.dp import bn_slot, exchange_bn_sets
+
+    sets = torch.full((world, 3, 5), -7.0)  # stale values in the other slots
+    bn_slot(sets).copy_(torch.arange(15, dtype=torch.float32).reshape(3, 5) + 100 * rank)
+    exchange_bn_sets(sets)
+    for r in range(world):
+        assert torch.equal(sets[r], torch.arange(15, dtype=torch.float32).reshape(3, 5) + 100 * r)
+
+
+def test_bn_set_exchange_in_place():
+    _run(_bn_exchange_case)

@@ -1,0 +1,101 @@
+"""SE excite folded into the MBConv project 1x1 GEMM:
+kernels.gemm_excite forms y = swish(BN(z)) * s inside the tcgen05 GEMM from
+the z tiles TMA brings in (reference: Mul(a, Sigmoid(...)) feeding a 1x1 Conv,
+frontend.py:293, 598-678).  Checked against the unfused path (the excite pass
+of dfx_mbconv_fwd_se, then dfx_gemm) — y must be bitwise identical, the
+projection equal up to fp32 accumulation order — and against an fp32 torch
+restatement, over image sizes whose 128-row tiles straddle images and channel
+counts with a K tail."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(n_img, hw, C, N, seed):
+    g = torch.Generator().manual_seed(seed)
+    z = (torch.randn(n_img * hw, C, generator=g) * 2 + 0.3).bfloat16().cuda()
+    mean = (torch.randn(C, generator=g) * 0.3).cuda()
+    rstd = (0.5 + torch.rand(C, generator=g)).cuda()
+    gamma = (1 + 0.2 * torch.randn(C, generator=g)).cuda()
+    beta = (0.2 * torch.randn(C, generator=g)).cuda()
+    gate = torch.rand(n_img, C, generator=g).cuda()
+    w = (torch.randn(N, C, generator=g) / C ** 0.5).bfloat16().cuda()
+    return z, mean, rstd, gamma, beta, gate, w
+
+
+def _torch_y(z, hw, mean, rstd, gamma, beta, gate):
+    sc = rstd * gamma
+    sh = beta - mean * sc
+    u = z.float() * sc + sh
+    sig = 0.5 * torch.tanh(0.5 * u) + 0.5
+    img = torch.arange(z.shape[0], device=z.device) // hw
+    return (u * sig * gate[img]).bfloat16()
+
+
+@pytest.mark.parametrize("n_img,hw,C,N", [(3, 49, 1152, 320), (2, 196, 144, 40), (5, 3136, 96, 24),
+                                          (1, 100, 24, 16), (4, 784, 240, 80)])
+def test_gemm_excite_vs_torch(n_img, hw, C, N):
+    from paper_2110_10802_b200 import kernels as K
+
+    z, mean, rstd, gamma, beta, gate, w = _case(n_img, hw, C, N, seed=C + N)
+    d = torch.empty(z.shape[0], N, dtype=torch.bfloat16, device="cuda")
+    y = torch.empty_like(z)
+    K.gemm_excite(z, hw, mean, rstd, gamma, beta, gate, w, d, y_out=y)
+    torch.cuda.synchronize()
+    yw = _torch_y(z, hw, mean, rstd, gamma, beta, gate)
+    # tanh.approx vs torch tanh: a bf16 ulp at most on a few elements
+    dy = (y.float() - yw.float()).abs() / yw.float().abs().clamp_min(1e-2)
+    assert float(dy.max()) <= 1.6e-2, float(dy.max())
+    dw = (y.float() @ w.float().t())
+    err = float((d.float() - dw).abs().max()) / max(1.0, float(dw.abs().max()))
+    assert err <= 1e-2, err
+
+
+def test_gemm_excite_matches_unfused_mbconv_path():
+    """y bitwise equal to the excite pass of the unfused block forward, and the
+    projection equal to dfx_gemm over that y up to accumulation order."""
+    from paper_2110_10802_b200 import kernels as K
+    from paper_2110_10802_b200.mbconv import MBConvBlock, MBConvConfig
+
+    C, Nout = 144, 40
+    blk = MBConvBlock(MBConvConfig(channels=C, se=6, stride=1, pads=(1, 1, 1, 1), eps=1e-3, momentum=0.9,
+                                   dtype=torch.bfloat16), seed=4)
+    x = torch.randn(3, 14, 14, C, generator=torch.Generator().manual_seed(9)).bfloat16().cuda()
+    w = (torch.randn(Nout, C, generator=torch.Generator().manual_seed(10)) / C ** 0.5).bfloat16().cuda()
+    y_ref = blk.forward(x).clone()
+    pr_ref = torch.empty(3 * 14 * 14, Nout, dtype=torch.bfloat16, device="cuda")
+    K.gemm(y_ref.view(-1, C), w, pr_ref)
+    blk2 = MBConvBlock(MBConvConfig(channels=C, se=6, stride=1, pads=(1, 1, 1, 1), eps=1e-3, momentum=0.9,
+                                    dtype=torch.bfloat16), seed=4)
+    assert blk2.forward(x, excite=False) is None
+    b = blk2.buffers(x.shape)
+    y = torch.empty_like(y_ref)
+    pr = torch.empty_like(pr_ref)
+    K.gemm_excite(b["z"].view(-1, C), 14 * 14, b["mean"], b["rstd"], blk2.master["g"], blk2.master["b"], b["s"], w,
+                  pr, y_out=y.view(-1, C))
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)
+    err = float((pr.float() - pr_ref.float()).abs().max()) / max(1.0, float(pr_ref.float().abs().max()))
+    assert err <= 1e-2, err
+
+
+def test_effnet_fold_equals_unfolded():
+    """Whole EfficientNet-B0 training step (bf16): the folded excite changes no
+    number beyond GEMM accumulation order — loss and every gradient agree."""
+    from paper_2110_10802_b200.efficientnet import EfficientNetB0, EffNetConfig
+
+    g = torch.Generator().manual_seed(3)
+    x = torch.randn(4, 96, 96, 3, generator=g).bfloat16().cuda()
+    lab = torch.randint(0, 50, (4,), generator=g, dtype=torch.int32).cuda()
+    out = []
+    for fold in (True, False):
+        net = EfficientNetB0(EffNetConfig(image=96, classes=50, fold_excite=fold), device="cuda:0", seed=2)
+        loss = net.train_step(x, lab, lr=None)
+        torch.cuda.synchronize()
+        out.append((float(loss.item()), net.grad.flat.double().cpu().numpy().copy()))
+    assert abs(out[0][0] - out[1][0]) <= 1e-3 * max(1.0, abs(out[1][0]))
+    ga, gb = out[0][1], out[1][1]
+    assert float(np.abs(ga - gb).max()) <= 2e-2 * max(1.0, float(np.abs(gb).max()))
