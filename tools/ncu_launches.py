@@ -34,6 +34,11 @@ def main():
     # last step = launches after the last torch fill (the L2 flush)
     idx = [i for i, d in enumerate(data) if "FillFunctor" in d["Kernel Name"]]
     step = data[idx[-1] + 1:] if idx and not a.per_step else data[-a.per_step:]
+    if not a.per_step:  # several back-to-back replays after the flush: keep the last period
+        names = [d["Kernel Name"] for d in step]
+        per = next(p for p in range(1, len(names) + 1)
+                   if len(names) % p == 0 and names == names[:p] * (len(names) // p))
+        step = step[-per:]
     tot = sum(float(d["Metric Value"]) for d in step)
     print(f"| # | kernel | grid | block | us | share |\n|---|---|---|---|---|---|")
     for i, d in enumerate(step):
