@@ -37,6 +37,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "gemm.h"
 #include "tc_ptx.cuh"
 
 namespace dfx {
@@ -720,6 +721,7 @@ struct AttnBwdParams {
   float ks, sc2, scale;       // keep scale, inv_divisor*log2e, inv_divisor
   __nv_bfloat16* dqkv;        // [T, ld_dqkv]: dQ | dK | dV column blocks
   float* bias_part;           // [B*S/128][3H]: per-strip column sums of dQ | dK | dV (qkv bias gradient)
+  int ds_store;               // dkdv: also store dSᵀ (map_ds) and the strip's dQ column sums (dQ = dS·K GEMM path)
 };
 
 constexpr int CH = 128;  // keys (dq) / queries (dkdv) per chunk
@@ -749,7 +751,8 @@ struct DkvSmem {
   static constexpr int LSE = DS + QT * CH * 2;
   static constexpr int DEL = LSE + kMaxSeq * 4;
   static constexpr int LUT = DEL + kMaxSeq * 4;  // keep nibble -> 4 x {0, 1}
-  static constexpr int BAR = LUT + 16 * 16;
+  static constexpr int CS = LUT + 16 * 16;       // [4][128] per-part Σ_q dS (ds_store)
+  static constexpr int BAR = CS + 4 * QT * 4;
   static constexpr int TOTAL = BAR + 256 + KB;
 };
 static_assert(DkvSmem::TOTAL <= 227 * 1024, "attention dkdv exceeds shared memory");
@@ -1025,7 +1028,7 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
 // dK / dV strip: CTA = (b, h, 128-key block); loops over 128-query chunks.
 __global__ void __launch_bounds__(kAttnThreads, 1)
 attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
-                     const AttnBwdParams p) {
+                     const __grid_constant__ CUtensorMap map_ds, const AttnBwdParams p) {
   // dynamic smem opens the CTA's window (no static smem in this kernel): it is
   // 1024-B aligned, and indexing it directly keeps every access LDS/STS
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1105,6 +1108,11 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
       auto issue_grads = [&](int j) {  // dV += Pdᵀ·dO_j ; dK += dSᵀ·Q_j   (B operands MN-major)
         mbar_wait(bar_pds, j & 1);
         tc_fence_after();
+        if (p.ds_store) {  // dSᵀ tile (two 64-query SW128 halves) -> HBM, the dQ GEMM's A operand
+          tma_store_4d(&map_ds, sbase + DkvSmem::DS, j * CH, bh * S + k0, 0, 0);
+          tma_store_4d(&map_ds, sbase + DkvSmem::DS + 16 * KB, j * CH + 64, bh * S + k0, 0, 0);
+          bulk_commit();
+        }
         const uint32_t stq = sbase + DkvSmem::RING + (j % NST) * DkvSmem::STAGE;
         const uint64_t qmn = make_sdesc(stq, 8 * KB, 1024);
         const uint64_t domn = make_sdesc(stq + CH * 128, 8 * KB, 1024);
@@ -1116,6 +1124,7 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
           tc_mma_cg<1>(tmem + T_DV, pd + 2 * (kc & 3), domn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
           tc_mma_cg<1>(tmem + T_DK, ds + 2 * (kc & 3), qmn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
         }
+        if (p.ds_store) bulk_wait_read<0>();  // the DS tile is overwritten once pdsfree fires
         tc_commit_cg<1>(&empty[j % NST]);
         tc_commit_cg<1>(bar_pdsfree);
       };
@@ -1156,6 +1165,7 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
     mbar_wait(bar_a, 0);  // lse / D rows landed (with K, V)
     // P' = P / divisor: the divisor's log2 folds into the row mask term
     const float mrow = mraw * kLog2e + __log2f(p.scale);
+    float cs = 0.f;  // Σ_q dS[q, key] over this thread's columns (ds_store: the dQ column sums)
     if (sw == 0 && lane == 0) ATRACE(12);
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     for (int j = 0; j < nch; ++j) {
@@ -1175,6 +1185,7 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
       // by ks * divisor); dS = P' * (dPd * keep * ks - D)
       const float2 sc2x2 = make_float2(p.sc2, p.sc2), mrow2 = make_float2(mrow, mrow), ks2 = make_float2(p.ks, p.ks);
       float4 kf;
+      float2 csum = make_float2(0.f, 0.f);
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         const float2 l = reinterpret_cast<const float2*>(lse_s + qc0)[i >> 1];
@@ -1186,9 +1197,11 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
         const float2 pd = __fmul2_rn(P, kk);
         const float2 dpm = __fmul2_rn(make_float2(dp[i], dp[i + 1]), kk);
         const float2 ds = __fmul2_rn(P, __ffma2_rn(dpm, ks2, make_float2(-dd.x, -dd.y)));
+        csum = __fadd2_rn(csum, ds);
         pkp[i >> 1] = pack_bf16x2(pd.x, pd.y);
         pks[i >> 1] = pack_bf16x2(ds.x, ds.y);
       }
+      cs += csum.x + csum.y;
       if (j > 0) mbar_wait(bar_pdsfree, (j - 1) & 1);
       st_row32(sbase + DkvSmem::PD, rl, part * 32, pkp);
       st_row32(sbase + DkvSmem::DS, rl, part * 32, pks);
@@ -1216,6 +1229,32 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
       float* const scr[2] = {lse_s, del_s};
       float* const dst[2] = {bp + p.H, bp + 2 * p.H};
       tile_colsum_128x64<2>(stg, scr, rl, part * 16, g2, st, dst);
+      if (p.ds_store) {
+        // dQ = dS·K comes from the GEMM over the stored dSᵀ; its column sums
+        // over this strip's keys are Σ_k cs[k] K[k][:] with cs[k] = Σ_q dS[q, k]
+        // (the K strip is still staged: SW128 rows of 64 bf16)
+        float* cs_s = reinterpret_cast<float*>(smem + DkvSmem::CS);
+        cs_s[part * QT + rl] = cs;
+        named_bar(1, kSoftWarps * 32);
+        const int d = st & 63, grp = st >> 6;  // 8 groups of 16 keys
+        float acc = 0.f;
+#pragma unroll 4
+        for (int r = grp * 16; r < grp * 16 + 16; ++r) {
+          const float c = cs_s[r] + cs_s[QT + r] + cs_s[2 * QT + r] + cs_s[3 * QT + r];
+          const __nv_bfloat16 kv = *reinterpret_cast<const __nv_bfloat16*>(
+              smem + DkvSmem::K + r * 128 + (((d >> 3) ^ (r & 7)) << 4) + (d & 7) * 2);
+          acc = fmaf(c, __bfloat162float(kv), acc);
+        }
+        float* scr2 = lse_s;  // free after the colsum above
+        scr2[grp * 64 + d] = acc;
+        named_bar(1, kSoftWarps * 32);
+        if (st < 64) {
+          float u = 0.f;
+#pragma unroll
+          for (int g = 0; g < 8; ++g) u += scr2[g * 64 + st];
+          bp[st] = u;
+        }
+      }
     }
   }
   tc_fence_before();
@@ -1223,6 +1262,41 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// D = rowsum(dO ∘ O) for the key-strip backward when no dq strip kernel runs
+// first: four threads per (row, head) slice of 64, a 4-lane shuffle reduction
+__global__ void __launch_bounds__(256) attn_bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
+                                                             const __nv_bfloat16* __restrict__ dout, int64_t ld,
+                                                             int T, int S, int NH, float* __restrict__ delta) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slice = t >> 2, qtr = t & 3;
+  const bool live = slice < T * NH;
+  const int row = live ? slice / NH : 0, h = live ? slice - row * NH : 0;
+  float2 acc = make_float2(0.f, 0.f);
+  if (live) {
+    const uint4* a = reinterpret_cast<const uint4*>(o + (size_t)row * ld + h * DH + qtr * 16);
+    const uint4* g = reinterpret_cast<const uint4*>(dout + (size_t)row * ld + h * DH + qtr * 16);
+    const uint4 va0 = __ldg(a), va1 = __ldg(a + 1), vg0 = __ldg(g), vg1 = __ldg(g + 1);
+    const __nv_bfloat162* x0 = reinterpret_cast<const __nv_bfloat162*>(&va0);
+    const __nv_bfloat162* x1 = reinterpret_cast<const __nv_bfloat162*>(&va1);
+    const __nv_bfloat162* y0 = reinterpret_cast<const __nv_bfloat162*>(&vg0);
+    const __nv_bfloat162* y1 = reinterpret_cast<const __nv_bfloat162*>(&vg1);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      acc = __ffma2_rn(__bfloat1622float2(x0[e]), __bfloat1622float2(y0[e]), acc);
+      acc = __ffma2_rn(__bfloat1622float2(x1[e]), __bfloat1622float2(y1[e]), acc);
+    }
+  }
+  float v = acc.x + acc.y;
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  if (live && qtr == 0) {
+    const int b = row / S, srow = row - b * S;
+    delta[((size_t)b * NH + h) * S + srow] = v;
   }
 }
 
@@ -1294,8 +1368,31 @@ extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
 static size_t attn_delta_bytes(int64_t batch, int64_t heads, int64_t seq) {
   return ((size_t)(batch * heads * seq) * sizeof(float) + 255) & ~(size_t)255;
 }
+static size_t attn_part_bytes(int64_t batch, int64_t heads, int64_t seq) {
+  return ((size_t)(batch * (seq / QT)) * 3 * heads * DH * sizeof(float) + 255) & ~(size_t)255;
+}
+static size_t attn_ds_bytes(int64_t batch, int64_t heads, int64_t seq) {
+  return ((size_t)(batch * heads) * seq * seq * 2 + 255) & ~(size_t)255;
+}
+// dQ[b, h] = dS[b, h] · K[b, h]: A = the stored dSᵀ read MN-major, B = K read MN-major from qkv
+static dfx_gemm_args dq_gemm_args(int64_t batch, int64_t heads, int64_t seq, const void* qkv, int64_t ld_qkv,
+                                  const void* dsT, void* dqkv, int64_t ld_dqkv) {
+  dfx_gemm_args g{};
+  g.in_dtype = DFX_BF16; g.out_dtype = DFX_BF16; g.epilogue = DFX_EPI_NONE;
+  g.m = seq; g.n = DH; g.k = seq; g.batch1 = batch; g.batch2 = heads;
+  g.a = dsT; g.a_stride_m = 1; g.a_stride_k = seq; g.a_stride_b2 = seq * seq; g.a_stride_b1 = heads * seq * seq;
+  g.b = reinterpret_cast<const __nv_bfloat16*>(qkv) + heads * DH;
+  g.b_stride_n = 1; g.b_stride_k = ld_qkv; g.b_stride_b2 = DH; g.b_stride_b1 = seq * ld_qkv;
+  g.d = dqkv; g.d_stride_m = ld_dqkv; g.d_stride_b2 = DH; g.d_stride_b1 = seq * ld_dqkv;
+  g.alpha = 1.f; g.beta = 0.f;
+  return g;
+}
+// delta [B, NH, S] f32 | qkv-bias column partials [B*S/128][3*NH*64] f32 |
+// dSᵀ [B, NH, S(key), S(query)] bf16 | the dQ GEMM's split-K partials (few heads)
 extern "C" size_t dfx_attn_bwd_workspace(int64_t batch, int64_t heads, int64_t seq) {
-  return attn_delta_bytes(batch, heads, seq) + (size_t)(batch * (seq / QT)) * 3 * heads * DH * sizeof(float) + 256;
+  const dfx_gemm_args g = dq_gemm_args(batch, heads, seq, nullptr, 3 * heads * DH, nullptr, nullptr, 3 * heads * DH);
+  return attn_delta_bytes(batch, heads, seq) + attn_part_bytes(batch, heads, seq) + attn_ds_bytes(batch, heads, seq) +
+         gemm_tc_workspace(g) + 256;
 }
 
 extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t head_dim, const void* qkv,
@@ -1343,13 +1440,37 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
     attr = true;
   }
   const int grid = (int)(batch * heads * (seq / QT));
+  static const bool legacy = getenv("DFX_ATTN_BWD_LEGACY") != nullptr;  // A/B: the dq strip kernel for dQ
+  if (!legacy) {
+    // D pre-pass -> key-strip kernel (dK, dV, dSᵀ to HBM, bias sums) -> dQ = dS·K GEMM
+    uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+    __nv_bfloat16* dsT = reinterpret_cast<__nv_bfloat16*>(ws + attn_delta_bytes(batch, heads, seq) +
+                                                          attn_part_bytes(batch, heads, seq));
+    CUtensorMap mds;
+    rc = make_map(&mds, dsT, 2, (uint64_t)seq, (uint64_t)(batch * heads * seq), seq, 1, 0, 1, 0, 64, 128, true);
+    if (rc) return rc;
+    const int nthr = (int)(T * heads * 4);
+    launch_k(attn_bwd_delta_kernel, (nthr + 255) / 256, 256, 0, as_stream(stream), p.ctx, p.dctx, ld_ctx, (int)T,
+             (int)seq, (int)heads, p.delta);
+    DFX_LAUNCH_CHECK("dfx_attn_bwd (delta)");
+    p.ds_store = 1;
+    p.trace = g_attn_trace;
+    launch_k(attn_bwd_dkdv_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, mds, p);
+    DFX_LAUNCH_CHECK("dfx_attn_bwd (dk, dv, dS)");
+    dfx_gemm_args g = dq_gemm_args(batch, heads, seq, qkv, ld_qkv, dsT, dqkv, ld_dqkv);
+    g.workspace = reinterpret_cast<uint8_t*>(dsT) + attn_ds_bytes(batch, heads, seq);
+    g.workspace_bytes = gemm_tc_workspace(g);
+    DFX_REQUIRE(gemm_tc_supported(g), DFX_ERR_UNSUPPORTED, "dfx_attn_bwd: dQ GEMM shape not on the tcgen05 path");
+    return gemm_tc(g, as_stream(stream));
+  }
+  p.ds_store = 0;
   // debug timeline of the dq kernel, or of dkdv with DFX_ATTN_TRACE_DKDV set (tools/attn_trace.py)
   const bool trace_dkdv = getenv("DFX_ATTN_TRACE_DKDV") != nullptr;
   p.trace = trace_dkdv ? nullptr : g_attn_trace;
   launch_k(attn_bwd_dq_kernel, grid, kAttnThreads, DqSmem::TOTAL, as_stream(stream), mqkv, mdo, mo, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dq)");
   p.trace = trace_dkdv ? g_attn_trace : nullptr;
-  launch_k(attn_bwd_dkdv_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, p);
+  launch_k(attn_bwd_dkdv_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, mqkv, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dk, dv)");
   return DFX_OK;
 }

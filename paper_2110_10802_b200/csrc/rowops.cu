@@ -19,6 +19,7 @@
 // float atomics, so results are bitwise reproducible.
 #include "common.cuh"
 #include "lnsmall.h"
+#include "tc_ptx.cuh"
 
 namespace dfx {
 namespace {
@@ -290,6 +291,145 @@ __device__ __forceinline__ float2 bf2(uint32_t w) {
 __device__ __forceinline__ uint32_t pk_bf2(float2 v) {
   __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
   return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// bf16 forward, no activation (the BERT case): every global load of the row
+// (h, residual, keep flags) is issued before any use, and gamma / beta / bias
+// are staged once per CTA in shared memory in the meantime, so a warp pays
+// one DRAM round trip per row instead of one per chunk plus a parameter
+// round trip after the reductions (the generic kernel's branches per chunk
+// keep the compiler from hoisting its loads).  Arithmetic as bdrln_fwd_kernel.
+constexpr int kFwdWarps = 7;  // 224-thread CTAs: 4 per SM at <= 72 registers, 28 row-warps per SM (one wave at C2)
+
+template <int NCH> struct BdrlnRow {
+  uint4 hv[NCH], rv[NCH];
+  uint32_t kw[NCH];  // keep flags of the lane's 8 columns per chunk, as bits
+};
+
+template <int NCH>
+__device__ __forceinline__ BdrlnRow<NCH> bdrln_load_row(int64_t r, int64_t rows, int cols, int lane,
+                                                        const __nv_bfloat16* __restrict__ h,
+                                                        const __nv_bfloat16* __restrict__ res,
+                                                        const uint8_t* __restrict__ keep,
+                                                        const uint8_t* __restrict__ kbits) {
+  BdrlnRow<NCH> d;
+  const size_t base = (size_t)r * cols;
+  const int nvec = cols / 8;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    const bool on = r < rows && vi < nvec;
+    d.hv[c] = on ? __ldg(reinterpret_cast<const uint4*>(h + base + vi * 8)) : make_uint4(0, 0, 0, 0);
+    d.rv[c] = on && res ? __ldg(reinterpret_cast<const uint4*>(res + base + vi * 8)) : make_uint4(0, 0, 0, 0);
+    if (on && keep) {
+      const uint2 k2 = __ldg(reinterpret_cast<const uint2*>(keep + base + vi * 8));
+      d.kw[c] = ((k2.x * 0x01020408u) >> 24) | (((k2.y * 0x01020408u) >> 24) << 4);
+    } else if (on && kbits) {
+      d.kw[c] = __ldg(kbits + ((base + vi * 8) >> 3));
+    } else {
+      d.kw[c] = 0xFFu;
+    }
+  }
+  return d;
+}
+
+template <int NCH>
+__device__ __forceinline__ void bdrln_row(const BdrlnRow<NCH>& d, int64_t row, int cols, int lane, bool masked,
+                                          float ks, float eps, const float* gam, const float* bet, const float* bia,
+                                          __nv_bfloat16* __restrict__ y, __nv_bfloat16* __restrict__ s_out,
+                                          float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  constexpr int V = 8;
+  const int nvec = cols / V;
+  const float inv_n = 1.f / (float)cols;
+  const size_t base = (size_t)row * cols;
+  float x[NCH][V];
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      const float4 b0 = reinterpret_cast<const float4*>(bia + vi * V)[0];
+      const float4 b1 = reinterpret_cast<const float4*>(bia + vi * V)[1];
+      const float pb[V] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      float hf[V], rf[V];
+      unpack4<__nv_bfloat16>(d.hv[c], hf);
+      unpack4<__nv_bfloat16>(d.rv[c], rf);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const float m = masked ? (((d.kw[c] >> i) & 1u) ? ks : 0.f) : 1.f;
+        x[c][i] = (hf[i] + pb[i]) * m + rf[i];
+        sum += x[c][i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[c][i] = 0.f;
+    }
+  }
+  const float mu = warp_sum(sum) * inv_n;
+  float sq = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (lane + c * 32 < nvec) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) { const float dd = x[c][i] - mu; sq += dd * dd; }
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(sq) * inv_n + eps);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int vi = lane + c * 32;
+    if (vi < nvec) {
+      const int col = vi * V;
+      if (s_out) *reinterpret_cast<uint4*>(s_out + base + col) = pack4<__nv_bfloat16>(x[c]);
+      const float4 g0 = reinterpret_cast<const float4*>(gam + col)[0];
+      const float4 g1 = reinterpret_cast<const float4*>(gam + col)[1];
+      const float4 e0 = reinterpret_cast<const float4*>(bet + col)[0];
+      const float4 e1 = reinterpret_cast<const float4*>(bet + col)[1];
+      const float gv[V] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const float bv[V] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+      float yv[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) yv[i] = (x[c][i] - mu) * rstd * gv[i] + bv[i];
+      *reinterpret_cast<uint4*>(y + base + col) = pack4<__nv_bfloat16>(yv);
+    }
+  }
+  if (lane == 0) {
+    if (mean_out) mean_out[row] = mu;
+    if (rstd_out) rstd_out[row] = rstd;
+  }
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(kFwdWarps * 32, 4) bdrln_fwd_bf16_kernel(
+    int64_t rows, int cols, const __nv_bfloat16* __restrict__ h, const float* __restrict__ bias,
+    const uint8_t* __restrict__ keep, const uint8_t* __restrict__ kbits, float ks,
+    const __nv_bfloat16* __restrict__ res, const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+    __nv_bfloat16* __restrict__ y, __nv_bfloat16* __restrict__ s_out, float* __restrict__ mean_out,
+    float* __restrict__ rstd_out) {
+  extern __shared__ float prm[];  // gamma [cols] | beta [cols] | bias [cols]
+  pdl_trigger();
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = (int64_t)blockIdx.x * kFwdWarps + warp;
+  const int64_t stride = (int64_t)gridDim.x * kFwdWarps;
+  // the first row's loads go out before the parameter staging
+  const BdrlnRow<NCH> first = bdrln_load_row<NCH>(row0, rows, cols, lane, h, res, keep, kbits);
+  float* gam = prm;
+  float* bet = prm + cols;
+  float* bia = prm + 2 * cols;
+  for (int i = threadIdx.x; i < cols / 4; i += blockDim.x) {
+    reinterpret_cast<float4*>(gam)[i] = __ldg(reinterpret_cast<const float4*>(gamma) + i);
+    reinterpret_cast<float4*>(bet)[i] = __ldg(reinterpret_cast<const float4*>(beta) + i);
+    reinterpret_cast<float4*>(bia)[i] = bias ? __ldg(reinterpret_cast<const float4*>(bias) + i)
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  const bool masked = keep || kbits;
+  if (row0 < rows) bdrln_row<NCH>(first, row0, cols, lane, masked, ks, eps, gam, bet, bia, y, s_out, mean_out, rstd_out);
+  for (int64_t row = row0 + stride; row < rows; row += stride) {
+    const BdrlnRow<NCH> d = bdrln_load_row<NCH>(row, rows, cols, lane, h, res, keep, kbits);
+    bdrln_row<NCH>(d, row, cols, lane, masked, ks, eps, gam, bet, bia, y, s_out, mean_out, rstd_out);
+  }
 }
 
 template <int NCH>
@@ -850,6 +990,22 @@ int bdrln_fwd_t(int64_t rows, int64_t cols, const void* h, const float* bias, co
   const int nch = pick_nch((int)(cols / V));
   const int grid = grid_for(rows, kWarps, 4 * num_sms());
   if (rows == 0) return DFX_OK;
+  if constexpr (sizeof(T) == 2) {
+    // bf16, no activation, <= 768 columns with 16-byte aligned parameters: loads-first kernel
+    const bool al = ((reinterpret_cast<uintptr_t>(gamma) | reinterpret_cast<uintptr_t>(beta) |
+                      reinterpret_cast<uintptr_t>(bias)) & 15) == 0;
+    if (!act && nch <= 3 && cols % 4 == 0 && al && (!keep || (reinterpret_cast<uintptr_t>(keep) & 7) == 0)) {
+      const size_t sm = (size_t)3 * cols * sizeof(float);
+#define LF(N)                                                                                      \
+  if (nch == N)                                                                                    \
+    launch_k(bdrln_fwd_bf16_kernel<N>, grid_for(rows, kFwdWarps, 4 * num_sms()), kFwdWarps * 32, sm, st, rows, (int)cols, (const __nv_bfloat16*)h, bias, keep, \
+             kbits, ks, (const __nv_bfloat16*)res, gamma, beta, eps, (__nv_bfloat16*)y, (__nv_bfloat16*)s_out, mean, rstd);
+      LF(1) LF(2) LF(3)
+#undef LF
+      DFX_LAUNCH_CHECK("dfx_bdrln_fwd");
+      return DFX_OK;
+    }
+  }
 #define L(N)                                                                                        \
   if (nch == N) {                                                                                   \
     if (act)                                                                                        \
