@@ -337,10 +337,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // (mbconv.cu), so y is bitwise the unfused path's.
     const int tt = threadIdx.x - (2 + kEpiWarps) * 32;
     const int ch = tt & 7, r0 = tt >> 3;
+    const int hw = (int)p.x_hw;  // rows per image (>= 16: one carry per 16-row step below)
     uint32_t it = 0;
     for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
       const TileIdx ti = tile_of(t, p);
       const int64_t m0 = (int64_t)ti.mb * BM;
+      // image of this thread's first row, then carried across its 16-row steps (no divisions per chunk)
+      const int first = (int)(m0 + r0);
+      const int img0 = first / hw, rem0 = first - img0 * hw;
       for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
@@ -354,15 +358,20 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
         mbar_wait(&full[s], ph);
         const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
-#pragma unroll 2
+        int img = img0, rem = rem0;
+#pragma unroll 4
         for (int i = 0; i < 8; ++i) {
           const int r = r0 + 16 * i;
           const int64_t gm = m0 + r;
+          if (i > 0) {
+            rem += 16;
+            if (rem >= hw) { rem -= hw; ++img; }
+          }
           const uint32_t addr = sa + r * 128 + ((ch ^ (r & 7)) << 4);
           uint4 out = make_uint4(0u, 0u, 0u, 0u);
           if (kin && gm < p.m) {
             const uint4 zv = lds128(addr);
-            const float* gp = p.x_gate + (gm / p.x_hw) * p.k + k;
+            const float* gp = p.x_gate + (int64_t)img * p.k + k;
             const float4 g0 = __ldg(reinterpret_cast<const float4*>(gp));
             const float4 g1 = __ldg(reinterpret_cast<const float4*>(gp) + 1);
             const float se[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
@@ -810,6 +819,7 @@ int gemm_excite(int64_t m, int64_t k, int64_t n, const void* z, int64_t hw, cons
                 cudaStream_t st) {
   DFX_REQUIRE(m > 0 && n > 0 && k > 0 && hw > 0, DFX_ERR_SHAPE, "dfx_gemm_excite: empty extent");
   DFX_REQUIRE(k % 8 == 0 && n % 8 == 0, DFX_ERR_SHAPE, "dfx_gemm_excite: k and n must be multiples of 8");
+  DFX_REQUIRE(hw >= 16 && m < (1ll << 31), DFX_ERR_UNSUPPORTED, "dfx_gemm_excite: needs >= 16 rows per image");
   DFX_REQUIRE(z && w && d && mean && rstd && gamma && beta && gate, DFX_ERR_SHAPE, "dfx_gemm_excite: null operand");
   DFX_REQUIRE(aligned16(z) && aligned16(w) && aligned16(d) && aligned16(gate) && (!y_out || aligned16(y_out)),
               DFX_ERR_ALIGN, "dfx_gemm_excite: operands must be 16-byte aligned");

@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import contextlib
 import ctypes
+import os
 from dataclasses import dataclass
 
 import torch
@@ -68,7 +69,7 @@ class EffNetConfig:
     dtype: torch.dtype = torch.bfloat16
     # bf16: the SE excite is folded into the project 1x1 GEMM (kernels.gemm_excite:
     # y = swish(BN(z)) * s formed from z inside the tcgen05 GEMM, SURVEY §8f row 2)
-    fold_excite: bool = True
+    fold_excite: bool = os.environ.get("DFX_EXCITE_FOLD", "1") != "0"
 
     def blocks(self):
         """[(expand, k, stride, cin, cexp, cout, se)] for the 16 blocks."""
@@ -175,6 +176,12 @@ class _Block:
     def w(self, name):
         return self.Wl[self.p + name] if self.Wl is not None else self.net.master[self.p + name]
 
+    def _out_hw(self, x):
+        """Output pixels per image of the depthwise conv (the fold needs >= 16)."""
+        _, H, W, _ = x.shape
+        p = self.k // 2
+        return ((H + 2 * p - self.k) // self.s + 1) * ((W + 2 * p - self.k) // self.s + 1)
+
     def forward(self, x):
         N, H, W, _ = x.shape
         self.x = x
@@ -186,7 +193,7 @@ class _Block:
         else:
             a = x
         self.a = a
-        if self.net.cfg.fold_excite and x.dtype == torch.bfloat16:
+        if self.net.cfg.fold_excite and x.dtype == torch.bfloat16 and self._out_hw(x) >= 16:
             # excite + project as one GEMM over z; y is still written for the weight gradient
             self.mb.forward(a, excite=False)
             mbb = self.mb.buffers(a.shape)

@@ -89,10 +89,10 @@ def test_effnet_fold_equals_unfolded():
 
     g = torch.Generator().manual_seed(3)
     x = torch.randn(4, 96, 96, 3, generator=g).bfloat16().cuda()
-    lab = torch.randint(0, 50, (4,), generator=g, dtype=torch.int32).cuda()
+    lab = torch.randint(0, 56, (4,), generator=g, dtype=torch.int32).cuda()
     out = []
     for fold in (True, False):
-        net = EfficientNetB0(EffNetConfig(image=96, classes=50, fold_excite=fold), device="cuda:0", seed=2)
+        net = EfficientNetB0(EffNetConfig(image=96, classes=56, fold_excite=fold), device="cuda:0", seed=2)
         loss = net.train_step(x, lab, lr=None)
         torch.cuda.synchronize()
         out.append((float(loss.item()), net.grad.flat.double().cpu().numpy().copy()))
