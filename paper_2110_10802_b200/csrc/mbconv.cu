@@ -502,19 +502,28 @@ __global__ void __launch_bounds__(1024) se_bwd_kernel(Geo g, int SE, const float
     de_out[(size_t)n * g.C + c] = d;
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int j = warp; j < SE; j += nw) {
+  // dr[j] = Σ_c We[c][j] de[c]: thread (j, part) walks c = part, part + P, ...
+  // so consecutive threads read consecutive We entries (We is [C][SE]); the P
+  // partial sums of each j are then added in part order (deterministic)
+  const int P = (int)blockDim.x / SE;  // SE <= blockDim.x (host check)
+  float* red = dr + SE;                 // [P][SE] <= 1024 floats after dr
+  __syncthreads();
+  if ((int)threadIdx.x < P * SE) {
+    const int j = (int)threadIdx.x % SE, part = (int)threadIdx.x / SE;
     float acc = 0.f;
-#pragma unroll 8
-    for (int c = lane; c < g.C; c += 32) acc += we[(size_t)c * SE + j] * de[c];
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      const float rv = r[(size_t)n * SE + j];
-      const float sg = sigmoidf_(rv);
-      const float v = acc * (sg + rv * sg * (1.f - sg));
-      dr[j] = v;
-      dr_out[(size_t)n * SE + j] = v;
-    }
+#pragma unroll 4
+    for (int c = part; c < g.C; c += P) acc = fmaf(we[(size_t)c * SE + j], de[c], acc);
+    red[part * SE + j] = acc;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < SE; j += blockDim.x) {
+    float acc = 0.f;
+    for (int q = 0; q < P; ++q) acc += red[q * SE + j];
+    const float rv = r[(size_t)n * SE + j];
+    const float sg = sigmoidf_(rv);
+    const float v = acc * (sg + rv * sg * (1.f - sg));
+    dr[j] = v;
+    dr_out[(size_t)n * SE + j] = v;
   }
   __syncthreads();
   const float inv_hw = 1.f / (float)(g.Ho * g.Wo);
@@ -531,9 +540,12 @@ __global__ void __launch_bounds__(1024) se_bwd_kernel(Geo g, int SE, const float
 }
 
 // ---------------------------------------------------------------- B3
-// one WARP per output scalar: lanes stride the samples (n = lane, lane+32,
-// ...), then a fixed-order warp sum — deterministic, and every sample's load
-// is in flight at once instead of an N-long serial chain per thread.
+// Sample reductions of the SE-MLP and BN parameter gradients.  A block owns 32
+// consecutive outputs (lanes; channel-fastest flat index, so loads of one
+// sample row are coalesced and the per-(n, j) factor is a broadcast) and its 8
+// warps take samples n = w, w + 8, ...; the 8 partials of each output are then
+// added in warp order (deterministic).  Outputs: dWe [C][SE] (written through
+// the transposed index), dWr [SE][C], dbe [C], dbr [SE], bnsum [2][C].
 __global__ void __launch_bounds__(256) se_bwd_reduce_kernel(int N, int C, int SE, const float* __restrict__ de,
                                                             const float* __restrict__ dr, const float* __restrict__ r,
                                                             const float* __restrict__ pooled,
@@ -542,39 +554,53 @@ __global__ void __launch_bounds__(256) se_bwd_reduce_kernel(int N, int C, int SE
                                                             float* __restrict__ dbr, float* __restrict__ bnsum /*[2][C]*/) {
   pdl_trigger();
   pdl_wait();
-  const int lane = threadIdx.x & 31;
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t total = (int64_t)C * SE * 2 + C + SE + 2 * C;
-  for (int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; idx < total;
-       idx += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t n_we = (int64_t)C * SE, n_wr = (int64_t)SE * C;
+  const int64_t n_w = (int64_t)C * SE;
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < total; base += (int64_t)gridDim.x * 32) {
+    int64_t k = base + lane;
     float acc = 0.f;
-    float* out;
-    int64_t k = idx;
-    if (k < n_we) {
-      const int c = (int)(k / SE), j = (int)(k % SE);
-      for (int n = lane; n < N; n += 32) {
-        const float rv = r[(size_t)n * SE + j];
-        acc += de[(size_t)n * C + c] * rv * sigmoidf_(rv);
+    if (k < total) {
+      if (k < n_w) {  // dWe[c][j] = Σ_n de[n][c] swish(r[n][j]),  k = j * C + c
+        const int j = (int)(k / C), c = (int)(k % C);
+        for (int n = w; n < N; n += 8) {
+          const float rv = __ldg(r + (size_t)n * SE + j);
+          acc = fmaf(__ldg(de + (size_t)n * C + c), rv * sigmoidf_(rv), acc);
+        }
+      } else if ((k -= n_w) < n_w) {  // dWr[j][c] = Σ_n dr[n][j] pooled[n][c],  k = j * C + c
+        const int j = (int)(k / C), c = (int)(k % C);
+        for (int n = w; n < N; n += 8) acc = fmaf(__ldg(dr + (size_t)n * SE + j), __ldg(pooled + (size_t)n * C + c), acc);
+      } else if ((k -= n_w) < C) {
+        for (int n = w; n < N; n += 8) acc += __ldg(de + (size_t)n * C + k);
+      } else if ((k -= C) < SE) {
+        for (int n = w; n < N; n += 8) acc += __ldg(dr + (size_t)n * SE + k);
+      } else {
+        k -= SE;
+        const int q = (int)(k / C), c = (int)(k % C);
+        for (int n = w; n < N; n += 8) acc += __ldg(nsum + ((size_t)n * 2 + q) * C + c);
       }
-      out = dwe + k;
-    } else if ((k -= n_we) < C) {
-      for (int n = lane; n < N; n += 32) acc += de[(size_t)n * C + k];
-      out = dbe + k;
-    } else if ((k -= C) < n_wr) {
-      const int j = (int)(k / C), c = (int)(k % C);
-      for (int n = lane; n < N; n += 32) acc += dr[(size_t)n * SE + j] * pooled[(size_t)n * C + c];
-      out = dwr + k;
-    } else if ((k -= n_wr) < SE) {
-      for (int n = lane; n < N; n += 32) acc += dr[(size_t)n * SE + k];
-      out = dbr + k;
-    } else {
-      k -= SE;
-      const int q = (int)(k / C), c = (int)(k % C);
-      for (int n = lane; n < N; n += 32) acc += nsum[((size_t)n * 2 + q) * C + c];
-      out = bnsum + k;
     }
-    acc = warp_sum(acc);
-    if (lane == 0) *out = acc;
+    red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && base + lane < total) {
+      float t = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t += red[q][lane];
+      int64_t kk = base + lane;
+      if (kk < n_w) {
+        dwe[(size_t)(kk % C) * SE + kk / C] = t;
+      } else if ((kk -= n_w) < n_w) {
+        dwr[kk] = t;
+      } else if ((kk -= n_w) < C) {
+        dbe[kk] = t;
+      } else if ((kk -= C) < SE) {
+        dbr[kk] = t;
+      } else {
+        bnsum[kk - SE] = t;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -944,11 +970,14 @@ int dfx_mbconv_bwd_reduce(int dtype, int64_t N, int64_t H, int64_t W, int64_t C,
     return fail(DFX_ERR_DTYPE, "dfx_mbconv_bwd_reduce: dtype must be f32 or bf16");
   }
   DFX_LAUNCH_CHECK("dfx_mbconv_bwd_reduce reduce");
-  launch_k(se_bwd_kernel, g.N, 1024, (size_t)(6 * g.C + SE) * sizeof(float), st, g, (int)SE, bwd_part, s, r, w_r, w_e,
+  DFX_REQUIRE(SE <= 1024, DFX_ERR_UNSUPPORTED, "dfx_mbconv_bwd_reduce: squeeze width must be <= 1024");
+  const size_t sm_se = (size_t)(6 * g.C + SE + 1024) * sizeof(float);
+  if (sm_se > 48 * 1024) cudaFuncSetAttribute(se_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_se);
+  launch_k(se_bwd_kernel, g.N, 1024, sm_se, st, g, (int)SE, bwd_part, s, r, w_r, w_e,
                                                                                 de, dr, dpool, nsum);
   DFX_LAUNCH_CHECK("dfx_mbconv_bwd_reduce se_bwd");
   const int64_t total = (int64_t)C * SE * 2 + C + SE + 2 * C;
-  const int grid5 = (int)std::min<int64_t>((total * 32 + 255) / 256, (int64_t)num_sms() * 16);
+  const int grid5 = (int)std::min<int64_t>((total + 31) / 32, (int64_t)num_sms() * 16);
   launch_k(se_bwd_reduce_kernel, grid5, 256, 0, st, g.N, g.C, (int)SE, de, dr, r, pooled, nsum, dw_e, db_e,
            dw_r, db_r, bnsum);
   DFX_LAUNCH_CHECK("dfx_mbconv_bwd_reduce se_reduce");
