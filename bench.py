@@ -683,12 +683,15 @@ def run_ours(args):
     # DRAM bytes per launch of the dominant kernel from the committed ncu --set
     # full capture (profiles/r01_traffic.json, tools/gpu_profile.sh); null if absent
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom["kernel"])
+    tsrc = None
+    for tname in ("r02_traffic.json", "r01_traffic.json"):  # newest capture first
+        tpath = os.path.join(ROOT, "profiles", tname)
+        if os.path.exists(tpath) and dom["kernel"] in json.load(open(tpath)):
+            traffic, tsrc = json.load(open(tpath))[dom["kernel"]], f"profiles/{tname} (ncu DRAM bytes)"
+            break
     roofline = {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"],
                 "peak": pk["hbm_gbs"] if dom["bound"] == "hbm" else pk["tflops"], "unit": dom["unit"],
-                "frac": dom["frac"], "traffic": traffic, "traffic_source": "profiles/r01_traffic.json (ncu --set full)",
+                "frac": dom["frac"], "traffic": traffic, "traffic_source": tsrc,
                 "peak_source": pk["source"] + (", tensor " + pk["tensor_peak"] if dom["bound"] == "tensor" else "")}
     gemm_us = sum(r["us_per_call"] * r["calls_per_step"] for r in rows if r["bound"] == "tensor")
     flops = layer.step_flops(B, S)

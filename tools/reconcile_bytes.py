@@ -76,6 +76,8 @@ def main():
     ap.add_argument("--block", type=int, default=None, help="index of the flush-delimited block to use (default: "
                     "the last block of the most common length = one timed replay of the step)")
     ap.add_argument("--slack", type=float, default=1.5)
+    ap.add_argument("--traffic-out", default=None,
+                    help="write DRAM bytes per launch of the attention call sites (bench.py roofline 'traffic')")
     a = ap.parse_args()
     blocks = [b for b in steps(load(a.csv)) if len(b) > 20]
     if a.block is None:
@@ -104,6 +106,20 @@ def main():
         print(f"| {i} | `{nm}` | {d['grid']} | {d.get('dram__bytes_read.sum', 0) / 1e6:.2f} | "
               f"{d.get('dram__bytes_write.sum', 0) / 1e6:.2f} | {d.get('gpu__time_duration.sum', 0) / 1e3:.1f} |")
     meas = rd + wr
+    if a.traffic_out:
+        def dram(d):
+            return d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+        tr = {}
+        for i, d in enumerate(step):
+            if "attn_fwd" in d["name"]:
+                tr["fwd.attention"] = tr.get("fwd.attention", 0.0) + dram(d)
+            elif "attn_bwd" in d["name"]:
+                tr["bwd.attention"] = tr.get("bwd.attention", 0.0) + dram(d)
+                # the dQ GEMM over the stored dSᵀ follows the key-strip kernel in the same call
+                if "dkdv" in d["name"] and i + 1 < len(step) and "tc_gemm_kernel<64" in step[i + 1]["name"]:
+                    tr["bwd.attention"] += dram(step[i + 1])
+        tr["source"] = "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (tools/reconcile_bytes.py)"
+        json.dump(tr, open(a.traffic_out, "w"), indent=1)
     print(f"\n| quantity | bytes per step | vs schedule |\n|---|---|---|")
     print(f"| measured (ncu DRAM read + write, {len(step)} launches, {us:.1f} us serialised) | {meas / 1e6:.1f} MB | "
           f"{meas / sched:.3f} |")
