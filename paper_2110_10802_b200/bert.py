@@ -607,9 +607,10 @@ def fused_step_bytes(c: BertLayerConfig, B: int, S: int) -> int:
     kb = T * H // 8 if fused and H % 32 == 0 else T * H  # BDRLN keep flags (packed or u8)
     w = lambda n, k: n * k * e  # noqa: E731  (bf16 weight operand)
     g32 = lambda n, k: n * k * 4  # noqa: E731  (f32 weight gradient)
-    # dq strip kernel: Q, K, V, O, dO, lse, row keep bits -> dQ, D; dK/dV strip kernel: Q, K, V, dO, lse,
-    # D, column keep bits -> dK, dV
-    attn_bwd = (t3 + 2 * th + lse + bits + t3 // 3 + lse) + (t3 + th + 2 * lse + bits + 2 * t3 // 3)
+    # D pre-pass: O, dO -> D; key-strip kernel: Q, K, V, dO, lse, D, column keep bits -> dK, dV, dSᵀ;
+    # dQ GEMM: dSᵀ, K -> dQ
+    ds = B * NH * S * S * e
+    attn_bwd = (2 * th + lse) + (t3 + th + 2 * lse + bits + 2 * t3 // 3 + ds) + (ds + t3 // 3 + t3 // 3)
     fwd = (th + w(3 * H, H) + t3) + (t3 + bits + th + bits + lse) + (th + w(H, H) + th) \
         + (2 * th + kb + 2 * th) + (th + w(F, H) + 2 * tf) + (tf + w(H, F) + th) + (2 * th + kb + 2 * th)
     bwd = (2 * th + kb + 2 * th) + (th + w(H, F) + tf + tf) + (th + tf + g32(H, F)) + tf \

@@ -36,9 +36,9 @@ def main():
     step = data[idx[-1] + 1:] if idx and not a.per_step else data[-a.per_step:]
     if not a.per_step:  # several back-to-back replays after the flush: keep the last period
         names = [d["Kernel Name"] for d in step]
-        per = next(p for p in range(1, len(names) + 1)
-                   if len(names) % p == 0 and names == names[:p] * (len(names) // p))
-        step = step[-per:]
+        per = next(p for p in range(1, len(names) + 1) if all(names[i] == names[i % p] for i in range(len(names))))
+        k = len(names) // per
+        step = step[(k - 1) * per:k * per]
     tot = sum(float(d["Metric Value"]) for d in step)
     print(f"| # | kernel | grid | block | us | share |\n|---|---|---|---|---|---|")
     for i, d in enumerate(step):

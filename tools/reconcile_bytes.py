@@ -86,9 +86,10 @@ def main():
         # the launch-name sequence, taken from the last block
         blk = blocks[-1]
         names = [d["name"] for d in blk]
-        per = next(p for p in range(1, len(names) + 1)
-                   if len(names) % p == 0 and names == names[:p] * (len(names) // p))
-        step = blk[-per:]
+        # smallest period (the capture may end mid-step: a truncated last repeat is allowed)
+        per = next(p for p in range(1, len(names) + 1) if all(names[i] == names[i % p] for i in range(len(names))))
+        k = len(names) // per
+        step = blk[(k - 1) * per:k * per]
     else:
         step = blocks[a.block]
     rd = sum(d.get("dram__bytes_read.sum", 0.0) for d in step)
