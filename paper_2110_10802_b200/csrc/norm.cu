@@ -390,8 +390,11 @@ int check_bn(int dtype, int64_t rows, int64_t C, const char* op) {
   } while (0)
 
 // elementwise passes: >= 8 rows per thread lane, at most 8 blocks per SM
-void stream_blocks(int64_t rows, int PY, int64_t* rpb, int* nb) {
+// (rounded to whole waves of the kernel's resident CTAs when there is enough work)
+void stream_blocks(int64_t rows, int PY, int64_t* rpb, int* nb, int resident = 8, int nch = 1) {
   int64_t b = std::min<int64_t>((int64_t)num_sms() * 8, (rows + 8 * PY - 1) / (8 * PY));
+  const int64_t wave = std::max<int64_t>(1, (int64_t)resident * num_sms() / std::max(nch, 1));
+  if (b > wave) b = (b + wave - 1) / wave * wave;  // whole waves
   if (b < 1) b = 1;
   *rpb = (rows + b - 1) / b;
   *nb = (int)((rows + *rpb - 1) / *rpb);
@@ -409,11 +412,22 @@ Lanes lanes_for(int64_t C, int V) {
   return Lanes{nch, cvc, kThreads / cvc};
 }
 
-void blocks_for(int64_t rows, int64_t* rpb, int* nb) {
-  int64_t b = std::min<int64_t>(kMaxBlocks, (rows + 63) / 64);
+// `resident`: CTAs of the launched kernel that fit one SM at once (its
+// register / shared-memory occupancy); the row blocks x channel chunks then
+// fill exactly one wave (a 4-per-SM grid of an 80-register kernel that only
+// fits 3 per SM ran a 1/3-full second wave)
+void blocks_for(int64_t rows, int64_t* rpb, int* nb, int resident = 4, int nch = 1) {
+  const int64_t wave = std::max<int64_t>(1, (int64_t)resident * num_sms() / std::max(nch, 1));
+  int64_t b = std::min<int64_t>(std::min<int64_t>(kMaxBlocks, wave), (rows + 63) / 64);
   if (b < 1) b = 1;
   *rpb = (rows + b - 1) / b;
   *nb = (int)((rows + *rpb - 1) / *rpb);
+}
+
+template <typename K> int resident_ctas(K kern, int threads, size_t smem) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  return occ;
 }
 
 }  // namespace
@@ -434,9 +448,8 @@ int dfx_batchnorm_stats(int dtype, int64_t rows, int64_t C, const void* x, float
   DFX_REQUIRE(x && local && workspace, DFX_ERR_SHAPE, "dfx_batchnorm_stats: null pointer");
   DFX_REQUIRE(ws_bytes >= dfx_batchnorm_workspace(rows, C), DFX_ERR_WORKSPACE, "dfx_batchnorm_stats: workspace too small");
   cudaStream_t st = as_stream(stream);
-  int64_t rpb;
-  int nb;
-  blocks_for(rows, &rpb, &nb);
+  int64_t rpb = 0;
+  int nb = 0;
   const int V = vec_width(dtype, C);
   const Lanes ln = lanes_for(C, V);
   const int PY = ln.py;
@@ -445,6 +458,7 @@ int dfx_batchnorm_stats(int dtype, int64_t rows, int64_t C, const void* x, float
   {                                                                                                       \
     auto k = bn_stats_kernel<TT, VV>;                                                                     \
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);   \
+    blocks_for(rows, &rpb, &nb, resident_ctas(k, ln.cvc * PY, sm), ln.nch);                               \
     launch_k(k, dim3(nb, ln.nch), ln.cvc * PY, sm, st, rows, (int)C, rpb, (const TT*)x, (float*)workspace);     \
   }
   BN_DISPATCH(S, 0);
@@ -463,10 +477,9 @@ int dfx_batchnorm_act_apply(int dtype, int64_t rows, int64_t C, const void* x, c
   cudaStream_t st = as_stream(stream);
   const int V = vec_width(dtype, C);
   const Lanes ln = lanes_for(C, V);
-  int64_t rpb;
-  int nb;
-  stream_blocks(rows, ln.py * ln.nch, &rpb, &nb);
-#define A(TT, VV, ACT) { launch_k(bn_apply_kernel<TT, VV, ACT>, dim3(nb, ln.nch), ln.cvc * ln.py, 0, st, rows, (int)C, rpb, (const TT*)x, mean, rstd, gamma, beta, (TT*)y); }
+  int64_t rpb = 0;
+  int nb = 0;
+#define A(TT, VV, ACT) { stream_blocks(rows, ln.py * ln.nch, &rpb, &nb, resident_ctas(bn_apply_kernel<TT, VV, ACT>, ln.cvc * ln.py, 0), ln.nch); launch_k(bn_apply_kernel<TT, VV, ACT>, dim3(nb, ln.nch), ln.cvc * ln.py, 0, st, rows, (int)C, rpb, (const TT*)x, mean, rstd, gamma, beta, (TT*)y); }
   BN_DISPATCH(A, act);
 #undef A
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_apply");
@@ -482,9 +495,8 @@ int dfx_batchnorm_act_bwd_reduce(int dtype, int64_t rows, int64_t C, const void*
   DFX_REQUIRE(ws_bytes >= dfx_batchnorm_workspace(rows, C), DFX_ERR_WORKSPACE,
               "dfx_batchnorm_act_bwd_reduce: workspace too small");
   cudaStream_t st = as_stream(stream);
-  int64_t rpb;
-  int nb;
-  blocks_for(rows, &rpb, &nb);
+  int64_t rpb = 0;
+  int nb = 0;
   const int V = vec_width(dtype, C);
   const Lanes ln = lanes_for(C, V);
   const int PY = ln.py;
@@ -493,6 +505,7 @@ int dfx_batchnorm_act_bwd_reduce(int dtype, int64_t rows, int64_t C, const void*
   {                                                                                                         \
     auto k = bn_bwd_reduce_kernel<TT, VV, ACT>;                                                             \
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
+    blocks_for(rows, &rpb, &nb, resident_ctas(k, ln.cvc * PY, sm), ln.nch);                                 \
     launch_k(k, dim3(nb, ln.nch), ln.cvc * PY, sm, st, rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, \
                                (float*)workspace);                                                          \
   }
@@ -514,12 +527,11 @@ int dfx_batchnorm_act_bwd_dx(int dtype, int64_t rows, int64_t C, const void* dy,
   cudaStream_t st = as_stream(stream);
   const int V = vec_width(dtype, C);
   const Lanes ln = lanes_for(C, V);
-  int64_t rpb;
-  int nb;
-  stream_blocks(rows, ln.py * ln.nch, &rpb, &nb);
+  int64_t rpb = 0;
+  int nb = 0;
   const float ic = count > 0 ? (float)(1.0 / count) : -1.f;  // -1: per-channel count from bnsum[2]
 #define D(TT, VV, ACT) \
-  { launch_k(bn_bwd_dx_kernel<TT, VV, ACT>, dim3(nb, ln.nch), ln.cvc * ln.py, 0, st, rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, bnsum, ic, (TT*)dx); }
+  { stream_blocks(rows, ln.py * ln.nch, &rpb, &nb, resident_ctas(bn_bwd_dx_kernel<TT, VV, ACT>, ln.cvc * ln.py, 0), ln.nch); launch_k(bn_bwd_dx_kernel<TT, VV, ACT>, dim3(nb, ln.nch), ln.cvc * ln.py, 0, st, rows, (int)C, rpb, (const TT*)dy, (const TT*)x, mean, rstd, gamma, beta, bnsum, ic, (TT*)dx); }
   BN_DISPATCH(D, act);
 #undef D
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_dx");
