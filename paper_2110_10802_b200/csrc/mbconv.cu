@@ -783,8 +783,28 @@ int make_geo(int64_t N, int64_t H, int64_t W, int64_t C, int stride, int ks, con
   g->Ho = (int)((H + pads[0] + pads[2] - ks) / stride + 1);
   g->Wo = (int)((W + pads[1] + pads[3] - ks) / stride + 1);
   DFX_REQUIRE(g->Ho > 0 && g->Wo > 0, DFX_ERR_SHAPE, std::string(op) + ": output would be empty");
-  g->tile_rows = std::max(1, 2048 / g->Wo);
-  if (g->tile_rows > g->Ho) g->tile_rows = g->Ho;
+  // rows per pixel tile of the stream kernels (pool / excite / bwd_reduce,
+  // grid = images x tiles x channel chunks): fewest (whole waves x rows per
+  // tile) at the 2-CTA/SM residency of bwd_reduce (128 registers), so the
+  // last wave is not a sliver (C3: 13-row tiles, 864 CTAs = 2.9 waves, instead
+  // of 18-row tiles, 672 CTAs = 2.3 waves)
+  {
+    const int cvt = (int)C / vec;
+    const int nch = cvt > 64 ? (cvt + 63) / 64 : 1;
+    const long slots = 2L * num_sms();
+    const int rmax = std::max(1, std::min(g->Ho, 4096 / g->Wo));
+    long best = -1;
+    int bestR = std::min(g->Ho, std::max(1, 2048 / g->Wo));
+    for (int R = rmax; R >= 1; --R) {
+      const long ctas = (long)N * ((g->Ho + R - 1) / R) * nch;
+      const long cost = (ctas + slots - 1) / slots * (long)(R * g->Wo + 64);  // + per-tile fixed cost
+      if (best < 0 || cost < best) {
+        best = cost;
+        bestR = R;
+      }
+    }
+    g->tile_rows = bestR;
+  }
   g->tiles_per_img = (g->Ho + g->tile_rows - 1) / g->tile_rows;
   return DFX_OK;
 }

@@ -2,7 +2,8 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
-timeout 900 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_norms.py tests/test_gpu_effnet.py tests/test_gpu_syncbn.py tests/test_gpu_library_eval.py > gpurun_out/round_g_tests.log 2>&1
+timeout 900 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_norms.py tests/test_gpu_mbconv.py tests/test_gpu_excite_fold.py tests/test_gpu_effnet.py tests/test_gpu_syncbn.py tests/test_gpu_library_eval.py > gpurun_out/round_g_tests.log 2>&1
 echo "tests rc=$?"; tail -5 gpurun_out/round_g_tests.log
 timeout 300 python tools/effnet_profile.py > gpurun_out/effnet_profile.txt 2>&1; head -3 gpurun_out/effnet_profile.txt; sed -n '/by kernel type/,$p' gpurun_out/effnet_profile.txt | head -16
 grep -E "dwconv_bwd|dwconv_stats" gpurun_out/effnet_profile.txt | head -34
+timeout 300 python tools/mbconv_time.py 2>&1 | tail -12
