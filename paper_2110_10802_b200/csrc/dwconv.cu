@@ -645,13 +645,20 @@ struct Plan {
 
 size_t rnd128(size_t b) { return (b + 127) & ~size_t(127); }
 
-int pick_cb(int C, int V, int esz) {
-  for (int d = std::min(C, 128); d >= V; --d)
+int pick_cb(int C, int V, int esz, int cap = 128) {
+  for (int d = std::min(C, cap); d >= V; --d)
     if (C % d == 0 && d % V == 0 && (d * esz) % 16 == 0) return d;
   return 0;
 }
 
-// in grid (Hi, Wi) -> out grid (Ho, Wo) with (pt, pl): the correlation this launch computes
+bool make_plan_cb(int N, int Ho, int Wo, int C, int ks, int s, int pt, int pl, int esz, int mode, int Cb,
+                  Plan* pl_out, long* cost_out);
+
+// in grid (Hi, Wi) -> out grid (Ho, Wo) with (pt, pl): the correlation this launch computes.
+// The channel chunk Cb is chosen by the cost model too: narrow maps (EfficientNet's
+// 14x14 / 7x7 stages) want wide chunks and whole-row column segments (a 2-column
+// segment of a 7-wide row loads a 6-column window: 3x halo), wide maps want
+// narrow chunks and many CTAs.
 bool make_plan(int N, int Hi, int Wi, int Ho, int Wo, int C, int ks, int s, int pt, int pl, int esz, int mode,
                Plan* pl_out) {
   (void)Hi;
@@ -660,7 +667,26 @@ bool make_plan(int N, int Hi, int Wi, int Ho, int Wo, int C, int ks, int s, int 
   if (s != 1 && s != 2) return false;
   if ((C * esz) % 16 != 0) return false;
   const int V = ks == 3 ? 4 : 2;
-  const int Cb = pick_cb(C, V, esz);
+  bool found = false;
+  long best = 0;
+  for (int cap : {128, 192, 256}) {  // a TMA box dimension is at most 256 elements
+    const int cb = pick_cb(C, V, esz, cap);
+    if (!cb || (cap > 128 && cb <= 128)) continue;  // no new chunk width at this cap
+    Plan cand;
+    long cost = 0;
+    if (!make_plan_cb(N, Ho, Wo, C, ks, s, pt, pl, esz, mode, cb, &cand, &cost)) continue;
+    if (!found || cost < best) {
+      best = cost;
+      *pl_out = cand;
+      found = true;
+    }
+  }
+  return found;
+}
+
+bool make_plan_cb(int N, int Ho, int Wo, int C, int ks, int s, int pt, int pl, int esz, int mode, int Cb,
+                  Plan* pl_out, long* cost_out) {
+  const int V = ks == 3 ? 4 : 2;
   if (!Cb) return false;
   const int CVn = Cb / V;
   if (CVn > kMaxThreads) return false;
@@ -727,6 +753,9 @@ bool make_plan(int N, int Hi, int Wi, int Ho, int Wo, int C, int ks, int s, int 
   pl_out->threads = CVn * nseg;
   pl_out->grid = N * p.nbands * nwt * p.ncb;
   pl_out->smem = smem_of(Wt, K);
+  // per-thread work of one output row ~ the window columns a segment loads
+  // (L outputs + KS - s halo); wave-quantised over the whole grid
+  *cost_out = best * (long)(L * s + ks - s + 2);
   return true;
 }
 
