@@ -31,6 +31,7 @@
 //   CONV (backward, stride 1): dx = conv(dz, flipped w) with the transposed
 //       padding (KS-1-pt, KS-1-pl).  Stride 2 uses a direct gather kernel.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <utility>
 
@@ -636,6 +637,80 @@ __global__ void __launch_bounds__(512) dw_dx_s2_same_kernel(const DwShape g, con
   }
 }
 
+// bf16 variant of dw_dx_s2_same_kernel with 16-byte channel vectors (8
+// channels): the k5 kernel above moves 4-byte vectors (its 25 weights x V
+// channels live in registers, capping V at 2), so it issues 4x the memory
+// instructions per byte.  Here the weights sit in shared memory ([KS*KS][C]
+// f32, staged once per CTA) and a thread's 2x2 input block reads its dz window
+// as uint4 rows.  Same tap arithmetic and order as the generic kernel.
+template <int KS>
+__global__ void __launch_bounds__(256) dw_dx_s2_v8_kernel(const DwShape g, const __nv_bfloat16* __restrict__ dz,
+                                                          const float* __restrict__ w, __nv_bfloat16* __restrict__ dx) {
+  constexpr int V = 8;
+  constexpr int PT = KS / 2;
+  constexpr int OMIN = -((KS - 1 - PT) / 2), OMAX = (1 + PT) / 2;
+  constexpr int RW = OMAX - OMIN + 1;
+  extern __shared__ float wsm[];  // [KS*KS][C]
+  pdl_wait();
+  pdl_trigger();
+  for (int i = threadIdx.x; i < KS * KS * g.C / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(wsm)[i] = __ldg(reinterpret_cast<const float4*>(w) + i);
+  __syncthreads();
+  const int CVn = g.C / V;
+  const int BH = (g.Hi + 1) / 2, BW = (g.Wi + 1) / 2;
+  const int64_t items = (int64_t)g.N * BH * BW * CVn;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (int64_t)gridDim.x * blockDim.x) {
+    const int cv = (int)(it % CVn);
+    int64_t blk = it / CVn;
+    const int b = (int)(blk % BW);
+    blk /= BW;
+    const int a = (int)(blk % BH);
+    const int n = (int)(blk / BH);
+    const int c = cv * V;
+    const __nv_bfloat16* dzn = dz + (size_t)n * g.Ho * g.Wo * g.C + c;
+    float win[RW][RW][V];
+#pragma unroll
+    for (int oy = 0; oy < RW; ++oy)
+#pragma unroll
+      for (int ox = 0; ox < RW; ++ox) {
+        const int y = a + OMIN + oy, x = b + OMIN + ox;
+        if (y >= 0 && y < g.Ho && x >= 0 && x < g.Wo) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(dzn + ((size_t)y * g.Wo + x) * g.C));
+          unpack4<__nv_bfloat16>(v, win[oy][ox]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) win[oy][ox][i] = 0.f;
+        }
+      }
+#pragma unroll
+    for (int dyy = 0; dyy < 2; ++dyy)
+#pragma unroll
+      for (int dxx = 0; dxx < 2; ++dxx) {
+        const int iy = 2 * a + dyy, ix = 2 * b + dxx;
+        if (iy >= g.Hi || ix >= g.Wi) continue;
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+#pragma unroll
+        for (int ky = 0; ky < KS; ++ky) {
+          if ((dyy + PT - ky) & 1) continue;
+          const int oy = (dyy + PT - ky) / 2 - OMIN;
+#pragma unroll
+          for (int kx = 0; kx < KS; ++kx) {
+            if ((dxx + PT - kx) & 1) continue;
+            const int ox = (dxx + PT - kx) / 2 - OMIN;
+            const float4 w0 = reinterpret_cast<const float4*>(wsm + (ky * KS + kx) * g.C + c)[0];
+            const float4 w1 = reinterpret_cast<const float4*>(wsm + (ky * KS + kx) * g.C + c)[1];
+            const float wv[V] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] = fmaf(win[oy][ox][i], wv[i], acc[i]);
+          }
+        }
+        *reinterpret_cast<uint4*>(dx + (((size_t)n * g.Hi + iy) * g.Wi + ix) * g.C + c) = pack4<__nv_bfloat16>(acc);
+      }
+  }
+}
+
 // ---------------------------------------------------------------- planning
 struct Plan {
   RingP p;
@@ -856,6 +931,28 @@ int dw_dx(int dtype, const DwShape& g, const void* dz, const float* w, void* dx,
     const int64_t total = (int64_t)g.N * g.Hi * g.Wi * CVn;
     const int grid = (int)std::min<int64_t>((total + per_block - 1) / per_block, (int64_t)num_sms() * 8);
     const bool same = g.pt == g.ks / 2 && g.pl == g.ks / 2;
+    if (same && dtype == DFX_BF16 && g.C % 8 == 0 && (size_t)g.ks * g.ks * g.C * 4 <= 160 * 1024 &&
+        getenv("DFX_DW_DX_S2_V2") == nullptr) {
+      const size_t wsm = (size_t)g.ks * g.ks * g.C * sizeof(float);
+      const int64_t items = (int64_t)g.N * ((g.Hi + 1) / 2) * ((g.Wi + 1) / 2) * (g.C / 8);
+      if (g.ks == 3) {
+        auto k = dw_dx_s2_v8_kernel<3>;
+        if (wsm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, wsm);
+        const int grid3 = (int)std::min<int64_t>((items + 255) / 256, (int64_t)num_sms() * std::max(occ, 1));
+        launch_k(k, grid3, 256, wsm, st, g, (const __nv_bfloat16*)dz, w, (__nv_bfloat16*)dx);
+      } else {
+        auto k = dw_dx_s2_v8_kernel<5>;
+        if (wsm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, wsm);
+        const int grid3 = (int)std::min<int64_t>((items + 255) / 256, (int64_t)num_sms() * std::max(occ, 1));
+        launch_k(k, grid3, 256, wsm, st, g, (const __nv_bfloat16*)dz, w, (__nv_bfloat16*)dx);
+      }
+      DFX_LAUNCH_CHECK("dwconv dx (stride 2, same padding, 16-byte vectors)");
+      return DFX_OK;
+    }
     if (same) {
       const int64_t blocks = (int64_t)g.N * ((g.Hi + 1) / 2) * ((g.Wi + 1) / 2) * CVn;
       const int grid2 = (int)std::min<int64_t>((blocks + per_block - 1) / per_block, (int64_t)num_sms() * 8);
