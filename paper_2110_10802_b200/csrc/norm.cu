@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kThreads) bn_apply_kernel(int64_t rows, int C,
 }
 
 template <typename T, int V, int ACT>
-__global__ void __launch_bounds__(kThreads, 4) bn_bwd_reduce_kernel(int64_t rows, int C, int64_t rpb,
+__global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(int64_t rows, int C, int64_t rpb,
                                                                  const T* __restrict__ dy, const T* __restrict__ x,
                                                                  const float* __restrict__ mean,
                                                                  const float* __restrict__ rstd,
