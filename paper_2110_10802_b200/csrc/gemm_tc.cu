@@ -42,7 +42,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle atom row
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = (2 + kEpiWarps) * 32;
-constexpr int kXfThreads = 128;  // A-operand transform warps of the XF = 1 (excite-folded) instantiation
+constexpr int kXfThreads = 256;  // A-operand transform warps of the XF = 1 (excite-folded) instantiation (2 per SMSP)
 // Epilogue unit geometry (shared with the host, which builds the bulk-store
 // tensor maps): columns per epilogue warp, and bytes per staged unit row.
 __host__ __device__ constexpr int epi_wcols(int bn) { return bn <= 128 ? bn : bn / 4; }
@@ -329,20 +329,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     }
   } else if (XF != 0 && warp >= 2 + kEpiWarps) {
     // ------------------------------------------------- A transform (XF = 1)
-    // Thread = one 16-byte chunk column (8 channels, fixed per stage) x 8 rows
-    // (r0 + 16 i) of each landed [128 x 64] A stage: the per-channel BN
+    // Thread = one 16-byte chunk column (8 channels, fixed per stage) x XIT rows
+    // (r0 + XSTEP i) of each landed [128 x 64] A stage: the per-channel BN
     // constants are loaded once per stage, the SE gate per row's image.  Rows
     // past m and channels past k become zeros (TMA zero-fill would otherwise
     // turn into swish(shift) * gate).  Same arithmetic as excite_kernel
     // (mbconv.cu), so y is bitwise the unfused path's.
+    constexpr int XSTEP = kXfThreads / 8, XIT = BM / XSTEP;
     const int tt = threadIdx.x - (2 + kEpiWarps) * 32;
     const int ch = tt & 7, r0 = tt >> 3;
-    const int hw = (int)p.x_hw;  // rows per image (>= 16: one carry per 16-row step below)
+    const int hw = (int)p.x_hw;  // rows per image (>= XSTEP: one carry per row step below)
     uint32_t it = 0;
     for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
       const TileIdx ti = tile_of(t, p);
       const int64_t m0 = (int64_t)ti.mb * BM;
-      // image of this thread's first row, then carried across its 16-row steps (no divisions per chunk)
+      // image of this thread's first row, then carried across its row steps (no divisions per chunk)
       const int first = (int)(m0 + r0);
       const int img0 = first / hw, rem0 = first - img0 * hw;
       for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
@@ -359,12 +360,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         mbar_wait(&full[s], ph);
         const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
         int img = img0, rem = rem0;
-#pragma unroll 4
-        for (int i = 0; i < 8; ++i) {
-          const int r = r0 + 16 * i;
+#pragma unroll
+        for (int i = 0; i < XIT; ++i) {
+          const int r = r0 + XSTEP * i;
           const int64_t gm = m0 + r;
           if (i > 0) {
-            rem += 16;
+            rem += XSTEP;
             if (rem >= hw) { rem -= hw; ++img; }
           }
           const uint32_t addr = sa + r * 128 + ((ch ^ (r & 7)) << 4);
@@ -819,7 +820,8 @@ int gemm_excite(int64_t m, int64_t k, int64_t n, const void* z, int64_t hw, cons
                 cudaStream_t st) {
   DFX_REQUIRE(m > 0 && n > 0 && k > 0 && hw > 0, DFX_ERR_SHAPE, "dfx_gemm_excite: empty extent");
   DFX_REQUIRE(k % 8 == 0 && n % 8 == 0, DFX_ERR_SHAPE, "dfx_gemm_excite: k and n must be multiples of 8");
-  DFX_REQUIRE(hw >= 16 && m < (1ll << 31), DFX_ERR_UNSUPPORTED, "dfx_gemm_excite: needs >= 16 rows per image");
+  DFX_REQUIRE(hw >= kXfThreads / 8 && m < (1ll << 31), DFX_ERR_UNSUPPORTED,
+              "dfx_gemm_excite: needs >= 32 rows per image");
   DFX_REQUIRE(z && w && d && mean && rstd && gamma && beta && gate, DFX_ERR_SHAPE, "dfx_gemm_excite: null operand");
   DFX_REQUIRE(aligned16(z) && aligned16(w) && aligned16(d) && aligned16(gate) && (!y_out || aligned16(y_out)),
               DFX_ERR_ALIGN, "dfx_gemm_excite: operands must be 16-byte aligned");

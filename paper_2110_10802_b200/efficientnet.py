@@ -177,7 +177,7 @@ class _Block:
         return self.Wl[self.p + name] if self.Wl is not None else self.net.master[self.p + name]
 
     def _out_hw(self, x):
-        """Output pixels per image of the depthwise conv (the fold needs >= 16)."""
+        """Output pixels per image of the depthwise conv (the fold needs >= 32)."""
         _, H, W, _ = x.shape
         p = self.k // 2
         return ((H + 2 * p - self.k) // self.s + 1) * ((W + 2 * p - self.k) // self.s + 1)
@@ -193,7 +193,7 @@ class _Block:
         else:
             a = x
         self.a = a
-        if self.net.cfg.fold_excite and x.dtype == torch.bfloat16 and self._out_hw(x) >= 16:
+        if self.net.cfg.fold_excite and x.dtype == torch.bfloat16 and self._out_hw(x) >= 32:
             # excite + project as one GEMM over z; y is still written for the weight gradient
             self.mb.forward(a, excite=False)
             mbb = self.mb.buffers(a.shape)
