@@ -450,9 +450,16 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     }                                                                                              \
   } while (0)
   constexpr int V = 8;
-  extern __shared__ float red[];  // [2][16][cols] staging planes, then gamma [cols]
-  float* red2 = red + 16 * cols;
-  float* gam = red2 + 16 * cols;
+  extern __shared__ float red[];  // [2][16][pst] staging planes, then gamma [cols]
+  // plane position of column c: c + 2 * (c >> 5) (every 32-column group shifted
+  // two floats further).  The writers (lane l holds columns 8l..8l+7 of a
+  // 256-column chunk) then hit 16 distinct bank pairs per float2 store instead
+  // of 4 (8-way conflicts), and the column-sum readers (consecutive threads,
+  // consecutive columns) stay conflict-free.
+  const int pst = cols + 2 * ((cols + 31) >> 5);
+  auto ppos = [](int c) { return c + 2 * (c >> 5); };
+  float* red2 = red + 16 * pst;
+  float* gam = red2 + 16 * pst;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvec = cols / V;
   const float inv_n = 1.f / (float)cols;
@@ -546,8 +553,8 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
       const uint32_t ws[4] = {sr[c].x, sr[c].y, sr[c].z, sr[c].w};
       const uint32_t wd[4] = {dr[c].x, dr[c].y, dr[c].z, dr[c].w};
       uint32_t pds[4], pdh[4];
-      float2* r1 = reinterpret_cast<float2*>(red + warp * cols + col);
-      float2* r2 = reinterpret_cast<float2*>(red2 + warp * cols + col);
+      float2* r1 = reinterpret_cast<float2*>(red + warp * pst + ppos(col));
+      float2* r2 = reinterpret_cast<float2*>(red2 + warp * pst + ppos(col));
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float2 y = bf2(wd[i]);
@@ -578,8 +585,8 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     float th = 0.f, tg = 0.f;
 #pragma unroll
     for (int w = 0; w < 16; ++w) {
-      th += red[w * cols + col];
-      tg += red2[w * cols + col];
+      th += red[w * pst + ppos(col)];
+      tg += red2[w * pst + ppos(col)];
     }
     part[((size_t)2 * nparts + blockIdx.x) * cols + col] = th;
     part[((size_t)0 * nparts + blockIdx.x) * cols + col] = tg;
@@ -591,17 +598,16 @@ __global__ void __launch_bounds__(512, 2) bdrln_bwd_wave_kernel(
     const int vi = lane + c * 32;
     if (vi < nvec) {
       const uint32_t wd[4] = {dr[c].x, dr[c].y, dr[c].z, dr[c].w};
-      float4* r1 = reinterpret_cast<float4*>(red + warp * cols + vi * V);
-      const float2 y0 = bf2(wd[0]), y1 = bf2(wd[1]), y2 = bf2(wd[2]), y3 = bf2(wd[3]);
-      r1[0] = make_float4(y0.x, y0.y, y1.x, y1.y);
-      r1[1] = make_float4(y2.x, y2.y, y3.x, y3.y);
+      float2* r1 = reinterpret_cast<float2*>(red + warp * pst + ppos(vi * V));  // 8-byte aligned (skewed planes)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) r1[i] = bf2(wd[i]);
     }
   }
   __syncthreads();
   for (int col = threadIdx.x; col < cols; col += blockDim.x) {
     float t = 0.f;
 #pragma unroll
-    for (int w = 0; w < 16; ++w) t += red[w * cols + col];
+    for (int w = 0; w < 16; ++w) t += red[w * pst + ppos(col)];
     part[((size_t)1 * nparts + blockIdx.x) * cols + col] = t;
   }
   RTRACE(7);
@@ -1074,7 +1080,7 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
   float* ph = pb + (size_t)grid * cols;
   int rc;
   if (wave) {
-    const size_t wsm = (size_t)(2 * 16 + 1) * cols * sizeof(float);  // two staging planes + gamma
+    const size_t wsm = ((size_t)2 * 16 * (cols + 2 * ((cols + 31) / 32)) + cols) * sizeof(float);  // planes + gamma
 #define LW(N)                                                                                      \
   if (nch == N) {                                                                                  \
     auto kfn = bdrln_bwd_wave_kernel<N>;                                                           \
