@@ -139,19 +139,26 @@ __device__ __forceinline__ void block_colsum_store(float (&acc)[NCH][V], int col
                                                    float* __restrict__ part) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvec = cols / V;
+  // staging position of column c: c + (c >> 5).  Lanes write V-strided
+  // columns; the one-float skew per 32-column group spreads them over all 32
+  // banks (unskewed: 32 / V distinct banks), the column readers stay linear.
+  const int pst = cols + ((cols + 31) >> 5);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int vi = lane + c * 32;
     if (vi < nvec) {
 #pragma unroll
-      for (int i = 0; i < V; ++i) red[warp * cols + vi * V + i] = acc[c][i];
+      for (int i = 0; i < V; ++i) {
+        const int col = vi * V + i;
+        red[warp * pst + col + (col >> 5)] = acc[c][i];
+      }
     }
   }
   __syncthreads();
   for (int col = threadIdx.x; col < cols; col += blockDim.x) {
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += red[w * cols + col];
+    for (int w = 0; w < kWarps; ++w) s += red[w * pst + col + (col >> 5)];
     part[(size_t)blockIdx.x * cols + col] = s;
   }
   __syncthreads();
@@ -1098,7 +1105,7 @@ int bdrln_bwd_t(int64_t rows, int64_t cols, const void* dy, const void* s, const
     }
     return DFX_OK;
   }
-  const size_t smem = (size_t)kWarps * cols * sizeof(float);
+  const size_t smem = (size_t)kWarps * (cols + (cols + 31) / 32) * sizeof(float);  // skewed staging (block_colsum_store)
   rc = act ? bdrln_bwd_launch<T, V, 1>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, kbits, ks, eps, ds, dh,
                                         pg, pb, ph, st)
                : bdrln_bwd_launch<T, V, 0>(nch, grid, smem, rows, cols, dy, s, gamma, beta, keep, kbits, ks, eps, ds, dh,
