@@ -27,8 +27,9 @@
 //          keep flags in each backward kernel.
 //   bwd_dq   per 128-query strip, 128-key chunks: S and dPd = dO·Vᵀ in TMEM,
 //            dS = P∘(dPd∘M - D)·c in smem, dQ += dS·K.   D = rowsum(dO∘O).
-//   bwd_dkdv per 128-key strip, 128-query chunks: Sᵀ = K·Qᵀ, dPdᵀ = V·dOᵀ,
-//            dV += Pdᵀ·dO, dK += dSᵀ·Q.
+//   bwd_kstrip per 128-key strip, 128-query chunks: Sᵀ = K·Qᵀ, dPdᵀ = V·dOᵀ,
+//            dV += Pdᵀ·dO, dK += dSᵀ·Q; dSᵀ tiles to HBM for dQ = dS·K
+//            (a tcgen05 GEMM), or dQ from bwd_dq (DFX_ATTN_BWD_LEGACY).
 // No cross-CTA reductions: every output element is produced by one CTA in a
 // fixed order (bitwise reproducible, no atomics).
 #include <cuda.h>
@@ -715,16 +716,18 @@ struct AttnBwdParams {
   const __nv_bfloat16* dctx;  // dO  [T, ld_ctx]
   const float* add_mask;      // [B, S] or null
   const float* lse;           // [B, NH, S] log2 domain
-  float* delta;               // [B, NH, S]  D = rowsum(dO∘O) (written by dq, read by dkdv)
+  float* delta;               // [B, NH, S]  D = rowsum(dO∘O) (written by dq / the delta pre-pass, read by kstrip)
   const uint32_t* kb_row;     // or null (no dropout)
   const uint32_t* kb_col;
   float ks, sc2, scale;       // keep scale, inv_divisor*log2e, inv_divisor
   __nv_bfloat16* dqkv;        // [T, ld_dqkv]: dQ | dK | dV column blocks
   float* bias_part;           // [B*S/128][3H]: per-strip column sums of dQ | dK | dV (qkv bias gradient)
-  int ds_store;               // dkdv: also store dSᵀ (map_ds) and the strip's dQ column sums (dQ = dS·K GEMM path)
+  int ds_store;               // kstrip: also store dSᵀ (map_ds) and the strip's dQ column sums (dQ = dS·K GEMM path)
+  const __nv_bfloat16* qkv;   // Q | K | V [T, ld_qkv] (the key-strip kernel reads K rows for dQ's column sums)
+  int64_t ld_qkv;
 };
 
-constexpr int CH = 128;  // keys (dq) / queries (dkdv) per chunk
+constexpr int CH = 128;  // keys (dq) / queries (kstrip) per chunk
 
 struct DqSmem {
   static constexpr int Q = 0;
@@ -740,22 +743,6 @@ struct DqSmem {
 };
 static_assert(DqSmem::TOTAL <= 227 * 1024, "attention dq exceeds shared memory");
 
-struct DkvSmem {
-  static constexpr int K = 0;
-  static constexpr int V = K + QT * 128;
-  static constexpr int NST = 2;                      // ring depth (3 measured slower)
-  static constexpr int RING = V + QT * 128;          // NST stages x (Q_j, dO_j)
-  static constexpr int STAGE = 2 * CH * 128;
-  static constexpr int PD = RING + NST * STAGE;
-  static constexpr int DS = PD + QT * CH * 2;
-  static constexpr int LSE = DS + QT * CH * 2;
-  static constexpr int DEL = LSE + kMaxSeq * 4;
-  static constexpr int LUT = DEL + kMaxSeq * 4;  // keep nibble -> 4 x {0, 1}
-  static constexpr int CS = LUT + 16 * 16;       // [4][128] per-part Σ_q dS (ds_store)
-  static constexpr int BAR = CS + 4 * QT * 4;
-  static constexpr int TOTAL = BAR + 256 + KB;
-};
-static_assert(DkvSmem::TOTAL <= 227 * 1024, "attention dkdv exceeds shared memory");
 
 // Write 32 consecutive columns (col0 % 32 == 0, within a 128-column chunk) of
 // row r of a [128 x 128] bf16 operand stored as two [128 x 64] SW128 tiles.
@@ -764,6 +751,40 @@ __device__ __forceinline__ void st_row32(uint32_t buf, int r, int col0, const ui
   const int ch0 = (col0 & 63) >> 3;
 #pragma unroll
   for (int u = 0; u < 4; ++u) st_sw128(tile, r, ch0 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+}
+
+// Column sums of NT [128 x 64] fp32 tiles held one row slice per softmax
+// thread (warp quarter q: rows 32 q + lane; part: columns 16 part .. + 15), in a
+// fixed order: a halving butterfly over the warp's 32 rows (16 shuffles per
+// tile; lane l ends with column (l >> 1) & 15), then the four quarters in
+// order q = 0..3 through smem (red: NT x 4 x 64 floats) -> out_t[0..63].
+template <int NT>
+__device__ __forceinline__ void strip_colsum(float (&v)[NT][16], int lane, int q, int part, int st, float* red,
+                                             float* const (&out)[NT]) {
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1) {
+      const bool hi = lane & (2 * w);
+#pragma unroll
+      for (int i = 0; i < w; ++i) {
+        const float send = hi ? v[t][i] : v[t][i + w];
+        const float keep = hi ? v[t][i + w] : v[t][i];
+        v[t][i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * w);
+      }
+    }
+    v[t][0] += __shfl_xor_sync(0xffffffffu, v[t][0], 1);
+    if (!(lane & 1)) red[(t * 4 + q) * 64 + part * 16 + ((lane >> 1) & 15)] = v[t][0];
+  }
+  named_bar(1, kSoftWarps * 32);
+  if (st < NT * 64) {
+    const int t = st >> 6, col = st & 63;
+    const float* r = red + t * 256 + col;
+    float* o = out[0];  // (selects, not an indexed local array)
+#pragma unroll
+    for (int u = 1; u < NT; ++u) o = t == u ? out[u] : o;
+    o[col] = ((r[0] + r[64]) + r[128]) + r[192];
+  }
 }
 
 // Column sums of NT 128 x 64 fp32 tiles whose rows are spread one 16-column
@@ -1025,36 +1046,79 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_con
   }
 }
 
-// dK / dV strip: CTA = (b, h, 128-key block); loops over 128-query chunks.
-__global__ void __launch_bounds__(kAttnThreads, 1)
-attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
-                     const __grid_constant__ CUtensorMap map_ds, const AttnBwdParams p) {
-  // dynamic smem opens the CTA's window (no static smem in this kernel): it is
-  // 1024-B aligned, and indexing it directly keeps every access LDS/STS
+// ----------------------------------------------- persistent key-strip backward
+// One CTA per SM walks the (b, h, 128-key) strips blockIdx.x, + grid, ...: the
+// Q / dO ring, the S / dPd TMEM buffers and the chunk barriers run on one
+// chunk sequence across strips, so the next strip's K / V / lse / D loads and
+// its first Sᵀ / dPdᵀ MMAs overlap this strip's last chunk and epilogue (the
+// next strip's first dK / dV MMA follows its first Pd / dS tiles, which the
+// softmax warps write only after reading this strip's dK / dV).  Per chunk:
+// P and dS = P∘(dPd∘keep·ks − D) in packed fp32 from Sᵀ / dPdᵀ, Pdᵀ / dSᵀ as
+// SW128 bf16 tiles, dV += Pdᵀ·dO_j and dK += dSᵀ·Q_j.  A 19th warp TMA-stores
+// each dSᵀ tile (so the MMA thread never waits on a bulk read), the epilogue stores dK / dV by TMA
+// from bf16 tiles staged in the Pd buffer and reduces the bias column sums by
+// shuffles.
+constexpr int kKsThreads = kAttnThreads + 32;
+struct KsSmem {
+  static constexpr int K = 0;
+  static constexpr int V = K + QT * 128;
+  static constexpr int NST = 3;
+  static constexpr int RING = V + QT * 128;
+  static constexpr int STAGE = 2 * CH * 128;         // Q_j | dO_j
+  static constexpr int PD = RING + NST * STAGE;      // Pdᵀ tile; the dK | dV bf16 tiles in the epilogue
+  static constexpr int DS = PD + QT * CH * 2;
+  static constexpr int ROWS = DS + QT * CH * 2;      // two buffers (strip parity) of lse | D | key mask
+  static constexpr int ROWB = 2 * kMaxSeq * 4 + QT * 4;
+  static constexpr int LUT = ROWS + 2 * ROWB;
+  static constexpr int CS = LUT + 16 * 16;           // [4][128] per-part Σ_q dS
+  static constexpr int RED = CS + 4 * QT * 4;        // [3][4][64] column-sum quarters
+  static constexpr int BAR = RED + 3 * 4 * 64 * 4;
+  static constexpr int TOTAL = BAR + 256 + KB;
+};
+static_assert(KsSmem::TOTAL <= 227 * 1024, "attention key-strip kernel exceeds shared memory");
+
+struct StripIdx {
+  int bh, b, h, k0, row0;
+};
+__device__ __forceinline__ StripIdx strip_idx(int sidx, const AttnBwdParams& p) {
+  const int nkb = p.S / QT, kb = sidx % nkb, bh = sidx / nkb;
+  return {bh, bh / p.NH, bh % p.NH, kb * QT, (bh / p.NH) * p.S};
+}
+
+__global__ void __launch_bounds__(kKsThreads, 1)
+attn_bwd_kstrip_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
+                       const __grid_constant__ CUtensorMap map_ds, const __grid_constant__ CUtensorMap map_dkv,
+                       const AttnBwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + DkvSmem::BAR);
-  uint64_t *bar_a = bar, *bar_s = bar + 1, *bar_tfree = bar + 2, *bar_pds = bar + 3, *bar_pdsfree = bar + 4;
-  uint64_t* full = bar + 8;    // [NST]
-  uint64_t* empty = bar + 12;  // [NST]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-  constexpr int NST = DkvSmem::NST;
-  float* lse_s = reinterpret_cast<float*>(smem + DkvSmem::LSE);
-  float* del_s = reinterpret_cast<float*>(smem + DkvSmem::DEL);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + KsSmem::BAR);
+  uint64_t *bar_kv = bar, *bar_s = bar + 1, *bar_tfree = bar + 2, *bar_pds = bar + 3, *bar_pdsfree = bar + 4;
+  uint64_t* kv_free = bar + 5;
+  uint64_t* bar_rows = bar + 6;   // [2]
+  uint64_t* rows_free = bar + 8;  // [2]
+  uint64_t* ds_free = bar + 10;   // the dSᵀ tile's store has read it
+  uint64_t* full = bar + 11;      // [NST]
+  uint64_t* empty = bar + 14;     // [NST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+  constexpr int NST = KsSmem::NST;
+  auto rows = [&](int it) { return reinterpret_cast<float*>(smem + KsSmem::ROWS + (it & 1) * KsSmem::ROWB); };
 
   const int S = p.S, nch = S / CH;
-  const int kb = blockIdx.x % (S / QT);
-  const int bh = blockIdx.x / (S / QT);
-  const int b = bh / p.NH, h = bh % p.NH;
-  const int k0 = kb * QT, row0 = b * S;
+  const int nstrips = p.B * p.NH * (S / QT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    mbar_init(bar_a, 1);
+    mbar_init(bar_kv, 1);
     mbar_init(bar_s, 1);
     mbar_init(bar_tfree, kSoftWarps);
     mbar_init(bar_pds, kSoftWarps);
     mbar_init(bar_pdsfree, 1);
+    mbar_init(kv_free, 1);  // the strip's last Sᵀ / dPdᵀ MMAs completed
+    mbar_init(ds_free, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_rows[b], 1);
+      mbar_init(&rows_free[b], kSoftWarps);  // every softmax warp's last lse / D read of the buffer's strip
+    }
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1070,30 +1134,42 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
   // dependents launch only once this CTA holds its TMEM: a dependent grid's CTA
   // allocating first on this SM would block our alloc while it waits on us
   pdl_trigger();
-  pdl_wait();  // setup above overlapped the previous kernel's tail
+  pdl_wait();
   if (threadIdx.x == 0) ATRACE(0);
   constexpr uint32_t T_S = 0, T_DP = 128, T_DK = 256, T_DV = 320;
 
   if (warp == 0) {
     if (lane == 0) {
-      // K, V strips and the head's lse / D rows (bulk copies)
-      mbar_expect_tx(bar_a, 2 * QT * 128 + 2 * S * 4);
-      const uint32_t ba = smem_u32(bar_a);
-      bulk_g2s(lse_s, p.lse + (size_t)bh * S, S * 4, ba);
-      bulk_g2s(del_s, p.delta + (size_t)bh * S, S * 4, ba);
-      for (int u = 0; u < 2; ++u) {
-        tma_load_4d_cg<1>(&map_qkv, ba, smem + DkvSmem::K + u * 8 * KB, p.H + h * DH, row0 + k0 + 64 * u, 0, 0);
-        tma_load_4d_cg<1>(&map_qkv, ba, smem + DkvSmem::V + u * 8 * KB, 2 * p.H + h * DH, row0 + k0 + 64 * u, 0, 0);
-      }
-      for (int j = 0; j < nch; ++j) {
-        const int s = j % NST;
-        mbar_wait(&empty[s], ((j / NST) & 1) ^ 1);
-        mbar_expect_tx(&full[s], DkvSmem::STAGE);
-        const uint32_t bf = smem_u32(&full[s]);
-        uint8_t* stq = smem + DkvSmem::RING + s * DkvSmem::STAGE;
+      int J = 0, it = 0;
+      for (int sidx = blockIdx.x; sidx < nstrips; sidx += gridDim.x, ++it) {
+        const StripIdx t = strip_idx(sidx, p);
+        // K / V once the previous strip's Sᵀ / dPdᵀ MMAs are done; lse / D /
+        // mask rows into the buffer the strip two back released
+        if (it > 0) mbar_wait(kv_free, (it - 1) & 1);
+        mbar_expect_tx(bar_kv, 2 * QT * 128);
+        const uint32_t ba = smem_u32(bar_kv);
         for (int u = 0; u < 2; ++u) {
-          tma_load_4d_cg<1>(&map_qkv, bf, stq + u * 8 * KB, h * DH, row0 + j * CH + 64 * u, 0, 0);
-          tma_load_4d_cg<1>(&map_do, bf, stq + CH * 128 + u * 8 * KB, h * DH, row0 + j * CH + 64 * u, 0, 0);
+          tma_load_4d_cg<1>(&map_qkv, ba, smem + KsSmem::K + u * 8 * KB, p.H + t.h * DH, t.row0 + t.k0 + 64 * u, 0, 0);
+          tma_load_4d_cg<1>(&map_qkv, ba, smem + KsSmem::V + u * 8 * KB, 2 * p.H + t.h * DH, t.row0 + t.k0 + 64 * u, 0,
+                            0);
+        }
+        if (it >= 2) mbar_wait(&rows_free[it & 1], ((it - 2) >> 1) & 1);
+        mbar_expect_tx(&bar_rows[it & 1], 2 * S * 4 + (p.add_mask ? QT * 4 : 0));
+        const uint32_t br = smem_u32(&bar_rows[it & 1]);
+        float* rw = rows(it);
+        bulk_g2s(rw, p.lse + (size_t)t.bh * S, S * 4, br);
+        bulk_g2s(rw + kMaxSeq, p.delta + (size_t)t.bh * S, S * 4, br);
+        if (p.add_mask) bulk_g2s(rw + 2 * kMaxSeq, p.add_mask + (size_t)t.b * S + t.k0, QT * 4, br);
+        for (int j = 0; j < nch; ++j, ++J) {
+          const int s = J % NST;
+          mbar_wait(&empty[s], ((J / NST) & 1) ^ 1);
+          mbar_expect_tx(&full[s], KsSmem::STAGE);
+          const uint32_t bf = smem_u32(&full[s]);
+          uint8_t* stq = smem + KsSmem::RING + s * KsSmem::STAGE;
+          for (int u = 0; u < 2; ++u) {
+            tma_load_4d_cg<1>(&map_qkv, bf, stq + u * 8 * KB, t.h * DH, t.row0 + j * CH + 64 * u, 0, 0);
+            tma_load_4d_cg<1>(&map_do, bf, stq + CH * 128 + u * 8 * KB, t.h * DH, t.row0 + j * CH + 64 * u, 0, 0);
+          }
         }
       }
     }
@@ -1101,164 +1177,210 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_c
     if (lane == 0) {
       const uint32_t idesc_s = make_idesc(CH, QT, 0, 0);
       const uint32_t idesc_g = make_idesc(DH, QT, 0, 1);
-      const uint64_t kdesc = make_sdesc(sbase + DkvSmem::K, 16, 1024);
-      const uint64_t vdesc = make_sdesc(sbase + DkvSmem::V, 16, 1024);
-      mbar_wait(bar_a, 0);
-      ATRACE(1);
-      auto issue_grads = [&](int j) {  // dV += Pdᵀ·dO_j ; dK += dSᵀ·Q_j   (B operands MN-major)
-        mbar_wait(bar_pds, j & 1);
+      const uint64_t kdesc = make_sdesc(sbase + KsSmem::K, 16, 1024);
+      const uint64_t vdesc = make_sdesc(sbase + KsSmem::V, 16, 1024);
+      // dV += Pdᵀ·dO_j ; dK += dSᵀ·Q_j for chunk J = chunk j of the it-th strip
+      auto issue_grads = [&](int J, int j) {
+        mbar_wait(bar_pds, J & 1);
         tc_fence_after();
-        if (p.ds_store) {  // dSᵀ tile (two 64-query SW128 halves) -> HBM, the dQ GEMM's A operand
-          tma_store_4d(&map_ds, sbase + DkvSmem::DS, j * CH, bh * S + k0, 0, 0);
-          tma_store_4d(&map_ds, sbase + DkvSmem::DS + 16 * KB, j * CH + 64, bh * S + k0, 0, 0);
-          bulk_commit();
-        }
-        const uint32_t stq = sbase + DkvSmem::RING + (j % NST) * DkvSmem::STAGE;
+        const uint32_t dsb = sbase + KsSmem::DS;
+        const uint32_t stq = sbase + KsSmem::RING + (J % NST) * KsSmem::STAGE;
         const uint64_t qmn = make_sdesc(stq, 8 * KB, 1024);
         const uint64_t domn = make_sdesc(stq + CH * 128, 8 * KB, 1024);
 #pragma unroll
         for (int kc = 0; kc < CH / 16; ++kc) {
-          const uint64_t pd = make_sdesc(sbase + DkvSmem::PD + (kc >> 2) * 16 * KB, 16, 1024);
-          const uint64_t ds = make_sdesc(sbase + DkvSmem::DS + (kc >> 2) * 16 * KB, 16, 1024);
+          const uint64_t pd = make_sdesc(sbase + KsSmem::PD + (kc >> 2) * 16 * KB, 16, 1024);
+          const uint64_t ds = make_sdesc(dsb + (kc >> 2) * 16 * KB, 16, 1024);
           const uint32_t acc = (j > 0 || kc > 0) ? 1u : 0u;
           tc_mma_cg<1>(tmem + T_DV, pd + 2 * (kc & 3), domn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
           tc_mma_cg<1>(tmem + T_DK, ds + 2 * (kc & 3), qmn + (uint64_t)(kc * (2048 >> 4)), idesc_g, acc);
         }
-        if (p.ds_store) bulk_wait_read<0>();  // the DS tile is overwritten once pdsfree fires
-        tc_commit_cg<1>(&empty[j % NST]);
+        tc_commit_cg<1>(&empty[J % NST]);
         tc_commit_cg<1>(bar_pdsfree);
       };
-      for (int j = 0; j < nch; ++j) {
-        mbar_wait(&full[j % NST], (j / NST) & 1);
-        if (j > 0) mbar_wait(bar_tfree, (j - 1) & 1);
-        tc_fence_after();
-        const uint32_t stq = sbase + DkvSmem::RING + (j % NST) * DkvSmem::STAGE;
-        const uint64_t qdesc = make_sdesc(stq, 16, 1024);
-        const uint64_t dodesc = make_sdesc(stq + CH * 128, 16, 1024);
+      int J = 0, it = 0;
+      for (int sidx = blockIdx.x; sidx < nstrips; sidx += gridDim.x, ++it) {
+        mbar_wait(bar_kv, it & 1);
+        if (it == 0) ATRACE(1);
+        for (int j = 0; j < nch; ++j, ++J) {
+          mbar_wait(&full[J % NST], (J / NST) & 1);
+          if (J > 0) mbar_wait(bar_tfree, (J - 1) & 1);
+          tc_fence_after();
+          const uint32_t stq = sbase + KsSmem::RING + (J % NST) * KsSmem::STAGE;
+          const uint64_t qdesc = make_sdesc(stq, 16, 1024);
+          const uint64_t dodesc = make_sdesc(stq + CH * 128, 16, 1024);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          tc_mma_cg<1>(tmem + T_S, kdesc + 2 * kk, qdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
-          tc_mma_cg<1>(tmem + T_DP, vdesc + 2 * kk, dodesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            tc_mma_cg<1>(tmem + T_S, kdesc + 2 * kk, qdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
+            tc_mma_cg<1>(tmem + T_DP, vdesc + 2 * kk, dodesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
+          }
+          tc_commit_cg<1>(bar_s);
+          if (j == nch - 1) tc_commit_cg<1>(kv_free);  // K / V read once these complete
+          if (j > 0) issue_grads(J - 1, j - 1);
         }
-        tc_commit_cg<1>(bar_s);
-        if (j > 0) issue_grads(j - 1);
+        // the strip's last gradients before the next strip's first Sᵀ / dPdᵀ,
+        // which wait for its K / V: the epilogue needs the former, not the latter
+        issue_grads(J - 1, nch - 1);
       }
-      issue_grads(nch - 1);
+    }
+  } else if (warp == 2 + kSoftWarps) {
+    if (lane == 0) {  // dSᵀ tiles (two 64-query SW128 halves) -> HBM, the dQ GEMM's A operand
+      int J = 0;
+      for (int sidx = blockIdx.x; sidx < nstrips; sidx += gridDim.x) {
+        const StripIdx t = strip_idx(sidx, p);
+        for (int j = 0; j < nch; ++j, ++J) {
+          mbar_wait(bar_pds, J & 1);
+          if (p.ds_store) {
+            tma_store_4d(&map_ds, sbase + KsSmem::DS, j * CH, t.bh * S + t.k0, 0, 0);
+            tma_store_4d(&map_ds, sbase + KsSmem::DS + 16 * KB, j * CH + 64, t.bh * S + t.k0, 0, 0);
+            bulk_commit();
+            bulk_wait_read<0>();
+          }
+          mbar_arrive(ds_free);
+        }
+      }
     }
   } else {
     const int sw = warp - 2, q = warp & 3, part = sw >> 2;
-    const int rl = q * 32 + lane, key = k0 + rl;
+    const int rl = q * 32 + lane;
     const int st = threadIdx.x - 64;
     const int words = S / 32;
-    const size_t keyi = (size_t)bh * S + key;
-    // packed keep words, issued first so their latency overlaps the prologue
-    uint32_t kbw[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    if (p.kb_col) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < nch) kbw[j] = __ldg(p.kb_col + keyi * words + ((j * CH + part * 32) >> 5));
-    }
-    const float mraw = p.add_mask ? __ldg(p.add_mask + (size_t)b * S + key) : 0.f;  // consumed after the waits
-    const float4* klut = reinterpret_cast<const float4*>(smem + DkvSmem::LUT);
-    fill_keep_lut(reinterpret_cast<float4*>(smem + DkvSmem::LUT), st, 1.f);
+    const float4* klut = reinterpret_cast<const float4*>(smem + KsSmem::LUT);
+    fill_keep_lut(reinterpret_cast<float4*>(smem + KsSmem::LUT), st, 1.f);
     named_bar(1, kSoftWarps * 32);
-    mbar_wait(bar_a, 0);  // lse / D rows landed (with K, V)
-    // P' = P / divisor: the divisor's log2 folds into the row mask term
-    const float mrow = mraw * kLog2e + __log2f(p.scale);
-    float cs = 0.f;  // Σ_q dS[q, key] over this thread's columns (ds_store: the dQ column sums)
-    if (sw == 0 && lane == 0) ATRACE(12);
+    const float lsc = __log2f(p.scale);
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    for (int j = 0; j < nch; ++j) {
-      mbar_wait(bar_s, j & 1);
-      if (sw == 0 && lane == 0 && j < 4) ATRACE(2 + j);
+    const float2 sc2x2 = make_float2(p.sc2, p.sc2), ks2 = make_float2(p.ks, p.ks);
+    int J = 0, it = 0;
+    for (int sidx = blockIdx.x; sidx < nstrips; sidx += gridDim.x, ++it) {
+      const StripIdx t = strip_idx(sidx, p);
+      const size_t keyi = (size_t)t.bh * S + t.k0 + rl;
+      const uint32_t* kbp = p.kb_col ? p.kb_col + keyi * words + part : nullptr;  // chunk j's word: kbp[4 j]
+      uint32_t bits_n = kbp ? __ldg(kbp) : 0xFFFFFFFFu;
+      const float* lse_s = rows(it);
+      const float* del_s = lse_s + kMaxSeq;
+      mbar_wait(&bar_rows[it & 1], (it >> 1) & 1);  // lse / D / mask rows landed
+      // P' = P / divisor: the divisor's log2 folds into the row mask term
+      const float mrow = (p.add_mask ? lse_s[2 * kMaxSeq + rl] * kLog2e : 0.f) + lsc;
+      const float2 mrow2 = make_float2(mrow, mrow);
+      float cs = 0.f;  // Σ_q dS[q, key] over this thread's columns (ds_store: the dQ column sums)
+      for (int j = 0; j < nch; ++j, ++J) {
+        const uint32_t bits = bits_n;
+        if (kbp && j + 1 < nch) bits_n = __ldg(kbp + 4 * (j + 1));
+        mbar_wait(bar_s, J & 1);
+        if (it == 0 && sw == 0 && lane == 0 && j < 4) ATRACE(2 + j);
+        tc_fence_after();
+        float sv[32], dp[32];
+        tmem_ld32(trow + T_S + part * 32, sv);
+        tmem_ld32(trow + T_DP + part * 32, dp);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_tfree);
+        const int qc0 = j * CH + part * 32;
+        uint32_t pkp[16], pks[16];
+        float4 kf;
+        float2 csum = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float2 l = reinterpret_cast<const float2*>(lse_s + qc0)[i >> 1];
+          const float2 dd = reinterpret_cast<const float2*>(del_s + qc0)[i >> 1];
+          const float2 tt = __ffma2_rn(make_float2(sv[i], sv[i + 1]), sc2x2, __fadd2_rn(mrow2, make_float2(-l.x, -l.y)));
+          const float2 P = make_float2(ex2(tt.x), ex2(tt.y));
+          if ((i & 3) == 0) kf = klut[(bits >> i) & 15u];
+          const float2 kk = (i & 3) ? make_float2(kf.z, kf.w) : make_float2(kf.x, kf.y);  // keep in {0, 1}
+          const float2 pd = __fmul2_rn(P, kk);
+          const float2 dpm = __fmul2_rn(make_float2(dp[i], dp[i + 1]), kk);
+          const float2 ds = __fmul2_rn(P, __ffma2_rn(dpm, ks2, make_float2(-dd.x, -dd.y)));
+          csum = __fadd2_rn(csum, ds);
+          pkp[i >> 1] = pack_bf16x2(pd.x, pd.y);
+          pks[i >> 1] = pack_bf16x2(ds.x, ds.y);
+        }
+        cs += csum.x + csum.y;
+        if (j == nch - 1) {  // the strip's lse / D / mask rows are no longer read
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rows_free[it & 1]);
+        }
+        if (J > 0) {  // the previous Pd / dS tiles: MMAs done, dS stored
+          mbar_wait(bar_pdsfree, (J - 1) & 1);
+          mbar_wait(ds_free, (J - 1) & 1);
+        }
+        st_row32(sbase + KsSmem::PD, rl, part * 32, pkp);
+        st_row32(sbase + KsSmem::DS, rl, part * 32, pks);
+        fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_pds);
+      }
+      // ---- epilogue: the strip's gradient MMAs are done once the last chunk's Pd / dS are released
+      mbar_wait(bar_pdsfree, (J - 1) & 1);
+      if (it < 3 && sw == 0 && lane == 0) ATRACE(6 + it);
       tc_fence_after();
-      float s[32], dp[32];
-      tmem_ld32(trow + T_S + part * 32, s);
-      tmem_ld32(trow + T_DP + part * 32, dp);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_tfree);
-      const int qc0 = j * CH + part * 32;
-      const uint32_t bits = j == 0 ? kbw[0] : (j == 1 ? kbw[1] : (j == 2 ? kbw[2] : kbw[3]));
-      uint32_t pkp[16], pks[16];
-      // packed fp32 pairs.  P' = P / divisor; Pd' = P' * keep (dV is rescaled
-      // by ks * divisor); dS = P' * (dPd * keep * ks - D)
-      const float2 sc2x2 = make_float2(p.sc2, p.sc2), mrow2 = make_float2(mrow, mrow), ks2 = make_float2(p.ks, p.ks);
-      float4 kf;
-      float2 csum = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        const float2 l = reinterpret_cast<const float2*>(lse_s + qc0)[i >> 1];
-        const float2 dd = reinterpret_cast<const float2*>(del_s + qc0)[i >> 1];
-        const float2 t = __ffma2_rn(make_float2(s[i], s[i + 1]), sc2x2, __fadd2_rn(mrow2, make_float2(-l.x, -l.y)));
-        const float2 P = make_float2(ex2(t.x), ex2(t.y));
-        if ((i & 3) == 0) kf = klut[(bits >> i) & 15u];
-        const float2 kk = (i & 3) ? make_float2(kf.z, kf.w) : make_float2(kf.x, kf.y);  // keep in {0, 1}
-        const float2 pd = __fmul2_rn(P, kk);
-        const float2 dpm = __fmul2_rn(make_float2(dp[i], dp[i + 1]), kk);
-        const float2 ds = __fmul2_rn(P, __ffma2_rn(dpm, ks2, make_float2(-dd.x, -dd.y)));
-        csum = __fadd2_rn(csum, ds);
-        pkp[i >> 1] = pack_bf16x2(pd.x, pd.y);
-        pks[i >> 1] = pack_bf16x2(ds.x, ds.y);
+      const bool dq_sums = p.bias_part && p.ds_store;
+      uint4 kr[2];
+      if (dq_sums) {  // this key's K row slice, for dQ's column sums below
+        const uint4* kp = reinterpret_cast<const uint4*>(p.qkv + (size_t)(t.row0 + t.k0 + rl) * p.ld_qkv + p.H +
+                                                         t.h * DH + part * 16);
+        kr[0] = __ldg(kp);
+        kr[1] = __ldg(kp + 1);
       }
-      cs += csum.x + csum.y;
-      if (j > 0) mbar_wait(bar_pdsfree, (j - 1) & 1);
-      st_row32(sbase + DkvSmem::PD, rl, part * 32, pkp);
-      st_row32(sbase + DkvSmem::DS, rl, part * 32, pks);
+      float g2[3][16];  // dK, dV rows of this thread (and dQ's bias terms)
+      tmem_ld16(trow + T_DK + part * 16, g2[0]);
+      tmem_ld16(trow + T_DV + part * 16, g2[1]);
+      const float dvs = p.ks / p.scale;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) g2[1][i] *= dvs;
+      // bf16 dK / dV strips through SW128 tiles in the (released) Pd buffer, out by TMA
+      const uint32_t tdk = sbase + KsSmem::PD, tdv = tdk + QT * 128;
+#pragma unroll
+      for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          st_sw128(tt ? tdv : tdk, rl, part * 2 + u,
+                   make_uint4(pack_bf16x2(g2[tt][8 * u], g2[tt][8 * u + 1]),
+                              pack_bf16x2(g2[tt][8 * u + 2], g2[tt][8 * u + 3]),
+                              pack_bf16x2(g2[tt][8 * u + 4], g2[tt][8 * u + 5]),
+                              pack_bf16x2(g2[tt][8 * u + 6], g2[tt][8 * u + 7])));
       fence_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_pds);
-      if (sw == 0 && lane == 0 && j < 4) ATRACE(6 + j);
-    }
-    mbar_wait(bar_pdsfree, (nch - 1) & 1);
-    if (sw == 0 && lane == 0) ATRACE(10);
-    tc_fence_after();
-    __nv_bfloat16* grow_ptr = p.dqkv + (size_t)(row0 + key) * p.ld_dqkv + h * DH + part * 16;
-    float g2[2][16];  // dK, dV rows of this thread
-    tmem_ld16(trow + T_DK + part * 16, g2[0]);
-    store_bf16x16(grow_ptr + p.H, g2[0]);
-    tmem_ld16(trow + T_DV + part * 16, g2[1]);
-    const float dvs = p.ks / p.scale;
+      named_bar(1, kSoftWarps * 32);
+      if (st == 0) {
+        tma_store_4d(&map_dkv, tdk, p.H + t.h * DH, t.row0 + t.k0, 0, 0);
+        tma_store_4d(&map_dkv, tdv, 2 * p.H + t.h * DH, t.row0 + t.k0, 0, 0);
+        bulk_commit();
+      }
+      if (p.bias_part) {  // column sums of dK, dV (and dQ) over this key strip
+        float* bp = p.bias_part + (size_t)(t.b * (S / QT) + t.k0 / QT) * 3 * p.H + t.h * DH;
+        float* red = reinterpret_cast<float*>(smem + KsSmem::RED);
+        if (p.ds_store) {
+          // dQ = dS·K comes from the GEMM over the stored dSᵀ; its column sums
+          // over this strip's keys are Σ_k cs[k] K[k][:] with cs[k] = Σ_q dS[q, k]
+          float* cs_s = reinterpret_cast<float*>(smem + KsSmem::CS);
+          cs_s[part * QT + rl] = cs;
+          named_bar(1, kSoftWarps * 32);
+          const float c = ((cs_s[rl] + cs_s[QT + rl]) + cs_s[2 * QT + rl]) + cs_s[3 * QT + rl];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) g2[1][i] *= dvs;
-    store_bf16x16(grow_ptr + 2 * p.H, g2[1]);
-    if (p.bias_part) {  // dK / dV column sums of this key strip (Pd / dS buffers and lse / D rows are free now)
-      float* bp = p.bias_part + (size_t)(b * (S / QT) + kb) * 3 * p.H + h * DH;
-      float* const stg[2] = {reinterpret_cast<float*>(smem + DkvSmem::DS), reinterpret_cast<float*>(smem + DkvSmem::PD)};
-      float* const scr[2] = {lse_s, del_s};
-      float* const dst[2] = {bp + p.H, bp + 2 * p.H};
-      tile_colsum_128x64<2>(stg, scr, rl, part * 16, g2, st, dst);
-      if (p.ds_store) {
-        // dQ = dS·K comes from the GEMM over the stored dSᵀ; its column sums
-        // over this strip's keys are Σ_k cs[k] K[k][:] with cs[k] = Σ_q dS[q, k]
-        // (the K strip is still staged: SW128 rows of 64 bf16)
-        float* cs_s = reinterpret_cast<float*>(smem + DkvSmem::CS);
-        cs_s[part * QT + rl] = cs;
-        named_bar(1, kSoftWarps * 32);
-        const int d = st & 63, grp = st >> 6;  // 8 groups of 16 keys
-        float acc = 0.f;
-#pragma unroll 4
-        for (int r = grp * 16; r < grp * 16 + 16; ++r) {
-          const float c = cs_s[r] + cs_s[QT + r] + cs_s[2 * QT + r] + cs_s[3 * QT + r];
-          const __nv_bfloat16 kv = *reinterpret_cast<const __nv_bfloat16*>(
-              smem + DkvSmem::K + r * 128 + (((d >> 3) ^ (r & 7)) << 4) + (d & 7) * 2);
-          acc = fmaf(c, __bfloat162float(kv), acc);
-        }
-        float* scr2 = lse_s;  // free after the colsum above
-        scr2[grp * 64 + d] = acc;
-        named_bar(1, kSoftWarps * 32);
-        if (st < 64) {
-          float u = 0.f;
+          for (int u = 0; u < 2; ++u) {
+            const uint32_t w4[4] = {kr[u].x, kr[u].y, kr[u].z, kr[u].w};
 #pragma unroll
-          for (int g = 0; g < 8; ++g) u += scr2[g * 64 + st];
-          bp[st] = u;
+            for (int i = 0; i < 4; ++i) {
+              g2[2][8 * u + 2 * i] = c * __uint_as_float(w4[i] << 16);
+              g2[2][8 * u + 2 * i + 1] = c * __uint_as_float(w4[i] & 0xFFFF0000u);
+            }
+          }
+          float* const dst[3] = {bp + p.H, bp + 2 * p.H, bp};
+          strip_colsum<3>(g2, lane, q, part, st, red, dst);
+        } else {
+          float* const dst[2] = {bp + p.H, bp + 2 * p.H};
+          strip_colsum<2>(reinterpret_cast<float(&)[2][16]>(g2), lane, q, part, st, red, dst);
         }
       }
+      if (st == 0) bulk_wait_read<0>();  // the dK / dV tiles are read: Pd is free for the next strip
+      named_bar(1, kSoftWarps * 32);
+      if (it < 3 && sw == 0 && lane == 0) ATRACE(10 + it);
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 64) ATRACE(15);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
@@ -1419,10 +1541,14 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   if (rc) return rc;
   rc = make_map(&mo, ctx, 2, (uint64_t)ld_ctx, (uint64_t)T, ld_ctx, 1, 0, 1, 0, 64, 64, true);
   if (rc) return rc;
+  CUtensorMap mdkv;  // dK / dV strips: [128 keys x 64] boxes of dqkv
+  rc = make_map(&mdkv, dqkv, 2, (uint64_t)ld_dqkv, (uint64_t)T, ld_dqkv, 1, 0, 1, 0, 64, 128, true);
+  if (rc) return rc;
   AttnBwdParams p;
   p.trace = nullptr;
   p.B = (int)batch; p.NH = (int)heads; p.S = (int)seq; p.H = (int)(heads * DH);
   p.ld_ctx = ld_ctx; p.ld_dqkv = ld_dqkv;
+  p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv); p.ld_qkv = ld_qkv;
   p.ctx = reinterpret_cast<const __nv_bfloat16*>(ctx);
   p.dctx = reinterpret_cast<const __nv_bfloat16*>(dctx);
   p.add_mask = add_mask; p.lse = lse;
@@ -1436,7 +1562,7 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem::TOTAL);
-    cudaFuncSetAttribute(attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvSmem::TOTAL);
+    cudaFuncSetAttribute(attn_bwd_kstrip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, KsSmem::TOTAL);
     attr = true;
   }
   const int grid = (int)(batch * heads * (seq / QT));
@@ -1455,7 +1581,8 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
     DFX_LAUNCH_CHECK("dfx_attn_bwd (delta)");
     p.ds_store = 1;
     p.trace = g_attn_trace;
-    launch_k(attn_bwd_dkdv_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, mds, p);
+    launch_k(attn_bwd_kstrip_kernel, std::min(grid, num_sms()), kKsThreads, KsSmem::TOTAL, as_stream(stream), mqkv,
+             mdo, mds, mdkv, p);
     DFX_LAUNCH_CHECK("dfx_attn_bwd (dk, dv, dS)");
     dfx_gemm_args g = dq_gemm_args(batch, heads, seq, qkv, ld_qkv, dsT, dqkv, ld_dqkv);
     g.workspace = reinterpret_cast<uint8_t*>(dsT) + attn_ds_bytes(batch, heads, seq);
@@ -1464,13 +1591,14 @@ extern "C" int dfx_attn_bwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
     return gemm_tc(g, as_stream(stream));
   }
   p.ds_store = 0;
-  // debug timeline of the dq kernel, or of dkdv with DFX_ATTN_TRACE_DKDV set (tools/attn_trace.py)
-  const bool trace_dkdv = getenv("DFX_ATTN_TRACE_DKDV") != nullptr;
-  p.trace = trace_dkdv ? nullptr : g_attn_trace;
+  // debug timeline of the dq kernel, or of kstrip with DFX_ATTN_TRACE_KSTRIP set (tools/attn_trace.py)
+  const bool trace_ks = getenv("DFX_ATTN_TRACE_KSTRIP") != nullptr;
+  p.trace = trace_ks ? nullptr : g_attn_trace;
   launch_k(attn_bwd_dq_kernel, grid, kAttnThreads, DqSmem::TOTAL, as_stream(stream), mqkv, mdo, mo, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dq)");
-  p.trace = trace_dkdv ? g_attn_trace : nullptr;
-  launch_k(attn_bwd_dkdv_kernel, grid, kAttnThreads, DkvSmem::TOTAL, as_stream(stream), mqkv, mdo, mqkv, p);
+  p.trace = trace_ks ? g_attn_trace : nullptr;
+  launch_k(attn_bwd_kstrip_kernel, std::min(grid, num_sms()), kKsThreads, KsSmem::TOTAL, as_stream(stream), mqkv, mdo,
+           mqkv, mdkv, p);
   DFX_LAUNCH_CHECK("dfx_attn_bwd (dk, dv)");
   return DFX_OK;
 }

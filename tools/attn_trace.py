@@ -35,9 +35,31 @@ else:
 for _ in range(3):
     run()
 ncta = B * NH * S // 128
-if "--dkdv" in sys.argv:  # dkdv timeline: 0 start, 1 K/V landed (MMA), 2-5 S_j ready, 6-9 Pd/dS_j stored, 10 grads done
-    os.environ["DFX_ATTN_TRACE_DKDV"] = "1"
-    sys.argv.append("--bwd")
+if "--kstrip" in sys.argv:  # persistent key-strip kernel: 0 start, 1 K/V of strip 0, 2-5 S_j of strip 0,
+    # 6-8 strip it's gradients done, 10-12 strip it's epilogue done, 15 exit
+    run()
+    dctx = torch.randn_like(ctx)
+    dqkv = torch.empty_like(qkv)
+    bwd = lambda: K.attn_bwd(qkv, ctx, dctx, B, S, NH, am, lse, kr, kc, 1 / 0.9, 0.125, dqkv)  # noqa: E731
+    for _ in range(3):
+        bwd()
+    ngrid = min(ncta, torch.cuda.get_device_properties(0).multi_processor_count)
+    tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
+    fn(tr.data_ptr())
+    bwd()
+    torch.cuda.synchronize()
+    fn(None)
+    t = tr.view(ncta, 16)[:ngrid].cpu().double()
+    rel = (t - t[:, 0].min()) / 1e3
+    names = {1: "K/V landed", 2: "S0", 3: "S1", 4: "S2", 5: "S3", 6: "grads0", 10: "epi0", 7: "grads1", 11: "epi1",
+             8: "grads2", 12: "epi2", 15: "exit"}
+    three = rel[:, 12] > 0
+    for lab, m in (("3-strip CTAs", three), ("2-strip CTAs", ~three)):
+        r = rel[m]
+        print(lab, int(m.sum()), {n: round((r[:, i] - r[:, 0]).mean().item(), 2) for i, n in names.items()
+                                  if (r[:, i] > 0).all()})
+    print("kernel span", round(rel[:, 15].max().item(), 2), "start spread", round(rel[:, 0].max().item(), 2))
+    sys.exit(0)
 if "--fwd2" in sys.argv:  # online-softmax forward: 0 start, 1 Q landed, 2-5 S_j ready, 6-9 P_j stored, 10 O done, 11 exit
     tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
     fn(tr.data_ptr())

@@ -117,7 +117,7 @@ def main():
             elif "attn_bwd" in d["name"]:
                 tr["bwd.attention"] = tr.get("bwd.attention", 0.0) + dram(d)
                 # the dQ GEMM over the stored dSᵀ follows the key-strip kernel in the same call
-                if "dkdv" in d["name"] and i + 1 < len(step) and "tc_gemm_kernel<64" in step[i + 1]["name"]:
+                if "kstrip" in d["name"] and i + 1 < len(step) and "tc_gemm_kernel<64" in step[i + 1]["name"]:
                     tr["bwd.attention"] += dram(step[i + 1])
         tr["source"] = "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (tools/reconcile_bytes.py)"
         json.dump(tr, open(a.traffic_out, "w"), indent=1)
