@@ -1072,7 +1072,8 @@ struct KsSmem {
   static constexpr int LUT = ROWS + 2 * ROWB;
   static constexpr int CS = LUT + 16 * 16;           // [4][128] per-part Σ_q dS
   static constexpr int RED = CS + 4 * QT * 4;        // [3][4][64] column-sum quarters
-  static constexpr int BAR = RED + 3 * 4 * 64 * 4;
+  static constexpr int KROW = RED + 3 * 4 * 64 * 4;  // the strip's K rows (SW128), kept for dQ's column sums
+  static constexpr int BAR = KROW + QT * 128;
   static constexpr int TOTAL = BAR + 256 + KB;
 };
 static_assert(KsSmem::TOTAL <= 227 * 1024, "attention key-strip kernel exceeds shared memory");
@@ -1113,7 +1114,7 @@ attn_bwd_kstrip_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid
     mbar_init(bar_tfree, kSoftWarps);
     mbar_init(bar_pds, kSoftWarps);
     mbar_init(bar_pdsfree, 1);
-    mbar_init(kv_free, 1);  // the strip's last Sᵀ / dPdᵀ MMAs completed
+    mbar_init(kv_free, kSoftWarps);  // every softmax warp saw the strip's last Sᵀ / dPdᵀ (and copied its K rows)
     mbar_init(ds_free, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_rows[b], 1);
@@ -1215,7 +1216,6 @@ attn_bwd_kstrip_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid
             tc_mma_cg<1>(tmem + T_DP, vdesc + 2 * kk, dodesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
           }
           tc_commit_cg<1>(bar_s);
-          if (j == nch - 1) tc_commit_cg<1>(kv_free);  // K / V read once these complete
           if (j > 0) issue_grads(J - 1, j - 1);
         }
         // the strip's last gradients before the next strip's first Sᵀ / dPdᵀ,
@@ -1269,6 +1269,18 @@ attn_bwd_kstrip_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid
         if (kbp && j + 1 < nch) bits_n = __ldg(kbp + 4 * (j + 1));
         mbar_wait(bar_s, J & 1);
         if (it == 0 && sw == 0 && lane == 0 && j < 4) ATRACE(2 + j);
+        if (j == nch - 1) {  // the strip's last Sᵀ / dPdᵀ are done: K / V are free once K's rows are kept
+          if (p.bias_part && p.ds_store) {
+            mbar_wait(bar_kv, it & 1);  // (observed by this thread too: the TMA writes are visible to it)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int off = rl * 128 + (((part * 2 + u) ^ (rl & 7)) << 4);
+              sts128(sbase + KsSmem::KROW + off, *reinterpret_cast<const uint4*>(smem + KsSmem::K + off));
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(kv_free);
+        }
         tc_fence_after();
         float sv[32], dp[32];
         tmem_ld32(trow + T_S + part * 32, sv);
@@ -1311,19 +1323,33 @@ attn_bwd_kstrip_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_pds);
       }
-      // ---- epilogue: the strip's gradient MMAs are done once the last chunk's Pd / dS are released
+      // ---- epilogue
+      float g2[3][16];  // dK, dV rows of this thread (and dQ's bias terms)
+      const bool dq_sums = p.bias_part && p.ds_store;
+      if (dq_sums) {
+        // dQ = dS·K comes from the GEMM over the stored dSᵀ; its column sums
+        // over this strip's keys are Σ_k cs[k] K[k][:] with cs[k] = Σ_q dS[q, k]
+        // (prepared while the last gradient MMAs run)
+        float* cs_s = reinterpret_cast<float*>(smem + KsSmem::CS);
+        cs_s[part * QT + rl] = cs;
+        named_bar(1, kSoftWarps * 32);
+        const float c = ((cs_s[rl] + cs_s[QT + rl]) + cs_s[2 * QT + rl]) + cs_s[3 * QT + rl];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint4 kv = *reinterpret_cast<const uint4*>(smem + KsSmem::KROW + rl * 128 +
+                                                            (((part * 2 + u) ^ (rl & 7)) << 4));
+          const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            g2[2][8 * u + 2 * i] = c * __uint_as_float(w4[i] << 16);
+            g2[2][8 * u + 2 * i + 1] = c * __uint_as_float(w4[i] & 0xFFFF0000u);
+          }
+        }
+      }
+      // the strip's gradient MMAs are done once the last chunk's Pd / dS are released
       mbar_wait(bar_pdsfree, (J - 1) & 1);
       if (it < 3 && sw == 0 && lane == 0) ATRACE(6 + it);
       tc_fence_after();
-      const bool dq_sums = p.bias_part && p.ds_store;
-      uint4 kr[2];
-      if (dq_sums) {  // this key's K row slice, for dQ's column sums below
-        const uint4* kp = reinterpret_cast<const uint4*>(p.qkv + (size_t)(t.row0 + t.k0 + rl) * p.ld_qkv + p.H +
-                                                         t.h * DH + part * 16);
-        kr[0] = __ldg(kp);
-        kr[1] = __ldg(kp + 1);
-      }
-      float g2[3][16];  // dK, dV rows of this thread (and dQ's bias terms)
       tmem_ld16(trow + T_DK + part * 16, g2[0]);
       tmem_ld16(trow + T_DV + part * 16, g2[1]);
       const float dvs = p.ks / p.scale;
@@ -1351,21 +1377,6 @@ attn_bwd_kstrip_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid
         float* bp = p.bias_part + (size_t)(t.b * (S / QT) + t.k0 / QT) * 3 * p.H + t.h * DH;
         float* red = reinterpret_cast<float*>(smem + KsSmem::RED);
         if (p.ds_store) {
-          // dQ = dS·K comes from the GEMM over the stored dSᵀ; its column sums
-          // over this strip's keys are Σ_k cs[k] K[k][:] with cs[k] = Σ_q dS[q, k]
-          float* cs_s = reinterpret_cast<float*>(smem + KsSmem::CS);
-          cs_s[part * QT + rl] = cs;
-          named_bar(1, kSoftWarps * 32);
-          const float c = ((cs_s[rl] + cs_s[QT + rl]) + cs_s[2 * QT + rl]) + cs_s[3 * QT + rl];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const uint32_t w4[4] = {kr[u].x, kr[u].y, kr[u].z, kr[u].w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              g2[2][8 * u + 2 * i] = c * __uint_as_float(w4[i] << 16);
-              g2[2][8 * u + 2 * i + 1] = c * __uint_as_float(w4[i] & 0xFFFF0000u);
-            }
-          }
           float* const dst[3] = {bp + p.H, bp + 2 * p.H, bp};
           strip_colsum<3>(g2, lane, q, part, st, red, dst);
         } else {
