@@ -11,16 +11,17 @@
 // per-query-row map (SURVEY.md §3D kernel 4, §8f.1); here the [B,NH,S,S]
 // score / probability tensors never touch HBM.
 //
-// One CTA owns a 128-row strip (128 TMEM lanes) against all S <= 512 keys:
-// the whole fp32 score strip fits the 512 TMEM columns, so the softmax is
-// exact (two passes over TMEM: row max, then exp/sum) instead of online.
-// Warp roles (576 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
-// single-thread tcgen05.mma issuer, warps 2..17 = 16 softmax warps (four per
-// TMEM lane quadrant, each owning S/4 columns).
+// Work unit: a 128-row strip (128 TMEM lanes) of one (batch, head) against
+// all S <= 512 keys.  Warp roles (576 threads): warp 0 = TMA producer, warp 1
+// = TMEM allocator + single-thread tcgen05.mma issuer, warps 2..17 = 16
+// softmax warps (four per TMEM lane quadrant).  The default forward and
+// key-strip backward are persistent: one CTA per SM walks the strips.
 //
-//   fwd    S = Q·Kᵀ (TMEM) -> P̃d = exp2(S·c·log2e + mask·log2e - max)·keep·ks
-//          written as bf16 into 128B-swizzled smem (UMMA K-major A operand)
-//          -> O = P̃d·V (TMEM, reusing S's columns) -> ctx = O / rowsum.
+//   fwd3   per 128-query strip, 128-key chunks: S = Q·Kᵀ (TMEM, double
+//          buffered) -> online softmax, P̃d = exp2(S·c·log2e + mask·log2e -
+//          m)·keep as bf16 in TMEM (the A operand of the PV MMA) -> O += P̃d·V
+//          -> ctx = O·ks / rowsum.  (fwd, DFX_ATTN_FWD_LEGACY: the r01 exact
+//          two-pass softmax over the whole 512-column score strip in TMEM.)
 //          Also writes lse (log2 domain) and the dropout keep flags packed to
 //          bits twice: row-major (for dQ) and transposed (for dK/dV, built
 //          with warp ballots) — 2 x 3.1 MB instead of re-reading 25 MB of u8
@@ -403,65 +404,81 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams
   }
 }
 
-// ------------------------------------------------- forward, online softmax
-// CTA = (b, h, 128-query strip) as before, but TWO CTAs per SM: 256 TMEM
-// columns each (S chunk 128 | P 64 | O 64) and ~90 KB of shared memory, so one
-// CTA's exp pass overlaps the other's loads, MMAs and epilogue.  Per 128-key
-// chunk j: S = Q·K_jᵀ (TMEM) -> online softmax with a lazily rescaled
-// reference max (the O accumulator and the row sum are rescaled only when the
-// chunk max exceeds the reference by more than 2^8, so P = exp2(t - m) <= 256
-// always fits bf16) -> P̃d = P∘keep written to TMEM as bf16 (tcgen05.st) ->
-// O += P̃d·V_j with the A operand read from TMEM.  Eight softmax warps, two
-// per TMEM lane quadrant, 64 key columns each.
-constexpr int kF2Soft = 8;
-constexpr int kF2Threads = (2 + kF2Soft) * 32;
-
-struct F2Smem {
-  static constexpr int Q = 0;
-  static constexpr int NST = 2;
+// ------------------------------------------ persistent forward, online softmax
+// One CTA per SM walks the (b, h, 128-query) strips blockIdx.x, + grid, ...
+// (384 strips at C2 are 1.3 waves of two-per-SM CTAs: the last 88 ran alone).
+// Sixteen softmax warps, four per TMEM lane quadrant, 32 key columns each of a
+// 128-key chunk; S is double-buffered in TMEM so the next chunk's Q·Kᵀ runs
+// under this chunk's exp pass, and P̃d (bf16, the A operand of the PV MMA read
+// from TMEM) is double-buffered so the exp pass of chunk j + 1 overlaps
+// PV_j.  Online softmax with a lazily rescaled reference max: the O
+// accumulator and the row sum are rescaled only when a chunk max exceeds the
+// reference by more than 2^8, so P = exp2(t - m) <= 256 always fits bf16 (the
+// rescale branch is warp-uniform: tcgen05.ld/st are .sync.aligned).  The row
+// max of a chunk meets over the four warps of a lane quadrant only.  Q and the
+// key-mask row are double-buffered per strip; ctx leaves by TMA from a bf16
+// staging tile.  TMEM: S0 | S1 | P0 | P1 | O.
+struct F3Smem {
+  static constexpr int Q = 0;                        // two strip buffers
+  static constexpr int NST = 3;
   static constexpr int STAGE = 2 * 128 * 128;        // K_j | V_j
-  static constexpr int RING = Q + QT * 128;
-  static constexpr int MASK = RING + NST * STAGE;   // S floats
-  static constexpr int RED = MASK + kMaxSeq * 4;    // [2][128] chunk max, [2][128] row sum
-  static constexpr int LUT = RED + 4 * QT * 4;      // keep byte -> 4 bf16-pair AND masks
+  static constexpr int RING = Q + 2 * QT * 128;
+  static constexpr int MASK = RING + NST * STAGE;    // two strip buffers of S floats (log2 domain)
+  static constexpr int RED = MASK + 2 * kMaxSeq * 4; // [2 chunk parities][4 parts][128] chunk max
+  static constexpr int SUM = RED + 2 * 4 * QT * 4;   // [4][128] row sums
+  static constexpr int OST = SUM + 4 * QT * 4;       // ctx staging tile [128 x 64] bf16 SW128
+  static constexpr int LUT = OST + QT * 128;         // keep byte -> 4 bf16-pair AND masks
   static constexpr int BAR = LUT + 256 * 16;
-  static constexpr int TOTAL = BAR + 128 + KB;
+  static constexpr int TOTAL = BAR + 256 + KB;
 };
-static_assert(2 * F2Smem::TOTAL <= 228 * 1024 - 2 * KB, "two forward CTAs must fit one SM");
+static_assert(F3Smem::TOTAL <= 227 * 1024, "persistent forward exceeds shared memory");
 
-__global__ void __launch_bounds__(kF2Threads, 2)
-attn_fwd2_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParams p) {
+__global__ void __launch_bounds__(kAttnThreads, 1)
+attn_fwd3_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_ctx,
+                 const AttnFwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + F2Smem::BAR);
-  uint64_t *bar_q = bar, *bar_s = bar + 1, *bar_sfree = bar + 2, *bar_p = bar + 3, *bar_pv = bar + 4;
-  uint64_t* full = bar + 5;   // [NST]
-  uint64_t* empty = bar + 7;  // [NST]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
-  float* mask2 = reinterpret_cast<float*>(smem + F2Smem::MASK);
-  float* red_max = reinterpret_cast<float*>(smem + F2Smem::RED);
-  float* red_sum = red_max + 2 * QT;
-  constexpr int NST = F2Smem::NST;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + F3Smem::BAR);
+  uint64_t* bar_q = bar;            // [2] Q of the strip (parity it & 1) landed
+  uint64_t* q_free = bar + 2;       // [2] its last Q·Kᵀ completed
+  uint64_t* bar_m = bar + 4;        // [2] key-mask row landed
+  uint64_t* m_free = bar + 6;       // [2] its last read
+  uint64_t* bar_s = bar + 8;        // [2] S_J in buffer J & 1
+  uint64_t* bar_sfree = bar + 10;   // [2] S_J read
+  uint64_t* bar_p = bar + 12;       // [2] P̃d_J written
+  uint64_t* bar_pv = bar + 14;      // [2] PV_J completed
+  uint64_t* full = bar + 16;        // [NST]
+  uint64_t* empty = bar + 19;       // [NST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 22);
+  constexpr int NST = F3Smem::NST;
+  float* red_max = reinterpret_cast<float*>(smem + F3Smem::RED);
+  float* red_sum = reinterpret_cast<float*>(smem + F3Smem::SUM);
 
   const int S = p.S, nch = S / 128;
-  const int qb = blockIdx.x % nch;
-  const int bh = blockIdx.x / nch;
-  const int b = bh / p.NH, h = bh % p.NH;
-  const int q0 = qb * QT, row0 = b * S;
+  const int nstrips = p.B * p.NH * (S / QT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto strip = [&](int sidx, int& bh, int& b, int& h, int& q0) {
+    const int nqb = S / QT;
+    bh = sidx / nqb; q0 = (sidx % nqb) * QT; b = bh / p.NH; h = bh % p.NH;
+  };
 
   if (threadIdx.x == 0) {
-    mbar_init(bar_q, 1);
-    mbar_init(bar_s, 1);
-    mbar_init(bar_sfree, kF2Soft);
-    mbar_init(bar_p, kF2Soft);
-    mbar_init(bar_pv, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_q[i], 1);
+      mbar_init(&q_free[i], 1);
+      mbar_init(&bar_m[i], 1);
+      mbar_init(&m_free[i], kSoftWarps);
+      mbar_init(&bar_s[i], 1);
+      mbar_init(&bar_sfree[i], kSoftWarps);
+      mbar_init(&bar_p[i], kSoftWarps);
+      mbar_init(&bar_pv[i], 1);
+    }
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -474,24 +491,36 @@ attn_fwd2_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParam
   pdl_trigger();
   pdl_wait();
   if (threadIdx.x == 64) ATRACE(0);
-  constexpr uint32_t T_S = 0, T_P = 128, T_O = 192;
+  constexpr uint32_t T_P = 256, T_O = 384;  // S_J at 128 (J & 1); P̃d_J at T_P + 64 (J & 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(bar_q, QT * 128);
-      const uint32_t bq = smem_u32(bar_q);
-      for (int u = 0; u < 2; ++u)
-        tma_load_4d_cg<1>(&map_qkv, bq, smem + F2Smem::Q + u * 8 * KB, h * DH, row0 + q0 + 64 * u, 0, 0);
-      for (int j = 0; j < nch; ++j) {
-        const int s = j % NST;
-        mbar_wait(&empty[s], ((j / NST) & 1) ^ 1);
-        mbar_expect_tx(&full[s], F2Smem::STAGE);
-        const uint32_t bf = smem_u32(&full[s]);
-        uint8_t* stg = smem + F2Smem::RING + s * F2Smem::STAGE;
-        for (int u = 0; u < 2; ++u) {
-          tma_load_4d_cg<1>(&map_qkv, bf, stg + u * 8 * KB, p.H + h * DH, row0 + j * 128 + 64 * u, 0, 0);
-          tma_load_4d_cg<1>(&map_qkv, bf, stg + 16 * KB + u * 8 * KB, 2 * p.H + h * DH, row0 + j * 128 + 64 * u, 0,
-                            0);
+      int J = 0, it = 0;
+      for (int sidx = blockIdx.x; sidx < nstrips; sidx += gridDim.x, ++it) {
+        int bh, b, h, q0;
+        strip(sidx, bh, b, h, q0);
+        const int qb = it & 1;
+        if (it >= 2) mbar_wait(&q_free[qb], ((it - 2) >> 1) & 1);
+        mbar_expect_tx(&bar_q[qb], QT * 128);
+        for (int u = 0; u < 2; ++u)
+          tma_load_4d_cg<1>(&map_qkv, smem_u32(&bar_q[qb]), smem + F3Smem::Q + qb * QT * 128 + u * 8 * KB, h * DH,
+                            b * S + q0 + 64 * u, 0, 0);
+        if (p.add_mask) {
+          if (it >= 2) mbar_wait(&m_free[qb], ((it - 2) >> 1) & 1);
+          mbar_expect_tx(&bar_m[qb], S * 4);
+          bulk_g2s(smem + F3Smem::MASK + qb * kMaxSeq * 4, p.add_mask + (size_t)b * S, S * 4, smem_u32(&bar_m[qb]));
+        }
+        for (int j = 0; j < nch; ++j, ++J) {
+          const int s = J % NST;
+          mbar_wait(&empty[s], ((J / NST) & 1) ^ 1);
+          mbar_expect_tx(&full[s], F3Smem::STAGE);
+          const uint32_t bf = smem_u32(&full[s]);
+          uint8_t* stg = smem + F3Smem::RING + s * F3Smem::STAGE;
+          for (int u = 0; u < 2; ++u) {
+            tma_load_4d_cg<1>(&map_qkv, bf, stg + u * 8 * KB, p.H + h * DH, b * S + j * 128 + 64 * u, 0, 0);
+            tma_load_4d_cg<1>(&map_qkv, bf, stg + 16 * KB + u * 8 * KB, 2 * p.H + h * DH, b * S + j * 128 + 64 * u,
+                              0, 0);
+          }
         }
       }
     }
@@ -499,191 +528,204 @@ attn_fwd2_kernel(const __grid_constant__ CUtensorMap map_qkv, const AttnFwdParam
     if (lane == 0) {
       const uint32_t idesc_s = make_idesc(128, QT, 0, 0);
       const uint32_t idesc_o = make_idesc(DH, QT, 0, 1);  // A = P̃d from TMEM, B = V_j MN-major
-      const uint64_t qdesc = make_sdesc(sbase + F2Smem::Q, 16, 1024);
-      mbar_wait(bar_q, 0);
-      ATRACE(1);
-      auto issue_pv = [&](int c) {
-        mbar_wait(bar_p, c & 1);
+      auto issue_pv = [&](int J, int j) {
+        mbar_wait(&bar_p[J & 1], (J >> 1) & 1);
         tc_fence_after();
-        const uint32_t stg = sbase + F2Smem::RING + (c % NST) * F2Smem::STAGE;
+        const uint32_t stg = sbase + F3Smem::RING + (J % NST) * F3Smem::STAGE;
         const uint64_t vdesc = make_sdesc(stg + 16 * KB, 8 * KB, 1024);
+        const uint32_t tp = tmem + T_P + 64 * (J & 1);
 #pragma unroll
         for (int kc = 0; kc < 8; ++kc)
-          tc_mma_ts(tmem + T_O, tmem + T_P + kc * 8, vdesc + (uint64_t)(kc * (2048 >> 4)), idesc_o,
-                    (c > 0 || kc > 0) ? 1u : 0u);
-        tc_commit_cg<1>(&empty[c % NST]);
-        tc_commit_cg<1>(bar_pv);
+          tc_mma_ts(tmem + T_O, tp + kc * 8, vdesc + (uint64_t)(kc * (2048 >> 4)), idesc_o, (j > 0 || kc > 0) ? 1u : 0u);
+        tc_commit_cg<1>(&empty[J % NST]);
+        tc_commit_cg<1>(&bar_pv[J & 1]);
       };
-      for (int j = 0; j < nch; ++j) {
-        mbar_wait(&full[j % NST], (j / NST) & 1);
-        if (j > 0) mbar_wait(bar_sfree, (j - 1) & 1);
-        tc_fence_after();
-        const uint32_t stg = sbase + F2Smem::RING + (j % NST) * F2Smem::STAGE;
-        const uint64_t kdesc = make_sdesc(stg, 16, 1024);
+      int J = 0, it = 0;
+      for (int sidx = blockIdx.x; sidx < nstrips; sidx += gridDim.x, ++it) {
+        const int qb = it & 1;
+        mbar_wait(&bar_q[qb], (it >> 1) & 1);
+        if (it == 0) ATRACE(1);
+        const uint64_t qdesc = make_sdesc(sbase + F3Smem::Q + qb * QT * 128, 16, 1024);
+        for (int j = 0; j < nch; ++j, ++J) {
+          mbar_wait(&full[J % NST], (J / NST) & 1);
+          if (J >= 2) mbar_wait(&bar_sfree[J & 1], ((J - 2) >> 1) & 1);
+          tc_fence_after();
+          const uint32_t stg = sbase + F3Smem::RING + (J % NST) * F3Smem::STAGE;
+          const uint64_t kdesc = make_sdesc(stg, 16, 1024);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          tc_mma_cg<1>(tmem + T_S, qdesc + 2 * kk, kdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
-        tc_commit_cg<1>(bar_s);
-        if (j > 0) issue_pv(j - 1);
+          for (int kk = 0; kk < DH / 16; ++kk)
+            tc_mma_cg<1>(tmem + 128 * (J & 1), qdesc + 2 * kk, kdesc + 2 * kk, idesc_s, kk > 0 ? 1u : 0u);
+          tc_commit_cg<1>(&bar_s[J & 1]);
+          if (j == nch - 1) tc_commit_cg<1>(&q_free[qb]);
+          if (j > 0) issue_pv(J - 1, j - 1);
+        }
+        // the strip's last PV before the next strip's first Q·Kᵀ (which waits for its Q)
+        issue_pv(J - 1, nch - 1);
       }
-      issue_pv(nch - 1);
     }
   } else {
     // -------------------------------------------------------------- softmax
-    const int sw = warp - 2, qd = warp & 3, hf = sw >> 2;  // hf: key columns [64 hf, 64 hf + 64) of a chunk
-    const int rl = qd * 32 + lane, grow = q0 + rl;
-    const int st = threadIdx.x - 64;                        // 0..255
-    for (int i = st; i < S; i += kF2Soft * 32) mask2[i] = p.add_mask ? p.add_mask[(size_t)b * S + i] * kLog2e : 0.f;
-    uint4* klut = reinterpret_cast<uint4*>(smem + F2Smem::LUT);
-    {
+    const int sw = warp - 2, qd = warp & 3, part = sw >> 2;  // part: key columns [32 part, 32 part + 32) of a chunk
+    const int rl = qd * 32 + lane;
+    const int st = threadIdx.x - 64;  // 0..511
+    uint4* klut = reinterpret_cast<uint4*>(smem + F3Smem::LUT);
+    if (st < 256) {
       uint32_t m[4];
 #pragma unroll
       for (int w = 0; w < 4; ++w)
         m[w] = (((st >> (2 * w)) & 1) ? 0x0000FFFFu : 0u) | (((st >> (2 * w + 1)) & 1) ? 0xFFFF0000u : 0u);
       klut[st] = make_uint4(m[0], m[1], m[2], m[3]);
     }
-    named_bar(1, kF2Soft * 32);
+    named_bar(1, kSoftWarps * 32);
     const int words = S / 32;
-    const size_t rowi = (size_t)bh * S + grow;
     const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
-    float mref = 0.f, lsum = 0.f;  // reference max (log2 domain) and this thread's partial row sum
-    for (int j = 0; j < nch; ++j) {
-      const int col = j * 128 + hf * 64;  // first key column of this thread's slice
-      // keep flags of the slice: 2 words of 32 columns
-      uint32_t kw[2];
-      uint4 kv[4];
-      if (p.kb_in) {
-        kw[0] = __ldg(p.kb_row + rowi * words + (col >> 5));
-        kw[1] = __ldg(p.kb_row + rowi * words + (col >> 5) + 1);
-      } else if (p.keep) {
-        const uint4* kp = reinterpret_cast<const uint4*>(p.keep + rowi * S + col);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) kv[u] = __ldg(kp + u);
-      }
-      mbar_wait(bar_s, j & 1);
-      if (sw == 0 && lane == 0 && j < 4) ATRACE(2 + j);
-      tc_fence_after();
-      const float4* mask4 = reinterpret_cast<const float4*>(mask2 + col);
-      const float2 sc2x2 = make_float2(p.sc2, p.sc2);
-      // pass A: chunk max of t = s*c + mask over this thread's 64 columns
-      float mx = -INFINITY;
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
+    const float2 sc2x2 = make_float2(p.sc2, p.sc2);
+    int J = 0, it = 0;
+    for (int sidx = blockIdx.x; sidx < nstrips; sidx += gridDim.x, ++it) {
+      int bh, b, h, q0;
+      strip(sidx, bh, b, h, q0);
+      const int qb = it & 1;
+      const int grow = q0 + rl;
+      const size_t rowi = (size_t)bh * S + grow;
+      const float* mask2 = reinterpret_cast<const float*>(smem + F3Smem::MASK + qb * kMaxSeq * 4);
+      if (p.add_mask) mbar_wait(&bar_m[qb], (it >> 1) & 1);
+      float mref = 0.f, lsum = 0.f;  // reference max (log2 domain) and this thread's partial row sum
+      // packed keep words one chunk ahead (their latency stays off the exp pass)
+      uint32_t kw_n = p.kb_in ? __ldg(p.kb_row + rowi * words + part) : 0xFFFFFFFFu;
+      for (int j = 0; j < nch; ++j, ++J) {
+        const int col = j * 128 + part * 32;  // first key column of this thread's slice
+        const uint32_t kw = kw_n;
+        if (p.kb_in && j + 1 < nch) kw_n = __ldg(p.kb_row + rowi * words + 4 * (j + 1) + part);
+        uint4 kv[2];
+        if (p.keep) {
+          const uint4* kp = reinterpret_cast<const uint4*>(p.keep + rowi * S + col);
+          kv[0] = __ldg(kp);
+          kv[1] = __ldg(kp + 1);
+        }
+        mbar_wait(&bar_s[J & 1], (J >> 1) & 1);
+        if (it == 0 && sw == 0 && lane == 0 && j < 4) ATRACE(2 + j);
+        tc_fence_after();
         float t[32];
-        tmem_ld32(trow + T_S + hf * 64 + 32 * hh, t);
+        tmem_ld32(trow + 128 * (J & 1) + part * 32, t);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_sfree[J & 1]);  // S_J is in registers
+        // t = s * c + mask (log2 domain), and its max over the slice
+        const float4* mask4 = reinterpret_cast<const float4*>(mask2 + col);
+        float mx = -INFINITY;
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
-          const float4 m = mask4[(32 * hh + i) >> 2];
+          const float4 m = p.add_mask ? mask4[i >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
           const float2 a = __ffma2_rn(make_float2(t[i], t[i + 1]), sc2x2, make_float2(m.x, m.y));
           const float2 c2 = __ffma2_rn(make_float2(t[i + 2], t[i + 3]), sc2x2, make_float2(m.z, m.w));
+          t[i] = a.x; t[i + 1] = a.y; t[i + 2] = c2.x; t[i + 3] = c2.y;
           mx = fmax3(mx, fmaxf(a.x, a.y), fmaxf(c2.x, c2.y));
         }
-      }
-      red_max[hf * QT + rl] = mx;
-      named_bar(1, kF2Soft * 32);
-      const float cmax = fmaxf(red_max[rl], red_max[QT + rl]);
-      if (j == 0) {
-        mref = cmax;
-      } else if (__any_sync(0xffffffffu, cmax > mref + 8.f)) {
-        // rare: a row's reference max moves up; O (after PV_{j-1}) and the row
-        // sum rescale.  The TMEM load / store are warp-collective (.sync.aligned):
-        // the whole warp takes this branch (a lane-divergent tcgen05.ld hung the
-        // GPU), rows that keep their max use f = 1
-        const bool up = cmax > mref + 8.f;
-        const float f = up ? ex2(mref - cmax) : 1.f;
-        mbar_wait(bar_pv, (j - 1) & 1);
-        tc_fence_after();
-        float o[32];
-        tmem_ld32(trow + T_O + hf * 32, o);
-        uint32_t ou[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) ou[i] = __float_as_uint(o[i] * f);
-        tmem_st32(trow + T_O + hf * 32, ou);
-        tmem_wait_st();
-        lsum *= f;
-        if (up) mref = cmax;
-      }
-      // pass B: P = exp2(t - mref), P̃d = P ∘ keep -> bf16 pairs -> TMEM (A of the PV MMA)
-      const float2 nm2 = make_float2(-mref, -mref);
-      float2 sacc = make_float2(0.f, 0.f);
-      uint32_t bits[2] = {0u, 0u};
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        float t[32];
-        tmem_ld32(trow + T_S + hf * 64 + 32 * hh, t);
-        if (hh == 1) {  // S buffer free for the next chunk's MMA
-          tc_fence_before();
+        // the row's max over the four parts: only the quadrant's four warps meet
+        float* rm = red_max + (J & 1) * 4 * QT;
+        rm[part * QT + rl] = mx;
+        named_bar(2 + qd, 4 * 32);
+        const float cmax = fmaxf(fmaxf(rm[rl], rm[QT + rl]), fmaxf(rm[2 * QT + rl], rm[3 * QT + rl]));
+        if (j == nch - 1 && p.add_mask) {  // the strip's mask row is no longer read
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar_sfree);
+          if (lane == 0) mbar_arrive(&m_free[qb]);
         }
+        if (j == 0) {
+          mref = cmax;
+        } else if (__any_sync(0xffffffffu, cmax > mref + 8.f)) {
+          // rare: a row's reference max moves up; O (after PV_{J-1}) and the
+          // row sum rescale (warp-uniform branch: tcgen05.ld/st are .sync.aligned)
+          const bool up = cmax > mref + 8.f;
+          const float f = up ? ex2(mref - cmax) : 1.f;
+          mbar_wait(&bar_pv[(J - 1) & 1], ((J - 1) >> 1) & 1);
+          tc_fence_after();
+          float o[16];
+          tmem_ld16(trow + T_O + part * 16, o);
+          uint32_t ou[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) ou[i] = __float_as_uint(o[i] * f);
+          tmem_st16(trow + T_O + part * 16, ou);
+          tmem_wait_st();
+          lsum *= f;
+          if (up) mref = cmax;
+        }
+        // P = exp2(t - mref); P̃d = P ∘ keep -> bf16 pairs -> TMEM (A of the PV MMA)
+        float2 sacc = make_float2(0.f, 0.f);
+        uint32_t bits = 0u;
         uint32_t pk[16];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {  // 4 columns per step
-          const int uu = 8 * hh + u;
-          const float4 m = mask4[uu];
-          const float2 ta = __ffma2_rn(make_float2(t[4 * u], t[4 * u + 1]), sc2x2, __fadd2_rn(make_float2(m.x, m.y), nm2));
-          const float2 tb = __ffma2_rn(make_float2(t[4 * u + 2], t[4 * u + 3]), sc2x2, __fadd2_rn(make_float2(m.z, m.w), nm2));
-          const float e0 = ex2(ta.x), e1 = ex2(ta.y), e2 = ex2(tb.x), e3 = ex2(tb.y);
+          const float e0 = ex2(t[4 * u] - mref), e1 = ex2(t[4 * u + 1] - mref);
+          const float e2 = ex2(t[4 * u + 2] - mref), e3 = ex2(t[4 * u + 3] - mref);
           sacc = __fadd2_rn(sacc, __fadd2_rn(make_float2(e0, e1), make_float2(e2, e3)));
           uint32_t m0 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu;
           if (p.kb_in) {
-            const uint4 lm = klut[(kw[hh] >> (8 * (u >> 1))) & 0xFFu];
+            const uint4 lm = klut[(kw >> (8 * (u >> 1))) & 0xFFu];
             m0 = (u & 1) ? lm.z : lm.x;
             m1 = (u & 1) ? lm.w : lm.y;
           } else if (p.keep) {
-            const uint4 q4 = kv[uu >> 2];
-            const uint32_t w = (uu & 3) == 0 ? q4.x : ((uu & 3) == 1 ? q4.y : ((uu & 3) == 2 ? q4.z : q4.w));
+            const uint4 q4 = kv[u >> 2];
+            const uint32_t w = (u & 3) == 0 ? q4.x : ((u & 3) == 1 ? q4.y : ((u & 3) == 2 ? q4.z : q4.w));
             const uint32_t ff = w * 0xFFu;
             m0 = __byte_perm(ff, 0, 0x1100);
             m1 = __byte_perm(ff, 0, 0x3322);
-            bits[hh] |= keep_nibble(w) << (4 * u);
+            bits |= keep_nibble(w) << (4 * u);
           }
           pk[2 * u] = pack_bf16x2(e0, e1) & m0;
           pk[2 * u + 1] = pack_bf16x2(e2, e3) & m1;
         }
-        if (hh == 0 && j > 0) mbar_wait(bar_pv, (j - 1) & 1);  // P buffer free once PV_{j-1} read it
+        lsum += sacc.x + sacc.y;
+        if (J >= 2) mbar_wait(&bar_pv[J & 1], ((J - 2) >> 1) & 1);  // P buffer J & 1 free once PV_{J-2} read it
         tc_fence_after();
-        tmem_st16(trow + T_P + hf * 32 + 16 * hh, pk);
-      }
-      lsum += sacc.x + sacc.y;
-      if (p.kb_in) { bits[0] = kw[0]; bits[1] = kw[1]; }
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_p);
-      if (sw == 0 && lane == 0 && j < 4) ATRACE(6 + j);
-      if (p.kb_col) {
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-          if (!p.kb_in) p.kb_row[rowi * words + (col >> 5) + w] = bits[w];
-          const uint32_t colword = warp_transpose32(bits[w], lane);
-          p.kb_col[((size_t)bh * S + col + 32 * w + lane) * words + (grow >> 5)] = colword;
+        tmem_st16(trow + T_P + 64 * (J & 1) + part * 16, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_p[J & 1]);
+        if (it == 0 && sw == 0 && lane == 0 && j < 4) ATRACE(6 + j);
+        if (p.kb_col) {
+          if (p.kb_in) bits = kw;
+          else p.kb_row[rowi * words + (col >> 5)] = bits;
+          const uint32_t colword = warp_transpose32(bits, lane);
+          p.kb_col[((size_t)bh * S + col + lane) * words + (grow >> 5)] = colword;
         }
       }
+      // ---- epilogue: ctx = O / rowsum, lse
+      if (st == 0) bulk_wait_read<0>();  // the previous strip's ctx tile left the staging buffer
+      red_sum[part * QT + rl] = lsum;
+      named_bar(1, kSoftWarps * 32);
+      const float tot = ((red_sum[rl] + red_sum[QT + rl]) + red_sum[2 * QT + rl]) + red_sum[3 * QT + rl];
+      if (part == 0) p.lse[rowi] = mref + __log2f(tot);
+      const float inv = p.ks / tot;
+      mbar_wait(&bar_pv[(J - 1) & 1], ((J - 1) >> 1) & 1);  // O complete
+      if (it < 3 && sw == 0 && lane == 0) ATRACE(10 + it);
+      tc_fence_after();
+      float o[16];
+      tmem_ld16(trow + T_O + part * 16, o);
+      const uint32_t ost = sbase + F3Smem::OST;
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        st_sw128(ost, rl, part * 2 + u,
+                 make_uint4(pack_bf16x2(o[8 * u] * inv, o[8 * u + 1] * inv),
+                            pack_bf16x2(o[8 * u + 2] * inv, o[8 * u + 3] * inv),
+                            pack_bf16x2(o[8 * u + 4] * inv, o[8 * u + 5] * inv),
+                            pack_bf16x2(o[8 * u + 6] * inv, o[8 * u + 7] * inv)));
+      fence_async_smem();
+      tc_fence_before();  // O is read: the next strip's first PV may overwrite it
+      named_bar(1, kSoftWarps * 32);
+      if (st == 0) {
+        tma_store_4d(&map_ctx, ost, h * DH, b * S + q0, 0, 0);
+        bulk_commit();
+      }
     }
-    red_sum[hf * QT + rl] = lsum;
-    mbar_wait(bar_pv, (nch - 1) & 1);  // O complete
-    if (sw == 0 && lane == 0) ATRACE(10);
-    tc_fence_after();
-    named_bar(1, kF2Soft * 32);
-    const float tot = red_sum[rl] + red_sum[QT + rl];
-    if (hf == 0) p.lse[rowi] = mref + __log2f(tot);
-    const float inv = p.ks / tot;
-    float o[32];
-    tmem_ld32(trow + T_O + hf * 32, o);
-    uint32_t w8[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) w8[i] = pack_bf16x2(o[2 * i] * inv, o[2 * i + 1] * inv);
-    uint4* dst = reinterpret_cast<uint4*>(p.ctx + ((size_t)b * S + grow) * p.ld_ctx + h * DH + hf * 32);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w8[4 * i], w8[4 * i + 1], w8[4 * i + 2], w8[4 * i + 3]);
+    if (st == 0) bulk_wait_read<0>();
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 64) ATRACE(11);
+  if (threadIdx.x == 64) ATRACE(15);
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -1483,15 +1525,20 @@ extern "C" int dfx_attn_fwd(int64_t batch, int64_t heads, int64_t seq, int64_t h
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem::TOTAL);
-    cudaFuncSetAttribute(attn_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F2Smem::TOTAL);
+    cudaFuncSetAttribute(attn_fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F3Smem::TOTAL);
     attr = true;
   }
   const int grid = (int)(batch * heads * (seq / QT));
   static const bool legacy = getenv("DFX_ATTN_FWD_LEGACY") != nullptr;  // A/B: exact two-pass, 1 CTA / SM
-  if (legacy)
+  if (legacy) {
     launch_k(attn_fwd_kernel, grid, kAttnThreads, FwdSmem::TOTAL, as_stream(stream), map, p);
-  else
-    launch_k(attn_fwd2_kernel, grid, kF2Threads, F2Smem::TOTAL, as_stream(stream), map, p);
+  } else {
+    CUtensorMap mctx;  // ctx strips: [128 rows x 64] boxes
+    rc = make_map(&mctx, ctx, 2, (uint64_t)ld_ctx, (uint64_t)T, ld_ctx, 1, 0, 1, 0, 64, 128, true);
+    if (rc) return rc;
+    launch_k(attn_fwd3_kernel, std::min(grid, num_sms()), kAttnThreads, F3Smem::TOTAL, as_stream(stream), map, mctx,
+             p);
+  }
   DFX_LAUNCH_CHECK("dfx_attn_fwd");
   return DFX_OK;
 }

@@ -60,6 +60,25 @@ if "--kstrip" in sys.argv:  # persistent key-strip kernel: 0 start, 1 K/V of str
                                   if (r[:, i] > 0).all()})
     print("kernel span", round(rel[:, 15].max().item(), 2), "start spread", round(rel[:, 0].max().item(), 2))
     sys.exit(0)
+if "--fwd3" in sys.argv:  # persistent forward: 0 start, 1 Q of strip 0, 2-5 S_j / 6-9 P_j of strip 0,
+    # 10-12 strip it's O complete, 15 exit
+    ngrid = min(ncta, torch.cuda.get_device_properties(0).multi_processor_count)
+    tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
+    fn(tr.data_ptr())
+    run()
+    torch.cuda.synchronize()
+    fn(None)
+    t = tr.view(ncta, 16)[:ngrid].cpu().double()
+    rel = (t - t[:, 0].min()) / 1e3
+    names = {1: "Q", 2: "S0", 6: "P0", 3: "S1", 7: "P1", 4: "S2", 8: "P2", 5: "S3", 9: "P3", 10: "O0", 11: "O1",
+             12: "O2", 15: "exit"}
+    three = rel[:, 12] > 0
+    for lab, m in (("3-strip CTAs", three), ("2-strip CTAs", ~three)):
+        r = rel[m]
+        print(lab, int(m.sum()), {n: round((r[:, i] - r[:, 0]).mean().item(), 2) for i, n in names.items()
+                                  if (r[:, i] > 0).all()})
+    print("kernel span", round(rel[:, 15].max().item(), 2))
+    sys.exit(0)
 if "--fwd2" in sys.argv:  # online-softmax forward: 0 start, 1 Q landed, 2-5 S_j ready, 6-9 P_j stored, 10 O done, 11 exit
     tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
     fn(tr.data_ptr())
