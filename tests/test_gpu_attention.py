@@ -76,7 +76,11 @@ def _run(qkv, am, keep, dctx, B, S, NH, dropout=True):
     return f(ctx), f(lse), f(dqkv), kr, kc
 
 
-@pytest.mark.parametrize("B,NH,S", [(2, 2, 128), (1, 3, 256), (2, 2, 384), (2, 12, 512), (8, 12, 512)])
+# the persistent forward / key-strip kernels run min(strips, SMs) CTAs: the
+# last four shapes give every CTA two or three strips (1, 2, 3 and 4 chunks per
+# strip), so the cross-strip buffer parities and barrier phases are exercised
+@pytest.mark.parametrize("B,NH,S", [(2, 2, 128), (1, 3, 256), (2, 2, 384), (2, 12, 512), (8, 12, 512),
+                                    (24, 12, 128), (6, 16, 256), (4, 16, 384)])
 def test_attention_vs_oracle(B, NH, S):
     qkv, am, keep, dctx = _case(B, NH, S, seed=S + NH)
     ctx, lse, dqkv, _, _ = _run(qkv, am, keep, dctx, B, S, NH)
@@ -90,7 +94,7 @@ def test_attention_vs_oracle(B, NH, S):
         assert err <= 2e-2, f"d{nm}: {err:.3e}"
 
 
-@pytest.mark.parametrize("B,NH,S", [(2, 2, 128), (2, 12, 512), (1, 3, 384)])
+@pytest.mark.parametrize("B,NH,S", [(2, 2, 128), (2, 12, 512), (1, 3, 384), (4, 16, 384)])
 def test_qkv_bias_grad_from_strip_partials(B, NH, S):
     """dfx_attn_bwd_bias_grad (per-strip fp32 column sums left by the backward)
     against the oracle's column sums of dQ | dK | dV, and against a column sum
@@ -147,6 +151,20 @@ def test_attention_online_rescale():
     # sequence 1: large keys in chunk 2 for head 0, so rows with large q see a jump there
     qkv[S + 256:S + 384, H:H + 64] *= 6.0
     qkv = O.round_bf16(qkv).astype(np.float64)
+    ctx, lse, dqkv, _, _ = _run(qkv, am, keep, dctx, B, S, NH)
+    w_ctx, w_lse, w_dqkv = _oracle(qkv, am, keep, dctx, B, S, NH)
+    assert O.compare(ctx, w_ctx) <= 2e-2, O.compare(ctx, w_ctx)
+    assert np.abs(lse - w_lse).max() <= 1e-2 * max(1.0, np.abs(w_lse).max())
+    assert O.compare_scaled(dqkv, w_dqkv) <= 2e-2
+
+
+def test_attention_online_rescale_every_strip():
+    """The rescale in every strip of a 384-strip grid (each persistent CTA walks
+    two or three strips, so the rescale meets every buffer parity): the first
+    128 keys of every sequence sit ~2^43 below the rest."""
+    B, NH, S = 8, 12, 512
+    qkv, am, keep, dctx = _case(B, NH, S, seed=23)
+    am[:, :128] = -30.0
     ctx, lse, dqkv, _, _ = _run(qkv, am, keep, dctx, B, S, NH)
     w_ctx, w_lse, w_dqkv = _oracle(qkv, am, keep, dctx, B, S, NH)
     assert O.compare(ctx, w_ctx) <= 2e-2, O.compare(ctx, w_ctx)
