@@ -568,14 +568,11 @@ attn_fwd3_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_const
     const int sw = warp - 2, qd = warp & 3, part = sw >> 2;  // part: key columns [32 part, 32 part + 32) of a chunk
     const int rl = qd * 32 + lane;
     const int st = threadIdx.x - 64;  // 0..511
-    uint4* klut = reinterpret_cast<uint4*>(smem + F3Smem::LUT);
-    if (st < 256) {
-      uint32_t m[4];
-#pragma unroll
-      for (int w = 0; w < 4; ++w)
-        m[w] = (((st >> (2 * w)) & 1) ? 0x0000FFFFu : 0u) | (((st >> (2 * w + 1)) & 1) ? 0xFFFF0000u : 0u);
-      klut[st] = make_uint4(m[0], m[1], m[2], m[3]);
-    }
+    // keep-bit pair -> AND mask of a bf16 pair: four words, so a warp's lookups
+    // hit at most four banks (a 256-entry byte table of uint4 masks cost ~1.5 M
+    // bank-conflict wavefronts per launch)
+    uint32_t* klut = reinterpret_cast<uint32_t*>(smem + F3Smem::LUT);
+    if (st < 4) klut[st] = (st & 1 ? 0x0000FFFFu : 0u) | (st & 2 ? 0xFFFF0000u : 0u);
     named_bar(1, kSoftWarps * 32);
     const int words = S / 32;
     const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
@@ -660,9 +657,8 @@ attn_fwd3_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_const
           sacc = __fadd2_rn(sacc, __fadd2_rn(make_float2(e0, e1), make_float2(e2, e3)));
           uint32_t m0 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu;
           if (p.kb_in) {
-            const uint4 lm = klut[(kw >> (8 * (u >> 1))) & 0xFFu];
-            m0 = (u & 1) ? lm.z : lm.x;
-            m1 = (u & 1) ? lm.w : lm.y;
+            m0 = klut[(kw >> (4 * u)) & 3u];
+            m1 = klut[(kw >> (4 * u + 2)) & 3u];
           } else if (p.keep) {
             const uint4 q4 = kv[u >> 2];
             const uint32_t w = (u & 3) == 0 ? q4.x : ((u & 3) == 1 ? q4.y : ((u & 3) == 2 ? q4.z : q4.w));
@@ -1287,8 +1283,11 @@ attn_bwd_kstrip_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid
     const int rl = q * 32 + lane;
     const int st = threadIdx.x - 64;
     const int words = S / 32;
-    const float4* klut = reinterpret_cast<const float4*>(smem + KsSmem::LUT);
-    fill_keep_lut(reinterpret_cast<float4*>(smem + KsSmem::LUT), st, 1.f);
+    // keep-bit pair -> {0, 1} multipliers of a column pair: four float2, so a
+    // warp's lookups hit at most eight banks (a 16-entry float4 table of
+    // nibbles cost ~1.5 M bank-conflict wavefronts per launch)
+    const float2* klut = reinterpret_cast<const float2*>(smem + KsSmem::LUT);
+    if (st < 4) reinterpret_cast<float2*>(smem + KsSmem::LUT)[st] = make_float2(st & 1 ? 1.f : 0.f, st & 2 ? 1.f : 0.f);
     named_bar(1, kSoftWarps * 32);
     const float lsc = __log2f(p.scale);
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
@@ -1332,7 +1331,6 @@ attn_bwd_kstrip_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid
         if (lane == 0) mbar_arrive(bar_tfree);
         const int qc0 = j * CH + part * 32;
         uint32_t pkp[16], pks[16];
-        float4 kf;
         float2 csum = make_float2(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
@@ -1340,8 +1338,7 @@ attn_bwd_kstrip_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid
           const float2 dd = reinterpret_cast<const float2*>(del_s + qc0)[i >> 1];
           const float2 tt = __ffma2_rn(make_float2(sv[i], sv[i + 1]), sc2x2, __fadd2_rn(mrow2, make_float2(-l.x, -l.y)));
           const float2 P = make_float2(ex2(tt.x), ex2(tt.y));
-          if ((i & 3) == 0) kf = klut[(bits >> i) & 15u];
-          const float2 kk = (i & 3) ? make_float2(kf.z, kf.w) : make_float2(kf.x, kf.y);  // keep in {0, 1}
+          const float2 kk = klut[(bits >> i) & 3u];  // keep in {0, 1}
           const float2 pd = __fmul2_rn(P, kk);
           const float2 dpm = __fmul2_rn(make_float2(dp[i], dp[i + 1]), kk);
           const float2 ds = __fmul2_rn(P, __ffma2_rn(dpm, ks2, make_float2(-dd.x, -dd.y)));
