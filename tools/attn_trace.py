@@ -1,7 +1,11 @@
-"""Per-CTA timeline of the fused attention forward (debug hook
-dfx_debug_attn_trace): 0 start (after setup), 1 Q/K landed, 2 softmax ready,
-3 S in TMEM, 4 pass-1 done (warp 2), 5 P complete (MMA side), 6 pass-2 done,
-7 O in TMEM, 8 exit — µs from the earliest start."""
+"""Per-CTA timelines of the fused attention kernels (debug hook
+dfx_debug_attn_trace; µs from the earliest CTA start):
+  --fwd3    persistent forward (default path)
+  --kstrip  persistent key-strip backward (default path)
+  --bwd     the r01 dq strip kernel (DFX_ATTN_BWD_LEGACY=1)
+  (none)    the r01 exact two-pass forward (DFX_ATTN_FWD_LEGACY=1): 0 start,
+            1 Q/K landed, 2 softmax ready, 3 S in TMEM, 4 pass-1 done, 5 P
+            complete, 6 pass-2 done, 7 O in TMEM, 8 exit."""
 import ctypes
 import os
 import sys
@@ -78,23 +82,6 @@ if "--fwd3" in sys.argv:  # persistent forward: 0 start, 1 Q of strip 0, 2-5 S_j
         print(lab, int(m.sum()), {n: round((r[:, i] - r[:, 0]).mean().item(), 2) for i, n in names.items()
                                   if (r[:, i] > 0).all()})
     print("kernel span", round(rel[:, 15].max().item(), 2))
-    sys.exit(0)
-if "--fwd2" in sys.argv:  # online-softmax forward: 0 start, 1 Q landed, 2-5 S_j ready, 6-9 P_j stored, 10 O done, 11 exit
-    tr = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
-    fn(tr.data_ptr())
-    run()
-    torch.cuda.synchronize()
-    fn(None)
-    t = tr.view(ncta, 16).cpu().double()
-    rel = (t - t[:, 0].min()) / 1e3
-    names = ["start->Q", "Q->S0", "S0->P0", "P0->S1", "S1->P1", "P1->S2", "S2->P2", "P2->S3", "S3->P3", "P3->O", "O->exit"]
-    order = [0, 1, 2, 6, 3, 7, 4, 8, 5, 9, 10, 11]
-    d = [rel[:, order[i + 1]] - rel[:, order[i]] for i in range(len(order) - 1)]
-    print("fwd2 mean phase durations (us):", {n: round(x.mean().item(), 2) for n, x in zip(names, d)})
-    print("per-CTA total mean", round((rel[:, 11] - rel[:, 0]).mean().item(), 2), "kernel span",
-          round(rel[:, 11].max().item(), 2))
-    starts = sorted(rel[:, 0].tolist())
-    print("CTA start quantiles:", [round(starts[int(q * (len(starts) - 1))], 2) for q in (0, .25, .5, .75, 1)])
     sys.exit(0)
 if "--bwd" in sys.argv:  # dq kernel timeline: 0 start, 1 Q/dO landed (MMA), 2-5 S_j ready, 6-9 dS_j done, 10 dQ done, 11 exit
     run()
