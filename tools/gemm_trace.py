@@ -21,11 +21,23 @@ fn.argtypes = [ctypes.c_void_p]
 a = torch.randn(m, k, device="cuda").bfloat16()
 b = torch.randn(n, k, device="cuda").bfloat16()
 d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+epi = os.environ.get("GT_EPI", "none")  # none | gelu (bias + GELU + pre-activation stash, the FFN1 forward)
+bias = torch.randn(n, device="cuda") * 0.1
+pre = torch.empty_like(d)
+
+
+def run():
+    if epi == "gelu":
+        K.gemm(a, b, d, _lib.EPI_BIAS_GELU, bias=bias, aux_out=pre)
+    else:
+        K.gemm(a, b, d, beta=float(os.environ.get("GT_BETA", "1.0")))
+
+
 for _ in range(3):
-    K.gemm(a, b, d)
+    run()
 tr = torch.zeros(148 * 32, dtype=torch.int64, device="cuda")
 fn(tr.data_ptr())
-K.gemm(a, b, d, beta=float(os.environ.get("GT_BETA", "1.0")))
+run()
 torch.cuda.synchronize()
 fn(None)
 t = tr.view(148, 32).cpu()
