@@ -210,4 +210,35 @@ template <typename T> __device__ __forceinline__ T from_f(float x);
 template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
 template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 
+
+// Fixed-order f64 sum of nparts partial rows (row stride ld floats) at column
+// col, for a 1024-thread block whose 32 lanes own 32 consecutive columns: warp
+// w takes rows w, w + 32, ... in four independent chains (rows w + 128 i + 32 k
+// into chain k), the chains add in order, then warp 0 adds the 32 warps in
+// order.  Returns the column total in warp 0 (bitwise reproducible; ~nparts/128
+// dependent adds per thread instead of nparts/8).
+__device__ __forceinline__ double sum_part_rows(int nparts, const float* __restrict__ part, size_t ld, int col,
+                                                bool ok, double (*red)[33]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (ok) {
+    int b = w;
+    for (; b + 96 < nparts; b += 128) {
+      a0 += part[(size_t)b * ld + col];
+      a1 += part[(size_t)(b + 32) * ld + col];
+      a2 += part[(size_t)(b + 64) * ld + col];
+      a3 += part[(size_t)(b + 96) * ld + col];
+    }
+    for (; b < nparts; b += 32) a0 += part[(size_t)b * ld + col];
+  }
+  red[w][lane] = ((a0 + a1) + a2) + a3;
+  __syncthreads();
+  double v = 0.0;
+  if (w == 0) {
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) v += red[j][lane];
+  }
+  return v;
+}
+
 }  // namespace dfx

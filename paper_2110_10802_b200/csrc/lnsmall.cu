@@ -179,23 +179,16 @@ __global__ void __launch_bounds__(256) ln_small_bwd_kernel(int64_t rows, const T
 }
 
 // dgamma / dbeta = fixed-order f64 sums of the CTA partials [nb][2][C]
-__global__ void __launch_bounds__(256) ln_small_finalize_kernel(int nb, int C, const float* __restrict__ part,
-                                                                float* __restrict__ dgamma,
-                                                                float* __restrict__ dbeta) {
+// (1024 threads per 32 columns, sum_part_rows)
+__global__ void __launch_bounds__(1024) ln_small_finalize_kernel(int nb, int C, const float* __restrict__ part,
+                                                                 float* __restrict__ dgamma,
+                                                                 float* __restrict__ dbeta) {
   pdl_wait();
   pdl_trigger();
-  __shared__ double sred[8][33];
-  const int lane = threadIdx.x & 31, pl = threadIdx.x >> 5;
-  const int idx = blockIdx.x * 32 + lane;  // over 2C
-  double acc = 0.0;
-  if (idx < 2 * C)
-    for (int b = pl; b < nb; b += 8) acc += part[(size_t)b * 2 * C + idx];
-  sred[pl][lane] = acc;
-  __syncthreads();
-  if (pl == 0 && idx < 2 * C) {
-    double v = 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v += sred[j][lane];
+  __shared__ double sred[32][33];
+  const int idx = blockIdx.x * 32 + (threadIdx.x & 31);  // over 2C
+  const double v = sum_part_rows(nb, part, (size_t)2 * C, idx, idx < 2 * C, sred);
+  if (threadIdx.x < 32 && idx < 2 * C) {
     if (idx < C) dgamma[idx] = (float)v;
     else dbeta[idx - C] = (float)v;
   }
@@ -232,7 +225,7 @@ int bwd_launch(int64_t rows, const void* dy, const void* x, const float* gamma, 
     launch_k(ln_small_bwd_kernel<T, V, G, 0>, grid, 256, 0, st, rows, (const T*)dy, (const T*)x, gamma, beta, eps,
              (T*)dx, part);
   DFX_LAUNCH_CHECK("dfx_layernorm_act_bwd (short rows)");
-  launch_k(ln_small_finalize_kernel, (unsigned)((2 * C + 31) / 32), 256, 0, st, grid, C, (const float*)part, dgamma,
+  launch_k(ln_small_finalize_kernel, (unsigned)((2 * C + 31) / 32), 1024, 0, st, grid, C, (const float*)part, dgamma,
            dbeta);
   DFX_LAUNCH_CHECK("dfx_layernorm_act_bwd (short rows) finalize");
   return DFX_OK;

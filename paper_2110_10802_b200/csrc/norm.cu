@@ -274,26 +274,14 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(int64_t rows, i
 
 // out[i] = sum_b part[b][i] (i over 2C): block = 32 outputs x 8 part lanes,
 // fixed-order f64 combine
-__global__ void __launch_bounds__(256) bn_sum_parts_kernel(int nparts, int C, const float* __restrict__ part,
-                                                           float* __restrict__ out) {
+__global__ void __launch_bounds__(1024) bn_sum_parts_kernel(int nparts, int C, const float* __restrict__ part,
+                                                            float* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
-  __shared__ double red[8][33];
-  const int lane = threadIdx.x & 31, pl = threadIdx.x >> 5;
-  const int idx = blockIdx.x * 32 + lane;
-  double acc = 0.0;
-  if (idx < 2 * C) {
-#pragma unroll 4
-    for (int b = pl; b < nparts; b += 8) acc += part[(size_t)b * 2 * C + idx];
-  }
-  red[pl][lane] = acc;
-  __syncthreads();
-  if (pl == 0 && idx < 2 * C) {
-    double v = 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v += red[j][lane];
-    out[idx] = (float)v;
-  }
+  __shared__ double red[32][33];
+  const int idx = blockIdx.x * 32 + (threadIdx.x & 31);
+  const double v = sum_part_rows(nparts, part, (size_t)2 * C, idx, idx < 2 * C, red);
+  if (threadIdx.x < 32 && idx < 2 * C) out[idx] = (float)v;
 }
 
 // dx = A*du + Cx*x + B with A = gamma*rstd and the BN-VJP means folded into
@@ -512,7 +500,7 @@ int dfx_batchnorm_act_bwd_reduce(int dtype, int64_t rows, int64_t C, const void*
   BN_DISPATCH(R, act);
 #undef R
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_reduce");
-  launch_k(bn_sum_parts_kernel, (unsigned)((2 * C + 31) / 32), 256, 0, st, nb, (int)C, (const float*)workspace, bnsum);
+  launch_k(bn_sum_parts_kernel, (unsigned)((2 * C + 31) / 32), 1024, 0, st, nb, (int)C, (const float*)workspace, bnsum);
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_reduce sum");
   return DFX_OK;
 }
