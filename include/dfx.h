@@ -323,6 +323,20 @@ int dfx_batchnorm_act_bwd_dx(int dtype, int64_t rows, int64_t C, const void* dy,
                              const float* mean, const float* rstd, const float* gamma,
                              const float* beta, int act, const float* bnsum, double count, void* dx,
                              void* stream);
+/* Single-replica fusions of the calls above (one launch fewer each):
+ *   stats_finalize = dfx_batchnorm_stats + dfx_bn_finalize(nsets = 1) — the
+ *     statistics of the one set written by the merge (local as before);
+ *   bwd_reduce_grads = dfx_batchnorm_act_bwd_reduce that also writes the local
+ *     parameter gradients dbeta = bnsum[0], dgamma = bnsum[1] (either may be NULL). */
+int dfx_batchnorm_stats_finalize(int dtype, int64_t rows, int64_t C, const void* x, float* local,
+                                 float eps, float momentum, float* mean, float* var, float* rstd,
+                                 float* run_mean, float* run_var, void* workspace, size_t ws_bytes,
+                                 void* stream);
+int dfx_batchnorm_act_bwd_reduce_grads(int dtype, int64_t rows, int64_t C, const void* dy,
+                                       const void* x, const float* mean, const float* rstd,
+                                       const float* gamma, const float* beta, int act, float* bnsum,
+                                       float* dbeta, float* dgamma, void* workspace, size_t ws_bytes,
+                                       void* stream);
 
 /* ---- C5: EfficientNet-B0 training-step glue (NHWC) ------------------------
  * stem im2col for a 3x3 conv (frontend.py:598-678): cols [N*Ho*Wo, Kp] with

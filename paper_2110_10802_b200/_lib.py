@@ -115,6 +115,12 @@ _SIGS = [
     ("dfx_batchnorm_act_bwd_dx", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                          c_void_p, c_void_p, c_int, c_void_p, ctypes.c_double, c_void_p,
                                          c_void_p]),
+    ("dfx_batchnorm_stats_finalize", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_float, c_float,
+                                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                             c_size_t, c_void_p]),
+    ("dfx_batchnorm_act_bwd_reduce_grads", c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                                   c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+                                                   c_void_p, c_void_p, c_size_t, c_void_p]),
     ("dfx_attn_fwd", c_int, [c_int64, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                              c_float, c_float, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("dfx_attn_bwd_workspace", c_size_t, [c_int64, c_int64, c_int64]),

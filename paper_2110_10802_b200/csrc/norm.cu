@@ -115,9 +115,16 @@ __global__ void __launch_bounds__(kThreads) bn_stats_kernel(int64_t rows, int C,
   }
 }
 
+// single-replica finalize fused into the merge (dfx_batchnorm_stats_finalize):
+// the statistics of the one set, exactly as dfx_bn_finalize computes them
+struct BnFin {
+  float eps, momentum;
+  float *mean, *var, *rstd, *run_mean, *run_var;  // rstd == null: merge only
+};
+
 // one block per channel: merge block partials in a fixed tree order
 __global__ void __launch_bounds__(kThreads) bn_merge_kernel(int nparts, int C, const float* __restrict__ part,
-                                                           float* __restrict__ out /*[3][C]*/) {
+                                                           float* __restrict__ out /*[3][C]*/, BnFin fin) {
   pdl_trigger();
   pdl_wait();
   __shared__ float sn[kThreads], smn[kThreads], sm2[kThreads];
@@ -136,7 +143,17 @@ __global__ void __launch_bounds__(kThreads) bn_merge_kernel(int nparts, int C, c
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) { out[c] = sn[0]; out[C + c] = smn[0]; out[2 * C + c] = sm2[0]; }
+  if (threadIdx.x == 0) {
+    out[c] = sn[0]; out[C + c] = smn[0]; out[2 * C + c] = sm2[0];
+    if (fin.rstd) {
+      const float v = sm2[0] / sn[0];  // biased variance (frontend.py:565)
+      if (fin.mean) fin.mean[c] = smn[0];
+      if (fin.var) fin.var[c] = v;
+      fin.rstd[c] = rsqrtf(v + fin.eps);
+      if (fin.run_mean) fin.run_mean[c] = fin.run_mean[c] * fin.momentum + smn[0] * (1.f - fin.momentum);
+      if (fin.run_var) fin.run_var[c] = fin.run_var[c] * fin.momentum + v * (1.f - fin.momentum);
+    }
+  }
 }
 
 // swish'(u) = s + u s (1 - s); bf16 storage uses the one-MUFU sigmoid
@@ -275,13 +292,18 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(int64_t rows, i
 // out[i] = sum_b part[b][i] (i over 2C): block = 32 outputs x 8 part lanes,
 // fixed-order f64 combine
 __global__ void __launch_bounds__(1024) bn_sum_parts_kernel(int nparts, int C, const float* __restrict__ part,
-                                                            float* __restrict__ out) {
+                                                            float* __restrict__ out, float* __restrict__ dbeta,
+                                                            float* __restrict__ dgamma) {
   pdl_trigger();
   pdl_wait();
   __shared__ double red[32][33];
   const int idx = blockIdx.x * 32 + (threadIdx.x & 31);
   const double v = sum_part_rows(nparts, part, (size_t)2 * C, idx, idx < 2 * C, red);
-  if (threadIdx.x < 32 && idx < 2 * C) out[idx] = (float)v;
+  if (threadIdx.x < 32 && idx < 2 * C) {
+    out[idx] = (float)v;
+    float* g = idx < C ? dbeta : dgamma;  // the local parameter gradients (bnsum before any SyncBN allreduce)
+    if (g) g[idx < C ? idx : idx - C] = (float)v;
+  }
 }
 
 // dx = A*du + Cx*x + B with A = gamma*rstd and the BN-VJP means folded into
@@ -418,20 +440,8 @@ template <typename K> int resident_ctas(K kern, int threads, size_t smem) {
   return occ;
 }
 
-}  // namespace
-}  // namespace dfx
-
-using namespace dfx;
-
-extern "C" {
-
-size_t dfx_batchnorm_workspace(int64_t rows, int64_t C) {
-  (void)rows;
-  return (size_t)kMaxBlocks * 3 * C * sizeof(float) + 256;
-}
-
-int dfx_batchnorm_stats(int dtype, int64_t rows, int64_t C, const void* x, float* local, void* workspace,
-                        size_t ws_bytes, void* stream) {
+int bn_stats_impl(int dtype, int64_t rows, int64_t C, const void* x, float* local, void* workspace, size_t ws_bytes,
+                  const BnFin& fin, void* stream) {
   if (int rc = check_bn(dtype, rows, C, "dfx_batchnorm_stats")) return rc;
   DFX_REQUIRE(x && local && workspace, DFX_ERR_SHAPE, "dfx_batchnorm_stats: null pointer");
   DFX_REQUIRE(ws_bytes >= dfx_batchnorm_workspace(rows, C), DFX_ERR_WORKSPACE, "dfx_batchnorm_stats: workspace too small");
@@ -452,9 +462,35 @@ int dfx_batchnorm_stats(int dtype, int64_t rows, int64_t C, const void* x, float
   BN_DISPATCH(S, 0);
 #undef S
   DFX_LAUNCH_CHECK("dfx_batchnorm_stats");
-  launch_k(bn_merge_kernel, (unsigned)C, kThreads, 0, st, nb, (int)C, (const float*)workspace, local);
+  launch_k(bn_merge_kernel, (unsigned)C, kThreads, 0, st, nb, (int)C, (const float*)workspace, local, fin);
   DFX_LAUNCH_CHECK("dfx_batchnorm_stats merge");
   return DFX_OK;
+}
+}  // namespace
+}  // namespace dfx
+
+using namespace dfx;
+
+extern "C" {
+
+size_t dfx_batchnorm_workspace(int64_t rows, int64_t C) {
+  (void)rows;
+  return (size_t)kMaxBlocks * 3 * C * sizeof(float) + 256;
+}
+
+
+int dfx_batchnorm_stats(int dtype, int64_t rows, int64_t C, const void* x, float* local, void* workspace,
+                        size_t ws_bytes, void* stream) {
+  return bn_stats_impl(dtype, rows, C, x, local, workspace, ws_bytes, BnFin{0.f, 0.f, nullptr, nullptr, nullptr,
+                                                                           nullptr, nullptr}, stream);
+}
+
+int dfx_batchnorm_stats_finalize(int dtype, int64_t rows, int64_t C, const void* x, float* local, float eps,
+                                 float momentum, float* mean, float* var, float* rstd, float* run_mean,
+                                 float* run_var, void* workspace, size_t ws_bytes, void* stream) {
+  DFX_REQUIRE(rstd, DFX_ERR_SHAPE, "dfx_batchnorm_stats_finalize: rstd is required");
+  return bn_stats_impl(dtype, rows, C, x, local, workspace, ws_bytes,
+                       BnFin{eps, momentum, mean, var, rstd, run_mean, run_var}, stream);
 }
 
 int dfx_batchnorm_act_apply(int dtype, int64_t rows, int64_t C, const void* x, const float* mean, const float* rstd,
@@ -477,6 +513,14 @@ int dfx_batchnorm_act_apply(int dtype, int64_t rows, int64_t C, const void* x, c
 int dfx_batchnorm_act_bwd_reduce(int dtype, int64_t rows, int64_t C, const void* dy, const void* x,
                                  const float* mean, const float* rstd, const float* gamma, const float* beta,
                                  int act, float* bnsum, void* workspace, size_t ws_bytes, void* stream) {
+  return dfx_batchnorm_act_bwd_reduce_grads(dtype, rows, C, dy, x, mean, rstd, gamma, beta, act, bnsum, nullptr,
+                                            nullptr, workspace, ws_bytes, stream);
+}
+
+int dfx_batchnorm_act_bwd_reduce_grads(int dtype, int64_t rows, int64_t C, const void* dy, const void* x,
+                                       const float* mean, const float* rstd, const float* gamma, const float* beta,
+                                       int act, float* bnsum, float* dbeta, float* dgamma, void* workspace,
+                                       size_t ws_bytes, void* stream) {
   if (int rc = check_bn(dtype, rows, C, "dfx_batchnorm_act_bwd_reduce")) return rc;
   DFX_REQUIRE(dy && x && mean && rstd && gamma && beta && bnsum && workspace, DFX_ERR_SHAPE,
               "dfx_batchnorm_act_bwd_reduce: null pointer");
@@ -500,7 +544,8 @@ int dfx_batchnorm_act_bwd_reduce(int dtype, int64_t rows, int64_t C, const void*
   BN_DISPATCH(R, act);
 #undef R
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_reduce");
-  launch_k(bn_sum_parts_kernel, (unsigned)((2 * C + 31) / 32), 1024, 0, st, nb, (int)C, (const float*)workspace, bnsum);
+  launch_k(bn_sum_parts_kernel, (unsigned)((2 * C + 31) / 32), 1024, 0, st, nb, (int)C, (const float*)workspace, bnsum,
+           dbeta, dgamma);
   DFX_LAUNCH_CHECK("dfx_batchnorm_act_bwd_reduce sum");
   return DFX_OK;
 }

@@ -86,13 +86,20 @@ class BatchNormAct:
         y = torch.empty_like(x) if y is None else y
         # SyncBN: the statistics land directly in this rank's slot of the exchange buffer
         stats = bn_slot(self.sets, self.pg) if self.world > 1 else self.local
-        with K._span("bn_stats", "hbm", lambda: x.numel() * x.element_size()):
-            _lib.call("dfx_batchnorm_stats", dt, rows, self.C, x.data_ptr(), stats.data_ptr(), ws.data_ptr(),
-                      ws.numel(), st)
-        sets = exchange_bn_sets(self.sets, group=self.pg) if self.world > 1 else self.local
-        _lib.call("dfx_bn_finalize", self.C, self.world, sets.data_ptr(), float(self.eps), float(self.momentum),
-                  self.mean.data_ptr(), self.var.data_ptr(), self.rstd.data_ptr(), self.running_mean.data_ptr(),
-                  self.running_var.data_ptr(), st)
+        if self.world == 1:  # statistics and their finalize in one pass over the block partials
+            with K._span("bn_stats", "hbm", lambda: x.numel() * x.element_size()):
+                _lib.call("dfx_batchnorm_stats_finalize", dt, rows, self.C, x.data_ptr(), stats.data_ptr(),
+                          float(self.eps), float(self.momentum), self.mean.data_ptr(), self.var.data_ptr(),
+                          self.rstd.data_ptr(), self.running_mean.data_ptr(), self.running_var.data_ptr(),
+                          ws.data_ptr(), ws.numel(), st)
+        else:
+            with K._span("bn_stats", "hbm", lambda: x.numel() * x.element_size()):
+                _lib.call("dfx_batchnorm_stats", dt, rows, self.C, x.data_ptr(), stats.data_ptr(), ws.data_ptr(),
+                          ws.numel(), st)
+            sets = exchange_bn_sets(self.sets, group=self.pg)
+            _lib.call("dfx_bn_finalize", self.C, self.world, sets.data_ptr(), float(self.eps), float(self.momentum),
+                      self.mean.data_ptr(), self.var.data_ptr(), self.rstd.data_ptr(), self.running_mean.data_ptr(),
+                      self.running_var.data_ptr(), st)
         with K._span("bn_act_apply", "hbm", lambda: 2 * x.numel() * x.element_size()):
             _lib.call("dfx_batchnorm_act_apply", dt, rows, self.C, x.data_ptr(), self.mean.data_ptr(),
                       self.rstd.data_ptr(), self.gamma.data_ptr(), self.beta.data_ptr(), self.act, y.data_ptr(), st)
@@ -105,10 +112,11 @@ class BatchNormAct:
         ws = K.WORKSPACE.get(_lib.load().dfx_batchnorm_workspace(rows, self.C))
         dx = torch.empty_like(x) if dx is None else dx
         with K._span("bn_act_bwd_reduce", "hbm", lambda: 2 * x.numel() * x.element_size()):
-            _lib.call("dfx_batchnorm_act_bwd_reduce", dt, rows, self.C, dy.data_ptr(), x.data_ptr(),
+            # bnsum, and the local parameter gradients dbeta / dgamma straight from the same sums
+            _lib.call("dfx_batchnorm_act_bwd_reduce_grads", dt, rows, self.C, dy.data_ptr(), x.data_ptr(),
                       self.mean.data_ptr(), self.rstd.data_ptr(), self.gamma.data_ptr(), self.beta.data_ptr(),
-                      self.act, self.bnsum.data_ptr(), ws.data_ptr(), ws.numel(), st)
-        K.cast2(self.bnsum[0], self.dbeta, self.bnsum[1], self.dgamma)  # local parameter gradients
+                      self.act, self.bnsum.data_ptr(), self.dbeta.data_ptr(), self.dgamma.data_ptr(),
+                      ws.data_ptr(), ws.numel(), st)
         count = float(rows)
         if self.world > 1:  # SyncBN: (sum du, sum du*xhat, count) over ranks; count 0 = read bnsum[2]
             self.bnsum[2].fill_(count)
