@@ -19,7 +19,8 @@
 namespace dfx {
 namespace {
 
-constexpr int kU = 4;  // rows in flight per thread
+constexpr int kU = 4;   // rows in flight per thread (forward)
+constexpr int kUb = 2;  // backward: x and dy rows in flight; bf16 rows of <= 64 channels fit 80 registers -> 3 CTAs per SM
 
 template <int G> __device__ __forceinline__ float gsum(float v) {
 #pragma unroll
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(256) ln_small_fwd_kernel(int64_t rows, const T
 }
 
 template <typename T, int V, int G, int ACT>
-__global__ void __launch_bounds__(256) ln_small_bwd_kernel(int64_t rows, const T* __restrict__ dy,
+__global__ void __launch_bounds__(256, (sizeof(T) == 2 && G <= 8) ? 3 : 2) ln_small_bwd_kernel(int64_t rows, const T* __restrict__ dy,
                                                            const T* __restrict__ x, const float* __restrict__ gamma,
                                                            const float* __restrict__ beta, float eps,
                                                            T* __restrict__ dx, float* __restrict__ part) {
@@ -110,10 +111,10 @@ __global__ void __launch_bounds__(256) ln_small_bwd_kernel(int64_t rows, const T
     ag[i] = 0.f;
     ab[i] = 0.f;
   }
-  for (int64_t r0 = wid * RPW * kU; r0 < rows; r0 += nw * RPW * kU) {
-    Vec<T, V> xv[kU], dv[kU];
+  for (int64_t r0 = wid * RPW * kUb; r0 < rows; r0 += nw * RPW * kUb) {
+    Vec<T, V> xv[kUb], dv[kUb];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kUb; ++u) {
       const int64_t r = r0 + u * RPW + rs;
       if (r < rows) {
         xv[u].load(x + r * C + gl * V);
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(256) ln_small_bwd_kernel(int64_t rows, const T
       }
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kUb; ++u) {
       float s = 0.f;
 #pragma unroll
       for (int i = 0; i < V; ++i) s += xv[u].v[i];
@@ -214,7 +215,7 @@ template <typename T, int V, int G>
 int bwd_launch(int64_t rows, const void* dy, const void* x, const float* gamma, const float* beta, float eps,
                int act, void* dx, float* dgamma, float* dbeta, float* part, size_t part_floats, cudaStream_t st) {
   constexpr int RPW = 32 / G, C = G * V;
-  const int64_t per_block = 8LL * RPW * kU;
+  const int64_t per_block = 8LL * RPW * kUb;
   int grid = (int)std::min<int64_t>((rows + per_block - 1) / per_block, (int64_t)std::min(kMaxBlocks, num_sms() * 8));
   grid = (int)std::min<int64_t>(grid, (int64_t)(part_floats / (2 * C)));
   if (grid < 1) return fail(DFX_ERR_WORKSPACE, "dfx_layernorm_act_bwd: workspace too small");
