@@ -95,3 +95,59 @@ def test_sweep_shapes_vs_oracle(dtype, tol, shape):
     assert O.compare(np.moveaxis(_h(dxb), -1, 1), wdxb) <= tol
     assert metric(_h(bn.dgamma), wdgb) <= tol
     assert metric(_h(bn.dbeta), wdbb) <= tol
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("shape", [(32, 56, 56, 64), (3, 7, 7, 1152), (5, 9, 24)])
+def test_bn_single_replica_entry_points_match_the_split_calls(dtype, shape):
+    """dfx_batchnorm_stats_finalize == dfx_batchnorm_stats + dfx_bn_finalize(nsets 1)
+    and dfx_batchnorm_act_bwd_reduce_grads == dfx_batchnorm_act_bwd_reduce + the
+    dbeta/dgamma copies: bitwise for the merged sets, bnsum, dbeta and dgamma;
+    the finalize arithmetic (var, rstd, running-stat blends) to one fp32 rounding
+    (the two kernels may contract it into FMAs differently)."""
+    from paper_2110_10802_b200 import _lib
+    from paper_2110_10802_b200 import kernels as K
+
+    C = shape[-1]
+    rows = int(np.prod(shape[:-1]))
+    g = torch.Generator(device="cpu").manual_seed(C + rows)
+    x = (torch.randn(shape, generator=g) * 1.5 + 0.3).to(dtype).cuda()
+    dy = torch.randn(shape, generator=g).to(dtype).cuda()
+    gamma = (1 + 0.1 * torch.randn(C, generator=g)).cuda()
+    beta = (0.1 * torch.randn(C, generator=g)).cuda()
+    lib = _lib.load()
+    ws = torch.empty(lib.dfx_batchnorm_workspace(rows, C), dtype=torch.uint8, device="cuda")
+    dt = K.dfx_dtype(x)
+    f = lambda *s: torch.zeros(*s, device="cuda")  # noqa: E731
+    out = {}
+    for fused in (False, True):
+        local, mean, var, rstd = f(3, C), f(C), f(C), f(C)
+        rm, rv = torch.full((C,), 0.5, device="cuda"), torch.full((C,), 2.0, device="cuda")
+        if fused:
+            _lib.call("dfx_batchnorm_stats_finalize", dt, rows, C, x.data_ptr(), local.data_ptr(), 1e-3, 0.9,
+                      mean.data_ptr(), var.data_ptr(), rstd.data_ptr(), rm.data_ptr(), rv.data_ptr(), ws.data_ptr(),
+                      ws.numel(), K._stream())
+        else:
+            _lib.call("dfx_batchnorm_stats", dt, rows, C, x.data_ptr(), local.data_ptr(), ws.data_ptr(), ws.numel(),
+                      K._stream())
+            _lib.call("dfx_bn_finalize", C, 1, local.data_ptr(), 1e-3, 0.9, mean.data_ptr(), var.data_ptr(),
+                      rstd.data_ptr(), rm.data_ptr(), rv.data_ptr(), K._stream())
+        bnsum, dbeta, dgamma = f(3, C), f(C), f(C)
+        if fused:
+            _lib.call("dfx_batchnorm_act_bwd_reduce_grads", dt, rows, C, dy.data_ptr(), x.data_ptr(), mean.data_ptr(),
+                      rstd.data_ptr(), gamma.data_ptr(), beta.data_ptr(), 1, bnsum.data_ptr(), dbeta.data_ptr(),
+                      dgamma.data_ptr(), ws.data_ptr(), ws.numel(), K._stream())
+        else:
+            _lib.call("dfx_batchnorm_act_bwd_reduce", dt, rows, C, dy.data_ptr(), x.data_ptr(), mean.data_ptr(),
+                      rstd.data_ptr(), gamma.data_ptr(), beta.data_ptr(), 1, bnsum.data_ptr(), ws.data_ptr(),
+                      ws.numel(), K._stream())
+            dbeta.copy_(bnsum[0])
+            dgamma.copy_(bnsum[1])
+        torch.cuda.synchronize()
+        out[fused] = [t.clone() for t in (local, mean, var, rstd, rm, rv, bnsum[:2], dbeta, dgamma)]
+    names = ("local", "mean", "var", "rstd", "running_mean", "running_var", "bnsum", "dbeta", "dgamma")
+    for nm, a, b in zip(names, out[False], out[True]):
+        if nm in ("var", "rstd", "running_mean", "running_var"):
+            assert torch.allclose(a, b, rtol=1e-6, atol=0), nm
+        else:
+            assert torch.equal(a, b), nm
