@@ -447,10 +447,10 @@ attn_fwd3_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_const
   uint64_t* bar_sfree = bar + 10;   // [2] S_J read
   uint64_t* bar_p = bar + 12;       // [2] P̃d_J written
   uint64_t* bar_pv = bar + 14;      // [2] PV_J completed
-  uint64_t* full = bar + 16;        // [NST]
-  uint64_t* empty = bar + 19;       // [NST]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 22);
   constexpr int NST = F3Smem::NST;
+  uint64_t* full = bar + 16;          // [NST]
+  uint64_t* empty = bar + 16 + NST;   // [NST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16 + 2 * NST);
   float* red_max = reinterpret_cast<float*>(smem + F3Smem::RED);
   float* red_sum = reinterpret_cast<float*>(smem + F3Smem::SUM);
 
