@@ -448,6 +448,7 @@ attn_fwd3_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_const
   uint64_t* bar_p = bar + 12;       // [2] P̃d_J written
   uint64_t* bar_pv = bar + 14;      // [2] PV_J completed
   constexpr int NST = F3Smem::NST;
+  static_assert((16 + 2 * NST) * 8 + 4 <= 256, "forward barriers exceed their smem slot");
   uint64_t* full = bar + 16;          // [NST]
   uint64_t* empty = bar + 16 + NST;   // [NST]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16 + 2 * NST);
@@ -1136,10 +1137,11 @@ attn_bwd_kstrip_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid
   uint64_t* bar_rows = bar + 6;   // [2]
   uint64_t* rows_free = bar + 8;  // [2]
   uint64_t* ds_free = bar + 10;   // the dSᵀ tile's store has read it
-  uint64_t* full = bar + 11;      // [NST]
-  uint64_t* empty = bar + 14;     // [NST]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
   constexpr int NST = KsSmem::NST;
+  static_assert((11 + 2 * NST) * 8 + 4 <= 256, "key-strip barriers exceed their smem slot");
+  uint64_t* full = bar + 11;              // [NST]
+  uint64_t* empty = bar + 11 + NST;       // [NST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11 + 2 * NST);
   auto rows = [&](int it) { return reinterpret_cast<float*>(smem + KsSmem::ROWS + (it & 1) * KsSmem::ROWB); };
 
   const int S = p.S, nch = S / CH;
